@@ -1,0 +1,202 @@
+"""CPU oracle of the COMM-RAND mini-batch hot path -- TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
+product path (``paper_2504_18082_b200``) never imports it and shares no code
+with it.  The arithmetic lives in ``oracle.c`` (plain single-threaded C, one
+function per step, each citing the paper passage it follows); this module only
+marshals numpy arrays through ctypes and composes the per-hop calls in the
+order of Alg. 1.
+
+Pins (tests/test_oracle_*.py, ``-m "not gpu"``): Philox KAT, mulhi64 closed
+forms, brute-force graph prep, Knob-1 invariants + chi^2, the exact
+without-replacement law of Knob-2 by enumeration + chi^2, brute-force relabel,
+fp64 closed forms for the aggregate.  See DESIGN.md "Oracle and pins".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.c")
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
+
+MODE_RAND, MODE_NORAND, MODE_COMM = 0, 1, 2
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _SO + ".tmp", _SRC])
+        os.replace(_SO + ".tmp", _SO)
+    return _SO
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        P, I64, I32, U32, U64, D = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32,
+                                    ctypes.c_uint64, ctypes.c_double)
+        L.or_philox4x32_10.argtypes = [P, P, P]
+        L.or_mulhi64.argtypes = [U64, U64]
+        L.or_mulhi64.restype = U64
+        L.or_graph_prep.argtypes = [I64, P, P, P, I32, P, P, P]
+        L.or_graph_prep.restype = ctypes.c_int
+        L.or_order_roots.argtypes = [I64, P, P, I32, I32, D, U64, U32, P]
+        L.or_order_roots.restype = ctypes.c_int
+        L.or_sample_hop.argtypes = [P, I64, P, P, P, P, I32, D, U64, I32, U32, P, P, I64]
+        L.or_sample_hop.restype = I64
+        L.or_relabel_hop.argtypes = [P, I64, I64, P, I64, P, P]
+        L.or_relabel_hop.restype = I64
+        L.or_gather.argtypes = [P, I64, P, I64, I32, P, I64]
+        L.or_sage_mean.argtypes = [P, P, I64, P, I64, P, I32, P, I64, P]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+# ---------------------------------------------------------------- O1
+def philox(ctr, key) -> np.ndarray:
+    c, k = _c(ctr, np.uint32), _c(key, np.uint32)
+    out = np.zeros(4, dtype=np.uint32)
+    lib().or_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def mulhi64(r: int, n: int) -> int:
+    return int(lib().or_mulhi64(r, n))
+
+
+# ---------------------------------------------------------------- a0
+class Prep:
+    def __init__(self, indptr, indices, comm, num_comm):
+        self.indptr = _c(indptr, np.int64)
+        self.indices = _c(indices, np.int32)
+        self.comm = _c(comm, np.int32)
+        self.num_comm = int(num_comm)
+        n = self.indptr.shape[0] - 1
+        self.cbeg = np.zeros(self.num_comm + 1, dtype=np.int32)
+        self.lo = np.zeros(n, dtype=np.uint32)
+        self.hi = np.zeros(n, dtype=np.uint32)
+        self.status = lib().or_graph_prep(n, _p(self.indptr), _p(self.indices), _p(self.comm),
+                                          self.num_comm, _p(self.cbeg), _p(self.lo), _p(self.hi))
+
+    @property
+    def num_nodes(self):
+        return self.indptr.shape[0] - 1
+
+
+def graph_prep(bundle) -> Prep:
+    return Prep(bundle.indptr, bundle.indices, bundle.comm, bundle.cfg.num_communities)
+
+
+# ---------------------------------------------------------------- a1
+def order_roots(train, comm, num_comm, mode, mix=0.0, seed=42, epoch=0) -> np.ndarray:
+    t, cm = _c(train, np.int32), _c(comm, np.int32)
+    out = np.zeros(t.shape[0], dtype=np.int32)
+    rc = lib().or_order_roots(t.shape[0], _p(t), _p(cm), int(num_comm), int(mode), float(mix),
+                              int(seed), int(epoch), _p(out))
+    if rc != 0:
+        raise ValueError("or_order_roots failed (empty train set?)")
+    return out
+
+
+def batch_roots(order: np.ndarray, batch_size: int, b: int) -> np.ndarray:
+    """Alg. 1 line 2 "Divide nodes across mini-batches": consecutive B-slices, last partial kept."""
+    return order[b * batch_size: min((b + 1) * batch_size, order.shape[0])]
+
+
+# ---------------------------------------------------------------- a2
+def sample_hop(prep: Prep, dst_nodes, fanout, p, seed, hop, batch):
+    d = _c(dst_nodes, np.int32)
+    cap = d.shape[0] * int(fanout)
+    indptr_h = np.zeros(d.shape[0] + 1, dtype=np.int64)
+    nbr = np.zeros(max(1, cap), dtype=np.int32)
+    e = lib().or_sample_hop(_p(d), d.shape[0], _p(prep.indptr), _p(prep.indices), _p(prep.lo),
+                            _p(prep.hi), int(fanout), float(p), int(seed), int(hop), int(batch),
+                            _p(indptr_h), _p(nbr), cap)
+    assert e >= 0
+    return indptr_h, nbr[:e]
+
+
+# ---------------------------------------------------------------- a3
+def relabel_hop(nodes_prefix, nbr, num_nodes, scratch=None):
+    n_dst = nodes_prefix.shape[0]
+    cap = n_dst + nbr.shape[0]
+    nodes = np.zeros(max(1, cap), dtype=np.int32)
+    nodes[:n_dst] = nodes_prefix
+    local = np.zeros(max(1, nbr.shape[0]), dtype=np.int32)
+    m = scratch if scratch is not None else np.full(num_nodes, -1, dtype=np.int32)
+    nb = _c(nbr, np.int32)
+    n_next = lib().or_relabel_hop(_p(nodes), n_dst, cap, _p(nb), nb.shape[0], _p(local), _p(m))
+    assert n_next >= 0
+    return nodes[:n_next], local[: nb.shape[0]]
+
+
+def sample_blocks(prep: Prep, roots, fanouts, p, seed, batch, scratch=None):
+    """Alg. 1 lines 4-5 for one batch: hop h = 0..L-1 expands nodes[0:n_h).
+
+    Returns dict: nodes (nested prefixes), n (list n_0..n_L), e (list e_0..e_{L-1}),
+    indptr[h] (int64 [n_h+1]), indices[h] (local ids), nbr[h] (global ids)."""
+    nodes = _c(roots, np.int32)
+    n, e, indptr, indices, nbrs = [nodes.shape[0]], [], [], [], []
+    if scratch is None:
+        scratch = np.full(prep.num_nodes, -1, dtype=np.int32)
+    for h, f in enumerate(fanouts):
+        ip, nbr = sample_hop(prep, nodes, f, p, seed, h, batch)
+        nodes, local = relabel_hop(nodes, nbr, prep.num_nodes, scratch)
+        indptr.append(ip)
+        indices.append(local)
+        nbrs.append(nbr)
+        e.append(nbr.shape[0])
+        n.append(nodes.shape[0])
+    return {"nodes": nodes, "n": n, "e": e, "indptr": indptr, "indices": indices, "nbr": nbrs}
+
+
+# ---------------------------------------------------------------- a4
+def gather(nodes, X, F=None) -> np.ndarray:
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    F = X.shape[1] if F is None else F
+    nd = _c(nodes, np.int32)
+    out = np.zeros((nd.shape[0], F), dtype=np.float32)
+    lib().or_gather(_p(nd), nd.shape[0], _p(X), X.shape[1], int(F), _p(out), F)
+    return out
+
+
+# ---------------------------------------------------------------- a5
+def sage_mean(indptr_h, idx, Xsrc, F=None, src_map=None):
+    Xsrc = np.ascontiguousarray(Xsrc, dtype=np.float32)
+    F = Xsrc.shape[1] if F is None else F
+    ip, ix = _c(indptr_h, np.int64), _c(idx, np.int32)
+    n_dst = ip.shape[0] - 1
+    out = np.zeros((n_dst, F), dtype=np.float32)
+    out64 = np.zeros((n_dst, F), dtype=np.float64)
+    sm = None if src_map is None else _c(src_map, np.int32)
+    lib().or_sage_mean(_p(ip), _p(ix), n_dst, _p(Xsrc), Xsrc.shape[1], _p(sm), int(F), _p(out), F,
+                       _p(out64))
+    return out, out64
+
+
+def run_batch(prep: Prep, X, F, roots, fanouts, p, seed, batch, scratch=None):
+    """One whole hot-path step (a2-a5) for one batch, as the oracle defines it."""
+    blk = sample_blocks(prep, roots, fanouts, p, seed, batch, scratch)
+    L = len(fanouts)
+    Xin = gather(blk["nodes"], X, F)
+    H, H64 = sage_mean(blk["indptr"][L - 1], blk["indices"][L - 1], Xin, F)
+    blk.update({"X_in": Xin, "H": H, "H64": H64})
+    return blk
