@@ -1,0 +1,209 @@
+/*
+ * cmb.h -- C ABI of the B200-native COMM-RAND mini-batch hot path
+ * (arXiv 2504.18082, "community-structure-aware randomized mini-batching").
+ *
+ * One mini-batch step (Alg. 1) is:
+ *   a0 cmb_load_graph            community offsets + per-row intra segment (once per graph)
+ *   a1 cmb_order_roots           Knob-1 root order (Table 1; S4.1 P:653-680), once per epoch
+ *   a2+a3 cmb_sample_blocks      Knob-2 biased fanout sampling (S4.2 P:683-691) + dedup/relabel
+ *                                into per-hop blocks ("Build sub-graph S_i")
+ *   a4 cmb_gather_features       input-feature rows of the sub-graph
+ *   a5 cmb_sage_mean_aggregate   GraphSAGE mean aggregation of the input-side block
+ *   a4+a5 cmb_gather_aggregate   both in one pass over the feature table
+ *
+ * Conventions (all entry points):
+ *  - extern "C", plain pointers and sizes; "device" = CUDA global memory of the
+ *    current device, "host" = ordinary host memory.
+ *  - Every device buffer is OWNED BY THE CALLER (allocate it with any CUDA
+ *    allocator, e.g. PyTorch's caching allocator).  The library never allocates
+ *    or frees device memory; workspaces are sized by the *_workspace_bytes
+ *    queries and must be 256-byte aligned.
+ *  - Work is enqueued asynchronously on `stream` (a cudaStream_t, NULL = the
+ *    legacy default stream).  Buffers must stay valid until it completes.
+ *    No entry point except cmb_load_graph(validate=1) and cmb_get_device_status
+ *    synchronises; sizes produced on the device stay on the device, so a whole
+ *    batch can be enqueued (or graph-captured) without host round trips.
+ *  - Errors: host-checkable errors are returned immediately.  Conditions only
+ *    the device can see (capacity overflow, a full hash table, invalid input
+ *    data) set a sticky status word inside the workspace, read with
+ *    cmb_get_device_status.  No call aborts or traps; no exception crosses the
+ *    ABI; cmb_last_error_message() holds a thread-local detail string.
+ *  - Requires a compute capability 10.0 device (B200, sm_100a) and returns
+ *    CMB_ERR_UNSUPPORTED_DEVICE otherwise.
+ *  - Randomness: Philox4x32-10 (Salmon et al., SC'11), key = seed, counter =
+ *    (slot, node-or-community id, (tag << 24) | hop, batch-or-epoch)
+ *    (reading R11); tags 1 = sampling, 2 = root key, 3 = community key.
+ *    Every result is a pure function of (graph, seed, batch/epoch, knobs).
+ */
+#ifndef CMB_H_
+#define CMB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define CMB_API __attribute__((visibility("default")))
+#else
+#define CMB_API
+#endif
+
+#define CMB_VERSION_MAJOR 0
+#define CMB_VERSION_MINOR 1
+#define CMB_MAX_HOPS 8
+#define CMB_MAX_FANOUT 32
+
+typedef enum {
+  CMB_OK = 0,
+  CMB_ERR_INVALID_ARGUMENT = 1,      /* null pointer, bad size/knob, misaligned buffer      */
+  CMB_ERR_INVALID_GRAPH = 2,         /* CSR row unsorted / duplicate / id out of range      */
+  CMB_ERR_NOT_COMMUNITY_ORDERED = 3, /* community ids not non-decreasing / gap / out of range */
+  CMB_ERR_CAPACITY = 4,              /* output or workspace capacity too small               */
+  CMB_ERR_CUDA = 5,                  /* a CUDA runtime call failed (see last_error_message)  */
+  CMB_ERR_UNSUPPORTED_DEVICE = 6,    /* current device is not compute capability 10.x        */
+  CMB_ERR_INVALID_INPUT = 7          /* device-detected bad input (duplicate / unsorted ids) */
+} cmb_status;
+
+/* Knob-1 root partitioning policies (Table 1). */
+typedef enum {
+  CMB_ROOTS_RAND = 0,   /* RAND-ROOTS: uniform shuffle of the training set               */
+  CMB_ROOTS_NORAND = 1, /* NORAND-ROOTS: no shuffle; static across epochs                */
+  CMB_ROOTS_COMM = 2    /* COMM-RAND-MIX-k%: shuffle communities as blocks, group k% of
+                           the training-set communities into super-blocks, shuffle the
+                           nodes inside each super-block (k = mix_fraction)              */
+} cmb_roots_mode;
+
+typedef struct cmb_graph cmb_graph; /* opaque host handle; holds borrowed device pointers */
+
+/* Graph description (a0).  The graph must be community-ordered:
+ * community c owns a contiguous id range, i.e. community[] is non-decreasing and
+ * every id in [0, num_communities) occurs.  Rows are strictly ascending (simple
+ * graph), ids < num_nodes; the graph is expected to be symmetric but the
+ * path does not rely on it. */
+typedef struct {
+  int64_t num_nodes;        /* N                                                        */
+  int64_t num_edges;        /* nnz = number of CSR entries                              */
+  const int64_t* indptr;    /* device [N+1]                                             */
+  const int32_t* indices;   /* device [nnz]                                             */
+  const int32_t* community; /* device [N]                                               */
+  int32_t num_communities;  /* C >= 1                                                   */
+  const float* features;    /* device [N * feat_ld] row-major fp32, or NULL (sample-only) */
+  int32_t feat_dim;         /* F (columns used)                                         */
+  int64_t feat_ld;          /* row stride in floats, >= F                               */
+  void* workspace;          /* device, >= cmb_graph_workspace_bytes(N, C), lives as long as the handle */
+  size_t workspace_bytes;
+  int32_t validate;         /* 1: check CSR + community order on the device and synchronise */
+} cmb_graph_desc;
+
+/* Bytes of graph workspace: community offsets int32[C+1] + per-row intra segment
+ * uint32x2[N] + status word. */
+CMB_API size_t cmb_graph_workspace_bytes(int64_t num_nodes, int32_t num_communities);
+
+/* a0: builds the per-row intra-community segment [lo, hi) of every row (the
+ * neighbours u of v with community[u] == community[v] are contiguous in a
+ * sorted row of a community-ordered graph; reading R5) and returns a handle.
+ * With validate = 1 it synchronises `stream` and returns CMB_ERR_INVALID_GRAPH /
+ * CMB_ERR_NOT_COMMUNITY_ORDERED for bad input. */
+CMB_API cmb_status cmb_load_graph(const cmb_graph_desc* desc, void* stream, cmb_graph** out);
+CMB_API cmb_status cmb_free_graph(cmb_graph* g); /* frees the host handle only */
+/* Device pointers of the a0 products (for tests / tools): cbeg int32[C+1],
+ * bounds uint32[2N] = (lo, hi) per row. */
+CMB_API cmb_status cmb_graph_arrays(const cmb_graph* g, const int32_t** cbeg, const uint32_t** bounds);
+
+/* ------------------------------------------------------------------ a1 */
+CMB_API size_t cmb_order_roots_workspace_bytes(int64_t n_train, int32_t num_communities);
+/* Root order for one epoch (Knob-1).  train_ids: device int32[n_train], ascending
+ * and unique (the training set).  out_order: device int32[n_train], a permutation
+ * of train_ids.  Batches are consecutive batch_size slices of out_order, the last
+ * one partial (reading R21).
+ *   RAND:   sorted by (key(v), v), key(v) = 64-bit Philox(0, v, 2<<24, epoch)
+ *   NORAND: train_ids unchanged
+ *   COMM:   C_tr = distinct communities of the training set (ascending); they are
+ *           shuffled (sorted by (ckey(c), c)); consecutive runs of
+ *           S = max(1, floor(mix_fraction * C_tr + 0.5)) of them form super-blocks;
+ *           nodes are sorted by (super-block, key(v), v).  mix_fraction = 0 is
+ *           COMM-RAND-MIX-0%, 1 reproduces RAND bit for bit (readings R9, R10).
+ * mix_fraction in [0, 1].  Non-ascending train_ids set CMB_ERR_INVALID_INPUT in
+ * the workspace status word. */
+CMB_API cmb_status cmb_order_roots(const cmb_graph* g, const int32_t* train_ids, int64_t n_train,
+                           cmb_roots_mode mode, double mix_fraction, uint64_t seed, uint32_t epoch,
+                           int32_t* out_order, void* workspace, size_t workspace_bytes,
+                           void* stream);
+
+/* ------------------------------------------------------------------ a2 + a3 */
+/* Per-batch sub-graph in HOP order: hop h expands dst nodes nodes[0:n_h) and its
+ * block has src nodes nodes[0:n_{h+1}) (the dst list is the src prefix, reading
+ * R7; DGL's block index is L-1-h).  New src nodes are appended in order of first
+ * occurrence over (dst index, row position) (reading R8).  All buffers device. */
+typedef struct {
+  int32_t* nodes;                      /* [nodes_cap] global ids; nodes[0:n_L) = input nodes  */
+  int64_t nodes_cap;
+  int32_t* indptr[CMB_MAX_HOPS];       /* hop h: [n_cap[h] + 1]; entries beyond n_h equal e_h */
+  int32_t* indices[CMB_MAX_HOPS];      /* hop h: [e_cap[h]] local src ids in [0, n_{h+1})     */
+  int64_t indices_cap[CMB_MAX_HOPS];
+  uint32_t* new_src_mask;              /* optional (NULL): [(e_cap[L-1]+31)/32] words; bit e set
+                                          iff edge e of hop L-1 is the first occurrence of a src
+                                          node that is not a dst node (used by cmb_gather_aggregate) */
+  int64_t* sizes;                      /* [2L+1]: n_0..n_L then e_0..e_{L-1}                  */
+} cmb_blocks;
+
+/* Capacity bounds (host): n_cap[0] = n_roots, e_cap[h] = n_cap[h] * f_h,
+ * n_cap[h+1] = min(num_nodes, n_cap[h] + e_cap[h]).  n_cap has n_hops+1 entries. */
+CMB_API void cmb_blocks_capacity(int64_t n_roots, const int32_t* fanouts, int32_t n_hops,
+                         int64_t num_nodes, int64_t* n_cap, int64_t* e_cap);
+CMB_API size_t cmb_sample_workspace_bytes(int64_t n_roots, const int32_t* fanouts, int32_t n_hops,
+                                  int64_t num_nodes);
+/* Samples an n_hops-hop sub-graph from `roots` (device int32[n_roots], distinct).
+ * fanouts: HOST int32[n_hops] in hop order (fanouts[0] expands the roots; reading
+ * R6), each in [1, CMB_MAX_FANOUT].  p_intra in [0, 1] (Knob-2; the paper's range
+ * is [0.5, 1]): every intra-community edge of the expanded node has weight
+ * P16 = floor(p*65536 + 0.5), every other edge 65536 - P16, and each row draws
+ * min(f, #positive-weight neighbours) distinct neighbours by successive weighted
+ * sampling without replacement (DGL NeighborSampler(prob=...); readings
+ * R1-R4, R13).  batch_id keys the RNG (use epoch * n_batches + b).  Blocks in
+ * `out` must have at least the cmb_blocks_capacity capacities. */
+CMB_API cmb_status cmb_sample_blocks(const cmb_graph* g, const int32_t* roots, int64_t n_roots,
+                             const int32_t* fanouts, int32_t n_hops, double p_intra, uint64_t seed,
+                             uint32_t batch_id, cmb_blocks* out, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------ a4 / a5 */
+/* a4: out[i, 0:F] = features[node_ids[i], 0:F] for i < *n_dev (device count; rows
+ * beyond it up to n_cap are untouched).  Bit-exact copy.  out_ld >= F floats. */
+CMB_API cmb_status cmb_gather_features(const cmb_graph* g, const int32_t* node_ids, const int64_t* n_dev,
+                               int64_t n_cap, float* out, int64_t out_ld, void* stream);
+
+/* a5: H[d, j] = (sum over e in [indptr[d], indptr[d+1]) in CSR order of
+ * src[row(e), j]) / deg_d, fp32 accumulation and IEEE division; H[d] = 0 for an
+ * empty row (reading R12: neighbours only).  row(e) = indices[e], or
+ * src_map[indices[e]] when src_map != NULL (the fused form reading the feature
+ * table directly).  d < *n_dst_dev (device count) <= n_dst_cap. */
+CMB_API cmb_status cmb_sage_mean_aggregate(const int32_t* indptr, const int32_t* indices,
+                                   const int64_t* n_dst_dev, int64_t n_dst_cap, const float* src,
+                                   int64_t src_ld, const int32_t* src_map, int32_t feat_dim,
+                                   float* out, int64_t out_ld, void* stream);
+
+/* a4 + a5 in one pass over the feature table for the input-side block (hop L-1):
+ * writes X_in[i] = features[nodes[i]] for every i < n_L and H = mean aggregate of
+ * hop L-1 (same arithmetic as cmb_sage_mean_aggregate).  Each feature row is
+ * read once per reference; X_in rows of new src nodes are written at their first
+ * occurrence (blocks->new_src_mask must have been filled by cmb_sample_blocks). */
+CMB_API cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* blocks, int32_t n_hops,
+                                int64_t n_last_dst_cap, int64_t nodes_cap, float* x_in,
+                                int64_t x_in_ld, float* h_out, int64_t h_ld, void* stream);
+
+/* ------------------------------------------------------------------ status */
+/* Synchronises `stream`, returns (and clears) the sticky device status word of a
+ * graph / order / sample workspace. */
+CMB_API cmb_status cmb_get_device_status(void* workspace, void* stream);
+CMB_API const char* cmb_status_string(cmb_status s);
+CMB_API const char* cmb_last_error_message(void);
+CMB_API int cmb_version(void); /* major * 100 + minor */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CMB_H_ */

@@ -1,0 +1,366 @@
+"""B200-native COMM-RAND mini-batch hot path (arXiv 2504.18082) -- Python binding.
+
+Thin ctypes layer over ``libcmb.so`` (the C ABI declared in ``include/cmb.h``).
+It only marshals arguments: PyTorch supplies device memory (every buffer and
+workspace is a torch tensor) and the current CUDA stream; every step of the
+path runs in the library's sm_100a kernels.  There is no CPU fallback: if the
+extension is missing or the device is not a B200 the calls raise.
+
+Public API (names follow the C ABI):
+  Graph(...)                       a0  cmb_load_graph
+  order_roots(graph, train, ...)   a1  cmb_order_roots
+  Sampler(graph, ...).sample(...)  a2+a3 cmb_sample_blocks
+  gather_features(...)             a4  cmb_gather_features
+  sage_mean_aggregate(...)         a5  cmb_sage_mean_aggregate
+  Sampler.gather_aggregate(...)    a4+a5 cmb_gather_aggregate
+  MiniBatchPipeline                the whole step (Alg. 1)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcmb.so")
+MAX_HOPS = 8
+MAX_FANOUT = 32
+
+ROOTS_RAND, ROOTS_NORAND, ROOTS_COMM = 0, 1, 2
+_MODES = {"rand": ROOTS_RAND, "norand": ROOTS_NORAND, "comm": ROOTS_COMM}
+
+STATUS = {0: "CMB_OK", 1: "CMB_ERR_INVALID_ARGUMENT", 2: "CMB_ERR_INVALID_GRAPH",
+          3: "CMB_ERR_NOT_COMMUNITY_ORDERED", 4: "CMB_ERR_CAPACITY", 5: "CMB_ERR_CUDA",
+          6: "CMB_ERR_UNSUPPORTED_DEVICE", 7: "CMB_ERR_INVALID_INPUT"}
+
+# C ABI symbols (include/cmb.h); tests check the library exports all of them.
+SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb_graph_arrays",
+           "cmb_order_roots_workspace_bytes", "cmb_order_roots", "cmb_blocks_capacity",
+           "cmb_sample_workspace_bytes", "cmb_sample_blocks", "cmb_gather_features",
+           "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_get_device_status",
+           "cmb_status_string", "cmb_last_error_message", "cmb_version"]
+
+
+class CmbError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class GraphDesc(ctypes.Structure):
+    _fields_ = [("num_nodes", ctypes.c_int64), ("num_edges", ctypes.c_int64),
+                ("indptr", ctypes.c_void_p), ("indices", ctypes.c_void_p),
+                ("community", ctypes.c_void_p), ("num_communities", ctypes.c_int32),
+                ("features", ctypes.c_void_p), ("feat_dim", ctypes.c_int32),
+                ("feat_ld", ctypes.c_int64), ("workspace", ctypes.c_void_p),
+                ("workspace_bytes", ctypes.c_size_t), ("validate", ctypes.c_int32)]
+
+
+class Blocks(ctypes.Structure):
+    _fields_ = [("nodes", ctypes.c_void_p), ("nodes_cap", ctypes.c_int64),
+                ("indptr", ctypes.c_void_p * MAX_HOPS), ("indices", ctypes.c_void_p * MAX_HOPS),
+                ("indices_cap", ctypes.c_int64 * MAX_HOPS), ("new_src_mask", ctypes.c_void_p),
+                ("sizes", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libcmb.so; raise loudly if it was not built (no fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (nvcc, sm_100a); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I64, I32, U32, U64, D, SZ = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                        ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double,
+                                        ctypes.c_size_t)
+        sig = {
+            "cmb_graph_workspace_bytes": (SZ, [I64, I32]),
+            "cmb_load_graph": (I32, [ctypes.POINTER(GraphDesc), P, ctypes.POINTER(P)]),
+            "cmb_free_graph": (I32, [P]),
+            "cmb_graph_arrays": (I32, [P, ctypes.POINTER(P), ctypes.POINTER(P)]),
+            "cmb_order_roots_workspace_bytes": (SZ, [I64, I32]),
+            "cmb_order_roots": (I32, [P, P, I64, I32, D, U64, U32, P, P, SZ, P]),
+            "cmb_blocks_capacity": (None, [I64, P, I32, I64, P, P]),
+            "cmb_sample_workspace_bytes": (SZ, [I64, P, I32, I64]),
+            "cmb_sample_blocks": (I32, [P, P, I64, P, I32, D, U64, U32, ctypes.POINTER(Blocks), P,
+                                        SZ, P]),
+            "cmb_gather_features": (I32, [P, P, P, I64, P, I64, P]),
+            "cmb_sage_mean_aggregate": (I32, [P, P, P, I64, P, I64, P, I32, P, I64, P]),
+            "cmb_gather_aggregate": (I32, [P, ctypes.POINTER(Blocks), I32, I64, I64, P, I64, P,
+                                           I64, P]),
+            "cmb_get_device_status": (I32, [P, P]),
+            "cmb_status_string": (ctypes.c_char_p, [I32]),
+            "cmb_last_error_message": (ctypes.c_char_p, []),
+            "cmb_version": (ctypes.c_int, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(code):
+    if code != 0:
+        raise CmbError(code, lib().cmb_last_error_message().decode())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _dev_tensor(t, dtype, device):
+    if not isinstance(t, torch.Tensor):
+        t = torch.as_tensor(t)
+    return t.to(device=device, dtype=dtype).contiguous()
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    # zero-initialised: its first word is the sticky device status (include/cmb.h)
+    return torch.zeros(max(256, int(nbytes)), dtype=torch.uint8, device=device)
+
+
+class Graph:
+    """a0: a community-ordered CSR graph (+ optional feature table) resident in HBM."""
+
+    def __init__(self, indptr, indices, community, num_communities, features=None, feat_dim=None,
+                 validate=True, device="cuda"):
+        dev = torch.device(device)
+        self.device = dev
+        self.indptr = _dev_tensor(indptr, torch.int64, dev)
+        self.indices = _dev_tensor(indices, torch.int32, dev)
+        self.community = _dev_tensor(community, torch.int32, dev)
+        self.num_nodes = int(self.indptr.shape[0] - 1)
+        self.num_edges = int(self.indices.shape[0])
+        self.num_communities = int(num_communities)
+        self.features = None
+        self.feat_dim = 0
+        self.feat_ld = 0
+        if features is not None:
+            X = features if isinstance(features, torch.Tensor) else torch.as_tensor(features)
+            X = X.to(device=dev, dtype=torch.float32)
+            if X.dim() != 2 or X.stride(1) != 1:
+                X = X.contiguous()
+            self.features = X
+            self.feat_dim = int(feat_dim if feat_dim is not None else X.shape[1])
+            self.feat_ld = int(X.stride(0))
+        nb = lib().cmb_graph_workspace_bytes(self.num_nodes, self.num_communities)
+        self.workspace = _workspace(nb, dev)
+        d = GraphDesc(self.num_nodes, self.num_edges, self.indptr.data_ptr(),
+                      self.indices.data_ptr(), self.community.data_ptr(), self.num_communities,
+                      self.features.data_ptr() if self.features is not None else None,
+                      self.feat_dim, self.feat_ld, self.workspace.data_ptr(), nb, int(validate))
+        h = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            _check(lib().cmb_load_graph(ctypes.byref(d), _stream(), ctypes.byref(h)))
+        self.handle = h
+
+    @classmethod
+    def from_bundle(cls, bundle, device="cuda", features=True, validate=True):
+        X = torch.from_numpy(bundle.X) if (features and bundle.X is not None) else None
+        return cls(torch.from_numpy(bundle.indptr), torch.from_numpy(bundle.indices),
+                   torch.from_numpy(bundle.comm), bundle.cfg.num_communities, X,
+                   bundle.cfg.feat_dim if X is not None else None, validate, device)
+
+    def arrays(self):
+        """(cbeg int32[C+1], bounds int32[N, 2]) device tensors produced by a0."""
+        cb, bd = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib().cmb_graph_arrays(self.handle, ctypes.byref(cb), ctypes.byref(bd)))
+        ws = self.workspace
+        base = ws.data_ptr()
+        cbeg = ws[cb.value - base: cb.value - base + 4 * (self.num_communities + 1)].view(torch.int32)
+        bounds = ws[bd.value - base: bd.value - base + 8 * self.num_nodes].view(torch.int32)
+        return cbeg, bounds.view(self.num_nodes, 2)
+
+    def status(self):
+        return lib().cmb_get_device_status(_ptr(self.workspace), _stream())
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.cmb_free_graph(h)
+            self.handle = None
+
+
+class RootOrderer:
+    """a1: Knob-1 root order per epoch (owns its workspace)."""
+
+    def __init__(self, graph: Graph, train):
+        self.graph = graph
+        self.train = _dev_tensor(train, torch.int32, graph.device)
+        self.n = int(self.train.shape[0])
+        self.workspace = _workspace(lib().cmb_order_roots_workspace_bytes(self.n,
+                                                                          graph.num_communities),
+                                    graph.device)
+        self.out = torch.empty(self.n, dtype=torch.int32, device=graph.device)
+
+    def order(self, mode="rand", mix=0.0, seed=42, epoch=0, out=None):
+        m = _MODES[mode] if isinstance(mode, str) else int(mode)
+        o = self.out if out is None else out
+        _check(lib().cmb_order_roots(self.graph.handle, _ptr(self.train), self.n, m, float(mix),
+                                     int(seed), int(epoch), _ptr(o), _ptr(self.workspace),
+                                     self.workspace.numel(), _stream()))
+        return o
+
+    def status(self):
+        return lib().cmb_get_device_status(_ptr(self.workspace), _stream())
+
+
+def order_roots(graph: Graph, train, mode="rand", mix=0.0, seed=42, epoch=0):
+    return RootOrderer(graph, train).order(mode, mix, seed, epoch).clone()
+
+
+def blocks_capacity(n_roots: int, fanouts: Sequence[int], num_nodes: int):
+    L = len(fanouts)
+    f = (ctypes.c_int32 * L)(*fanouts)
+    nc = (ctypes.c_int64 * (L + 1))()
+    ec = (ctypes.c_int64 * L)()
+    lib().cmb_blocks_capacity(n_roots, f, L, num_nodes, nc, ec)
+    return list(nc), list(ec)
+
+
+@dataclass
+class BatchView:
+    """Device views of one sampled batch (valid until the next sample() call)."""
+    nodes: torch.Tensor           # [nodes_cap] (valid prefix n_L)
+    sizes: torch.Tensor           # [2L+1] n_0..n_L, e_0..e_{L-1} (device)
+    indptr: List[torch.Tensor]    # hop h: [n_cap[h]+1]
+    indices: List[torch.Tensor]   # hop h: [e_cap[h]]
+    new_src_mask: torch.Tensor
+
+    def host_sizes(self):
+        s = self.sizes.cpu().tolist()
+        L = len(self.indptr)
+        return s[: L + 1], s[L + 1:]
+
+
+class Sampler:
+    """a2+a3 (+ a4/a5): owns the workspace and the output blocks for batches of at
+    most `max_roots` roots with the given hop-ordered fanouts."""
+
+    def __init__(self, graph: Graph, max_roots: int, fanouts: Sequence[int]):
+        self.graph = graph
+        self.fanouts = [int(f) for f in fanouts]
+        self.L = L = len(self.fanouts)
+        if not (1 <= L <= MAX_HOPS) or any(f < 1 or f > MAX_FANOUT for f in self.fanouts):
+            raise ValueError("fanouts: 1..8 hops, each in [1, 32]")
+        self.max_roots = int(max_roots)
+        dev = graph.device
+        self.n_cap, self.e_cap = blocks_capacity(self.max_roots, self.fanouts, graph.num_nodes)
+        self._f = (ctypes.c_int32 * L)(*self.fanouts)
+        self.workspace = _workspace(lib().cmb_sample_workspace_bytes(self.max_roots, self._f, L,
+                                                                     graph.num_nodes), dev)
+        self.nodes = torch.empty(self.n_cap[L], dtype=torch.int32, device=dev)
+        self.indptr = [torch.empty(self.n_cap[h] + 1, dtype=torch.int32, device=dev)
+                       for h in range(L)]
+        self.indices = [torch.empty(max(1, self.e_cap[h]), dtype=torch.int32, device=dev)
+                        for h in range(L)]
+        self.mask = torch.empty((self.e_cap[L - 1] + 31) // 32 + 1, dtype=torch.int32, device=dev)
+        self.sizes = torch.zeros(2 * L + 1, dtype=torch.int64, device=dev)
+        b = Blocks()
+        b.nodes = self.nodes.data_ptr()
+        b.nodes_cap = self.n_cap[L]
+        for h in range(L):
+            b.indptr[h] = self.indptr[h].data_ptr()
+            b.indices[h] = self.indices[h].data_ptr()
+            b.indices_cap[h] = self.e_cap[h]
+        b.new_src_mask = self.mask.data_ptr()
+        b.sizes = self.sizes.data_ptr()
+        self._blocks = b
+        self.x_in = None
+        self.h = None
+
+    def sample(self, roots: torch.Tensor, p: float, seed: int, batch_id: int) -> BatchView:
+        n = int(roots.shape[0])
+        if n > self.max_roots:
+            raise ValueError("more roots than max_roots")
+        _check(lib().cmb_sample_blocks(self.graph.handle, _ptr(roots), n, self._f, self.L,
+                                       float(p), int(seed), int(batch_id), ctypes.byref(self._blocks),
+                                       _ptr(self.workspace), self.workspace.numel(), _stream()))
+        return BatchView(self.nodes, self.sizes, self.indptr, self.indices, self.mask)
+
+    def alloc_features(self):
+        g = self.graph
+        if self.x_in is None:
+            self.x_in = torch.empty(self.n_cap[self.L], g.feat_ld, dtype=torch.float32,
+                                    device=g.device)
+            self.h = torch.empty(self.n_cap[self.L - 1], g.feat_ld, dtype=torch.float32,
+                                 device=g.device)
+        return self.x_in, self.h
+
+    def gather_aggregate(self):
+        """a4 + a5 fused for the last sampled batch -> (X_in [n_L, ld], H [n_{L-1}, ld])."""
+        x_in, h = self.alloc_features()
+        _check(lib().cmb_gather_aggregate(self.graph.handle, ctypes.byref(self._blocks), self.L,
+                                          self.n_cap[self.L - 1], self.n_cap[self.L], _ptr(x_in),
+                                          x_in.stride(0), _ptr(h), h.stride(0), _stream()))
+        return x_in, h
+
+    def status(self):
+        return lib().cmb_get_device_status(_ptr(self.workspace), _stream())
+
+
+def gather_features(graph: Graph, node_ids: torch.Tensor, n_dev: torch.Tensor, out: torch.Tensor):
+    """a4: out[i] = X[node_ids[i]] for i < n_dev[0] (n_dev: device int64 scalar tensor)."""
+    _check(lib().cmb_gather_features(graph.handle, _ptr(node_ids), _ptr(n_dev), out.shape[0],
+                                     _ptr(out), out.stride(0), _stream()))
+    return out
+
+
+def sage_mean_aggregate(indptr: torch.Tensor, indices: torch.Tensor, n_dst_dev: torch.Tensor,
+                        src: torch.Tensor, feat_dim: int, out: torch.Tensor,
+                        src_map: Optional[torch.Tensor] = None, n_dst_cap: Optional[int] = None):
+    """a5: out[d] = mean over the CSR row d of src[row] (row = src_map[idx] if given)."""
+    cap = out.shape[0] if n_dst_cap is None else n_dst_cap
+    _check(lib().cmb_sage_mean_aggregate(_ptr(indptr), _ptr(indices), _ptr(n_dst_dev), cap,
+                                         _ptr(src), src.stride(0), _ptr(src_map), int(feat_dim),
+                                         _ptr(out), out.stride(0), _stream()))
+    return out
+
+
+class MiniBatchPipeline:
+    """One COMM-RAND mini-batch step per call (Alg. 1), all on the GPU:
+    Knob-1 order once per epoch, then per batch Knob-2 sampling + relabel (a2, a3) and
+    the fused input-feature gather + SAGE-mean aggregation (a4, a5)."""
+
+    def __init__(self, graph: Graph, train, batch_size: int, fanouts: Sequence[int],
+                 mode="rand", mix=0.0, p=0.5, seed=42):
+        self.graph = graph
+        self.orderer = RootOrderer(graph, train)
+        self.batch_size = int(batch_size)
+        self.n_batches = (self.orderer.n + self.batch_size - 1) // self.batch_size
+        self.sampler = Sampler(graph, self.batch_size, fanouts)
+        self.mode, self.mix, self.p, self.seed = mode, float(mix), float(p), int(seed)
+        self.epoch = None
+        self.order = None
+
+    def start_epoch(self, epoch: int):
+        self.order = self.orderer.order(self.mode, self.mix, self.seed, epoch)
+        self.epoch = int(epoch)
+
+    def batch_roots(self, b: int) -> torch.Tensor:
+        return self.order[b * self.batch_size: min((b + 1) * self.batch_size, self.orderer.n)]
+
+    def step(self, global_batch: int, roots: Optional[torch.Tensor] = None):
+        """Run batch `global_batch` (= epoch * n_batches + b).  Returns (BatchView, X_in, H)."""
+        epoch, b = divmod(int(global_batch), self.n_batches)
+        if roots is None:
+            if self.epoch != epoch:
+                self.start_epoch(epoch)
+            roots = self.batch_roots(b)
+        view = self.sampler.sample(roots, self.p, self.seed, int(global_batch))
+        x_in, h = self.sampler.gather_aggregate()
+        return view, x_in, h

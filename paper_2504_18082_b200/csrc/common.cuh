@@ -1,0 +1,119 @@
+// common.cuh -- shared device/host helpers of the cmb CUDA library (sm_100a).
+// Product code only: nothing here is shared with oracle/ (see DESIGN.md).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "cmb.h"
+
+namespace cmb {
+
+// ---------------------------------------------------------------- errors
+void set_error(const char* fmt, ...);
+cmb_status cuda_fail(cudaError_t e, const char* what);
+cmb_status require_sm100();
+
+#define CMB_CUDA(call)                                        \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return ::cmb::cuda_fail(e_, #call); \
+  } while (0)
+
+#define CMB_ARG(cond, ...)                         \
+  do {                                             \
+    if (!(cond)) {                                 \
+      ::cmb::set_error(__VA_ARGS__);               \
+      return CMB_ERR_INVALID_ARGUMENT;             \
+    }                                              \
+  } while (0)
+
+// Sticky device status word (first 4 bytes of every workspace header).
+struct WsHeader {
+  int32_t status;
+  int32_t pad[63];
+};
+static_assert(sizeof(WsHeader) == 256, "header is one 256-byte line");
+
+__device__ __forceinline__ void raise_status(int32_t* st, int32_t code) {
+  atomicCAS(st, 0, code);  // first error wins
+}
+
+// ---------------------------------------------------------------- workspace carving
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+  size_t bytes() const { return (off + 255) & ~size_t(255); }
+};
+
+// ---------------------------------------------------------------- Philox4x32-10
+// Salmon et al., SC'11.  Written independently of oracle/oracle.c.
+struct PhiloxOut {
+  uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ PhiloxOut philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
+                                                   uint32_t c3, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t a = 0xD2511F53u * c0;
+    const uint32_t ah = __umulhi(0xD2511F53u, c0);
+    const uint32_t b = 0xCD9E8D57u * c2;
+    const uint32_t bh = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = bh ^ c1 ^ k0;
+    const uint32_t n2 = ah ^ c3 ^ k1;
+    c0 = n0;
+    c1 = b;
+    c2 = n2;
+    c3 = a;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return PhiloxOut{c0, c1, c2, c3};
+}
+
+enum : uint32_t { kTagSample = 1u, kTagRoot = 2u, kTagComm = 3u };
+
+__device__ __forceinline__ uint64_t lo64(const PhiloxOut& w) {
+  return (static_cast<uint64_t>(w.y) << 32) | w.x;
+}
+__device__ __forceinline__ uint64_t hi64(const PhiloxOut& w) {
+  return (static_cast<uint64_t>(w.w) << 32) | w.z;
+}
+
+// Graph as seen by kernels.
+struct DevGraph {
+  int64_t n;
+  int64_t nnz;
+  const int64_t* indptr;
+  const int32_t* indices;
+  const int32_t* comm;
+  int32_t ncomm;
+  const int32_t* cbeg;   // [C+1]
+  const uint2* bounds;   // [N] (lo, hi) row offsets of the intra segment
+  const float* x;
+  int32_t f;
+  int64_t ld;
+};
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace cmb
+
+struct cmb_graph {
+  cmb::DevGraph d;
+  int32_t* status;  // graph workspace header
+  int device;
+  int num_sms;
+};

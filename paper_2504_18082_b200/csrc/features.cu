@@ -1,0 +1,325 @@
+// features.cu -- a4 (input-feature gather) and a5 (GraphSAGE mean
+// aggregation of the input-side block; reading R12), separately and fused.
+//
+// These are the HBM-bound steps: the paper attributes the per-epoch time to the input-
+// feature volume and the COMM-RAND speedup to L2 reuse.  Rows are
+// moved with 128-bit coalesced loads/stores by groups of LPR lanes (one group per row, LPR
+// = the smallest power of two covering F/4 float4s, capped at 32), with several independent
+// rows/edges in flight per lane (Little's law: ~6 MB in flight chip-wide at ~8 TB/s).
+// Aggregation keeps columns in lanes and walks the edges of a row in CSR order, so the fp32
+// sum is formed in exactly the oracle's order (bit-exact; then IEEE division).
+#include "common.cuh"
+
+namespace cmb {
+namespace {
+
+__device__ __forceinline__ float4 ldg4(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void add4(float4& a, const float4& b) {
+  a.x = __fadd_rn(a.x, b.x);
+  a.y = __fadd_rn(a.y, b.y);
+  a.z = __fadd_rn(a.z, b.z);
+  a.w = __fadd_rn(a.w, b.w);
+}
+
+// ------------------------------------------------------------------ a4 gather
+// U rows in flight per lane group; NV float4 per lane per row.
+template <int LPR, int NV, int U>
+__global__ void __launch_bounds__(256) k_gather_v4(const float4* __restrict__ x, int64_t ld4,
+                                                   const int32_t* __restrict__ ids,
+                                                   const int64_t* __restrict__ n_dev,
+                                                   int64_t n_cap, int f4,
+                                                   float4* __restrict__ out, int64_t out_ld4) {
+  const int64_t n = min(*n_dev, n_cap);
+  const int lane = threadIdx.x % LPR;
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / LPR);
+  const int64_t g0 = blockIdx.x * (int64_t)(blockDim.x / LPR) + threadIdx.x / LPR;
+  for (int64_t base = g0; base < n; base += groups * U) {
+    for (int c0 = 0; c0 < f4; c0 += LPR * NV) {
+      float4 v[U][NV];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t row = base + u * groups;
+        const float4* src = x + (row < n ? (int64_t)__ldg(ids + row) * ld4 : 0);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          const int c = c0 + lane + k * LPR;
+          if (row < n && c < f4) v[u][k] = ldg4(src + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t row = base + u * groups;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          const int c = c0 + lane + k * LPR;
+          if (row < n && c < f4) out[row * out_ld4 + c] = v[u][k];
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_gather_scalar(const float* __restrict__ x, int64_t ld,
+                                const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev,
+                                int64_t n_cap, int f, float* __restrict__ out, int64_t out_ld) {
+  const int64_t n = min(*n_dev, n_cap);
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = w0; row < n; row += nw) {
+    const float* src = x + (int64_t)ids[row] * ld;
+    for (int c = lane; c < f; c += 32) out[row * out_ld + c] = src[c];
+  }
+}
+
+// ------------------------------------------------------------------ a5 (+ a4 fused)
+// One group of LPR lanes per dst row d.  For every edge e of row d (CSR order) the src row
+// r(e) = map ? map[idx[e]] : idx[e] is loaded (CH edges in flight), accumulated, and --
+// when x_in != NULL (fused a4) and bit e of new_mask is set -- also stored as X_in[idx[e]]
+// (the first occurrence of that src node).  Rows d < n_dst also store X_in[d] (self row).
+template <int LPR, int NV, int CH>
+__global__ void __launch_bounds__(256) k_sage_mean_v4(
+    const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+    const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap, const float4* __restrict__ src,
+    int64_t src_ld4, const int32_t* __restrict__ map, int f4, float4* __restrict__ out,
+    int64_t out_ld4, float4* __restrict__ x_in, int64_t x_in_ld4,
+    const uint32_t* __restrict__ new_mask) {
+  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
+  const int lane = threadIdx.x % LPR;
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / LPR);
+  for (int64_t d = blockIdx.x * (int64_t)(blockDim.x / LPR) + threadIdx.x / LPR; d < n_dst;
+       d += groups) {
+    const int32_t e0 = __ldg(indptr + d), e1 = __ldg(indptr + d + 1);
+    const int32_t deg = e1 - e0;
+    for (int c0 = 0; c0 < f4; c0 += LPR * NV) {
+      float4 acc[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (x_in) {  // self row of dst d -> X_in[d]
+        const float4* s = src + (int64_t)__ldg(map + d) * src_ld4;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          const int c = c0 + lane + k * LPR;
+          if (c < f4) x_in[d * x_in_ld4 + c] = ldg4(s + c);
+        }
+      }
+      for (int32_t eb = e0; eb < e1; eb += CH) {
+        float4 v[CH][NV];
+        int32_t li[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int32_t e = eb + j;
+          li[j] = e < e1 ? __ldg(idx + e) : 0;
+          const int64_t r = map ? (int64_t)__ldg(map + li[j]) : (int64_t)li[j];
+          const float4* s = src + r * src_ld4;
+#pragma unroll
+          for (int k = 0; k < NV; ++k) {
+            const int c = c0 + lane + k * LPR;
+            if (e < e1 && c < f4) v[j][k] = ldg4(s + c);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int32_t e = eb + j;
+          if (e < e1) {
+#pragma unroll
+            for (int k = 0; k < NV; ++k) add4(acc[k], v[j][k]);
+            if (x_in && ((__ldg(new_mask + (e >> 5)) >> (e & 31)) & 1u)) {
+#pragma unroll
+              for (int k = 0; k < NV; ++k) {
+                const int c = c0 + lane + k * LPR;
+                if (c < f4) x_in[(int64_t)li[j] * x_in_ld4 + c] = v[j][k];
+              }
+            }
+          }
+        }
+      }
+      const float fd = static_cast<float>(deg);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int c = c0 + lane + k * LPR;
+        if (c < f4) {
+          float4 h = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (deg > 0) {
+            h.x = __fdiv_rn(acc[k].x, fd);
+            h.y = __fdiv_rn(acc[k].y, fd);
+            h.z = __fdiv_rn(acc[k].z, fd);
+            h.w = __fdiv_rn(acc[k].w, fd);
+          }
+          out[d * out_ld4 + c] = h;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_sage_mean_scalar(const int32_t* __restrict__ indptr,
+                                   const int32_t* __restrict__ idx,
+                                   const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
+                                   const float* __restrict__ src, int64_t src_ld,
+                                   const int32_t* __restrict__ map, int f, float* __restrict__ out,
+                                   int64_t out_ld, float* __restrict__ x_in, int64_t x_in_ld,
+                                   const uint32_t* __restrict__ new_mask) {
+  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t d = w0; d < n_dst; d += nw) {
+    const int32_t e0 = indptr[d], e1 = indptr[d + 1];
+    for (int c = lane; c < f; c += 32) {
+      if (x_in) x_in[d * x_in_ld + c] = src[(int64_t)map[d] * src_ld + c];
+      float acc = 0.f;
+      for (int32_t e = e0; e < e1; ++e) {
+        const int32_t l = idx[e];
+        const float xv = src[(map ? (int64_t)map[l] : (int64_t)l) * src_ld + c];
+        acc = __fadd_rn(acc, xv);
+        if (x_in && ((new_mask[e >> 5] >> (e & 31)) & 1u)) x_in[(int64_t)l * x_in_ld + c] = xv;
+      }
+      out[d * out_ld + c] = e1 > e0 ? __fdiv_rn(acc, static_cast<float>(e1 - e0)) : 0.f;
+    }
+  }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int lanes_for(int f4) {
+  int l = 1;
+  while (l < f4 && l < 32) l <<= 1;
+  return l < 4 ? 4 : l;  // groups of >= 4 lanes keep one row per 64-byte segment
+}
+
+template <int LPR, int NV>
+void launch_gather(int grid, cudaStream_t s, const float* x, int64_t ld, const int32_t* ids,
+                   const int64_t* n_dev, int64_t n_cap, int f4, float* out, int64_t out_ld) {
+  k_gather_v4<LPR, NV, 4><<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(x), ld / 4, ids,
+                                               n_dev, n_cap, f4, reinterpret_cast<float4*>(out),
+                                               out_ld / 4);
+}
+
+cmb_status gather_dispatch(const float* x, int64_t ld, int f, const int32_t* ids,
+                           const int64_t* n_dev, int64_t n_cap, float* out, int64_t out_ld,
+                           int sms, cudaStream_t s) {
+  if (n_cap <= 0) return CMB_OK;
+  const int f4 = (f + 3) / 4;
+  const bool vec = aligned16(x) && aligned16(out) && ld % 4 == 0 && out_ld % 4 == 0;
+  if (!vec) {
+    k_gather_scalar<<<sms * 8, 256, 0, s>>>(x, ld, ids, n_dev, n_cap, f, out, out_ld);
+    CMB_CUDA(cudaGetLastError());
+    return CMB_OK;
+  }
+  const int lpr = lanes_for(f4);
+  const int rows_per_block = 256 / lpr;
+  int64_t want = (n_cap + rows_per_block * 4 - 1) / (rows_per_block * 4);
+  const int grid = static_cast<int>(want < sms * 16 ? (want > 0 ? want : 1) : sms * 16);
+  switch (lpr) {
+    case 4: launch_gather<4, 1>(grid, s, x, ld, ids, n_dev, n_cap, f4, out, out_ld); break;
+    case 8: launch_gather<8, 1>(grid, s, x, ld, ids, n_dev, n_cap, f4, out, out_ld); break;
+    case 16: launch_gather<16, 1>(grid, s, x, ld, ids, n_dev, n_cap, f4, out, out_ld); break;
+    default:
+      if (f4 <= 32) launch_gather<32, 1>(grid, s, x, ld, ids, n_dev, n_cap, f4, out, out_ld);
+      else launch_gather<32, 2>(grid, s, x, ld, ids, n_dev, n_cap, f4, out, out_ld);
+  }
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+template <int LPR, int NV, int CH>
+void launch_mean(int grid, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
+                 const int64_t* n_dev, int64_t n_cap, const float* src, int64_t src_ld,
+                 const int32_t* map, int f4, float* out, int64_t out_ld, float* x_in,
+                 int64_t x_in_ld, const uint32_t* mask) {
+  k_sage_mean_v4<LPR, NV, CH><<<grid, 256, 0, s>>>(
+      indptr, idx, n_dev, n_cap, reinterpret_cast<const float4*>(src), src_ld / 4, map, f4,
+      reinterpret_cast<float4*>(out), out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4,
+      mask);
+}
+
+cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int64_t* n_dev,
+                         int64_t n_cap, const float* src, int64_t src_ld, const int32_t* map,
+                         int f, float* out, int64_t out_ld, float* x_in, int64_t x_in_ld,
+                         const uint32_t* mask, int sms, cudaStream_t s) {
+  if (n_cap <= 0) return CMB_OK;
+  const int f4 = (f + 3) / 4;
+  const bool vec = aligned16(src) && aligned16(out) && src_ld % 4 == 0 && out_ld % 4 == 0 &&
+                   (!x_in || (aligned16(x_in) && x_in_ld % 4 == 0));
+  if (!vec) {
+    k_sage_mean_scalar<<<sms * 8, 256, 0, s>>>(indptr, idx, n_dev, n_cap, src, src_ld, map, f,
+                                               out, out_ld, x_in, x_in_ld, mask);
+    CMB_CUDA(cudaGetLastError());
+    return CMB_OK;
+  }
+  const int lpr = lanes_for(f4);
+  const int rows_per_block = 256 / lpr;
+  int64_t want = (n_cap + rows_per_block - 1) / rows_per_block;
+  const int grid = static_cast<int>(want < sms * 16 ? (want > 0 ? want : 1) : sms * 16);
+#define CMB_MEAN(L_, NV_, CH_)                                                            \
+  launch_mean<L_, NV_, CH_>(grid, s, indptr, idx, n_dev, n_cap, src, src_ld, map, f4, out, \
+                            out_ld, x_in, x_in_ld, mask)
+  switch (lpr) {
+    case 4: CMB_MEAN(4, 1, 8); break;
+    case 8: CMB_MEAN(8, 1, 8); break;
+    case 16: CMB_MEAN(16, 1, 8); break;
+    default:
+      if (f4 <= 32) CMB_MEAN(32, 1, 8);
+      else if (f4 <= 64) CMB_MEAN(32, 2, 4);
+      else if (f4 <= 128) CMB_MEAN(32, 4, 2);
+      else CMB_MEAN(32, 5, 2);  // F = 602 -> 151 float4 = 32 x 5 (column tiles beyond)
+  }
+#undef CMB_MEAN
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+}  // namespace
+}  // namespace cmb
+
+using namespace cmb;
+
+extern "C" {
+
+cmb_status cmb_gather_features(const cmb_graph* g, const int32_t* node_ids, const int64_t* n_dev,
+                               int64_t n_cap, float* out, int64_t out_ld, void* stream) {
+  CMB_ARG(g && node_ids && n_dev && out, "cmb_gather_features: null argument");
+  CMB_ARG(g->d.x != nullptr, "cmb_gather_features: graph has no feature table");
+  CMB_ARG(n_cap >= 0 && out_ld >= g->d.f, "cmb_gather_features: n_cap < 0 or out_ld < F");
+  return gather_dispatch(g->d.x, g->d.ld, g->d.f, node_ids, n_dev, n_cap, out, out_ld,
+                         g->num_sms, static_cast<cudaStream_t>(stream));
+}
+
+cmb_status cmb_sage_mean_aggregate(const int32_t* indptr, const int32_t* indices,
+                                   const int64_t* n_dst_dev, int64_t n_dst_cap, const float* src,
+                                   int64_t src_ld, const int32_t* src_map, int32_t feat_dim,
+                                   float* out, int64_t out_ld, void* stream) {
+  CMB_ARG(indptr && indices && n_dst_dev && src && out, "cmb_sage_mean_aggregate: null argument");
+  CMB_ARG(feat_dim >= 1 && src_ld >= feat_dim && out_ld >= feat_dim && n_dst_cap >= 0,
+          "cmb_sage_mean_aggregate: bad feat_dim / ld / n_dst_cap");
+  int dev = 0, sms = 148;
+  CMB_CUDA(cudaGetDevice(&dev));
+  CMB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  return mean_dispatch(indptr, indices, n_dst_dev, n_dst_cap, src, src_ld, src_map, feat_dim, out,
+                       out_ld, nullptr, 0, nullptr, sms, static_cast<cudaStream_t>(stream));
+}
+
+cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                int64_t n_last_dst_cap, int64_t nodes_cap, float* x_in,
+                                int64_t x_in_ld, float* h_out, int64_t h_ld, void* stream) {
+  CMB_ARG(g && b && x_in && h_out, "cmb_gather_aggregate: null argument");
+  CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_gather_aggregate: bad n_hops");
+  CMB_ARG(g->d.x != nullptr, "cmb_gather_aggregate: graph has no feature table");
+  CMB_ARG(b->new_src_mask != nullptr, "cmb_gather_aggregate: blocks->new_src_mask is required");
+  CMB_ARG(x_in_ld >= g->d.f && h_ld >= g->d.f, "cmb_gather_aggregate: ld < F");
+  CMB_ARG(n_last_dst_cap <= nodes_cap, "cmb_gather_aggregate: n_last_dst_cap > nodes_cap");
+  const int L = n_hops;
+  return mean_dispatch(b->indptr[L - 1], b->indices[L - 1], b->sizes + (L - 1), n_last_dst_cap,
+                       g->d.x, g->d.ld, b->nodes, g->d.f, h_out, h_ld, x_in, x_in_ld,
+                       b->new_src_mask, g->num_sms, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
