@@ -1,0 +1,469 @@
+#!/usr/bin/env python
+"""Benchmark of the COMM-RAND mini-batch hot path on B200 (BASELINE.json metric).
+
+A step = one pass of the whole hot path over one mini-batch of the
+products-shaped synthetic workload (BASELINE.json configs[3]; the config the
+metric's "1/2/4/8 B200" is quoted on): Knob-2 biased 3-hop sampling + dedup/
+relabel (a2, a3) and the fused input-feature gather + GraphSAGE-mean aggregation
+(a4, a5); the Knob-1 root order (a1) is recomputed at the start of the timed
+region and at every epoch boundary inside it (it is once per epoch).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cmb|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+
+Multi-GPU: batches are independent units (reading R22): rank r runs global
+batches r, r+N, r+2N, ... with the graph and features replicated; there is no
+per-batch collective (weak scaling).  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="cmb", choices=["cmb", "reference"])
+    ap.add_argument("--config", default="products")
+    ap.add_argument("--mode", default="rand", choices=["rand", "norand", "comm"])
+    ap.add_argument("--mix", type=float, default=0.0)
+    ap.add_argument("--p", type=float, default=None)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--no-extra", action="store_true", help="skip the knob-sweep extra points")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+METRIC = "mini-batches/s"
+
+
+# ------------------------------------------------------------------ helpers
+class ClockSampler:
+    """SM clock + clock-event (throttle) reasons sampled every ~5 ms during the timed
+    region through NVML (the same counters nvidia-smi's clocks line reads)."""
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return
+        while not self._stop.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            self._stop.wait(0.005)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        time.sleep(0.02)
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for _, rs in self.rows for n, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows), "source": "NVML during the timed region"}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload, knob):
+    """Per-launch DRAM bytes of the fused gather/aggregate kernel from the committed
+    ncu --set full capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(f"{workload}|{knob}")
+    except Exception:
+        return None
+
+
+def algorithmic_bytes(n, e, F, L):
+    """Fused a4+a5 launch: every unique input row read once
+    (U*R), X_in written (U*R), H written (n_{L-1}*R), plus the int32 index streams
+    (indices of hop L-1, indptr of hop L-1, the relabel map nodes[0:U))."""
+    R = 4 * F
+    U, nd, ed = n[L], n[L - 1], e[L - 1]
+    return 2 * U * R + nd * R + 4 * ed + 4 * (nd + 1) + 4 * U
+
+
+# ------------------------------------------------------------------ cpu (oracle) legs
+def oracle_batches(bundle, mode, mix, p, seed, budget_s, max_batches=None):
+    """Times the oracle (as it stands, single thread) on consecutive batches of epoch 0."""
+    import oracle
+    cfg = bundle.cfg
+    prep = oracle.graph_prep(bundle)
+    modes = {"rand": oracle.MODE_RAND, "norand": oracle.MODE_NORAND, "comm": oracle.MODE_COMM}
+    scratch = np.full(prep.num_nodes, -1, dtype=np.int32)
+    t0 = time.perf_counter()
+    order = oracle.order_roots(bundle.train, bundle.comm, cfg.num_communities, modes[mode], mix,
+                               seed, 0)
+    nb = (order.shape[0] + cfg.batch_size - 1) // cfg.batch_size
+    done, edges = 0, 0
+    while True:
+        r = oracle.run_batch(prep, bundle.X, cfg.feat_dim, oracle.batch_roots(order, cfg.batch_size, done % nb),
+                             cfg.fanouts, p, seed, done % nb, scratch)
+        edges += sum(r["e"])
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or (max_batches and done >= max_batches):
+            break
+    return done, el, edges
+
+
+def run_reference(args, bundle):
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = bundle.cfg
+    p = cfg.p_intra if args.p is None else args.p
+    import oracle
+    prep = oracle.graph_prep(bundle)
+    modes = {"rand": oracle.MODE_RAND, "norand": oracle.MODE_NORAND, "comm": oracle.MODE_COMM}
+    order = oracle.order_roots(bundle.train, bundle.comm, cfg.num_communities, modes[args.mode],
+                               args.mix, args.seed, 0)
+    nb = (order.shape[0] + cfg.batch_size - 1) // cfg.batch_size
+    scratch = np.full(prep.num_nodes, -1, dtype=np.int32)
+
+    def step(b):
+        return oracle.run_batch(prep, bundle.X, cfg.feat_dim, oracle.batch_roots(order, cfg.batch_size, b % nb),
+                                cfg.fanouts, p, args.seed, b % nb, scratch)
+
+    for w in range(args.warmup):
+        step(w)
+    t0 = time.perf_counter()
+    edges = 0
+    for k in range(args.steps):
+        edges += sum(step(args.warmup + k)["e"])
+    el = time.perf_counter() - t0
+    val = args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "batches/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args, cfg, bundle, p),
+            "sampled_edges_per_s": edges / el,
+            "cpu_baseline": {"value": val, "unit": "batches/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} consecutive batches of epoch 0, one per step, "
+                                       f"single-threaded plain-C oracle (oracle/oracle.c)"},
+            "e2e": {"value": val, "unit": "batches/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, cfg, bundle, p):
+    return {"workload": f"{cfg.name}-shaped synthetic (BASELINE.json configs[3])"
+            if cfg.name == "products" else f"{cfg.name}-shaped synthetic",
+            "num_nodes": cfg.num_nodes, "nnz": int(bundle.nnz), "feat_dim": cfg.feat_dim,
+            "batch": cfg.batch_size, "fanouts_hop_order": list(cfg.fanouts),
+            "knob1": args.mode + (f"(k={args.mix})" if args.mode == "comm" else ""),
+            "p_intra": p, "seed": args.seed,
+            "l2": "no flush: inputs larger than L2 (X %.0f MB, CSR %.0f MB > 126 MB)"
+                  % (cfg.num_nodes * cfg.feat_ld * 4 / 1e6, bundle.nnz * 4 / 1e6),
+            "parallelism": f"dp{args.gpus} (batches round-robin over ranks, graph replicated)"}
+
+
+# ------------------------------------------------------------------ gpu leg
+def count_launches(fn):
+    """Kernels our library launches in one call of fn (CUPTI via torch.profiler)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+    ours = [n for n in names if ("cmb" in n or "cub" in n.lower()) and "emcpy" not in n and "emset" not in n]
+    return len(ours), sorted(set(ours))
+
+
+def run_cmb(args, bundle):
+    import torch
+    import torch.distributed as dist
+    import paper_2504_18082_b200 as cmb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = bundle.cfg
+    p = cfg.p_intra if args.p is None else args.p
+    L = len(cfg.fanouts)
+    graph = cmb.Graph.from_bundle(bundle, device=dev, validate=True)
+    pipe = cmb.MiniBatchPipeline(graph, torch.from_numpy(bundle.train), cfg.batch_size,
+                                 cfg.fanouts, mode=args.mode, mix=args.mix, p=p, seed=args.seed)
+    nb = pipe.n_batches
+    stream = torch.cuda.current_stream()
+    K, W = args.steps, args.warmup
+    sizes_log = torch.zeros(K, 2 * L + 1, dtype=torch.int64, device=dev)
+
+    def gbatch(t):  # global batch id of this rank's t-th step
+        return t * world + rank
+
+    def one_step(t, ev=None, ev_s=None):
+        gb = gbatch(t)
+        epoch, b = divmod(gb, nb)
+        if pipe.epoch != epoch:
+            pipe.start_epoch(epoch)
+        roots = pipe.batch_roots(b)
+        if ev_s is not None:
+            ev_s[0].record(stream)
+        pipe.sampler.sample(roots, p, args.seed, gb)
+        if ev is not None:
+            ev[0].record(stream)
+        pipe.sampler.gather_aggregate()
+        if ev is not None:
+            ev[1].record(stream)
+
+    # warm-up (also compiles nothing: the library is prebuilt)
+    for t in range(W):
+        one_step(t)
+    torch.cuda.synchronize()
+    for obj in (graph, pipe.orderer, pipe.sampler):
+        st = obj.status()
+        if st != 0:
+            raise RuntimeError(f"device status {st} after warm-up")
+    n_launch_step, kernel_names = count_launches(lambda: one_step(W))
+    n_launch_order, _ = count_launches(lambda: pipe.start_epoch(pipe.epoch))
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(K)]
+    evs_s = [(torch.cuda.Event(enable_timing=True),) for _ in range(K)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    orders_in_region = 0
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        pipe.start_epoch(gbatch(W) // nb)       # a1 for the current epoch, inside the region
+        orders_in_region += 1
+        for k in range(K):
+            t = W + k
+            ep = gbatch(t) // nb
+            if pipe.epoch != ep:
+                orders_in_region += 1
+            one_step(t, evs[k], evs_s[k])
+            sizes_log[k].copy_(pipe.sampler.sizes, non_blocking=True)
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    agg_ms = [evs[k][0].elapsed_time(evs[k][1]) for k in range(K)]
+    samp_ms = [evs_s[k][0].elapsed_time(evs[k][0]) for k in range(K)]
+    sz = sizes_log.cpu().numpy()
+    n_h = sz[:, : L + 1]
+    e_h = sz[:, L + 1:]
+    alg = [algorithmic_bytes(n_h[k], e_h[k], cfg.feat_dim, L) for k in range(K)]
+    tot = torch.tensor([float(e_h.sum()), float(K)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot)
+    total_edges, total_batches = float(tot[0]), float(tot[1])
+
+    # ---------------- e2e: host buffers through the public API (rank-local)
+    e2e = run_e2e(args, pipe, cfg, stream, K, W, world, rank)
+
+    extra = None
+    if not args.no_extra and world == 1:
+        extra = knob_points(bundle, graph, cfg, args, K)
+
+    if rank == 0:
+        peak, peak_src = measured_peak_hbm()
+        achieved = float(np.mean(alg)) / (float(np.mean(agg_ms)) * 1e-3) / 1e9
+        knob = args.mode + (f"(k={args.mix})" if args.mode == "comm" else "") + f"|{p}"
+        traffic = ncu_traffic(cfg.name, knob)
+        cpu = None
+        if world == 1:
+            done, el, ed = oracle_batches(bundle, args.mode, args.mix, p, args.seed, args.cpu_seconds)
+            cpu = {"value": done / el, "unit": "batches/s", "cores": 1, "kind": "oracle",
+                   "sample": f"first {done} batches of epoch 0 of the same workload/knobs "
+                             f"({el:.1f} s, single-threaded plain-C oracle, a1 included)"}
+        value = total_batches / (ms_max * 1e-3)
+        line = {
+            "metric": METRIC, "value": value, "unit": "batches/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args, cfg, bundle, p),
+            "sampled_edges_per_s": total_edges / (ms_max * 1e-3),
+            "feature_gbps": achieved,
+            "unique_input_rows_per_batch": float(n_h[:, L].mean()),
+            "unique_feature_bytes_per_batch": float(n_h[:, L].mean() * 4 * cfg.feat_dim),
+            "stage_ms_per_step": {"sample_relabel": float(np.mean(samp_ms)),
+                                  "gather_aggregate": float(np.mean(agg_ms))},
+            "roofline": {"bound": "hbm", "kernel": "k_sage_mean_v4 (fused a4+a5, cmb_gather_aggregate)",
+                         "achieved": achieved, "peak": peak, "peak_source": peak_src,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": float(np.mean(alg))},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(n_launch_step * K + n_launch_order * orders_in_region),
+            "gpu_launches_detail": {"per_step": n_launch_step, "per_epoch_order": n_launch_order,
+                                    "orders_in_region": orders_in_region,
+                                    "kernels": kernel_names},
+            "clocks": clk.summary(),
+            "knob_points": extra,
+            "graph_meta": {k: (float(v) if isinstance(v, (np.floating, float)) else v)
+                           for k, v in bundle.meta.items()},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, pipe, cfg, stream, K, W, world, rank):
+    """Same metric through the public API with HOST buffers: per step the batch's roots
+    are copied host->device from pinned memory and the batch's result sizes
+    (n_0..n_L, e_0..e_{L-1}) are read back device->host and consumed by the host."""
+    import torch
+    L = len(cfg.fanouts)
+    nb = pipe.n_batches
+    dev = pipe.sampler.sizes.device
+    B = cfg.batch_size
+    order_host = torch.empty(pipe.orderer.n, dtype=torch.int32, pin_memory=True)
+    roots_dev = torch.empty(B, dtype=torch.int32, device=dev)
+    sizes_host = torch.empty(2 * L + 1, dtype=torch.int64, pin_memory=True)
+    h2d = d2h = 0
+
+    def step(t, epoch_cache):
+        nonlocal h2d, d2h
+        gb = t * world + rank
+        epoch, b = divmod(gb, nb)
+        if epoch_cache.get("epoch") != epoch:
+            pipe.start_epoch(epoch)
+            order_host.copy_(pipe.order, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            epoch_cache["epoch"] = epoch
+            d2h += order_host.numel() * 4
+        lo, hi = b * B, min((b + 1) * B, pipe.orderer.n)
+        r = roots_dev[: hi - lo]
+        r.copy_(order_host[lo:hi], non_blocking=True)
+        h2d += (hi - lo) * 4
+        view, x_in, h = pipe.step(gb, roots=r)
+        sizes_host.copy_(view.sizes, non_blocking=True)
+        d2h += sizes_host.numel() * 8
+        torch.cuda.current_stream().synchronize()
+        return int(sizes_host[L])  # the host consumes the result
+
+    cache = {}
+    for t in range(W):
+        step(t, cache)
+    h2d = d2h = 0
+    cache = {}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(K):
+        step(W + k, cache)
+    el = time.perf_counter() - t0
+    return {"value": K * world / el if world == 1 else K / el * world, "unit": "batches/s",
+            "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
+            "note": "per step: pinned H2D of the roots, sample+relabel+gather+aggregate, D2H of "
+                    "the batch sizes, host sync; the epoch's Knob-1 order is computed on the GPU "
+                    "and read back once per epoch inside the region (wall clock, rank-local)"}
+
+
+def knob_points(bundle, graph, cfg, args, K):
+    """The paper's knob effect on this workload: batches/s, unique input rows
+    and the fused kernel's achieved GB/s at a few (Knob-1, Knob-2) points."""
+    import torch
+    import paper_2504_18082_b200 as cmb
+    pts = []
+    L = len(cfg.fanouts)
+    for mode, mix, p in (("rand", 0.0, 0.5), ("comm", 0.5, 0.5), ("comm", 0.125, 1.0),
+                         ("comm", 0.0, 1.0), ("norand", 0.0, 1.0)):
+        pipe = cmb.MiniBatchPipeline(graph, torch.from_numpy(bundle.train), cfg.batch_size,
+                                     cfg.fanouts, mode=mode, mix=mix, p=p, seed=args.seed)
+        n = min(K, pipe.n_batches)
+        for t in range(3):
+            pipe.step(t)
+        s = torch.cuda.current_stream()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n + 2)]
+        sizes = torch.zeros(n, 2 * L + 1, dtype=torch.int64, device=graph.device)
+        torch.cuda.synchronize()
+        ev[0].record(s)
+        pipe.start_epoch(0)
+        for k in range(n):
+            pipe.sampler.sample(pipe.batch_roots(k), p, args.seed, k)
+            ev[2 + 2 * k].record(s)
+            pipe.sampler.gather_aggregate()
+            ev[3 + 2 * k].record(s)
+            sizes[k].copy_(pipe.sampler.sizes, non_blocking=True)
+        ev[1].record(s)
+        torch.cuda.synchronize()
+        ms = ev[0].elapsed_time(ev[1])
+        agg = [ev[2 + 2 * k].elapsed_time(ev[3 + 2 * k]) for k in range(n)]
+        sz = sizes.cpu().numpy()
+        alg = [algorithmic_bytes(sz[k, : L + 1], sz[k, L + 1:], cfg.feat_dim, L) for k in range(n)]
+        pts.append({"knob1": mode + (f"(k={mix})" if mode == "comm" else ""), "p_intra": p,
+                    "batches_per_s": n / (ms * 1e-3),
+                    "unique_input_rows": float(sz[:, L].mean()),
+                    "gather_aggregate_ms": float(np.mean(agg)),
+                    "gather_aggregate_alg_gbps": float(np.mean(alg) / (np.mean(agg) * 1e-3) / 1e9)})
+    return pts
+
+
+def main():
+    args = parse()
+    from gen import CONFIGS, generate
+    cfg = CONFIGS[args.config]
+    bundle = generate(cfg)
+    if args.impl == "reference":
+        return run_reference(args, bundle)
+    return run_cmb(args, bundle)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
