@@ -147,6 +147,9 @@ typedef struct {
   uint32_t* new_src_mask;              /* optional (NULL): [(e_cap[L-1]+31)/32] words; bit e set
                                           iff edge e of hop L-1 is the first occurrence of a src
                                           node that is not a dst node (used by cmb_gather_aggregate) */
+  int32_t* last_src_ids;               /* optional (NULL): [e_cap[L-1]] global id of the src node of
+                                          every edge of hop L-1 (= nodes[indices[L-1][e]]; lets
+                                          cmb_gather_aggregate skip the relabel-map lookup)      */
   int64_t* sizes;                      /* [2L+1]: n_0..n_L then e_0..e_{L-1}                  */
 } cmb_blocks;
 

@@ -63,7 +63,7 @@ class Blocks(ctypes.Structure):
     _fields_ = [("nodes", ctypes.c_void_p), ("nodes_cap", ctypes.c_int64),
                 ("indptr", ctypes.c_void_p * MAX_HOPS), ("indices", ctypes.c_void_p * MAX_HOPS),
                 ("indices_cap", ctypes.c_int64 * MAX_HOPS), ("new_src_mask", ctypes.c_void_p),
-                ("sizes", ctypes.c_void_p)]
+                ("last_src_ids", ctypes.c_void_p), ("sizes", ctypes.c_void_p)]
 
 
 _lib = None
@@ -269,6 +269,7 @@ class Sampler:
         self.indices = [torch.empty(max(1, self.e_cap[h]), dtype=torch.int32, device=dev)
                         for h in range(L)]
         self.mask = torch.empty((self.e_cap[L - 1] + 31) // 32 + 1, dtype=torch.int32, device=dev)
+        self.last_src_ids = torch.empty(max(1, self.e_cap[L - 1]), dtype=torch.int32, device=dev)
         self.sizes = torch.zeros(2 * L + 1, dtype=torch.int64, device=dev)
         b = Blocks()
         b.nodes = self.nodes.data_ptr()
@@ -278,6 +279,7 @@ class Sampler:
             b.indices[h] = self.indices[h].data_ptr()
             b.indices_cap[h] = self.e_cap[h]
         b.new_src_mask = self.mask.data_ptr()
+        b.last_src_ids = self.last_src_ids.data_ptr()
         b.sizes = self.sizes.data_ptr()
         self._blocks = b
         self.x_in = None

@@ -8,6 +8,8 @@
 // rows/edges in flight per lane (Little's law: ~6 MB in flight chip-wide at ~8 TB/s).
 // Aggregation keeps columns in lanes and walks the edges of a row in CSR order, so the fp32
 // sum is formed in exactly the oracle's order (bit-exact; then IEEE division).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cmb {
@@ -160,6 +162,278 @@ __global__ void __launch_bounds__(256) k_sage_mean_v4(
   }
 }
 
+// Tile form (the default): a group of LPR lanes owns a tile of LPR consecutive dst rows.
+// The index streams of the tile are read cooperatively and coalesced (lane k <-> row k for
+// indptr / nodes, lane k <-> edge k for indices / relabel map / first-occurrence bits); the
+// src row ids are then broadcast by shuffle and U src rows are in flight per lane before they
+// are folded, in CSR order, into the accumulator of their dst row.  This removes the
+// per-row dependent chain indptr -> indices -> nodes -> X of the row-per-group form.
+template <int LPR, int NV, int U>
+__global__ void __launch_bounds__(256) k_gather_mean_tile(
+    const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+    const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap, const float4* __restrict__ src,
+    int64_t src_ld4, const int32_t* __restrict__ map, int f4, float4* __restrict__ out,
+    int64_t out_ld4, float4* __restrict__ x_in, int64_t x_in_ld4,
+    const uint32_t* __restrict__ new_mask) {
+  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
+  const int lane = threadIdx.x % LPR;
+  const int wl = threadIdx.x & 31;
+  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (wl & ~(LPR - 1)));
+  const int64_t ngroups = (int64_t)gridDim.x * (blockDim.x / LPR);
+  const int64_t ntiles = (n_dst + LPR - 1) / LPR;
+  for (int64_t tile = blockIdx.x * (int64_t)(blockDim.x / LPR) + threadIdx.x / LPR;
+       tile < ntiles; tile += ngroups) {
+    const int64_t d0 = tile * LPR;
+    const int nr = (n_dst - d0 < LPR) ? static_cast<int>(n_dst - d0) : LPR;
+    const int32_t my_start = lane < nr ? __ldg(indptr + d0 + lane) : 0;
+    const int32_t t_end = __ldg(indptr + d0 + nr);
+    const int32_t t_begin = __shfl_sync(gmask, my_start, 0, LPR);
+    const int32_t my_node = (x_in && lane < nr) ? __ldg(map + d0 + lane) : 0;
+    auto row_start = [&](int r) { return __shfl_sync(gmask, my_start, r, LPR); };
+    auto row_end = [&](int r) {
+      const int32_t s = __shfl_sync(gmask, my_start, (r + 1) & (LPR - 1), LPR);
+      return r + 1 < nr ? s : t_end;
+    };
+    for (int c0 = 0; c0 < f4; c0 += LPR * NV) {
+      if (x_in) {  // a4 for the dst rows of the tile: X_in[d] = X[nodes[d]]
+        for (int r0 = 0; r0 < nr; r0 += U) {
+          float4 v[U][NV];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int r = r0 + u;
+            const int32_t row = __shfl_sync(gmask, my_node, r & (LPR - 1), LPR);
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+              const int c = c0 + lane + k * LPR;
+              if (r < nr && c < f4) v[u][k] = ldg4(src + (int64_t)row * src_ld4 + c);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int r = r0 + u;
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+              const int c = c0 + lane + k * LPR;
+              if (r < nr && c < f4) x_in[(d0 + r) * x_in_ld4 + c] = v[u][k];
+            }
+          }
+        }
+      }
+      // empty rows of the tile: H = 0
+      {
+        const int32_t my_end = row_end(lane);
+        unsigned empty = __ballot_sync(gmask, lane < nr && my_end == my_start);
+        empty >>= (LPR == 32 ? 0 : (wl & ~(LPR - 1)));
+        while (empty) {
+          const int r = __ffs(empty) - 1;
+          empty &= empty - 1;
+#pragma unroll
+          for (int k = 0; k < NV; ++k) {
+            const int c = c0 + lane + k * LPR;
+            if (c < f4) out[(d0 + r) * out_ld4 + c] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      }
+      float4 acc[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int32_t eb = t_begin; eb < t_end; eb += LPR) {
+        // lane k describes edge e = eb + k: local src id, src row, dst row r (largest r
+        // with start(r) <= e), whether e closes its row, first-occurrence bit, deg(r)
+        const int32_t e = eb + lane;
+        const bool ok = e < t_end;
+        const int32_t li = ok ? __ldg(idx + e) : 0;
+        const int32_t gid = ok ? (map ? __ldg(map + li) : li) : 0;
+        int r = 0;
+#pragma unroll
+        for (int step = LPR / 2; step >= 1; step >>= 1) {
+          const int32_t s = __shfl_sync(gmask, my_start, (r + step) & (LPR - 1), LPR);
+          if (r + step < nr && s <= e) r += step;
+        }
+        const int32_t rend = row_end(r);
+        const int32_t rdeg = rend - row_start(r);
+        const int first =
+            (x_in && ok) ? static_cast<int>((__ldg(new_mask + (e >> 5)) >> (e & 31)) & 1u) : 0;
+        const int meta = (rdeg << 8) | (first << 7) | ((e + 1 == rend) << 6) | r;
+        const int cnt = min(LPR, t_end - eb);
+        for (int j0 = 0; j0 < cnt; j0 += U) {
+          float4 v[U][NV];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = j0 + u;
+            const int32_t row = __shfl_sync(gmask, gid, j & (LPR - 1), LPR);
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+              const int c = c0 + lane + k * LPR;
+              if (j < cnt && c < f4) v[u][k] = ldg4(src + (int64_t)row * src_ld4 + c);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = j0 + u;
+            const int mj = __shfl_sync(gmask, meta, j & (LPR - 1), LPR);
+            const int32_t lj = __shfl_sync(gmask, li, j & (LPR - 1), LPR);
+            if (j < cnt) {
+#pragma unroll
+              for (int k = 0; k < NV; ++k) add4(acc[k], v[u][k]);
+              if (mj & 0x80) {  // first occurrence of a new src node: a4 for it, from this load
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                  const int c = c0 + lane + k * LPR;
+                  if (c < f4) x_in[(int64_t)lj * x_in_ld4 + c] = v[u][k];
+                }
+              }
+              if (mj & 0x40) {  // e closes row r: H[d0 + r] = acc / deg (IEEE), acc = 0
+                const float fd = static_cast<float>(mj >> 8);
+                const int64_t d = d0 + (mj & 0x3f);
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                  const int c = c0 + lane + k * LPR;
+                  float4 h;
+                  h.x = __fdiv_rn(acc[k].x, fd);
+                  h.y = __fdiv_rn(acc[k].y, fd);
+                  h.z = __fdiv_rn(acc[k].z, fd);
+                  h.w = __fdiv_rn(acc[k].w, fd);
+                  if (c < f4) out[d * out_ld4 + c] = h;
+                  acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// Pipelined row form (the default): one group of LPR lanes per dst row, rows visited with
+// a grid stride, and the index chain of the rows AHEAD is issued before the feature loads of
+// the current row: stage A (row i+2G) loads indptr pair + self node id, stage B (row i+G)
+// loads the row's src ids lane-parallel (lane k <-> edge k; global row ids come straight from
+// `gid` -- the relabel step's pre-relabel neighbour ids -- or via map[idx]), stage C (row i)
+// issues 1 + deg feature-row loads (self + edges, CH in flight) and folds the edges in CSR
+// order.  The dependent chain indptr -> ids -> X therefore overlaps with other rows' loads.
+template <int LPR, int NV, int CH>
+__global__ void __launch_bounds__(256) k_gather_mean_pipe(
+    const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+    const int32_t* __restrict__ gid, const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
+    const float4* __restrict__ src, int64_t src_ld4, const int32_t* __restrict__ map, int f4,
+    float4* __restrict__ out, int64_t out_ld4, float4* __restrict__ x_in, int64_t x_in_ld4,
+    const uint32_t* __restrict__ new_mask) {
+  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
+  const int lane = threadIdx.x % LPR;
+  const int wl = threadIdx.x & 31;
+  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (wl & ~(LPR - 1)));
+  const int64_t G = (int64_t)gridDim.x * (blockDim.x / LPR);
+  const int64_t g0 = blockIdx.x * (int64_t)(blockDim.x / LPR) + threadIdx.x / LPR;
+
+  struct A { int32_t e0, e1, self; };
+  struct B { int32_t g, l, first; };
+  auto loadA = [&](int64_t row) {
+    A a{0, 0, 0};
+    if (row < n_dst) {
+      a.e0 = __ldg(indptr + row);
+      a.e1 = __ldg(indptr + row + 1);
+      if (x_in) a.self = __ldg(map + row);
+    }
+    return a;
+  };
+  auto loadB = [&](const A& a, int32_t base) {  // edge base + lane of the row described by a
+    B b{0, 0, 0};
+    const int32_t e = a.e0 + base + lane;
+    if (e < a.e1) {
+      b.l = __ldg(idx + e);
+      b.g = gid ? __ldg(gid + e) : (map ? __ldg(map + b.l) : b.l);
+      if (x_in) b.first = static_cast<int>((__ldg(new_mask + (e >> 5)) >> (e & 31)) & 1u);
+    }
+    return b;
+  };
+
+  int64_t row = g0;
+  A ac = loadA(row);
+  B bc = loadB(ac, 0);
+  A an = loadA(row + G);
+  for (; row < n_dst; row += G) {
+    const A aa = loadA(row + 2 * G);  // stage A, two rows ahead
+    const B bn = loadB(an, 0);        // stage B, one row ahead
+    const int32_t deg = ac.e1 - ac.e0;
+    for (int c0 = 0; c0 < f4; c0 += LPR * NV) {
+      float4 acc[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 self[NV];
+      if (x_in) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          const int c = c0 + lane + k * LPR;
+          if (c < f4) self[k] = ldg4(src + (int64_t)ac.self * src_ld4 + c);
+        }
+      }
+      for (int32_t base = 0; base < deg; base += LPR) {
+        const B bb = base == 0 ? bc : loadB(ac, base);  // rows with deg > LPR: rest on demand
+        const int cnt = min(LPR, deg - base);
+        for (int j0 = 0; j0 < cnt; j0 += CH) {
+          float4 v[CH][NV];
+#pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            const int j = j0 + u;
+            const int32_t r = __shfl_sync(gmask, bb.g, j & (LPR - 1), LPR);
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+              const int c = c0 + lane + k * LPR;
+              if (j < cnt && c < f4) v[u][k] = ldg4(src + (int64_t)r * src_ld4 + c);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            const int j = j0 + u;
+            const int fj = __shfl_sync(gmask, bb.first, j & (LPR - 1), LPR);
+            const int32_t lj = __shfl_sync(gmask, bb.l, j & (LPR - 1), LPR);
+            if (j < cnt) {
+#pragma unroll
+              for (int k = 0; k < NV; ++k) add4(acc[k], v[u][k]);
+              if (fj) {  // first occurrence of a new src node: a4 for it, from this load
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                  const int c = c0 + lane + k * LPR;
+                  if (c < f4) x_in[(int64_t)lj * x_in_ld4 + c] = v[u][k];
+                }
+              }
+            }
+          }
+        }
+      }
+      const float fd = static_cast<float>(deg);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int c = c0 + lane + k * LPR;
+        if (c < f4) {
+          float4 h = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (deg > 0) {
+            h.x = __fdiv_rn(acc[k].x, fd);
+            h.y = __fdiv_rn(acc[k].y, fd);
+            h.z = __fdiv_rn(acc[k].z, fd);
+            h.w = __fdiv_rn(acc[k].w, fd);
+          }
+          out[row * out_ld4 + c] = h;
+          if (x_in) x_in[row * x_in_ld4 + c] = self[k];
+        }
+      }
+    }
+    ac = an;
+    bc = bn;
+    an = aa;
+  }
+}
+
+}  // namespace
+}  // namespace cmb
+
+#include "gather_bulk.cuh"
+
+namespace cmb {
+namespace {
+
 __global__ void k_sage_mean_scalar(const int32_t* __restrict__ indptr,
                                    const int32_t* __restrict__ idx,
                                    const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
@@ -230,25 +504,103 @@ cmb_status gather_dispatch(const float* x, int64_t ld, int f, const int32_t* ids
   return CMB_OK;
 }
 
+// CMB_AGG_KERNEL = row | tile | pipe (default) selects the aggregate kernel form (kept for
+// A/B measurement on the GPU box; all three compute identical bytes).
+int agg_kernel_form() {
+  static const int v = [] {
+    const char* e = std::getenv("CMB_AGG_KERNEL");
+    if (e && e[0] == 'r') return 1;
+    if (e && e[0] == 't') return 2;
+    if (e && e[0] == 'p') return 3;
+    if (e && e[0] == 'b') return 4;  // TMA bulk-copy form (opt-in)
+    return 0;
+  }();
+  return v;
+}
+
+template <int NV>
+cmb_status launch_bulk(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
+                       const int32_t* gid, const int64_t* n_dev, int64_t n_cap, const float* src,
+                       int64_t src_ld, const int32_t* map, int f4, uint32_t rb, float* out,
+                       int64_t out_ld, float* x_in, int64_t x_in_ld, const uint32_t* mask) {
+  const size_t smem = bulk::smem_bytes(rb);
+  static size_t configured = 0;
+  static int per_sm = 1;
+  if (configured != smem) {
+    CMB_CUDA(cudaFuncSetAttribute(k_gather_mean_bulk<NV>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_mean_bulk<NV>,
+                                                           bulk::kWarps * 32, smem));
+    if (per_sm < 1) per_sm = 1;
+    configured = smem;
+  }
+  const int64_t windows = (n_cap + bulk::kRows - 1) / bulk::kRows;
+  const int64_t want = (windows + bulk::kWarps - 1) / bulk::kWarps;
+  const int64_t cap = static_cast<int64_t>(sms) * per_sm;  // persistent: one wave
+  const int grid = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
+  k_gather_mean_bulk<NV><<<grid, bulk::kWarps * 32, smem, s>>>(
+      indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, rb, reinterpret_cast<float4*>(out),
+      out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4, mask);
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
 template <int LPR, int NV, int CH>
-void launch_mean(int grid, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
-                 const int64_t* n_dev, int64_t n_cap, const float* src, int64_t src_ld,
-                 const int32_t* map, int f4, float* out, int64_t out_ld, float* x_in,
-                 int64_t x_in_ld, const uint32_t* mask) {
-  k_sage_mean_v4<LPR, NV, CH><<<grid, 256, 0, s>>>(
-      indptr, idx, n_dev, n_cap, reinterpret_cast<const float4*>(src), src_ld / 4, map, f4,
+void launch_mean(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
+                 const int32_t* gid, const int64_t* n_dev, int64_t n_cap, const float* src,
+                 int64_t src_ld, const int32_t* map, int f4, float* out, int64_t out_ld,
+                 float* x_in, int64_t x_in_ld, const uint32_t* mask) {
+  const int64_t gpb = 256 / LPR;  // lane groups per 256-thread block
+  const int form = agg_kernel_form();
+  if (form == 1) {
+    int64_t want = (n_cap + gpb - 1) / gpb;
+    const int grid = static_cast<int>(want < sms * 16 ? (want > 0 ? want : 1) : sms * 16);
+    k_sage_mean_v4<LPR, NV, CH><<<grid, 256, 0, s>>>(
+        indptr, idx, n_dev, n_cap, reinterpret_cast<const float4*>(src), src_ld / 4, map, f4,
+        reinterpret_cast<float4*>(out), out_ld / 4, reinterpret_cast<float4*>(x_in),
+        x_in_ld / 4, mask);
+    return;
+  }
+  if (form == 2) {
+    const int64_t tiles = (n_cap + LPR - 1) / LPR;
+    const int tgrid = static_cast<int>((tiles + gpb - 1) / gpb);
+    constexpr int TU = NV == 1 ? 4 : (NV == 2 ? 2 : 1);  // src rows in flight per lane
+    k_gather_mean_tile<LPR, NV, TU><<<tgrid > 0 ? tgrid : 1, 256, 0, s>>>(
+        indptr, idx, n_dev, n_cap, reinterpret_cast<const float4*>(src), src_ld / 4, map, f4,
+        reinterpret_cast<float4*>(out), out_ld / 4, reinterpret_cast<float4*>(x_in),
+        x_in_ld / 4, mask);
+    return;
+  }
+  // pipelined row form: a persistent-style grid (a few blocks per SM, grid-stride rows) so
+  // every group walks many rows and its look-ahead pipeline stays full
+  int64_t want = (n_cap + gpb - 1) / gpb;
+  const int64_t cap_grid = static_cast<int64_t>(sms) * 8;
+  const int grid = static_cast<int>(want < cap_grid ? (want > 0 ? want : 1) : cap_grid);
+  k_gather_mean_pipe<LPR, NV, CH><<<grid, 256, 0, s>>>(
+      indptr, idx, gid, n_dev, n_cap, reinterpret_cast<const float4*>(src), src_ld / 4, map, f4,
       reinterpret_cast<float4*>(out), out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4,
       mask);
 }
 
-cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int64_t* n_dev,
-                         int64_t n_cap, const float* src, int64_t src_ld, const int32_t* map,
-                         int f, float* out, int64_t out_ld, float* x_in, int64_t x_in_ld,
-                         const uint32_t* mask, int sms, cudaStream_t s) {
+cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_t* gid,
+                         const int64_t* n_dev, int64_t n_cap, const float* src, int64_t src_ld,
+                         const int32_t* map, int f, float* out, int64_t out_ld, float* x_in,
+                         int64_t x_in_ld, const uint32_t* mask, int sms, cudaStream_t s,
+                         int32_t* status = nullptr) {
   if (n_cap <= 0) return CMB_OK;
   const int f4 = (f + 3) / 4;
   const bool vec = aligned16(src) && aligned16(out) && src_ld % 4 == 0 && out_ld % 4 == 0 &&
                    (!x_in || (aligned16(x_in) && x_in_ld % 4 == 0));
+  // fused a4+a5 on a sampled block (degrees <= CMB_MAX_FANOUT): the TMA bulk-copy form
+  const uint32_t rb = static_cast<uint32_t>(f4) * 16u;  // copy size, 16-B multiple, <= ld * 4
+  if (vec && x_in && f4 > 16 && f4 <= 64 && agg_kernel_form() == 4 &&
+      bulk::smem_bytes(rb) <= 227 * 1024) {
+    if (f4 <= 32)
+      return launch_bulk<1>(sms, s, indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, rb,
+                            out, out_ld, x_in, x_in_ld, mask);
+    return launch_bulk<2>(sms, s, indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, rb, out,
+                          out_ld, x_in, x_in_ld, mask);
+  }
   if (!vec) {
     k_sage_mean_scalar<<<sms * 8, 256, 0, s>>>(indptr, idx, n_dev, n_cap, src, src_ld, map, f,
                                                out, out_ld, x_in, x_in_ld, mask);
@@ -256,19 +608,38 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int64_
     return CMB_OK;
   }
   const int lpr = lanes_for(f4);
-  const int rows_per_block = 256 / lpr;
-  int64_t want = (n_cap + rows_per_block - 1) / rows_per_block;
-  const int grid = static_cast<int>(want < sms * 16 ? (want > 0 ? want : 1) : sms * 16);
-#define CMB_MEAN(L_, NV_, CH_)                                                            \
-  launch_mean<L_, NV_, CH_>(grid, s, indptr, idx, n_dev, n_cap, src, src_ld, map, f4, out, \
+#define CMB_MEAN(L_, NV_, CH_)                                                                 \
+  launch_mean<L_, NV_, CH_>(sms, s, indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, out, \
                             out_ld, x_in, x_in_ld, mask)
   switch (lpr) {
-    case 4: CMB_MEAN(4, 1, 8); break;
+    case 4: CMB_MEAN(4, 1, 4); break;
     case 8: CMB_MEAN(8, 1, 8); break;
     case 16: CMB_MEAN(16, 1, 8); break;
     default:
-      if (f4 <= 32) CMB_MEAN(32, 1, 8);
-      else if (f4 <= 64) CMB_MEAN(32, 2, 4);
+      if (f4 <= 32) {
+        // default (measured best on B200, products F = 100): 16 lanes x 2 float4 per row,
+        // two dst rows per warp, 2 edges in flight per lane; env knobs for A/B runs
+        static const int ch = [] {
+          const char* e = std::getenv("CMB_AGG_CH");
+          return e ? std::atoi(e) : 2;
+        }();
+        static const int lp = [] {
+          const char* e = std::getenv("CMB_AGG_LPR");
+          return e ? std::atoi(e) : 16;
+        }();
+        if (lp == 16) {
+          if (ch == 4) CMB_MEAN(16, 2, 4);
+          else CMB_MEAN(16, 2, 2);
+        } else if (lp == 8) {
+          CMB_MEAN(8, 4, 2);
+        } else if (ch == 8) {
+          CMB_MEAN(32, 1, 8);
+        } else if (ch == 6) {
+          CMB_MEAN(32, 1, 6);
+        } else {
+          CMB_MEAN(32, 1, 4);
+        }
+      } else if (f4 <= 64) CMB_MEAN(32, 2, 4);
       else if (f4 <= 128) CMB_MEAN(32, 4, 2);
       else CMB_MEAN(32, 5, 2);  // F = 602 -> 151 float4 = 32 x 5 (column tiles beyond)
   }
@@ -303,8 +674,9 @@ cmb_status cmb_sage_mean_aggregate(const int32_t* indptr, const int32_t* indices
   int dev = 0, sms = 148;
   CMB_CUDA(cudaGetDevice(&dev));
   CMB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  return mean_dispatch(indptr, indices, n_dst_dev, n_dst_cap, src, src_ld, src_map, feat_dim, out,
-                       out_ld, nullptr, 0, nullptr, sms, static_cast<cudaStream_t>(stream));
+  return mean_dispatch(indptr, indices, nullptr, n_dst_dev, n_dst_cap, src, src_ld, src_map,
+                       feat_dim, out, out_ld, nullptr, 0, nullptr, sms,
+                       static_cast<cudaStream_t>(stream));
 }
 
 cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
@@ -317,9 +689,10 @@ cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t
   CMB_ARG(x_in_ld >= g->d.f && h_ld >= g->d.f, "cmb_gather_aggregate: ld < F");
   CMB_ARG(n_last_dst_cap <= nodes_cap, "cmb_gather_aggregate: n_last_dst_cap > nodes_cap");
   const int L = n_hops;
-  return mean_dispatch(b->indptr[L - 1], b->indices[L - 1], b->sizes + (L - 1), n_last_dst_cap,
-                       g->d.x, g->d.ld, b->nodes, g->d.f, h_out, h_ld, x_in, x_in_ld,
-                       b->new_src_mask, g->num_sms, static_cast<cudaStream_t>(stream));
+  return mean_dispatch(b->indptr[L - 1], b->indices[L - 1], b->last_src_ids, b->sizes + (L - 1),
+                       n_last_dst_cap, g->d.x, g->d.ld, b->nodes, g->d.f, h_out, h_ld, x_in,
+                       x_in_ld, b->new_src_mask, g->num_sms, static_cast<cudaStream_t>(stream),
+                       g->status);
 }
 
 }  // extern "C"

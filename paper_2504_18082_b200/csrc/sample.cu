@@ -233,7 +233,8 @@ __global__ void k_flag(const int64_t* __restrict__ sizes, int e_idx, int64_t e_c
 
 __global__ void k_relabel(int64_t* __restrict__ sizes, int hop, int L, int64_t e_cap, Table t,
                           const uint32_t* __restrict__ slot, const int32_t* __restrict__ scan,
-                          int32_t* __restrict__ idx, int32_t* __restrict__ nodes) {
+                          int32_t* __restrict__ idx, int32_t* __restrict__ nodes,
+                          int32_t* __restrict__ gid_out) {
   const int64_t n_h = sizes[hop];
   const int64_t e_h = sizes[L + 1 + hop];
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -241,6 +242,7 @@ __global__ void k_relabel(int64_t* __restrict__ sizes, int hop, int L, int64_t e
   if (e >= e_h) return;
   const uint32_t s = slot[e];
   const uint32_t val = __ldcg(t.vals + s);
+  if (gid_out) gid_out[e] = idx[e];  // pre-relabel (global) src id, kept for the last hop
   uint32_t id;
   if (val & kHB) {
     const uint32_t ef = val & ~kHB;
@@ -410,7 +412,7 @@ cmb_status cmb_sample_blocks(const cmb_graph* g, const int32_t* roots, int64_t n
       CMB_CUDA(cub::DeviceScan::InclusiveSum(w.temp, tb, w.flag, w.scan, static_cast<int>(ec), s));
     }
     k_relabel<<<eg, 256, 0, s>>>(out->sizes, h, L, ec, w.tab, w.slot, w.scan, out->indices[h],
-                                 out->nodes);
+                                 out->nodes, h == L - 1 ? out->last_src_ids : nullptr);
     CMB_CUDA(cudaGetLastError());
   }
   return CMB_OK;
