@@ -366,3 +366,54 @@ class MiniBatchPipeline:
         view = self.sampler.sample(roots, self.p, self.seed, int(global_batch))
         x_in, h = self.sampler.gather_aggregate()
         return view, x_in, h
+
+
+class OverlappedPipeline(MiniBatchPipeline):
+    """The same step with `depth` batches in flight: the sampler of batch k+1 (latency-bound,
+    stream `s_sample`) runs while the fused gather + aggregate of batch k (HBM-bound, stream
+    `s_gather`) streams features.  Outputs are `depth`-buffered; events order the reuse."""
+
+    def __init__(self, graph: Graph, train, batch_size: int, fanouts: Sequence[int],
+                 mode="rand", mix=0.0, p=0.5, seed=42, depth: int = 2):
+        super().__init__(graph, train, batch_size, fanouts, mode, mix, p, seed)
+        self.depth = int(depth)
+        self.samplers = [self.sampler] + [Sampler(graph, self.batch_size, fanouts)
+                                          for _ in range(self.depth - 1)]
+        self.s_sample = torch.cuda.Stream(device=graph.device)
+        self.s_gather = torch.cuda.Stream(device=graph.device)
+        self.ev_sampled = [torch.cuda.Event() for _ in range(self.depth)]
+        self.ev_gathered = [torch.cuda.Event() for _ in range(self.depth)]
+        self.gather_events = None  # optional list collecting (start, end) events per gather
+
+    def step(self, global_batch: int, roots: Optional[torch.Tensor] = None):
+        """Enqueue batch `global_batch`; returns its Sampler (outputs valid once
+        `ev_gathered[j]` completes, j = global_batch % depth).  Never blocks the host."""
+        gb = int(global_batch)
+        j = gb % self.depth
+        s = self.samplers[j]
+        epoch, b = divmod(gb, self.n_batches)
+        with torch.cuda.stream(self.s_sample):
+            self.s_sample.wait_event(self.ev_gathered[j])  # buffer j consumed by batch gb-depth
+            if roots is None:
+                if self.epoch != epoch:
+                    self.start_epoch(epoch)
+                roots = self.batch_roots(b)
+            s.sample(roots, self.p, self.seed, gb)
+            self.ev_sampled[j].record(self.s_sample)
+        with torch.cuda.stream(self.s_gather):
+            self.s_gather.wait_event(self.ev_sampled[j])
+            if self.gather_events is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(self.s_gather)
+            s.gather_aggregate()
+            if self.gather_events is not None:
+                e1.record(self.s_gather)
+                self.gather_events.append((e0, e1))
+            self.ev_gathered[j].record(self.s_gather)
+        return s
+
+    def join(self, stream=None):
+        """Make `stream` (default: current) wait for all enqueued work."""
+        st = stream if stream is not None else torch.cuda.current_stream()
+        st.wait_stream(self.s_sample)
+        st.wait_stream(self.s_gather)

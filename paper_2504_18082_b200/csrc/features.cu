@@ -574,7 +574,13 @@ void launch_mean(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* 
   // pipelined row form: a persistent-style grid (a few blocks per SM, grid-stride rows) so
   // every group walks many rows and its look-ahead pipeline stays full
   int64_t want = (n_cap + gpb - 1) / gpb;
-  const int64_t cap_grid = static_cast<int64_t>(sms) * 8;
+  // CMB_AGG_BLOCKS_PER_SM caps the grid so the kernel can share the SMs with a concurrently
+  // running sampler of the next batch (overlapped pipeline)
+  static const int bps = [] {
+    const char* e = std::getenv("CMB_AGG_BLOCKS_PER_SM");
+    return e ? std::atoi(e) : 8;
+  }();
+  const int64_t cap_grid = static_cast<int64_t>(sms) * (bps > 0 ? bps : 8);
   const int grid = static_cast<int>(want < cap_grid ? (want > 0 ? want : 1) : cap_grid);
   k_gather_mean_pipe<LPR, NV, CH><<<grid, 256, 0, s>>>(
       indptr, idx, gid, n_dev, n_cap, reinterpret_cast<const float4*>(src), src_ld / 4, map, f4,

@@ -1,0 +1,40 @@
+// sample_dev.cuh -- per-row helpers of a2 (biased fanout sampling).
+//
+// PAPER.md S4.2 P:683-691, S5 P:717: intra-community edges get unnormalised weight p,
+// inter-community edges 1-p, and DGL's NeighborSampler draws `fanout` neighbours per node
+// WITHOUT replacement (reading R1).  With two weight classes that law factorises exactly:
+// the class sequence of successive draws is an urn (P(intra) = wi*ri / (wi*ri + wo*ro)),
+// and given K intra picks the intra (inter) subset is uniform -> Floyd's subset sampler.
+// So a row costs O(f) Philox draws whatever its degree.
+#pragma once
+
+#include "common.cuh"
+
+namespace cmb {
+namespace smp {
+
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+
+// A row split into its intra-community segment [lo, hi) and the rest (a0 bounds), with the
+// eligible sizes under the Knob-2 weights (a zero-weight class is ineligible, reading R3).
+struct RowInfo {
+  int64_t rs, deg, ni_e, no_e;
+  uint32_t lo, hi;
+};
+
+__device__ __forceinline__ RowInfo row_info(const DevGraph& g, int32_t v, uint32_t wi,
+                                            uint32_t wo) {
+  RowInfo r;
+  r.rs = __ldg(g.indptr + v);
+  r.deg = __ldg(g.indptr + v + 1) - r.rs;
+  const uint2 b = __ldg(g.bounds + v);
+  r.lo = b.x;
+  r.hi = b.y;
+  const int64_t ni = static_cast<int64_t>(b.y) - b.x;
+  r.ni_e = wi ? ni : 0;
+  r.no_e = wo ? r.deg - ni : 0;
+  return r;
+}
+
+}  // namespace smp
+}  // namespace cmb

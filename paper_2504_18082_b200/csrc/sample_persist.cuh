@@ -1,0 +1,563 @@
+// sample_persist.cuh -- the persistent cooperative schedule of a2 + a3 (included by sample.cu).
+//
+// One launch per batch, one block per SM (cooperative launch: all blocks co-resident), grid
+// barriers between the phases of a hop.  Dedup uses a DIRECT map over node ids (uint64[N] in
+// the workspace; L2-resident for N up to ~15M) instead of a hash table.  An entry is
+// (batch tag << 32) | value, the tag being a per-workspace batch counter, so entries written
+// by earlier batches read as empty and the map is never cleared:
+//     value = kFinal | id          node u has local id `id` (dst nodes, relabelled nodes)
+//           = kMarkerTop - e       e = smallest edge position seen so far for new node u
+// "First occurrence" is then ONE fire-and-forget 64-bit atomicMax per warp-deduplicated edge:
+// a newer tag beats a stale entry, final ids beat markers, smaller e beats larger e.
+//
+// Phases of hop h:
+//  A  [relabel(h-1)] + count + prefix + positions + picks
+//     block b owns dst rows [b*R, (b+1)*R): row info cached in shared memory; counts; block scan;
+//     single-pass cross-block prefix (publish own total, add the totals of blocks < b);
+//     positions: the urn + Floyd draws of each row (one thread per row for f <= 16, G-lane
+//     groups otherwise) write the absolute CSR index of each pick; picks: one thread per pick
+//     loads indices[pos] (all random loads of the hop independent).
+//  B  mark: warp-deduplicated atomicMax(map[u], tag | kMarkerTop - e)
+//  C  flag + prefix + assign: first occurrences (map[u] == tag | kMarkerTop - e) get
+//     id = n_h + global flag scan - 1: map[u] := tag | kFinal | id, nodes[id] := u
+// then (after the barrier) relabel(h): indices[e] := id(map[u]), fused into hop h+1's A.
+#pragma once
+
+namespace cmb {
+namespace pst {
+
+using namespace smp;
+
+constexpr int kMaxBlocks = 4096;
+constexpr int kRowCap = 3072;  // dst rows per block cached in shared memory
+constexpr int kTiles = 8;      // edge tiles per block whose flags are loaded before scanning
+constexpr uint32_t kFinal = 0x80000000u;
+constexpr uint32_t kMarkerTop = 0x7FFFFFFFu;
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct PArgs {
+  DevGraph g;
+  const int32_t* roots;
+  int64_t n_roots;
+  int L;
+  int fan[CMB_MAX_HOPS];
+  uint32_t wi, wo, k0, k1, batch;
+  int32_t* nodes;
+  int32_t* indptr[CMB_MAX_HOPS];
+  int32_t* indices[CMB_MAX_HOPS];
+  uint32_t* mask;
+  int32_t* last_src;
+  int64_t* sizes;
+  unsigned long long* map;  // [N] tagged direct dedup map (see above)
+  unsigned* tag_ctr;        // [1] last batch tag used with this workspace
+  uint32_t* scan;           // [max e_cap] flag << 31 | block-local inclusive flag scan
+  int64_t* pick;            // [max e_cap] absolute CSR index of each pick
+  unsigned long long* pub;  // [2][kMaxBlocks] tagged block aggregates
+  unsigned* bar;            // [0] arrivals, [1] generation
+  uint64_t* prof;           // [kMaxBlocks][64] per-block %globaltimer at sub-step boundaries
+  int32_t* status;
+};
+
+// Per-block sub-step timeline (profiling aid, one store per sub-step per block):
+// thread 0 of every block records %globaltimer into prof[block][k], k counting the calls.
+#define CMB_PROF(a, k)                                                               \
+  do {                                                                               \
+    if (threadIdx.x == 0 && (k) < 64)                                                \
+      (a).prof[(size_t)blockIdx.x * 64 + (k)] = globaltimer();                       \
+    ++(k);                                                                           \
+  } while (0)
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Generation-counting grid barrier (all blocks co-resident).
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned arrived = atomicAdd(bar, 1u);
+    if (arrived == gridDim.x - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (ld_acquire(bar + 1) == gen) {
+      }
+    }
+    gen += 1u;
+  }
+  __syncthreads();
+}
+
+struct RowCache {
+  int64_t rs[kRowCap];
+  uint32_t deg[kRowCap];
+  uint32_t lo[kRowCap];
+  uint32_t hi[kRowCap];
+  int32_t v[kRowCap];
+  int32_t off[kRowCap];
+};
+
+template <int PB>
+struct Smem {
+  union {
+    typename cub::BlockScan<int32_t, PB>::TempStorage scan;
+    typename cub::BlockReduce<int32_t, PB>::TempStorage reduce;
+  } cub;
+  int32_t bc;
+  RowCache rows;
+};
+
+// Block b publishes its aggregate (tagged) and adds the aggregates of blocks [0, b) as they
+// appear.  Every block publishes before it waits -> the wait always ends.  Only the numbers
+// are exchanged, so relaxed accesses suffice.
+template <int PB>
+__device__ __forceinline__ int32_t publish_and_prefix(unsigned long long* pub, unsigned tag,
+                                                      int32_t agg, Smem<PB>& sm) {
+  if (threadIdx.x == 0)
+    st_relaxed64(pub + blockIdx.x, (static_cast<unsigned long long>(tag) << 32) |
+                                       static_cast<uint32_t>(agg));
+  int32_t s = 0;
+  for (int j = threadIdx.x; j < (int)blockIdx.x; j += PB) {
+    unsigned long long v;
+    while (((v = ld_relaxed64(pub + j)) >> 32) != tag) {
+    }
+    s += static_cast<int32_t>(v & 0xffffffffu);
+  }
+  const int32_t tot = cub::BlockReduce<int32_t, PB>(sm.cub.reduce).Sum(s);
+  if (threadIdx.x == 0) sm.bc = tot;
+  __syncthreads();
+  const int32_t r = sm.bc;
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ void range_of(int64_t n, int64_t align, int64_t& lo, int64_t& hi) {
+  int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  per = (per + align - 1) / align * align;
+  lo = (int64_t)blockIdx.x * per;
+  if (lo > n) lo = n;
+  hi = lo + per;
+  if (hi > n) hi = n;
+}
+
+// relabel of hop h (all entries final): indices[e] := local id of its node
+template <int PB>
+__device__ void phase_relabel(const PArgs& a, int h) {
+  const int64_t e_h = __ldcg(a.sizes + a.L + 1 + h);
+  int32_t* gid = (h == a.L - 1) ? a.last_src : nullptr;
+  int32_t* ind = a.indices[h];
+  const int64_t stride = (int64_t)gridDim.x * PB;
+  for (int64_t e0 = blockIdx.x * (int64_t)PB + threadIdx.x; e0 < e_h; e0 += 4 * stride) {
+    int32_t u[4];
+    unsigned long long v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) u[k] = e0 + k * stride < e_h ? __ldcg(ind + e0 + k * stride) : 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = e0 + k * stride < e_h ? __ldcg(a.map + u[k]) : 0ull;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t e = e0 + k * stride;
+      if (e < e_h) {
+        if (gid) gid[e] = u[k];
+        ind[e] = static_cast<int32_t>(static_cast<uint32_t>(v[k]) & ~kFinal);
+      }
+    }
+  }
+}
+
+// ---- positions of the picks of one row, written as absolute CSR indices rs + position
+
+// take-all (reading R4): every eligible position, ascending; returns true if taken
+__device__ __forceinline__ bool take_all(int64_t rs, int64_t deg, uint32_t lo, uint32_t hi,
+                                         int64_t ni_e, int64_t no_e, int f, int lane, int G,
+                                         int64_t* __restrict__ o) {
+  if (f < ni_e + no_e) return false;
+  if (ni_e && no_e) {
+    for (int64_t q = lane; q < deg; q += G) o[q] = rs + q;
+  } else if (ni_e) {
+    for (int64_t q = lane; q < ni_e; q += G) o[q] = rs + lo + q;
+  } else {
+    for (int64_t q = lane; q < no_e; q += G) o[q] = rs + (q < lo ? q : hi + (q - lo));
+  }
+  return true;
+}
+
+// G lanes per row (f <= G): lane s owns Philox slot s
+template <int G>
+__device__ __forceinline__ void row_positions_group(int32_t v, int64_t rs, int64_t deg,
+                                                    uint32_t lo, uint32_t hi, int hop, int f,
+                                                    uint32_t wi, uint32_t wo, uint32_t k0,
+                                                    uint32_t k1, uint32_t batch, int lane,
+                                                    unsigned gmask, int64_t* __restrict__ o) {
+  const int64_t ni = static_cast<int64_t>(hi) - lo;
+  const int64_t ni_e = wi ? ni : 0, no_e = wo ? deg - ni : 0;
+  if (take_all(rs, deg, lo, hi, ni_e, no_e, f, lane, G, o)) return;
+  PhiloxOut w{0u, 0u, 0u, 0u};
+  if (lane < f)
+    w = philox4x32_10(static_cast<uint32_t>(lane), static_cast<uint32_t>(v),
+                      (kTagSample << 24) | static_cast<uint32_t>(hop), batch, k0, k1);
+  const uint64_t u01 = lo64(w), u23 = hi64(w);
+  uint64_t ri = static_cast<uint64_t>(ni_e), ro = static_cast<uint64_t>(no_e);
+  int K = 0;
+  for (int s = 0; s < f; ++s) {
+    const uint64_t x = __shfl_sync(gmask, u01, s, G);
+    const uint64_t wri = wi * ri;
+    if (__umul64hi(x, wri + wo * ro) < wri) {
+      ++K;
+      --ri;
+    } else {
+      --ro;
+    }
+  }
+  const bool in = lane < K;
+  const uint64_t n_cls = in ? static_cast<uint64_t>(ni_e) : static_cast<uint64_t>(no_e);
+  const int k_cls = in ? K : f - K;
+  const int t = in ? lane : lane - K;
+  const uint32_t j = static_cast<uint32_t>(n_cls - static_cast<uint64_t>(k_cls) + t);
+  const uint32_t rr = static_cast<uint32_t>(__umul64hi(u23, static_cast<uint64_t>(j) + 1u));
+  uint32_t sel = kEmpty;
+  for (int s = 0; s < f; ++s) {
+    const uint32_t rs_ = __shfl_sync(gmask, rr, s, G);
+    const bool same_cls = (lane < K) == (s < K);
+    const unsigned hit = __ballot_sync(gmask, lane < s && same_cls && sel == rs_);
+    if (lane == s) sel = hit ? j : rr;
+  }
+  uint32_t pos = in ? lo + sel : (sel < lo ? sel : hi + (sel - lo));
+  if (lane >= f) pos = kEmpty;
+  int rank = 0;
+  for (int s = 0; s < f; ++s) rank += __shfl_sync(gmask, pos, s, G) < pos;
+  if (lane < f) o[rank] = rs + pos;
+}
+
+// one thread per row (f <= FM): the same draws with every loop statically unrolled over FM
+// slots (register arrays, predicated on s < f) -- no shuffles, 32 rows per warp.
+template <int FM>
+__device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int64_t deg,
+                                                     uint32_t lo, uint32_t hi, int hop, int f,
+                                                     uint32_t wi, uint32_t wo, uint32_t k0,
+                                                     uint32_t k1, uint32_t batch,
+                                                     int64_t* __restrict__ o) {
+  const int64_t ni = static_cast<int64_t>(hi) - lo;
+  const int64_t ni_e = wi ? ni : 0, no_e = wo ? deg - ni : 0;
+  if (take_all(rs, deg, lo, hi, ni_e, no_e, f, 0, 1, o)) return;
+  uint64_t r23[FM];
+  uint64_t ri = static_cast<uint64_t>(ni_e), ro = static_cast<uint64_t>(no_e);
+  int K = 0;
+  const uint32_t c2 = (kTagSample << 24) | static_cast<uint32_t>(hop);
+#pragma unroll
+  for (int s = 0; s < FM; ++s) {  // urn over f successive draws; keep r23 of each slot
+    r23[s] = 0;
+    if (s < f) {
+      const PhiloxOut w = philox4x32_10(static_cast<uint32_t>(s), static_cast<uint32_t>(v), c2,
+                                        batch, k0, k1);
+      r23[s] = hi64(w);
+      const uint64_t wri = wi * ri;
+      if (__umul64hi(lo64(w), wri + wo * ro) < wri) {
+        ++K;
+        --ri;
+      } else {
+        --ro;
+      }
+    }
+  }
+  uint32_t pos[FM];
+  const int kb = f - K;
+#pragma unroll
+  for (int s = 0; s < FM; ++s) {  // Floyd: slots [0,K) intra subset, [K,f) inter subset
+    pos[s] = kEmpty;
+    if (s < f) {
+      const bool in = s < K;
+      const uint64_t n_cls = in ? static_cast<uint64_t>(ni_e) : static_cast<uint64_t>(no_e);
+      const int k_cls = in ? K : kb;
+      const int t = in ? s : s - K;
+      const uint32_t j = static_cast<uint32_t>(n_cls - static_cast<uint64_t>(k_cls) + t);
+      const uint32_t r = static_cast<uint32_t>(__umul64hi(r23[s], static_cast<uint64_t>(j) + 1u));
+      bool hit = false;
+#pragma unroll
+      for (int q = 0; q < s; ++q) hit |= ((q < K) == in) && pos[q] == r;
+      pos[s] = hit ? j : r;
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < FM; ++s) {  // class offsets -> row positions
+    if (s < f) {
+      const uint32_t q = pos[s];
+      pos[s] = s < K ? lo + q : (q < lo ? q : hi + (q - lo));
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < FM; ++s) {  // ascending emit by rank
+    if (s < f) {
+      int rank = 0;
+#pragma unroll
+      for (int q = 0; q < FM; ++q) rank += (q < f) && pos[q] < pos[s];
+      o[rank] = rs + pos[s];
+    }
+  }
+}
+
+template <int PB, int G>
+__device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk) {
+  const int64_t n_h = h == 0 ? a.n_roots : __ldcg(a.sizes + h);
+  const int32_t* dst = h == 0 ? a.roots : a.nodes;
+  const int f = a.fan[h];
+  int64_t lo, hi;
+  range_of(n_h, 1, lo, hi);
+  RowCache& rc = sm.rows;
+  // (1) counts, block scan, cached row info
+  int32_t run = 0;
+  for (int64_t t0 = lo; t0 < hi; t0 += PB) {
+    const int64_t i = t0 + threadIdx.x;
+    int32_t c = 0;
+    RowInfo r{};
+    int32_t v = 0;
+    if (i < hi) {
+      v = __ldcg(dst + i);
+      r = row_info(a.g, v, a.wi, a.wo);
+      const int64_t m = r.ni_e + r.no_e;
+      c = static_cast<int32_t>(m < f ? m : f);
+    }
+    int32_t ex, agg;
+    cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(c, ex, agg);
+    __syncthreads();
+    if (i < hi) {
+      const int64_t k = i - lo;
+      a.indptr[h][i] = run + ex;
+      if (k < kRowCap) {
+        rc.rs[k] = r.rs;
+        rc.deg[k] = static_cast<uint32_t>(r.deg);
+        rc.lo[k] = r.lo;
+        rc.hi[k] = r.hi;
+        rc.v[k] = v;
+        rc.off[k] = run + ex;
+      }
+    }
+    run += agg;
+  }
+  CMB_PROF(a, pk);
+  const int32_t base = publish_and_prefix<PB>(a.pub, static_cast<unsigned>(h + 1), run, sm);
+  CMB_PROF(a, pk);
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    a.indptr[h][n_h] = base + run;
+    a.sizes[a.L + 1 + h] = base + run;
+  }
+  // (2) positions
+  auto fetch = [&](int64_t i, int32_t& v, int64_t& rs, int64_t& deg, uint32_t& rlo,
+                   uint32_t& rhi, int32_t& off) {
+    const int64_t k = i - lo;
+    if (k < kRowCap) {
+      v = rc.v[k];
+      rs = rc.rs[k];
+      deg = rc.deg[k];
+      rlo = rc.lo[k];
+      rhi = rc.hi[k];
+      off = rc.off[k];
+    } else {
+      v = __ldcg(dst + i);
+      const RowInfo r = row_info(a.g, v, a.wi, a.wo);
+      rs = r.rs;
+      deg = r.deg;
+      rlo = r.lo;
+      rhi = r.hi;
+      off = __ldcg(a.indptr[h] + i);
+    }
+  };
+  // thread per row when the block has many rows (every thread busy); G-lane groups when the
+  // rows are few (small hops: spread each row's f draws over lanes instead)
+  if (f <= 16 && (hi - lo) * G > PB) {
+    for (int64_t i = lo + threadIdx.x; i < hi; i += PB) {
+      int32_t v, off;
+      int64_t rs, deg;
+      uint32_t rlo, rhi;
+      fetch(i, v, rs, deg, rlo, rhi, off);
+      a.indptr[h][i] = base + off;
+      if (f <= 8)
+        row_positions_thread<8>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch,
+                                a.pick + base + off);
+      else
+        row_positions_thread<16>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch,
+                                 a.pick + base + off);
+    }
+  } else {
+    const int lane = threadIdx.x & (G - 1);
+    const int wl = threadIdx.x & 31;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (wl & ~(G - 1)));
+    for (int64_t i = lo + threadIdx.x / G; i < hi; i += PB / G) {
+      int32_t v, off;
+      int64_t rs, deg;
+      uint32_t rlo, rhi;
+      fetch(i, v, rs, deg, rlo, rhi, off);
+      if (lane == 0) a.indptr[h][i] = base + off;
+      row_positions_group<G>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, lane,
+                             gmask, a.pick + base + off);
+    }
+  }
+  __syncthreads();
+  CMB_PROF(a, pk);
+  // (3) picks: the block's edges are the contiguous range [base, base + run)
+  const int32_t* __restrict__ ind = a.g.indices;
+  int32_t* __restrict__ out = a.indices[h];
+  const int64_t e1 = (int64_t)base + run;
+  constexpr int U = 8;
+  for (int64_t e0 = base + threadIdx.x; e0 < e1; e0 += U * PB) {
+    int64_t p[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * PB;
+      p[u] = e < e1 ? __ldcg(a.pick + e) : 0;
+    }
+    int32_t val[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) val[u] = (e0 + u * PB < e1) ? __ldg(ind + p[u]) : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * PB < e1) out[e0 + u * PB] = val[u];
+  }
+}
+
+// mark: first occurrence of every new node = atomicMax(map[u], tag | kMarkerTop - e)
+template <int PB>
+__device__ void phase_mark(const PArgs& a, int h, unsigned long long tag) {
+  const int64_t e_h = __ldcg(a.sizes + a.L + 1 + h);
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (PB / 32);
+  const int32_t* nbr = a.indices[h];
+  constexpr int U = 4;
+  for (int64_t c0 = (int64_t)blockIdx.x * (PB / 32) + (threadIdx.x >> 5); c0 * 32 < e_h;
+       c0 += U * nw) {
+    uint32_t u[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = (c0 + k * nw) * 32 + lane;
+      u[k] = e < e_h ? static_cast<uint32_t>(__ldcg(nbr + e)) : kEmpty - lane;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = (c0 + k * nw) * 32 + lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, u[k]);
+      if (e < e_h && lane == __ffs(peers) - 1)  // lowest lane = smallest e of the duplicates
+        atomicMax(a.map + u[k], tag | (kMarkerTop - static_cast<uint32_t>(e)));
+    }
+  }
+}
+
+// flags + prefix + assign
+template <int PB>
+__device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
+                                  unsigned long long tag) {
+  const int64_t n_h = h == 0 ? a.n_roots : __ldcg(a.sizes + h);
+  const int64_t e_h = __ldcg(a.sizes + a.L + 1 + h);
+  int64_t lo, hi;
+  range_of(e_h, 32, lo, hi);
+  uint32_t* mask = (h == a.L - 1) ? a.mask : nullptr;
+  const int32_t* nbr = a.indices[h];
+  int32_t run = 0;
+  for (int64_t c0 = lo; c0 < hi; c0 += (int64_t)kTiles * PB) {
+    bool fl[kTiles];
+#pragma unroll
+    for (int k = 0; k < kTiles; ++k) {  // all loads of up to kTiles tiles in flight
+      const int64_t e = c0 + k * PB + threadIdx.x;
+      fl[k] = e < hi && __ldcg(a.map + __ldcg(nbr + e)) ==
+                            (tag | (kMarkerTop - static_cast<uint32_t>(e)));
+    }
+#pragma unroll
+    for (int k = 0; k < kTiles; ++k) {
+      const int64_t t0 = c0 + k * PB;
+      if (t0 >= hi) break;
+      const int64_t e = t0 + threadIdx.x;
+      int32_t inc, agg;
+      cub::BlockScan<int32_t, PB>(sm.cub.scan).InclusiveSum(fl[k] ? 1 : 0, inc, agg);
+      __syncthreads();
+      if (e < hi) a.scan[e] = (fl[k] ? 0x80000000u : 0u) | static_cast<uint32_t>(run + inc);
+      if (mask) {
+        const unsigned word = __ballot_sync(0xffffffffu, fl[k]);
+        if ((threadIdx.x & 31) == 0 && e < hi) mask[e >> 5] = word;
+      }
+      run += agg;
+    }
+  }
+  CMB_PROF(a, pk);
+  const int32_t base =
+      publish_and_prefix<PB>(a.pub + kMaxBlocks, static_cast<unsigned>(h + 1), run, sm);
+  CMB_PROF(a, pk);
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) a.sizes[h + 1] = n_h + base + run;
+  for (int64_t e = lo + threadIdx.x; e < hi; e += PB) {
+    const uint32_t sc = __ldcg(a.scan + e);
+    if (sc & 0x80000000u) {
+      const uint32_t id = static_cast<uint32_t>(n_h + base + (sc & 0x7fffffffu) - 1);
+      const int32_t u = __ldcg(nbr + e);
+      a.nodes[id] = u;
+      a.map[u] = tag | kFinal | id;
+    }
+  }
+}
+
+template <int PB>
+__global__ void __launch_bounds__(PB, 1024 / PB) k_sample_persistent(PArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem<PB>& sm = *reinterpret_cast<Smem<PB>*>(smem_raw);
+  __shared__ unsigned gen_s, tag_s;
+  if (threadIdx.x == 0) {
+    gen_s = ld_acquire(a.bar + 1);
+    tag_s = __ldcg(a.tag_ctr) + 1u;  // this batch's map tag (published by block 0 below)
+  }
+  __syncthreads();
+  unsigned gen = gen_s;
+  const unsigned long long tag = static_cast<unsigned long long>(tag_s) << 32;
+  int pk = 0;
+  CMB_PROF(a, pk);
+  for (int64_t i = blockIdx.x * (int64_t)PB + threadIdx.x; i < a.n_roots;
+       i += (int64_t)gridDim.x * PB) {
+    const uint32_t u = static_cast<uint32_t>(a.roots[i]);
+    a.nodes[i] = static_cast<int32_t>(u);
+    const unsigned long long old = atomicExch(a.map + u, tag | kFinal | static_cast<uint32_t>(i));
+    if ((old & 0xffffffff00000000ull) == tag) raise_status(a.status, CMB_ERR_INVALID_INPUT);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.sizes[0] = a.n_roots;
+  for (int h = 0; h < a.L; ++h) {
+    if (h > 0) phase_relabel<PB>(a, h - 1);
+    CMB_PROF(a, pk);                                  // +0 relabel(h-1)
+    const int f = a.fan[h];
+    if (f <= 16) phase_count_sample<PB, 16>(a, h, sm, pk);
+    else phase_count_sample<PB, 32>(a, h, sm, pk);   // +1 count, +2 prefix, +3 positions
+    CMB_PROF(a, pk);                                  // +4 picks
+    grid_barrier(a.bar, gen);
+    CMB_PROF(a, pk);                                  // +5 barrier (roots in map, picks written)
+    if (h == 0 && blockIdx.x == 0 && threadIdx.x == 0) *a.tag_ctr = tag_s;  // all have read it
+    phase_mark<PB>(a, h, tag);
+    CMB_PROF(a, pk);                                  // +6 mark
+    grid_barrier(a.bar, gen);
+    CMB_PROF(a, pk);                                  // +7 barrier
+    phase_flag_assign<PB>(a, h, sm, pk, tag);         // +8 flag scan, +9 prefix
+    CMB_PROF(a, pk);                                  // +10 assign
+    grid_barrier(a.bar, gen);
+    CMB_PROF(a, pk);                                  // +11 barrier
+  }
+  phase_relabel<PB>(a, a.L - 1);
+  CMB_PROF(a, pk);
+}
+
+template <int PB>
+constexpr size_t smem_bytes() {
+  return sizeof(Smem<PB>);
+}
+
+}  // namespace pst
+}  // namespace cmb

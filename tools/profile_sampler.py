@@ -1,0 +1,58 @@
+"""Sub-step timeline of the persistent sampler kernel.
+
+Every block's thread 0 writes %globaltimer at fixed sub-step boundaries into the workspace
+(sample_persist.cuh CMB_PROF).  For each sub-step this prints the critical-path increment
+dT = max_b t_b[k] - max_b t_b[k-1] and the mean / max per-block duration (microseconds),
+averaged over a few batches of the chosen workload (env CFG, P, MODE, MIX)."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2504_18082_b200 as cmb  # noqa: E402
+from gen import CONFIGS, generate  # noqa: E402
+
+PROF_OFFSET = 66048          # carve order: header 256, barrier 256, pub 2*4096*8 (sample.cu)
+SUB = ["relabel(h-1)", "count", "prefix", "positions", "picks", "barrierA", "mark",
+       "barrierB", "flag_scan", "prefix2", "assign", "barrierC"]
+
+
+def main():
+    cfg = CONFIGS[os.environ.get("CFG", "products")]
+    p = float(os.environ.get("P", cfg.p_intra))
+    b = generate(cfg)
+    g = cmb.Graph.from_bundle(b)
+    pipe = cmb.MiniBatchPipeline(g, torch.from_numpy(b.train), cfg.batch_size, cfg.fanouts,
+                                 mode=os.environ.get("MODE", "rand"),
+                                 mix=float(os.environ.get("MIX", "0")), p=p)
+    L = len(cfg.fanouts)
+    npts = 2 + 12 * L
+    nblk = torch.cuda.get_device_properties(0).multi_processor_count
+    labels = [f"h{h}.{s}" for h in range(L) for s in SUB] + ["relabel(L-1)"]
+    crit, mean, mx = [], [], []
+    pipe.start_epoch(0)
+    for t in range(25):
+        pipe.sampler.sample(pipe.batch_roots(t), p, 42, t)
+        torch.cuda.synchronize()
+        ws = pipe.sampler.workspace
+        raw = ws[PROF_OFFSET: PROF_OFFSET + nblk * 64 * 8].view(torch.int64).cpu().numpy()
+        tb = raw.reshape(nblk, 64)[:, :npts].astype(np.float64)
+        if t >= 5:
+            T = tb.max(axis=0)
+            crit.append(np.diff(T) / 1e3)
+            d = np.diff(tb, axis=1) / 1e3
+            mean.append(d.mean(axis=0))
+            mx.append(d.max(axis=0))
+    crit, mean, mx = (np.mean(x, axis=0) for x in (crit, mean, mx))
+    rows = {lab: [round(float(c), 2), round(float(m), 2), round(float(x), 2)]
+            for lab, c, m, x in zip(labels, crit, mean, mx)}
+    print(json.dumps({"unit": "us [critical dT, mean block, max block]", "total_us":
+                      round(float(crit.sum()), 1), "steps": rows,
+                      "sizes": pipe.sampler.sizes.cpu().tolist()}))
+
+
+if __name__ == "__main__":
+    main()
