@@ -225,6 +225,7 @@ def run_cmb(args, bundle):
     import torch
     import torch.distributed as dist
     import paper_2504_18082_b200 as cmb
+    from paper_2504_18082_b200 import dist as cmb_dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -244,8 +245,8 @@ def run_cmb(args, bundle):
     K, W = args.steps, args.warmup
     sizes_log = torch.zeros(K, 2 * L + 1, dtype=torch.int64, device=dev)
 
-    def gbatch(t):  # global batch id of this rank's t-th step
-        return t * world + rank
+    def gbatch(t):  # global batch id of this rank's t-th step (round-robin, reading R22)
+        return cmb_dist.global_batch(rank, world, t)
 
     def one_step(t, ev=None, ev_s=None):
         gb = gbatch(t)
@@ -297,20 +298,14 @@ def run_cmb(args, bundle):
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
     agg_ms = [evs[k][0].elapsed_time(evs[k][1]) for k in range(K)]
     samp_ms = [evs_s[k][0].elapsed_time(evs[k][0]) for k in range(K)]
     sz = sizes_log.cpu().numpy()
     n_h = sz[:, : L + 1]
     e_h = sz[:, L + 1:]
     alg = [algorithmic_bytes(n_h[k], e_h[k], cfg.feat_dim, L) for k in range(K)]
-    tot = torch.tensor([float(e_h.sum()), float(K)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tot)
-    total_edges, total_batches = float(tot[0]), float(tot[1])
+    ms_max, (total_edges, total_batches) = cmb_dist.reduce_timing(
+        ms, [float(e_h.sum()), float(K)], device=dev)
 
     # ---------------- e2e: host buffers through the public API (rank-local)
     e2e = run_e2e(args, pipe, cfg, stream, K, W, world, rank)

@@ -270,3 +270,30 @@ def test_deterministic_repeat():
                      h[: n[2]].cpu().numpy().copy()))
     for a, c in zip(outs[0], outs[1]):
         assert a.tobytes() == c.tobytes()
+
+
+def test_overlapped_pipeline_matches_sequential():
+    """Two batches in flight on two streams (OverlappedPipeline) give the same bytes as the
+    sequential pipeline (double-buffered outputs, event-ordered reuse)."""
+    b, prep, g = _bundle("products", 0.01)
+    cfg = b.cfg
+    train = torch.from_numpy(b.train)
+    seq = cmb.MiniBatchPipeline(g, train, 512, (15, 10, 5), mode="comm", mix=0.125, p=0.9)
+    ov = cmb.OverlappedPipeline(g, train, 512, (15, 10, 5), mode="comm", mix=0.125, p=0.9)
+    ref = []
+    for t in range(6):
+        view, x_in, h = seq.step(t)
+        torch.cuda.synchronize()
+        n, e = view.host_sizes()
+        ref.append((view.nodes[: n[-1]].cpu().numpy().copy(), h[: n[2]].cpu().numpy().copy()))
+    for t in range(6):
+        s = ov.step(t)
+        j = t % ov.depth
+        ov.ev_gathered[j].synchronize()
+        n = s.sizes.cpu().tolist()
+        nodes = s.nodes[: n[3]].cpu().numpy()
+        hh = s.h[: n[2]].cpu().numpy()
+        assert nodes.tobytes() == ref[t][0].tobytes()
+        assert hh.tobytes() == ref[t][1].tobytes()
+    ov.join()
+    torch.cuda.synchronize()
