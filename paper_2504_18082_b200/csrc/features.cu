@@ -313,13 +313,46 @@ __global__ void __launch_bounds__(256) k_gather_mean_tile(
 // `gid` -- the relabel step's pre-relabel neighbour ids -- or via map[idx]), stage C (row i)
 // issues 1 + deg feature-row loads (self + edges, CH in flight) and folds the edges in CSR
 // order.  The dependent chain indptr -> ids -> X therefore overlaps with other rows' loads.
+// L2 cache-policy hints (createpolicy): feature rows are loaded evict_last (a row referenced
+// by several dst rows of the batch should survive until its next use -- the paper's L2 reuse),
+// outputs (X_in, H) are stored evict_first (written once, never re-read by this kernel).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ldg4_hint(const float4* p, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st4_hint(float4* p, const float4& v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+
 template <int LPR, int NV, int CH>
-__global__ void __launch_bounds__(256) k_gather_mean_pipe(
+__global__ void __launch_bounds__(256, (LPR == 16 && NV == 2 && CH == 2) ? 4 : 1)
+    k_gather_mean_pipe(
     const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ gid, const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
     const float4* __restrict__ src, int64_t src_ld4, const int32_t* __restrict__ map, int f4,
     float4* __restrict__ out, int64_t out_ld4, float4* __restrict__ x_in, int64_t x_in_ld4,
-    const uint32_t* __restrict__ new_mask) {
+    const uint32_t* __restrict__ new_mask, int hint) {
+  const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+  auto LD = [&](const float4* p) { return hint ? ldg4_hint(p, pol_keep) : ldg4(p); };
+  auto ST = [&](float4* p, const float4& v) {
+    if (hint) st4_hint(p, v, pol_stream);
+    else *p = v;
+  };
   const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
   const int lane = threadIdx.x % LPR;
   const int wl = threadIdx.x & 31;
@@ -366,7 +399,7 @@ __global__ void __launch_bounds__(256) k_gather_mean_pipe(
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
           const int c = c0 + lane + k * LPR;
-          if (c < f4) self[k] = ldg4(src + (int64_t)ac.self * src_ld4 + c);
+          if (c < f4) self[k] = LD(src + (int64_t)ac.self * src_ld4 + c);
         }
       }
       for (int32_t base = 0; base < deg; base += LPR) {
@@ -381,7 +414,7 @@ __global__ void __launch_bounds__(256) k_gather_mean_pipe(
 #pragma unroll
             for (int k = 0; k < NV; ++k) {
               const int c = c0 + lane + k * LPR;
-              if (j < cnt && c < f4) v[u][k] = ldg4(src + (int64_t)r * src_ld4 + c);
+              if (j < cnt && c < f4) v[u][k] = LD(src + (int64_t)r * src_ld4 + c);
             }
           }
 #pragma unroll
@@ -396,7 +429,7 @@ __global__ void __launch_bounds__(256) k_gather_mean_pipe(
 #pragma unroll
                 for (int k = 0; k < NV; ++k) {
                   const int c = c0 + lane + k * LPR;
-                  if (c < f4) x_in[(int64_t)lj * x_in_ld4 + c] = v[u][k];
+                  if (c < f4) ST(x_in + (int64_t)lj * x_in_ld4 + c, v[u][k]);
                 }
               }
             }
@@ -415,8 +448,8 @@ __global__ void __launch_bounds__(256) k_gather_mean_pipe(
             h.z = __fdiv_rn(acc[k].z, fd);
             h.w = __fdiv_rn(acc[k].w, fd);
           }
-          out[row * out_ld4 + c] = h;
-          if (x_in) x_in[row * x_in_ld4 + c] = self[k];
+          ST(out + row * out_ld4 + c, h);
+          if (x_in) ST(x_in + row * x_in_ld4 + c, self[k]);
         }
       }
     }
@@ -582,10 +615,14 @@ void launch_mean(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* 
   }();
   const int64_t cap_grid = static_cast<int64_t>(sms) * (bps > 0 ? bps : 8);
   const int grid = static_cast<int>(want < cap_grid ? (want > 0 ? want : 1) : cap_grid);
+  static const int hint = [] {  // CMB_AGG_HINT=0 disables the L2 cache-policy hints
+    const char* e = std::getenv("CMB_AGG_HINT");
+    return e ? std::atoi(e) : 1;
+  }();
   k_gather_mean_pipe<LPR, NV, CH><<<grid, 256, 0, s>>>(
       indptr, idx, gid, n_dev, n_cap, reinterpret_cast<const float4*>(src), src_ld / 4, map, f4,
       reinterpret_cast<float4*>(out), out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4,
-      mask);
+      mask, hint);
 }
 
 cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_t* gid,
