@@ -314,7 +314,8 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
 }
 
 template <int PB, int G>
-__device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk) {
+__device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
+                                   unsigned long long tag) {
   const int64_t n_h = h == 0 ? a.n_roots : __ldcg(a.sizes + h);
   const int32_t* dst = h == 0 ? a.roots : a.nodes;
   const int f = a.fan[h];
@@ -411,49 +412,36 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk)
   }
   __syncthreads();
   CMB_PROF(a, pk);
-  // (3) picks: the block's edges are the contiguous range [base, base + run)
+  // (3) picks + mark: the block's edges are the contiguous range [base, base + run); each
+  // picked neighbour u is written out and its first occurrence marked right away:
+  // warp-deduplicated atomicMax(map[u], tag | kMarkerTop - e) (fire-and-forget reductions).
+  // Final entries (roots, earlier hops) always beat markers, so no ordering is needed with
+  // the root insertion of hop 0 or across blocks.
   const int32_t* __restrict__ ind = a.g.indices;
   int32_t* __restrict__ out = a.indices[h];
   const int64_t e1 = (int64_t)base + run;
+  const int lane = threadIdx.x & 31;
   constexpr int U = 8;
-  for (int64_t e0 = base + threadIdx.x; e0 < e1; e0 += U * PB) {
+  for (int64_t w0 = base + (threadIdx.x & ~31); w0 < e1; w0 += U * PB) {  // warp-uniform
     int64_t p[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t e = e0 + u * PB;
+      const int64_t e = w0 + lane + u * PB;
       p[u] = e < e1 ? __ldcg(a.pick + e) : 0;
     }
-    int32_t val[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) val[u] = (e0 + u * PB < e1) ? __ldg(ind + p[u]) : 0;
+    uint32_t val[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (e0 + u * PB < e1) out[e0 + u * PB] = val[u];
-  }
-}
-
-// mark: first occurrence of every new node = atomicMax(map[u], tag | kMarkerTop - e)
-template <int PB>
-__device__ void phase_mark(const PArgs& a, int h, unsigned long long tag) {
-  const int64_t e_h = __ldcg(a.sizes + a.L + 1 + h);
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (PB / 32);
-  const int32_t* nbr = a.indices[h];
-  constexpr int U = 4;
-  for (int64_t c0 = (int64_t)blockIdx.x * (PB / 32) + (threadIdx.x >> 5); c0 * 32 < e_h;
-       c0 += U * nw) {
-    uint32_t u[U];
+      val[u] = (w0 + lane + u * PB < e1) ? static_cast<uint32_t>(__ldg(ind + p[u])) : kEmpty - lane;
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t e = (c0 + k * nw) * 32 + lane;
-      u[k] = e < e_h ? static_cast<uint32_t>(__ldcg(nbr + e)) : kEmpty - lane;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t e = (c0 + k * nw) * 32 + lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, u[k]);
-      if (e < e_h && lane == __ffs(peers) - 1)  // lowest lane = smallest e of the duplicates
-        atomicMax(a.map + u[k], tag | (kMarkerTop - static_cast<uint32_t>(e)));
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = w0 + lane + u * PB;
+      const unsigned peers = __match_any_sync(0xffffffffu, val[u]);
+      if (e < e1) {
+        out[e] = static_cast<int32_t>(val[u]);
+        if (lane == __ffs(peers) - 1)  // lowest lane = smallest e of the duplicates
+          atomicMax(a.map + val[u], tag | (kMarkerTop - static_cast<uint32_t>(e)));
+      }
     }
   }
 }
@@ -528,27 +516,26 @@ __global__ void __launch_bounds__(PB, 1024 / PB) k_sample_persistent(PArgs a) {
     const uint32_t u = static_cast<uint32_t>(a.roots[i]);
     a.nodes[i] = static_cast<int32_t>(u);
     const unsigned long long old = atomicExch(a.map + u, tag | kFinal | static_cast<uint32_t>(i));
-    if ((old & 0xffffffff00000000ull) == tag) raise_status(a.status, CMB_ERR_INVALID_INPUT);
+    // duplicate root <=> the entry already holds a final id of THIS batch (a marker of this
+    // batch -- hop-0 picks run concurrently -- is not a duplicate: the final id replaces it)
+    if ((old & 0xffffffff00000000ull) == tag && (static_cast<uint32_t>(old) & kFinal))
+      raise_status(a.status, CMB_ERR_INVALID_INPUT);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) a.sizes[0] = a.n_roots;
   for (int h = 0; h < a.L; ++h) {
     if (h > 0) phase_relabel<PB>(a, h - 1);
     CMB_PROF(a, pk);                                  // +0 relabel(h-1)
     const int f = a.fan[h];
-    if (f <= 16) phase_count_sample<PB, 16>(a, h, sm, pk);
-    else phase_count_sample<PB, 32>(a, h, sm, pk);   // +1 count, +2 prefix, +3 positions
-    CMB_PROF(a, pk);                                  // +4 picks
+    if (f <= 16) phase_count_sample<PB, 16>(a, h, sm, pk, tag);
+    else phase_count_sample<PB, 32>(a, h, sm, pk, tag);  // +1 count, +2 prefix, +3 positions
+    CMB_PROF(a, pk);                                  // +4 picks + marks
     grid_barrier(a.bar, gen);
-    CMB_PROF(a, pk);                                  // +5 barrier (roots in map, picks written)
+    CMB_PROF(a, pk);                                  // +5 barrier (marks final)
     if (h == 0 && blockIdx.x == 0 && threadIdx.x == 0) *a.tag_ctr = tag_s;  // all have read it
-    phase_mark<PB>(a, h, tag);
-    CMB_PROF(a, pk);                                  // +6 mark
+    phase_flag_assign<PB>(a, h, sm, pk, tag);         // +6 flag scan, +7 prefix
+    CMB_PROF(a, pk);                                  // +8 assign
     grid_barrier(a.bar, gen);
-    CMB_PROF(a, pk);                                  // +7 barrier
-    phase_flag_assign<PB>(a, h, sm, pk, tag);         // +8 flag scan, +9 prefix
-    CMB_PROF(a, pk);                                  // +10 assign
-    grid_barrier(a.bar, gen);
-    CMB_PROF(a, pk);                                  // +11 barrier
+    CMB_PROF(a, pk);                                  // +9 barrier
   }
   phase_relabel<PB>(a, a.L - 1);
   CMB_PROF(a, pk);

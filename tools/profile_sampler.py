@@ -16,8 +16,8 @@ import paper_2504_18082_b200 as cmb  # noqa: E402
 from gen import CONFIGS, generate  # noqa: E402
 
 PROF_OFFSET = 66048          # carve order: header 256, barrier 256, pub 2*4096*8 (sample.cu)
-SUB = ["relabel(h-1)", "count", "prefix", "positions", "picks", "barrierA", "mark",
-       "barrierB", "flag_scan", "prefix2", "assign", "barrierC"]
+SUB = ["relabel(h-1)", "count", "prefix", "positions", "picks+mark", "barrierA",
+       "flag_scan", "prefix2", "assign", "barrierC"]
 
 
 def main():
@@ -29,7 +29,7 @@ def main():
                                  mode=os.environ.get("MODE", "rand"),
                                  mix=float(os.environ.get("MIX", "0")), p=p)
     L = len(cfg.fanouts)
-    npts = 2 + 12 * L
+    npts = 2 + 10 * L
     nblk = torch.cuda.get_device_properties(0).multi_processor_count
     labels = [f"h{h}.{s}" for h in range(L) for s in SUB] + ["relabel(L-1)"]
     crit, mean, mx = [], [], []
