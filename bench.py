@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--no-extra", action="store_true", help="skip the knob-sweep extra points")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--batches-per-launch", type=int, default=4,
+                    help="batches sampled per persistent-sampler launch (1..4)")
     return ap.parse_args()
 
 
@@ -238,8 +240,10 @@ def run_cmb(args, bundle):
     p = cfg.p_intra if args.p is None else args.p
     L = len(cfg.fanouts)
     graph = cmb.Graph.from_bundle(bundle, device=dev, validate=True)
-    pipe = cmb.MiniBatchPipeline(graph, torch.from_numpy(bundle.train), cfg.batch_size,
-                                 cfg.fanouts, mode=args.mode, mix=args.mix, p=p, seed=args.seed)
+    G = max(1, min(args.batches_per_launch, cmb.MAX_BATCHES_PER_LAUNCH))
+    pipe = cmb.BatchedPipeline(graph, torch.from_numpy(bundle.train), cfg.batch_size,
+                               cfg.fanouts, mode=args.mode, mix=args.mix, p=p, seed=args.seed,
+                               nb=G)
     nb = pipe.n_batches
     stream = torch.cuda.current_stream()
     K, W = args.steps, args.warmup
@@ -248,58 +252,50 @@ def run_cmb(args, bundle):
     def gbatch(t):  # global batch id of this rank's t-th step (round-robin, reading R22)
         return cmb_dist.global_batch(rank, world, t)
 
-    def one_step(t, ev=None, ev_s=None):
-        gb = gbatch(t)
-        epoch, b = divmod(gb, nb)
-        if pipe.epoch != epoch:
-            pipe.start_epoch(epoch)
-        roots = pipe.batch_roots(b)
-        if ev_s is not None:
-            ev_s[0].record(stream)
-        pipe.sampler.sample(roots, p, args.seed, gb)
-        if ev is not None:
-            ev[0].record(stream)
-        pipe.sampler.gather_aggregate()
-        if ev is not None:
-            ev[1].record(stream)
+    def group(t0, count, events=None):
+        """Steps t0 .. t0+count-1 of this rank: one sampler launch + `count` gather launches."""
+        return pipe.step_group([gbatch(t) for t in range(t0, t0 + count)], events=events)
 
     # warm-up (also compiles nothing: the library is prebuilt)
-    for t in range(W):
-        one_step(t)
+    for t in range(0, W, G):
+        group(t, min(G, W - t))
     torch.cuda.synchronize()
-    for obj in (graph, pipe.orderer, pipe.sampler):
+    for obj in [graph, pipe.orderer] + list(pipe.samplers):
         st = obj.status()
         if st != 0:
             raise RuntimeError(f"device status {st} after warm-up")
-    n_launch_step, kernel_names = count_launches(lambda: one_step(W))
+    n_launch_group, kernel_names = count_launches(lambda: group(W, G))
     n_launch_order, _ = count_launches(lambda: pipe.start_epoch(pipe.epoch))
 
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(K)]
-    evs_s = [(torch.cuda.Event(enable_timing=True),) for _ in range(K)]
+    evlog = []
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     orders_in_region = 0
+    n_groups = 0
     with ClockSampler(local) as clk:
         start.record(stream)
         pipe.start_epoch(gbatch(W) // nb)       # a1 for the current epoch, inside the region
         orders_in_region += 1
-        for k in range(K):
-            t = W + k
-            ep = gbatch(t) // nb
-            if pipe.epoch != ep:
-                orders_in_region += 1
-            one_step(t, evs[k], evs_s[k])
-            sizes_log[k].copy_(pipe.sampler.sizes, non_blocking=True)
+        for k0 in range(0, K, G):
+            cnt = min(G, K - k0)
+            ep0 = pipe.epoch
+            orders_in_region += len({gbatch(W + k) // nb for k in range(k0, k0 + cnt)} - {ep0})
+            ev = {}
+            ss = group(W + k0, cnt, ev)
+            evlog.append(ev)
+            n_groups += 1
+            for i, s in enumerate(ss):
+                sizes_log[k0 + i].copy_(s.sizes, non_blocking=True)
         end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end)
-    agg_ms = [evs[k][0].elapsed_time(evs[k][1]) for k in range(K)]
-    samp_ms = [evs_s[k][0].elapsed_time(evs[k][0]) for k in range(K)]
+    agg_ms = [g0.elapsed_time(g1) for ev in evlog for (g0, g1) in ev["gather"]]
+    samp_ms = [ev["sample"][0].elapsed_time(ev["sample"][1]) / len(ev["gather"]) for ev in evlog
+               for _ in ev["gather"]]
     sz = sizes_log.cpu().numpy()
     n_h = sz[:, : L + 1]
     e_h = sz[:, L + 1:]
@@ -337,14 +333,17 @@ def run_cmb(args, bundle):
             "unique_feature_bytes_per_batch": float(n_h[:, L].mean() * 4 * cfg.feat_dim),
             "stage_ms_per_step": {"sample_relabel": float(np.mean(samp_ms)),
                                   "gather_aggregate": float(np.mean(agg_ms))},
-            "roofline": {"bound": "hbm", "kernel": "k_sage_mean_v4 (fused a4+a5, cmb_gather_aggregate)",
+            "roofline": {"bound": "hbm",
+                         "kernel": "k_gather_mean_pipe (fused a4+a5, cmb_gather_aggregate)",
                          "achieved": achieved, "peak": peak, "peak_source": peak_src,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": float(np.mean(alg))},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": int(n_launch_step * K + n_launch_order * orders_in_region),
-            "gpu_launches_detail": {"per_step": n_launch_step, "per_epoch_order": n_launch_order,
+            "gpu_launches": int(n_launch_group * n_groups + n_launch_order * orders_in_region),
+            "gpu_launches_detail": {"per_group_of_batches": n_launch_group,
+                                    "batches_per_sampler_launch": G, "groups": n_groups,
+                                    "per_epoch_order": n_launch_order,
                                     "orders_in_region": orders_in_region,
                                     "kernels": kernel_names},
             "clocks": clk.summary(),
@@ -366,48 +365,56 @@ def run_e2e(args, pipe, cfg, stream, K, W, world, rank):
     import torch
     L = len(cfg.fanouts)
     nb = pipe.n_batches
+    G = pipe.nb
     dev = pipe.sampler.sizes.device
     B = cfg.batch_size
     order_host = torch.empty(pipe.orderer.n, dtype=torch.int32, pin_memory=True)
-    roots_dev = torch.empty(B, dtype=torch.int32, device=dev)
-    sizes_host = torch.empty(2 * L + 1, dtype=torch.int64, pin_memory=True)
+    roots_dev = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(G)]
+    sizes_host = torch.empty(G, 2 * L + 1, dtype=torch.int64, pin_memory=True)
     h2d = d2h = 0
+    epoch_cache = {}
 
-    def step(t, epoch_cache):
+    def steps(t0, count):
+        """Steps t0 .. t0+count-1 (one sampler launch): per batch a pinned H2D copy of its
+        roots, then per batch a D2H copy of its sizes, consumed by the host after one sync."""
         nonlocal h2d, d2h
-        gb = t * world + rank
-        epoch, b = divmod(gb, nb)
-        if epoch_cache.get("epoch") != epoch:
-            pipe.start_epoch(epoch)
-            order_host.copy_(pipe.order, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            epoch_cache["epoch"] = epoch
-            d2h += order_host.numel() * 4
-        lo, hi = b * B, min((b + 1) * B, pipe.orderer.n)
-        r = roots_dev[: hi - lo]
-        r.copy_(order_host[lo:hi], non_blocking=True)
-        h2d += (hi - lo) * 4
-        view, x_in, h = pipe.step(gb, roots=r)
-        sizes_host.copy_(view.sizes, non_blocking=True)
-        d2h += sizes_host.numel() * 8
+        gbs = [t * world + rank for t in range(t0, t0 + count)]
+        roots = []
+        for i, gb in enumerate(gbs):
+            epoch, b = divmod(gb, nb)
+            if epoch_cache.get("epoch") != epoch:
+                pipe.start_epoch(epoch)
+                order_host.copy_(pipe.order, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                epoch_cache["epoch"] = epoch
+                d2h += order_host.numel() * 4
+            lo, hi = b * B, min((b + 1) * B, pipe.orderer.n)
+            r = roots_dev[i][: hi - lo]
+            r.copy_(order_host[lo:hi], non_blocking=True)
+            h2d += (hi - lo) * 4
+            roots.append(r)
+        ss = pipe.step_group(gbs, roots=roots)
+        for i, s in enumerate(ss):
+            sizes_host[i].copy_(s.sizes, non_blocking=True)
+            d2h += sizes_host.shape[1] * 8
         torch.cuda.current_stream().synchronize()
-        return int(sizes_host[L])  # the host consumes the result
+        return [int(sizes_host[i, L]) for i in range(count)]  # the host consumes the results
 
-    cache = {}
-    for t in range(W):
-        step(t, cache)
+    for t in range(0, W, G):
+        steps(t, min(G, W - t))
     h2d = d2h = 0
-    cache = {}
+    epoch_cache.clear()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for k in range(K):
-        step(W + k, cache)
+    for k in range(0, K, G):
+        steps(W + k, min(G, K - k))
     el = time.perf_counter() - t0
-    return {"value": K * world / el if world == 1 else K / el * world, "unit": "batches/s",
+    return {"value": K * world / el, "unit": "batches/s",
             "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
-            "note": "per step: pinned H2D of the roots, sample+relabel+gather+aggregate, D2H of "
-                    "the batch sizes, host sync; the epoch's Knob-1 order is computed on the GPU "
-                    "and read back once per epoch inside the region (wall clock, rank-local)"}
+            "note": f"per step: pinned H2D of the batch's roots and D2H of its sizes read by the "
+                    f"host (one sync per launch group of {G} batches), sample+relabel+gather+"
+                    f"aggregate on the GPU; the epoch's Knob-1 order is computed on the GPU and "
+                    f"read back once per epoch inside the region (wall clock, rank-local x world)"}
 
 
 def knob_points(bundle, graph, cfg, args, K):
@@ -419,27 +426,28 @@ def knob_points(bundle, graph, cfg, args, K):
     L = len(cfg.fanouts)
     for mode, mix, p in (("rand", 0.0, 0.5), ("comm", 0.5, 0.5), ("comm", 0.125, 1.0),
                          ("comm", 0.0, 1.0), ("norand", 0.0, 1.0)):
-        pipe = cmb.MiniBatchPipeline(graph, torch.from_numpy(bundle.train), cfg.batch_size,
-                                     cfg.fanouts, mode=mode, mix=mix, p=p, seed=args.seed)
+        G = max(1, min(args.batches_per_launch, cmb.MAX_BATCHES_PER_LAUNCH))
+        pipe = cmb.BatchedPipeline(graph, torch.from_numpy(bundle.train), cfg.batch_size,
+                                   cfg.fanouts, mode=mode, mix=mix, p=p, seed=args.seed, nb=G)
         n = min(K, pipe.n_batches)
-        for t in range(3):
-            pipe.step(t)
+        pipe.step_group(range(G))
         s = torch.cuda.current_stream()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n + 2)]
+        e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         sizes = torch.zeros(n, 2 * L + 1, dtype=torch.int64, device=graph.device)
+        evs = []
         torch.cuda.synchronize()
-        ev[0].record(s)
+        e_start.record(s)
         pipe.start_epoch(0)
-        for k in range(n):
-            pipe.sampler.sample(pipe.batch_roots(k), p, args.seed, k)
-            ev[2 + 2 * k].record(s)
-            pipe.sampler.gather_aggregate()
-            ev[3 + 2 * k].record(s)
-            sizes[k].copy_(pipe.sampler.sizes, non_blocking=True)
-        ev[1].record(s)
+        for k0 in range(0, n, G):
+            ev = {}
+            ss = pipe.step_group(range(k0, min(n, k0 + G)), events=ev)
+            evs.append(ev)
+            for i, smp in enumerate(ss):
+                sizes[k0 + i].copy_(smp.sizes, non_blocking=True)
+        e_end.record(s)
         torch.cuda.synchronize()
-        ms = ev[0].elapsed_time(ev[1])
-        agg = [ev[2 + 2 * k].elapsed_time(ev[3 + 2 * k]) for k in range(n)]
+        ms = e_start.elapsed_time(e_end)
+        agg = [g0.elapsed_time(g1) for ev in evs for (g0, g1) in ev["gather"]]
         sz = sizes.cpu().numpy()
         alg = [algorithmic_bytes(sz[k, : L + 1], sz[k, L + 1:], cfg.feat_dim, L) for k in range(n)]
         pts.append({"knob1": mode + (f"(k={mix})" if mode == "comm" else ""), "p_intra": p,

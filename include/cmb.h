@@ -173,6 +173,25 @@ CMB_API cmb_status cmb_sample_blocks(const cmb_graph* g, const int32_t* roots, i
                              uint32_t batch_id, cmb_blocks* out, void* workspace,
                              size_t workspace_bytes, void* stream);
 
+/* Several independent batches in ONE launch (up to CMB_MAX_BATCHES_PER_LAUNCH): the SMs are
+ * split evenly between the batches, which run the same phases concurrently, so the latency-
+ * bound phases of small hops overlap across batches.  Each batch has its own roots, batch id,
+ * output blocks and workspace (workspaces must be distinct); results are identical to
+ * calling cmb_sample_blocks once per batch. */
+#define CMB_MAX_BATCHES_PER_LAUNCH 4
+typedef struct {
+  const int32_t* roots; /* device int32[n_roots], distinct */
+  int64_t n_roots;
+  uint32_t batch_id;
+  cmb_blocks* out;
+  void* workspace;
+  size_t workspace_bytes;
+} cmb_batch;
+CMB_API cmb_status cmb_sample_blocks_multi(const cmb_graph* g, const cmb_batch* batches,
+                                           int32_t n_batches, const int32_t* fanouts,
+                                           int32_t n_hops, double p_intra, uint64_t seed,
+                                           void* stream);
+
 /* ------------------------------------------------------------------ a4 / a5 */
 /* a4: out[i, 0:F] = features[node_ids[i], 0:F] for i < *n_dev (device count; rows
  * beyond it up to n_cap are untouched).  Bit-exact copy.  out_ld >= F floats. */

@@ -39,7 +39,8 @@ STATUS = {0: "CMB_OK", 1: "CMB_ERR_INVALID_ARGUMENT", 2: "CMB_ERR_INVALID_GRAPH"
 # C ABI symbols (include/cmb.h); tests check the library exports all of them.
 SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb_graph_arrays",
            "cmb_order_roots_workspace_bytes", "cmb_order_roots", "cmb_blocks_capacity",
-           "cmb_sample_workspace_bytes", "cmb_sample_blocks", "cmb_gather_features",
+           "cmb_sample_workspace_bytes", "cmb_sample_blocks", "cmb_sample_blocks_multi",
+           "cmb_gather_features",
            "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -66,6 +67,13 @@ class Blocks(ctypes.Structure):
                 ("last_src_ids", ctypes.c_void_p), ("sizes", ctypes.c_void_p)]
 
 
+class Batch(ctypes.Structure):
+    _fields_ = [("roots", ctypes.c_void_p), ("n_roots", ctypes.c_int64),
+                ("batch_id", ctypes.c_uint32), ("out", ctypes.POINTER(Blocks)),
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
+
+
+MAX_BATCHES_PER_LAUNCH = 4
 _lib = None
 
 
@@ -91,6 +99,7 @@ def lib():
             "cmb_sample_workspace_bytes": (SZ, [I64, P, I32, I64]),
             "cmb_sample_blocks": (I32, [P, P, I64, P, I32, D, U64, U32, ctypes.POINTER(Blocks), P,
                                         SZ, P]),
+            "cmb_sample_blocks_multi": (I32, [P, ctypes.POINTER(Batch), I32, P, I32, D, U64, P]),
             "cmb_gather_features": (I32, [P, P, P, I64, P, I64, P]),
             "cmb_sage_mean_aggregate": (I32, [P, P, P, I64, P, I64, P, I32, P, I64, P]),
             "cmb_gather_aggregate": (I32, [P, ctypes.POINTER(Blocks), I32, I64, I64, P, I64, P,
@@ -294,6 +303,13 @@ class Sampler:
                                        _ptr(self.workspace), self.workspace.numel(), _stream()))
         return BatchView(self.nodes, self.sizes, self.indptr, self.indices, self.mask)
 
+    def batch_desc(self, roots: torch.Tensor, batch_id: int) -> "Batch":
+        n = int(roots.shape[0])
+        if n > self.max_roots:
+            raise ValueError("more roots than max_roots")
+        return Batch(roots.data_ptr(), n, int(batch_id), ctypes.pointer(self._blocks),
+                     self.workspace.data_ptr(), self.workspace.numel())
+
     def alloc_features(self):
         g = self.graph
         if self.x_in is None:
@@ -313,6 +329,20 @@ class Sampler:
 
     def status(self):
         return lib().cmb_get_device_status(_ptr(self.workspace), _stream())
+
+
+def sample_multi(samplers: Sequence["Sampler"], roots: Sequence[torch.Tensor],
+                 batch_ids: Sequence[int], p: float, seed: int):
+    """a2+a3 for up to 4 independent batches in ONE launch (cmb_sample_blocks_multi); the
+    samplers must share graph and fanouts and own distinct workspaces."""
+    s0 = samplers[0]
+    n = len(samplers)
+    if not (1 <= n <= MAX_BATCHES_PER_LAUNCH) or len(roots) != n or len(batch_ids) != n:
+        raise ValueError("1..4 samplers, one roots tensor and batch id each")
+    arr = (Batch * n)(*[s.batch_desc(r, b) for s, r, b in zip(samplers, roots, batch_ids)])
+    _check(lib().cmb_sample_blocks_multi(s0.graph.handle, arr, n, s0._f, s0.L, float(p), int(seed),
+                                         _stream()))
+    return [BatchView(s.nodes, s.sizes, s.indptr, s.indices, s.mask) for s in samplers]
 
 
 def gather_features(graph: Graph, node_ids: torch.Tensor, n_dev: torch.Tensor, out: torch.Tensor):
@@ -366,6 +396,57 @@ class MiniBatchPipeline:
         view = self.sampler.sample(roots, self.p, self.seed, int(global_batch))
         x_in, h = self.sampler.gather_aggregate()
         return view, x_in, h
+
+
+class BatchedPipeline(MiniBatchPipeline):
+    """The same step, `nb` batches per sampler launch (cmb_sample_blocks_multi: the SMs are
+    split between the batches so the latency-bound sampling phases overlap), followed by the
+    fused gather + aggregate of each batch.  Same bytes as the sequential pipeline."""
+
+    def __init__(self, graph: Graph, train, batch_size: int, fanouts: Sequence[int],
+                 mode="rand", mix=0.0, p=0.5, seed=42, nb: int = 2):
+        super().__init__(graph, train, batch_size, fanouts, mode, mix, p, seed)
+        self.nb = int(nb)
+        self.samplers = [self.sampler] + [Sampler(graph, self.batch_size, fanouts)
+                                          for _ in range(self.nb - 1)]
+
+    def step_group(self, gbs: Sequence[int], roots: Optional[Sequence[torch.Tensor]] = None,
+                   events=None):
+        """Run the global batches `gbs` (at most nb) with one sampler launch, then the fused
+        gather + aggregate of each.  `roots` optionally overrides the epoch order.  If `events`
+        is a dict, ('sample' -> (start, end)) and ('gather' -> [(start, end), ...]) CUDA events
+        are recorded around the launches.  Returns the samplers used (one per batch)."""
+        gbs = [int(x) for x in gbs]
+        if not 1 <= len(gbs) <= self.nb:
+            raise ValueError(f"1..{self.nb} batches per group")
+        if roots is None:
+            roots = []
+            for gb in gbs:
+                epoch, b = divmod(gb, self.n_batches)
+                if self.epoch != epoch:
+                    if roots:  # epoch boundary inside the group: keep the earlier epoch's roots
+                        roots = [r.clone() for r in roots]
+                    self.start_epoch(epoch)
+                roots.append(self.batch_roots(b))
+        ss = self.samplers[: len(gbs)]
+        timing = events is not None
+        if timing:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        sample_multi(ss, roots, gbs, self.p, self.seed)
+        if timing:
+            e1.record()
+            events["sample"] = (e0, e1)
+            events["gather"] = []
+        for s in ss:
+            if timing:
+                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                g0.record()
+            s.gather_aggregate()
+            if timing:
+                g1.record()
+                events["gather"].append((g0, g1))
+        return ss
 
 
 class OverlappedPipeline(MiniBatchPipeline):

@@ -56,14 +56,9 @@ int sampler_threads() {
   return pb;
 }
 
-cmb_status run_persistent(const cmb_graph* g, const int32_t* roots, int64_t n_roots,
-                          const int32_t* fanouts, int L, uint32_t wi, uint32_t wo, uint32_t k0,
-                          uint32_t k1, uint32_t batch_id, cmb_blocks* out, SampleWs& w,
-                          cudaStream_t s) {
-  const int pb = sampler_threads();
-  int grid = g->num_sms;  // one block per SM: co-resident by construction
-  if (grid > kMaxPersistBlocks) grid = kMaxPersistBlocks;
-  pst::PArgs a;
+void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t n_roots,
+               const int32_t* fanouts, int L, uint32_t wi, uint32_t wo, uint32_t k0, uint32_t k1,
+               uint32_t batch_id, const cmb_blocks* out, const SampleWs& w) {
   a.g = g->d;
   a.roots = roots;
   a.n_roots = n_roots;
@@ -90,7 +85,14 @@ cmb_status run_persistent(const cmb_graph* g, const int32_t* roots, int64_t n_ro
   a.bar = w.bar;
   a.prof = w.prof;
   a.status = &w.hdr->status;
-  void* args[] = {&a};
+}
+
+cmb_status launch_persistent(const cmb_graph* g, pst::PMulti& m, cudaStream_t s) {
+  const int pb = sampler_threads();
+  int grid = g->num_sms;  // one block per SM: co-resident by construction
+  if (grid > kMaxPersistBlocks) grid = kMaxPersistBlocks;
+  grid -= grid % m.nb;    // equal virtual grids per batch
+  void* args[] = {&m};
   const void* fn;
   size_t smem;
   if (pb == 512) {
@@ -105,43 +107,17 @@ cmb_status run_persistent(const cmb_graph* g, const int32_t* roots, int64_t n_ro
     CMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured[pb == 512] = true;
   }
-  // barrier state + tagged aggregates (contiguous) are cleared for every batch
-  CMB_CUDA(cudaMemsetAsync(w.bar, 0,
-                           reinterpret_cast<char*>(w.pub + 2 * kMaxPersistBlocks) -
-                               reinterpret_cast<char*>(w.bar),
-                           s));
   CMB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(pb), args, smem, s));
   return CMB_OK;
 }
 
-}  // namespace
-}  // namespace cmb
-
-using namespace cmb;
-
-extern "C" {
-
-size_t cmb_sample_workspace_bytes(int64_t n_roots, const int32_t* fanouts, int32_t n_hops,
-                                  int64_t num_nodes) {
-  if (!fanouts || n_hops < 1 || n_hops > CMB_MAX_HOPS) return 0;
-  size_t b = 0;
-  carve_sample_ws(nullptr, n_roots, fanouts, n_hops, num_nodes, &b);
-  return b;
-}
-
-cmb_status cmb_sample_blocks(const cmb_graph* g, const int32_t* roots, int64_t n_roots,
-                             const int32_t* fanouts, int32_t n_hops, double p_intra, uint64_t seed,
-                             uint32_t batch_id, cmb_blocks* out, void* workspace,
-                             size_t workspace_bytes, void* stream) {
-  CMB_ARG(g && roots && fanouts && out, "cmb_sample_blocks: null graph/roots/fanouts/out");
-  CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_sample_blocks: n_hops %d outside [1,%d]",
-          n_hops, CMB_MAX_HOPS);
+// host-checkable validation of one batch (capacities, workspace)
+cmb_status check_batch(const cmb_graph* g, const int32_t* roots, int64_t n_roots,
+                       const int32_t* fanouts, int n_hops, const cmb_blocks* out,
+                       const void* workspace, size_t workspace_bytes) {
+  CMB_ARG(roots && out, "cmb_sample_blocks: null roots/out");
   CMB_ARG(n_roots >= 1 && n_roots <= g->d.n, "cmb_sample_blocks: n_roots %lld outside [1, N]",
           (long long)n_roots);
-  CMB_ARG(p_intra >= 0.0 && p_intra <= 1.0, "cmb_sample_blocks: p_intra outside [0, 1]");
-  for (int h = 0; h < n_hops; ++h)
-    CMB_ARG(fanouts[h] >= 1 && fanouts[h] <= CMB_MAX_FANOUT,
-            "cmb_sample_blocks: fanout[%d] = %d outside [1, %d]", h, fanouts[h], CMB_MAX_FANOUT);
   int64_t n_cap[CMB_MAX_HOPS + 1], e_cap[CMB_MAX_HOPS];
   cmb_blocks_capacity(n_roots, fanouts, n_hops, g->d.n, n_cap, e_cap);
   CMB_ARG(out->nodes && out->sizes, "cmb_sample_blocks: null nodes/sizes");
@@ -163,13 +139,73 @@ cmb_status cmb_sample_blocks(const cmb_graph* g, const int32_t* roots, int64_t n
   const size_t need = cmb_sample_workspace_bytes(n_roots, fanouts, n_hops, g->d.n);
   CMB_ARG(workspace && workspace_bytes >= need && (reinterpret_cast<uintptr_t>(workspace) & 255) == 0,
           "cmb_sample_blocks: workspace must be 256-B aligned and >= %zu bytes", need);
+  return CMB_OK;
+}
 
+}  // namespace
+}  // namespace cmb
+
+using namespace cmb;
+
+extern "C" {
+
+size_t cmb_sample_workspace_bytes(int64_t n_roots, const int32_t* fanouts, int32_t n_hops,
+                                  int64_t num_nodes) {
+  if (!fanouts || n_hops < 1 || n_hops > CMB_MAX_HOPS) return 0;
+  size_t b = 0;
+  carve_sample_ws(nullptr, n_roots, fanouts, n_hops, num_nodes, &b);
+  return b;
+}
+
+cmb_status cmb_sample_blocks_multi(const cmb_graph* g, const cmb_batch* batches,
+                                   int32_t n_batches, const int32_t* fanouts, int32_t n_hops,
+                                   double p_intra, uint64_t seed, void* stream) {
+  CMB_ARG(g && batches && fanouts, "cmb_sample_blocks: null graph/batches/fanouts");
+  CMB_ARG(n_batches >= 1 && n_batches <= CMB_MAX_BATCHES_PER_LAUNCH,
+          "cmb_sample_blocks_multi: n_batches %d outside [1, %d]", n_batches,
+          CMB_MAX_BATCHES_PER_LAUNCH);
+  CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_sample_blocks: n_hops %d outside [1,%d]",
+          n_hops, CMB_MAX_HOPS);
+  CMB_ARG(p_intra >= 0.0 && p_intra <= 1.0, "cmb_sample_blocks: p_intra outside [0, 1]");
+  for (int h = 0; h < n_hops; ++h)
+    CMB_ARG(fanouts[h] >= 1 && fanouts[h] <= CMB_MAX_FANOUT,
+            "cmb_sample_blocks: fanout[%d] = %d outside [1, %d]", h, fanouts[h], CMB_MAX_FANOUT);
+  for (int i = 0; i < n_batches; ++i) {
+    const cmb_status st = check_batch(g, batches[i].roots, batches[i].n_roots, fanouts, n_hops,
+                                      batches[i].out, batches[i].workspace,
+                                      batches[i].workspace_bytes);
+    if (st != CMB_OK) return st;
+    for (int j = 0; j < i; ++j)
+      CMB_ARG(batches[j].workspace != batches[i].workspace,
+              "cmb_sample_blocks_multi: batches %d and %d share a workspace", j, i);
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  SampleWs w = carve_sample_ws(workspace, n_roots, fanouts, n_hops, g->d.n, nullptr);
   const uint32_t P16 = static_cast<uint32_t>(p_intra * 65536.0 + 0.5);
   const uint32_t wi = P16, wo = 65536u - P16;
   const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
-  return run_persistent(g, roots, n_roots, fanouts, n_hops, wi, wo, k0, k1, batch_id, out, w, s);
+  pst::PMulti m;
+  m.nb = n_batches;
+  for (int i = 0; i < n_batches; ++i) {
+    const cmb_batch& b = batches[i];
+    SampleWs w = carve_sample_ws(b.workspace, b.n_roots, fanouts, n_hops, g->d.n, nullptr);
+    fill_args(m.a[i], g, b.roots, b.n_roots, fanouts, n_hops, wi, wo, k0, k1, b.batch_id, b.out,
+              w);
+    // barrier state + tagged aggregates (contiguous) are cleared for every batch
+    CMB_CUDA(cudaMemsetAsync(w.bar, 0,
+                             reinterpret_cast<char*>(w.pub + 2 * kMaxPersistBlocks) -
+                                 reinterpret_cast<char*>(w.bar),
+                             s));
+  }
+  return launch_persistent(g, m, s);
+}
+
+cmb_status cmb_sample_blocks(const cmb_graph* g, const int32_t* roots, int64_t n_roots,
+                             const int32_t* fanouts, int32_t n_hops, double p_intra, uint64_t seed,
+                             uint32_t batch_id, cmb_blocks* out, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+  CMB_ARG(g && roots && fanouts && out, "cmb_sample_blocks: null graph/roots/fanouts/out");
+  cmb_batch b{roots, n_roots, batch_id, out, workspace, workspace_bytes};
+  return cmb_sample_blocks_multi(g, &b, 1, fanouts, n_hops, p_intra, seed, stream);
 }
 
 }  // extern "C"

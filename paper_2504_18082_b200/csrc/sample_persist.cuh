@@ -40,6 +40,13 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// Several batches can share one launch: block b works on batch b % nb as virtual block
+// b / nb of a virtual grid of the blocks with that residue (its own barrier, prefixes and
+// map).  All phase code addresses blocks through vblk() / vgrid().
+__shared__ int g_vblk, g_vgrid;
+__device__ __forceinline__ int vblk() { return g_vblk; }
+__device__ __forceinline__ int vgrid() { return g_vgrid; }
+
 struct PArgs {
   DevGraph g;
   const int32_t* roots;
@@ -68,7 +75,7 @@ struct PArgs {
 #define CMB_PROF(a, k)                                                               \
   do {                                                                               \
     if (threadIdx.x == 0 && (k) < 64)                                                \
-      (a).prof[(size_t)blockIdx.x * 64 + (k)] = globaltimer();                       \
+      (a).prof[(size_t)vblk() * 64 + (k)] = globaltimer();                       \
     ++(k);                                                                           \
   } while (0)
 
@@ -92,7 +99,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned arrived = atomicAdd(bar, 1u);
-    if (arrived == gridDim.x - 1) {
+    if (arrived == vgrid() - 1) {
       bar[0] = 0u;
       __threadfence();
       atomicAdd(bar + 1, 1u);
@@ -131,10 +138,10 @@ template <int PB>
 __device__ __forceinline__ int32_t publish_and_prefix(unsigned long long* pub, unsigned tag,
                                                       int32_t agg, Smem<PB>& sm) {
   if (threadIdx.x == 0)
-    st_relaxed64(pub + blockIdx.x, (static_cast<unsigned long long>(tag) << 32) |
+    st_relaxed64(pub + vblk(), (static_cast<unsigned long long>(tag) << 32) |
                                        static_cast<uint32_t>(agg));
   int32_t s = 0;
-  for (int j = threadIdx.x; j < (int)blockIdx.x; j += PB) {
+  for (int j = threadIdx.x; j < (int)vblk(); j += PB) {
     unsigned long long v;
     while (((v = ld_relaxed64(pub + j)) >> 32) != tag) {
     }
@@ -149,9 +156,9 @@ __device__ __forceinline__ int32_t publish_and_prefix(unsigned long long* pub, u
 }
 
 __device__ __forceinline__ void range_of(int64_t n, int64_t align, int64_t& lo, int64_t& hi) {
-  int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  int64_t per = (n + vgrid() - 1) / vgrid();
   per = (per + align - 1) / align * align;
-  lo = (int64_t)blockIdx.x * per;
+  lo = (int64_t)vblk() * per;
   if (lo > n) lo = n;
   hi = lo + per;
   if (hi > n) hi = n;
@@ -163,8 +170,8 @@ __device__ void phase_relabel(const PArgs& a, int h) {
   const int64_t e_h = __ldcg(a.sizes + a.L + 1 + h);
   int32_t* gid = (h == a.L - 1) ? a.last_src : nullptr;
   int32_t* ind = a.indices[h];
-  const int64_t stride = (int64_t)gridDim.x * PB;
-  for (int64_t e0 = blockIdx.x * (int64_t)PB + threadIdx.x; e0 < e_h; e0 += 4 * stride) {
+  const int64_t stride = (int64_t)vgrid() * PB;
+  for (int64_t e0 = vblk() * (int64_t)PB + threadIdx.x; e0 < e_h; e0 += 4 * stride) {
     int32_t u[4];
     unsigned long long v[4];
 #pragma unroll
@@ -355,7 +362,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   CMB_PROF(a, pk);
   const int32_t base = publish_and_prefix<PB>(a.pub, static_cast<unsigned>(h + 1), run, sm);
   CMB_PROF(a, pk);
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+  if (vblk() == vgrid() - 1 && threadIdx.x == 0) {
     a.indptr[h][n_h] = base + run;
     a.sizes[a.L + 1 + h] = base + run;
   }
@@ -485,7 +492,7 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   const int32_t base =
       publish_and_prefix<PB>(a.pub + kMaxBlocks, static_cast<unsigned>(h + 1), run, sm);
   CMB_PROF(a, pk);
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) a.sizes[h + 1] = n_h + base + run;
+  if (vblk() == vgrid() - 1 && threadIdx.x == 0) a.sizes[h + 1] = n_h + base + run;
   for (int64_t e = lo + threadIdx.x; e < hi; e += PB) {
     const uint32_t sc = __ldcg(a.scan + e);
     if (sc & 0x80000000u) {
@@ -497,8 +504,14 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   }
 }
 
+constexpr int kMaxNB = 4;  // batches per launch
+struct PMulti {
+  int nb;
+  PArgs a[kMaxNB];
+};
+
 template <int PB>
-__global__ void __launch_bounds__(PB, 1024 / PB) k_sample_persistent(PArgs a) {
+__device__ __forceinline__ void run_batch(const PArgs& a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<PB>& sm = *reinterpret_cast<Smem<PB>*>(smem_raw);
   __shared__ unsigned gen_s, tag_s;
@@ -511,8 +524,8 @@ __global__ void __launch_bounds__(PB, 1024 / PB) k_sample_persistent(PArgs a) {
   const unsigned long long tag = static_cast<unsigned long long>(tag_s) << 32;
   int pk = 0;
   CMB_PROF(a, pk);
-  for (int64_t i = blockIdx.x * (int64_t)PB + threadIdx.x; i < a.n_roots;
-       i += (int64_t)gridDim.x * PB) {
+  for (int64_t i = vblk() * (int64_t)PB + threadIdx.x; i < a.n_roots;
+       i += (int64_t)vgrid() * PB) {
     const uint32_t u = static_cast<uint32_t>(a.roots[i]);
     a.nodes[i] = static_cast<int32_t>(u);
     const unsigned long long old = atomicExch(a.map + u, tag | kFinal | static_cast<uint32_t>(i));
@@ -521,7 +534,7 @@ __global__ void __launch_bounds__(PB, 1024 / PB) k_sample_persistent(PArgs a) {
     if ((old & 0xffffffff00000000ull) == tag && (static_cast<uint32_t>(old) & kFinal))
       raise_status(a.status, CMB_ERR_INVALID_INPUT);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.sizes[0] = a.n_roots;
+  if (vblk() == 0 && threadIdx.x == 0) a.sizes[0] = a.n_roots;
   for (int h = 0; h < a.L; ++h) {
     if (h > 0) phase_relabel<PB>(a, h - 1);
     CMB_PROF(a, pk);                                  // +0 relabel(h-1)
@@ -531,7 +544,7 @@ __global__ void __launch_bounds__(PB, 1024 / PB) k_sample_persistent(PArgs a) {
     CMB_PROF(a, pk);                                  // +4 picks + marks
     grid_barrier(a.bar, gen);
     CMB_PROF(a, pk);                                  // +5 barrier (marks final)
-    if (h == 0 && blockIdx.x == 0 && threadIdx.x == 0) *a.tag_ctr = tag_s;  // all have read it
+    if (h == 0 && vblk() == 0 && threadIdx.x == 0) *a.tag_ctr = tag_s;  // all have read it
     phase_flag_assign<PB>(a, h, sm, pk, tag);         // +6 flag scan, +7 prefix
     CMB_PROF(a, pk);                                  // +8 assign
     grid_barrier(a.bar, gen);
@@ -539,6 +552,19 @@ __global__ void __launch_bounds__(PB, 1024 / PB) k_sample_persistent(PArgs a) {
   }
   phase_relabel<PB>(a, a.L - 1);
   CMB_PROF(a, pk);
+}
+
+template <int PB>
+__global__ void __launch_bounds__(PB, 1024 / PB)
+    k_sample_persistent(const __grid_constant__ PMulti m) {
+  const int nb = m.nb;
+  const int grp = blockIdx.x % nb;
+  if (threadIdx.x == 0) {
+    g_vblk = blockIdx.x / nb;
+    g_vgrid = (gridDim.x - grp + nb - 1) / nb;
+  }
+  __syncthreads();
+  run_batch<PB>(m.a[grp]);
 }
 
 template <int PB>

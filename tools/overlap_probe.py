@@ -40,9 +40,22 @@ def main():
             ov.step(t)
         ov.join()
 
+    bats = {nb: cmb.BatchedPipeline(g, torch.from_numpy(b.train), cfg.batch_size, cfg.fanouts,
+                                    p=0.5, nb=nb) for nb in (2, 4)}
+
+    def run_bat(nb):
+        def f(K):
+            for t in range(0, K, nb):
+                bats[nb].step_group(range(t, t + nb))
+        return f
+
     run_seq(10)
     run_ov(10)
+    for nb in bats:
+        run_bat(nb)(8)
     out = {"seq": timed(run_seq, K), "overlap": timed(run_ov, K)}
+    for nb in bats:
+        out[f"batched{nb}"] = timed(run_bat(nb), K)
     print(json.dumps({k: round(v, 1) for k, v in out.items()}))
 
 
