@@ -2,6 +2,7 @@
 // Product code only: nothing here is shared with oracle/ (see DESIGN.md).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -116,4 +117,9 @@ struct cmb_graph {
   int32_t* status;  // graph workspace header
   int device;
   int num_sms;
+  // TMA descriptor of the feature table for tile::gather4 row loads (2D: W columns x N rows,
+  // box W x 1); has_xmap = 0 when the layout does not allow it (W > 256 or unaligned)
+  alignas(64) CUtensorMap xmap;
+  int has_xmap;
+  int xmap_w;  // columns per row fetched by TMA (F rounded up to a 16-byte multiple)
 };

@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(256, (LPR == 16 && NV == 2 && CH == 2) ? 4 : 1
 }  // namespace cmb
 
 #include "gather_bulk.cuh"
+#include "gather_tma.cuh"
 
 namespace cmb {
 namespace {
@@ -545,7 +546,8 @@ int agg_kernel_form() {
     if (e && e[0] == 'r') return 1;
     if (e && e[0] == 't') return 2;
     if (e && e[0] == 'p') return 3;
-    if (e && e[0] == 'b') return 4;  // TMA bulk-copy form (opt-in)
+    if (e && e[0] == 'b') return 4;  // per-row cp.async.bulk form (opt-in)
+    if (e && e[0] == 'g') return 5;  // TMA tile::gather4 form
     return 0;
   }();
   return v;
@@ -732,6 +734,47 @@ cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t
   CMB_ARG(x_in_ld >= g->d.f && h_ld >= g->d.f, "cmb_gather_aggregate: ld < F");
   CMB_ARG(n_last_dst_cap <= nodes_cap, "cmb_gather_aggregate: n_last_dst_cap > nodes_cap");
   const int L = n_hops;
+  const int f4 = (g->d.f + 3) / 4;
+  if (agg_kernel_form() == 5 && g->has_xmap && f4 <= 64 && (x_in_ld % 4) == 0 &&
+      (h_ld % 4) == 0 && aligned16(x_in) && aligned16(h_out)) {
+    // TMA tile::gather4 form
+    const uint32_t rb = static_cast<uint32_t>(g->xmap_w) * 4u;
+    static const int stages_env = [] {
+      const char* e = std::getenv("CMB_TMA_STAGES");
+      return e ? std::atoi(e) : 2;
+    }();
+    int stages = stages_env < 1 ? 1 : (stages_env > 8 ? 8 : stages_env);
+    while (stages > 1 && tma::smem_bytes(rb, stages) > 227 * 1024) --stages;
+    const size_t smem = tma::smem_bytes(rb, stages);
+    const void* fn = f4 <= 32 ? reinterpret_cast<const void*>(&k_gather_mean_tma<1>)
+                              : reinterpret_cast<const void*>(&k_gather_mean_tma<2>);
+    static size_t configured[2] = {0, 0};
+    int per_sm = 1;
+    if (configured[f4 > 32] < smem) {
+      CMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      configured[f4 > 32] = smem;
+    }
+    CMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, tma::kWarps * 32, smem));
+    if (per_sm < 1) per_sm = 1;
+    const int64_t windows = (n_last_dst_cap + tma::kRows - 1) / tma::kRows;
+    const int64_t want = (windows + tma::kWarps - 1) / tma::kWarps;
+    const int64_t cap = static_cast<int64_t>(g->num_sms) * per_sm;
+    const int grid = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t* nd = b->sizes + (L - 1);
+    if (f4 <= 32)
+      k_gather_mean_tma<1><<<grid, tma::kWarps * 32, smem, s>>>(
+          g->xmap, stages, b->indptr[L - 1], b->indices[L - 1], b->last_src_ids, nd,
+          n_last_dst_cap, b->nodes, f4, rb, reinterpret_cast<float4*>(h_out), h_ld / 4,
+          reinterpret_cast<float4*>(x_in), x_in_ld / 4, b->new_src_mask);
+    else
+      k_gather_mean_tma<2><<<grid, tma::kWarps * 32, smem, s>>>(
+          g->xmap, stages, b->indptr[L - 1], b->indices[L - 1], b->last_src_ids, nd,
+          n_last_dst_cap, b->nodes, f4, rb, reinterpret_cast<float4*>(h_out), h_ld / 4,
+          reinterpret_cast<float4*>(x_in), x_in_ld / 4, b->new_src_mask);
+    CMB_CUDA(cudaGetLastError());
+    return CMB_OK;
+  }
   return mean_dispatch(b->indptr[L - 1], b->indices[L - 1], b->last_src_ids, b->sizes + (L - 1),
                        n_last_dst_cap, g->d.x, g->d.ld, b->nodes, g->d.f, h_out, h_ld, x_in,
                        x_in_ld, b->new_src_mask, g->num_sms, static_cast<cudaStream_t>(stream),

@@ -7,6 +7,7 @@
 // per-edge probability tensor (P:717, 4 B/edge): the sampler splits a row into
 // intra / inter parts with one 8-byte load and no per-edge work.
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -89,6 +90,45 @@ GraphWs carve_graph_ws(void* base, int64_t n, int32_t ncomm, size_t* bytes) {
   return w;
 }
 
+// TMA descriptor of the feature table for tile::gather4 (cp.async.bulk.tensor.2d ... gather4):
+// a 2D fp32 tensor of ld columns x N rows, box W x 1 with W = F rounded up to a 16-byte
+// multiple (W <= 256 and W <= ld).  The L2 promotion (fetch granularity from DRAM) is
+// CMB_TMA_L2PROMO = 0 none, 64, 128 (default) or 256.  Obtained through the runtime's
+// driver entry point so the library needs no link-time libcuda.
+void make_feature_tensor_map(cmb_graph* g) {
+  const int64_t w = (g->d.f + 3) / 4 * 4;
+  if (w > 256 || w > g->d.ld || (g->d.ld * 4) % 16 != 0 ||
+      (reinterpret_cast<uintptr_t>(g->d.x) & 15) != 0)
+    return;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      fn == nullptr)
+    return;
+  auto encode = reinterpret_cast<CUresult(CUDAAPI*)(
+      CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+      const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+      CUtensorMapL2promotion, CUtensorMapFloatOOBfill)>(fn);
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  if (const char* e = std::getenv("CMB_TMA_L2PROMO")) {
+    const int v = std::atoi(e);
+    promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+          : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+          : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                     : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  }
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g->d.ld), static_cast<cuuint64_t>(g->d.n)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g->d.ld) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(w), 1u};
+  const cuuint32_t estr[2] = {1u, 1u};
+  if (encode(&g->xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(g->d.x), dims,
+             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+    g->has_xmap = 1;
+    g->xmap_w = static_cast<int>(w);
+  }
+}
+
 }  // namespace
 }  // namespace cmb
 
@@ -151,7 +191,10 @@ cmb_status cmb_load_graph(const cmb_graph_desc* d, void* stream, cmb_graph** out
                                       w.bounds);
   CMB_CUDA(cudaGetLastError());
 
-  cmb_graph* g = static_cast<cmb_graph*>(std::calloc(1, sizeof(cmb_graph)));
+  // 64-byte aligned (the embedded CUtensorMap requires it)
+  const size_t gbytes = (sizeof(cmb_graph) + 63) / 64 * 64;
+  cmb_graph* g = static_cast<cmb_graph*>(std::aligned_alloc(64, gbytes));
+  if (g) std::memset(static_cast<void*>(g), 0, gbytes);
   if (!g) {
     set_error("cmb_load_graph: out of host memory");
     return CMB_ERR_INVALID_ARGUMENT;
@@ -170,6 +213,9 @@ cmb_status cmb_load_graph(const cmb_graph_desc* d, void* stream, cmb_graph** out
   g->status = &w.hdr->status;
   g->device = dev;
   g->num_sms = sms;
+  g->has_xmap = 0;
+  g->xmap_w = 0;
+  if (d->features) make_feature_tensor_map(g);
   *out = g;
   return CMB_OK;
 }
