@@ -217,6 +217,32 @@ CMB_API cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* bl
                                 int64_t n_last_dst_cap, int64_t nodes_cap, float* x_in,
                                 int64_t x_in_ld, float* h_out, int64_t h_ld, void* stream);
 
+/* ------------------------------------------------------------------ a6: row-sharded features */
+/* Rank r of `world` owns feature rows [r*S, min(N, (r+1)*S)), S = rows_per_shard (north_star:
+ * "for papers100M-scale inputs the feature table is row-sharded, with an NCCL all-to-all over
+ * NVLink for remote rows").  The exchange of one batch is: cmb_shard_plan on the requesting
+ * rank, all-to-all of counts and ids (NCCL, host side), cmb_gather_rows on every owner,
+ * all-to-all of the rows back, cmb_scatter_rows -> X_in byte-identical to cmb_gather_features
+ * on a replicated table. */
+CMB_API size_t cmb_shard_plan_workspace_bytes(int64_t n_cap);
+/* Stable bucketing of nodes[0:*n_dev) by owner = id / rows_per_shard: counts (device int64
+ * [world]), send_ids (device int32 [n_cap], owner-major, original order within an owner) and
+ * perm (device int32 [n_cap], the X_in row of each send slot).  An id whose owner is >= world
+ * sets CMB_ERR_INVALID_INPUT in the workspace status. */
+CMB_API cmb_status cmb_shard_plan(const int32_t* nodes, const int64_t* n_dev, int64_t n_cap,
+                                  int64_t rows_per_shard, int32_t world, int64_t* counts,
+                                  int32_t* send_ids, int32_t* perm, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+/* Row gather from a (shard of a) feature table whose first row is global row `row0`:
+ * out[i, 0:F] = x[(ids[i] - row0) * ld + 0:F] for i < *n_dev <= n_cap.  Bit-exact copy. */
+CMB_API cmb_status cmb_gather_rows(const float* x, int64_t ld, int64_t row0, int32_t feat_dim,
+                                   const int32_t* ids, const int64_t* n_dev, int64_t n_cap,
+                                   float* out, int64_t out_ld, void* stream);
+/* out[perm[k], 0:F] = rows[k, 0:F] for k < *n_dev <= n_cap. */
+CMB_API cmb_status cmb_scatter_rows(const float* rows, int64_t rows_ld, const int32_t* perm,
+                                    const int64_t* n_dev, int64_t n_cap, int32_t feat_dim,
+                                    float* out, int64_t out_ld, void* stream);
+
 /* ------------------------------------------------------------------ status */
 /* Synchronises `stream`, returns (and clears) the sticky device status word of a
  * graph / order / sample workspace. */

@@ -41,7 +41,8 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_order_roots_workspace_bytes", "cmb_order_roots", "cmb_blocks_capacity",
            "cmb_sample_workspace_bytes", "cmb_sample_blocks", "cmb_sample_blocks_multi",
            "cmb_gather_features",
-           "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_get_device_status",
+           "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_shard_plan_workspace_bytes",
+           "cmb_shard_plan", "cmb_gather_rows", "cmb_scatter_rows", "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
 
@@ -104,6 +105,10 @@ def lib():
             "cmb_sage_mean_aggregate": (I32, [P, P, P, I64, P, I64, P, I32, P, I64, P]),
             "cmb_gather_aggregate": (I32, [P, ctypes.POINTER(Blocks), I32, I64, I64, P, I64, P,
                                            I64, P]),
+            "cmb_shard_plan_workspace_bytes": (SZ, [I64]),
+            "cmb_shard_plan": (I32, [P, P, I64, I64, I32, P, P, P, P, SZ, P]),
+            "cmb_gather_rows": (I32, [P, I64, I64, I32, P, P, I64, P, I64, P]),
+            "cmb_scatter_rows": (I32, [P, I64, P, P, I64, I32, P, I64, P]),
             "cmb_get_device_status": (I32, [P, P]),
             "cmb_status_string": (ctypes.c_char_p, [I32]),
             "cmb_last_error_message": (ctypes.c_char_p, []),

@@ -709,6 +709,20 @@ cmb_status cmb_gather_features(const cmb_graph* g, const int32_t* node_ids, cons
                          g->num_sms, static_cast<cudaStream_t>(stream));
 }
 
+cmb_status cmb_gather_rows(const float* x, int64_t ld, int64_t row0, int32_t feat_dim,
+                           const int32_t* ids, const int64_t* n_dev, int64_t n_cap, float* out,
+                           int64_t out_ld, void* stream) {
+  CMB_ARG(x && ids && n_dev && out, "cmb_gather_rows: null argument");
+  CMB_ARG(feat_dim >= 1 && ld >= feat_dim && out_ld >= feat_dim && n_cap >= 0 && row0 >= 0,
+          "cmb_gather_rows: bad feat_dim / ld / n_cap / row0");
+  int dev = 0, sms = 148;
+  CMB_CUDA(cudaGetDevice(&dev));
+  CMB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // row id v lives at x[(v - row0) * ld]: shift the base (alignment is preserved)
+  return gather_dispatch(x - row0 * ld, ld, feat_dim, ids, n_dev, n_cap, out, out_ld, sms,
+                         static_cast<cudaStream_t>(stream));
+}
+
 cmb_status cmb_sage_mean_aggregate(const int32_t* indptr, const int32_t* indices,
                                    const int64_t* n_dst_dev, int64_t n_dst_cap, const float* src,
                                    int64_t src_ld, const int32_t* src_map, int32_t feat_dim,
