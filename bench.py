@@ -334,7 +334,7 @@ def run_cmb(args, bundle):
             "stage_ms_per_step": {"sample_relabel": float(np.mean(samp_ms)),
                                   "gather_aggregate": float(np.mean(agg_ms))},
             "roofline": {"bound": "hbm",
-                         "kernel": "k_gather_mean_pipe (fused a4+a5, cmb_gather_aggregate)",
+                         "kernel": "k_gather_mean_row (fused a4+a5, cmb_gather_aggregate)",
                          "achieved": achieved, "peak": peak, "peak_source": peak_src,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": float(np.mean(alg))},

@@ -347,6 +347,8 @@ __global__ void __launch_bounds__(256, (LPR == 16 && NV == 2 && CH == 2) ? 4 : 1
     const float4* __restrict__ src, int64_t src_ld4, const int32_t* __restrict__ map, int f4,
     float4* __restrict__ out, int64_t out_ld4, float4* __restrict__ x_in, int64_t x_in_ld4,
     const uint32_t* __restrict__ new_mask, int hint) {
+  constexpr unsigned kFull = 0xffffffffu;
+  constexpr int GPW = 32 / LPR;  // lane groups (dst rows) per warp
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
   auto LD = [&](const float4* p) { return hint ? ldg4_hint(p, pol_keep) : ldg4(p); };
   auto ST = [&](float4* p, const float4& v) {
@@ -355,10 +357,13 @@ __global__ void __launch_bounds__(256, (LPR == 16 && NV == 2 && CH == 2) ? 4 : 1
   };
   const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
   const int lane = threadIdx.x % LPR;
-  const int wl = threadIdx.x & 31;
-  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (wl & ~(LPR - 1)));
-  const int64_t G = (int64_t)gridDim.x * (blockDim.x / LPR);
-  const int64_t g0 = blockIdx.x * (int64_t)(blockDim.x / LPR) + threadIdx.x / LPR;
+  // Warp-uniform walk: the GPW groups of a warp take rows rb + q (q = group in the warp) and all
+  // lanes run the same trip counts (row loop, max degree over the warp's rows), so every shuffle
+  // uses the full mask.  (Per-group masks made the compiler wrap each shuffle in MATCH / REDUX /
+  // VOTEU convergence checks on the XU pipe: ~4 per edge, the XU at 94 % busy.)
+  const int q = (threadIdx.x & 31) / LPR;
+  const int64_t WG = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32) * GPW;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32) * GPW;
 
   struct A { int32_t e0, e1, self; };
   struct B { int32_t g, l, first; };
@@ -382,35 +387,41 @@ __global__ void __launch_bounds__(256, (LPR == 16 && NV == 2 && CH == 2) ? 4 : 1
     return b;
   };
 
-  int64_t row = g0;
-  A ac = loadA(row);
+  int64_t rb = w0;
+  A ac = loadA(rb + q);
   B bc = loadB(ac, 0);
-  A an = loadA(row + G);
-  for (; row < n_dst; row += G) {
-    const A aa = loadA(row + 2 * G);  // stage A, two rows ahead
-    const B bn = loadB(an, 0);        // stage B, one row ahead
+  A an = loadA(rb + q + WG);
+  for (; rb < n_dst; rb += WG) {
+    const int64_t row = rb + q;       // rows >= n_dst (tail of the last sweep) have deg 0
+    const bool live = row < n_dst;
+    const A aa = loadA(row + 2 * WG);  // stage A, two rows ahead
+    const B bn = loadB(an, 0);         // stage B, one row ahead
     const int32_t deg = ac.e1 - ac.e0;
+    int32_t degmax = deg;
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) degmax = max(degmax, __shfl_xor_sync(kFull, degmax, o));
     for (int c0 = 0; c0 < f4; c0 += LPR * NV) {
       float4 acc[NV];
 #pragma unroll
       for (int k = 0; k < NV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       float4 self[NV];
-      if (x_in) {
+      if (x_in && live) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
           const int c = c0 + lane + k * LPR;
           if (c < f4) self[k] = LD(src + (int64_t)ac.self * src_ld4 + c);
         }
       }
-      for (int32_t base = 0; base < deg; base += LPR) {
+      for (int32_t base = 0; base < degmax; base += LPR) {
         const B bb = base == 0 ? bc : loadB(ac, base);  // rows with deg > LPR: rest on demand
-        const int cnt = min(LPR, deg - base);
-        for (int j0 = 0; j0 < cnt; j0 += CH) {
+        const int cnt = min(LPR, deg - base);           // <= 0 for a group already done
+        const int cmax = min(LPR, degmax - base);
+        for (int j0 = 0; j0 < cmax; j0 += CH) {
           float4 v[CH][NV];
 #pragma unroll
           for (int u = 0; u < CH; ++u) {
             const int j = j0 + u;
-            const int32_t r = __shfl_sync(gmask, bb.g, j & (LPR - 1), LPR);
+            const int32_t r = __shfl_sync(kFull, bb.g, j & (LPR - 1), LPR);
 #pragma unroll
             for (int k = 0; k < NV; ++k) {
               const int c = c0 + lane + k * LPR;
@@ -420,8 +431,8 @@ __global__ void __launch_bounds__(256, (LPR == 16 && NV == 2 && CH == 2) ? 4 : 1
 #pragma unroll
           for (int u = 0; u < CH; ++u) {
             const int j = j0 + u;
-            const int fj = __shfl_sync(gmask, bb.first, j & (LPR - 1), LPR);
-            const int32_t lj = __shfl_sync(gmask, bb.l, j & (LPR - 1), LPR);
+            const int fj = __shfl_sync(kFull, bb.first, j & (LPR - 1), LPR);
+            const int32_t lj = __shfl_sync(kFull, bb.l, j & (LPR - 1), LPR);
             if (j < cnt) {
 #pragma unroll
               for (int k = 0; k < NV; ++k) add4(acc[k], v[u][k]);
@@ -440,7 +451,7 @@ __global__ void __launch_bounds__(256, (LPR == 16 && NV == 2 && CH == 2) ? 4 : 1
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         const int c = c0 + lane + k * LPR;
-        if (c < f4) {
+        if (c < f4 && live) {
           float4 h = make_float4(0.f, 0.f, 0.f, 0.f);
           if (deg > 0) {
             h.x = __fdiv_rn(acc[k].x, fd);
@@ -464,6 +475,8 @@ __global__ void __launch_bounds__(256, (LPR == 16 && NV == 2 && CH == 2) ? 4 : 1
 
 #include "gather_bulk.cuh"
 #include "gather_tma.cuh"
+#include "gather_async.cuh"
+#include "gather_row.cuh"
 
 namespace cmb {
 namespace {
@@ -548,9 +561,57 @@ int agg_kernel_form() {
     if (e && e[0] == 'p') return 3;
     if (e && e[0] == 'b') return 4;  // per-row cp.async.bulk form (opt-in)
     if (e && e[0] == 'g') return 5;  // TMA tile::gather4 form
+    if (e && e[0] == 'a') return 6;  // cp.async ring form
+    if (e && e[0] == 'w') return 7;  // warp-per-row form
     return 0;
   }();
   return v;
+}
+
+template <int KS>
+cmb_status launch_async_ks(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
+                           const int32_t* gid, const int64_t* n_dev, int64_t n_cap,
+                           const float* src, int64_t src_ld, const int32_t* map, int f4,
+                           float* out, int64_t out_ld, float* x_in, int64_t x_in_ld,
+                           const uint32_t* mask) {
+  const size_t smem = asyncg::smem_bytes(KS, f4);
+  static size_t configured = 0;
+  if (configured < smem) {
+    CMB_CUDA(cudaFuncSetAttribute(k_gather_mean_async<KS>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  int per_sm = 1;
+  CMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_mean_async<KS>,
+                                                         asyncg::kWarps * 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t want = (n_cap + asyncg::kWarps - 1) / asyncg::kWarps;
+  const int64_t cap = static_cast<int64_t>(sms) * per_sm;
+  const int grid = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
+  k_gather_mean_async<KS><<<grid, asyncg::kWarps * 32, smem, s>>>(
+      indptr, idx, gid, n_dev, n_cap, reinterpret_cast<const float4*>(src), src_ld / 4, map, f4,
+      reinterpret_cast<float4*>(out), out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4,
+      mask);
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+cmb_status launch_async(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
+                        const int32_t* gid, const int64_t* n_dev, int64_t n_cap, const float* src,
+                        int64_t src_ld, const int32_t* map, int f4, float* out, int64_t out_ld,
+                        float* x_in, int64_t x_in_ld, const uint32_t* mask) {
+  static const int ks = [] {  // ring slots per warp (feature rows in flight per warp)
+    const char* e = std::getenv("CMB_ASYNC_SLOTS");
+    return e ? std::atoi(e) : 16;
+  }();
+#define CMB_ASYNC(K_)                                                                        \
+  return launch_async_ks<K_>(sms, s, indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, out, \
+                             out_ld, x_in, x_in_ld, mask)
+  if (ks <= 8) CMB_ASYNC(8);
+  if (ks <= 12) CMB_ASYNC(12);
+  if (ks <= 16) CMB_ASYNC(16);
+  CMB_ASYNC(24);
+#undef CMB_ASYNC
 }
 
 template <int NV>
@@ -631,7 +692,7 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_
                          const int64_t* n_dev, int64_t n_cap, const float* src, int64_t src_ld,
                          const int32_t* map, int f, float* out, int64_t out_ld, float* x_in,
                          int64_t x_in_ld, const uint32_t* mask, int sms, cudaStream_t s,
-                         int32_t* status = nullptr) {
+                         int32_t* status = nullptr, int deg_hint = 8) {
   if (n_cap <= 0) return CMB_OK;
   const int f4 = (f + 3) / 4;
   const bool vec = aligned16(src) && aligned16(out) && src_ld % 4 == 0 && out_ld % 4 == 0 &&
@@ -646,6 +707,46 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_
     return launch_bulk<2>(sms, s, indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, rb, out,
                           out_ld, x_in, x_in_ld, mask);
   }
+  const int form = agg_kernel_form();
+  if (vec && x_in && gid && f4 <= 32 && (form == 0 || form == 7)) {
+    // default fused form: one warp per dst row (gather_row.cuh).  DMAX = edge rows issued per
+    // round: the block's fanout (deg_hint = e_cap / n_cap) clamped to [4, 8]
+    static const int dmax_env = [] {
+      const char* e = std::getenv("CMB_ROW_DMAX");
+      return e ? std::atoi(e) : 0;
+    }();
+    const int dmax = dmax_env > 0 ? dmax_env : deg_hint;
+    static const int bps = [] {  // 4 resident 256-thread blocks per SM (64 registers)
+      const char* e = std::getenv("CMB_AGG_BLOCKS_PER_SM");
+      return e ? std::atoi(e) : 4;
+    }();
+    const int64_t want = (n_cap + 7) / 8;  // 8 warps (rows) per 256-thread block
+    const int64_t cap = static_cast<int64_t>(sms) * (bps > 0 ? bps : 8);
+    const int grid = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
+    static const int minb = [] {
+      const char* e = std::getenv("CMB_ROW_MINB");
+      return e ? std::atoi(e) : 4;
+    }();
+#define CMB_ROWK(D_)                                                                          \
+  if (minb == 5) CMB_ROWK2(D_, 5); else CMB_ROWK2(D_, 4)
+#define CMB_ROWK2(D_, M_)                                                                     \
+  k_gather_mean_row<D_, M_><<<grid, 256, 0, s>>>(indptr, idx, gid, n_dev, n_cap,                  \
+                                             reinterpret_cast<const float4*>(src), src_ld / 4, \
+                                             map, f4, reinterpret_cast<float4*>(out),         \
+                                             out_ld / 4, reinterpret_cast<float4*>(x_in),     \
+                                             x_in_ld / 4, mask)
+    if (dmax <= 4) { CMB_ROWK(4); }
+    else if (dmax <= 5) { CMB_ROWK(5); }
+    else if (dmax <= 6) { CMB_ROWK(6); }
+    else { CMB_ROWK(8); }
+#undef CMB_ROWK
+#undef CMB_ROWK2
+    CMB_CUDA(cudaGetLastError());
+    return CMB_OK;
+  }
+  if (vec && x_in && f4 <= 32 && form == 6)
+    return launch_async(sms, s, indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, out, out_ld,
+                        x_in, x_in_ld, mask);
   if (!vec) {
     k_sage_mean_scalar<<<sms * 8, 256, 0, s>>>(indptr, idx, n_dev, n_cap, src, src_ld, map, f,
                                                out, out_ld, x_in, x_in_ld, mask);
@@ -792,7 +893,9 @@ cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t
   return mean_dispatch(b->indptr[L - 1], b->indices[L - 1], b->last_src_ids, b->sizes + (L - 1),
                        n_last_dst_cap, g->d.x, g->d.ld, b->nodes, g->d.f, h_out, h_ld, x_in,
                        x_in_ld, b->new_src_mask, g->num_sms, static_cast<cudaStream_t>(stream),
-                       g->status);
+                       g->status,
+                       n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
+                                          : 8);
 }
 
 }  // extern "C"

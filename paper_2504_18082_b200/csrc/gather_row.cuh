@@ -1,0 +1,116 @@
+// gather_row.cuh -- the warp-per-row form of the fused a4 + a5 kernel (included by
+// features.cu; arithmetic as in the comment of k_gather_mean_pipe).
+//
+// One warp per dst row (grid stride), lane c owning float4 column c (f4 <= 32).  The edge ids of
+// the row are held lane-parallel (lane j <-> edge j; a sampled block has deg <= 32) and were
+// loaded one row ahead; the self row and up to DMAX edge rows are then issued back to back, so a
+// row costs ONE memory round trip for deg <= DMAX (the 16-lane pipelined form needs
+// ceil(deg / 2) + 1).  The sum runs in CSR order from +0 (the oracle's order); H = acc / deg
+// uses the correctly rounded reciprocal y = RN(1/deg), computed once per row, and one FMA
+// correction per element (q = RN(a*y), r = a - deg*q exact, RN(q + r*y) = RN(a/deg) -- the
+// classical FMA division step), with __fdiv_rn kept for |a| outside [2^-100, 2^100] where the
+// step's no-underflow / no-overflow premise could fail.  Warp-uniform control flow throughout
+// (full-mask shuffles only).
+#pragma once
+
+namespace cmb {
+
+__device__ __forceinline__ float div_small(float a, float d, float y) {
+  const float aa = fabsf(a);
+  if (!(aa >= 0x1p-100f && aa <= 0x1p100f)) return a == 0.f ? a / d : __fdiv_rn(a, d);
+  const float q = __fmul_rn(a, y);
+  const float r = __fmaf_rn(-d, q, a);
+  return __fmaf_rn(r, y, q);
+}
+
+template <int DMAX, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    k_gather_mean_row(const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                      const int32_t* __restrict__ gid, const int64_t* __restrict__ n_dst_dev,
+                      int64_t n_dst_cap, const float4* __restrict__ src, int64_t src_ld4,
+                      const int32_t* __restrict__ map, int f4, float4* __restrict__ out,
+                      int64_t out_ld4, float4* __restrict__ x_in, int64_t x_in_ld4,
+                      const uint32_t* __restrict__ new_mask) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
+  const int lane = threadIdx.x & 31;
+  const bool col = lane < f4;
+  const int64_t W = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const float4* srcc = src + lane;  // this lane's column of every feature row
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  struct A { int32_t e0, e1, self; };
+  struct B { int32_t g, l, first; };
+  auto loadA = [&](int64_t row) {
+    A a{0, 0, 0};
+    if (row < n_dst) {
+      a.e0 = __ldg(indptr + row);
+      a.e1 = __ldg(indptr + row + 1);
+      a.self = __ldg(map + row);
+    }
+    return a;
+  };
+  auto loadB = [&](const A& a) {
+    B b{0, 0, 0};
+    const int32_t e = a.e0 + lane;
+    if (e < a.e1) {
+      b.l = __ldg(idx + e);
+      b.g = __ldg(gid + e);
+      b.first = static_cast<int>((__ldg(new_mask + (e >> 5)) >> (e & 31)) & 1u);
+    }
+    return b;
+  };
+
+  int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  A ac = loadA(row);
+  B bc = loadB(ac);
+  A an = loadA(row + W);
+  for (; row < n_dst; row += W) {
+    const A aa = loadA(row + 2 * W);  // index pipeline: A two rows ahead, B one row ahead
+    const B bn = loadB(an);
+    const int deg = ac.e1 - ac.e0;
+    const float4 sv = col ? ldg4_hint(srcc + static_cast<int64_t>(ac.self) * src_ld4, pol_keep)
+                          : zero;
+    const unsigned firsts = __ballot_sync(kFull, bc.first);
+    float4 acc = zero;
+    for (int base = 0; base < deg; base += DMAX) {
+      float4 v[DMAX];
+#pragma unroll
+      for (int j = 0; j < DMAX; ++j) {
+        const int32_t g = __shfl_sync(kFull, bc.g, (base + j) & 31);
+        v[j] = (col && base + j < deg)
+                   ? ldg4_hint(srcc + static_cast<int64_t>(g) * src_ld4, pol_keep)
+                   : zero;
+      }
+#pragma unroll
+      for (int j = 0; j < DMAX; ++j) {
+        if (base + j < deg) {
+          add4(acc, v[j]);
+          if ((firsts >> (base + j)) & 1u) {  // first occurrence of a new src node
+            const int32_t l = __shfl_sync(kFull, bc.l, base + j);
+            if (col) st4_hint(x_in + static_cast<int64_t>(l) * x_in_ld4 + lane, v[j], pol_stream);
+          }
+        }
+      }
+    }
+    if (col) {
+      float4 h = zero;
+      if (deg > 0) {
+        const float d = static_cast<float>(deg);
+        const float y = __frcp_rn(d);
+        h.x = div_small(acc.x, d, y);
+        h.y = div_small(acc.y, d, y);
+        h.z = div_small(acc.z, d, y);
+        h.w = div_small(acc.w, d, y);
+      }
+      st4_hint(out + row * out_ld4 + lane, h, pol_stream);
+      st4_hint(x_in + row * x_in_ld4 + lane, sv, pol_stream);
+    }
+    ac = an;
+    bc = bn;
+    an = aa;
+  }
+}
+
+}  // namespace cmb
