@@ -504,7 +504,7 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   }
 }
 
-constexpr int kMaxNB = 4;  // batches per launch
+constexpr int kMaxNB = CMB_MAX_BATCHES_PER_LAUNCH;  // batches per launch
 struct PMulti {
   int nb;
   PArgs a[kMaxNB];
