@@ -85,6 +85,14 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
   a.bar = w.bar;
   a.prof = w.prof;
   a.status = &w.hdr->status;
+  // CMB_PICK_DEDUP=1 warp-deduplicates the first-occurrence marks with match_any before the
+  // atomics (fewer same-address atomics on hub nodes); off by default: the MATCH costs more than
+  // it saves on the products-shaped graphs (sampler 86 vs 88 us per batch)
+  static const int dedup = [] {
+    const char* e = std::getenv("CMB_PICK_DEDUP");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.dedup = dedup;
 }
 
 cmb_status launch_persistent(const cmb_graph* g, pst::PMulti& m, cudaStream_t s) {

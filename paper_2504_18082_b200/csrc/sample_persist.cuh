@@ -68,6 +68,7 @@ struct PArgs {
   unsigned* bar;            // [0] arrivals, [1] generation
   uint64_t* prof;           // [kMaxBlocks][64] per-block %globaltimer at sub-step boundaries
   int32_t* status;
+  int dedup;                // warp-deduplicate the marks (match_any) before the atomics
 };
 
 // Per-block sub-step timeline (profiling aid, one store per sub-step per block):
@@ -443,7 +444,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t e = w0 + lane + u * PB;
-      const unsigned peers = __match_any_sync(0xffffffffu, val[u]);
+      const unsigned peers = a.dedup ? __match_any_sync(0xffffffffu, val[u]) : (1u << lane);
       if (e < e1) {
         out[e] = static_cast<int32_t>(val[u]);
         if (lane == __ffs(peers) - 1)  // lowest lane = smallest e of the duplicates

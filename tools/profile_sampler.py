@@ -25,17 +25,19 @@ def main():
     p = float(os.environ.get("P", cfg.p_intra))
     b = generate(cfg)
     g = cmb.Graph.from_bundle(b)
-    pipe = cmb.MiniBatchPipeline(g, torch.from_numpy(b.train), cfg.batch_size, cfg.fanouts,
-                                 mode=os.environ.get("MODE", "rand"),
-                                 mix=float(os.environ.get("MIX", "0")), p=p)
+    nb = int(os.environ.get("NB", "1"))  # batches per sampler launch (BatchedPipeline)
+    pipe = cmb.BatchedPipeline(g, torch.from_numpy(b.train), cfg.batch_size, cfg.fanouts,
+                               mode=os.environ.get("MODE", "rand"),
+                               mix=float(os.environ.get("MIX", "0")), p=p, nb=nb)
     L = len(cfg.fanouts)
     npts = 2 + 10 * L
-    nblk = torch.cuda.get_device_properties(0).multi_processor_count
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    nblk = (sms - sms % nb) // nb  # virtual blocks of batch 0 of each launch
     labels = [f"h{h}.{s}" for h in range(L) for s in SUB] + ["relabel(L-1)"]
     crit, mean, mx = [], [], []
     pipe.start_epoch(0)
     for t in range(25):
-        pipe.sampler.sample(pipe.batch_roots(t), p, 42, t)
+        pipe.step_group(list(range(t * nb, t * nb + nb)))
         torch.cuda.synchronize()
         ws = pipe.sampler.workspace
         raw = ws[PROF_OFFSET: PROF_OFFSET + nblk * 64 * 8].view(torch.int64).cpu().numpy()
