@@ -708,14 +708,15 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_
                           out_ld, x_in, x_in_ld, mask);
   }
   const int form = agg_kernel_form();
-  if (vec && x_in && gid && f4 <= 32 && (form == 0 || form == 7)) {
+  if (vec && x_in && gid && (form == 0 || form == 7)) {
     // default fused form: one warp per dst row (gather_row.cuh).  DMAX = edge rows issued per
-    // round: the block's fanout (deg_hint = e_cap / n_cap) clamped to [4, 8]
+    // round: the block's fanout (deg_hint = e_cap / n_cap) clamped to [4, 6]
     static const int dmax_env = [] {
       const char* e = std::getenv("CMB_ROW_DMAX");
       return e ? std::atoi(e) : 0;
     }();
-    const int dmax = dmax_env > 0 ? dmax_env : deg_hint;
+    // (8 spills at 64 registers: reddit's fanout-10 block runs best at 6, 178 vs 212 us)
+    const int dmax = dmax_env > 0 ? dmax_env : (deg_hint < 6 ? deg_hint : 6);
     static const int bps = [] {  // 4 resident 256-thread blocks per SM (64 registers)
       const char* e = std::getenv("CMB_AGG_BLOCKS_PER_SM");
       return e ? std::atoi(e) : 4;
@@ -730,7 +731,9 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_
 #define CMB_ROWK(D_)                                                                          \
   if (minb == 5) CMB_ROWK2(D_, 5); else CMB_ROWK2(D_, 4)
 #define CMB_ROWK2(D_, M_)                                                                     \
-  k_gather_mean_row<D_, M_><<<grid, 256, 0, s>>>(indptr, idx, gid, n_dev, n_cap,                  \
+  if (f4 > 32) CMB_ROWK3(D_, M_, true); else CMB_ROWK3(D_, M_, false)
+#define CMB_ROWK3(D_, M_, W_)                                                                 \
+  k_gather_mean_row<D_, M_, W_><<<grid, 256, 0, s>>>(indptr, idx, gid, n_dev, n_cap,                  \
                                              reinterpret_cast<const float4*>(src), src_ld / 4, \
                                              map, f4, reinterpret_cast<float4*>(out),         \
                                              out_ld / 4, reinterpret_cast<float4*>(x_in),     \
@@ -741,6 +744,7 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_
     else { CMB_ROWK(8); }
 #undef CMB_ROWK
 #undef CMB_ROWK2
+#undef CMB_ROWK3
     CMB_CUDA(cudaGetLastError());
     return CMB_OK;
   }

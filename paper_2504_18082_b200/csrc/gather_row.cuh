@@ -1,7 +1,7 @@
 // gather_row.cuh -- the warp-per-row form of the fused a4 + a5 kernel (included by
 // features.cu; arithmetic as in the comment of k_gather_mean_pipe).
 //
-// One warp per dst row (grid stride), lane c owning float4 column c (f4 <= 32).  The edge ids of
+// One warp per dst row (grid stride), lane c owning float4 column c of each 32-float4 chunk.  The edge ids of
 // the row are held lane-parallel (lane j <-> edge j; a sampled block has deg <= 32) and were
 // loaded one row ahead; the self row and up to DMAX edge rows are then issued back to back, so a
 // row costs ONE memory round trip for deg <= DMAX (the 16-lane pipelined form needs
@@ -23,7 +23,7 @@ __device__ __forceinline__ float div_small(float a, float d, float y) {
   return __fmaf_rn(r, y, q);
 }
 
-template <int DMAX, int MINB>
+template <int DMAX, int MINB, bool WIDE>
 __global__ void __launch_bounds__(256, MINB)
     k_gather_mean_row(const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
                       const int32_t* __restrict__ gid, const int64_t* __restrict__ n_dst_dev,
@@ -35,9 +35,7 @@ __global__ void __launch_bounds__(256, MINB)
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
   const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
   const int lane = threadIdx.x & 31;
-  const bool col = lane < f4;
   const int64_t W = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  const float4* srcc = src + lane;  // this lane's column of every feature row
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
 
   struct A { int32_t e0, e1, self; };
@@ -70,9 +68,13 @@ __global__ void __launch_bounds__(256, MINB)
     const A aa = loadA(row + 2 * W);  // index pipeline: A two rows ahead, B one row ahead
     const B bn = loadB(an);
     const int deg = ac.e1 - ac.e0;
+    const unsigned firsts = __ballot_sync(kFull, bc.first);
+    // column chunks of 32 float4 (one for F <= 128; wide rows, e.g. F = 602, take several)
+    for (int c0 = 0; c0 < (WIDE ? f4 : 1); c0 += 32) {
+    const bool col = c0 + lane < f4;
+    const float4* srcc = src + c0 + lane;
     const float4 sv = col ? ldg4_hint(srcc + static_cast<int64_t>(ac.self) * src_ld4, pol_keep)
                           : zero;
-    const unsigned firsts = __ballot_sync(kFull, bc.first);
     float4 acc = zero;
     for (int base = 0; base < deg; base += DMAX) {
       float4 v[DMAX];
@@ -89,7 +91,8 @@ __global__ void __launch_bounds__(256, MINB)
           add4(acc, v[j]);
           if ((firsts >> (base + j)) & 1u) {  // first occurrence of a new src node
             const int32_t l = __shfl_sync(kFull, bc.l, base + j);
-            if (col) st4_hint(x_in + static_cast<int64_t>(l) * x_in_ld4 + lane, v[j], pol_stream);
+            if (col)
+              st4_hint(x_in + static_cast<int64_t>(l) * x_in_ld4 + c0 + lane, v[j], pol_stream);
           }
         }
       }
@@ -104,8 +107,9 @@ __global__ void __launch_bounds__(256, MINB)
         h.z = div_small(acc.z, d, y);
         h.w = div_small(acc.w, d, y);
       }
-      st4_hint(out + row * out_ld4 + lane, h, pol_stream);
-      st4_hint(x_in + row * x_in_ld4 + lane, sv, pol_stream);
+      st4_hint(out + row * out_ld4 + c0 + lane, h, pol_stream);
+      st4_hint(x_in + row * x_in_ld4 + c0 + lane, sv, pol_stream);
+    }
     }
     ac = an;
     bc = bn;
