@@ -136,6 +136,23 @@ def algorithmic_bytes(n, e, F, L):
 
 
 # ------------------------------------------------------------------ cpu (oracle) legs
+def oracle_step(prep, bundle, roots, p, seed, batch, scratch):
+    """One oracle batch (a2-a5).  For device-generated feature tables the gathered rows come
+    from the generator's row formula (X[nodes] by definition), then the oracle's a5."""
+    import oracle
+    from gen.planted import feature_rows
+    cfg = bundle.cfg
+    if bundle.X is not None:
+        return oracle.run_batch(prep, bundle.X, cfg.feat_dim, roots, cfg.fanouts, p, seed, batch,
+                                scratch)
+    L = len(cfg.fanouts)
+    blk = oracle.sample_blocks(prep, roots, cfg.fanouts, p, seed, batch, scratch)
+    Xin = np.ascontiguousarray(feature_rows(bundle, blk["nodes"]))
+    H, H64 = oracle.sage_mean(blk["indptr"][L - 1], blk["indices"][L - 1], Xin, cfg.feat_dim)
+    blk.update({"X_in": Xin, "H": H, "H64": H64})
+    return blk
+
+
 def oracle_batches(bundle, mode, mix, p, seed, budget_s, max_batches=None):
     """Times the oracle (as it stands, single thread) on consecutive batches of epoch 0."""
     import oracle
@@ -149,8 +166,8 @@ def oracle_batches(bundle, mode, mix, p, seed, budget_s, max_batches=None):
     nb = (order.shape[0] + cfg.batch_size - 1) // cfg.batch_size
     done, edges = 0, 0
     while True:
-        r = oracle.run_batch(prep, bundle.X, cfg.feat_dim, oracle.batch_roots(order, cfg.batch_size, done % nb),
-                             cfg.fanouts, p, seed, done % nb, scratch)
+        r = oracle_step(prep, bundle, oracle.batch_roots(order, cfg.batch_size, done % nb), p,
+                        seed, done % nb, scratch)
         edges += sum(r["e"])
         done += 1
         el = time.perf_counter() - t0
@@ -175,8 +192,8 @@ def run_reference(args, bundle):
     scratch = np.full(prep.num_nodes, -1, dtype=np.int32)
 
     def step(b):
-        return oracle.run_batch(prep, bundle.X, cfg.feat_dim, oracle.batch_roots(order, cfg.batch_size, b % nb),
-                                cfg.fanouts, p, args.seed, b % nb, scratch)
+        return oracle_step(prep, bundle, oracle.batch_roots(order, cfg.batch_size, b % nb), p,
+                           args.seed, b % nb, scratch)
 
     for w in range(args.warmup):
         step(w)
@@ -253,7 +270,9 @@ def run_cmb(args, bundle):
     cfg = bundle.cfg
     p = cfg.p_intra if args.p is None else args.p
     L = len(cfg.fanouts)
-    graph = cmb.Graph.from_bundle(bundle, device=dev, validate=True)
+    from gen.device import feature_table
+    graph = cmb.Graph.from_bundle(bundle, device=dev, validate=True,
+                                  features=feature_table(bundle, dev))
     G = max(1, min(args.batches_per_launch, cmb.MAX_BATCHES_PER_LAUNCH))
     pipe = cmb.BatchedPipeline(graph, torch.from_numpy(bundle.train), cfg.batch_size,
                                cfg.fanouts, mode=args.mode, mix=args.mix, p=p, seed=args.seed,

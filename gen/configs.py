@@ -25,6 +25,9 @@ class GraphConfig:
     p_intra: float            # default Knob-2 value of the config
     gen_seed: int
     kind: str = "dcsbm"       # "sbm" (plain stochastic block model) or "dcsbm"
+    # features from a counter-based hash, generated on the GPU (the 57-GB papers100M table is
+    # never materialised on the host); rows for the oracle come from the same formula in numpy
+    device_features: bool = False
 
 
 _S = 250418082  # gen_seed base; + config index
@@ -44,7 +47,8 @@ CONFIGS = {
                             100, 196_615, 1024, (15, 10, 5), 0.5, _S + 3),
     # configs[4]: ogbn-papers100M shape (Table 2 row 4)
     "papers100m": GraphConfig("papers100m", 111_059_956, 3_228_124_712, 65_536, (256, 262_144),
-                              0.2, 128, 128, 1_207_179, 1024, (15, 10, 5), 0.5, _S + 4),
+                              0.2, 128, 128, 1_207_179, 1024, (15, 10, 5), 0.5, _S + 4,
+                              device_features=True),
 }
 
 

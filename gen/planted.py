@@ -178,12 +178,43 @@ def _dcsbm(cfg: GraphConfig, comm: np.ndarray, sizes: np.ndarray, seed_rng):
     return indptr, indices, {"stub_scale": scale, "iterations": it + 1, "nnz_rel_err": err}
 
 
+_SM_GAMMA = 0x9E3779B97F4A7C15
+_SM_M1 = 0xBF58476D1CE4E5B9
+_SM_M2 = 0x94D049BB133111EB
+
+
+def hash_features(cfg: GraphConfig, rows: np.ndarray) -> np.ndarray:
+    """Counter-based features (cfg.device_features): k = splitmix64(key(v, j)) >> 40,
+    key = gen_seed * GAMMA + v * F + j (mod 2^64); X[v, j] = k * 2^-23 - 1.  The same formula
+    runs on the GPU in ``gen.device.device_features``."""
+    rows = np.asarray(rows, dtype=np.uint64)
+    f = cfg.feat_dim
+    out = np.zeros((rows.shape[0], cfg.feat_ld), dtype=np.float32)
+    with np.errstate(over="ignore"):
+        base = np.uint64(cfg.gen_seed) * np.uint64(_SM_GAMMA)
+        z = base + rows[:, None] * np.uint64(f) + np.arange(f, dtype=np.uint64)[None, :]
+        z = z + np.uint64(_SM_GAMMA)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(_SM_M1)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(_SM_M2)
+        z = z ^ (z >> np.uint64(31))
+    k = (z >> np.uint64(40)).astype(np.float32)
+    out[:, :f] = k * np.float32(2.0 ** -23) - np.float32(1.0)
+    return out
+
+
 def make_features(cfg: GraphConfig, rows: Optional[np.ndarray] = None) -> np.ndarray:
     """X[v, j] = k * 2^-23 - 1, k ~ U[0, 2^24) (exact fp32 in [-1, 1)); pad columns zero.
 
     Generated in row chunks from a chunk-keyed stream so any row range can be
     regenerated independently.  ``rows`` (optional) selects rows."""
     n, f, ld = cfg.num_nodes, cfg.feat_dim, cfg.feat_ld
+    if cfg.device_features:
+        if rows is None:
+            rows = np.arange(n, dtype=np.int64)
+        out = np.zeros((len(rows), ld), dtype=np.float32)
+        for i in range(0, len(rows), 1 << 18):
+            out[i: i + (1 << 18)] = hash_features(cfg, rows[i: i + (1 << 18)])
+        return out
     chunk = 1 << 16
     if rows is None:
         out = np.zeros((n, ld), dtype=np.float32)
@@ -244,6 +275,14 @@ def generate(cfg: GraphConfig, features: bool = True, cache: bool = True) -> Bun
                 np.save(os.path.join(d, k + ".npy"), getattr(b, k))
             np.save(os.path.join(d, "meta.npy"), np.array(meta, dtype=object))
             open(os.path.join(d, "done"), "w").close()
-    if features:
+    if features and not cfg.device_features:
         b.X = make_features(cfg)
     return b
+
+
+def feature_rows(bundle: Bundle, rows) -> np.ndarray:
+    """X[rows, :F] of the bundle's table (host), also for device-generated tables."""
+    cfg = bundle.cfg
+    if bundle.X is not None:
+        return bundle.X[np.asarray(rows, dtype=np.int64), : cfg.feat_dim]
+    return make_features(cfg, np.asarray(rows, dtype=np.int64))[:, : cfg.feat_dim]

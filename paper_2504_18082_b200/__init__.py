@@ -184,7 +184,11 @@ class Graph:
 
     @classmethod
     def from_bundle(cls, bundle, device="cuda", features=True, validate=True):
-        X = torch.from_numpy(bundle.X) if (features and bundle.X is not None) else None
+        """features: True (the bundle's host table), False, or a ready [N, ld] tensor."""
+        if isinstance(features, torch.Tensor):
+            X = features
+        else:
+            X = torch.from_numpy(bundle.X) if (features and bundle.X is not None) else None
         return cls(torch.from_numpy(bundle.indptr), torch.from_numpy(bundle.indices),
                    torch.from_numpy(bundle.comm), bundle.cfg.num_communities, X,
                    bundle.cfg.feat_dim if X is not None else None, validate, device)
