@@ -52,7 +52,7 @@ def lib():
         L.or_graph_prep.restype = ctypes.c_int
         L.or_order_roots.argtypes = [I64, P, P, I32, I32, D, U64, U32, P]
         L.or_order_roots.restype = ctypes.c_int
-        L.or_sample_hop.argtypes = [P, I64, P, P, P, P, I32, D, U64, I32, U32, P, P, I64]
+        L.or_sample_hop.argtypes = [P, I64, P, P, P, P, I32, D, U64, I32, U32, P, P, I64, I32]
         L.or_sample_hop.restype = I64
         L.or_relabel_hop.argtypes = [P, I64, I64, P, I64, P, P]
         L.or_relabel_hop.restype = I64
@@ -122,14 +122,17 @@ def batch_roots(order: np.ndarray, batch_size: int, b: int) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- a2
-def sample_hop(prep: Prep, dst_nodes, fanout, p, seed, hop, batch):
+LAW_A, LAW_SLOT = 0, 1   # Knob-2 laws: successive weighted w/o replacement (R1) / slot (R23)
+
+
+def sample_hop(prep: Prep, dst_nodes, fanout, p, seed, hop, batch, law=LAW_A):
     d = _c(dst_nodes, np.int32)
     cap = d.shape[0] * int(fanout)
     indptr_h = np.zeros(d.shape[0] + 1, dtype=np.int64)
     nbr = np.zeros(max(1, cap), dtype=np.int32)
     e = lib().or_sample_hop(_p(d), d.shape[0], _p(prep.indptr), _p(prep.indices), _p(prep.lo),
                             _p(prep.hi), int(fanout), float(p), int(seed), int(hop), int(batch),
-                            _p(indptr_h), _p(nbr), cap)
+                            _p(indptr_h), _p(nbr), cap, int(law))
     assert e >= 0
     return indptr_h, nbr[:e]
 
@@ -148,7 +151,7 @@ def relabel_hop(nodes_prefix, nbr, num_nodes, scratch=None):
     return nodes[:n_next], local[: nb.shape[0]]
 
 
-def sample_blocks(prep: Prep, roots, fanouts, p, seed, batch, scratch=None):
+def sample_blocks(prep: Prep, roots, fanouts, p, seed, batch, scratch=None, law=LAW_A):
     """Alg. 1 lines 4-5 for one batch: hop h = 0..L-1 expands nodes[0:n_h).
 
     Returns dict: nodes (nested prefixes), n (list n_0..n_L), e (list e_0..e_{L-1}),
@@ -158,7 +161,7 @@ def sample_blocks(prep: Prep, roots, fanouts, p, seed, batch, scratch=None):
     if scratch is None:
         scratch = np.full(prep.num_nodes, -1, dtype=np.int32)
     for h, f in enumerate(fanouts):
-        ip, nbr = sample_hop(prep, nodes, f, p, seed, h, batch)
+        ip, nbr = sample_hop(prep, nodes, f, p, seed, h, batch, law)
         nodes, local = relabel_hop(nodes, nbr, prep.num_nodes, scratch)
         indptr.append(ip)
         indices.append(local)
@@ -192,9 +195,9 @@ def sage_mean(indptr_h, idx, Xsrc, F=None, src_map=None):
     return out, out64
 
 
-def run_batch(prep: Prep, X, F, roots, fanouts, p, seed, batch, scratch=None):
+def run_batch(prep: Prep, X, F, roots, fanouts, p, seed, batch, scratch=None, law=LAW_A):
     """One whole hot-path step (a2-a5) for one batch, as the oracle defines it."""
-    blk = sample_blocks(prep, roots, fanouts, p, seed, batch, scratch)
+    blk = sample_blocks(prep, roots, fanouts, p, seed, batch, scratch, law)
     L = len(fanouts)
     Xin = gather(blk["nodes"], X, F)
     H, H64 = sage_mean(blk["indptr"][L - 1], blk["indices"][L - 1], Xin, F)

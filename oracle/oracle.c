@@ -202,6 +202,12 @@ int or_order_roots(int64_t n_train, const int32_t *train, const int32_t *comm, i
  *            and a uniform (f-K)-subset of the inter positions from
  *            r23(W_{K+t}) (Floyd's algorithm, Bentley & Floyd CACM 1987)
  *   picks are emitted in ascending row position (reading R8).
+ * law = 1 selects the SLOT law instead (the north_star's
+ * literal "takes an intra-community neighbour with probability p_intra"; reading R23):
+ *   take-all as above; else slot s < f is intra iff unif(r01(W_s), 65536) < P16,
+ *   K_draw = number of intra slots, K = min(K_draw, ni_e), kb = min(f - K_draw, no_e)
+ *   (no refill: a row may return fewer than f picks), then the same Floyd steps:
+ *   intra subset from r23(W_t), t < K, inter subset from r23(W_{K+t}), t < kb.
  * Returns e_h (total picks) or -1 when cap is exceeded. */
 static int cmp_u32(const void *a, const void *b) {
     uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
@@ -217,7 +223,7 @@ static int contains(const uint32_t *set, int64_t n, uint32_t x) {
 int64_t or_sample_hop(const int32_t *dst_nodes, int64_t n_dst, const int64_t *indptr,
                       const int32_t *indices, const uint32_t *lo, const uint32_t *hi, int32_t fanout,
                       double p, uint64_t seed, int32_t hop, uint32_t batch, int64_t *indptr_h,
-                      int32_t *nbr, int64_t cap) {
+                      int32_t *nbr, int64_t cap, int32_t law) {
     const uint64_t P16 = (uint64_t)(p * 65536.0 + 0.5);
     const uint64_t wi = P16, wo = 65536u - P16;
     const int64_t f = fanout;
@@ -245,16 +251,27 @@ int64_t or_sample_hop(const int32_t *dst_nodes, int64_t n_dst, const int64_t *in
             }
         } else {
             for (int64_t s = 0; s < f; ++s) draw(seed, (uint32_t)s, (uint32_t)v, TAG_SAMPLE, (uint32_t)hop, batch, W[s]);
-            /* urn: number of intra picks K */
-            int64_t ri = ni_e, ro = no_e, K = 0;
-            for (int64_t s = 0; s < f; ++s) {
-                uint64_t T = wi * (uint64_t)ri + wo * (uint64_t)ro;
-                if (or_mulhi64(r01(W[s]), T) < wi * (uint64_t)ri) {
-                    K++;
-                    ri--;
-                } else {
-                    ro--;
+            int64_t K = 0, kb = 0;
+            if (law == 1) {
+                /* slot law: K_draw intra slots, then clip each class (no refill) */
+                int64_t k_draw = 0;
+                for (int64_t s = 0; s < f; ++s)
+                    if (or_mulhi64(r01(W[s]), 65536u) < P16) k_draw++;
+                K = k_draw < ni_e ? k_draw : ni_e;
+                kb = (f - k_draw) < no_e ? (f - k_draw) : no_e;
+            } else {
+                /* urn: number of intra picks K */
+                int64_t ri = ni_e, ro = no_e;
+                for (int64_t s = 0; s < f; ++s) {
+                    uint64_t T = wi * (uint64_t)ri + wo * (uint64_t)ro;
+                    if (or_mulhi64(r01(W[s]), T) < wi * (uint64_t)ri) {
+                        K++;
+                        ri--;
+                    } else {
+                        ro--;
+                    }
                 }
+                kb = f - K;
             }
             /* Floyd: uniform K-subset of [0, ni_e) */
             int64_t na = 0;
@@ -265,8 +282,8 @@ int64_t or_sample_hop(const int32_t *dst_nodes, int64_t n_dst, const int64_t *in
                 intra_set[na] = pick;
                 na++;
             }
-            /* Floyd: uniform (f-K)-subset of [0, no_e) */
-            int64_t nb = 0, kb = f - K;
+            /* Floyd: uniform kb-subset of [0, no_e) */
+            int64_t nb = 0;
             for (int64_t t = 0; t < kb; ++t) {
                 uint64_t j = (uint64_t)(no_e - kb + t);
                 uint32_t r = (uint32_t)or_mulhi64(r23(W[K + t]), j + 1);

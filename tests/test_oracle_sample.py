@@ -39,14 +39,14 @@ def exact_set_law(weights, f):
     return law
 
 
-def _sample_sets(intra, left, right, f, p, nbatch, hop=0):
+def _sample_sets(intra, left, right, f, p, nbatch, hop=0, law=oracle.LAW_A):
     ip, ix, comm, C, hub = star_graph(intra, left, right)
     prep = oracle.Prep(ip, ix, comm, C)
     assert prep.status == 0
     row = ix[ip[hub]: ip[hub + 1]]
     out = {}
     for b in range(nbatch):
-        iph, nbr = oracle.sample_hop(prep, np.array([hub], np.int32), f, p, 42, hop, b)
+        iph, nbr = oracle.sample_hop(prep, np.array([hub], np.int32), f, p, 42, hop, b, law)
         key = tuple(np.searchsorted(row, nbr).tolist())   # row positions of the picks
         out[key] = out.get(key, 0) + 1
     return out, row, comm, hub
@@ -179,3 +179,79 @@ def test_batch_and_hop_keying():
     x = oracle.sample_hop(prep, np.array([hub], np.int32), 3, 0.7, 42, 1, 1)[1]
     y = oracle.sample_hop(prep, np.array([hub], np.int32), 3, 0.7, 42, 1, 1)[1]
     assert np.array_equal(x, y)
+
+
+# ------------------------------------------------------------------ slot law (NEXT-2 (i), R23)
+def exact_slot_law(is_intra, f, p):
+    """P(selected set) under the slot law, from its definition (a different computation from
+    the oracle's loop): K_draw ~ Binomial(f, P16/65536) (each slot intra independently, the
+    16-bit comparison being exact); K = min(K_draw, ni), kb = min(f - K_draw, no); the intra
+    and inter subsets are uniform of those sizes.  Take-all when f >= ni_e + no_e."""
+    from math import comb
+    wi, wo = _p16(p)
+    ni = sum(is_intra) if wi else 0
+    no = (len(is_intra) - sum(is_intra)) if wo else 0
+    elig = [i for i, x in enumerate(is_intra) if (x and wi) or (not x and wo)]
+    if f >= ni + no:
+        return {tuple(elig): 1.0}
+    q = wi / 65536.0
+    intra = [i for i, x in enumerate(is_intra) if x]
+    inter = [i for i, x in enumerate(is_intra) if not x]
+    law = {}
+    for kd in range(f + 1):
+        pk = comb(f, kd) * q ** kd * (1 - q) ** (f - kd)
+        if pk == 0:
+            continue
+        K, kb = min(kd, ni), min(f - kd, no)
+        subsets = [(a, b) for a in itertools.combinations(intra if wi else [], K)
+                   for b in itertools.combinations(inter if wo else [], kb)]
+        for a, b in subsets:
+            key = tuple(sorted(a + b))
+            law[key] = law.get(key, 0.0) + pk / len(subsets)
+    return law
+
+
+@pytest.mark.parametrize("intra,left,right,f,p", [
+    (2, 2, 1, 2, 0.9), (3, 1, 2, 3, 0.7), (2, 2, 2, 2, 0.5), (1, 2, 2, 3, 0.6), (4, 1, 1, 3, 1.0),
+    (1, 3, 2, 3, 1.0), (2, 1, 1, 3, 0.0), (3, 2, 2, 4, 0.25)])
+def test_slot_law_exact(intra, left, right, f, p):
+    n = 20000
+    obs, row, comm, hub = _sample_sets(intra, left, right, f, p, n, law=oracle.LAW_SLOT)
+    law = exact_slot_law([comm[u] == comm[hub] for u in row], f, p)
+    assert abs(sum(law.values()) - 1) < 1e-12
+    assert _chi2_pvalue(obs, law, n) > 1e-4
+
+
+def test_slot_law_p1_returns_fewer_than_f():
+    # 1 intra + 4 inter neighbours, f = 3 < m: p = 1 -> the single intra neighbour only
+    obs, row, comm, hub = _sample_sets(1, 2, 2, 3, 1.0, 200, law=oracle.LAW_SLOT)
+    assert list(obs) == [tuple(i for i, u in enumerate(row) if comm[u] == comm[hub])]
+
+
+def test_slot_law_intra_count_is_binomial():
+    # ample neighbours in both classes: #intra picks = K_draw ~ Binomial(f, P16 / 65536)
+    f, p, n = 5, 0.7, 20000
+    obs, row, comm, hub = _sample_sets(12, 6, 6, f, p, n, law=oracle.LAW_SLOT)
+    cnt = np.zeros(f + 1)
+    for key, c in obs.items():
+        assert len(key) == f
+        cnt[sum(comm[row[i]] == comm[hub] for i in key)] += c
+    wi, _ = _p16(p)
+    exp = stats.binom.pmf(np.arange(f + 1), f, wi / 65536.0) * n
+    assert stats.chisquare(cnt, exp).pvalue > 1e-4
+
+
+def test_slot_law_take_all_and_same_words_as_law_a():
+    # f >= m: both laws take the whole eligible row; and at p = 1 with enough intra
+    # neighbours both laws pick f intra positions from the same words (the urn is
+    # then all-intra too), so the two laws coincide exactly there
+    ip, ix, comm, C, hub = star_graph(20, 3, 3)
+    prep = oracle.Prep(ip, ix, comm, C)
+    d = np.array([hub], np.int32)
+    for b in range(50):
+        a = oracle.sample_hop(prep, d, 40, 0.7, 42, 0, b, oracle.LAW_A)
+        s_ = oracle.sample_hop(prep, d, 40, 0.7, 42, 0, b, oracle.LAW_SLOT)
+        assert np.array_equal(a[1], s_[1])
+        a = oracle.sample_hop(prep, d, 5, 1.0, 42, 1, b, oracle.LAW_A)
+        s_ = oracle.sample_hop(prep, d, 5, 1.0, 42, 1, b, oracle.LAW_SLOT)
+        assert np.array_equal(a[1], s_[1])
