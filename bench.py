@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--no-extra", action="store_true", help="skip the knob-sweep extra points")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--law", default="A", choices=["A", "slot"],
+                    help="Knob-2 law: A = weighted w/o replacement (default), slot = R23")
     ap.add_argument("--flush-l2", default="auto", choices=["auto", "on", "off"],
                     help="write 256 MB before every launch group and time only the groups "
                          "(auto: on when features + CSR < 4x L2)")
@@ -136,7 +138,7 @@ def algorithmic_bytes(n, e, F, L):
 
 
 # ------------------------------------------------------------------ cpu (oracle) legs
-def oracle_step(prep, bundle, roots, p, seed, batch, scratch):
+def oracle_step(prep, bundle, roots, p, seed, batch, scratch, law=0):
     """One oracle batch (a2-a5).  For device-generated feature tables the gathered rows come
     from the generator's row formula (X[nodes] by definition), then the oracle's a5."""
     import oracle
@@ -144,16 +146,16 @@ def oracle_step(prep, bundle, roots, p, seed, batch, scratch):
     cfg = bundle.cfg
     if bundle.X is not None:
         return oracle.run_batch(prep, bundle.X, cfg.feat_dim, roots, cfg.fanouts, p, seed, batch,
-                                scratch)
+                                scratch, law)
     L = len(cfg.fanouts)
-    blk = oracle.sample_blocks(prep, roots, cfg.fanouts, p, seed, batch, scratch)
+    blk = oracle.sample_blocks(prep, roots, cfg.fanouts, p, seed, batch, scratch, law)
     Xin = np.ascontiguousarray(feature_rows(bundle, blk["nodes"]))
     H, H64 = oracle.sage_mean(blk["indptr"][L - 1], blk["indices"][L - 1], Xin, cfg.feat_dim)
     blk.update({"X_in": Xin, "H": H, "H64": H64})
     return blk
 
 
-def oracle_batches(bundle, mode, mix, p, seed, budget_s, max_batches=None):
+def oracle_batches(bundle, mode, mix, p, seed, budget_s, max_batches=None, law=0):
     """Times the oracle (as it stands, single thread) on consecutive batches of epoch 0."""
     import oracle
     cfg = bundle.cfg
@@ -167,7 +169,7 @@ def oracle_batches(bundle, mode, mix, p, seed, budget_s, max_batches=None):
     done, edges = 0, 0
     while True:
         r = oracle_step(prep, bundle, oracle.batch_roots(order, cfg.batch_size, done % nb), p,
-                        seed, done % nb, scratch)
+                        seed, done % nb, scratch, law)
         edges += sum(r["e"])
         done += 1
         el = time.perf_counter() - t0
@@ -193,7 +195,7 @@ def run_reference(args, bundle):
 
     def step(b):
         return oracle_step(prep, bundle, oracle.batch_roots(order, cfg.batch_size, b % nb), p,
-                           args.seed, b % nb, scratch)
+                           args.seed, b % nb, scratch, 0 if args.law == "A" else 1)
 
     for w in range(args.warmup):
         step(w)
@@ -231,7 +233,7 @@ def workload_config(args, cfg, bundle, p, flush=False):
             "num_nodes": cfg.num_nodes, "nnz": int(bundle.nnz), "feat_dim": cfg.feat_dim,
             "batch": cfg.batch_size, "fanouts_hop_order": list(cfg.fanouts),
             "knob1": args.mode + (f"(k={args.mix})" if args.mode == "comm" else ""),
-            "p_intra": p, "seed": args.seed,
+            "p_intra": p, "knob2_law": args.law, "seed": args.seed,
             "l2": ("L2 flushed (256 MB write) before every launch group of %d batches; "
                    "ms = sum of the groups' device events (X %.0f MB, CSR %.0f MB)"
                    % (args.batches_per_launch, cfg.num_nodes * cfg.feat_ld * 4 / 1e6,
@@ -276,7 +278,7 @@ def run_cmb(args, bundle):
     G = max(1, min(args.batches_per_launch, cmb.MAX_BATCHES_PER_LAUNCH))
     pipe = cmb.BatchedPipeline(graph, torch.from_numpy(bundle.train), cfg.batch_size,
                                cfg.fanouts, mode=args.mode, mix=args.mix, p=p, seed=args.seed,
-                               nb=G)
+                               nb=G, law=args.law)
     nb = pipe.n_batches
     stream = torch.cuda.current_stream()
     K, W = args.steps, args.warmup
@@ -356,7 +358,8 @@ def run_cmb(args, bundle):
         traffic = ncu_traffic(cfg.name, knob)
         cpu = None
         if world == 1:
-            done, el, ed = oracle_batches(bundle, args.mode, args.mix, p, args.seed, args.cpu_seconds)
+            done, el, ed = oracle_batches(bundle, args.mode, args.mix, p, args.seed, args.cpu_seconds,
+                                          law=0 if args.law == "A" else 1)
             cpu = {"value": done / el, "unit": "batches/s", "cores": 1, "kind": "oracle",
                    "sample": f"first {done} batches of epoch 0 of the same workload/knobs "
                              f"({el:.1f} s, single-threaded plain-C oracle, a1 included)"}

@@ -173,6 +173,23 @@ CMB_API cmb_status cmb_sample_blocks(const cmb_graph* g, const int32_t* roots, i
                              uint32_t batch_id, cmb_blocks* out, void* workspace,
                              size_t workspace_bytes, void* stream);
 
+/* Knob-2 laws.  CMB_LAW_A (default of cmb_sample_blocks): successive weighted sampling without
+ * replacement with per-edge weights P16 / 65536 - P16 (DGL NeighborSampler(prob=...);
+ * reading R1).  CMB_LAW_SLOT (reading R23, the north_star's literal
+ * "takes an intra-community neighbour with probability p_intra"): take-all first; else each of
+ * the f slots is intra iff unif(r01(W_s), 65536) < P16, the K_draw intra slots take
+ * min(K_draw, ni_e) distinct intra neighbours and the rest min(f - K_draw, no_e) distinct inter
+ * ones (no refill: a row may return fewer than f picks), with the same Philox words and Floyd
+ * steps as law A. */
+typedef enum { CMB_LAW_A = 0, CMB_LAW_SLOT = 1 } cmb_sample_law;
+
+/* cmb_sample_blocks under an explicit law (CMB_INVALID_ARGUMENT for an unknown law). */
+CMB_API cmb_status cmb_sample_blocks_law(const cmb_graph* g, const int32_t* roots, int64_t n_roots,
+                                         const int32_t* fanouts, int32_t n_hops, double p_intra,
+                                         int32_t law, uint64_t seed, uint32_t batch_id,
+                                         cmb_blocks* out, void* workspace, size_t workspace_bytes,
+                                         void* stream);
+
 /* Several independent batches in ONE launch (up to CMB_MAX_BATCHES_PER_LAUNCH): the SMs are
  * split evenly between the batches, which run the same phases concurrently, so the latency-
  * bound phases of small hops overlap across batches.  Each batch has its own roots, batch id,
@@ -189,8 +206,8 @@ typedef struct {
 } cmb_batch;
 CMB_API cmb_status cmb_sample_blocks_multi(const cmb_graph* g, const cmb_batch* batches,
                                            int32_t n_batches, const int32_t* fanouts,
-                                           int32_t n_hops, double p_intra, uint64_t seed,
-                                           void* stream);
+                                           int32_t n_hops, double p_intra, int32_t law,
+                                           uint64_t seed, void* stream);
 
 /* ------------------------------------------------------------------ a4 / a5 */
 /* a4: out[i, 0:F] = features[node_ids[i], 0:F] for i < *n_dev (device count; rows

@@ -39,7 +39,8 @@ STATUS = {0: "CMB_OK", 1: "CMB_ERR_INVALID_ARGUMENT", 2: "CMB_ERR_INVALID_GRAPH"
 # C ABI symbols (include/cmb.h); tests check the library exports all of them.
 SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb_graph_arrays",
            "cmb_order_roots_workspace_bytes", "cmb_order_roots", "cmb_blocks_capacity",
-           "cmb_sample_workspace_bytes", "cmb_sample_blocks", "cmb_sample_blocks_multi",
+           "cmb_sample_workspace_bytes", "cmb_sample_blocks", "cmb_sample_blocks_law",
+           "cmb_sample_blocks_multi",
            "cmb_gather_features",
            "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_shard_plan_workspace_bytes",
            "cmb_shard_plan", "cmb_gather_rows", "cmb_scatter_rows", "cmb_get_device_status",
@@ -75,6 +76,13 @@ class Batch(ctypes.Structure):
 
 
 MAX_BATCHES_PER_LAUNCH = 4
+LAW_A, LAW_SLOT = 0, 1  # Knob-2 laws (include/cmb.h cmb_sample_law)
+
+
+def _law(law) -> int:
+    if isinstance(law, str):
+        return {"a": LAW_A, "slot": LAW_SLOT}[law.lower()]
+    return int(law)
 _lib = None
 
 
@@ -100,7 +108,10 @@ def lib():
             "cmb_sample_workspace_bytes": (SZ, [I64, P, I32, I64]),
             "cmb_sample_blocks": (I32, [P, P, I64, P, I32, D, U64, U32, ctypes.POINTER(Blocks), P,
                                         SZ, P]),
-            "cmb_sample_blocks_multi": (I32, [P, ctypes.POINTER(Batch), I32, P, I32, D, U64, P]),
+            "cmb_sample_blocks_law": (I32, [P, P, I64, P, I32, D, I32, U64, U32,
+                                            ctypes.POINTER(Blocks), P, SZ, P]),
+            "cmb_sample_blocks_multi": (I32, [P, ctypes.POINTER(Batch), I32, P, I32, D, I32, U64,
+                                              P]),
             "cmb_gather_features": (I32, [P, P, P, I64, P, I64, P]),
             "cmb_sage_mean_aggregate": (I32, [P, P, P, I64, P, I64, P, I32, P, I64, P]),
             "cmb_gather_aggregate": (I32, [P, ctypes.POINTER(Blocks), I32, I64, I64, P, I64, P,
@@ -303,13 +314,22 @@ class Sampler:
         self.x_in = None
         self.h = None
 
-    def sample(self, roots: torch.Tensor, p: float, seed: int, batch_id: int) -> BatchView:
+    def sample(self, roots: torch.Tensor, p: float, seed: int, batch_id: int,
+               law=LAW_A) -> BatchView:
         n = int(roots.shape[0])
         if n > self.max_roots:
             raise ValueError("more roots than max_roots")
-        _check(lib().cmb_sample_blocks(self.graph.handle, _ptr(roots), n, self._f, self.L,
-                                       float(p), int(seed), int(batch_id), ctypes.byref(self._blocks),
-                                       _ptr(self.workspace), self.workspace.numel(), _stream()))
+        lw = _law(law)
+        if lw == LAW_A:
+            _check(lib().cmb_sample_blocks(self.graph.handle, _ptr(roots), n, self._f, self.L,
+                                           float(p), int(seed), int(batch_id),
+                                           ctypes.byref(self._blocks), _ptr(self.workspace),
+                                           self.workspace.numel(), _stream()))
+        else:
+            _check(lib().cmb_sample_blocks_law(self.graph.handle, _ptr(roots), n, self._f,
+                                               self.L, float(p), lw, int(seed), int(batch_id),
+                                               ctypes.byref(self._blocks), _ptr(self.workspace),
+                                               self.workspace.numel(), _stream()))
         return BatchView(self.nodes, self.sizes, self.indptr, self.indices, self.mask)
 
     def batch_desc(self, roots: torch.Tensor, batch_id: int) -> "Batch":
@@ -341,7 +361,7 @@ class Sampler:
 
 
 def sample_multi(samplers: Sequence["Sampler"], roots: Sequence[torch.Tensor],
-                 batch_ids: Sequence[int], p: float, seed: int):
+                 batch_ids: Sequence[int], p: float, seed: int, law=LAW_A):
     """a2+a3 for up to 4 independent batches in ONE launch (cmb_sample_blocks_multi); the
     samplers must share graph and fanouts and own distinct workspaces."""
     s0 = samplers[0]
@@ -349,8 +369,8 @@ def sample_multi(samplers: Sequence["Sampler"], roots: Sequence[torch.Tensor],
     if not (1 <= n <= MAX_BATCHES_PER_LAUNCH) or len(roots) != n or len(batch_ids) != n:
         raise ValueError("1..4 samplers, one roots tensor and batch id each")
     arr = (Batch * n)(*[s.batch_desc(r, b) for s, r, b in zip(samplers, roots, batch_ids)])
-    _check(lib().cmb_sample_blocks_multi(s0.graph.handle, arr, n, s0._f, s0.L, float(p), int(seed),
-                                         _stream()))
+    _check(lib().cmb_sample_blocks_multi(s0.graph.handle, arr, n, s0._f, s0.L, float(p),
+                                         _law(law), int(seed), _stream()))
     return [BatchView(s.nodes, s.sizes, s.indptr, s.indices, s.mask) for s in samplers]
 
 
@@ -378,8 +398,9 @@ class MiniBatchPipeline:
     the fused input-feature gather + SAGE-mean aggregation (a4, a5)."""
 
     def __init__(self, graph: Graph, train, batch_size: int, fanouts: Sequence[int],
-                 mode="rand", mix=0.0, p=0.5, seed=42):
+                 mode="rand", mix=0.0, p=0.5, seed=42, law=LAW_A):
         self.graph = graph
+        self.law = _law(law)
         self.orderer = RootOrderer(graph, train)
         self.batch_size = int(batch_size)
         self.n_batches = (self.orderer.n + self.batch_size - 1) // self.batch_size
@@ -402,7 +423,7 @@ class MiniBatchPipeline:
             if self.epoch != epoch:
                 self.start_epoch(epoch)
             roots = self.batch_roots(b)
-        view = self.sampler.sample(roots, self.p, self.seed, int(global_batch))
+        view = self.sampler.sample(roots, self.p, self.seed, int(global_batch), self.law)
         x_in, h = self.sampler.gather_aggregate()
         return view, x_in, h
 
@@ -413,8 +434,8 @@ class BatchedPipeline(MiniBatchPipeline):
     fused gather + aggregate of each batch.  Same bytes as the sequential pipeline."""
 
     def __init__(self, graph: Graph, train, batch_size: int, fanouts: Sequence[int],
-                 mode="rand", mix=0.0, p=0.5, seed=42, nb: int = 2):
-        super().__init__(graph, train, batch_size, fanouts, mode, mix, p, seed)
+                 mode="rand", mix=0.0, p=0.5, seed=42, nb: int = 2, law=LAW_A):
+        super().__init__(graph, train, batch_size, fanouts, mode, mix, p, seed, law)
         self.nb = int(nb)
         self.samplers = [self.sampler] + [Sampler(graph, self.batch_size, fanouts)
                                           for _ in range(self.nb - 1)]
@@ -442,7 +463,7 @@ class BatchedPipeline(MiniBatchPipeline):
         if timing:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-        sample_multi(ss, roots, gbs, self.p, self.seed)
+        sample_multi(ss, roots, gbs, self.p, self.seed, self.law)
         if timing:
             e1.record()
             events["sample"] = (e0, e1)
@@ -464,8 +485,8 @@ class OverlappedPipeline(MiniBatchPipeline):
     `s_gather`) streams features.  Outputs are `depth`-buffered; events order the reuse."""
 
     def __init__(self, graph: Graph, train, batch_size: int, fanouts: Sequence[int],
-                 mode="rand", mix=0.0, p=0.5, seed=42, depth: int = 2):
-        super().__init__(graph, train, batch_size, fanouts, mode, mix, p, seed)
+                 mode="rand", mix=0.0, p=0.5, seed=42, depth: int = 2, law=LAW_A):
+        super().__init__(graph, train, batch_size, fanouts, mode, mix, p, seed, law)
         self.depth = int(depth)
         self.samplers = [self.sampler] + [Sampler(graph, self.batch_size, fanouts)
                                           for _ in range(self.depth - 1)]
@@ -488,7 +509,7 @@ class OverlappedPipeline(MiniBatchPipeline):
                 if self.epoch != epoch:
                     self.start_epoch(epoch)
                 roots = self.batch_roots(b)
-            s.sample(roots, self.p, self.seed, gb)
+            s.sample(roots, self.p, self.seed, gb, self.law)
             self.ev_sampled[j].record(self.s_sample)
         with torch.cuda.stream(self.s_gather):
             self.s_gather.wait_event(self.ev_sampled[j])

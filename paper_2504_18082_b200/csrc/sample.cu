@@ -58,7 +58,7 @@ int sampler_threads() {
 
 void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t n_roots,
                const int32_t* fanouts, int L, uint32_t wi, uint32_t wo, uint32_t k0, uint32_t k1,
-               uint32_t batch_id, const cmb_blocks* out, const SampleWs& w) {
+               uint32_t batch_id, const cmb_blocks* out, const SampleWs& w, int law) {
   a.g = g->d;
   a.roots = roots;
   a.n_roots = n_roots;
@@ -93,6 +93,7 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
     return e ? std::atoi(e) : 0;
   }();
   a.dedup = dedup;
+  a.law = law;
 }
 
 cmb_status launch_persistent(const cmb_graph* g, pst::PMulti& m, cudaStream_t s) {
@@ -167,7 +168,7 @@ size_t cmb_sample_workspace_bytes(int64_t n_roots, const int32_t* fanouts, int32
 
 cmb_status cmb_sample_blocks_multi(const cmb_graph* g, const cmb_batch* batches,
                                    int32_t n_batches, const int32_t* fanouts, int32_t n_hops,
-                                   double p_intra, uint64_t seed, void* stream) {
+                                   double p_intra, int32_t law, uint64_t seed, void* stream) {
   CMB_ARG(g && batches && fanouts, "cmb_sample_blocks: null graph/batches/fanouts");
   CMB_ARG(n_batches >= 1 && n_batches <= CMB_MAX_BATCHES_PER_LAUNCH,
           "cmb_sample_blocks_multi: n_batches %d outside [1, %d]", n_batches,
@@ -175,6 +176,7 @@ cmb_status cmb_sample_blocks_multi(const cmb_graph* g, const cmb_batch* batches,
   CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_sample_blocks: n_hops %d outside [1,%d]",
           n_hops, CMB_MAX_HOPS);
   CMB_ARG(p_intra >= 0.0 && p_intra <= 1.0, "cmb_sample_blocks: p_intra outside [0, 1]");
+  CMB_ARG(law == CMB_LAW_A || law == CMB_LAW_SLOT, "cmb_sample_blocks: unknown law %d", law);
   for (int h = 0; h < n_hops; ++h)
     CMB_ARG(fanouts[h] >= 1 && fanouts[h] <= CMB_MAX_FANOUT,
             "cmb_sample_blocks: fanout[%d] = %d outside [1, %d]", h, fanouts[h], CMB_MAX_FANOUT);
@@ -197,7 +199,7 @@ cmb_status cmb_sample_blocks_multi(const cmb_graph* g, const cmb_batch* batches,
     const cmb_batch& b = batches[i];
     SampleWs w = carve_sample_ws(b.workspace, b.n_roots, fanouts, n_hops, g->d.n, nullptr);
     fill_args(m.a[i], g, b.roots, b.n_roots, fanouts, n_hops, wi, wo, k0, k1, b.batch_id, b.out,
-              w);
+              w, law);
     // barrier state + tagged aggregates (contiguous) are cleared for every batch
     CMB_CUDA(cudaMemsetAsync(w.bar, 0,
                              reinterpret_cast<char*>(w.pub + 2 * kMaxPersistBlocks) -
@@ -213,7 +215,16 @@ cmb_status cmb_sample_blocks(const cmb_graph* g, const int32_t* roots, int64_t n
                              size_t workspace_bytes, void* stream) {
   CMB_ARG(g && roots && fanouts && out, "cmb_sample_blocks: null graph/roots/fanouts/out");
   cmb_batch b{roots, n_roots, batch_id, out, workspace, workspace_bytes};
-  return cmb_sample_blocks_multi(g, &b, 1, fanouts, n_hops, p_intra, seed, stream);
+  return cmb_sample_blocks_multi(g, &b, 1, fanouts, n_hops, p_intra, CMB_LAW_A, seed, stream);
+}
+
+cmb_status cmb_sample_blocks_law(const cmb_graph* g, const int32_t* roots, int64_t n_roots,
+                                 const int32_t* fanouts, int32_t n_hops, double p_intra,
+                                 int32_t law, uint64_t seed, uint32_t batch_id, cmb_blocks* out,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  CMB_ARG(g && roots && fanouts && out, "cmb_sample_blocks: null graph/roots/fanouts/out");
+  cmb_batch b{roots, n_roots, batch_id, out, workspace, workspace_bytes};
+  return cmb_sample_blocks_multi(g, &b, 1, fanouts, n_hops, p_intra, law, seed, stream);
 }
 
 }  // extern "C"

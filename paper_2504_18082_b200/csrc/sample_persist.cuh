@@ -69,6 +69,7 @@ struct PArgs {
   uint64_t* prof;           // [kMaxBlocks][64] per-block %globaltimer at sub-step boundaries
   int32_t* status;
   int dedup;                // warp-deduplicate the marks (match_any) before the atomics
+  int law;                  // Knob-2 law: 0 = successive weighted w/o replacement, 1 = slot
 };
 
 // Per-block sub-step timeline (profiling aid, one store per sub-step per block):
@@ -207,13 +208,31 @@ __device__ __forceinline__ bool take_all(int64_t rs, int64_t deg, uint32_t lo, u
   return true;
 }
 
+// slot law (R23): picks of a row with f < m -- K_draw intra slots from the same words the
+// positions step draws, then each class clipped (no refill)
+__device__ __forceinline__ int32_t slot_count(int32_t v, int hop, int f, uint32_t wi,
+                                              int64_t ni_e, int64_t no_e, uint32_t k0,
+                                              uint32_t k1, uint32_t batch) {
+  int kd = 0;
+  for (int s = 0; s < f; ++s) {
+    const PhiloxOut w = philox4x32_10(static_cast<uint32_t>(s), static_cast<uint32_t>(v),
+                                      (kTagSample << 24) | static_cast<uint32_t>(hop), batch,
+                                      k0, k1);
+    kd += (lo64(w) >> 48) < wi;
+  }
+  const int64_t K = kd < ni_e ? kd : ni_e;
+  const int64_t kb = f - kd < no_e ? f - kd : no_e;
+  return static_cast<int32_t>(K + kb);
+}
+
 // G lanes per row (f <= G): lane s owns Philox slot s
 template <int G>
 __device__ __forceinline__ void row_positions_group(int32_t v, int64_t rs, int64_t deg,
                                                     uint32_t lo, uint32_t hi, int hop, int f,
                                                     uint32_t wi, uint32_t wo, uint32_t k0,
                                                     uint32_t k1, uint32_t batch, int lane,
-                                                    unsigned gmask, int64_t* __restrict__ o) {
+                                                    unsigned gmask, int64_t* __restrict__ o,
+                                                    int law) {
   const int64_t ni = static_cast<int64_t>(hi) - lo;
   const int64_t ni_e = wi ? ni : 0, no_e = wo ? deg - ni : 0;
   if (take_all(rs, deg, lo, hi, ni_e, no_e, f, lane, G, o)) return;
@@ -222,36 +241,44 @@ __device__ __forceinline__ void row_positions_group(int32_t v, int64_t rs, int64
     w = philox4x32_10(static_cast<uint32_t>(lane), static_cast<uint32_t>(v),
                       (kTagSample << 24) | static_cast<uint32_t>(hop), batch, k0, k1);
   const uint64_t u01 = lo64(w), u23 = hi64(w);
-  uint64_t ri = static_cast<uint64_t>(ni_e), ro = static_cast<uint64_t>(no_e);
-  int K = 0;
-  for (int s = 0; s < f; ++s) {
-    const uint64_t x = __shfl_sync(gmask, u01, s, G);
-    const uint64_t wri = wi * ri;
-    if (__umul64hi(x, wri + wo * ro) < wri) {
-      ++K;
-      --ri;
-    } else {
-      --ro;
+  int K = 0, kb;
+  if (law == 1) {  // slot law: K_draw intra slots, each class clipped, no refill
+    const int kd = __popc(__ballot_sync(gmask, lane < f && (u01 >> 48) < wi));
+    K = kd < ni_e ? kd : static_cast<int>(ni_e);
+    kb = f - kd < no_e ? f - kd : static_cast<int>(no_e);
+  } else {
+    uint64_t ri = static_cast<uint64_t>(ni_e), ro = static_cast<uint64_t>(no_e);
+    for (int s = 0; s < f; ++s) {
+      const uint64_t x = __shfl_sync(gmask, u01, s, G);
+      const uint64_t wri = wi * ri;
+      if (__umul64hi(x, wri + wo * ro) < wri) {
+        ++K;
+        --ri;
+      } else {
+        --ro;
+      }
     }
+    kb = f - K;
   }
+  const int tot = K + kb;  // picks of this row (f under law A)
   const bool in = lane < K;
   const uint64_t n_cls = in ? static_cast<uint64_t>(ni_e) : static_cast<uint64_t>(no_e);
-  const int k_cls = in ? K : f - K;
+  const int k_cls = in ? K : kb;
   const int t = in ? lane : lane - K;
   const uint32_t j = static_cast<uint32_t>(n_cls - static_cast<uint64_t>(k_cls) + t);
   const uint32_t rr = static_cast<uint32_t>(__umul64hi(u23, static_cast<uint64_t>(j) + 1u));
   uint32_t sel = kEmpty;
-  for (int s = 0; s < f; ++s) {
+  for (int s = 0; s < tot; ++s) {
     const uint32_t rs_ = __shfl_sync(gmask, rr, s, G);
     const bool same_cls = (lane < K) == (s < K);
     const unsigned hit = __ballot_sync(gmask, lane < s && same_cls && sel == rs_);
     if (lane == s) sel = hit ? j : rr;
   }
   uint32_t pos = in ? lo + sel : (sel < lo ? sel : hi + (sel - lo));
-  if (lane >= f) pos = kEmpty;
+  if (lane >= tot) pos = kEmpty;
   int rank = 0;
-  for (int s = 0; s < f; ++s) rank += __shfl_sync(gmask, pos, s, G) < pos;
-  if (lane < f) o[rank] = rs + pos;
+  for (int s = 0; s < tot; ++s) rank += __shfl_sync(gmask, pos, s, G) < pos;
+  if (lane < tot) o[rank] = rs + pos;
 }
 
 // one thread per row (f <= FM): the same draws with every loop statically unrolled over FM
@@ -261,13 +288,13 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
                                                      uint32_t lo, uint32_t hi, int hop, int f,
                                                      uint32_t wi, uint32_t wo, uint32_t k0,
                                                      uint32_t k1, uint32_t batch,
-                                                     int64_t* __restrict__ o) {
+                                                     int64_t* __restrict__ o, int law) {
   const int64_t ni = static_cast<int64_t>(hi) - lo;
   const int64_t ni_e = wi ? ni : 0, no_e = wo ? deg - ni : 0;
   if (take_all(rs, deg, lo, hi, ni_e, no_e, f, 0, 1, o)) return;
   uint64_t r23[FM];
   uint64_t ri = static_cast<uint64_t>(ni_e), ro = static_cast<uint64_t>(no_e);
-  int K = 0;
+  int K = 0, kd = 0;
   const uint32_t c2 = (kTagSample << 24) | static_cast<uint32_t>(hop);
 #pragma unroll
   for (int s = 0; s < FM; ++s) {  // urn over f successive draws; keep r23 of each slot
@@ -276,6 +303,7 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
       const PhiloxOut w = philox4x32_10(static_cast<uint32_t>(s), static_cast<uint32_t>(v), c2,
                                         batch, k0, k1);
       r23[s] = hi64(w);
+      kd += (lo64(w) >> 48) < wi;  // slot law: slot s intra iff unif(r01, 65536) < P16
       const uint64_t wri = wi * ri;
       if (__umul64hi(lo64(w), wri + wo * ro) < wri) {
         ++K;
@@ -285,12 +313,17 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
       }
     }
   }
+  int kb = f - K;
+  if (law == 1) {
+    K = kd < ni_e ? kd : static_cast<int>(ni_e);
+    kb = f - kd < no_e ? f - kd : static_cast<int>(no_e);
+  }
+  const int tot = K + kb;  // picks of this row (f under law A)
   uint32_t pos[FM];
-  const int kb = f - K;
 #pragma unroll
-  for (int s = 0; s < FM; ++s) {  // Floyd: slots [0,K) intra subset, [K,f) inter subset
+  for (int s = 0; s < FM; ++s) {  // Floyd: slots [0,K) intra subset, [K,K+kb) inter subset
     pos[s] = kEmpty;
-    if (s < f) {
+    if (s < tot) {
       const bool in = s < K;
       const uint64_t n_cls = in ? static_cast<uint64_t>(ni_e) : static_cast<uint64_t>(no_e);
       const int k_cls = in ? K : kb;
@@ -305,17 +338,17 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
   }
 #pragma unroll
   for (int s = 0; s < FM; ++s) {  // class offsets -> row positions
-    if (s < f) {
+    if (s < tot) {
       const uint32_t q = pos[s];
       pos[s] = s < K ? lo + q : (q < lo ? q : hi + (q - lo));
     }
   }
 #pragma unroll
   for (int s = 0; s < FM; ++s) {  // ascending emit by rank
-    if (s < f) {
+    if (s < tot) {
       int rank = 0;
 #pragma unroll
-      for (int q = 0; q < FM; ++q) rank += (q < f) && pos[q] < pos[s];
+      for (int q = 0; q < FM; ++q) rank += (q < tot) && pos[q] < pos[s];
       o[rank] = rs + pos[s];
     }
   }
@@ -342,6 +375,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       r = row_info(a.g, v, a.wi, a.wo);
       const int64_t m = r.ni_e + r.no_e;
       c = static_cast<int32_t>(m < f ? m : f);
+      if (a.law == 1 && f < m) c = slot_count(v, h, f, a.wi, r.ni_e, r.no_e, a.k0, a.k1, a.batch);
     }
     int32_t ex, agg;
     cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(c, ex, agg);
@@ -399,10 +433,10 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       a.indptr[h][i] = base + off;
       if (f <= 8)
         row_positions_thread<8>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch,
-                                a.pick + base + off);
+                                a.pick + base + off, a.law);
       else
         row_positions_thread<16>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch,
-                                 a.pick + base + off);
+                                 a.pick + base + off, a.law);
     }
   } else {
     const int lane = threadIdx.x & (G - 1);
@@ -415,7 +449,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       fetch(i, v, rs, deg, rlo, rhi, off);
       if (lane == 0) a.indptr[h][i] = base + off;
       row_positions_group<G>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, lane,
-                             gmask, a.pick + base + off);
+                             gmask, a.pick + base + off, a.law);
     }
   }
   __syncthreads();

@@ -20,8 +20,8 @@ def small():
     return b, oracle.graph_prep(b), cmb.Graph.from_bundle(b)
 
 
-@pytest.mark.parametrize("nb", [2, 3, 4])
-def test_sample_multi_matches_oracle(small, nb):
+@pytest.mark.parametrize("nb,law", [(2, 0), (3, 0), (4, 0), (4, 1)])
+def test_sample_multi_matches_oracle(small, nb, law):
     b, prep, g = small
     fan = (15, 10, 5)
     order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_RAND, 0, SEED, 0)
@@ -29,11 +29,11 @@ def test_sample_multi_matches_oracle(small, nb):
     roots = [torch.from_numpy(oracle.batch_roots(order, 256 - 37 * i, i)).cuda() for i in range(nb)]
     ids = [100 + i for i in range(nb)]
     for rep in range(2):  # a second launch reuses the workspaces (tagged dedup maps)
-        views = cmb.sample_multi(samplers, roots, ids, 0.9, SEED)
+        views = cmb.sample_multi(samplers, roots, ids, 0.9, SEED, law)
         torch.cuda.synchronize()
         for s, v, r, bid in zip(samplers, views, roots, ids):
             assert s.status() == 0
-            ref = oracle.sample_blocks(prep, r.cpu().numpy(), fan, 0.9, SEED, bid)
+            ref = oracle.sample_blocks(prep, r.cpu().numpy(), fan, 0.9, SEED, bid, law=law)
             n, e = v.host_sizes()
             assert n == ref["n"] and e == ref["e"]
             assert np.array_equal(v.nodes[: n[-1]].cpu().numpy(), ref["nodes"])

@@ -40,9 +40,10 @@ def agg_tol_ok(H, H64, Xin, ip, idx):
     return np.all(np.abs(H.astype(np.float64) - H64) <= 1e-5 * np.maximum(np.abs(H64), scale) + 1e-30)
 
 
-def check_batch(bundle, prep, graph, sampler, roots_np, fanouts, p, batch_id, features=True):
+def check_batch(bundle, prep, graph, sampler, roots_np, fanouts, p, batch_id, features=True,
+                law=oracle.LAW_A):
     roots = torch.from_numpy(roots_np).cuda()
-    view = sampler.sample(roots, p, SEED, batch_id)
+    view = sampler.sample(roots, p, SEED, batch_id, law)
     if features:
         x_in, h = sampler.gather_aggregate()
     torch.cuda.synchronize()
@@ -50,9 +51,9 @@ def check_batch(bundle, prep, graph, sampler, roots_np, fanouts, p, batch_id, fe
     L = len(fanouts)
     if features:
         ref = oracle.run_batch(prep, bundle.X, bundle.cfg.feat_dim, roots_np, fanouts, p, SEED,
-                               batch_id)
+                               batch_id, law=law)
     else:
-        ref = oracle.sample_blocks(prep, roots_np, fanouts, p, SEED, batch_id)
+        ref = oracle.sample_blocks(prep, roots_np, fanouts, p, SEED, batch_id, law=law)
     n, e = view.host_sizes()
     assert n == ref["n"], (n, ref["n"])
     assert e == ref["e"], (e, ref["e"])
@@ -140,6 +141,30 @@ def test_products_scaled_knobs(p, fanouts):
                                SEED, 0)
     for bb in (0, 3):
         check_batch(b, prep, g, s, oracle.batch_roots(order, 512, bb), fanouts, p, bb)
+
+
+@pytest.mark.parametrize("p", [0.0, 0.5, 0.9, 1.0])
+@pytest.mark.parametrize("fanouts", [(15, 10, 5), (25, 10), (1, 32)])
+def test_slot_law_products_scaled(p, fanouts):
+    # NEXT-2 (i): the slot law (reading R23) through cmb_sample_blocks_law
+    b, prep, g = _bundle("products", 0.01)
+    s = cmb.Sampler(g, 512, fanouts)
+    order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_COMM, 0.5,
+                               SEED, 0)
+    for bb in (0, 3):
+        n, e = check_batch(b, prep, g, s, oracle.batch_roots(order, 512, bb), fanouts, p, bb,
+                           law=oracle.LAW_SLOT)
+    if p == 1.0:  # rows with fewer intra neighbours than f return short (no refill)
+        assert e[0] < 512 * fanouts[0]
+
+
+def test_slot_law_rejects_unknown_law():
+    b, prep, g = _bundle("tiny")
+    s = cmb.Sampler(g, 64, (5, 5))
+    roots = torch.arange(10, dtype=torch.int32, device="cuda")
+    with pytest.raises(cmb.CmbError) as ei:
+        s.sample(roots, 0.9, SEED, 0, law=7)
+    assert ei.value.code == 1
 
 
 def test_ragged_last_batch_and_single_root():
