@@ -260,6 +260,30 @@ CMB_API cmb_status cmb_scatter_rows(const float* rows, int64_t rows_ld, const in
                                     const int64_t* n_dev, int64_t n_cap, int32_t feat_dim,
                                     float* out, int64_t out_ld, void* stream);
 
+/* ------------------------------------------------------------------ NEXT-1: one-sided gather */
+/* the same a4 + a5 as cmb_gather_aggregate, but feature row v is read
+ * from shards[v / rows_per_shard] at row v % rows_per_shard (row stride shard_ld floats):
+ * with the peers' shards mapped into this process (cmb_ipc_open) the kernel reads remote rows
+ * over NVLink itself -- the exchange is fused into the gather, no staging and no all-to-all.
+ * shards: HOST array of `world` (<= 8) device pointers, 16-B aligned; rows_per_shard * world
+ * must cover num_nodes; feat_dim columns are gathered.  Results are byte-identical to
+ * cmb_gather_aggregate on the concatenated table.  blocks->new_src_mask and last_src_ids are
+ * required (filled by cmb_sample_blocks). */
+CMB_API cmb_status cmb_gather_aggregate_sharded(const cmb_graph* g, const cmb_blocks* blocks,
+                                                int32_t n_hops, int64_t n_last_dst_cap,
+                                                int64_t nodes_cap, const float* const* shards,
+                                                int32_t world, int64_t rows_per_shard,
+                                                int64_t shard_ld, int32_t feat_dim, float* x_in,
+                                                int64_t x_in_ld, float* h_out, int64_t h_ld,
+                                                void* stream);
+/* CUDA IPC export of the allocation holding dev_ptr: writes the 64-byte handle to `handle`
+ * (caller-owned, >= 64 bytes) and dev_ptr's byte offset inside the allocation. */
+CMB_API cmb_status cmb_ipc_export(const void* dev_ptr, void* handle, uint64_t* offset);
+/* Maps a peer process's exported allocation: *dev_ptr = mapped base + offset, *base = the
+ * mapped base (pass it to cmb_ipc_close).  Fails (CMB_ERR_CUDA) in the exporting process. */
+CMB_API cmb_status cmb_ipc_open(const void* handle, uint64_t offset, void** dev_ptr, void** base);
+CMB_API cmb_status cmb_ipc_close(void* base);
+
 /* ------------------------------------------------------------------ status */
 /* Synchronises `stream`, returns (and clears) the sticky device status word of a
  * graph / order / sample workspace. */

@@ -43,7 +43,9 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sample_blocks_multi",
            "cmb_gather_features",
            "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_shard_plan_workspace_bytes",
-           "cmb_shard_plan", "cmb_gather_rows", "cmb_scatter_rows", "cmb_get_device_status",
+           "cmb_shard_plan", "cmb_gather_rows", "cmb_scatter_rows",
+           "cmb_gather_aggregate_sharded", "cmb_ipc_export", "cmb_ipc_open", "cmb_ipc_close",
+           "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
 
@@ -120,6 +122,11 @@ def lib():
             "cmb_shard_plan": (I32, [P, P, I64, I64, I32, P, P, P, P, SZ, P]),
             "cmb_gather_rows": (I32, [P, I64, I64, I32, P, P, I64, P, I64, P]),
             "cmb_scatter_rows": (I32, [P, I64, P, P, I64, I32, P, I64, P]),
+            "cmb_gather_aggregate_sharded": (I32, [P, ctypes.POINTER(Blocks), I32, I64, I64, P,
+                                                   I32, I64, I64, I32, P, I64, P, I64, P]),
+            "cmb_ipc_export": (I32, [P, P, ctypes.POINTER(ctypes.c_uint64)]),
+            "cmb_ipc_open": (I32, [P, ctypes.c_uint64, ctypes.POINTER(P), ctypes.POINTER(P)]),
+            "cmb_ipc_close": (I32, [P]),
             "cmb_get_device_status": (I32, [P, P]),
             "cmb_status_string": (ctypes.c_char_p, [I32]),
             "cmb_last_error_message": (ctypes.c_char_p, []),
@@ -356,8 +363,82 @@ class Sampler:
                                           x_in.stride(0), _ptr(h), h.stride(0), _stream()))
         return x_in, h
 
+    def gather_aggregate_sharded(self, table: "ShardTable"):
+        """NEXT-1: a4 + a5 reading every feature row from its owner's shard (peer shards mapped
+        over NVLink); same bytes as gather_aggregate on the concatenated table."""
+        x_in, h = self.alloc_features_ld(table.feat_ld)
+        _check(lib().cmb_gather_aggregate_sharded(
+            self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
+            self.n_cap[self.L], table.ptr_array, table.world, table.rows_per_shard, table.shard_ld,
+            table.feat_dim, _ptr(x_in), x_in.stride(0), _ptr(h), h.stride(0), _stream()))
+        return x_in, h
+
+    def alloc_features_ld(self, ld: int):
+        if self.x_in is None or self.x_in.stride(0) != ld:
+            dev = self.graph.device
+            self.x_in = torch.empty(self.n_cap[self.L], ld, dtype=torch.float32, device=dev)
+            self.h = torch.empty(self.n_cap[self.L - 1], ld, dtype=torch.float32, device=dev)
+        return self.x_in, self.h
+
     def status(self):
         return lib().cmb_get_device_status(_ptr(self.workspace), _stream())
+
+
+class ShardTable:
+    """NEXT-1: the row-sharded feature table as seen by one process -- `world` device pointers,
+    shard r holding rows [r*S, (r+1)*S).  Built from local tensors (virtual shards on one GPU,
+    or world = 1) or by `ShardTable.exchange` (CUDA IPC handles shared over a process group,
+    peers' shards mapped into this process)."""
+
+    def __init__(self, shards: Sequence, num_nodes: int, feat_dim: int, shard_ld=None,
+                 mapped_bases=()):
+        """shards: per rank a device tensor [rows, ld] or a raw device pointer (int)."""
+        self.world = len(shards)
+        if not 1 <= self.world <= 8:
+            raise ValueError("1..8 shards")
+        self.rows_per_shard = (int(num_nodes) + self.world - 1) // self.world
+        self.feat_dim = int(feat_dim)
+        lds = {int(t.stride(0)) for t in shards if isinstance(t, torch.Tensor)}
+        if shard_ld is not None:
+            lds.add(int(shard_ld))
+        if len(lds) != 1:
+            raise ValueError("shards must share one row stride")
+        self.shard_ld = self.feat_ld = lds.pop()
+        self._keep = [t for t in shards if isinstance(t, torch.Tensor)]
+        self._ptrs = [t.data_ptr() if isinstance(t, torch.Tensor) else int(t) for t in shards]
+        self.ptr_array = (ctypes.c_void_p * self.world)(*self._ptrs)
+        self._mapped = list(mapped_bases)
+
+    @classmethod
+    def exchange(cls, x_local: torch.Tensor, num_nodes: int, feat_dim: int, rank: int, world: int,
+                 group=None):
+        """Collective: every rank exports its shard, all-gathers the handles and maps the
+        peers' shards (CUDA IPC; NVLink on a multi-GPU node)."""
+        import torch.distributed as tdist
+        h = (ctypes.c_char * 64)()
+        off = ctypes.c_uint64()
+        _check(lib().cmb_ipc_export(ctypes.c_void_p(x_local.data_ptr()), h, ctypes.byref(off)))
+        mine = (bytes(h), int(off.value), int(x_local.stride(0)))
+        allh = [None] * world
+        tdist.all_gather_object(allh, mine, group=group)
+        ptrs, bases = [], []
+        for r, (hb, o, ld) in enumerate(allh):
+            if ld != x_local.stride(0):
+                raise ValueError("all shards must share one row stride")
+            if r == rank:
+                ptrs.append(x_local)
+                continue
+            p, b = ctypes.c_void_p(), ctypes.c_void_p()
+            _check(lib().cmb_ipc_open((ctypes.c_char * 64).from_buffer_copy(hb), o,
+                                      ctypes.byref(p), ctypes.byref(b)))
+            ptrs.append(int(p.value))
+            bases.append(int(b.value))
+        return cls(ptrs, num_nodes, feat_dim, shard_ld=x_local.stride(0), mapped_bases=bases)
+
+    def close(self):
+        for b in self._mapped:
+            _check(lib().cmb_ipc_close(ctypes.c_void_p(b)))
+        self._mapped = []
 
 
 def sample_multi(samplers: Sequence["Sampler"], roots: Sequence[torch.Tensor],

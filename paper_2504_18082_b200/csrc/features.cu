@@ -688,6 +688,49 @@ void launch_mean(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* 
       mask, hint);
 }
 
+// the default fused form: one warp per dst row (gather_row.cuh).  DMAX = edge rows issued per
+// round: the block's fanout (deg_hint = e_cap / n_cap) clamped to [4, 6] (8 spills at 64
+// registers: reddit's fanout-10 block runs best at 6, 178 vs 212 us)
+template <class Rows>
+cmb_status launch_row(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
+                      const int32_t* gid, const int64_t* n_dev, int64_t n_cap, const Rows& rows,
+                      const int32_t* map, int f4, float* out, int64_t out_ld, float* x_in,
+                      int64_t x_in_ld, const uint32_t* mask, int deg_hint) {
+  static const int dmax_env = [] {
+    const char* e = std::getenv("CMB_ROW_DMAX");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int dmax = dmax_env > 0 ? dmax_env : (deg_hint < 6 ? deg_hint : 6);
+  static const int bps = [] {  // 4 resident 256-thread blocks per SM (64 registers)
+    const char* e = std::getenv("CMB_AGG_BLOCKS_PER_SM");
+    return e ? std::atoi(e) : 4;
+  }();
+  const int64_t want = (n_cap + 7) / 8;  // 8 warps (rows) per 256-thread block
+  const int64_t cap = static_cast<int64_t>(sms) * (bps > 0 ? bps : 8);
+  const int grid = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
+  static const int minb = [] {
+    const char* e = std::getenv("CMB_ROW_MINB");
+    return e ? std::atoi(e) : 4;
+  }();
+#define CMB_ROWK(D_)                                                                          \
+  if (minb == 5) CMB_ROWK2(D_, 5); else CMB_ROWK2(D_, 4)
+#define CMB_ROWK2(D_, M_)                                                                     \
+  if (f4 > 32) CMB_ROWK3(D_, M_, true); else CMB_ROWK3(D_, M_, false)
+#define CMB_ROWK3(D_, M_, W_)                                                                 \
+  k_gather_mean_row<D_, M_, W_, Rows><<<grid, 256, 0, s>>>(                                   \
+      indptr, idx, gid, n_dev, n_cap, rows, map, f4, reinterpret_cast<float4*>(out),          \
+      out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4, mask)
+  if (dmax <= 4) { CMB_ROWK(4); }
+  else if (dmax <= 5) { CMB_ROWK(5); }
+  else if (dmax <= 6) { CMB_ROWK(6); }
+  else { CMB_ROWK(8); }
+#undef CMB_ROWK
+#undef CMB_ROWK2
+#undef CMB_ROWK3
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
 cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_t* gid,
                          const int64_t* n_dev, int64_t n_cap, const float* src, int64_t src_ld,
                          const int32_t* map, int f, float* out, int64_t out_ld, float* x_in,
@@ -708,46 +751,10 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_
                           out_ld, x_in, x_in_ld, mask);
   }
   const int form = agg_kernel_form();
-  if (vec && x_in && gid && (form == 0 || form == 7)) {
-    // default fused form: one warp per dst row (gather_row.cuh).  DMAX = edge rows issued per
-    // round: the block's fanout (deg_hint = e_cap / n_cap) clamped to [4, 6]
-    static const int dmax_env = [] {
-      const char* e = std::getenv("CMB_ROW_DMAX");
-      return e ? std::atoi(e) : 0;
-    }();
-    // (8 spills at 64 registers: reddit's fanout-10 block runs best at 6, 178 vs 212 us)
-    const int dmax = dmax_env > 0 ? dmax_env : (deg_hint < 6 ? deg_hint : 6);
-    static const int bps = [] {  // 4 resident 256-thread blocks per SM (64 registers)
-      const char* e = std::getenv("CMB_AGG_BLOCKS_PER_SM");
-      return e ? std::atoi(e) : 4;
-    }();
-    const int64_t want = (n_cap + 7) / 8;  // 8 warps (rows) per 256-thread block
-    const int64_t cap = static_cast<int64_t>(sms) * (bps > 0 ? bps : 8);
-    const int grid = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
-    static const int minb = [] {
-      const char* e = std::getenv("CMB_ROW_MINB");
-      return e ? std::atoi(e) : 4;
-    }();
-#define CMB_ROWK(D_)                                                                          \
-  if (minb == 5) CMB_ROWK2(D_, 5); else CMB_ROWK2(D_, 4)
-#define CMB_ROWK2(D_, M_)                                                                     \
-  if (f4 > 32) CMB_ROWK3(D_, M_, true); else CMB_ROWK3(D_, M_, false)
-#define CMB_ROWK3(D_, M_, W_)                                                                 \
-  k_gather_mean_row<D_, M_, W_><<<grid, 256, 0, s>>>(indptr, idx, gid, n_dev, n_cap,                  \
-                                             reinterpret_cast<const float4*>(src), src_ld / 4, \
-                                             map, f4, reinterpret_cast<float4*>(out),         \
-                                             out_ld / 4, reinterpret_cast<float4*>(x_in),     \
-                                             x_in_ld / 4, mask)
-    if (dmax <= 4) { CMB_ROWK(4); }
-    else if (dmax <= 5) { CMB_ROWK(5); }
-    else if (dmax <= 6) { CMB_ROWK(6); }
-    else { CMB_ROWK(8); }
-#undef CMB_ROWK
-#undef CMB_ROWK2
-#undef CMB_ROWK3
-    CMB_CUDA(cudaGetLastError());
-    return CMB_OK;
-  }
+  if (vec && x_in && gid && (form == 0 || form == 7))
+    return launch_row(sms, s, indptr, idx, gid, n_dev, n_cap,
+                      DenseRows{reinterpret_cast<const float4*>(src), src_ld / 4}, map, f4, out,
+                      out_ld, x_in, x_in_ld, mask, deg_hint);
   if (vec && x_in && f4 <= 32 && form == 6)
     return launch_async(sms, s, indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, out, out_ld,
                         x_in, x_in_ld, mask);
@@ -841,6 +848,44 @@ cmb_status cmb_sage_mean_aggregate(const int32_t* indptr, const int32_t* indices
   return mean_dispatch(indptr, indices, nullptr, n_dst_dev, n_dst_cap, src, src_ld, src_map,
                        feat_dim, out, out_ld, nullptr, 0, nullptr, sms,
                        static_cast<cudaStream_t>(stream));
+}
+
+cmb_status cmb_gather_aggregate_sharded(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                        int64_t n_last_dst_cap, int64_t nodes_cap,
+                                        const float* const* shards, int32_t world,
+                                        int64_t rows_per_shard, int64_t shard_ld, int32_t feat_dim,
+                                        float* x_in, int64_t x_in_ld, float* h_out, int64_t h_ld,
+                                        void* stream) {
+  CMB_ARG(g && b && shards && x_in && h_out, "cmb_gather_aggregate_sharded: null argument");
+  CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_gather_aggregate_sharded: bad n_hops");
+  CMB_ARG(world >= 1 && world <= kMaxShards, "cmb_gather_aggregate_sharded: world %d outside [1, %d]",
+          world, kMaxShards);
+  CMB_ARG(rows_per_shard >= 1 && rows_per_shard * world >= g->d.n &&
+              rows_per_shard <= INT32_MAX,
+          "cmb_gather_aggregate_sharded: rows_per_shard * world must cover the %lld nodes",
+          static_cast<long long>(g->d.n));
+  CMB_ARG(feat_dim >= 1 && shard_ld >= feat_dim && x_in_ld >= feat_dim && h_ld >= feat_dim,
+          "cmb_gather_aggregate_sharded: bad feat_dim / ld");
+  CMB_ARG(shard_ld % 4 == 0 && x_in_ld % 4 == 0 && h_ld % 4 == 0 && aligned16(x_in) &&
+              aligned16(h_out),
+          "cmb_gather_aggregate_sharded: rows must be 16-B aligned");
+  CMB_ARG(b->new_src_mask && b->last_src_ids,
+          "cmb_gather_aggregate_sharded: blocks->new_src_mask and last_src_ids are required");
+  CMB_ARG(n_last_dst_cap <= nodes_cap, "cmb_gather_aggregate_sharded: n_last_dst_cap > nodes_cap");
+  ShardedRows rows{};
+  for (int r = 0; r < world; ++r) {
+    CMB_ARG(shards[r] && aligned16(shards[r]), "cmb_gather_aggregate_sharded: shard %d", r);
+    rows.base[r] = reinterpret_cast<const float4*>(shards[r]);
+  }
+  rows.ld4 = shard_ld / 4;
+  rows.rows_per_shard = static_cast<uint32_t>(rows_per_shard);
+  rows.inv = ((1ull << 32) + rows_per_shard - 1) / rows_per_shard;
+  const int L = n_hops;
+  return launch_row(g->num_sms, static_cast<cudaStream_t>(stream), b->indptr[L - 1],
+                    b->indices[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap, rows,
+                    b->nodes, (feat_dim + 3) / 4, h_out, h_ld, x_in, x_in_ld, b->new_src_mask,
+                    n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
+                                       : 8);
 }
 
 cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,

@@ -23,11 +23,36 @@ __device__ __forceinline__ float div_small(float a, float d, float y) {
   return __fmaf_rn(r, y, q);
 }
 
-template <int DMAX, int MINB, bool WIDE>
+// Where feature row v lives.  DenseRows: one table in this GPU's HBM.  ShardedRows
+// (NEXT-1): rows [r*S, (r+1)*S) in shard r, base[r] being this GPU's own shard or a peer's
+// shard mapped into this process (CUDA IPC over NVLink), so the loads of remote rows travel
+// over NVLink inside the kernel -- no staging copy, no separate collective.
+struct DenseRows {
+  const float4* base;
+  int64_t ld4;
+  __device__ __forceinline__ const float4* row(int32_t v) const {
+    return base + static_cast<int64_t>(v) * ld4;
+  }
+};
+constexpr int kMaxShards = 8;
+struct ShardedRows {
+  const float4* base[kMaxShards];
+  int64_t ld4;
+  uint64_t inv;  // ceil(2^32 / rows_per_shard): owner = (v * inv) >> 32, at most 1 too high
+  uint32_t rows_per_shard;
+  __device__ __forceinline__ const float4* row(int32_t v) const {
+    const uint32_t u = static_cast<uint32_t>(v);
+    uint32_t r = static_cast<uint32_t>((static_cast<uint64_t>(u) * inv) >> 32);
+    if (static_cast<uint64_t>(r) * rows_per_shard > u) --r;
+    return base[r] + static_cast<int64_t>(u - r * rows_per_shard) * ld4;
+  }
+};
+
+template <int DMAX, int MINB, bool WIDE, class Rows>
 __global__ void __launch_bounds__(256, MINB)
     k_gather_mean_row(const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
                       const int32_t* __restrict__ gid, const int64_t* __restrict__ n_dst_dev,
-                      int64_t n_dst_cap, const float4* __restrict__ src, int64_t src_ld4,
+                      int64_t n_dst_cap, const __grid_constant__ Rows rows,
                       const int32_t* __restrict__ map, int f4, float4* __restrict__ out,
                       int64_t out_ld4, float4* __restrict__ x_in, int64_t x_in_ld4,
                       const uint32_t* __restrict__ new_mask) {
@@ -72,18 +97,14 @@ __global__ void __launch_bounds__(256, MINB)
     // column chunks of 32 float4 (one for F <= 128; wide rows, e.g. F = 602, take several)
     for (int c0 = 0; c0 < (WIDE ? f4 : 1); c0 += 32) {
     const bool col = c0 + lane < f4;
-    const float4* srcc = src + c0 + lane;
-    const float4 sv = col ? ldg4_hint(srcc + static_cast<int64_t>(ac.self) * src_ld4, pol_keep)
-                          : zero;
+    const float4 sv = col ? ldg4_hint(rows.row(ac.self) + c0 + lane, pol_keep) : zero;
     float4 acc = zero;
     for (int base = 0; base < deg; base += DMAX) {
       float4 v[DMAX];
 #pragma unroll
       for (int j = 0; j < DMAX; ++j) {
         const int32_t g = __shfl_sync(kFull, bc.g, (base + j) & 31);
-        v[j] = (col && base + j < deg)
-                   ? ldg4_hint(srcc + static_cast<int64_t>(g) * src_ld4, pol_keep)
-                   : zero;
+        v[j] = (col && base + j < deg) ? ldg4_hint(rows.row(g) + c0 + lane, pol_keep) : zero;
       }
 #pragma unroll
       for (int j = 0; j < DMAX; ++j) {
