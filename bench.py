@@ -265,10 +265,17 @@ def run_cmb(args, bundle):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; CMB_DIST_BACKEND=gloo (+ more ranks than GPUs) only to exercise the
+    # multi-rank flow on a single-GPU box
+    backend = os.environ.get("CMB_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg = bundle.cfg
     p = cfg.p_intra if args.p is None else args.p
     L = len(cfg.fanouts)
@@ -342,7 +349,7 @@ def run_cmb(args, bundle):
     e_h = sz[:, L + 1:]
     alg = [algorithmic_bytes(n_h[k], e_h[k], cfg.feat_dim, L) for k in range(K)]
     ms_max, (total_edges, total_batches) = cmb_dist.reduce_timing(
-        ms, [float(e_h.sum()), float(K)], device=dev)
+        ms, [float(e_h.sum()), float(K)], device=dev if backend == "nccl" else None)
 
     # ---------------- e2e: host buffers through the public API (rank-local)
     e2e = run_e2e(args, pipe, cfg, stream, K, W, world, rank)
@@ -507,6 +514,8 @@ def knob_points(bundle, graph, cfg, args, K, flush=False):
 
 def main():
     args = parse()
+    if args.impl == "reference" and int(os.environ.get("RANK", "0")) != 0:
+        return 0  # the reference arm runs on rank 0 only; the other ranks exit without work
     from gen import CONFIGS, generate
     cfg = CONFIGS[args.config]
     bundle = generate(cfg)

@@ -269,12 +269,18 @@ def generate(cfg: GraphConfig, features: bool = True, cache: bool = True) -> Bun
         })
         del src_comm
         b = Bundle(cfg, indptr, indices, comm, train, None, meta)
-        if d:
-            os.makedirs(d, exist_ok=True)
+        if d:  # written under a private name, then renamed: concurrent ranks never see half a cache
+            tmp = f"{d}.tmp.{os.getpid()}"
+            os.makedirs(tmp, exist_ok=True)
             for k in ("indptr", "indices", "comm", "train"):
-                np.save(os.path.join(d, k + ".npy"), getattr(b, k))
-            np.save(os.path.join(d, "meta.npy"), np.array(meta, dtype=object))
-            open(os.path.join(d, "done"), "w").close()
+                np.save(os.path.join(tmp, k + ".npy"), getattr(b, k))
+            np.save(os.path.join(tmp, "meta.npy"), np.array(meta, dtype=object))
+            open(os.path.join(tmp, "done"), "w").close()
+            try:
+                os.rename(tmp, d)
+            except OSError:  # another process published it first
+                import shutil
+                shutil.rmtree(tmp, ignore_errors=True)
     if features and not cfg.device_features:
         b.X = make_features(cfg)
     return b
