@@ -94,6 +94,11 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
   }();
   a.dedup = dedup;
   a.law = law;
+  static const int fuse = [] {  // CMB_FUSE_PICKS=0: separate coalesced picks pass (A/B knob)
+    const char* e = std::getenv("CMB_FUSE_PICKS");
+    return e ? std::atoi(e) : 1;
+  }();
+  a.fuse_picks = fuse;
 }
 
 cmb_status launch_persistent(const cmb_graph* g, pst::PMulti& m, cudaStream_t s) {

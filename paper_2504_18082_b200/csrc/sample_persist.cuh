@@ -70,6 +70,7 @@ struct PArgs {
   int32_t* status;
   int dedup;                // warp-deduplicate the marks (match_any) before the atomics
   int law;                  // Knob-2 law: 0 = successive weighted w/o replacement, 1 = slot
+  int fuse_picks;           // load + mark each pick in the positions step (else a picks pass)
 };
 
 // Per-block sub-step timeline (profiling aid, one store per sub-step per block):
@@ -191,19 +192,47 @@ __device__ void phase_relabel(const PArgs& a, int h) {
   }
 }
 
-// ---- positions of the picks of one row, written as absolute CSR indices rs + position
+// ---- the picks of one row: rank k (ascending position) at absolute CSR index p
+
+// PosEmit: record the CSR index (a separate picks pass loads and marks the neighbours).
+struct PosEmit {
+  int64_t* o;
+  __device__ __forceinline__ void put(int k, int64_t p) const { o[k] = p; }
+};
+// PickEmit (default): load the neighbour id right away, write it to the block and mark its
+// first occurrence -- atomicMax(map[u], tag | kMarkerTop - e), a fire-and-forget reduction;
+// final entries (roots, earlier hops) always beat markers, smaller e beats larger e.  The
+// random CSR loads then overlap with the Philox work of the other rows of the phase instead of
+// forming a pass of their own, and the pick array round trip disappears.
+struct PickEmit {
+  const int32_t* ind;
+  int32_t* out;                // block indices of this row's first pick
+  unsigned long long* map;
+  unsigned long long tag;
+  uint32_t e0;                 // absolute edge index of the row's first pick
+  __device__ __forceinline__ void put(int k, int64_t p) const {
+    const uint32_t u = static_cast<uint32_t>(__ldg(ind + p));
+    out[k] = static_cast<int32_t>(u);
+    atomicMax(map + u, tag | (kMarkerTop - (e0 + static_cast<uint32_t>(k))));
+  }
+};
 
 // take-all (reading R4): every eligible position, ascending; returns true if taken
+template <class Emit>
 __device__ __forceinline__ bool take_all(int64_t rs, int64_t deg, uint32_t lo, uint32_t hi,
                                          int64_t ni_e, int64_t no_e, int f, int lane, int G,
-                                         int64_t* __restrict__ o) {
+                                         const Emit& em) {
   if (f < ni_e + no_e) return false;
   if (ni_e && no_e) {
-    for (int64_t q = lane; q < deg; q += G) o[q] = rs + q;
+#pragma unroll 4
+    for (int64_t q = lane; q < deg; q += G) em.put(static_cast<int>(q), rs + q);
   } else if (ni_e) {
-    for (int64_t q = lane; q < ni_e; q += G) o[q] = rs + lo + q;
+#pragma unroll 4
+    for (int64_t q = lane; q < ni_e; q += G) em.put(static_cast<int>(q), rs + lo + q);
   } else {
-    for (int64_t q = lane; q < no_e; q += G) o[q] = rs + (q < lo ? q : hi + (q - lo));
+#pragma unroll 4
+    for (int64_t q = lane; q < no_e; q += G)
+      em.put(static_cast<int>(q), rs + (q < lo ? q : hi + (q - lo)));
   }
   return true;
 }
@@ -226,16 +255,15 @@ __device__ __forceinline__ int32_t slot_count(int32_t v, int hop, int f, uint32_
 }
 
 // G lanes per row (f <= G): lane s owns Philox slot s
-template <int G>
+template <int G, class Emit>
 __device__ __forceinline__ void row_positions_group(int32_t v, int64_t rs, int64_t deg,
                                                     uint32_t lo, uint32_t hi, int hop, int f,
                                                     uint32_t wi, uint32_t wo, uint32_t k0,
                                                     uint32_t k1, uint32_t batch, int lane,
-                                                    unsigned gmask, int64_t* __restrict__ o,
-                                                    int law) {
+                                                    unsigned gmask, const Emit& em, int law) {
   const int64_t ni = static_cast<int64_t>(hi) - lo;
   const int64_t ni_e = wi ? ni : 0, no_e = wo ? deg - ni : 0;
-  if (take_all(rs, deg, lo, hi, ni_e, no_e, f, lane, G, o)) return;
+  if (take_all(rs, deg, lo, hi, ni_e, no_e, f, lane, G, em)) return;
   PhiloxOut w{0u, 0u, 0u, 0u};
   if (lane < f)
     w = philox4x32_10(static_cast<uint32_t>(lane), static_cast<uint32_t>(v),
@@ -278,20 +306,20 @@ __device__ __forceinline__ void row_positions_group(int32_t v, int64_t rs, int64
   if (lane >= tot) pos = kEmpty;
   int rank = 0;
   for (int s = 0; s < tot; ++s) rank += __shfl_sync(gmask, pos, s, G) < pos;
-  if (lane < tot) o[rank] = rs + pos;
+  if (lane < tot) em.put(rank, rs + pos);
 }
 
 // one thread per row (f <= FM): the same draws with every loop statically unrolled over FM
 // slots (register arrays, predicated on s < f) -- no shuffles, 32 rows per warp.
-template <int FM>
+template <int FM, class Emit>
 __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int64_t deg,
                                                      uint32_t lo, uint32_t hi, int hop, int f,
                                                      uint32_t wi, uint32_t wo, uint32_t k0,
                                                      uint32_t k1, uint32_t batch,
-                                                     int64_t* __restrict__ o, int law) {
+                                                     const Emit& em, int law) {
   const int64_t ni = static_cast<int64_t>(hi) - lo;
   const int64_t ni_e = wi ? ni : 0, no_e = wo ? deg - ni : 0;
-  if (take_all(rs, deg, lo, hi, ni_e, no_e, f, 0, 1, o)) return;
+  if (take_all(rs, deg, lo, hi, ni_e, no_e, f, 0, 1, em)) return;
   uint64_t r23[FM];
   uint64_t ri = static_cast<uint64_t>(ni_e), ro = static_cast<uint64_t>(no_e);
   int K = 0, kd = 0;
@@ -349,7 +377,7 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
       int rank = 0;
 #pragma unroll
       for (int q = 0; q < FM; ++q) rank += (q < tot) && pos[q] < pos[s];
-      o[rank] = rs + pos[s];
+      em.put(rank, rs + pos[s]);
     }
   }
 }
@@ -431,12 +459,24 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       uint32_t rlo, rhi;
       fetch(i, v, rs, deg, rlo, rhi, off);
       a.indptr[h][i] = base + off;
-      if (f <= 8)
-        row_positions_thread<8>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch,
-                                a.pick + base + off, a.law);
-      else
-        row_positions_thread<16>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch,
-                                 a.pick + base + off, a.law);
+      const uint32_t e0 = static_cast<uint32_t>(base + off);
+      if (a.fuse_picks) {
+        const PickEmit em{a.g.indices, a.indices[h] + e0, a.map, tag, e0};
+        if (f <= 8)
+          row_positions_thread<8>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
+                                  a.law);
+        else
+          row_positions_thread<16>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch,
+                                   em, a.law);
+      } else {
+        const PosEmit em{a.pick + e0};
+        if (f <= 8)
+          row_positions_thread<8>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
+                                  a.law);
+        else
+          row_positions_thread<16>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch,
+                                   em, a.law);
+      }
     }
   } else {
     const int lane = threadIdx.x & (G - 1);
@@ -448,12 +488,19 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       uint32_t rlo, rhi;
       fetch(i, v, rs, deg, rlo, rhi, off);
       if (lane == 0) a.indptr[h][i] = base + off;
-      row_positions_group<G>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, lane,
-                             gmask, a.pick + base + off, a.law);
+      const uint32_t e0 = static_cast<uint32_t>(base + off);
+      if (a.fuse_picks)
+        row_positions_group<G>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, lane,
+                               gmask, PickEmit{a.g.indices, a.indices[h] + e0, a.map, tag, e0},
+                               a.law);
+      else
+        row_positions_group<G>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, lane,
+                               gmask, PosEmit{a.pick + e0}, a.law);
     }
   }
   __syncthreads();
   CMB_PROF(a, pk);
+  if (a.fuse_picks) return;  // picks and marks were emitted with the positions
   // (3) picks + mark: the block's edges are the contiguous range [base, base + run); each
   // picked neighbour u is written out and its first occurrence marked right away:
   // warp-deduplicated atomicMax(map[u], tag | kMarkerTop - e) (fire-and-forget reductions).
