@@ -128,3 +128,38 @@ def test_virtual_shards_match_oracle_gather(W):
         sf.gather(nodes, n, out2)
         torch.cuda.synchronize()
         assert out2[:, : cfg.feat_dim].cpu().numpy().tobytes() == ref.tobytes()
+
+
+# ------------------------------------------------------------------ NEXT-1 host logic (CPU)
+def test_shard_table_layout_and_validation():
+    from paper_2504_18082_b200 import ShardTable
+    N, F = 1001, 8
+    X = torch.zeros(N, 8)
+    W = 3
+    S = (N + W - 1) // W
+    t = ShardTable([X[r * S:(r + 1) * S] for r in range(W)], N, F)
+    assert t.world == W and t.rows_per_shard == S and t.shard_ld == 8
+    assert list(t.ptr_array) == [X[r * S:].data_ptr() for r in range(W)]
+    # raw pointers need the row stride
+    t2 = ShardTable([X.data_ptr(), X[S:].data_ptr()], N, F, shard_ld=8)
+    assert t2.world == 2 and t2.rows_per_shard == (N + 1) // 2
+    with pytest.raises(ValueError):
+        ShardTable([X, torch.zeros(N, 12)], N, F)          # mixed strides
+    with pytest.raises(ValueError):
+        ShardTable([X] * 9, N, F)                           # more than 8 shards
+    with pytest.raises(ValueError):
+        ShardTable([X.data_ptr()], N, F)                    # pointer without a stride
+
+
+def test_owner_formula_matches_division():
+    # the device's owner computation (gather_row.cuh ShardedRows::row), restated on the host
+    rng = np.random.default_rng(5)
+    for S in (1, 2, 3, 7, 1000, 1_388_237, 13_882_495, 2 ** 30):
+        inv = ((1 << 32) + S - 1) // S
+        us = np.concatenate([[0, 1, S - 1, S, S + 1, 2 * S - 1, 2 * S, 2 ** 31 - 1],
+                             rng.integers(0, 2 ** 31, 3000)])
+        for u in us.tolist():
+            r = (u * inv) >> 32
+            if r * S > u:
+                r -= 1
+            assert r == u // S
