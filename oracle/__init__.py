@@ -26,7 +26,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.c")
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
 
-MODE_RAND, MODE_NORAND, MODE_COMM = 0, 1, 2
+MODE_RAND, MODE_NORAND, MODE_COMM, MODE_COMM_STATIC = 0, 1, 2, 3
 
 _lib = None
 

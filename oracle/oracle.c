@@ -123,6 +123,12 @@ int or_graph_prep(int64_t n, const int64_t *indptr, const int32_t *indices, cons
  *          S = max(1, floor(k*C_tr + 0.5)) shuffled communities form a
  *          super-block; the train nodes are ordered by (super-block, key(v), v),
  *          i.e. the contents of each super-block are shuffled.
+ *   mode 3 COMM-RAND-MIX-k with STATIC adjacent-community super-blocks (SURVEY.md 8(f)
+ *          NEXT-2 (ii); reading R24): the C_tr train communities in ascending id order,
+ *          j = 0..C_tr-1, form super-blocks b = j / S of S ADJACENT communities (fixed across
+ *          epochs); each epoch the super-blocks are shuffled as units (sorted by (sbkey(b), b),
+ *          sbkey(b) = r01(Philox(1, b, 3<<24, epoch))) and the train nodes are ordered by
+ *          (rank of their super-block, key(v), v).
  * Batches are consecutive B-slices of the result (caller).  Returns 0 or -1. */
 typedef struct { uint64_t k1, k2; int64_t v; } key3;
 
@@ -168,12 +174,41 @@ int or_order_roots(int64_t n_train, const int32_t *train, const int32_t *comm, i
         for (int64_t rank = 0; rank < ctr; ++rank) sb_of[cs[rank].v] = (uint64_t)(rank / S);
         free(cs);
         free(has);
+    } else if (mode == 3) {
+        char *has = (char *)calloc((size_t)num_comm, 1);
+        int64_t ctr = 0;
+        for (int64_t i = 0; i < n_train; ++i) has[comm[train[i]]] = 1;
+        for (int32_t c = 0; c < num_comm; ++c) ctr += has[c];
+        int64_t S = (int64_t)(mix * (double)ctr + 0.5);    /* floor(k*C_tr + 0.5) */
+        if (S < 1) S = 1;
+        const int64_t nsb = (ctr + S - 1) / S;
+        key3 *bs = (key3 *)malloc(sizeof(key3) * (size_t)(nsb ? nsb : 1));
+        for (int64_t b = 0; b < nsb; ++b) {                /* one key per super-block */
+            uint32_t w[4];
+            draw(seed, 1, (uint32_t)b, TAG_COMM, 0, epoch, w);
+            bs[b].k1 = r01(w);
+            bs[b].k2 = 0;
+            bs[b].v = b;
+        }
+        qsort(bs, (size_t)nsb, sizeof(key3), cmp_key3);    /* shuffle the super-blocks */
+        uint64_t *ord = (uint64_t *)calloc((size_t)(nsb ? nsb : 1), sizeof(uint64_t));
+        for (int64_t r = 0; r < nsb; ++r) ord[bs[r].v] = (uint64_t)r;
+        sb_of = (uint64_t *)calloc((size_t)num_comm, sizeof(uint64_t));
+        int64_t j = 0;                                     /* train-community index, by id */
+        for (int32_t c = 0; c < num_comm; ++c) {
+            if (!has[c]) continue;
+            sb_of[c] = ord[j / S];
+            ++j;
+        }
+        free(ord);
+        free(bs);
+        free(has);
     }
     for (int64_t i = 0; i < n_train; ++i) {
         uint32_t w[4];
         int32_t v = train[i];
         draw(seed, 0, (uint32_t)v, TAG_ROOT, 0, epoch, w);
-        rows[i].k1 = (mode == 2) ? sb_of[comm[v]] : 0;
+        rows[i].k1 = (mode == 2 || mode == 3) ? sb_of[comm[v]] : 0;
         rows[i].k2 = r01(w);
         rows[i].v = v;
     }

@@ -134,3 +134,57 @@ def test_train_communities_only():
     groups = _superblocks(a, comm)
     S = max(1, int(np.floor(0.25 * 20 + 0.5)))
     assert all(len(g) == S for g in groups[:-1])
+
+
+# ------------------------------------------------------------------ static super-blocks (R24)
+from oracle import MODE_COMM_STATIC  # noqa: E402
+
+
+@pytest.mark.parametrize("k", [0.0, 0.1, 0.25, 0.5])
+def test_static_superblocks_are_adjacent_runs(k):
+    """Each super-block is a contiguous run of the order holding the train nodes of S
+    communities that are ADJACENT in id order (the same groups every epoch), and inside a run
+    the nodes follow the RAND order restricted to them (same node keys)."""
+    train, comm, C = _setup()
+    ctr_ids = np.unique(comm[train])                  # train communities, ascending
+    S = max(1, int(np.floor(k * ctr_ids.shape[0] + 0.5)))
+    group = {c: j // S for j, c in enumerate(ctr_ids)}
+    for epoch in (0, 1, 2):
+        o = oracle.order_roots(train, comm, C, MODE_COMM_STATIC, k, seed=11, epoch=epoch)
+        r = oracle.order_roots(train, comm, C, MODE_RAND, 0.0, seed=11, epoch=epoch)
+        assert np.array_equal(np.sort(o), train)
+        g = np.array([group[c] for c in comm[o]])
+        runs = g[np.r_[True, g[1:] != g[:-1]]]
+        assert len(runs) == len(set(runs.tolist())) == len(set(group.values()))  # contiguous
+        pos_in_rand = {v: i for i, v in enumerate(r.tolist())}
+        for b in set(runs.tolist()):
+            run = o[g == b]
+            assert np.all(np.diff([pos_in_rand[v] for v in run.tolist()]) > 0)
+    o0 = oracle.order_roots(train, comm, C, MODE_COMM_STATIC, k, seed=11, epoch=0)
+    o1 = oracle.order_roots(train, comm, C, MODE_COMM_STATIC, k, seed=11, epoch=1)
+    assert not np.array_equal(o0, o1)
+
+
+def test_static_k1_equals_rand_bitwise():
+    train, comm, C = _setup()
+    for e in range(3):
+        assert np.array_equal(oracle.order_roots(train, comm, C, MODE_COMM_STATIC, 1.0, 5, e),
+                              oracle.order_roots(train, comm, C, MODE_RAND, 0.0, 5, e))
+
+
+def test_static_superblock_order_is_uniform_chi2():
+    """The super-block sequence is a uniformly random permutation: the position of super-block
+    0 among nsb super-blocks is uniform over epochs."""
+    train, comm, C = _setup()
+    ctr_ids = np.unique(comm[train])
+    S = 5
+    k = S / ctr_ids.shape[0]
+    group = {c: j // S for j, c in enumerate(ctr_ids)}
+    nsb = (ctr_ids.shape[0] + S - 1) // S
+    cnt = np.zeros(nsb)
+    for e in range(1500):
+        o = oracle.order_roots(train, comm, C, MODE_COMM_STATIC, k, seed=3, epoch=e)
+        g = np.array([group[c] for c in comm[o]])
+        runs = g[np.r_[True, g[1:] != g[:-1]]]
+        cnt[int(np.nonzero(runs == 0)[0][0])] += 1
+    assert stats.chisquare(cnt).pvalue > 1e-4
