@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="cmb", choices=["cmb", "reference"])
     ap.add_argument("--config", default="products")
-    ap.add_argument("--mode", default="rand", choices=["rand", "norand", "comm"])
+    ap.add_argument("--mode", default="rand", choices=["rand", "norand", "comm", "comm_static"])
     ap.add_argument("--mix", type=float, default=0.0)
     ap.add_argument("--p", type=float, default=None)
     ap.add_argument("--seed", type=int, default=42)
@@ -160,7 +160,8 @@ def oracle_batches(bundle, mode, mix, p, seed, budget_s, max_batches=None, law=0
     import oracle
     cfg = bundle.cfg
     prep = oracle.graph_prep(bundle)
-    modes = {"rand": oracle.MODE_RAND, "norand": oracle.MODE_NORAND, "comm": oracle.MODE_COMM}
+    modes = {"rand": oracle.MODE_RAND, "norand": oracle.MODE_NORAND, "comm": oracle.MODE_COMM,
+             "comm_static": oracle.MODE_COMM_STATIC}
     scratch = np.full(prep.num_nodes, -1, dtype=np.int32)
     t0 = time.perf_counter()
     order = oracle.order_roots(bundle.train, bundle.comm, cfg.num_communities, modes[mode], mix,
@@ -187,7 +188,8 @@ def run_reference(args, bundle):
     p = cfg.p_intra if args.p is None else args.p
     import oracle
     prep = oracle.graph_prep(bundle)
-    modes = {"rand": oracle.MODE_RAND, "norand": oracle.MODE_NORAND, "comm": oracle.MODE_COMM}
+    modes = {"rand": oracle.MODE_RAND, "norand": oracle.MODE_NORAND, "comm": oracle.MODE_COMM,
+             "comm_static": oracle.MODE_COMM_STATIC}
     order = oracle.order_roots(bundle.train, bundle.comm, cfg.num_communities, modes[args.mode],
                                args.mix, args.seed, 0)
     nb = (order.shape[0] + cfg.batch_size - 1) // cfg.batch_size
@@ -232,7 +234,7 @@ def workload_config(args, cfg, bundle, p, flush=False):
             if cfg.name == "products" else f"{cfg.name}-shaped synthetic",
             "num_nodes": cfg.num_nodes, "nnz": int(bundle.nnz), "feat_dim": cfg.feat_dim,
             "batch": cfg.batch_size, "fanouts_hop_order": list(cfg.fanouts),
-            "knob1": args.mode + (f"(k={args.mix})" if args.mode == "comm" else ""),
+            "knob1": args.mode + (f"(k={args.mix})" if args.mode.startswith("comm") else ""),
             "p_intra": p, "knob2_law": args.law, "seed": args.seed,
             "l2": ("L2 flushed (256 MB write) before every launch group of %d batches; "
                    "ms = sum of the groups' device events (X %.0f MB, CSR %.0f MB)"
@@ -361,7 +363,7 @@ def run_cmb(args, bundle):
     if rank == 0:
         peak, peak_src = measured_peak_hbm()
         achieved = float(np.mean(alg)) / (float(np.mean(agg_ms)) * 1e-3) / 1e9
-        knob = args.mode + (f"(k={args.mix})" if args.mode == "comm" else "") + f"|{p}"
+        knob = args.mode + (f"(k={args.mix})" if args.mode.startswith("comm") else "") + f"|{p}"
         traffic = ncu_traffic(cfg.name, knob)
         cpu = None
         if world == 1:

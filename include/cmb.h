@@ -71,9 +71,13 @@ typedef enum {
 typedef enum {
   CMB_ROOTS_RAND = 0,   /* RAND-ROOTS: uniform shuffle of the training set               */
   CMB_ROOTS_NORAND = 1, /* NORAND-ROOTS: no shuffle; static across epochs                */
-  CMB_ROOTS_COMM = 2    /* COMM-RAND-MIX-k%: shuffle communities as blocks, group k% of
+  CMB_ROOTS_COMM = 2,   /* COMM-RAND-MIX-k%: shuffle communities as blocks, group k% of
                            the training-set communities into super-blocks, shuffle the
                            nodes inside each super-block (k = mix_fraction)              */
+  CMB_ROOTS_COMM_STATIC = 3 /* COMM-RAND-MIX-k% with STATIC super-blocks of k% ADJACENT
+                           training-set communities (id order; SURVEY.md 8(f) NEXT-2 (ii),
+                           reading R24): the super-blocks are shuffled as units each epoch,
+                           the nodes inside each super-block shuffled                    */
 } cmb_roots_mode;
 
 typedef struct cmb_graph cmb_graph; /* opaque host handle; holds borrowed device pointers */
@@ -126,6 +130,10 @@ CMB_API size_t cmb_order_roots_workspace_bytes(int64_t n_train, int32_t num_comm
  *           S = max(1, floor(mix_fraction * C_tr + 0.5)) of them form super-blocks;
  *           nodes are sorted by (super-block, key(v), v).  mix_fraction = 0 is
  *           COMM-RAND-MIX-0%, 1 reproduces RAND bit for bit (readings R9, R10).
+ *   COMM_STATIC: the C_tr communities in ascending id order, j = 0..C_tr-1, form
+ *           super-blocks b = j / S (adjacent, fixed across epochs); super-blocks are
+ *           ranked by (sbkey(b), b), sbkey(b) = 64-bit Philox(1, b, 3<<24, epoch), and
+ *           nodes sorted by (super-block rank, key(v), v) (reading R24).
  * mix_fraction in [0, 1].  Non-ascending train_ids set CMB_ERR_INVALID_INPUT in
  * the workspace status word. */
 CMB_API cmb_status cmb_order_roots(const cmb_graph* g, const int32_t* train_ids, int64_t n_train,

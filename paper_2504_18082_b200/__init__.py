@@ -29,8 +29,9 @@ LIB_PATH = os.path.join(_HERE, "libcmb.so")
 MAX_HOPS = 8
 MAX_FANOUT = 32
 
-ROOTS_RAND, ROOTS_NORAND, ROOTS_COMM = 0, 1, 2
-_MODES = {"rand": ROOTS_RAND, "norand": ROOTS_NORAND, "comm": ROOTS_COMM}
+ROOTS_RAND, ROOTS_NORAND, ROOTS_COMM, ROOTS_COMM_STATIC = 0, 1, 2, 3
+_MODES = {"rand": ROOTS_RAND, "norand": ROOTS_NORAND, "comm": ROOTS_COMM,
+          "comm_static": ROOTS_COMM_STATIC}
 
 STATUS = {0: "CMB_OK", 1: "CMB_ERR_INVALID_ARGUMENT", 2: "CMB_ERR_INVALID_GRAPH",
           3: "CMB_ERR_NOT_COMMUNITY_ORDERED", 4: "CMB_ERR_CAPACITY", 5: "CMB_ERR_CUDA",

@@ -75,6 +75,40 @@ __global__ void k_comm_superblock(const int32_t* __restrict__ cval_sorted,
   }
 }
 
+// static adjacent super-blocks (mode 3): one Philox key per super-block b < nsb (slot 1 of the
+// community stream), padded with ~0 up to ncomm so the sort length is host-known
+__global__ void k_static_sb_keys(const int32_t* __restrict__ cpos, int64_t n, double mix,
+                                 int32_t ncomm, uint64_t seed, uint32_t epoch,
+                                 uint64_t* __restrict__ key, int32_t* __restrict__ val) {
+  const int64_t c_tr = cpos[n - 1];
+  int64_t S = static_cast<int64_t>(__dadd_rn(__dmul_rn(mix, static_cast<double>(c_tr)), 0.5));
+  if (S < 1) S = 1;
+  const int64_t nsb = (c_tr + S - 1) / S;
+  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+  for (int32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < ncomm; b += gridDim.x * blockDim.x) {
+    key[b] = b < nsb ? lo64(philox4x32_10(1u, static_cast<uint32_t>(b), kTagComm << 24, epoch, k0,
+                                          k1))
+                     : ~0ull;
+    val[b] = b;
+  }
+}
+
+// sb_of_j[j] = rank of super-block j / S in the shuffled super-block order
+__global__ void k_static_superblock(const int32_t* __restrict__ b_sorted,
+                                    const int32_t* __restrict__ cpos, int64_t n, double mix,
+                                    int32_t ncomm, uint32_t* __restrict__ ord,
+                                    uint32_t* __restrict__ sb_of_j) {
+  const int64_t c_tr = cpos[n - 1];
+  int64_t S = static_cast<int64_t>(__dadd_rn(__dmul_rn(mix, static_cast<double>(c_tr)), 0.5));
+  if (S < 1) S = 1;
+  const int64_t nsb = (c_tr + S - 1) / S;
+  // single block: ranks first, then the per-community lookup
+  for (int32_t r = threadIdx.x; r < nsb; r += blockDim.x) ord[b_sorted[r]] = static_cast<uint32_t>(r);
+  __syncthreads();
+  for (int32_t j = threadIdx.x; j < ncomm && j < c_tr; j += blockDim.x)
+    sb_of_j[j] = ord[j / S];
+}
+
 __global__ void k_node_superblock(const int32_t* __restrict__ pos_sorted,
                                   const int32_t* __restrict__ cpos,
                                   const uint32_t* __restrict__ sb_of_j, int64_t n,
@@ -170,7 +204,8 @@ cmb_status cmb_order_roots(const cmb_graph* g, const int32_t* train_ids, int64_t
   CMB_ARG(g && train_ids && out_order, "cmb_order_roots: null graph/train_ids/out_order");
   CMB_ARG(n_train >= 1 && n_train <= g->d.n, "cmb_order_roots: n_train %lld outside [1, N]",
           (long long)n_train);
-  CMB_ARG(mode == CMB_ROOTS_RAND || mode == CMB_ROOTS_NORAND || mode == CMB_ROOTS_COMM,
+  CMB_ARG(mode == CMB_ROOTS_RAND || mode == CMB_ROOTS_NORAND || mode == CMB_ROOTS_COMM ||
+              mode == CMB_ROOTS_COMM_STATIC,
           "cmb_order_roots: unknown mode %d", (int)mode);
   CMB_ARG(mix_fraction >= 0.0 && mix_fraction <= 1.0, "cmb_order_roots: mix_fraction outside [0,1]");
   const size_t need = cmb_order_roots_workspace_bytes(n_train, g->d.ncomm);
@@ -191,20 +226,32 @@ cmb_status cmb_order_roots(const cmb_graph* g, const int32_t* train_ids, int64_t
   // sort train positions by key(v) (stable: equal keys keep ascending v)
   CMB_CUDA(cub::DeviceRadixSort::SortPairs(w.temp, tb, w.k0, w.k1, w.v0, w.v1, ni, 0, 64, s));
   const int32_t* pos = w.v1;
-  if (mode == CMB_ROOTS_COMM) {
+  if (mode == CMB_ROOTS_COMM || mode == CMB_ROOTS_COMM_STATIC) {
     const int32_t C = g->d.ncomm;
     k_comm_flags<<<grid, blk, 0, s>>>(train_ids, g->d.comm, n_train, w.flag);
     CMB_CUDA(cudaGetLastError());
     tb = w.temp_bytes;
     CMB_CUDA(cub::DeviceScan::InclusiveSum(w.temp, tb, w.flag, w.cpos, ni, s));
-    k_comm_pad<<<ceil_div(C, blk), blk, 0, s>>>(C, w.ck0, w.cv0);
-    k_comm_keys<<<grid, blk, 0, s>>>(train_ids, g->d.comm, w.flag, w.cpos, n_train, seed, epoch,
-                                     w.ck0);
-    CMB_CUDA(cudaGetLastError());
-    tb = w.temp_bytes;
-    CMB_CUDA(cub::DeviceRadixSort::SortPairs(w.temp, tb, w.ck0, w.ck1, w.cv0, w.cv1, C, 0, 64, s));
-    k_comm_superblock<<<ceil_div(C, blk), blk, 0, s>>>(w.cv1, w.cpos, n_train, mix_fraction, C,
-                                                       w.sb_of_j);
+    if (mode == CMB_ROOTS_COMM) {
+      k_comm_pad<<<ceil_div(C, blk), blk, 0, s>>>(C, w.ck0, w.cv0);
+      k_comm_keys<<<grid, blk, 0, s>>>(train_ids, g->d.comm, w.flag, w.cpos, n_train, seed,
+                                       epoch, w.ck0);
+      CMB_CUDA(cudaGetLastError());
+      tb = w.temp_bytes;
+      CMB_CUDA(
+          cub::DeviceRadixSort::SortPairs(w.temp, tb, w.ck0, w.ck1, w.cv0, w.cv1, C, 0, 64, s));
+      k_comm_superblock<<<ceil_div(C, blk), blk, 0, s>>>(w.cv1, w.cpos, n_train, mix_fraction, C,
+                                                         w.sb_of_j);
+    } else {
+      k_static_sb_keys<<<ceil_div(C, blk), blk, 0, s>>>(w.cpos, n_train, mix_fraction, C, seed,
+                                                        epoch, w.ck0, w.cv0);
+      CMB_CUDA(cudaGetLastError());
+      tb = w.temp_bytes;
+      CMB_CUDA(
+          cub::DeviceRadixSort::SortPairs(w.temp, tb, w.ck0, w.ck1, w.cv0, w.cv1, C, 0, 64, s));
+      k_static_superblock<<<1, 1024, 0, s>>>(w.cv1, w.cpos, n_train, mix_fraction, C,
+                                             reinterpret_cast<uint32_t*>(w.cv0), w.sb_of_j);
+    }
     k_node_superblock<<<grid, blk, 0, s>>>(w.v1, w.cpos, w.sb_of_j, n_train, w.sbk);
     CMB_CUDA(cudaGetLastError());
     tb = w.temp_bytes;

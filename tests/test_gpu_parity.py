@@ -29,7 +29,8 @@ def _bundle(name, factor=None):
 
 
 def _mode(m):
-    return {"rand": oracle.MODE_RAND, "norand": oracle.MODE_NORAND, "comm": oracle.MODE_COMM}[m]
+    return {"rand": oracle.MODE_RAND, "norand": oracle.MODE_NORAND, "comm": oracle.MODE_COMM,
+            "comm_static": oracle.MODE_COMM_STATIC}[m]
 
 
 def agg_tol_ok(H, H64, Xin, ip, idx):
@@ -106,7 +107,9 @@ def test_load_graph_rejects_bad_input():
 # ------------------------------------------------------------------ a1
 @pytest.mark.parametrize("name,factor", [("tiny", None), ("arxiv", None), ("products", None)])
 @pytest.mark.parametrize("mode,k", [("rand", 0.0), ("norand", 0.0), ("comm", 0.0),
-                                    ("comm", 0.125), ("comm", 0.5), ("comm", 1.0)])
+                                    ("comm", 0.125), ("comm", 0.5), ("comm", 1.0),
+                                    ("comm_static", 0.0), ("comm_static", 0.125),
+                                    ("comm_static", 1.0)])
 def test_order_roots_parity(name, factor, mode, k):
     b, prep, g = _bundle(name, factor)
     ro = cmb.RootOrderer(g, torch.from_numpy(b.train))
