@@ -314,6 +314,8 @@ def run_cmb(args, bundle):
     flush = args.flush_l2 == "on" or (args.flush_l2 == "auto" and not inputs_exceed_l2(cfg, bundle))
     scrub = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
     evlog = []
+    # per-group timing events created before the region (creating them inside costs host time)
+    evpool = [pipe.make_events(min(G, K - k0)) for k0 in range(0, K, G)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -328,11 +330,12 @@ def run_cmb(args, bundle):
             cnt = min(G, K - k0)
             ep0 = pipe.epoch
             orders_in_region += len({gbatch(W + k) // nb for k in range(k0, k0 + cnt)} - {ep0})
-            ev = {}
+            evs = evpool[k0 // G]
             if flush:
                 scrub.fill_(k0 & 0xFF)   # evicts the previous group's lines from L2
-            ss = group(W + k0, cnt, ev)
-            evlog.append(ev)
+            ss = group(W + k0, cnt, evs)
+            evlog.append({"sample": (evs[0], evs[1]),
+                          "gather": [(evs[2 + 2 * i], evs[3 + 2 * i]) for i in range(cnt)]})
             n_groups += 1
             for i, s in enumerate(ss):
                 sizes_log[k0 + i].copy_(s.sizes, non_blocking=True)
@@ -486,16 +489,19 @@ def knob_points(bundle, graph, cfg, args, K, flush=False):
         e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         sizes = torch.zeros(n, 2 * L + 1, dtype=torch.int64, device=graph.device)
         evs = []
+        scrub = torch.empty(256 << 20, dtype=torch.uint8, device=graph.device) if flush else None
+        pool = [pipe.make_events(min(G, n - k0)) for k0 in range(0, n, G)]
         torch.cuda.synchronize()
         e_start.record(s)
         pipe.start_epoch(0)
-        scrub = torch.empty(256 << 20, dtype=torch.uint8, device=graph.device) if flush else None
         for k0 in range(0, n, G):
-            ev = {}
+            el = pool[k0 // G]
+            cnt = min(G, n - k0)
             if flush:
                 scrub.fill_(k0 & 0xFF)
-            ss = pipe.step_group(range(k0, min(n, k0 + G)), events=ev)
-            evs.append(ev)
+            ss = pipe.step_group(range(k0, k0 + cnt), events=el)
+            evs.append({"sample": (el[0], el[1]),
+                        "gather": [(el[2 + 2 * i], el[3 + 2 * i]) for i in range(cnt)]})
             for i, smp in enumerate(ss):
                 sizes[k0 + i].copy_(smp.sizes, non_blocking=True)
         e_end.record(s)

@@ -268,6 +268,25 @@ CMB_API cmb_status cmb_scatter_rows(const float* rows, int64_t rows_ld, const in
                                     const int64_t* n_dev, int64_t n_cap, int32_t feat_dim,
                                     float* out, int64_t out_ld, void* stream);
 
+/* ------------------------------------------------------------------ step executor */
+/* Where cmb_step_group writes the a4 + a5 outputs of one batch (see cmb_gather_aggregate). */
+typedef struct {
+  float* x_in;
+  int64_t x_in_ld;
+  float* h_out;
+  int64_t h_ld;
+  int64_t n_last_dst_cap; /* n_cap[L-1] of the batch's blocks */
+  int64_t nodes_cap;      /* n_cap[L]                         */
+} cmb_batch_features;
+/* One launch group of the step, enqueued by ONE call: cmb_sample_blocks_multi over the
+ * n_batches batches, then cmb_gather_aggregate of each (same arguments and results as calling
+ * them in that order).  events: NULL, or 2 + 2 * n_batches cudaEvent_t (entries may be NULL)
+ * recorded on `stream` before/after the sampler launch and before/after every gather. */
+CMB_API cmb_status cmb_step_group(const cmb_graph* g, const cmb_batch* batches,
+                                  const cmb_batch_features* feats, int32_t n_batches,
+                                  const int32_t* fanouts, int32_t n_hops, double p_intra,
+                                  int32_t law, uint64_t seed, void* const* events, void* stream);
+
 /* ------------------------------------------------------------------ NEXT-1: one-sided gather */
 /* the same a4 + a5 as cmb_gather_aggregate, but feature row v is read
  * from shards[v / rows_per_shard] at row v % rows_per_shard (row stride shard_ld floats):

@@ -46,6 +46,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_shard_plan_workspace_bytes",
            "cmb_shard_plan", "cmb_gather_rows", "cmb_scatter_rows",
            "cmb_gather_aggregate_sharded", "cmb_ipc_export", "cmb_ipc_open", "cmb_ipc_close",
+           "cmb_step_group",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -76,6 +77,12 @@ class Batch(ctypes.Structure):
     _fields_ = [("roots", ctypes.c_void_p), ("n_roots", ctypes.c_int64),
                 ("batch_id", ctypes.c_uint32), ("out", ctypes.POINTER(Blocks)),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
+
+
+class BatchFeatures(ctypes.Structure):
+    _fields_ = [("x_in", ctypes.c_void_p), ("x_in_ld", ctypes.c_int64), ("h_out", ctypes.c_void_p),
+                ("h_ld", ctypes.c_int64), ("n_last_dst_cap", ctypes.c_int64),
+                ("nodes_cap", ctypes.c_int64)]
 
 
 MAX_BATCHES_PER_LAUNCH = 4
@@ -128,6 +135,8 @@ def lib():
             "cmb_ipc_export": (I32, [P, P, ctypes.POINTER(ctypes.c_uint64)]),
             "cmb_ipc_open": (I32, [P, ctypes.c_uint64, ctypes.POINTER(P), ctypes.POINTER(P)]),
             "cmb_ipc_close": (I32, [P]),
+            "cmb_step_group": (I32, [P, ctypes.POINTER(Batch), ctypes.POINTER(BatchFeatures), I32,
+                                     P, I32, D, I32, U64, P, P]),
             "cmb_get_device_status": (I32, [P, P]),
             "cmb_status_string": (ctypes.c_char_p, [I32]),
             "cmb_last_error_message": (ctypes.c_char_p, []),
@@ -519,8 +528,28 @@ class BatchedPipeline(MiniBatchPipeline):
                  mode="rand", mix=0.0, p=0.5, seed=42, nb: int = 2, law=LAW_A):
         super().__init__(graph, train, batch_size, fanouts, mode, mix, p, seed, law)
         self.nb = int(nb)
+        if not 1 <= self.nb <= MAX_BATCHES_PER_LAUNCH:
+            raise ValueError(f"nb must be in [1, {MAX_BATCHES_PER_LAUNCH}]")
         self.samplers = [self.sampler] + [Sampler(graph, self.batch_size, fanouts)
                                           for _ in range(self.nb - 1)]
+        # step-executor argument arrays, filled once (per group only roots / ids change)
+        self._batches = (Batch * self.nb)()
+        self._feats = (BatchFeatures * self.nb)()
+        for i, s in enumerate(self.samplers):
+            x_in, h = s.alloc_features()
+            self._batches[i] = Batch(0, 0, 0, ctypes.pointer(s._blocks), s.workspace.data_ptr(),
+                                     s.workspace.numel())
+            self._feats[i] = BatchFeatures(x_in.data_ptr(), x_in.stride(0), h.data_ptr(),
+                                           h.stride(0), s.n_cap[s.L - 1], s.n_cap[s.L])
+
+    def make_events(self, n: int = None):
+        """2 + 2n timing events for one step_group call, created and recorded once (so their
+        handles exist) -- preallocate them outside a timed region."""
+        n = self.nb if n is None else n
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 + 2 * n)]
+        for e in evs:
+            e.record()
+        return evs
 
     def step_group(self, gbs: Sequence[int], roots: Optional[Sequence[torch.Tensor]] = None,
                    events=None):
@@ -541,23 +570,32 @@ class BatchedPipeline(MiniBatchPipeline):
                     self.start_epoch(epoch)
                 roots.append(self.batch_roots(b))
         ss = self.samplers[: len(gbs)]
-        timing = events is not None
-        if timing:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-        sample_multi(ss, roots, gbs, self.p, self.seed, self.law)
-        if timing:
-            e1.record()
-            events["sample"] = (e0, e1)
-            events["gather"] = []
-        for s in ss:
-            if timing:
-                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                g0.record()
-            s.gather_aggregate()
-            if timing:
-                g1.record()
-                events["gather"].append((g0, g1))
+        n = len(gbs)
+        ev_list = None
+        if isinstance(events, dict):  # fresh events (convenient, but costs host time per group)
+            ev_list = [torch.cuda.Event(enable_timing=True) for _ in range(2 + 2 * n)]
+            for e in ev_list:  # materialise the cudaEvent_t handles
+                e.record()
+            events["sample"] = (ev_list[0], ev_list[1])
+            events["gather"] = [(ev_list[2 + 2 * i], ev_list[3 + 2 * i]) for i in range(n)]
+        elif events is not None:      # a pre-created list of 2 + 2n recorded-once events
+            ev_list = events
+        for i, (s, r, gb) in enumerate(zip(ss, roots, gbs)):
+            nr = int(r.shape[0])
+            if nr > s.max_roots:
+                raise ValueError("more roots than max_roots")
+            bt = self._batches[i]
+            bt.roots, bt.n_roots, bt.batch_id = r.data_ptr(), nr, gb
+            x_in, h = s.alloc_features()
+            if self._feats[i].x_in != x_in.data_ptr():  # outputs were re-allocated
+                self._feats[i] = BatchFeatures(x_in.data_ptr(), x_in.stride(0), h.data_ptr(),
+                                               h.stride(0), s.n_cap[s.L - 1], s.n_cap[s.L])
+        evp = None
+        if ev_list is not None:
+            evp = (ctypes.c_void_p * (2 + 2 * n))(*[e.cuda_event for e in ev_list[: 2 + 2 * n]])
+        s0 = ss[0]
+        _check(lib().cmb_step_group(self.graph.handle, self._batches, self._feats, n, s0._f, s0.L,
+                                    float(self.p), self.law, int(self.seed), evp, _stream()))
         return ss
 
 

@@ -99,6 +99,11 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
     return e ? std::atoi(e) : 1;
   }();
   a.fuse_picks = fuse;
+  static const int check = [] {  // CMB_MARK_CHECK (A/B knob)
+    const char* e = std::getenv("CMB_MARK_CHECK");
+    return e ? std::atoi(e) : 1;
+  }();
+  a.mark_check = check;
 }
 
 cmb_status launch_persistent(const cmb_graph* g, pst::PMulti& m, cudaStream_t s) {

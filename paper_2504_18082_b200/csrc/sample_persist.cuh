@@ -71,6 +71,7 @@ struct PArgs {
   int dedup;                // warp-deduplicate the marks (match_any) before the atomics
   int law;                  // Knob-2 law: 0 = successive weighted w/o replacement, 1 = slot
   int fuse_picks;           // load + mark each pick in the positions step (else a picks pass)
+  int mark_check;           // fused marks: load the entry first, atomic only if it can win
 };
 
 // Per-block sub-step timeline (profiling aid, one store per sub-step per block):
@@ -210,10 +211,14 @@ struct PickEmit {
   unsigned long long* map;
   unsigned long long tag;
   uint32_t e0;                 // absolute edge index of the row's first pick
+  int check;                   // read the entry first; skip the atomic if it cannot win
   __device__ __forceinline__ void put(int k, int64_t p) const {
     const uint32_t u = static_cast<uint32_t>(__ldg(ind + p));
     out[k] = static_cast<int32_t>(u);
-    atomicMax(map + u, tag | (kMarkerTop - (e0 + static_cast<uint32_t>(k))));
+    const unsigned long long m = tag | (kMarkerTop - (e0 + static_cast<uint32_t>(k)));
+    // a node picked by many rows (hubs; every pick of a community at p = 1) would otherwise
+    // queue one same-address atomic per pick in L2
+    if (!check || __ldcg(map + u) < m) atomicMax(map + u, m);
   }
 };
 
@@ -461,7 +466,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       a.indptr[h][i] = base + off;
       const uint32_t e0 = static_cast<uint32_t>(base + off);
       if (a.fuse_picks) {
-        const PickEmit em{a.g.indices, a.indices[h] + e0, a.map, tag, e0};
+        const PickEmit em{a.g.indices, a.indices[h] + e0, a.map, tag, e0, a.mark_check};
         if (f <= 8)
           row_positions_thread<8>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
                                   a.law);
@@ -491,7 +496,9 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       const uint32_t e0 = static_cast<uint32_t>(base + off);
       if (a.fuse_picks)
         row_positions_group<G>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, lane,
-                               gmask, PickEmit{a.g.indices, a.indices[h] + e0, a.map, tag, e0},
+                               gmask,
+                               PickEmit{a.g.indices, a.indices[h] + e0, a.map, tag, e0,
+                                        a.mark_check},
                                a.law);
       else
         row_positions_group<G>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, lane,
