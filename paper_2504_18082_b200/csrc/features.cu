@@ -81,232 +81,8 @@ __global__ void k_gather_scalar(const float* __restrict__ x, int64_t ld,
   }
 }
 
-// ------------------------------------------------------------------ a5 (+ a4 fused)
-// One group of LPR lanes per dst row d.  For every edge e of row d (CSR order) the src row
-// r(e) = map ? map[idx[e]] : idx[e] is loaded (CH edges in flight), accumulated, and --
-// when x_in != NULL (fused a4) and bit e of new_mask is set -- also stored as X_in[idx[e]]
-// (the first occurrence of that src node).  Rows d < n_dst also store X_in[d] (self row).
-template <int LPR, int NV, int CH>
-__global__ void __launch_bounds__(256) k_sage_mean_v4(
-    const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
-    const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap, const float4* __restrict__ src,
-    int64_t src_ld4, const int32_t* __restrict__ map, int f4, float4* __restrict__ out,
-    int64_t out_ld4, float4* __restrict__ x_in, int64_t x_in_ld4,
-    const uint32_t* __restrict__ new_mask) {
-  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
-  const int lane = threadIdx.x % LPR;
-  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / LPR);
-  for (int64_t d = blockIdx.x * (int64_t)(blockDim.x / LPR) + threadIdx.x / LPR; d < n_dst;
-       d += groups) {
-    const int32_t e0 = __ldg(indptr + d), e1 = __ldg(indptr + d + 1);
-    const int32_t deg = e1 - e0;
-    for (int c0 = 0; c0 < f4; c0 += LPR * NV) {
-      float4 acc[NV];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (x_in) {  // self row of dst d -> X_in[d]
-        const float4* s = src + (int64_t)__ldg(map + d) * src_ld4;
-#pragma unroll
-        for (int k = 0; k < NV; ++k) {
-          const int c = c0 + lane + k * LPR;
-          if (c < f4) x_in[d * x_in_ld4 + c] = ldg4(s + c);
-        }
-      }
-      for (int32_t eb = e0; eb < e1; eb += CH) {
-        float4 v[CH][NV];
-        int32_t li[CH];
-#pragma unroll
-        for (int j = 0; j < CH; ++j) {
-          const int32_t e = eb + j;
-          li[j] = e < e1 ? __ldg(idx + e) : 0;
-          const int64_t r = map ? (int64_t)__ldg(map + li[j]) : (int64_t)li[j];
-          const float4* s = src + r * src_ld4;
-#pragma unroll
-          for (int k = 0; k < NV; ++k) {
-            const int c = c0 + lane + k * LPR;
-            if (e < e1 && c < f4) v[j][k] = ldg4(s + c);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < CH; ++j) {
-          const int32_t e = eb + j;
-          if (e < e1) {
-#pragma unroll
-            for (int k = 0; k < NV; ++k) add4(acc[k], v[j][k]);
-            if (x_in && ((__ldg(new_mask + (e >> 5)) >> (e & 31)) & 1u)) {
-#pragma unroll
-              for (int k = 0; k < NV; ++k) {
-                const int c = c0 + lane + k * LPR;
-                if (c < f4) x_in[(int64_t)li[j] * x_in_ld4 + c] = v[j][k];
-              }
-            }
-          }
-        }
-      }
-      const float fd = static_cast<float>(deg);
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int c = c0 + lane + k * LPR;
-        if (c < f4) {
-          float4 h = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (deg > 0) {
-            h.x = __fdiv_rn(acc[k].x, fd);
-            h.y = __fdiv_rn(acc[k].y, fd);
-            h.z = __fdiv_rn(acc[k].z, fd);
-            h.w = __fdiv_rn(acc[k].w, fd);
-          }
-          out[d * out_ld4 + c] = h;
-        }
-      }
-    }
-  }
-}
-
-// Tile form (the default): a group of LPR lanes owns a tile of LPR consecutive dst rows.
-// The index streams of the tile are read cooperatively and coalesced (lane k <-> row k for
-// indptr / nodes, lane k <-> edge k for indices / relabel map / first-occurrence bits); the
-// src row ids are then broadcast by shuffle and U src rows are in flight per lane before they
-// are folded, in CSR order, into the accumulator of their dst row.  This removes the
-// per-row dependent chain indptr -> indices -> nodes -> X of the row-per-group form.
-template <int LPR, int NV, int U>
-__global__ void __launch_bounds__(256) k_gather_mean_tile(
-    const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
-    const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap, const float4* __restrict__ src,
-    int64_t src_ld4, const int32_t* __restrict__ map, int f4, float4* __restrict__ out,
-    int64_t out_ld4, float4* __restrict__ x_in, int64_t x_in_ld4,
-    const uint32_t* __restrict__ new_mask) {
-  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
-  const int lane = threadIdx.x % LPR;
-  const int wl = threadIdx.x & 31;
-  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (wl & ~(LPR - 1)));
-  const int64_t ngroups = (int64_t)gridDim.x * (blockDim.x / LPR);
-  const int64_t ntiles = (n_dst + LPR - 1) / LPR;
-  for (int64_t tile = blockIdx.x * (int64_t)(blockDim.x / LPR) + threadIdx.x / LPR;
-       tile < ntiles; tile += ngroups) {
-    const int64_t d0 = tile * LPR;
-    const int nr = (n_dst - d0 < LPR) ? static_cast<int>(n_dst - d0) : LPR;
-    const int32_t my_start = lane < nr ? __ldg(indptr + d0 + lane) : 0;
-    const int32_t t_end = __ldg(indptr + d0 + nr);
-    const int32_t t_begin = __shfl_sync(gmask, my_start, 0, LPR);
-    const int32_t my_node = (x_in && lane < nr) ? __ldg(map + d0 + lane) : 0;
-    auto row_start = [&](int r) { return __shfl_sync(gmask, my_start, r, LPR); };
-    auto row_end = [&](int r) {
-      const int32_t s = __shfl_sync(gmask, my_start, (r + 1) & (LPR - 1), LPR);
-      return r + 1 < nr ? s : t_end;
-    };
-    for (int c0 = 0; c0 < f4; c0 += LPR * NV) {
-      if (x_in) {  // a4 for the dst rows of the tile: X_in[d] = X[nodes[d]]
-        for (int r0 = 0; r0 < nr; r0 += U) {
-          float4 v[U][NV];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int r = r0 + u;
-            const int32_t row = __shfl_sync(gmask, my_node, r & (LPR - 1), LPR);
-#pragma unroll
-            for (int k = 0; k < NV; ++k) {
-              const int c = c0 + lane + k * LPR;
-              if (r < nr && c < f4) v[u][k] = ldg4(src + (int64_t)row * src_ld4 + c);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int r = r0 + u;
-#pragma unroll
-            for (int k = 0; k < NV; ++k) {
-              const int c = c0 + lane + k * LPR;
-              if (r < nr && c < f4) x_in[(d0 + r) * x_in_ld4 + c] = v[u][k];
-            }
-          }
-        }
-      }
-      // empty rows of the tile: H = 0
-      {
-        const int32_t my_end = row_end(lane);
-        unsigned empty = __ballot_sync(gmask, lane < nr && my_end == my_start);
-        empty >>= (LPR == 32 ? 0 : (wl & ~(LPR - 1)));
-        while (empty) {
-          const int r = __ffs(empty) - 1;
-          empty &= empty - 1;
-#pragma unroll
-          for (int k = 0; k < NV; ++k) {
-            const int c = c0 + lane + k * LPR;
-            if (c < f4) out[(d0 + r) * out_ld4 + c] = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-      }
-      float4 acc[NV];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int32_t eb = t_begin; eb < t_end; eb += LPR) {
-        // lane k describes edge e = eb + k: local src id, src row, dst row r (largest r
-        // with start(r) <= e), whether e closes its row, first-occurrence bit, deg(r)
-        const int32_t e = eb + lane;
-        const bool ok = e < t_end;
-        const int32_t li = ok ? __ldg(idx + e) : 0;
-        const int32_t gid = ok ? (map ? __ldg(map + li) : li) : 0;
-        int r = 0;
-#pragma unroll
-        for (int step = LPR / 2; step >= 1; step >>= 1) {
-          const int32_t s = __shfl_sync(gmask, my_start, (r + step) & (LPR - 1), LPR);
-          if (r + step < nr && s <= e) r += step;
-        }
-        const int32_t rend = row_end(r);
-        const int32_t rdeg = rend - row_start(r);
-        const int first =
-            (x_in && ok) ? static_cast<int>((__ldg(new_mask + (e >> 5)) >> (e & 31)) & 1u) : 0;
-        const int meta = (rdeg << 8) | (first << 7) | ((e + 1 == rend) << 6) | r;
-        const int cnt = min(LPR, t_end - eb);
-        for (int j0 = 0; j0 < cnt; j0 += U) {
-          float4 v[U][NV];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int j = j0 + u;
-            const int32_t row = __shfl_sync(gmask, gid, j & (LPR - 1), LPR);
-#pragma unroll
-            for (int k = 0; k < NV; ++k) {
-              const int c = c0 + lane + k * LPR;
-              if (j < cnt && c < f4) v[u][k] = ldg4(src + (int64_t)row * src_ld4 + c);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int j = j0 + u;
-            const int mj = __shfl_sync(gmask, meta, j & (LPR - 1), LPR);
-            const int32_t lj = __shfl_sync(gmask, li, j & (LPR - 1), LPR);
-            if (j < cnt) {
-#pragma unroll
-              for (int k = 0; k < NV; ++k) add4(acc[k], v[u][k]);
-              if (mj & 0x80) {  // first occurrence of a new src node: a4 for it, from this load
-#pragma unroll
-                for (int k = 0; k < NV; ++k) {
-                  const int c = c0 + lane + k * LPR;
-                  if (c < f4) x_in[(int64_t)lj * x_in_ld4 + c] = v[u][k];
-                }
-              }
-              if (mj & 0x40) {  // e closes row r: H[d0 + r] = acc / deg (IEEE), acc = 0
-                const float fd = static_cast<float>(mj >> 8);
-                const int64_t d = d0 + (mj & 0x3f);
-#pragma unroll
-                for (int k = 0; k < NV; ++k) {
-                  const int c = c0 + lane + k * LPR;
-                  float4 h;
-                  h.x = __fdiv_rn(acc[k].x, fd);
-                  h.y = __fdiv_rn(acc[k].y, fd);
-                  h.z = __fdiv_rn(acc[k].z, fd);
-                  h.w = __fdiv_rn(acc[k].w, fd);
-                  if (c < f4) out[d * out_ld4 + c] = h;
-                  acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-              }
-            }
-          }
-        }
-      }
-    }
-  }
-}
-
-// Pipelined row form (the default): one group of LPR lanes per dst row, rows visited with
+// Pipelined row form (the unfused a5 path; CMB_AGG_KERNEL=p for the fused one): one group of
+// LPR lanes per dst row, rows visited with
 // a grid stride, and the index chain of the rows AHEAD is issued before the feature loads of
 // the current row: stage A (row i+2G) loads indptr pair + self node id, stage B (row i+G)
 // loads the row's src ids lane-parallel (lane k <-> edge k; global row ids come straight from
@@ -473,9 +249,7 @@ __global__ void __launch_bounds__(256, (LPR == 16 && NV == 2 && CH == 2) ? 4 : 1
 }  // namespace
 }  // namespace cmb
 
-#include "gather_bulk.cuh"
 #include "gather_tma.cuh"
-#include "gather_async.cuh"
 #include "gather_row.cuh"
 
 namespace cmb {
@@ -551,94 +325,18 @@ cmb_status gather_dispatch(const float* x, int64_t ld, int f, const int32_t* ids
   return CMB_OK;
 }
 
-// CMB_AGG_KERNEL = row | tile | pipe (default) selects the aggregate kernel form (kept for
-// A/B measurement on the GPU box; all three compute identical bytes).
+// CMB_AGG_KERNEL selects the fused a4+a5 form for A/B runs: unset / w = warp per row
+// (gather_row.cuh, the default), p = the 16-lane pipelined form, g = TMA tile::gather4
+// (gather_tma.cuh).  All compute identical bytes.
 int agg_kernel_form() {
   static const int v = [] {
     const char* e = std::getenv("CMB_AGG_KERNEL");
-    if (e && e[0] == 'r') return 1;
-    if (e && e[0] == 't') return 2;
     if (e && e[0] == 'p') return 3;
-    if (e && e[0] == 'b') return 4;  // per-row cp.async.bulk form (opt-in)
-    if (e && e[0] == 'g') return 5;  // TMA tile::gather4 form
-    if (e && e[0] == 'a') return 6;  // cp.async ring form
-    if (e && e[0] == 'w') return 7;  // warp-per-row form
+    if (e && e[0] == 'g') return 5;
+    if (e && e[0] == 'w') return 7;
     return 0;
   }();
   return v;
-}
-
-template <int KS>
-cmb_status launch_async_ks(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
-                           const int32_t* gid, const int64_t* n_dev, int64_t n_cap,
-                           const float* src, int64_t src_ld, const int32_t* map, int f4,
-                           float* out, int64_t out_ld, float* x_in, int64_t x_in_ld,
-                           const uint32_t* mask) {
-  const size_t smem = asyncg::smem_bytes(KS, f4);
-  static size_t configured = 0;
-  if (configured < smem) {
-    CMB_CUDA(cudaFuncSetAttribute(k_gather_mean_async<KS>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
-  int per_sm = 1;
-  CMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_mean_async<KS>,
-                                                         asyncg::kWarps * 32, smem));
-  if (per_sm < 1) per_sm = 1;
-  const int64_t want = (n_cap + asyncg::kWarps - 1) / asyncg::kWarps;
-  const int64_t cap = static_cast<int64_t>(sms) * per_sm;
-  const int grid = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
-  k_gather_mean_async<KS><<<grid, asyncg::kWarps * 32, smem, s>>>(
-      indptr, idx, gid, n_dev, n_cap, reinterpret_cast<const float4*>(src), src_ld / 4, map, f4,
-      reinterpret_cast<float4*>(out), out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4,
-      mask);
-  CMB_CUDA(cudaGetLastError());
-  return CMB_OK;
-}
-
-cmb_status launch_async(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
-                        const int32_t* gid, const int64_t* n_dev, int64_t n_cap, const float* src,
-                        int64_t src_ld, const int32_t* map, int f4, float* out, int64_t out_ld,
-                        float* x_in, int64_t x_in_ld, const uint32_t* mask) {
-  static const int ks = [] {  // ring slots per warp (feature rows in flight per warp)
-    const char* e = std::getenv("CMB_ASYNC_SLOTS");
-    return e ? std::atoi(e) : 16;
-  }();
-#define CMB_ASYNC(K_)                                                                        \
-  return launch_async_ks<K_>(sms, s, indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, out, \
-                             out_ld, x_in, x_in_ld, mask)
-  if (ks <= 8) CMB_ASYNC(8);
-  if (ks <= 12) CMB_ASYNC(12);
-  if (ks <= 16) CMB_ASYNC(16);
-  CMB_ASYNC(24);
-#undef CMB_ASYNC
-}
-
-template <int NV>
-cmb_status launch_bulk(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
-                       const int32_t* gid, const int64_t* n_dev, int64_t n_cap, const float* src,
-                       int64_t src_ld, const int32_t* map, int f4, uint32_t rb, float* out,
-                       int64_t out_ld, float* x_in, int64_t x_in_ld, const uint32_t* mask) {
-  const size_t smem = bulk::smem_bytes(rb);
-  static size_t configured = 0;
-  static int per_sm = 1;
-  if (configured != smem) {
-    CMB_CUDA(cudaFuncSetAttribute(k_gather_mean_bulk<NV>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_mean_bulk<NV>,
-                                                           bulk::kWarps * 32, smem));
-    if (per_sm < 1) per_sm = 1;
-    configured = smem;
-  }
-  const int64_t windows = (n_cap + bulk::kRows - 1) / bulk::kRows;
-  const int64_t want = (windows + bulk::kWarps - 1) / bulk::kWarps;
-  const int64_t cap = static_cast<int64_t>(sms) * per_sm;  // persistent: one wave
-  const int grid = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
-  k_gather_mean_bulk<NV><<<grid, bulk::kWarps * 32, smem, s>>>(
-      indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, rb, reinterpret_cast<float4*>(out),
-      out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4, mask);
-  CMB_CUDA(cudaGetLastError());
-  return CMB_OK;
 }
 
 template <int LPR, int NV, int CH>
@@ -647,26 +345,6 @@ void launch_mean(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* 
                  int64_t src_ld, const int32_t* map, int f4, float* out, int64_t out_ld,
                  float* x_in, int64_t x_in_ld, const uint32_t* mask) {
   const int64_t gpb = 256 / LPR;  // lane groups per 256-thread block
-  const int form = agg_kernel_form();
-  if (form == 1) {
-    int64_t want = (n_cap + gpb - 1) / gpb;
-    const int grid = static_cast<int>(want < sms * 16 ? (want > 0 ? want : 1) : sms * 16);
-    k_sage_mean_v4<LPR, NV, CH><<<grid, 256, 0, s>>>(
-        indptr, idx, n_dev, n_cap, reinterpret_cast<const float4*>(src), src_ld / 4, map, f4,
-        reinterpret_cast<float4*>(out), out_ld / 4, reinterpret_cast<float4*>(x_in),
-        x_in_ld / 4, mask);
-    return;
-  }
-  if (form == 2) {
-    const int64_t tiles = (n_cap + LPR - 1) / LPR;
-    const int tgrid = static_cast<int>((tiles + gpb - 1) / gpb);
-    constexpr int TU = NV == 1 ? 4 : (NV == 2 ? 2 : 1);  // src rows in flight per lane
-    k_gather_mean_tile<LPR, NV, TU><<<tgrid > 0 ? tgrid : 1, 256, 0, s>>>(
-        indptr, idx, n_dev, n_cap, reinterpret_cast<const float4*>(src), src_ld / 4, map, f4,
-        reinterpret_cast<float4*>(out), out_ld / 4, reinterpret_cast<float4*>(x_in),
-        x_in_ld / 4, mask);
-    return;
-  }
   // pipelined row form: a persistent-style grid (a few blocks per SM, grid-stride rows) so
   // every group walks many rows and its look-ahead pipeline stays full
   int64_t want = (n_cap + gpb - 1) / gpb;
@@ -740,24 +418,11 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_
   const int f4 = (f + 3) / 4;
   const bool vec = aligned16(src) && aligned16(out) && src_ld % 4 == 0 && out_ld % 4 == 0 &&
                    (!x_in || (aligned16(x_in) && x_in_ld % 4 == 0));
-  // fused a4+a5 on a sampled block (degrees <= CMB_MAX_FANOUT): the TMA bulk-copy form
-  const uint32_t rb = static_cast<uint32_t>(f4) * 16u;  // copy size, 16-B multiple, <= ld * 4
-  if (vec && x_in && f4 > 16 && f4 <= 64 && agg_kernel_form() == 4 &&
-      bulk::smem_bytes(rb) <= 227 * 1024) {
-    if (f4 <= 32)
-      return launch_bulk<1>(sms, s, indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, rb,
-                            out, out_ld, x_in, x_in_ld, mask);
-    return launch_bulk<2>(sms, s, indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, rb, out,
-                          out_ld, x_in, x_in_ld, mask);
-  }
   const int form = agg_kernel_form();
   if (vec && x_in && gid && (form == 0 || form == 7))
     return launch_row(sms, s, indptr, idx, gid, n_dev, n_cap,
                       DenseRows{reinterpret_cast<const float4*>(src), src_ld / 4}, map, f4, out,
                       out_ld, x_in, x_in_ld, mask, deg_hint);
-  if (vec && x_in && f4 <= 32 && form == 6)
-    return launch_async(sms, s, indptr, idx, gid, n_dev, n_cap, src, src_ld, map, f4, out, out_ld,
-                        x_in, x_in_ld, mask);
   if (!vec) {
     k_sage_mean_scalar<<<sms * 8, 256, 0, s>>>(indptr, idx, n_dev, n_cap, src, src_ld, map, f,
                                                out, out_ld, x_in, x_in_ld, mask);
