@@ -287,6 +287,43 @@ CMB_API cmb_status cmb_step_group(const cmb_graph* g, const cmb_batch* batches,
                                   const int32_t* fanouts, int32_t n_hops, double p_intra,
                                   int32_t law, uint64_t seed, void* const* events, void* stream);
 
+/* ------------------------------------------------------------------ NEXT-3: HBM feature cache */
+/* SURVEY.md 8(f) NEXT-3; the paper's software-cache setting (S6.5.1: a GPU cache of
+ * node features with LRU replacement in front of UVA reads of a host-resident table).  The
+ * feature table stays in pinned host memory (host_x must be device-accessible, e.g.
+ * cudaHostAlloc'ed: UVA); `capacity` rows of it are cached in HBM (cache_rows, device,
+ * capacity x cache_ld floats).  Replacement is CLOCK (second chance, an LRU approximation);
+ * rows referenced by the current batch are never evicted during it.  All buffers are caller
+ * owned; the descriptor is plain data. */
+typedef struct {
+  void* workspace;            /* device, cmb_feature_cache_bytes(), 256-B aligned          */
+  size_t workspace_bytes;
+  int64_t num_nodes;          /* N of the graph                                           */
+  int64_t capacity;           /* cached rows; >= max_rows                                 */
+  int64_t max_rows;           /* >= nodes_cap of every batch (unique input rows, n_L cap)  */
+  int64_t max_edges;          /* >= indices_cap[L-1] of every batch                       */
+  const float* host_x;        /* device-accessible host table [N x host_ld]               */
+  int64_t host_ld;
+  float* cache_rows;          /* device [capacity x cache_ld]                              */
+  int64_t cache_ld;           /* multiple of 4 floats                                     */
+} cmb_feature_cache;
+CMB_API size_t cmb_feature_cache_bytes(int64_t num_nodes, int64_t capacity, int64_t max_rows,
+                                       int64_t max_edges);
+/* Empties the cache (every directory entry invalid). */
+CMB_API cmb_status cmb_feature_cache_init(void* workspace, size_t workspace_bytes,
+                                          int64_t num_nodes, int64_t capacity, int64_t max_rows,
+                                          int64_t max_edges, void* stream);
+/* a4 + a5 of a sampled batch through the cache: misses are copied from host_x into the cache,
+ * then the fused gather + aggregate reads every row from HBM.  Results are byte-identical to
+ * cmb_gather_aggregate on the host table.  batch_tag: distinct for consecutive calls, never
+ * 0xFFFFFFFF.  stats: NULL or device int64[2], incremented by (rows of the batch, misses). */
+CMB_API cmb_status cmb_cache_gather_aggregate(const cmb_graph* g, const cmb_blocks* blocks,
+                                              int32_t n_hops, int64_t n_last_dst_cap,
+                                              int64_t nodes_cap, const cmb_feature_cache* cache,
+                                              int32_t feat_dim, uint32_t batch_tag, float* x_in,
+                                              int64_t x_in_ld, float* h_out, int64_t h_ld,
+                                              int64_t* stats, void* stream);
+
 /* ------------------------------------------------------------------ NEXT-1: one-sided gather */
 /* the same a4 + a5 as cmb_gather_aggregate, but feature row v is read
  * from shards[v / rows_per_shard] at row v % rows_per_shard (row stride shard_ld floats):

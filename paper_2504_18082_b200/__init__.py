@@ -46,7 +46,8 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_shard_plan_workspace_bytes",
            "cmb_shard_plan", "cmb_gather_rows", "cmb_scatter_rows",
            "cmb_gather_aggregate_sharded", "cmb_ipc_export", "cmb_ipc_open", "cmb_ipc_close",
-           "cmb_step_group",
+           "cmb_step_group", "cmb_feature_cache_bytes", "cmb_feature_cache_init",
+           "cmb_cache_gather_aggregate",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -77,6 +78,14 @@ class Batch(ctypes.Structure):
     _fields_ = [("roots", ctypes.c_void_p), ("n_roots", ctypes.c_int64),
                 ("batch_id", ctypes.c_uint32), ("out", ctypes.POINTER(Blocks)),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
+
+
+class FeatureCacheDesc(ctypes.Structure):
+    _fields_ = [("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+                ("num_nodes", ctypes.c_int64), ("capacity", ctypes.c_int64),
+                ("max_rows", ctypes.c_int64), ("max_edges", ctypes.c_int64),
+                ("host_x", ctypes.c_void_p), ("host_ld", ctypes.c_int64),
+                ("cache_rows", ctypes.c_void_p), ("cache_ld", ctypes.c_int64)]
 
 
 class BatchFeatures(ctypes.Structure):
@@ -137,6 +146,11 @@ def lib():
             "cmb_ipc_close": (I32, [P]),
             "cmb_step_group": (I32, [P, ctypes.POINTER(Batch), ctypes.POINTER(BatchFeatures), I32,
                                      P, I32, D, I32, U64, P, P]),
+            "cmb_feature_cache_bytes": (SZ, [I64, I64, I64, I64]),
+            "cmb_feature_cache_init": (I32, [P, SZ, I64, I64, I64, I64, P]),
+            "cmb_cache_gather_aggregate": (I32, [P, ctypes.POINTER(Blocks), I32, I64, I64,
+                                                 ctypes.POINTER(FeatureCacheDesc), I32,
+                                                 ctypes.c_uint32, P, I64, P, I64, P, P]),
             "cmb_get_device_status": (I32, [P, P]),
             "cmb_status_string": (ctypes.c_char_p, [I32]),
             "cmb_last_error_message": (ctypes.c_char_p, []),
@@ -383,6 +397,15 @@ class Sampler:
             table.feat_dim, _ptr(x_in), x_in.stride(0), _ptr(h), h.stride(0), _stream()))
         return x_in, h
 
+    def gather_aggregate_cached(self, cache: "FeatureCache"):
+        """NEXT-3: a4 + a5 through the HBM feature cache (misses read from the host table)."""
+        x_in, h = self.alloc_features_ld(cache.rows.stride(0))
+        _check(lib().cmb_cache_gather_aggregate(
+            self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
+            self.n_cap[self.L], ctypes.byref(cache.desc), cache.feat_dim, cache.next_tag(),
+            _ptr(x_in), x_in.stride(0), _ptr(h), h.stride(0), _ptr(cache.stats), _stream()))
+        return x_in, h
+
     def alloc_features_ld(self, ld: int):
         if self.x_in is None or self.x_in.stride(0) != ld:
             dev = self.graph.device
@@ -392,6 +415,47 @@ class Sampler:
 
     def status(self):
         return lib().cmb_get_device_status(_ptr(self.workspace), _stream())
+
+
+class FeatureCache:
+    """NEXT-3: `capacity` feature rows cached in HBM in front of a host-resident table (pinned,
+    read by the device over the host link on a miss); CLOCK replacement."""
+
+    def __init__(self, graph: Graph, host_x: torch.Tensor, feat_dim: int, capacity: int,
+                 max_rows: int, max_edges: int):
+        if host_x.device.type != "cpu" or not host_x.is_pinned():
+            raise ValueError("host_x must be a pinned host tensor")
+        if host_x.stride(1) != 1:
+            raise ValueError("host_x rows must be contiguous")
+        self.graph, self.host_x, self.feat_dim = graph, host_x, int(feat_dim)
+        self.capacity, self.max_rows, self.max_edges = int(capacity), int(max_rows), int(max_edges)
+        ld = (self.feat_dim + 3) // 4 * 4
+        dev = graph.device
+        nb = lib().cmb_feature_cache_bytes(graph.num_nodes, self.capacity, self.max_rows,
+                                           self.max_edges)
+        self.workspace = _workspace(nb, dev)
+        self.rows = torch.empty(self.capacity, ld, dtype=torch.float32, device=dev)
+        self.stats = torch.zeros(2, dtype=torch.int64, device=dev)  # rows, misses
+        self.desc = FeatureCacheDesc(self.workspace.data_ptr(), self.workspace.numel(),
+                                     graph.num_nodes, self.capacity, self.max_rows,
+                                     self.max_edges, host_x.data_ptr(), host_x.stride(0),
+                                     self.rows.data_ptr(), ld)
+        self.tag = 0
+        self.reset()
+
+    def reset(self):
+        _check(lib().cmb_feature_cache_init(self.workspace.data_ptr(), self.workspace.numel(),
+                                            self.graph.num_nodes, self.capacity, self.max_rows,
+                                            self.max_edges, _stream()))
+        self.stats.zero_()
+
+    def next_tag(self) -> int:
+        self.tag = (self.tag + 1) % 0xFFFFFFFF
+        return self.tag
+
+    def miss_rate(self) -> float:
+        r, m = self.stats.tolist()
+        return m / r if r else 0.0
 
 
 class ShardTable:

@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(256, (LPR == 16 && NV == 2 && CH == 2) ? 4 : 1
 
 #include "gather_tma.cuh"
 #include "gather_row.cuh"
+#include "cache.cuh"
 
 namespace cmb {
 namespace {
@@ -549,6 +550,45 @@ cmb_status cmb_gather_aggregate_sharded(const cmb_graph* g, const cmb_blocks* b,
   return launch_row(g->num_sms, static_cast<cudaStream_t>(stream), b->indptr[L - 1],
                     b->indices[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap, rows,
                     b->nodes, (feat_dim + 3) / 4, h_out, h_ld, x_in, x_in_ld, b->new_src_mask,
+                    n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
+                                       : 8);
+}
+
+cmb_status cmb_cache_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                      int64_t n_last_dst_cap, int64_t nodes_cap,
+                                      const cmb_feature_cache* c, int32_t feat_dim,
+                                      uint32_t batch_tag, float* x_in, int64_t x_in_ld,
+                                      float* h_out, int64_t h_ld, int64_t* stats, void* stream) {
+  CMB_ARG(g && b && c && x_in && h_out, "cmb_cache_gather_aggregate: null argument");
+  CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_cache_gather_aggregate: bad n_hops");
+  CMB_ARG(c->workspace && c->host_x && c->cache_rows, "cmb_cache_gather_aggregate: bad cache");
+  CMB_ARG(c->num_nodes == g->d.n, "cmb_cache_gather_aggregate: cache built for another graph");
+  CMB_ARG(batch_tag != 0xFFFFFFFFu, "cmb_cache_gather_aggregate: batch_tag 0xFFFFFFFF reserved");
+  const int L = n_hops;
+  CMB_ARG(nodes_cap <= c->max_rows && b->indices_cap[L - 1] <= c->max_edges &&
+              c->capacity >= c->max_rows,
+          "cmb_cache_gather_aggregate: batch larger than the cache was sized for");
+  CMB_ARG(feat_dim >= 1 && c->host_ld >= feat_dim && c->cache_ld >= feat_dim &&
+              c->cache_ld % 4 == 0 && x_in_ld % 4 == 0 && h_ld % 4 == 0 &&
+              aligned16(c->cache_rows) && aligned16(x_in) && aligned16(h_out),
+          "cmb_cache_gather_aggregate: bad feat_dim / ld / alignment");
+  CMB_ARG(b->new_src_mask != nullptr, "cmb_cache_gather_aggregate: new_src_mask required");
+  size_t need = 0;
+  CacheWs w = carve_cache_ws(c->workspace, c->num_nodes, c->capacity, c->max_rows, c->max_edges,
+                             &need);
+  CMB_ARG(c->workspace_bytes >= need, "cmb_cache_gather_aggregate: workspace < %zu bytes", need);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cmb_status st = cache_prepare(w, c->capacity, b->nodes, b->sizes + L, nodes_cap,
+                                b->indices[L - 1], b->sizes + L + 1 + (L - 1),
+                                b->indices_cap[L - 1], c->host_x, c->host_ld, feat_dim,
+                                c->cache_rows, c->cache_ld, batch_tag, stats, g->num_sms, s);
+  if (st != CMB_OK) return st;
+  // every row of the batch is resident now: the fused kernel reads cache slots (gid = slot of
+  // each edge's src node, map = slot of each node of the batch)
+  return launch_row(g->num_sms, s, b->indptr[L - 1], b->indices[L - 1], w.gslot,
+                    b->sizes + (L - 1), n_last_dst_cap,
+                    DenseRows{reinterpret_cast<const float4*>(c->cache_rows), c->cache_ld / 4},
+                    w.slot_i, (feat_dim + 3) / 4, h_out, h_ld, x_in, x_in_ld, b->new_src_mask,
                     n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
                                        : 8);
 }
