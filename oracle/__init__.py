@@ -50,6 +50,8 @@ def lib():
         L.or_mulhi64.restype = U64
         L.or_graph_prep.argtypes = [I64, P, P, P, I32, P, P, P]
         L.or_graph_prep.restype = ctypes.c_int
+        L.or_community_order.argtypes = [I64, P, P, P, P, P, P, P, P]
+        L.or_community_order.restype = ctypes.c_int
         L.or_order_roots.argtypes = [I64, P, P, I32, I32, D, U64, U32, P]
         L.or_order_roots.restype = ctypes.c_int
         L.or_sample_hop.argtypes = [P, I64, P, P, P, P, I32, D, U64, I32, U32, P, P, I64, I32]
@@ -114,6 +116,17 @@ def order_roots(train, comm, num_comm, mode, mix=0.0, seed=42, epoch=0) -> np.nd
     if rc != 0:
         raise ValueError("or_order_roots failed (empty train set?)")
     return out
+
+
+def community_order(indptr, indices, comm):
+    """NEXT-2 (iii): (perm new->old, inv old->new, indptr, indices, comm) of the community-
+    ordered relabelling of an arbitrary graph (reading R25)."""
+    ip, ix, cm = _c(indptr, np.int64), _c(indices, np.int32), _c(comm, np.int32)
+    n = ip.shape[0] - 1
+    perm, inv = np.zeros(n, np.int32), np.zeros(n, np.int32)
+    ip2, ix2, cm2 = np.zeros(n + 1, np.int64), np.zeros(max(1, ix.shape[0]), np.int32), np.zeros(n, np.int32)
+    lib().or_community_order(n, _p(ip), _p(ix), _p(cm), _p(perm), _p(inv), _p(ip2), _p(ix2), _p(cm2))
+    return perm, inv, ip2, ix2[: ix.shape[0]], cm2
 
 
 def batch_roots(order: np.ndarray, batch_size: int, b: int) -> np.ndarray:

@@ -18,6 +18,7 @@
  *   or_graph_prep      a0  community offsets + per-row intra segment               pinned: brute force
  *   or_order_roots     a1  Knob-1 root order (Table 1; S4.1 P:653-680)  pinned: invariants, chi^2
  *   or_sample_hop      a2  Knob-2 biased fanout sampling (S4.2 P:683-691)   pinned: exact law, chi^2
+ *   or_community_order NEXT-2 (iii) community reordering of an unordered graph     pinned: isomorphism, brute force
  *   or_relabel_hop     a3  dedup + relabel into a block (Alg.1 l.4)     pinned: brute force
  *   or_gather          a4  X_in = X[nodes]                                 pinned: memcmp
  *   or_sage_mean       a5  GraphSAGE mean aggregation               pinned: fp64 closed form
@@ -341,6 +342,44 @@ int64_t or_sample_hop(const int32_t *dst_nodes, int64_t n_dst, const int64_t *in
     }
     free(intra_set); free(inter_set); free(sel); free(W);
     return out;
+}
+
+/* ------------------------------------------------------------------ NEXT-2 (iii) */
+/* Community reordering of a graph that is NOT community-ordered (
+ * the paper assumes community-ordered inputs; reading R25): the new id order
+ * sorts the nodes by (community, old id); perm[new] = old, inv[old] = new; row new i is old
+ * row perm[i] with every neighbour u renamed inv[u] and the row sorted ascending; the community
+ * array becomes comm[perm[i]] (non-decreasing).  indptr_out [n+1], indices_out [nnz],
+ * comm_out [n], perm [n], inv [n] are caller-allocated.  Returns 0. */
+static const int32_t *g_sort_comm;
+static int cmp_by_comm(const void *a, const void *b) {
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    if (g_sort_comm[x] != g_sort_comm[y]) return g_sort_comm[x] < g_sort_comm[y] ? -1 : 1;
+    return (x > y) - (x < y);
+}
+static int cmp_i32(const void *a, const void *b) {
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    return (x > y) - (x < y);
+}
+
+int or_community_order(int64_t n, const int64_t *indptr, const int32_t *indices,
+                       const int32_t *comm, int32_t *perm, int32_t *inv, int64_t *indptr_out,
+                       int32_t *indices_out, int32_t *comm_out) {
+    for (int64_t i = 0; i < n; ++i) perm[i] = (int32_t)i;
+    g_sort_comm = comm;
+    qsort(perm, (size_t)n, sizeof(int32_t), cmp_by_comm);
+    for (int64_t i = 0; i < n; ++i) inv[perm[i]] = (int32_t)i;
+    indptr_out[0] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t v = perm[i];
+        const int64_t d = indptr[v + 1] - indptr[v];
+        int32_t *row = indices_out + indptr_out[i];
+        for (int64_t k = 0; k < d; ++k) row[k] = inv[indices[indptr[v] + k]];
+        qsort(row, (size_t)d, sizeof(int32_t), cmp_i32);
+        indptr_out[i + 1] = indptr_out[i] + d;
+        comm_out[i] = comm[v];
+    }
+    return 0;
 }
 
 /* ------------------------------------------------------------------ a3 */
