@@ -268,6 +268,22 @@ CMB_API cmb_status cmb_scatter_rows(const float* rows, int64_t rows_ld, const in
                                     const int64_t* n_dev, int64_t n_cap, int32_t feat_dim,
                                     float* out, int64_t out_ld, void* stream);
 
+/* ------------------------------------------------------------------ NEXT-2 (iii): reorder */
+/* Community reordering of a graph that is NOT community-ordered (
+ * reading R25): new ids sort the nodes by (community, old id); perm[new] = old,
+ * inv[old] = new; row i of the output is old row perm[i] renamed through inv and sorted;
+ * community_out[i] = community[perm[i]] (non-decreasing, ready for cmb_load_graph).  All
+ * arrays are device, caller-allocated: perm / inv / community_out [N], indptr_out [N+1],
+ * indices_out [nnz].  N and nnz < 2^31.  Feature rows and train ids follow the permutation
+ * (e.g. cmb_gather_rows with perm; train_new = sort(inv[train])). */
+CMB_API size_t cmb_community_order_workspace_bytes(int64_t num_nodes, int64_t nnz);
+CMB_API cmb_status cmb_community_order(const int64_t* indptr, const int32_t* indices,
+                                       const int32_t* community, int64_t num_nodes, int64_t nnz,
+                                       int32_t num_communities, int32_t* perm, int32_t* inv,
+                                       int64_t* indptr_out, int32_t* indices_out,
+                                       int32_t* community_out, void* workspace,
+                                       size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------ step executor */
 /* Where cmb_step_group writes the a4 + a5 outputs of one batch (see cmb_gather_aggregate). */
 typedef struct {

@@ -47,6 +47,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_shard_plan", "cmb_gather_rows", "cmb_scatter_rows",
            "cmb_gather_aggregate_sharded", "cmb_ipc_export", "cmb_ipc_open", "cmb_ipc_close",
            "cmb_step_group", "cmb_feature_cache_bytes", "cmb_feature_cache_init",
+           "cmb_community_order_workspace_bytes", "cmb_community_order",
            "cmb_cache_gather_aggregate",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
@@ -147,6 +148,8 @@ def lib():
             "cmb_step_group": (I32, [P, ctypes.POINTER(Batch), ctypes.POINTER(BatchFeatures), I32,
                                      P, I32, D, I32, U64, P, P]),
             "cmb_feature_cache_bytes": (SZ, [I64, I64, I64, I64]),
+            "cmb_community_order_workspace_bytes": (SZ, [I64, I64]),
+            "cmb_community_order": (I32, [P, P, P, I64, I64, I32, P, P, P, P, P, P, SZ, P]),
             "cmb_feature_cache_init": (I32, [P, SZ, I64, I64, I64, I64, P]),
             "cmb_cache_gather_aggregate": (I32, [P, ctypes.POINTER(Blocks), I32, I64, I64,
                                                  ctypes.POINTER(FeatureCacheDesc), I32,
@@ -527,6 +530,26 @@ def sample_multi(samplers: Sequence["Sampler"], roots: Sequence[torch.Tensor],
     _check(lib().cmb_sample_blocks_multi(s0.graph.handle, arr, n, s0._f, s0.L, float(p),
                                          _law(law), int(seed), _stream()))
     return [BatchView(s.nodes, s.sizes, s.indptr, s.indices, s.mask) for s in samplers]
+
+
+def community_order(indptr, indices, community, num_communities: int, device="cuda"):
+    """NEXT-2 (iii): community-ordered relabelling of an arbitrary graph on the GPU ->
+    (perm new->old, inv old->new, indptr, indices, community) device tensors (reading R25)."""
+    dev = torch.device(device)
+    ip = _dev_tensor(indptr, torch.int64, dev)
+    ix = _dev_tensor(indices, torch.int32, dev)
+    cm = _dev_tensor(community, torch.int32, dev)
+    n, nnz = int(ip.shape[0] - 1), int(ix.shape[0])
+    perm = torch.empty(n, dtype=torch.int32, device=dev)
+    inv = torch.empty(n, dtype=torch.int32, device=dev)
+    ip2 = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    ix2 = torch.empty(max(1, nnz), dtype=torch.int32, device=dev)
+    cm2 = torch.empty(n, dtype=torch.int32, device=dev)
+    ws = _workspace(lib().cmb_community_order_workspace_bytes(n, nnz), dev)
+    _check(lib().cmb_community_order(_ptr(ip), _ptr(ix), _ptr(cm), n, nnz, int(num_communities),
+                                     _ptr(perm), _ptr(inv), _ptr(ip2), _ptr(ix2), _ptr(cm2),
+                                     _ptr(ws), ws.numel(), _stream()))
+    return perm, inv, ip2, ix2[:nnz], cm2
 
 
 def gather_features(graph: Graph, node_ids: torch.Tensor, n_dev: torch.Tensor, out: torch.Tensor):
