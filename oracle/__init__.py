@@ -216,3 +216,31 @@ def run_batch(prep: Prep, X, F, roots, fanouts, p, seed, batch, scratch=None, la
     H, H64 = sage_mean(blk["indptr"][L - 1], blk["indices"][L - 1], Xin, F)
     blk.update({"X_in": Xin, "H": H, "H64": H64})
     return blk
+
+
+# ---------------------------------------------------------------- NEXT-4: first SAGEConv layer
+def sage_conv(X_dst, H, W_self, W_neigh, bias=None, relu=False) -> np.ndarray:
+    """Forward of the input-side GraphSAGE layer (reading R26), fp64.
+
+    Eq. (1) (the layer update X^{l+1} = sigma(A' X^l W^l)) in the
+    GraphSAGE-mean form its footnote points to (Hamilton et al.; the paper trains
+    GraphSAGE, hidden dim 256):
+
+        Y[d, :] = sigma( X_dst[d, :] @ W_self + H[d, :] @ W_neigh + bias )
+
+    X_dst = X_in[0:n_dst] (the dst nodes are the prefix of the src nodes, reading R8),
+    H = the a5 mean aggregate of the same rows, W_self / W_neigh are F x Fo (row-major,
+    Y = X W as in Eq. (1)), sigma = ReLU when relu else identity.  Exact fp64 on the given
+    values: the bf16 operand rounding of the GPU kernel is NOT modelled here; the parity
+    tests bound it (R26).  Test infrastructure only (see the module header).
+    """
+    X = np.asarray(X_dst, dtype=np.float64)
+    Hn = np.asarray(H, dtype=np.float64)
+    Ws = np.asarray(W_self, dtype=np.float64)
+    Wn = np.asarray(W_neigh, dtype=np.float64)
+    Y = X @ Ws + Hn @ Wn
+    if bias is not None:
+        Y = Y + np.asarray(bias, dtype=np.float64)[None, :]
+    if relu:
+        Y = np.maximum(Y, 0.0)
+    return Y

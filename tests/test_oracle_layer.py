@@ -1,0 +1,107 @@
+"""Pins for the oracle's first SAGEConv layer (NEXT-4, reading R26; Eq. (1)
+in the GraphSAGE-mean form of its footnote; GraphSAGE trained with hidden dim 256,
+P:770-774).  CPU only: a hand-computed worked example (tests/golden/), the special cases that
+reduce the layer to a copy of X_dst or of H, an explicit-loop brute force on tiny inputs, the
+linearity / ReLU / column-permutation laws, and the composition with the C oracle's a5 mean."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "sage_layer_worked.txt")
+
+
+def _golden():
+    out = {}
+    with open(GOLD) as fh:
+        for line in fh:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            key, rest = line.split(None, 1)
+            rows = [[float(t) for t in r.split()] for r in rest.split(";")]
+            out[key] = np.array(rows if len(rows) > 1 else rows[0], dtype=np.float64)
+    return out
+
+
+def test_worked_example():
+    g = _golden()
+    y = oracle.sage_conv(g["X_dst"], g["H"], g["W_self"], g["W_neigh"], g["bias"], relu=False)
+    assert np.array_equal(y, g["Y_linear"])
+    y = oracle.sage_conv(g["X_dst"], g["H"], g["W_self"], g["W_neigh"], g["bias"], relu=True)
+    assert np.array_equal(y, g["Y_relu"])
+
+
+def test_special_cases_reduce_to_copies():
+    rng = np.random.default_rng(1)
+    n, F = 37, 11
+    X = rng.standard_normal((n, F))
+    H = rng.standard_normal((n, F))
+    eye, zero = np.eye(F), np.zeros((F, F))
+    assert np.array_equal(oracle.sage_conv(X, H, eye, zero), X)      # self path only
+    assert np.array_equal(oracle.sage_conv(X, H, zero, eye), H)      # neighbour path only
+    # a unit column picks one feature of each path: Y[:, 0] = X[:, 3] + H[:, 5]
+    ws, wn = np.zeros((F, 2)), np.zeros((F, 2))
+    ws[3, 0] = 1.0
+    wn[5, 0] = 1.0
+    wn[7, 1] = -2.0
+    y = oracle.sage_conv(X, H, ws, wn, bias=np.array([0.0, 0.25]))
+    assert np.array_equal(y[:, 0], X[:, 3] + H[:, 5])
+    assert np.array_equal(y[:, 1], -2.0 * H[:, 7] + 0.25)
+
+
+def test_brute_force_loops():
+    rng = np.random.default_rng(2)
+    for trial in range(5):
+        n, F, Fo = int(rng.integers(1, 6)), int(rng.integers(1, 7)), int(rng.integers(1, 5))
+        X, H = rng.standard_normal((n, F)), rng.standard_normal((n, F))
+        Ws, Wn = rng.standard_normal((F, Fo)), rng.standard_normal((F, Fo))
+        b = rng.standard_normal(Fo)
+        y = oracle.sage_conv(X, H, Ws, Wn, b, relu=True)
+        for d in range(n):
+            for o in range(Fo):
+                s = b[o]
+                for f in range(F):
+                    s += X[d, f] * Ws[f, o]
+                for f in range(F):
+                    s += H[d, f] * Wn[f, o]
+                assert abs(y[d, o] - max(s, 0.0)) <= 1e-12 * (1 + abs(s))
+
+
+def test_linearity_relu_and_permutation():
+    rng = np.random.default_rng(3)
+    n, F, Fo = 50, 9, 6
+    X, H = rng.standard_normal((n, F)), rng.standard_normal((n, F))
+    Ws, Wn = rng.standard_normal((F, Fo)), rng.standard_normal((F, Fo))
+    b = rng.standard_normal(Fo)
+    y = oracle.sage_conv(X, H, Ws, Wn, b)
+    # linear in the weights (exact for a power-of-two scale), additive in the bias
+    assert np.array_equal(oracle.sage_conv(X, H, 4 * Ws, 4 * Wn, 4 * b), 4 * y)
+    assert np.allclose(oracle.sage_conv(X, H, Ws, Wn), y - b[None, :], rtol=0, atol=1e-12)
+    # ReLU is max(0, .) of the linear output
+    assert np.array_equal(oracle.sage_conv(X, H, Ws, Wn, b, relu=True), np.maximum(y, 0))
+    # permuting output columns of the weights permutes Y's columns (no transposed operand)
+    perm = rng.permutation(Fo)
+    assert np.array_equal(oracle.sage_conv(X, H, Ws[:, perm], Wn[:, perm], b[perm]), y[:, perm])
+    # swapping the two paths swaps the roles of X_dst and H
+    assert np.array_equal(oracle.sage_conv(H, X, Wn, Ws, b), y)
+
+
+def test_composes_with_a5_mean(tiny_prep, tiny_bundle):
+    """W_self = 0, W_neigh = I returns the C oracle's fp64 a5 mean of the input-side block."""
+    from gen import CONFIGS
+    cfg = CONFIGS["tiny"]
+    order = oracle.order_roots(tiny_bundle.train, tiny_bundle.comm, cfg.num_communities,
+                               oracle.MODE_RAND, 0.0, 7, 0)
+    roots = oracle.batch_roots(order, cfg.batch_size, 0)
+    ref = oracle.run_batch(tiny_prep, tiny_bundle.X, cfg.feat_dim, roots, cfg.fanouts,
+                           cfg.p_intra, 7, 0)
+    L = len(cfg.fanouts)
+    nd = ref["n"][L - 1]
+    F = cfg.feat_dim
+    y = oracle.sage_conv(ref["X_in"][:nd], ref["H64"], np.zeros((F, F)), np.eye(F))
+    assert np.array_equal(y, ref["H64"])
+    y = oracle.sage_conv(ref["X_in"][:nd], ref["H64"], np.eye(F), np.zeros((F, F)))
+    assert np.array_equal(y, ref["X_in"][:nd].astype(np.float64))
