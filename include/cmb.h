@@ -10,6 +10,7 @@
  *   a4 cmb_gather_features       input-feature rows of the sub-graph
  *   a5 cmb_sage_mean_aggregate   GraphSAGE mean aggregation of the input-side block
  *   a4+a5 cmb_gather_aggregate   both in one pass over the feature table
+ *   NEXT-4 cmb_sage_layer_forward  a4+a5 fused with the first GraphSAGE layer (tcgen05 bf16 GEMM)
  *
  * Conventions (all entry points):
  *  - extern "C", plain pointers and sizes; "device" = CUDA global memory of the
@@ -363,6 +364,37 @@ CMB_API cmb_status cmb_ipc_export(const void* dev_ptr, void* handle, uint64_t* o
  * mapped base (pass it to cmb_ipc_close).  Fails (CMB_ERR_CUDA) in the exporting process. */
 CMB_API cmb_status cmb_ipc_open(const void* handle, uint64_t offset, void** dev_ptr, void** base);
 CMB_API cmb_status cmb_ipc_close(void* base);
+
+/* ------------------------------------------------------------------ NEXT-4: first SAGE layer */
+/* SURVEY.md 8(f) NEXT-4, reading R26: the input-side GraphSAGE-mean layer of the
+ * model the paper trains (Eq. (1), in the GraphSAGE form of its footnote,
+ * P:501; 3-layer GraphSAGE, hidden dim 256), fused with a4 + a5:
+ *     Y[d, :] = sigma( X[nodes[d]] W_self + H[d] W_neigh + bias ),   d < n_{L-1},
+ * H = the a5 mean of hop L-1 (neighbours only, R12), sigma = ReLU if relu else identity.
+ * Operands are rounded to bf16, products accumulate in fp32 on the tensor cores (tcgen05, TMEM);
+ * H and X_in are never written.  Accuracy: |Y - exact| <= 2^-7 * (|X_dst||W_self| + |H||W_neigh|
+ * + |b|) (+ 2^-8 |Y| for a bf16 output), see R26.
+ *
+ * cmb_sage_weights_bytes: size of the packed weight image for feat_dim F (1..128) and out_dim Fo
+ * (16..256, a multiple of 16); 0 if unsupported.
+ * cmb_sage_pack_weights: w_self, w_neigh = device fp32 [F x Fo] row-major (Y = X W); writes the
+ * bf16 image (device, caller-owned, 16-B aligned, >= cmb_sage_weights_bytes) in the tensor
+ * cores' K-major 128-byte-swizzled operand layout.  Pack once per weight update.
+ * cmb_sage_layer_forward: reads the feature table of g (feat_dim <= 128, ld % 4 == 0) through
+ * blocks (filled by cmb_sample_blocks; last_src_ids required), w_img (packed for g's F and
+ * out_dim), bias (device fp32 [Fo] or NULL); writes out (device, fp32 if out_bf16 == 0 else
+ * bf16, row stride out_ld elements >= Fo, rows 16-B aligned) for d < the device count
+ * n_{L-1} <= n_last_dst_cap.  One persistent CTA per SM (~197 KB shared memory, 256 TMEM
+ * columns).  Host-checkable errors return CMB_ERR_INVALID_ARGUMENT. */
+CMB_API size_t cmb_sage_weights_bytes(int32_t feat_dim, int32_t out_dim);
+CMB_API cmb_status cmb_sage_pack_weights(const float* w_self, const float* w_neigh,
+                                         int32_t feat_dim, int32_t out_dim, void* w_img,
+                                         size_t w_img_bytes, void* stream);
+CMB_API cmb_status cmb_sage_layer_forward(const cmb_graph* g, const cmb_blocks* blocks,
+                                          int32_t n_hops, int64_t n_last_dst_cap,
+                                          const void* w_img, const float* bias, int32_t out_dim,
+                                          int32_t relu, int32_t out_bf16, void* out,
+                                          int64_t out_ld, void* stream);
 
 /* ------------------------------------------------------------------ status */
 /* Synchronises `stream`, returns (and clears) the sticky device status word of a

@@ -49,6 +49,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_step_group", "cmb_feature_cache_bytes", "cmb_feature_cache_init",
            "cmb_community_order_workspace_bytes", "cmb_community_order",
            "cmb_cache_gather_aggregate",
+           "cmb_sage_weights_bytes", "cmb_sage_pack_weights", "cmb_sage_layer_forward",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -154,6 +155,10 @@ def lib():
             "cmb_cache_gather_aggregate": (I32, [P, ctypes.POINTER(Blocks), I32, I64, I64,
                                                  ctypes.POINTER(FeatureCacheDesc), I32,
                                                  ctypes.c_uint32, P, I64, P, I64, P, P]),
+            "cmb_sage_weights_bytes": (SZ, [I32, I32]),
+            "cmb_sage_pack_weights": (I32, [P, P, I32, I32, P, SZ, P]),
+            "cmb_sage_layer_forward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, P, I32, I32,
+                                             I32, P, I64, P]),
             "cmb_get_device_status": (I32, [P, P]),
             "cmb_status_string": (ctypes.c_char_p, [I32]),
             "cmb_last_error_message": (ctypes.c_char_p, []),
@@ -409,6 +414,17 @@ class Sampler:
             _ptr(x_in), x_in.stride(0), _ptr(h), h.stride(0), _ptr(cache.stats), _stream()))
         return x_in, h
 
+    def sage_layer(self, layer: "SageLayer", out: Optional[torch.Tensor] = None):
+        """NEXT-4: a4 + a5 fused with the first GraphSAGE layer for the last sampled batch ->
+        Y [n_cap[L-1], out_dim] (rows < n_{L-1} valid), fp32 or bf16 as the layer says."""
+        if out is None:
+            out = layer.alloc_out(self.n_cap[self.L - 1])
+        _check(lib().cmb_sage_layer_forward(
+            self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
+            _ptr(layer.w_img), _ptr(layer.bias), layer.out_dim, int(layer.relu),
+            int(layer.out_bf16), _ptr(out), out.stride(0), _stream()))
+        return out
+
     def alloc_features_ld(self, ld: int):
         if self.x_in is None or self.x_in.stride(0) != ld:
             dev = self.graph.device
@@ -418,6 +434,39 @@ class Sampler:
 
     def status(self):
         return lib().cmb_get_device_status(_ptr(self.workspace), _stream())
+
+
+class SageLayer:
+    """NEXT-4 (R26): weights of the input-side SAGEConv-mean layer, packed once into the
+    tensor cores' bf16 operand image.  w_self / w_neigh: [F, out_dim] (Y = X W), bias: [out_dim]."""
+
+    def __init__(self, w_self: torch.Tensor, w_neigh: torch.Tensor, bias=None, relu=True,
+                 out_bf16=False, device=None):
+        F, fo = int(w_self.shape[0]), int(w_self.shape[1])
+        if tuple(w_neigh.shape) != (F, fo):
+            raise ValueError("w_self and w_neigh must both be [F, out_dim]")
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        nbytes = lib().cmb_sage_weights_bytes(F, fo)
+        if nbytes == 0:
+            raise ValueError(f"unsupported layer shape F={F}, out_dim={fo} (F <= 128, out_dim in "
+                             f"[16, 256], a multiple of 16)")
+        self.feat_dim, self.out_dim = F, fo
+        self.relu, self.out_bf16 = bool(relu), bool(out_bf16)
+        self.w_self = _dev_tensor(w_self, torch.float32, dev)
+        self.w_neigh = _dev_tensor(w_neigh, torch.float32, dev)
+        self.bias = None if bias is None else _dev_tensor(bias, torch.float32, dev)
+        self.w_img = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.device = dev
+        self.repack()
+
+    def repack(self):
+        _check(lib().cmb_sage_pack_weights(_ptr(self.w_self), _ptr(self.w_neigh), self.feat_dim,
+                                           self.out_dim, _ptr(self.w_img), self.w_img.numel(),
+                                           _stream()))
+
+    def alloc_out(self, rows: int) -> torch.Tensor:
+        dt = torch.bfloat16 if self.out_bf16 else torch.float32
+        return torch.empty(max(1, rows), self.out_dim, dtype=dt, device=self.device)
 
 
 class FeatureCache:

@@ -10,7 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libcmb.so")
-SOURCES = ["capi.cu", "graph.cu", "order.cu", "sample.cu", "features.cu", "shard.cu", "peer.cu", "runtime.cu", "cache.cu", "reorder.cu"]
+SOURCES = ["capi.cu", "graph.cu", "order.cu", "sample.cu", "features.cu", "shard.cu", "peer.cu", "runtime.cu", "cache.cu", "reorder.cu",
+           "sage_layer.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v",
@@ -30,14 +31,19 @@ def build(force=False, verbose=False):
         return SO
     bdir = os.path.join(HERE, "build")
     os.makedirs(bdir, exist_ok=True)
-    objs = []
-    for src in SOURCES:
+    def one(src):
         obj = os.path.join(bdir, src.replace(".cu", ".o"))
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        log = os.path.join(bdir, src + ".ptxas.log")
-        with open(log, "w") as fh:
+        with open(os.path.join(bdir, src + ".ptxas.log"), "w") as fh:
             fh.write(r.stdout + r.stderr)
+        return src, obj, r
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(one, SOURCES))
+    objs = []
+    for src, obj, r in results:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed for {src}")

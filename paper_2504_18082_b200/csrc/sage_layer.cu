@@ -1,0 +1,420 @@
+// sage_layer.cu -- NEXT-4: the input-side GraphSAGE-mean layer fused with a4 + a5
+// on the 5th-generation tensor cores (reading R26; Eq. (1) in the GraphSAGE form
+// of its footnote; hidden dim 256):
+//
+//     Y[d, :] = sigma( X[nodes[d]] W_self + mean_{e in row d} X[gid[e]] W_neigh + b ),  d < n_{L-1}
+//
+// One persistent CTA per SM (512 threads), tiles of M = 128 dst rows.  Per tile:
+//  1. gather: every warp builds 8 rows of the A operand [X_dst | H] (K = 2 halves of kh*64
+//     columns) straight from the feature table -- the self row and the deg neighbour rows of a row
+//     are loaded back to back (two rows in flight per warp), H = fp32 sum in CSR order times
+//     RN(1/deg) -- converted to bf16 and stored into shared memory in the UMMA canonical K-major
+//     SWIZZLE_128B layout (8-row x 128-byte atoms, 16-byte chunk j of row r at chunk j ^ (r & 7):
+//     a warp writing one row touches 8 distinct chunk slots, no bank conflicts);
+//  2. one elected thread issues 2*ceil(F/16) tcgen05.mma.cta_group::1.kind::f16 (M=128, N=Fo,
+//     K=16, bf16 x bf16 -> fp32 in TMEM) against the packed weight image, resident in shared memory
+//     for the whole launch, and commits them to an mbarrier;
+//  3. epilogue: warp w reads TMEM lanes 32*(w%4).. (its lane quarter) with tcgen05.ld 32x32b.x16,
+//     adds the bias, applies ReLU and stores fp32 or bf16 rows.
+// H and X_in never reach HBM: the layer reads the feature rows once per reference and writes only
+// Y, which is what makes it HBM-bound rather than tensor-bound (K = 2F <= 256: ~2*K flops per
+// 4*(1+deg)*F bytes read).
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace cmb {
+namespace sl {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kM = 128;              // UMMA M (rows per tile)
+constexpr int kRowsPerWarp = kM / kWarps;  // 8
+constexpr int kAtomBytes = 128;      // one row of a SWIZZLE_128B atom (64 bf16)
+
+__host__ __device__ inline uint32_t w_img_bytes(int kh, int fo) {
+  return static_cast<uint32_t>(2 * kh) * static_cast<uint32_t>(fo) * kAtomBytes;
+}
+__host__ __device__ inline uint32_t a_bytes(int kh) {
+  return static_cast<uint32_t>(2 * kh) * kM * kAtomBytes;
+}
+inline size_t smem_bytes(int kh, int fo) {
+  return 1024 /*alignment slack*/ + w_img_bytes(kh, fo) + a_bytes(kh) + 64 /*barrier, tmem slot*/ +
+         static_cast<size_t>(fo) * 4 /*bias*/;
+}
+// byte offset of element (row r, column c of half h) in a K-major SWIZZLE_128B operand image whose
+// atoms hold `rows` rows each (atom = h*kh + c/64)
+__host__ __device__ inline uint32_t sw128_off(int r, int h, int c, int kh, int rows) {
+  const int atom = h * kh + (c >> 6);
+  const int j = (c & 63) >> 3;
+  return static_cast<uint32_t>(atom) * rows * kAtomBytes + (r >> 3) * 1024 + (r & 7) * 128 +
+         ((j ^ (r & 7)) << 4) + ((c & 7) << 1);
+}
+
+// ----------------------------------------------------------------- PTX wrappers (tcgen05, mbarrier)
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// UMMA shared-memory descriptor: start >> 4 [0,14), LBO >> 4 [16,30) (unused for swizzled K-major),
+// SBO >> 4 [32,46) = 1024 B between 8-row groups, version 1 [46,48), layout SWIZZLE_128B = 2 [61,64)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
+  return static_cast<uint64_t>((addr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+// instruction descriptor of kind::f16: D fp32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1, both
+// K-major, N >> 3 at [17,23), M >> 4 at [24,29)
+__host__ __device__ inline uint32_t idesc_bf16(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float4 ldg4nc(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 pack_bf16x4(float4 v) {
+  const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
+  const __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
+  return make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+}
+
+// ----------------------------------------------------------------- weight packing
+// w_img[element (n, k)] = bf16(W_h[c][n]) for k = half h, column c < F; 0 for the padding columns
+__global__ void k_pack_weights(const float* __restrict__ w_self, const float* __restrict__ w_neigh,
+                               int F, int fo, int kh, __nv_bfloat16* __restrict__ img) {
+  const int kcols = kh * 64;
+  const int64_t total = static_cast<int64_t>(2 * kcols) * fo;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int n = static_cast<int>(i % fo);
+    const int k = static_cast<int>(i / fo);
+    const int h = k / kcols, c = k % kcols;
+    float v = 0.f;
+    if (c < F) v = (h == 0 ? w_self : w_neigh)[static_cast<int64_t>(c) * fo + n];
+    img[sw128_off(n, h, c, kh, fo) >> 1] = __float2bfloat16_rn(v);
+  }
+}
+
+// ----------------------------------------------------------------- the fused layer kernel
+template <int DMAX>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_sage_layer(const int32_t* __restrict__ indptr, const int32_t* __restrict__ gid,
+                 const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
+                 const float4* __restrict__ x, int64_t ld4, const int32_t* __restrict__ map,
+                 int F, int kh, const uint4* __restrict__ w_img, const float* __restrict__ bias,
+                 int fo, int tmem_cols, int relu, int out_bf16, void* __restrict__ out,
+                 int64_t out_ld) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
+  const uint32_t wbytes = w_img_bytes(kh, fo);
+  uint8_t* sW = smem;
+  uint8_t* sA = sW + wbytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sA + a_bytes(kh));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  float* sbias = reinterpret_cast<float*>(bar + 8);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
+  const int64_t ntiles = (n_dst + kM - 1) / kM;
+
+  // weight image and bias -> shared memory, once per launch
+  for (uint32_t i = tid; i < wbytes / 16; i += kThreads)
+    reinterpret_cast<uint4*>(sW)[i] = __ldg(w_img + i);
+  for (int i = tid; i < fo; i += kThreads) sbias[i] = bias ? __ldg(bias + i) : 0.f;
+  if (tid == 0) {
+    mbar_init(saddr(bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     saddr(tmem_slot)),
+                 "r"(tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int f4 = (F + 3) >> 2;
+  const int c0 = lane * 4;                // this lane's 4 columns of each half
+  const bool col_live = c0 < kh * 64;     // inside the operand's K extent
+  const bool col_data = lane < f4;        // holds (some) feature columns
+  const int steps = (F + 15) >> 4;        // K = 16 MMA steps per half
+  const uint32_t idesc = idesc_bf16(kM, fo);
+  const uint32_t sA_addr = saddr(sA), sW_addr = saddr(sW);
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t phase = 0;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // ---------------------------------------------------------------- 1. gather -> A (bf16)
+    const int64_t rbase = tile * kM + warp * kRowsPerWarp;
+    const int64_t rem = n_dst - rbase;
+    const int nr = rem <= 0 ? 0 : (rem >= kRowsPerWarp ? kRowsPerWarp : static_cast<int>(rem));
+    int32_t ip = 0, self = 0;
+    if (lane <= nr) ip = __ldg(indptr + rbase + lane);
+    if (lane < nr) self = __ldg(map + rbase + lane);
+    int32_t e_lo[kRowsPerWarp], deg[kRowsPerWarp], g[kRowsPerWarp], sv[kRowsPerWarp];
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      e_lo[k] = __shfl_sync(0xffffffffu, ip, k);
+      deg[k] = k < nr ? __shfl_sync(0xffffffffu, ip, k + 1) - e_lo[k] : 0;
+      sv[k] = __shfl_sync(0xffffffffu, self, k);
+      g[k] = lane < deg[k] ? __ldg(gid + e_lo[k] + lane) : 0;
+    }
+#pragma unroll
+    for (int k0 = 0; k0 < kRowsPerWarp; k0 += 2) {
+      float4 s[2], acc[2], v[2][DMAX];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = k0 + u;
+        const bool live = k < nr && col_data;
+        s[u] = live ? ldg4nc(x + static_cast<int64_t>(sv[k]) * ld4 + lane) : zero;
+#pragma unroll
+        for (int j = 0; j < DMAX; ++j) {
+          const int32_t gj = __shfl_sync(0xffffffffu, g[k], j);
+          v[u][j] = (live && j < deg[k]) ? ldg4nc(x + static_cast<int64_t>(gj) * ld4 + lane) : zero;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = k0 + u;
+        acc[u] = zero;
+#pragma unroll
+        for (int j = 0; j < DMAX; ++j) {
+          acc[u].x = __fadd_rn(acc[u].x, v[u][j].x);
+          acc[u].y = __fadd_rn(acc[u].y, v[u][j].y);
+          acc[u].z = __fadd_rn(acc[u].z, v[u][j].z);
+          acc[u].w = __fadd_rn(acc[u].w, v[u][j].w);
+        }
+        // rows with deg > DMAX: the rest of the edges, in CSR order
+        for (int j0 = DMAX; j0 < deg[k]; j0 += DMAX) {
+#pragma unroll
+          for (int j = 0; j < DMAX; ++j) {
+            const int32_t gj = __shfl_sync(0xffffffffu, g[k], (j0 + j) & 31);
+            const float4 w = (col_data && j0 + j < deg[k])
+                                 ? ldg4nc(x + static_cast<int64_t>(gj) * ld4 + lane)
+                                 : zero;
+            acc[u].x = __fadd_rn(acc[u].x, w.x);
+            acc[u].y = __fadd_rn(acc[u].y, w.y);
+            acc[u].z = __fadd_rn(acc[u].z, w.z);
+            acc[u].w = __fadd_rn(acc[u].w, w.w);
+          }
+        }
+        if (k < nr && col_live) {
+          float4 hm = zero;
+          if (deg[k] > 0) {
+            const float y = __frcp_rn(static_cast<float>(deg[k]));
+            hm = make_float4(acc[u].x * y, acc[u].y * y, acc[u].z * y, acc[u].w * y);
+          }
+          float4 sf = s[u];
+          if (c0 + 4 > F) {  // columns at or beyond F are operand padding: exact zeros
+            if (c0 + 0 >= F) sf.x = hm.x = 0.f;
+            if (c0 + 1 >= F) sf.y = hm.y = 0.f;
+            if (c0 + 2 >= F) sf.z = hm.z = 0.f;
+            if (c0 + 3 >= F) sf.w = hm.w = 0.f;
+          }
+          const int r = warp * kRowsPerWarp + k;
+          *reinterpret_cast<uint2*>(sA + sw128_off(r, 0, c0, kh, kM)) = pack_bf16x4(sf);
+          *reinterpret_cast<uint2*>(sA + sw128_off(r, 1, c0, kh, kM)) = pack_bf16x4(hm);
+        }
+      }
+    }
+    fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core (async proxy)
+    __syncthreads();
+
+    // ---------------------------------------------------------------- 2. MMA (one thread)
+    if (tid == 0) {
+      tc_fence_after();
+      uint32_t acc_flag = 0;
+      for (int h = 0; h < 2; ++h) {
+        for (int st = 0; st < steps; ++st) {
+          const uint32_t atom = static_cast<uint32_t>(h * kh + (st >> 2));
+          const uint32_t koff = static_cast<uint32_t>(st & 3) * 32u;
+          const uint64_t da = sw128_desc(sA_addr + atom * (kM * kAtomBytes) + koff);
+          const uint64_t db = sw128_desc(sW_addr + atom * (fo * kAtomBytes) + koff);
+          mma_bf16(tmem, da, db, idesc, acc_flag);
+          acc_flag = 1;
+        }
+      }
+      mma_commit(saddr(bar));
+    }
+    mbar_wait(saddr(bar), phase);
+    phase ^= 1;
+    tc_fence_after();
+
+    // ---------------------------------------------------------------- 3. epilogue
+    {
+      const int q = warp & 3;
+      const int64_t row = tile * kM + q * 32 + lane;
+      const bool live = row < n_dst;
+      for (int ch = warp >> 2; ch < fo / 16; ch += kWarps / 4) {
+        uint32_t v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(ch * 16), v);
+        tmem_ld_wait();
+        float y[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          y[i] = __fadd_rn(__uint_as_float(v[i]), sbias[ch * 16 + i]);
+          if (relu) y[i] = fmaxf(y[i], 0.f);
+        }
+        if (live) {
+          if (out_bf16) {
+            uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + row * out_ld +
+                                                ch * 16);
+            uint32_t p[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[2 * i], y[2 * i + 1]);
+              p[i] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
+            o[0] = make_uint4(p[0], p[1], p[2], p[3]);
+            o[1] = make_uint4(p[4], p[5], p[6], p[7]);
+          } else {
+            float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + row * out_ld + ch * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) o[i] = make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
+          }
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // TMEM drained and A free before the next tile overwrites them
+  }
+
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(tmem_cols)
+                 : "memory");
+  }
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace sl
+}  // namespace cmb
+
+using namespace cmb;
+
+extern "C" {
+
+size_t cmb_sage_weights_bytes(int32_t feat_dim, int32_t out_dim) {
+  if (feat_dim < 1 || feat_dim > 128 || out_dim < 16 || out_dim > 256 || out_dim % 16) return 0;
+  return sl::w_img_bytes((feat_dim + 63) / 64, out_dim);
+}
+
+cmb_status cmb_sage_pack_weights(const float* w_self, const float* w_neigh, int32_t feat_dim,
+                                 int32_t out_dim, void* w_img, size_t w_img_bytes, void* stream) {
+  CMB_ARG(w_self && w_neigh && w_img, "cmb_sage_pack_weights: null argument");
+  const size_t need = cmb_sage_weights_bytes(feat_dim, out_dim);
+  CMB_ARG(need != 0, "cmb_sage_pack_weights: need 1 <= feat_dim <= 128, out_dim in [16, 256] "
+                     "and a multiple of 16 (got %d, %d)", feat_dim, out_dim);
+  CMB_ARG(w_img_bytes >= need, "cmb_sage_pack_weights: w_img_bytes %zu < %zu", w_img_bytes, need);
+  CMB_ARG(sl::aligned16(w_img), "cmb_sage_pack_weights: w_img must be 16-byte aligned");
+  cmb_status st = require_sm100();
+  if (st != CMB_OK) return st;
+  const int kh = (feat_dim + 63) / 64;
+  const int64_t total = static_cast<int64_t>(2 * kh * 64) * out_dim;
+  sl::k_pack_weights<<<static_cast<int>((total + 255) / 256), 256, 0,
+                       static_cast<cudaStream_t>(stream)>>>(
+      w_self, w_neigh, feat_dim, out_dim, kh, static_cast<__nv_bfloat16*>(w_img));
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+cmb_status cmb_sage_layer_forward(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                  int64_t n_last_dst_cap, const void* w_img, const float* bias,
+                                  int32_t out_dim, int32_t relu, int32_t out_bf16, void* out,
+                                  int64_t out_ld, void* stream) {
+  CMB_ARG(g && b && w_img && out, "cmb_sage_layer_forward: null argument");
+  CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_sage_layer_forward: bad n_hops");
+  CMB_ARG(g->d.x != nullptr, "cmb_sage_layer_forward: graph has no feature table");
+  const int F = g->d.f;
+  CMB_ARG(cmb_sage_weights_bytes(F, out_dim) != 0,
+          "cmb_sage_layer_forward: need feat_dim <= 128 and out_dim in [16, 256], a multiple of 16 "
+          "(got %d, %d)", F, out_dim);
+  CMB_ARG(b->last_src_ids != nullptr, "cmb_sage_layer_forward: blocks->last_src_ids is required");
+  CMB_ARG(g->d.ld % 4 == 0 && sl::aligned16(g->d.x), "cmb_sage_layer_forward: feature rows must "
+                                                      "be 16-byte aligned (ld %% 4 == 0)");
+  CMB_ARG(out_ld >= out_dim && out_ld % (out_bf16 ? 8 : 4) == 0 && sl::aligned16(out),
+          "cmb_sage_layer_forward: out_ld must be >= out_dim and keep rows 16-byte aligned");
+  CMB_ARG(sl::aligned16(w_img), "cmb_sage_layer_forward: w_img must be 16-byte aligned");
+  CMB_ARG(n_last_dst_cap >= 0 && n_last_dst_cap <= b->nodes_cap,
+          "cmb_sage_layer_forward: bad n_last_dst_cap");
+  if (n_last_dst_cap == 0) return CMB_OK;
+  const int L = n_hops;
+  const int kh = (F + 63) / 64;
+  const int cols = out_dim <= 32 ? 32 : out_dim <= 64 ? 64 : out_dim <= 128 ? 128 : 256;
+  const size_t smem = sl::smem_bytes(kh, out_dim);
+  static size_t configured = 0;
+  if (configured < smem) {
+    CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_layer<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sl::smem_bytes(2, 256))));
+    configured = sl::smem_bytes(2, 256);
+  }
+  const int64_t tiles = (n_last_dst_cap + sl::kM - 1) / sl::kM;
+  const int grid = static_cast<int>(tiles < g->num_sms ? tiles : g->num_sms);
+  sl::k_sage_layer<6><<<grid, sl::kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      b->indptr[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,
+      reinterpret_cast<const float4*>(g->d.x), g->d.ld / 4, b->nodes, F, kh,
+      static_cast<const uint4*>(w_img), bias, out_dim, cols, relu, out_bf16, out, out_ld);
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+}  // extern "C"

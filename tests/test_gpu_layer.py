@@ -1,0 +1,150 @@
+"""GPU parity of NEXT-4, the input-side SAGEConv-mean layer fused with a4 + a5 on the tensor cores
+(cmb_sage_layer_forward, reading R26), through the C ABI, against oracle.sage_conv on the
+oracle's own blocks, X_in and fp64 H.
+
+Bound (R26, derived from the arithmetic): bf16 operands (2^-9 relative each), fp32 accumulation
+over K <= 256 terms, optional bf16 output:
+    |Y_gpu - Y| <= 2^-7 * S + 2^-8 * |Y| (bf16 out),  S = |X_dst||W_self| + |H||W_neigh| + |b|.
+With bf16-representable features and weights and W_neigh = 0 the operands are exact and only fp32
+accumulation is left: 2^-16 * S."""
+import copy
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gen import CONFIGS, generate, scaled
+
+pytestmark = pytest.mark.gpu
+
+cmb = pytest.importorskip("paper_2504_18082_b200")
+
+SEED = 42
+_CACHE = {}
+
+
+def _bundle(name, factor=None):
+    key = (name, factor)
+    if key not in _CACHE:
+        cfg = CONFIGS[name] if factor is None else scaled(CONFIGS[name], factor)
+        b = generate(cfg)
+        _CACHE[key] = (b, oracle.graph_prep(b), cmb.Graph.from_bundle(b))
+    return _CACHE[key]
+
+
+def _weights(F, fo, seed, bf16_exact=False):
+    g = torch.Generator().manual_seed(seed)
+    ws = torch.randn(F, fo, generator=g) / np.sqrt(F)
+    wn = torch.randn(F, fo, generator=g) / np.sqrt(F)
+    b = torch.randn(fo, generator=g) * 0.1
+    if bf16_exact:
+        ws, wn, b = (t.to(torch.bfloat16).float() for t in (ws, wn, b))
+    return ws, wn, b
+
+
+def _run(bundle, prep, graph, fanouts, roots_np, batch_id, layer, p):
+    sampler = cmb.Sampler(graph, len(roots_np), fanouts)
+    sampler.sample(torch.from_numpy(roots_np).cuda(), p, SEED, batch_id)
+    y = sampler.sage_layer(layer)
+    torch.cuda.synchronize()
+    assert sampler.status() == 0
+    ref = oracle.run_batch(prep, bundle.X, bundle.cfg.feat_dim, roots_np, fanouts, p, SEED,
+                           batch_id)
+    L = len(fanouts)
+    nd = ref["n"][L - 1]
+    return y[:nd].float().cpu().numpy().astype(np.float64), ref, nd
+
+
+def _check(yg, ref, nd, F, ws, wn, b, relu, out_bf16, exact=False):
+    Xd = ref["X_in"][:nd, :F].astype(np.float64)
+    H = ref["H64"][:, :F]
+    Y = oracle.sage_conv(Xd, H, ws.double().numpy(), wn.double().numpy(), b.double().numpy(),
+                         relu=relu)
+    S = np.abs(Xd) @ np.abs(ws.double().numpy()) + np.abs(H) @ np.abs(wn.double().numpy()) + \
+        np.abs(b.double().numpy())[None, :]
+    tol = (2.0 ** -16 if exact else 2.0 ** -7) * S + (2.0 ** -8 * np.abs(Y) if out_bf16 else 0.0)
+    err = np.abs(yg - Y)
+    bad = err > tol + 1e-30
+    assert not bad.any(), (f"{bad.sum()} of {bad.size} outside the R26 bound; worst "
+                           f"{np.max(err - tol)} at {np.unravel_index(np.argmax(err - tol), err.shape)}")
+    return float(np.max(err / np.maximum(S, 1e-30)))
+
+
+@pytest.mark.parametrize("name,factor,fo,relu,out_bf16", [
+    ("tiny", None, 256, True, False),        # F = 16: one swizzle atom per half
+    ("tiny", None, 48, False, False),        # narrow N, no activation
+    ("products", 0.01, 256, True, False),    # F = 100: two atoms per half, ragged F and tail
+    ("products", 0.01, 128, False, True),    # bf16 output
+    ("arxiv", None, 256, True, True),        # F = 128: full K = 256
+])
+def test_layer_parity(name, factor, fo, relu, out_bf16):
+    b, prep, g = _bundle(name, factor)
+    cfg = b.cfg
+    F = cfg.feat_dim
+    ws, wn, bias = _weights(F, fo, 7)
+    layer = cmb.SageLayer(ws, wn, bias, relu=relu, out_bf16=out_bf16)
+    order = oracle.order_roots(b.train, b.comm, cfg.num_communities, oracle.MODE_RAND, 0.0, SEED, 0)
+    for bid in (0, 1):
+        roots = oracle.batch_roots(order, cfg.batch_size, bid)
+        yg, ref, nd = _run(b, prep, g, cfg.fanouts, roots, bid, layer, cfg.p_intra)
+        assert nd > 0
+        _check(yg, ref, nd, F, ws, wn, bias, relu, out_bf16)
+
+
+def test_layer_exact_operands():
+    """bf16-representable X and W, W_neigh = 0: only fp32 accumulation separates GPU and oracle,
+    so a layout / indexing / descriptor error cannot hide under the bf16 tolerance."""
+    b0, _, _ = _bundle("products", 0.01)
+    b = copy.copy(b0)
+    b.X = torch.from_numpy(b0.X).to(torch.bfloat16).float().numpy()
+    prep = oracle.graph_prep(b)
+    g = cmb.Graph.from_bundle(b)
+    F = b.cfg.feat_dim
+    ws, _, bias = _weights(F, 256, 11, bf16_exact=True)
+    wn = torch.zeros_like(ws)
+    layer = cmb.SageLayer(ws, wn, bias, relu=False)
+    order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_COMM, 0.25,
+                               SEED, 1)
+    roots = oracle.batch_roots(order, b.cfg.batch_size, 1)
+    yg, ref, nd = _run(b, prep, g, b.cfg.fanouts, roots, 1, layer, 1.0)
+    _check(yg, ref, nd, F, ws, wn, bias, False, False, exact=True)
+    # and the neighbour path alone (W_self = 0): H is not bf16-exact, so the R26 bound applies
+    ws2, wn2, _ = _weights(F, 256, 12)
+    layer2 = cmb.SageLayer(torch.zeros_like(ws2), wn2, None, relu=False)
+    yg, ref, nd = _run(b, prep, g, b.cfg.fanouts, roots, 1, layer2, 1.0)
+    _check(yg, ref, nd, F, torch.zeros_like(ws2), wn2, torch.zeros(256), False, False)
+
+
+def test_layer_full_size_products():
+    """The bench configuration (products-shaped, full size, RAND, p = 0.5): every row of one
+    batch against the oracle (one oracle batch is ~0.3 s)."""
+    b, prep, g = _bundle("products")
+    cfg = b.cfg
+    F = cfg.feat_dim
+    ws, wn, bias = _weights(F, 256, 5)
+    layer = cmb.SageLayer(ws, wn, bias, relu=True)
+    order = oracle.order_roots(b.train, b.comm, cfg.num_communities, oracle.MODE_RAND, 0.0, SEED, 0)
+    roots = oracle.batch_roots(order, cfg.batch_size, 5)
+    yg, ref, nd = _run(b, prep, g, cfg.fanouts, roots, 5, layer, 0.5)
+    assert nd > 100_000  # spans ~1000 tiles of 128 rows
+    _check(yg, ref, nd, F, ws, wn, bias, True, False)
+
+
+def test_layer_edge_cases():
+    b, prep, g = _bundle("tiny")
+    F = b.cfg.feat_dim
+    ws, wn, bias = _weights(F, 64, 3)
+    layer = cmb.SageLayer(ws, wn, bias, relu=False)
+    # a single root (one partial tile) and a zero-degree-heavy p = 1 batch
+    order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_NORAND, 0.0,
+                               SEED, 0)
+    for roots in (order[:1], order[:129]):
+        roots = np.ascontiguousarray(roots)
+        yg, ref, nd = _run(b, prep, g, b.cfg.fanouts, roots, 0, layer, 1.0)
+        _check(yg, ref, nd, F, ws, wn, bias, False, False)
+    # unsupported shapes are host-checked errors
+    with pytest.raises(ValueError):
+        cmb.SageLayer(torch.zeros(F, 20), torch.zeros(F, 20))
+    with pytest.raises(ValueError):
+        cmb.SageLayer(torch.zeros(200, 64), torch.zeros(200, 64))
