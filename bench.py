@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--p", type=float, default=None)
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--no-extra", action="store_true", help="skip the knob-sweep extra points")
+    ap.add_argument("--layer", action="store_true",
+                    help="with --no-extra: still measure the NEXT-4 fused layer point")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--law", default="A", choices=["A", "slot"],
                     help="Knob-2 law: A = weighted w/o replacement (default), slot = R23")
@@ -360,8 +362,11 @@ def run_cmb(args, bundle):
     e2e = run_e2e(args, pipe, cfg, stream, K, W, world, rank)
 
     extra = None
+    layer = None
     if not args.no_extra and world == 1:
         extra = knob_points(bundle, graph, cfg, args, K, flush)
+    if (not args.no_extra or args.layer) and world == 1:
+        layer = layer_point(bundle, graph, cfg, args)
 
     if rank == 0:
         peak, peak_src = measured_peak_hbm()
@@ -402,6 +407,7 @@ def run_cmb(args, bundle):
                                     "kernels": kernel_names},
             "clocks": clk.summary(),
             "knob_points": extra,
+            "next4_layer": layer,
             "graph_meta": {k: (float(v) if isinstance(v, (np.floating, float)) else v)
                            for k, v in bundle.meta.items()},
         }
@@ -518,6 +524,66 @@ def knob_points(bundle, graph, cfg, args, K, flush=False):
                     "gather_aggregate_ms": float(np.mean(agg)),
                     "gather_aggregate_alg_gbps": float(np.mean(alg) / (np.mean(agg) * 1e-3) / 1e9)})
     return pts
+
+
+def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
+    """NEXT-4 (R26): the fused a4 + a5 + first GraphSAGE layer kernel
+    (cmb_sage_layer_forward, tcgen05 bf16 GEMM, hidden dim 256, bf16 output) timed with
+    CUDA events on its stream per batch, next to the a4 + a5 kernel on the same batches.
+    Algorithmic bytes per launch: every unique input row once (n_L * 4F), the index streams
+    (indptr, last-hop src ids, dst ids) and Y (n_{L-1} * 2 Fo); flops 2 * n_{L-1} * 2F * Fo."""
+    import torch
+    import paper_2504_18082_b200 as cmb
+    if cfg.feat_dim > 128:
+        return {"skipped": f"feat_dim {cfg.feat_dim} > 128 (the fused layer keeps K = 2F <= 256 "
+                           f"resident; see DESIGN.md)"}
+    L = len(cfg.fanouts)
+    F = cfg.feat_dim
+    gen = torch.Generator().manual_seed(1)
+    ws = torch.randn(F, fo, generator=gen) / np.sqrt(F)
+    wn = torch.randn(F, fo, generator=gen) / np.sqrt(F)
+    layer = cmb.SageLayer(ws, wn, torch.zeros(fo), relu=True, out_bf16=True, device=graph.device)
+    p = cfg.p_intra if args.p is None else args.p
+    pipe = cmb.MiniBatchPipeline(graph, torch.from_numpy(bundle.train), cfg.batch_size,
+                                 cfg.fanouts, mode=args.mode, mix=args.mix, p=p, seed=args.seed)
+    pipe.start_epoch(0)
+    smp = pipe.sampler
+    out = layer.alloc_out(smp.n_cap[L - 1])
+    s = torch.cuda.current_stream()
+    n = min(n_batches, pipe.n_batches)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n)]
+    sizes = torch.zeros(n, 2 * L + 1, dtype=torch.int64, device=graph.device)
+    for warm in range(3):
+        smp.sample(pipe.batch_roots(warm), p, args.seed, warm)
+        smp.sage_layer(layer, out)
+        smp.gather_aggregate()
+    torch.cuda.synchronize()
+    for k in range(n):
+        smp.sample(pipe.batch_roots(k), p, args.seed, k)
+        ev[k][0].record(s)
+        smp.sage_layer(layer, out)
+        ev[k][1].record(s)
+        smp.gather_aggregate()
+        ev[k][2].record(s)
+        sizes[k].copy_(smp.sizes, non_blocking=True)
+    torch.cuda.synchronize()
+    assert smp.status() == 0
+    t_layer = np.array([e[0].elapsed_time(e[1]) for e in ev])
+    t_agg = np.array([e[1].elapsed_time(e[2]) for e in ev])
+    sz = sizes.cpu().numpy()
+    nL, nd, ed = sz[:, L], sz[:, L - 1], sz[:, L + 1 + L - 1]
+    alg = nL * 4 * F + 4 * (nd + 1) + 4 * ed + 4 * nd + nd * 2 * fo
+    flops = 2.0 * nd * 2 * F * fo
+    peak, peak_src = measured_peak_hbm()
+    gbps = float(np.mean(alg) / (np.mean(t_layer) * 1e-3) / 1e9)
+    return {"kernel": "k_sage_layer (a4+a5+SAGEConv layer 1, tcgen05 bf16, cmb_sage_layer_forward)",
+            "out_dim": fo, "out_dtype": "bf16", "relu": True, "batches": int(n),
+            "layer_ms": float(np.mean(t_layer)), "gather_aggregate_ms_same_batches": float(np.mean(t_agg)),
+            "dst_rows_per_batch": float(nd.mean()), "unique_input_rows_per_batch": float(nL.mean()),
+            "algorithmic_bytes_per_launch": float(np.mean(alg)),
+            "roofline": {"bound": "hbm", "achieved": gbps, "peak": peak, "peak_source": peak_src,
+                         "unit": "GB/s", "frac": gbps / peak},
+            "tensor_tflops": float(np.mean(flops) / (np.mean(t_layer) * 1e-3) / 1e12)}
 
 
 def main():
