@@ -6,16 +6,22 @@
 //
 // One persistent CTA per SM (512 threads), tiles of M = 128 dst rows.  Per tile:
 //  1. gather: every warp builds 8 rows of the A operand [X_dst | H] (K = 2 halves of kh*64
-//     columns) straight from the feature table -- the self row and the deg neighbour rows of a row
-//     are loaded back to back (two rows in flight per warp), H = fp32 sum in CSR order times
-//     RN(1/deg) -- converted to bf16 and stored into shared memory in the UMMA canonical K-major
-//     SWIZZLE_128B layout (8-row x 128-byte atoms, 16-byte chunk j of row r at chunk j ^ (r & 7):
-//     a warp writing one row touches 8 distinct chunk slots, no bank conflicts);
-//  2. one elected thread issues 2*ceil(F/16) tcgen05.mma.cta_group::1.kind::f16 (M=128, N=Fo,
-//     K=16, bf16 x bf16 -> fp32 in TMEM) against the packed weight image, resident in shared memory
+//     columns) straight from the feature table -- all edge-id shuffles of a group of RIF rows
+//     first, then the self row and the deg neighbour rows of each row issued back to back
+//     (RIF x (1 + DMAX) 16-byte loads in flight per lane), the next tile's indptr / dst ids /
+//     edge ids prefetched behind them; H = fp32 sum in CSR order times RN(1/deg); converted to
+//     bf16 and stored into shared memory in the UMMA canonical K-major SWIZZLE_128B layout
+//     (8-row x 128-byte atoms, 16-byte chunk j of row r at chunk j ^ (r & 7): a warp writing
+//     one row touches 8 distinct chunk slots, no bank conflicts);
+//  2. one thread issues 2*ceil(F/16) tcgen05.mma.cta_group::1.kind::f16 (M=128, N=Fo, K=16,
+//     bf16 x bf16 -> fp32 in TMEM) against the packed weight image, resident in shared memory
 //     for the whole launch, and commits them to an mbarrier;
 //  3. epilogue: warp w reads TMEM lanes 32*(w%4).. (its lane quarter) with tcgen05.ld 32x32b.x16,
-//     adds the bias, applies ReLU and stores fp32 or bf16 rows.
+//     adds the bias, applies ReLU and stores fp32 or bf16 rows (L2 evict_first).
+// Measured (profiles/r01_ncu_full_k_sage_layer.txt): the tensor pipe is ~7% busy; the kernel is
+// bound by the latency of the random row loads, like a4+a5.  A warp-specialised form (4 epilogue
+// warps, 8 gather warps, double-buffered TMEM) was slower (160 vs 116 us on products): fewer
+// gather warps means fewer loads in flight, and the register file, not the barriers, is the limit.
 // H and X_in never reach HBM: the layer reads the feature rows once per reference and writes only
 // Y, which is what makes it HBM-bound rather than tensor-bound (K = 2F <= 256: ~2*K flops per
 // 4*(1+deg)*F bytes read).
@@ -116,12 +122,35 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ float4 ldg4nc(const float4* p) {
+// predicated 16-byte load whose destination is zeroed inside the same asm block (no select after
+// the load, so no later register move waits on this load's scoreboard and the loads of several
+// rows stay in flight together), with an L2 cache policy (createpolicy): feature rows are loaded
+// evict_last so a row several dst rows of the batch reference survives until its next use (the
+// paper's L2 reuse)
+__device__ __forceinline__ float4 ldg4_or_zero(const float4* p, bool pred, uint64_t pol) {
   float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-               : "l"(p));
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\tmov.b32 %2, 0;\n\tmov.b32 %3, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %6;\n\t}"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p), "r"(static_cast<int>(pred)), "l"(pol));
   return r;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st16_hint(uint4* p, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
 }
 __device__ __forceinline__ uint2 pack_bf16x4(float4 v) {
   const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
@@ -147,7 +176,7 @@ __global__ void k_pack_weights(const float* __restrict__ w_self, const float* __
 }
 
 // ----------------------------------------------------------------- the fused layer kernel
-template <int DMAX>
+template <int DMAX, int RIF>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sage_layer(const int32_t* __restrict__ indptr, const int32_t* __restrict__ gid,
                  const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
@@ -167,6 +196,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
   const int64_t ntiles = (n_dst + kM - 1) / kM;
+  constexpr unsigned kFull = 0xffffffffu;
+  const uint64_t pol_keep = l2_evict_last(), pol_stream = l2_evict_first();
 
   // weight image and bias -> shared memory, once per launch
   for (uint32_t i = tid; i < wbytes / 16; i += kThreads)
@@ -199,66 +230,86 @@ __global__ void __launch_bounds__(kThreads, 1)
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t phase = 0;
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    // ---------------------------------------------------------------- 1. gather -> A (bf16)
+  // index state of this warp's 8 rows of a tile: lane-held indptr (9 values) and dst ids (8),
+  // lane j of g[k] = global id of edge j of row k
+  auto load_head = [&](int64_t tile, int32_t& ip, int32_t& self, int& nr) {
     const int64_t rbase = tile * kM + warp * kRowsPerWarp;
     const int64_t rem = n_dst - rbase;
-    const int nr = rem <= 0 ? 0 : (rem >= kRowsPerWarp ? kRowsPerWarp : static_cast<int>(rem));
-    int32_t ip = 0, self = 0;
-    if (lane <= nr) ip = __ldg(indptr + rbase + lane);
-    if (lane < nr) self = __ldg(map + rbase + lane);
-    int32_t e_lo[kRowsPerWarp], deg[kRowsPerWarp], g[kRowsPerWarp], sv[kRowsPerWarp];
+    nr = (tile >= ntiles || rem <= 0) ? 0 : (rem >= kRowsPerWarp ? kRowsPerWarp : static_cast<int>(rem));
+    ip = (lane <= nr && nr > 0) ? __ldg(indptr + rbase + lane) : 0;
+    self = lane < nr ? __ldg(map + rbase + lane) : 0;
+  };
+  auto load_edges = [&](int32_t ip, int nr, int32_t (&g)[kRowsPerWarp]) {
 #pragma unroll
     for (int k = 0; k < kRowsPerWarp; ++k) {
-      e_lo[k] = __shfl_sync(0xffffffffu, ip, k);
-      deg[k] = k < nr ? __shfl_sync(0xffffffffu, ip, k + 1) - e_lo[k] : 0;
-      sv[k] = __shfl_sync(0xffffffffu, self, k);
-      g[k] = lane < deg[k] ? __ldg(gid + e_lo[k] + lane) : 0;
+      const int32_t lo = __shfl_sync(kFull, ip, k);
+      const int32_t hi = __shfl_sync(kFull, ip, k + 1);
+      g[k] = (k < nr && lane < hi - lo) ? __ldg(gid + lo + lane) : 0;
     }
+  };
+  int32_t ip, self, g[kRowsPerWarp];
+  int nr;
+  load_head(blockIdx.x, ip, self, nr);
+  load_edges(ip, nr, g);
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // ---------------------------------------------------------------- 1. gather -> A (bf16)
+    int32_t nip, nself, ng[kRowsPerWarp];
+    int nnr;
+    load_head(tile + gridDim.x, nip, nself, nnr);  // next tile's indices, in flight now
 #pragma unroll
-    for (int k0 = 0; k0 < kRowsPerWarp; k0 += 2) {
-      float4 s[2], acc[2], v[2][DMAX];
+    for (int k0 = 0; k0 < kRowsPerWarp; k0 += RIF) {
+      float4 s[RIF], v[RIF][DMAX];
+      int deg[RIF];
+      int32_t sv[RIF], gj[RIF][DMAX];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < RIF; ++u) {  // all shuffles first, then every load back to back
         const int k = k0 + u;
-        const bool live = k < nr && col_data;
-        s[u] = live ? ldg4nc(x + static_cast<int64_t>(sv[k]) * ld4 + lane) : zero;
+        const int32_t lo = __shfl_sync(kFull, ip, k);
+        const int32_t hi = __shfl_sync(kFull, ip, k + 1);
+        deg[u] = k < nr ? hi - lo : 0;
+        sv[u] = __shfl_sync(kFull, self, k);
 #pragma unroll
-        for (int j = 0; j < DMAX; ++j) {
-          const int32_t gj = __shfl_sync(0xffffffffu, g[k], j);
-          v[u][j] = (live && j < deg[k]) ? ldg4nc(x + static_cast<int64_t>(gj) * ld4 + lane) : zero;
-        }
+        for (int j = 0; j < DMAX; ++j) gj[u][j] = __shfl_sync(kFull, g[k], j);
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < RIF; ++u) {
+        const bool live = k0 + u < nr && col_data;
+        s[u] = ldg4_or_zero(x + static_cast<int64_t>(sv[u]) * ld4 + lane, live, pol_keep);
+#pragma unroll
+        for (int j = 0; j < DMAX; ++j)
+          v[u][j] = ldg4_or_zero(x + static_cast<int64_t>(gj[u][j]) * ld4 + lane,
+                                 live && j < deg[u], pol_keep);
+      }
+      if (k0 == 0) load_edges(nip, nnr, ng);  // next tile's edge ids, behind this group's loads
+#pragma unroll
+      for (int u = 0; u < RIF; ++u) {
         const int k = k0 + u;
-        acc[u] = zero;
+        float4 acc = zero;
 #pragma unroll
         for (int j = 0; j < DMAX; ++j) {
-          acc[u].x = __fadd_rn(acc[u].x, v[u][j].x);
-          acc[u].y = __fadd_rn(acc[u].y, v[u][j].y);
-          acc[u].z = __fadd_rn(acc[u].z, v[u][j].z);
-          acc[u].w = __fadd_rn(acc[u].w, v[u][j].w);
+          acc.x = __fadd_rn(acc.x, v[u][j].x);
+          acc.y = __fadd_rn(acc.y, v[u][j].y);
+          acc.z = __fadd_rn(acc.z, v[u][j].z);
+          acc.w = __fadd_rn(acc.w, v[u][j].w);
         }
-        // rows with deg > DMAX: the rest of the edges, in CSR order
-        for (int j0 = DMAX; j0 < deg[k]; j0 += DMAX) {
+        for (int j0 = DMAX; j0 < deg[u]; j0 += DMAX) {  // rows longer than DMAX, CSR order
 #pragma unroll
           for (int j = 0; j < DMAX; ++j) {
-            const int32_t gj = __shfl_sync(0xffffffffu, g[k], (j0 + j) & 31);
-            const float4 w = (col_data && j0 + j < deg[k])
-                                 ? ldg4nc(x + static_cast<int64_t>(gj) * ld4 + lane)
-                                 : zero;
-            acc[u].x = __fadd_rn(acc[u].x, w.x);
-            acc[u].y = __fadd_rn(acc[u].y, w.y);
-            acc[u].z = __fadd_rn(acc[u].z, w.z);
-            acc[u].w = __fadd_rn(acc[u].w, w.w);
+            const int32_t e = __shfl_sync(kFull, g[k], (j0 + j) & 31);
+            const float4 w = ldg4_or_zero(x + static_cast<int64_t>(e) * ld4 + lane,
+                                          col_data && j0 + j < deg[u], pol_keep);
+            acc.x = __fadd_rn(acc.x, w.x);
+            acc.y = __fadd_rn(acc.y, w.y);
+            acc.z = __fadd_rn(acc.z, w.z);
+            acc.w = __fadd_rn(acc.w, w.w);
           }
         }
         if (k < nr && col_live) {
           float4 hm = zero;
-          if (deg[k] > 0) {
-            const float y = __frcp_rn(static_cast<float>(deg[k]));
-            hm = make_float4(acc[u].x * y, acc[u].y * y, acc[u].z * y, acc[u].w * y);
+          if (deg[u] > 0) {
+            const float y = __frcp_rn(static_cast<float>(deg[u]));
+            hm = make_float4(acc.x * y, acc.y * y, acc.z * y, acc.w * y);
           }
           float4 sf = s[u];
           if (c0 + 4 > F) {  // columns at or beyond F are operand padding: exact zeros
@@ -321,18 +372,26 @@ __global__ void __launch_bounds__(kThreads, 1)
               const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[2 * i], y[2 * i + 1]);
               p[i] = *reinterpret_cast<const uint32_t*>(&b2);
             }
-            o[0] = make_uint4(p[0], p[1], p[2], p[3]);
-            o[1] = make_uint4(p[4], p[5], p[6], p[7]);
+            st16_hint(o, make_uint4(p[0], p[1], p[2], p[3]), pol_stream);
+            st16_hint(o + 1, make_uint4(p[4], p[5], p[6], p[7]), pol_stream);
           } else {
-            float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + row * out_ld + ch * 16);
+            uint4* o = reinterpret_cast<uint4*>(static_cast<float*>(out) + row * out_ld + ch * 16);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) o[i] = make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
+            for (int i = 0; i < 4; ++i)
+              st16_hint(o + i, make_uint4(__float_as_uint(y[4 * i]), __float_as_uint(y[4 * i + 1]),
+                                          __float_as_uint(y[4 * i + 2]), __float_as_uint(y[4 * i + 3])),
+                        pol_stream);
           }
         }
       }
     }
     tc_fence_before();
     __syncthreads();  // TMEM drained and A free before the next tile overwrites them
+    ip = nip;
+    self = nself;
+    nr = nnr;
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) g[k] = ng[k];
   }
 
   __syncthreads();
@@ -401,18 +460,30 @@ cmb_status cmb_sage_layer_forward(const cmb_graph* g, const cmb_blocks* b, int32
   const int kh = (F + 63) / 64;
   const int cols = out_dim <= 32 ? 32 : out_dim <= 64 ? 64 : out_dim <= 128 ? 128 : 256;
   const size_t smem = sl::smem_bytes(kh, out_dim);
-  static size_t configured = 0;
-  if (configured < smem) {
-    CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_layer<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sl::smem_bytes(2, 256))));
-    configured = sl::smem_bytes(2, 256);
-  }
+  const size_t smem_max = sl::smem_bytes(2, 256);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t tiles = (n_last_dst_cap + sl::kM - 1) / sl::kM;
   const int grid = static_cast<int>(tiles < g->num_sms ? tiles : g->num_sms);
-  sl::k_sage_layer<6><<<grid, sl::kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
-      b->indptr[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,
-      reinterpret_cast<const float4*>(g->d.x), g->d.ld / 4, b->nodes, F, kh,
-      static_cast<const uint4*>(w_img), bias, out_dim, cols, relu, out_bf16, out, out_ld);
+  const int dmax = static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap);  // max fanout
+  static bool configured = false;
+  if (!configured) {
+    CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_layer<5, 2>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem_max)));
+    CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_layer<10, 2>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem_max)));
+    configured = true;
+  }
+#define CMB_LAYER_ARGS                                                                        \
+  b->indptr[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,                     \
+      reinterpret_cast<const float4*>(g->d.x), g->d.ld / 4, b->nodes, F, kh,                 \
+      static_cast<const uint4*>(w_img), bias, out_dim, cols, relu, out_bf16, out, out_ld
+  if (dmax <= 5)
+    sl::k_sage_layer<5, 2><<<grid, sl::kThreads, smem, s>>>(CMB_LAYER_ARGS);
+  else
+    sl::k_sage_layer<10, 2><<<grid, sl::kThreads, smem, s>>>(CMB_LAYER_ARGS);
+#undef CMB_LAYER_ARGS
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
 }

@@ -148,3 +148,18 @@ def test_layer_edge_cases():
         cmb.SageLayer(torch.zeros(F, 20), torch.zeros(F, 20))
     with pytest.raises(ValueError):
         cmb.SageLayer(torch.zeros(200, 64), torch.zeros(200, 64))
+
+
+@pytest.mark.parametrize("fanouts", [(10, 8), (4, 15), (3, 32)])
+def test_layer_wide_fanouts(fanouts):
+    """Last-hop fanouts above 5 take the DMAX = 10 kernel; above 10 the long-row loop (edges
+    folded in CSR order in chunks of DMAX), up to the 32-edge maximum."""
+    b, prep, g = _bundle("products", 0.01)
+    F = b.cfg.feat_dim
+    ws, wn, bias = _weights(F, 128, 9)
+    layer = cmb.SageLayer(ws, wn, bias, relu=True)
+    order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_RAND, 0.0,
+                               SEED, 0)
+    roots = np.ascontiguousarray(oracle.batch_roots(order, 512, 1))
+    yg, ref, nd = _run(b, prep, g, list(fanouts), roots, 1, layer, 0.7)
+    _check(yg, ref, nd, F, ws, wn, bias, True, False)
