@@ -244,3 +244,20 @@ def sage_conv(X_dst, H, W_self, W_neigh, bias=None, relu=False) -> np.ndarray:
     if relu:
         Y = np.maximum(Y, 0.0)
     return Y
+
+
+def sage_conv_backward(X_dst, H, dY, Y=None, relu=False):
+    """Weight gradients of the input-side GraphSAGE layer (NEXT-4 backward, reading R27), fp64.
+
+    For Y = sigma(Z), Z = X_dst W_self + H W_neigh + b (sage_conv) and an upstream gradient dY:
+    dZ = dY * sigma'(Z) (ReLU: 1[Y > 0], the decision taken on the given Y; identity: 1),
+    dW_self = X_dst^T dZ, dW_neigh = H^T dZ, db = sum_d dZ[d, :] -- the chain rule on Eq. (1)
+    (training learns W^l by minimising the loss).  X_dst and H of the first
+    layer are inputs (features), so no gradient flows to them.  Returns (dW_self, dW_neigh, db).
+    """
+    X = np.asarray(X_dst, dtype=np.float64)
+    Hn = np.asarray(H, dtype=np.float64)
+    dZ = np.asarray(dY, dtype=np.float64)
+    if relu:
+        dZ = dZ * (np.asarray(Y, dtype=np.float64) > 0)
+    return X.T @ dZ, Hn.T @ dZ, dZ.sum(axis=0)

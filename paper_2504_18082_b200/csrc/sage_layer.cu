@@ -176,6 +176,134 @@ __global__ void k_pack_weights(const float* __restrict__ w_self, const float* __
 }
 
 // ----------------------------------------------------------------- the fused layer kernel
+// Builds the A operand [X_dst | H] of 128-row tiles (bf16, K-major SWIZZLE_128B, one 16-KB atom
+// per 64 columns of each half) straight from the feature table.  Each of the 16 warps owns 8 rows
+// of a tile: all edge-id shuffles of a group of RIF rows first, then the self row and the deg edge
+// rows of each row issued back to back as predicated loads; H = fp32 sum in CSR order times
+// RN(1/deg).  The next tile's indptr / dst ids / edge ids are loaded behind the current loads.
+template <int DMAX, int RIF>
+struct ATileGather {
+  const int32_t* indptr;
+  const int32_t* gid;
+  const int32_t* map;
+  const float4* x;
+  int64_t ld4;
+  int F, kh;
+  int64_t n_dst, ntiles;
+  int warp, lane;
+  uint64_t pol;
+  int32_t ip, self, g[kRowsPerWarp];  // current tile: lane-held indptr (9) and dst ids (8)
+  int nr;
+  int32_t nip, nself, ng[kRowsPerWarp];  // next tile
+  int nnr;
+
+  __device__ __forceinline__ void load_head(int64_t tile, int32_t& ip_, int32_t& self_, int& nr_) {
+    const int64_t rbase = tile * kM + warp * kRowsPerWarp;
+    const int64_t rem = n_dst - rbase;
+    nr_ = (tile >= ntiles || rem <= 0) ? 0 : (rem >= kRowsPerWarp ? kRowsPerWarp : static_cast<int>(rem));
+    ip_ = (lane <= nr_ && nr_ > 0) ? __ldg(indptr + rbase + lane) : 0;
+    self_ = lane < nr_ ? __ldg(map + rbase + lane) : 0;
+  }
+  // lane j of g_[k] = global id of edge j of row k
+  __device__ __forceinline__ void load_edges(int32_t ip_, int nr_, int32_t (&g_)[kRowsPerWarp]) {
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const int32_t lo = __shfl_sync(0xffffffffu, ip_, k);
+      const int32_t hi = __shfl_sync(0xffffffffu, ip_, k + 1);
+      g_[k] = (k < nr_ && lane < hi - lo) ? __ldg(gid + lo + lane) : 0;
+    }
+  }
+  __device__ __forceinline__ void start(int64_t tile) {
+    load_head(tile, ip, self, nr);
+    load_edges(ip, nr, g);
+  }
+  __device__ __forceinline__ void advance() {
+    ip = nip;
+    self = nself;
+    nr = nnr;
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) g[k] = ng[k];
+  }
+  // gathers the current tile into sA (rows past n_dst: skipped, or zero-filled if zero_dead) and
+  // starts loading the indices of tile `next`
+  __device__ __forceinline__ void build(int64_t next, uint8_t* sA, bool zero_dead) {
+    constexpr unsigned kFull = 0xffffffffu;
+    const int f4 = (F + 3) >> 2;
+    const int c0 = lane * 4;             // this lane's 4 columns of each half
+    const bool col_live = c0 < kh * 64;  // inside the operand's K extent
+    const bool col_data = lane < f4;     // holds (some) feature columns
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    load_head(next, nip, nself, nnr);
+#pragma unroll
+    for (int k0 = 0; k0 < kRowsPerWarp; k0 += RIF) {
+      float4 s[RIF], v[RIF][DMAX];
+      int deg[RIF];
+      int32_t sv[RIF], gj[RIF][DMAX];
+#pragma unroll
+      for (int u = 0; u < RIF; ++u) {  // all shuffles first, then every load back to back
+        const int k = k0 + u;
+        const int32_t lo = __shfl_sync(kFull, ip, k);
+        const int32_t hi = __shfl_sync(kFull, ip, k + 1);
+        deg[u] = k < nr ? hi - lo : 0;
+        sv[u] = __shfl_sync(kFull, self, k);
+#pragma unroll
+        for (int j = 0; j < DMAX; ++j) gj[u][j] = __shfl_sync(kFull, g[k], j);
+      }
+#pragma unroll
+      for (int u = 0; u < RIF; ++u) {
+        const bool live = k0 + u < nr && col_data;
+        s[u] = ldg4_or_zero(x + static_cast<int64_t>(sv[u]) * ld4 + lane, live, pol);
+#pragma unroll
+        for (int j = 0; j < DMAX; ++j)
+          v[u][j] = ldg4_or_zero(x + static_cast<int64_t>(gj[u][j]) * ld4 + lane,
+                                 live && j < deg[u], pol);
+      }
+      if (k0 == 0) load_edges(nip, nnr, ng);  // next tile's edge ids, behind this group's loads
+#pragma unroll
+      for (int u = 0; u < RIF; ++u) {
+        const int k = k0 + u;
+        float4 acc = zero;
+#pragma unroll
+        for (int j = 0; j < DMAX; ++j) {
+          acc.x = __fadd_rn(acc.x, v[u][j].x);
+          acc.y = __fadd_rn(acc.y, v[u][j].y);
+          acc.z = __fadd_rn(acc.z, v[u][j].z);
+          acc.w = __fadd_rn(acc.w, v[u][j].w);
+        }
+        for (int j0 = DMAX; j0 < deg[u]; j0 += DMAX) {  // rows longer than DMAX, CSR order
+#pragma unroll
+          for (int j = 0; j < DMAX; ++j) {
+            const int32_t e = __shfl_sync(kFull, g[k], (j0 + j) & 31);
+            const float4 w = ldg4_or_zero(x + static_cast<int64_t>(e) * ld4 + lane,
+                                          col_data && j0 + j < deg[u], pol);
+            acc.x = __fadd_rn(acc.x, w.x);
+            acc.y = __fadd_rn(acc.y, w.y);
+            acc.z = __fadd_rn(acc.z, w.z);
+            acc.w = __fadd_rn(acc.w, w.w);
+          }
+        }
+        if (col_live && (k < nr || zero_dead)) {
+          float4 hm = zero;
+          if (deg[u] > 0) {
+            const float y = __frcp_rn(static_cast<float>(deg[u]));
+            hm = make_float4(acc.x * y, acc.y * y, acc.z * y, acc.w * y);
+          }
+          float4 sf = s[u];
+          if (c0 + 4 > F) {  // columns at or beyond F are operand padding: exact zeros
+            if (c0 + 0 >= F) sf.x = hm.x = 0.f;
+            if (c0 + 1 >= F) sf.y = hm.y = 0.f;
+            if (c0 + 2 >= F) sf.z = hm.z = 0.f;
+            if (c0 + 3 >= F) sf.w = hm.w = 0.f;
+          }
+          const int r = warp * kRowsPerWarp + k;
+          *reinterpret_cast<uint2*>(sA + sw128_off(r, 0, c0, kh, kM)) = pack_bf16x4(sf);
+          *reinterpret_cast<uint2*>(sA + sw128_off(r, 1, c0, kh, kM)) = pack_bf16x4(hm);
+        }
+      }
+    }
+  }
+};
+
 template <int DMAX, int RIF>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sage_layer(const int32_t* __restrict__ indptr, const int32_t* __restrict__ gid,
@@ -196,7 +324,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
   const int64_t ntiles = (n_dst + kM - 1) / kM;
-  constexpr unsigned kFull = 0xffffffffu;
   const uint64_t pol_keep = l2_evict_last(), pol_stream = l2_evict_first();
 
   // weight image and bias -> shared memory, once per launch
@@ -220,110 +347,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int f4 = (F + 3) >> 2;
-  const int c0 = lane * 4;                // this lane's 4 columns of each half
-  const bool col_live = c0 < kh * 64;     // inside the operand's K extent
-  const bool col_data = lane < f4;        // holds (some) feature columns
   const int steps = (F + 15) >> 4;        // K = 16 MMA steps per half
   const uint32_t idesc = idesc_bf16(kM, fo);
   const uint32_t sA_addr = saddr(sA), sW_addr = saddr(sW);
-  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t phase = 0;
 
-  // index state of this warp's 8 rows of a tile: lane-held indptr (9 values) and dst ids (8),
-  // lane j of g[k] = global id of edge j of row k
-  auto load_head = [&](int64_t tile, int32_t& ip, int32_t& self, int& nr) {
-    const int64_t rbase = tile * kM + warp * kRowsPerWarp;
-    const int64_t rem = n_dst - rbase;
-    nr = (tile >= ntiles || rem <= 0) ? 0 : (rem >= kRowsPerWarp ? kRowsPerWarp : static_cast<int>(rem));
-    ip = (lane <= nr && nr > 0) ? __ldg(indptr + rbase + lane) : 0;
-    self = lane < nr ? __ldg(map + rbase + lane) : 0;
-  };
-  auto load_edges = [&](int32_t ip, int nr, int32_t (&g)[kRowsPerWarp]) {
-#pragma unroll
-    for (int k = 0; k < kRowsPerWarp; ++k) {
-      const int32_t lo = __shfl_sync(kFull, ip, k);
-      const int32_t hi = __shfl_sync(kFull, ip, k + 1);
-      g[k] = (k < nr && lane < hi - lo) ? __ldg(gid + lo + lane) : 0;
-    }
-  };
-  int32_t ip, self, g[kRowsPerWarp];
-  int nr;
-  load_head(blockIdx.x, ip, self, nr);
-  load_edges(ip, nr, g);
+  ATileGather<DMAX, RIF> ga;
+  ga.indptr = indptr;
+  ga.gid = gid;
+  ga.map = map;
+  ga.x = x;
+  ga.ld4 = ld4;
+  ga.F = F;
+  ga.kh = kh;
+  ga.n_dst = n_dst;
+  ga.ntiles = ntiles;
+  ga.warp = warp;
+  ga.lane = lane;
+  ga.pol = pol_keep;
+  ga.start(blockIdx.x);
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     // ---------------------------------------------------------------- 1. gather -> A (bf16)
-    int32_t nip, nself, ng[kRowsPerWarp];
-    int nnr;
-    load_head(tile + gridDim.x, nip, nself, nnr);  // next tile's indices, in flight now
-#pragma unroll
-    for (int k0 = 0; k0 < kRowsPerWarp; k0 += RIF) {
-      float4 s[RIF], v[RIF][DMAX];
-      int deg[RIF];
-      int32_t sv[RIF], gj[RIF][DMAX];
-#pragma unroll
-      for (int u = 0; u < RIF; ++u) {  // all shuffles first, then every load back to back
-        const int k = k0 + u;
-        const int32_t lo = __shfl_sync(kFull, ip, k);
-        const int32_t hi = __shfl_sync(kFull, ip, k + 1);
-        deg[u] = k < nr ? hi - lo : 0;
-        sv[u] = __shfl_sync(kFull, self, k);
-#pragma unroll
-        for (int j = 0; j < DMAX; ++j) gj[u][j] = __shfl_sync(kFull, g[k], j);
-      }
-#pragma unroll
-      for (int u = 0; u < RIF; ++u) {
-        const bool live = k0 + u < nr && col_data;
-        s[u] = ldg4_or_zero(x + static_cast<int64_t>(sv[u]) * ld4 + lane, live, pol_keep);
-#pragma unroll
-        for (int j = 0; j < DMAX; ++j)
-          v[u][j] = ldg4_or_zero(x + static_cast<int64_t>(gj[u][j]) * ld4 + lane,
-                                 live && j < deg[u], pol_keep);
-      }
-      if (k0 == 0) load_edges(nip, nnr, ng);  // next tile's edge ids, behind this group's loads
-#pragma unroll
-      for (int u = 0; u < RIF; ++u) {
-        const int k = k0 + u;
-        float4 acc = zero;
-#pragma unroll
-        for (int j = 0; j < DMAX; ++j) {
-          acc.x = __fadd_rn(acc.x, v[u][j].x);
-          acc.y = __fadd_rn(acc.y, v[u][j].y);
-          acc.z = __fadd_rn(acc.z, v[u][j].z);
-          acc.w = __fadd_rn(acc.w, v[u][j].w);
-        }
-        for (int j0 = DMAX; j0 < deg[u]; j0 += DMAX) {  // rows longer than DMAX, CSR order
-#pragma unroll
-          for (int j = 0; j < DMAX; ++j) {
-            const int32_t e = __shfl_sync(kFull, g[k], (j0 + j) & 31);
-            const float4 w = ldg4_or_zero(x + static_cast<int64_t>(e) * ld4 + lane,
-                                          col_data && j0 + j < deg[u], pol_keep);
-            acc.x = __fadd_rn(acc.x, w.x);
-            acc.y = __fadd_rn(acc.y, w.y);
-            acc.z = __fadd_rn(acc.z, w.z);
-            acc.w = __fadd_rn(acc.w, w.w);
-          }
-        }
-        if (k < nr && col_live) {
-          float4 hm = zero;
-          if (deg[u] > 0) {
-            const float y = __frcp_rn(static_cast<float>(deg[u]));
-            hm = make_float4(acc.x * y, acc.y * y, acc.z * y, acc.w * y);
-          }
-          float4 sf = s[u];
-          if (c0 + 4 > F) {  // columns at or beyond F are operand padding: exact zeros
-            if (c0 + 0 >= F) sf.x = hm.x = 0.f;
-            if (c0 + 1 >= F) sf.y = hm.y = 0.f;
-            if (c0 + 2 >= F) sf.z = hm.z = 0.f;
-            if (c0 + 3 >= F) sf.w = hm.w = 0.f;
-          }
-          const int r = warp * kRowsPerWarp + k;
-          *reinterpret_cast<uint2*>(sA + sw128_off(r, 0, c0, kh, kM)) = pack_bf16x4(sf);
-          *reinterpret_cast<uint2*>(sA + sw128_off(r, 1, c0, kh, kM)) = pack_bf16x4(hm);
-        }
-      }
-    }
+    ga.build(tile + gridDim.x, sA, false);
     fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core (async proxy)
     __syncthreads();
 
@@ -387,11 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();  // TMEM drained and A free before the next tile overwrites them
-    ip = nip;
-    self = nself;
-    nr = nnr;
-#pragma unroll
-    for (int k = 0; k < kRowsPerWarp; ++k) g[k] = ng[k];
+    ga.advance();
   }
 
   __syncthreads();

@@ -105,3 +105,56 @@ def test_composes_with_a5_mean(tiny_prep, tiny_bundle):
     assert np.array_equal(y, ref["H64"])
     y = oracle.sage_conv(ref["X_in"][:nd], ref["H64"], np.eye(F), np.zeros((F, F)))
     assert np.array_equal(y, ref["X_in"][:nd].astype(np.float64))
+
+
+# ---------------------------------------------------------------- backward (reading R27)
+def _loss(X, H, Ws, Wn, b, G, relu):
+    """L = sum(G * Y): dL/dY = G, so its gradient in W is what sage_conv_backward returns."""
+    return float(np.sum(G * oracle.sage_conv(X, H, Ws, Wn, b, relu=relu)))
+
+
+@pytest.mark.parametrize("relu", [False, True])
+def test_backward_matches_finite_differences(relu):
+    """Central differences of the forward oracle (exact for the linear layer up to rounding; for
+    ReLU away from the kinks) -- a check that does not reuse the transpose formula."""
+    rng = np.random.default_rng(5)
+    n, F, Fo = 12, 5, 4
+    X, H = rng.standard_normal((n, F)), rng.standard_normal((n, F))
+    Ws, Wn, b = rng.standard_normal((F, Fo)), rng.standard_normal((F, Fo)), rng.standard_normal(Fo)
+    G = rng.standard_normal((n, Fo))
+    Y = oracle.sage_conv(X, H, Ws, Wn, b, relu=relu)
+    dWs, dWn, db = oracle.sage_conv_backward(X, H, G, Y, relu=relu)
+    eps = 1e-6
+    for (W, dW) in ((Ws, dWs), (Wn, dWn)):
+        for i in range(F):
+            for j in range(Fo):
+                W[i, j] += eps
+                lp = _loss(X, H, Ws, Wn, b, G, relu)
+                W[i, j] -= 2 * eps
+                lm = _loss(X, H, Ws, Wn, b, G, relu)
+                W[i, j] += eps
+                assert abs((lp - lm) / (2 * eps) - dW[i, j]) <= 1e-6 * (1 + abs(dW[i, j]))
+    for j in range(Fo):
+        b[j] += eps
+        lp = _loss(X, H, Ws, Wn, b, G, relu)
+        b[j] -= 2 * eps
+        lm = _loss(X, H, Ws, Wn, b, G, relu)
+        b[j] += eps
+        assert abs((lp - lm) / (2 * eps) - db[j]) <= 1e-6 * (1 + abs(db[j]))
+
+
+def test_backward_worked_example():
+    """Hand arithmetic on the golden layer: with dY = ones and no activation,
+    dW_self[f, o] = sum_d X_dst[d, f] = [0, 2.5], dW_neigh[f, o] = sum_d H[d, f] = [2.5, 1],
+    db = [2, 2, 2] (n = 2 rows)."""
+    g = _golden()
+    dY = np.ones((2, 3))
+    dWs, dWn, db = oracle.sage_conv_backward(g["X_dst"], g["H"], dY)
+    assert np.array_equal(dWs, np.array([[0.0] * 3, [2.5] * 3]))
+    assert np.array_equal(dWn, np.array([[2.5] * 3, [1.0] * 3]))
+    assert np.array_equal(db, np.array([2.0, 2.0, 2.0]))
+    # ReLU masks the rows whose output is not positive: Y_relu has zeros at (0,2) and (1,1)
+    dWs, dWn, db = oracle.sage_conv_backward(g["X_dst"], g["H"], dY, g["Y_relu"], relu=True)
+    assert np.array_equal(db, np.array([2.0, 1.0, 1.0]))
+    assert np.array_equal(dWs[:, 2], np.array([-1.0, 0.5]))   # only row 1 contributes to col 2
+    assert np.array_equal(dWn[:, 1], np.array([0.5, -1.0]))   # only row 0 contributes to col 1
