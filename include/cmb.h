@@ -396,6 +396,23 @@ CMB_API cmb_status cmb_sage_layer_forward(const cmb_graph* g, const cmb_blocks* 
                                           int32_t relu, int32_t out_bf16, void* out,
                                           int64_t out_ld, void* stream);
 
+/* NEXT-4 backward (reading R27): weight gradients of the same layer for one batch,
+ *     dZ = dY * 1[Y > 0] (y != NULL; y = NULL: dZ = dY),
+ *     dW_self = X_dst^T dZ,  dW_neigh = H^T dZ,  db = sum_d dZ[d, :],
+ * with [X_dst | H] recomputed from the feature table exactly as the forward builds it (bf16
+ * operands, fp32 accumulation on the tensor cores per CTA, fp64 sum of the per-CTA partials:
+ * deterministic).  dy, y: device bf16 [n_{L-1} x out_dim], row stride dy_ld / y_ld elements
+ * (multiples of 8, 16-B aligned).  dw: device fp32 [2 x F x out_dim] (dW_self then dW_neigh,
+ * row-major like the forward's W); db: device fp32 [out_dim].  out_dim: a power of two in
+ * [16, 256]; F <= 128.  workspace: device, >= cmb_sage_backward_workspace_bytes (partials).
+ * Accuracy: |dW - exact| <= 2^-7 * |A|^T |dZ|, |db - exact| <= 2^-12 * sum |dZ| (R27). */
+CMB_API size_t cmb_sage_backward_workspace_bytes(int32_t feat_dim, int32_t out_dim);
+CMB_API cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* blocks,
+                                           int32_t n_hops, int64_t n_last_dst_cap,
+                                           const void* dy, int64_t dy_ld, const void* y,
+                                           int64_t y_ld, int32_t out_dim, float* dw, float* db,
+                                           void* workspace, size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------ status */
 /* Synchronises `stream`, returns (and clears) the sticky device status word of a
  * graph / order / sample workspace. */

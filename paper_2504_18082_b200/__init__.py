@@ -50,6 +50,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_community_order_workspace_bytes", "cmb_community_order",
            "cmb_cache_gather_aggregate",
            "cmb_sage_weights_bytes", "cmb_sage_pack_weights", "cmb_sage_layer_forward",
+           "cmb_sage_backward_workspace_bytes", "cmb_sage_layer_backward",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -159,6 +160,9 @@ def lib():
             "cmb_sage_pack_weights": (I32, [P, P, I32, I32, P, SZ, P]),
             "cmb_sage_layer_forward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, P, I32, I32,
                                              I32, P, I64, P]),
+            "cmb_sage_backward_workspace_bytes": (SZ, [I32, I32]),
+            "cmb_sage_layer_backward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, I64, P, I64,
+                                              I32, P, P, P, SZ, P]),
             "cmb_get_device_status": (I32, [P, P]),
             "cmb_status_string": (ctypes.c_char_p, [I32]),
             "cmb_last_error_message": (ctypes.c_char_p, []),
@@ -425,6 +429,22 @@ class Sampler:
             int(layer.out_bf16), _ptr(out), out.stride(0), _stream()))
         return out
 
+    def sage_layer_backward(self, layer: "SageLayer", dy: torch.Tensor,
+                            y: Optional[torch.Tensor] = None):
+        """NEXT-4 backward for the last sampled batch: dY (bf16 [>= n_{L-1}, out_dim]) and, for a
+        ReLU layer, its output Y (bf16) -> (dW_self [F, out_dim], dW_neigh, db) fp32."""
+        if dy.dtype != torch.bfloat16 or (y is not None and y.dtype != torch.bfloat16):
+            raise ValueError("dy and y must be bf16")
+        F, fo = layer.feat_dim, layer.out_dim
+        ws = layer.backward_workspace()
+        dw = torch.empty(2, F, fo, dtype=torch.float32, device=layer.device)
+        db = torch.empty(fo, dtype=torch.float32, device=layer.device)
+        _check(lib().cmb_sage_layer_backward(
+            self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
+            _ptr(dy), dy.stride(0), _ptr(y), 0 if y is None else y.stride(0), fo, _ptr(dw),
+            _ptr(db), _ptr(ws), ws.numel(), _stream()))
+        return dw[0], dw[1], db
+
     def alloc_features_ld(self, ld: int):
         if self.x_in is None or self.x_in.stride(0) != ld:
             dev = self.graph.device
@@ -463,6 +483,15 @@ class SageLayer:
         _check(lib().cmb_sage_pack_weights(_ptr(self.w_self), _ptr(self.w_neigh), self.feat_dim,
                                            self.out_dim, _ptr(self.w_img), self.w_img.numel(),
                                            _stream()))
+
+    def backward_workspace(self) -> torch.Tensor:
+        if getattr(self, "_bws", None) is None:
+            n = lib().cmb_sage_backward_workspace_bytes(self.feat_dim, self.out_dim)
+            if n == 0:
+                raise ValueError(f"backward needs out_dim a power of two in [16, 256] "
+                                 f"(got {self.out_dim})")
+            self._bws = torch.empty(n, dtype=torch.uint8, device=self.device)
+        return self._bws
 
     def alloc_out(self, rows: int) -> torch.Tensor:
         dt = torch.bfloat16 if self.out_bf16 else torch.float32

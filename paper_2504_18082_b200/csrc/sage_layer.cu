@@ -27,6 +27,8 @@
 // 4*(1+deg)*F bytes read).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cmb {
@@ -445,6 +447,208 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ----------------------------------------------------------------- NEXT-4 backward (reading R27)
+// Weight gradients of the layer: dW = [X_dst | H]^T dZ, db = sum_rows dZ, dZ = dY * 1[Y > 0].
+// The reduction runs over the dst rows, so the tensor-core problem is transposed with respect to
+// the forward: M = the 2*kh*64 feature rows of A, N = Fo, K = the batch rows.  Each CTA rebuilds
+// the A tile of its 128-row tiles exactly as the forward does (same shared-memory image) and
+// reads it as an MN-major operand (features contiguous; LBO = 16 KB between 64-feature atoms,
+// SBO = 1 KB between 8-row groups); the dZ tile is staged in the same 128-byte-swizzled
+// MN-major layout.  The per-CTA accumulators ([M_all x Fo] fp32, kh x Fo TMEM columns) are
+// written as partials and summed over CTAs in fp64 by a second kernel (deterministic).
+constexpr int kMaxBwdCtas = 160;
+
+__host__ __device__ inline uint32_t b_bytes(int fo) {  // dZ tile: one 16-KB atom per 64 columns
+  return static_cast<uint32_t>((fo + 63) / 64) * kM * kAtomBytes;
+}
+inline size_t bwd_smem_bytes(int kh, int fo) {
+  return 1024 + a_bytes(kh) + b_bytes(fo) + 64 + static_cast<size_t>(fo) * 4;
+}
+// MN-major SWIZZLE_128B descriptor: LBO = byte stride between 64-element MN atoms, SBO = byte
+// stride between 8-row K groups
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t addr, uint32_t lbo) {
+  return static_cast<uint64_t>((addr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>(lbo >> 4) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+template <int DMAX, int RIF>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_sage_layer_bwd(const int32_t* __restrict__ indptr, const int32_t* __restrict__ gid,
+                     const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
+                     const float4* __restrict__ x, int64_t ld4, const int32_t* __restrict__ map,
+                     int F, int kh, const __nv_bfloat16* __restrict__ dy, int64_t dy_ld,
+                     const __nv_bfloat16* __restrict__ y, int64_t y_ld, int fo, int tmem_alloc,
+                     float* __restrict__ part, float* __restrict__ part_db) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + a_bytes(kh);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sB + b_bytes(fo));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  float* sdb = reinterpret_cast<float*>(bar + 8);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
+  const int64_t ntiles = (n_dst + kM - 1) / kM;
+  const uint64_t pol_keep = l2_evict_last();
+  const int m_all = 2 * kh * 64;
+  const int nmb = m_all / kM;  // M = 128 blocks of feature rows (= kh)
+
+  for (int i = tid; i < fo; i += kThreads) sdb[i] = 0.f;
+  if (tid == 0) {
+    mbar_init(saddr(bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     saddr(tmem_slot)),
+                 "r"(tmem_alloc)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  ATileGather<DMAX, RIF> ga;
+  ga.indptr = indptr;
+  ga.gid = gid;
+  ga.map = map;
+  ga.x = x;
+  ga.ld4 = ld4;
+  ga.F = F;
+  ga.kh = kh;
+  ga.n_dst = n_dst;
+  ga.ntiles = ntiles;
+  ga.warp = warp;
+  ga.lane = lane;
+  ga.pol = pol_keep;
+  ga.start(blockIdx.x);
+
+  // dZ staging: thread owns the 8-column chunk c = tid % (fo/8) of rows tid / (fo/8) + i*step
+  const int cpr = fo / 8;           // chunks per row (a power of two dividing kThreads)
+  const int c = tid % cpr;
+  const int rstep = kThreads / cpr;
+  float dbacc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dbacc[i] = 0.f;
+
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
+                         (static_cast<uint32_t>(fo >> 3) << 17) | (static_cast<uint32_t>(kM >> 4) << 24);
+  const uint32_t sA_addr = saddr(sA), sB_addr = saddr(sB);
+  uint32_t phase = 0;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    ga.build(tile + gridDim.x, sA, true);
+    for (int r = tid / cpr; r < kM; r += rstep) {
+      const int64_t row = tile * kM + r;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (row < n_dst) {
+        v = __ldg(reinterpret_cast<const uint4*>(dy + row * dy_ld) + c);
+        if (y) {
+          const uint4 m = __ldg(reinterpret_cast<const uint4*>(y + row * y_ld) + c);
+          const uint32_t* mw = reinterpret_cast<const uint32_t*>(&m);
+          uint32_t* vw = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {  // keep dY where Y > 0 (bf16 sign bit clear, nonzero)
+            const uint32_t lo = mw[i] & 0xFFFFu, hi = mw[i] >> 16;
+            const uint32_t keep = ((lo != 0u && !(lo & 0x8000u)) ? 0xFFFFu : 0u) |
+                                  ((hi != 0u && !(hi & 0x8000u)) ? 0xFFFF0000u : 0u);
+            vw[i] &= keep;
+          }
+        }
+        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f2 = __bfloat1622float2(p2[i]);
+          dbacc[2 * i] += f2.x;
+          dbacc[2 * i + 1] += f2.y;
+        }
+      }
+      const uint32_t off = static_cast<uint32_t>(c >> 3) * (kM * kAtomBytes) + (r >> 3) * 1024 +
+                           (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4);
+      *reinterpret_cast<uint4*>(sB + off) = v;
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      for (int mb = 0; mb < nmb; ++mb) {
+        for (int ks = 0; ks < kM / 16; ++ks) {
+          const uint64_t da = sw128_mn_desc(sA_addr + (2 * mb) * (kM * kAtomBytes) + ks * 2048,
+                                            kM * kAtomBytes);
+          const uint64_t db = sw128_mn_desc(sB_addr + ks * 2048, kM * kAtomBytes);
+          mma_bf16(tmem + static_cast<uint32_t>(mb * fo), da, db, idesc,
+                   (it > 0 || ks > 0) ? 1u : 0u);
+        }
+      }
+      mma_commit(saddr(bar));
+    }
+    mbar_wait(saddr(bar), phase);  // A and B may be overwritten once the MMAs have read them
+    phase ^= 1;
+    tc_fence_after();
+    __syncthreads();
+    ga.advance();
+  }
+
+  // ---------------------------------------------------------------- partials
+  {
+    const int q = warp & 3;
+    for (int mb = 0; mb < nmb; ++mb) {
+      const int m = mb * kM + q * 32 + lane;
+      float* dst = part + (static_cast<int64_t>(blockIdx.x) * m_all + m) * fo;
+      for (int ch = warp >> 2; ch < fo / 16; ch += kWarps / 4) {
+        uint32_t v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) +
+                      static_cast<uint32_t>(mb * fo + ch * 16), v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          reinterpret_cast<float4*>(dst + ch * 16)[i] =
+              it > 0 ? make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                   __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) atomicAdd(&sdb[c * 8 + i], dbacc[i]);
+  tc_fence_before();
+  __syncthreads();
+  for (int i = tid; i < fo; i += kThreads) part_db[static_cast<int64_t>(blockIdx.x) * fo + i] = sdb[i];
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(tmem_alloc)
+                 : "memory");
+  }
+}
+
+// dw[h][f][o] = sum over CTAs of part[cta][h*kh*64 + f][o] (fp64), db[o] = sum of part_db[cta][o]
+__global__ void k_sage_bwd_reduce(const float* __restrict__ part, const float* __restrict__ part_db,
+                                  int nparts, int F, int kh, int fo, float* __restrict__ dw,
+                                  float* __restrict__ db) {
+  const int m_all = 2 * kh * 64;
+  const int64_t nw = 2ll * F * fo;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nw + fo;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    if (i < nw) {
+      const int o = static_cast<int>(i % fo);
+      const int f = static_cast<int>((i / fo) % F);
+      const int h = static_cast<int>(i / (static_cast<int64_t>(F) * fo));
+      const int m = h * kh * 64 + f;
+      for (int p = 0; p < nparts; ++p) s += part[(static_cast<int64_t>(p) * m_all + m) * fo + o];
+      dw[i] = static_cast<float>(s);
+    } else {
+      const int o = static_cast<int>(i - nw);
+      for (int p = 0; p < nparts; ++p) s += part_db[static_cast<int64_t>(p) * fo + o];
+      db[o] = static_cast<float>(s);
+    }
+  }
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace sl
@@ -526,6 +730,81 @@ cmb_status cmb_sage_layer_forward(const cmb_graph* g, const cmb_blocks* b, int32
   else
     sl::k_sage_layer<10, 2><<<grid, sl::kThreads, smem, s>>>(CMB_LAYER_ARGS);
 #undef CMB_LAYER_ARGS
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+size_t cmb_sage_backward_workspace_bytes(int32_t feat_dim, int32_t out_dim) {
+  if (cmb_sage_weights_bytes(feat_dim, out_dim) == 0 || (out_dim & (out_dim - 1))) return 0;
+  const size_t kh = (feat_dim + 63) / 64;
+  return static_cast<size_t>(sl::kMaxBwdCtas) * (2 * kh * 64 + 1) * out_dim * sizeof(float);
+}
+
+cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                   int64_t n_last_dst_cap, const void* dy, int64_t dy_ld,
+                                   const void* y, int64_t y_ld, int32_t out_dim, float* dw,
+                                   float* db, void* workspace, size_t workspace_bytes,
+                                   void* stream) {
+  CMB_ARG(g && b && dy && dw && db && workspace, "cmb_sage_layer_backward: null argument");
+  CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_sage_layer_backward: bad n_hops");
+  CMB_ARG(g->d.x != nullptr, "cmb_sage_layer_backward: graph has no feature table");
+  const int F = g->d.f;
+  const size_t need = cmb_sage_backward_workspace_bytes(F, out_dim);
+  CMB_ARG(need != 0, "cmb_sage_layer_backward: need feat_dim <= 128 and out_dim a power of two "
+                     "in [16, 256] (got %d, %d)", F, out_dim);
+  CMB_ARG(workspace_bytes >= need && sl::aligned16(workspace),
+          "cmb_sage_layer_backward: workspace < %zu bytes or unaligned", need);
+  CMB_ARG(b->last_src_ids != nullptr, "cmb_sage_layer_backward: blocks->last_src_ids is required");
+  CMB_ARG(g->d.ld % 4 == 0 && sl::aligned16(g->d.x),
+          "cmb_sage_layer_backward: feature rows must be 16-byte aligned (ld %% 4 == 0)");
+  CMB_ARG(dy_ld >= out_dim && dy_ld % 8 == 0 && sl::aligned16(dy) &&
+              (!y || (y_ld >= out_dim && y_ld % 8 == 0 && sl::aligned16(y))),
+          "cmb_sage_layer_backward: dy / y rows must be 16-byte aligned bf16 with ld >= out_dim");
+  CMB_ARG(n_last_dst_cap >= 0 && n_last_dst_cap <= b->nodes_cap,
+          "cmb_sage_layer_backward: bad n_last_dst_cap");
+  const int L = n_hops;
+  const int kh = (F + 63) / 64;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t tiles = (n_last_dst_cap + sl::kM - 1) / sl::kM;
+  int grid = static_cast<int>(tiles < g->num_sms ? tiles : g->num_sms);
+  if (grid > sl::kMaxBwdCtas) grid = sl::kMaxBwdCtas;
+  if (const char* e = std::getenv("CMB_BWD_GRID")) {  // debugging: fewer CTAs, more tiles each
+    const int gm = std::atoi(e);
+    if (gm > 0 && gm < grid) grid = gm;
+  }
+  float* part = static_cast<float*>(workspace);
+  float* part_db = part + static_cast<size_t>(sl::kMaxBwdCtas) * 2 * kh * 64 * out_dim;
+  if (grid > 0) {
+    int cols = kh * out_dim;
+    int alloc = 32;
+    while (alloc < cols) alloc <<= 1;
+    const size_t smem = sl::bwd_smem_bytes(kh, out_dim);
+    static bool configured = false;
+    if (!configured) {
+      CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_layer_bwd<5, 2>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sl::bwd_smem_bytes(2, 256))));
+      CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_layer_bwd<10, 2>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sl::bwd_smem_bytes(2, 256))));
+      configured = true;
+    }
+    const int dmax = static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap);
+#define CMB_BWD_ARGS                                                                          \
+  b->indptr[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,                     \
+      reinterpret_cast<const float4*>(g->d.x), g->d.ld / 4, b->nodes, F, kh,                 \
+      static_cast<const __nv_bfloat16*>(dy), dy_ld, static_cast<const __nv_bfloat16*>(y), y_ld, \
+      out_dim, alloc, part, part_db
+    if (dmax <= 5)
+      sl::k_sage_layer_bwd<5, 2><<<grid, sl::kThreads, smem, s>>>(CMB_BWD_ARGS);
+    else
+      sl::k_sage_layer_bwd<10, 2><<<grid, sl::kThreads, smem, s>>>(CMB_BWD_ARGS);
+#undef CMB_BWD_ARGS
+    CMB_CUDA(cudaGetLastError());
+  }
+  const int64_t nout = 2ll * F * out_dim + out_dim;
+  sl::k_sage_bwd_reduce<<<static_cast<int>((nout + 255) / 256), 256, 0, s>>>(
+      part, part_db, grid, F, kh, out_dim, dw, db);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
 }

@@ -163,3 +163,76 @@ def test_layer_wide_fanouts(fanouts):
     roots = np.ascontiguousarray(oracle.batch_roots(order, 512, 1))
     yg, ref, nd = _run(b, prep, g, list(fanouts), roots, 1, layer, 0.7)
     _check(yg, ref, nd, F, ws, wn, bias, True, False)
+
+
+# ---------------------------------------------------------------- backward (reading R27)
+def _bwd_check(b, prep, g, fanouts, roots, bid, p, fo, relu, seed=21):
+    F = b.cfg.feat_dim
+    ws, wn, bias = _weights(F, fo, seed)
+    layer = cmb.SageLayer(ws, wn, bias, relu=relu, out_bf16=True)
+    sampler = cmb.Sampler(g, len(roots), fanouts)
+    sampler.sample(torch.from_numpy(roots).cuda(), p, SEED, bid)
+    ref = oracle.run_batch(prep, b.X, F, roots, fanouts, p, SEED, bid)
+    L = len(fanouts)
+    nd = ref["n"][L - 1]
+    Xd = ref["X_in"][:nd, :F].astype(np.float64)
+    H = ref["H64"][:, :F]
+    # upstream gradient and (for ReLU) the mask source: test inputs in bf16, the same values on
+    # both sides; Y is the oracle's forward output rounded to bf16 (never the GPU's)
+    gen = torch.Generator().manual_seed(seed + 1)
+    dY = (torch.randn(nd, fo, generator=gen) * 0.01).to(torch.bfloat16)
+    Yo = torch.from_numpy(oracle.sage_conv(Xd, H, ws.double().numpy(), wn.double().numpy(),
+                                           bias.double().numpy(), relu=True)).to(torch.bfloat16)
+    dy_d = torch.zeros(sampler.n_cap[L - 1], fo, dtype=torch.bfloat16, device="cuda")
+    dy_d[:nd] = dY.cuda()
+    y_d = None
+    if relu:
+        y_d = torch.zeros_like(dy_d)
+        y_d[:nd] = Yo.cuda()
+    dws, dwn, db = sampler.sage_layer_backward(layer, dy_d, y_d)
+    torch.cuda.synchronize()
+    assert sampler.status() == 0
+    dZ = dY.double().numpy()
+    if relu:
+        dZ = dZ * (Yo.double().numpy() > 0)
+    rs, rn, rb = oracle.sage_conv_backward(Xd, H, dZ)
+    for got, ref_, A in ((dws, rs, Xd), (dwn, rn, H)):
+        S = np.abs(A).T @ np.abs(dZ)
+        err = np.abs(got.double().cpu().numpy() - ref_)
+        assert np.all(err <= 2.0 ** -7 * S + 1e-30), float(np.max(err - 2.0 ** -7 * S))
+    errb = np.abs(db.double().cpu().numpy() - rb)
+    assert np.all(errb <= 2.0 ** -12 * np.abs(dZ).sum(0) + 1e-30), float(np.max(errb))
+    return nd
+
+
+@pytest.mark.parametrize("name,factor,fo,relu", [
+    ("tiny", None, 256, False),      # F = 16: M = 128 covers both halves (kh = 1)
+    ("tiny", None, 64, True),
+    ("products", 0.01, 256, True),   # F = 100: two M blocks, ragged F
+    ("arxiv", None, 128, False),     # F = 128
+])
+def test_layer_backward_parity(name, factor, fo, relu):
+    b, prep, g = _bundle(name, factor)
+    order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_RAND, 0.0,
+                               SEED, 0)
+    roots = oracle.batch_roots(order, b.cfg.batch_size, 1)
+    assert _bwd_check(b, prep, g, b.cfg.fanouts, roots, 1, b.cfg.p_intra, fo, relu) > 0
+
+
+def test_layer_backward_full_size_products():
+    b, prep, g = _bundle("products")
+    order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_RAND, 0.0,
+                               SEED, 0)
+    roots = oracle.batch_roots(order, b.cfg.batch_size, 5)
+    assert _bwd_check(b, prep, g, b.cfg.fanouts, roots, 5, 0.5, 256, True) > 100_000
+
+
+def test_layer_backward_edge_cases():
+    b, prep, g = _bundle("tiny")
+    order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_NORAND, 0.0,
+                               SEED, 0)
+    for roots in (order[:1], order[:129]):   # one partial tile; fewer tiles than SMs
+        _bwd_check(b, prep, g, b.cfg.fanouts, np.ascontiguousarray(roots), 0, 1.0, 32, True)
+    with pytest.raises(ValueError):   # backward needs a power-of-two out_dim
+        layer = cmb.SageLayer(torch.zeros(16, 48), torch.zeros(16, 48))
+        layer.backward_workspace()
