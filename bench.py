@@ -552,10 +552,14 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
     s = torch.cuda.current_stream()
     n = min(n_batches, pipe.n_batches)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n)]
+    gen_dy = torch.Generator(device=graph.device).manual_seed(2)
+    dy = (torch.randn(smp.n_cap[L - 1], fo, generator=gen_dy, device=graph.device) * 0.01
+          ).to(torch.bfloat16)
     sizes = torch.zeros(n, 2 * L + 1, dtype=torch.int64, device=graph.device)
     for warm in range(3):
         smp.sample(pipe.batch_roots(warm), p, args.seed, warm)
         smp.sage_layer(layer, out)
+        smp.sage_layer_backward(layer, dy, out)
         smp.gather_aggregate()
     torch.cuda.synchronize()
     for k in range(n):
@@ -565,17 +569,26 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
         ev[k][1].record(s)
         smp.gather_aggregate()
         ev[k][2].record(s)
+        smp.sage_layer_backward(layer, dy, out)   # weight gradients of the same batch
+        ev[k][3].record(s)
         sizes[k].copy_(smp.sizes, non_blocking=True)
     torch.cuda.synchronize()
     assert smp.status() == 0
     t_layer = np.array([e[0].elapsed_time(e[1]) for e in ev])
     t_agg = np.array([e[1].elapsed_time(e[2]) for e in ev])
+    t_bwd = np.array([e[2].elapsed_time(e[3]) for e in ev])
     sz = sizes.cpu().numpy()
     nL, nd, ed = sz[:, L], sz[:, L - 1], sz[:, L + 1 + L - 1]
     alg = nL * 4 * F + 4 * (nd + 1) + 4 * ed + 4 * nd + nd * 2 * fo
     flops = 2.0 * nd * 2 * F * fo
     peak, peak_src = measured_peak_hbm()
     gbps = float(np.mean(alg) / (np.mean(t_layer) * 1e-3) / 1e9)
+    # backward: the same unique rows + index streams, dY and Y read (bf16), partials written and
+    # re-read (148 x 2 kh 64 x Fo fp32), dW / db written; flops 2 * n_{L-1} * 2F * Fo
+    kh = (F + 63) // 64
+    part = 148 * (2 * kh * 64 + 1) * fo * 4
+    alg_b = nL * 4 * F + 4 * (nd + 1) + 4 * ed + 4 * nd + 2 * nd * 2 * fo + 2 * part + 4 * (2 * F + 1) * fo
+    gbps_b = float(np.mean(alg_b) / (np.mean(t_bwd) * 1e-3) / 1e9)
     return {"kernel": "k_sage_layer (a4+a5+SAGEConv layer 1, tcgen05 bf16, cmb_sage_layer_forward)",
             "out_dim": fo, "out_dtype": "bf16", "relu": True, "batches": int(n),
             "layer_ms": float(np.mean(t_layer)), "gather_aggregate_ms_same_batches": float(np.mean(t_agg)),
@@ -583,7 +596,13 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
             "algorithmic_bytes_per_launch": float(np.mean(alg)),
             "roofline": {"bound": "hbm", "achieved": gbps, "peak": peak, "peak_source": peak_src,
                          "unit": "GB/s", "frac": gbps / peak},
-            "tensor_tflops": float(np.mean(flops) / (np.mean(t_layer) * 1e-3) / 1e12)}
+            "tensor_tflops": float(np.mean(flops) / (np.mean(t_layer) * 1e-3) / 1e12),
+            "backward": {"kernels": "k_sage_layer_bwd + k_sage_bwd_reduce (cmb_sage_layer_backward)",
+                         "ms": float(np.mean(t_bwd)),
+                         "algorithmic_bytes_per_call": float(np.mean(alg_b)),
+                         "roofline": {"bound": "hbm", "achieved": gbps_b, "peak": peak,
+                                      "unit": "GB/s", "frac": gbps_b / peak},
+                         "tensor_tflops": float(np.mean(flops) / (np.mean(t_bwd) * 1e-3) / 1e12)}}
 
 
 def main():

@@ -396,6 +396,19 @@ CMB_API cmb_status cmb_sage_layer_forward(const cmb_graph* g, const cmb_blocks* 
                                           int32_t relu, int32_t out_bf16, void* out,
                                           int64_t out_ld, void* stream);
 
+/* NEXT-4 GCN variant (reading R28): Y = sigma(A' X_in W + bias) on the input-side block,
+ * A' = (D + I)^-1 (A + I) (row-normalised adjacency with a self loop, Eq. (1)), fused
+ * with the gather like cmb_sage_layer_forward (same arguments and limits; one weight matrix
+ * w = device fp32 [F x Fo] row-major, packed by cmb_gcn_pack_weights into a half-size image). */
+CMB_API size_t cmb_gcn_weights_bytes(int32_t feat_dim, int32_t out_dim);
+CMB_API cmb_status cmb_gcn_pack_weights(const float* w, int32_t feat_dim, int32_t out_dim,
+                                        void* w_img, size_t w_img_bytes, void* stream);
+CMB_API cmb_status cmb_gcn_layer_forward(const cmb_graph* g, const cmb_blocks* blocks,
+                                         int32_t n_hops, int64_t n_last_dst_cap,
+                                         const void* w_img, const float* bias, int32_t out_dim,
+                                         int32_t relu, int32_t out_bf16, void* out,
+                                         int64_t out_ld, void* stream);
+
 /* NEXT-4 backward (reading R27): weight gradients of the same layer for one batch,
  *     dZ = dY * 1[Y > 0] (y != NULL; y = NULL: dZ = dY),
  *     dW_self = X_dst^T dZ,  dW_neigh = H^T dZ,  db = sum_d dZ[d, :],

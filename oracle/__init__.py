@@ -261,3 +261,27 @@ def sage_conv_backward(X_dst, H, dY, Y=None, relu=False):
     if relu:
         dZ = dZ * (np.asarray(Y, dtype=np.float64) > 0)
     return X.T @ dZ, Hn.T @ dZ, dZ.sum(axis=0)
+
+
+def gcn_conv(indptr_h, idx, X_in, W, bias=None, relu=False) -> np.ndarray:
+    """GCN form of the input-side layer (NEXT-4 variant, reading R28), fp64.
+
+    Eq. (1) X^{l+1} = sigma(A' X^l W) with A' "the normalized and regularized
+    adjacency matrix", taken on the sampled block of hop L-1 as the row-normalised adjacency with
+    a self loop, A' = (D + I)^{-1} (A + I): row d of A' X_in is (X_in[d] + sum_{e in row d}
+    X_in[idx[e]]) / (deg_d + 1) -- dst node d is src node d (the dst list is the prefix of the
+    src list, reading R8).  Y = sigma(A' X_in W + bias), W F x Fo row-major.
+    """
+    ip = np.asarray(indptr_h, dtype=np.int64)
+    ix = np.asarray(idx, dtype=np.int64)
+    X = np.asarray(X_in, dtype=np.float64)
+    n_dst = ip.shape[0] - 1
+    deg = np.diff(ip)
+    S = X[:n_dst].copy()
+    np.add.at(S, np.repeat(np.arange(n_dst), deg), X[ix])
+    Y = (S / (deg + 1.0)[:, None]) @ np.asarray(W, dtype=np.float64)
+    if bias is not None:
+        Y = Y + np.asarray(bias, dtype=np.float64)[None, :]
+    if relu:
+        Y = np.maximum(Y, 0.0)
+    return Y

@@ -51,6 +51,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_cache_gather_aggregate",
            "cmb_sage_weights_bytes", "cmb_sage_pack_weights", "cmb_sage_layer_forward",
            "cmb_sage_backward_workspace_bytes", "cmb_sage_layer_backward",
+           "cmb_gcn_weights_bytes", "cmb_gcn_pack_weights", "cmb_gcn_layer_forward",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -161,6 +162,10 @@ def lib():
             "cmb_sage_layer_forward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, P, I32, I32,
                                              I32, P, I64, P]),
             "cmb_sage_backward_workspace_bytes": (SZ, [I32, I32]),
+            "cmb_gcn_weights_bytes": (SZ, [I32, I32]),
+            "cmb_gcn_pack_weights": (I32, [P, I32, I32, P, SZ, P]),
+            "cmb_gcn_layer_forward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, P, I32, I32,
+                                            I32, P, I64, P]),
             "cmb_sage_layer_backward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, I64, P, I64,
                                               I32, P, P, P, SZ, P]),
             "cmb_get_device_status": (I32, [P, P]),
@@ -429,6 +434,16 @@ class Sampler:
             int(layer.out_bf16), _ptr(out), out.stride(0), _stream()))
         return out
 
+    def gcn_layer(self, layer: "GcnLayer", out: Optional[torch.Tensor] = None):
+        """NEXT-4 GCN variant (R28): a4 + A' = (D + I)^-1 (A + I) aggregation + X W on tcgen05."""
+        if out is None:
+            out = layer.alloc_out(self.n_cap[self.L - 1])
+        _check(lib().cmb_gcn_layer_forward(
+            self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
+            _ptr(layer.w_img), _ptr(layer.bias), layer.out_dim, int(layer.relu),
+            int(layer.out_bf16), _ptr(out), out.stride(0), _stream()))
+        return out
+
     def sage_layer_backward(self, layer: "SageLayer", dy: torch.Tensor,
                             y: Optional[torch.Tensor] = None):
         """NEXT-4 backward for the last sampled batch: dY (bf16 [>= n_{L-1}, out_dim]) and, for a
@@ -492,6 +507,29 @@ class SageLayer:
                                  f"(got {self.out_dim})")
             self._bws = torch.empty(n, dtype=torch.uint8, device=self.device)
         return self._bws
+
+    def alloc_out(self, rows: int) -> torch.Tensor:
+        dt = torch.bfloat16 if self.out_bf16 else torch.float32
+        return torch.empty(max(1, rows), self.out_dim, dtype=dt, device=self.device)
+
+
+class GcnLayer:
+    """NEXT-4 GCN variant (R28): one weight matrix w [F, out_dim], packed once."""
+
+    def __init__(self, w: torch.Tensor, bias=None, relu=True, out_bf16=False, device=None):
+        F, fo = int(w.shape[0]), int(w.shape[1])
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        nbytes = lib().cmb_gcn_weights_bytes(F, fo)
+        if nbytes == 0:
+            raise ValueError(f"unsupported layer shape F={F}, out_dim={fo}")
+        self.feat_dim, self.out_dim = F, fo
+        self.relu, self.out_bf16 = bool(relu), bool(out_bf16)
+        self.w = _dev_tensor(w, torch.float32, dev)
+        self.bias = None if bias is None else _dev_tensor(bias, torch.float32, dev)
+        self.w_img = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.device = dev
+        _check(lib().cmb_gcn_pack_weights(_ptr(self.w), F, fo, _ptr(self.w_img), nbytes,
+                                          _stream()))
 
     def alloc_out(self, rows: int) -> torch.Tensor:
         dt = torch.bfloat16 if self.out_bf16 else torch.float32

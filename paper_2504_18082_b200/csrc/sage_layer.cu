@@ -40,8 +40,8 @@ constexpr int kM = 128;              // UMMA M (rows per tile)
 constexpr int kRowsPerWarp = kM / kWarps;  // 8
 constexpr int kAtomBytes = 128;      // one row of a SWIZZLE_128B atom (64 bf16)
 
-__host__ __device__ inline uint32_t w_img_bytes(int kh, int fo) {
-  return static_cast<uint32_t>(2 * kh) * static_cast<uint32_t>(fo) * kAtomBytes;
+__host__ __device__ inline uint32_t w_img_bytes(int kh, int fo, int halves = 2) {
+  return static_cast<uint32_t>(halves * kh) * static_cast<uint32_t>(fo) * kAtomBytes;
 }
 __host__ __device__ inline uint32_t a_bytes(int kh) {
   return static_cast<uint32_t>(2 * kh) * kM * kAtomBytes;
@@ -161,11 +161,12 @@ __device__ __forceinline__ uint2 pack_bf16x4(float4 v) {
 }
 
 // ----------------------------------------------------------------- weight packing
-// w_img[element (n, k)] = bf16(W_h[c][n]) for k = half h, column c < F; 0 for the padding columns
+// w_img[element (n, k)] = bf16(W_h[c][n]) for k = half h, column c < F; 0 for the padding columns.
+// w_neigh == NULL: one half only (the GCN form, W = w_self)
 __global__ void k_pack_weights(const float* __restrict__ w_self, const float* __restrict__ w_neigh,
                                int F, int fo, int kh, __nv_bfloat16* __restrict__ img) {
   const int kcols = kh * 64;
-  const int64_t total = static_cast<int64_t>(2 * kcols) * fo;
+  const int64_t total = static_cast<int64_t>((w_neigh ? 2 : 1) * kcols) * fo;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int n = static_cast<int>(i % fo);
@@ -227,8 +228,9 @@ struct ATileGather {
     for (int k = 0; k < kRowsPerWarp; ++k) g[k] = ng[k];
   }
   // gathers the current tile into sA (rows past n_dst: skipped, or zero-filled if zero_dead) and
-  // starts loading the indices of tile `next`
-  __device__ __forceinline__ void build(int64_t next, uint8_t* sA, bool zero_dead) {
+  // starts loading the indices of tile `next`.  gcn: one half only, the row of the self-loop,
+  // row-normalised adjacency (X_dst + sum of the edge rows) / (deg + 1) (reading R28)
+  __device__ __forceinline__ void build(int64_t next, uint8_t* sA, bool zero_dead, bool gcn = false) {
     constexpr unsigned kFull = 0xffffffffu;
     const int f4 = (F + 3) >> 2;
     const int c0 = lane * 4;             // this lane's 4 columns of each half
@@ -291,6 +293,11 @@ struct ATileGather {
             hm = make_float4(acc.x * y, acc.y * y, acc.z * y, acc.w * y);
           }
           float4 sf = s[u];
+          if (gcn) {
+            const float y = __frcp_rn(static_cast<float>(deg[u] + 1));
+            sf = make_float4(__fadd_rn(sf.x, acc.x) * y, __fadd_rn(sf.y, acc.y) * y,
+                             __fadd_rn(sf.z, acc.z) * y, __fadd_rn(sf.w, acc.w) * y);
+          }
           if (c0 + 4 > F) {  // columns at or beyond F are operand padding: exact zeros
             if (c0 + 0 >= F) sf.x = hm.x = 0.f;
             if (c0 + 1 >= F) sf.y = hm.y = 0.f;
@@ -299,7 +306,7 @@ struct ATileGather {
           }
           const int r = warp * kRowsPerWarp + k;
           *reinterpret_cast<uint2*>(sA + sw128_off(r, 0, c0, kh, kM)) = pack_bf16x4(sf);
-          *reinterpret_cast<uint2*>(sA + sw128_off(r, 1, c0, kh, kM)) = pack_bf16x4(hm);
+          if (!gcn) *reinterpret_cast<uint2*>(sA + sw128_off(r, 1, c0, kh, kM)) = pack_bf16x4(hm);
         }
       }
     }
@@ -313,10 +320,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                  const float4* __restrict__ x, int64_t ld4, const int32_t* __restrict__ map,
                  int F, int kh, const uint4* __restrict__ w_img, const float* __restrict__ bias,
                  int fo, int tmem_cols, int relu, int out_bf16, void* __restrict__ out,
-                 int64_t out_ld) {
+                 int64_t out_ld, int halves) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
-  const uint32_t wbytes = w_img_bytes(kh, fo);
+  const uint32_t wbytes = w_img_bytes(kh, fo, halves);
   uint8_t* sW = smem;
   uint8_t* sA = sW + wbytes;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sA + a_bytes(kh));
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     // ---------------------------------------------------------------- 1. gather -> A (bf16)
-    ga.build(tile + gridDim.x, sA, false);
+    ga.build(tile + gridDim.x, sA, false, halves == 1);
     fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core (async proxy)
     __syncthreads();
 
@@ -379,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0) {
       tc_fence_after();
       uint32_t acc_flag = 0;
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < halves; ++h) {
         for (int st = 0; st < steps; ++st) {
           const uint32_t atom = static_cast<uint32_t>(h * kh + (st >> 2));
           const uint32_t koff = static_cast<uint32_t>(st & 3) * 32u;
@@ -625,27 +632,38 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// dw[h][f][o] = sum over CTAs of part[cta][h*kh*64 + f][o] (fp64), db[o] = sum of part_db[cta][o]
-__global__ void k_sage_bwd_reduce(const float* __restrict__ part, const float* __restrict__ part_db,
-                                  int nparts, int F, int kh, int fo, float* __restrict__ dw,
-                                  float* __restrict__ db) {
+// dw[h][f][o] = sum over CTAs of part[cta][h*kh*64 + f][o], db[o] = sum of part_db[cta][o], in
+// fp64 and a fixed order (deterministic): a 256-thread block owns 32 consecutive outputs; its 8
+// warps sum the partials p = w, w + 8, ... (coalesced 128-B rows), then warp 0 adds the 8 sums.
+__global__ void __launch_bounds__(256) k_sage_bwd_reduce(const float* __restrict__ part,
+                                                         const float* __restrict__ part_db,
+                                                         int nparts, int F, int kh, int fo,
+                                                         float* __restrict__ dw,
+                                                         float* __restrict__ db) {
+  __shared__ double red[8][32];
   const int m_all = 2 * kh * 64;
   const int64_t nw = 2ll * F * fo;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nw + fo;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    double s = 0.0;
-    if (i < nw) {
-      const int o = static_cast<int>(i % fo);
-      const int f = static_cast<int>((i / fo) % F);
-      const int h = static_cast<int>(i / (static_cast<int64_t>(F) * fo));
-      const int m = h * kh * 64 + f;
-      for (int p = 0; p < nparts; ++p) s += part[(static_cast<int64_t>(p) * m_all + m) * fo + o];
-      dw[i] = static_cast<float>(s);
-    } else {
-      const int o = static_cast<int>(i - nw);
-      for (int p = 0; p < nparts; ++p) s += part_db[static_cast<int64_t>(p) * fo + o];
-      db[o] = static_cast<float>(s);
-    }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  double s = 0.0;
+  if (i < nw) {
+    const int o = static_cast<int>(i % fo);
+    const int f = static_cast<int>((i / fo) % F);
+    const int h = static_cast<int>(i / (static_cast<int64_t>(F) * fo));
+    const int64_t off = static_cast<int64_t>(h * kh * 64 + f) * fo + o;
+    for (int p = w; p < nparts; p += 8) s += __ldg(part + static_cast<int64_t>(p) * m_all * fo + off);
+  } else if (i < nw + fo) {
+    const int o = static_cast<int>(i - nw);
+    for (int p = w; p < nparts; p += 8) s += __ldg(part_db + static_cast<int64_t>(p) * fo + o);
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && i < nw + fo) {
+    double t = 0.0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) t += red[g][lane];
+    if (i < nw) dw[i] = static_cast<float>(t);
+    else db[i - nw] = static_cast<float>(t);
   }
 }
 
@@ -682,10 +700,10 @@ cmb_status cmb_sage_pack_weights(const float* w_self, const float* w_neigh, int3
   return CMB_OK;
 }
 
-cmb_status cmb_sage_layer_forward(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
-                                  int64_t n_last_dst_cap, const void* w_img, const float* bias,
-                                  int32_t out_dim, int32_t relu, int32_t out_bf16, void* out,
-                                  int64_t out_ld, void* stream) {
+static cmb_status layer_forward(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                int64_t n_last_dst_cap, const void* w_img, const float* bias,
+                                int32_t out_dim, int32_t relu, int32_t out_bf16, void* out,
+                                int64_t out_ld, void* stream, int halves) {
   CMB_ARG(g && b && w_img && out, "cmb_sage_layer_forward: null argument");
   CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_sage_layer_forward: bad n_hops");
   CMB_ARG(g->d.x != nullptr, "cmb_sage_layer_forward: graph has no feature table");
@@ -724,7 +742,7 @@ cmb_status cmb_sage_layer_forward(const cmb_graph* g, const cmb_blocks* b, int32
 #define CMB_LAYER_ARGS                                                                        \
   b->indptr[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,                     \
       reinterpret_cast<const float4*>(g->d.x), g->d.ld / 4, b->nodes, F, kh,                 \
-      static_cast<const uint4*>(w_img), bias, out_dim, cols, relu, out_bf16, out, out_ld
+      static_cast<const uint4*>(w_img), bias, out_dim, cols, relu, out_bf16, out, out_ld, halves
   if (dmax <= 5)
     sl::k_sage_layer<5, 2><<<grid, sl::kThreads, smem, s>>>(CMB_LAYER_ARGS);
   else
@@ -732,6 +750,46 @@ cmb_status cmb_sage_layer_forward(const cmb_graph* g, const cmb_blocks* b, int32
 #undef CMB_LAYER_ARGS
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
+}
+
+cmb_status cmb_sage_layer_forward(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                  int64_t n_last_dst_cap, const void* w_img, const float* bias,
+                                  int32_t out_dim, int32_t relu, int32_t out_bf16, void* out,
+                                  int64_t out_ld, void* stream) {
+  return layer_forward(g, b, n_hops, n_last_dst_cap, w_img, bias, out_dim, relu, out_bf16, out,
+                       out_ld, stream, 2);
+}
+
+size_t cmb_gcn_weights_bytes(int32_t feat_dim, int32_t out_dim) {
+  const size_t n = cmb_sage_weights_bytes(feat_dim, out_dim);
+  return n / 2;
+}
+
+cmb_status cmb_gcn_pack_weights(const float* w, int32_t feat_dim, int32_t out_dim, void* w_img,
+                                size_t w_img_bytes, void* stream) {
+  CMB_ARG(w && w_img, "cmb_gcn_pack_weights: null argument");
+  const size_t need = cmb_gcn_weights_bytes(feat_dim, out_dim);
+  CMB_ARG(need != 0, "cmb_gcn_pack_weights: need 1 <= feat_dim <= 128, out_dim in [16, 256] "
+                     "and a multiple of 16 (got %d, %d)", feat_dim, out_dim);
+  CMB_ARG(w_img_bytes >= need, "cmb_gcn_pack_weights: w_img_bytes %zu < %zu", w_img_bytes, need);
+  CMB_ARG(sl::aligned16(w_img), "cmb_gcn_pack_weights: w_img must be 16-byte aligned");
+  cmb_status st = require_sm100();
+  if (st != CMB_OK) return st;
+  const int kh = (feat_dim + 63) / 64;
+  const int64_t total = static_cast<int64_t>(kh * 64) * out_dim;
+  sl::k_pack_weights<<<static_cast<int>((total + 255) / 256), 256, 0,
+                       static_cast<cudaStream_t>(stream)>>>(
+      w, nullptr, feat_dim, out_dim, kh, static_cast<__nv_bfloat16*>(w_img));
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+cmb_status cmb_gcn_layer_forward(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                 int64_t n_last_dst_cap, const void* w_img, const float* bias,
+                                 int32_t out_dim, int32_t relu, int32_t out_bf16, void* out,
+                                 int64_t out_ld, void* stream) {
+  return layer_forward(g, b, n_hops, n_last_dst_cap, w_img, bias, out_dim, relu, out_bf16, out,
+                       out_ld, stream, 1);
 }
 
 size_t cmb_sage_backward_workspace_bytes(int32_t feat_dim, int32_t out_dim) {
@@ -803,7 +861,7 @@ cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* b, int3
     CMB_CUDA(cudaGetLastError());
   }
   const int64_t nout = 2ll * F * out_dim + out_dim;
-  sl::k_sage_bwd_reduce<<<static_cast<int>((nout + 255) / 256), 256, 0, s>>>(
+  sl::k_sage_bwd_reduce<<<static_cast<int>((nout + 31) / 32), 256, 0, s>>>(
       part, part_db, grid, F, kh, out_dim, dw, db);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;

@@ -236,3 +236,36 @@ def test_layer_backward_edge_cases():
     with pytest.raises(ValueError):   # backward needs a power-of-two out_dim
         layer = cmb.SageLayer(torch.zeros(16, 48), torch.zeros(16, 48))
         layer.backward_workspace()
+
+
+# ---------------------------------------------------------------- GCN variant (reading R28)
+@pytest.mark.parametrize("name,factor,fo,relu,out_bf16", [
+    ("tiny", None, 64, True, False),
+    ("products", 0.01, 256, False, True),
+    ("arxiv", None, 256, True, False),
+])
+def test_gcn_layer_parity(name, factor, fo, relu, out_bf16):
+    b, prep, g = _bundle(name, factor)
+    F = b.cfg.feat_dim
+    gen = torch.Generator().manual_seed(13)
+    W = torch.randn(F, fo, generator=gen) / np.sqrt(F)
+    bias = torch.randn(fo, generator=gen) * 0.1
+    layer = cmb.GcnLayer(W, bias, relu=relu, out_bf16=out_bf16)
+    order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_COMM, 0.5,
+                               SEED, 0)
+    roots = oracle.batch_roots(order, b.cfg.batch_size, 1)
+    sampler = cmb.Sampler(g, len(roots), b.cfg.fanouts)
+    sampler.sample(torch.from_numpy(roots).cuda(), b.cfg.p_intra, SEED, 1)
+    y = sampler.gcn_layer(layer)
+    torch.cuda.synchronize()
+    ref = oracle.run_batch(prep, b.X, F, roots, b.cfg.fanouts, b.cfg.p_intra, SEED, 1)
+    L = len(b.cfg.fanouts)
+    nd = ref["n"][L - 1]
+    ip, ix = ref["indptr"][L - 1], ref["indices"][L - 1]
+    X = ref["X_in"][:, :F].astype(np.float64)
+    Y = oracle.gcn_conv(ip, ix, X, W.double().numpy(), bias.double().numpy(), relu=relu)
+    Aabs = oracle.gcn_conv(ip, ix, np.abs(X), np.abs(W.double().numpy()),
+                           np.abs(bias.double().numpy()))  # |A'X|·|W| + |b| bound (A' >= 0)
+    tol = 2.0 ** -7 * Aabs + (2.0 ** -8 * np.abs(Y) if out_bf16 else 0.0)
+    err = np.abs(y[:nd].float().cpu().numpy().astype(np.float64) - Y)
+    assert np.all(err <= tol + 1e-30), float(np.max(err - tol))

@@ -158,3 +158,49 @@ def test_backward_worked_example():
     assert np.array_equal(db, np.array([2.0, 1.0, 1.0]))
     assert np.array_equal(dWs[:, 2], np.array([-1.0, 0.5]))   # only row 1 contributes to col 2
     assert np.array_equal(dWn[:, 1], np.array([0.5, -1.0]))   # only row 0 contributes to col 1
+
+
+# ---------------------------------------------------------------- GCN variant (reading R28)
+def test_gcn_worked_example():
+    """Block with 2 dst nodes over 4 src nodes: row 0 has edges to src 2 and 3, row 1 none.
+    Hand arithmetic: A' row 0 = (X0 + X2 + X3) / 3 = ([1,2] + [3,0] + [2,1]) / 3 = [2, 1];
+    A' row 1 = X1 / 1 = [-1, 4].  W = [[1, 0, 2], [0, 1, -1]], b = [0, 0, 1]:
+    Y0 = [2, 1, 4 - 1 + 1] = [2, 1, 4], Y1 = [-1, 4, -2 - 4 + 1] = [-1, 4, -5]."""
+    X = np.array([[1, 2], [-1, 4], [3, 0], [2, 1]], dtype=np.float64)
+    W = np.array([[1, 0, 2], [0, 1, -1]], dtype=np.float64)
+    y = oracle.gcn_conv([0, 2, 2], [2, 3], X, W, bias=[0, 0, 1])
+    assert np.array_equal(y, np.array([[2, 1, 4], [-1, 4, -5]], dtype=np.float64))
+    assert np.array_equal(oracle.gcn_conv([0, 2, 2], [2, 3], X, W, bias=[0, 0, 1], relu=True),
+                          np.array([[2, 1, 4], [0, 4, 0]], dtype=np.float64))
+
+
+def test_gcn_brute_force_and_identities(tiny_prep, tiny_bundle):
+    from gen import CONFIGS
+    cfg = CONFIGS["tiny"]
+    order = oracle.order_roots(tiny_bundle.train, tiny_bundle.comm, cfg.num_communities,
+                               oracle.MODE_RAND, 0.0, 3, 0)
+    ref = oracle.run_batch(tiny_prep, tiny_bundle.X, cfg.feat_dim,
+                           oracle.batch_roots(order, cfg.batch_size, 0), cfg.fanouts,
+                           cfg.p_intra, 3, 0)
+    L = len(cfg.fanouts)
+    ip, ix, X = ref["indptr"][L - 1], ref["indices"][L - 1], ref["X_in"].astype(np.float64)
+    nd, F = ip.shape[0] - 1, cfg.feat_dim
+    rng = np.random.default_rng(8)
+    W = rng.standard_normal((F, 6))
+    y = oracle.gcn_conv(ip, ix, X, W)
+    for d in range(0, nd, 17):   # explicit loops over a sample of rows
+        row = X[d].copy()
+        for e in range(ip[d], ip[d + 1]):
+            row = row + X[ix[e]]
+        row = row / (ip[d + 1] - ip[d] + 1)
+        assert np.allclose(y[d], row @ W, rtol=1e-12, atol=1e-12)
+    # W = I: every output row is the mean over the node and its sampled neighbours
+    yi = oracle.gcn_conv(ip, ix, X, np.eye(F))
+    deg = np.diff(ip)
+    H64 = ref["H64"]
+    assert np.allclose(yi, (X[:nd] + deg[:, None] * H64) / (deg[:, None] + 1), rtol=1e-12, atol=1e-12)
+    # rows of equal degree k: GCN(W) == SAGE(W_self = W/(k+1), W_neigh = k W/(k+1)) on them
+    for k in np.unique(deg):
+        rows = np.nonzero(deg == k)[0]
+        ys = oracle.sage_conv(X[rows], H64[rows], W / (k + 1), k * W / (k + 1))
+        assert np.allclose(y[rows], ys, rtol=1e-12, atol=1e-12)
