@@ -95,3 +95,40 @@ def test_rank_batch_helpers():
     assert ms == 3.5 and c == [1.0, 2.0]
     assert np.array_equal(np.sort(sum((cmb_dist.rank_batches(r, 3, 4) for r in range(3)), [])),
                           np.arange(12))
+
+
+# ---------------------------------------------------------------- NEXT-1: shard-aligned placement
+def test_aligned_schedule_partition_and_balance():
+    rng = np.random.default_rng(0)
+    for world in (1, 2, 3, 8):
+        for n in (1, 100, 1024 * 5 + 7, 20000):
+            o = rng.permutation(100000)[:n].astype(np.int32)
+            sch = cmb_dist.aligned_schedule(o, 1024, 100000, world)
+            nb = (n + 1023) // 1024
+            assert sorted(b for r in sch for b in r) == list(range(nb))
+            loads = [len(r) for r in sch]
+            assert max(loads) - min(loads) <= 1
+            assert all(r == sorted(r) for r in sch)    # epoch order kept on every rank
+
+
+def test_aligned_schedule_follows_the_shards():
+    """Batches whose roots sit in one shard go to that shard's owner when quotas allow."""
+    world, N, B = 4, 4000, 100
+    S = N // world
+    # 8 batches: two per shard, roots drawn inside the shard
+    rng = np.random.default_rng(1)
+    order = np.concatenate([rng.choice(np.arange(r * S, (r + 1) * S), B, replace=False)
+                            for r in (2, 0, 3, 1, 1, 3, 0, 2)]).astype(np.int32)
+    sch = cmb_dist.aligned_schedule(order, B, N, world)
+    assert sch == [[1, 6], [3, 4], [0, 7], [2, 5]]
+    # a skewed order (all roots in shard 0) still balances
+    sch = cmb_dist.aligned_schedule(np.arange(800, dtype=np.int32), B, N, world)
+    assert [len(r) for r in sch] == [2, 2, 2, 2] and sch[0] == [0, 1]
+
+
+def test_remote_fraction_counts_foreign_rows():
+    import torch
+    nodes = torch.tensor([0, 5, 10, 15, 19, 3], dtype=torch.int32)
+    assert cmb_dist.remote_fraction(nodes, 5, 0, 10) == 3 / 5    # rows 10, 15, 19 are rank 1's
+    assert cmb_dist.remote_fraction(nodes, 6, 1, 10) == 3 / 6
+    assert cmb_dist.remote_fraction(nodes, 0, 0, 10) == 0.0
