@@ -409,6 +409,24 @@ CMB_API cmb_status cmb_gcn_layer_forward(const cmb_graph* g, const cmb_blocks* b
                                          int32_t relu, int32_t out_bf16, void* out,
                                          int64_t out_ld, void* stream);
 
+/* NEXT-4 hidden layers (reading R29): layer l >= 2 of the model on hop h = L - l:
+ *     Y[d] = sigma( Yp[d] W_self + mean_{e in row d of hop h} Yp[indices[h][e]] W_neigh + b ),
+ * d < n_h (device count blocks->sizes[h] <= n_dst_cap).  y_prev: device bf16 [n_{h+1} x in_dim]
+ * (the previous layer's output, row = local src id of hop h), row stride y_prev_ld (multiple of
+ * 8, 16-B aligned); in_dim in {64, 128, 192, 256}; w_img packed by cmb_sage_hidden_pack_weights
+ * (w_self, w_neigh device fp32 [in_dim x out_dim]); out as for cmb_sage_layer_forward.  bf16
+ * operands, fp32 accumulation; the mean is summed in fp32 in CSR order. */
+CMB_API size_t cmb_sage_hidden_weights_bytes(int32_t in_dim, int32_t out_dim);
+CMB_API cmb_status cmb_sage_hidden_pack_weights(const float* w_self, const float* w_neigh,
+                                                int32_t in_dim, int32_t out_dim, void* w_img,
+                                                size_t w_img_bytes, void* stream);
+CMB_API cmb_status cmb_sage_hidden_forward(const cmb_blocks* blocks, int32_t hop,
+                                           int64_t n_dst_cap, const void* y_prev,
+                                           int64_t y_prev_ld, int32_t in_dim, const void* w_img,
+                                           const float* bias, int32_t out_dim, int32_t relu,
+                                           int32_t out_bf16, void* out, int64_t out_ld,
+                                           void* stream);
+
 /* NEXT-4 backward (reading R27): weight gradients of the same layer for one batch,
  *     dZ = dY * 1[Y > 0] (y != NULL; y = NULL: dZ = dY),
  *     dW_self = X_dst^T dZ,  dW_neigh = H^T dZ,  db = sum_d dZ[d, :],

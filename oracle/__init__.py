@@ -285,3 +285,18 @@ def gcn_conv(indptr_h, idx, X_in, W, bias=None, relu=False) -> np.ndarray:
     if relu:
         Y = np.maximum(Y, 0.0)
     return Y
+
+
+def sage_mean64(indptr_h, idx, Xsrc) -> np.ndarray:
+    """a5's mean (reading R12: neighbours only, 0 for an empty row) on fp64 inputs, for
+    the hidden layers of the model (reading R29), whose inputs are the previous layer's outputs:
+    H[d] = (sum_{e in row d} Xsrc[idx[e]]) / deg_d."""
+    ip = np.asarray(indptr_h, dtype=np.int64)
+    X = np.asarray(Xsrc, dtype=np.float64)
+    n = ip.shape[0] - 1
+    deg = np.diff(ip)
+    H = np.zeros((n, X.shape[1]), dtype=np.float64)
+    np.add.at(H, np.repeat(np.arange(n), deg), X[np.asarray(idx, dtype=np.int64)])
+    nz = deg > 0
+    H[nz] /= deg[nz, None]
+    return H

@@ -52,6 +52,8 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sage_weights_bytes", "cmb_sage_pack_weights", "cmb_sage_layer_forward",
            "cmb_sage_backward_workspace_bytes", "cmb_sage_layer_backward",
            "cmb_gcn_weights_bytes", "cmb_gcn_pack_weights", "cmb_gcn_layer_forward",
+           "cmb_sage_hidden_weights_bytes", "cmb_sage_hidden_pack_weights",
+           "cmb_sage_hidden_forward",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -163,6 +165,10 @@ def lib():
                                              I32, P, I64, P]),
             "cmb_sage_backward_workspace_bytes": (SZ, [I32, I32]),
             "cmb_gcn_weights_bytes": (SZ, [I32, I32]),
+            "cmb_sage_hidden_weights_bytes": (SZ, [I32, I32]),
+            "cmb_sage_hidden_pack_weights": (I32, [P, P, I32, I32, P, SZ, P]),
+            "cmb_sage_hidden_forward": (I32, [ctypes.POINTER(Blocks), I32, I64, P, I64, I32, P, P,
+                                              I32, I32, I32, P, I64, P]),
             "cmb_gcn_pack_weights": (I32, [P, I32, I32, P, SZ, P]),
             "cmb_gcn_layer_forward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, P, I32, I32,
                                             I32, P, I64, P]),
@@ -434,6 +440,22 @@ class Sampler:
             int(layer.out_bf16), _ptr(out), out.stride(0), _stream()))
         return out
 
+    def sage_hidden(self, layer: "SageLayer", hop: int, y_prev: torch.Tensor,
+                    out: Optional[torch.Tensor] = None):
+        """NEXT-4 hidden layer (R29) on hop `hop` of the last sampled batch: y_prev = the
+        previous layer's bf16 output (rows = local src ids of the hop) -> Y [n_cap[hop], out]."""
+        if not layer.hidden:
+            raise ValueError("layer was packed as a first layer; use SageLayer(..., hidden=True)")
+        if y_prev.dtype != torch.bfloat16:
+            raise ValueError("y_prev must be bf16")
+        if out is None:
+            out = layer.alloc_out(self.n_cap[hop])
+        _check(lib().cmb_sage_hidden_forward(
+            ctypes.byref(self._blocks), int(hop), self.n_cap[hop], _ptr(y_prev), y_prev.stride(0),
+            layer.feat_dim, _ptr(layer.w_img), _ptr(layer.bias), layer.out_dim, int(layer.relu),
+            int(layer.out_bf16), _ptr(out), out.stride(0), _stream()))
+        return out
+
     def gcn_layer(self, layer: "GcnLayer", out: Optional[torch.Tensor] = None):
         """NEXT-4 GCN variant (R28): a4 + A' = (D + I)^-1 (A + I) aggregation + X W on tcgen05."""
         if out is None:
@@ -476,12 +498,13 @@ class SageLayer:
     tensor cores' bf16 operand image.  w_self / w_neigh: [F, out_dim] (Y = X W), bias: [out_dim]."""
 
     def __init__(self, w_self: torch.Tensor, w_neigh: torch.Tensor, bias=None, relu=True,
-                 out_bf16=False, device=None):
+                 out_bf16=False, device=None, hidden=False):
         F, fo = int(w_self.shape[0]), int(w_self.shape[1])
         if tuple(w_neigh.shape) != (F, fo):
             raise ValueError("w_self and w_neigh must both be [F, out_dim]")
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-        nbytes = lib().cmb_sage_weights_bytes(F, fo)
+        self.hidden = bool(hidden)  # packed for cmb_sage_hidden_forward (layers >= 2, R29)
+        nbytes = (lib().cmb_sage_hidden_weights_bytes if hidden else lib().cmb_sage_weights_bytes)(F, fo)
         if nbytes == 0:
             raise ValueError(f"unsupported layer shape F={F}, out_dim={fo} (F <= 128, out_dim in "
                              f"[16, 256], a multiple of 16)")
@@ -495,9 +518,9 @@ class SageLayer:
         self.repack()
 
     def repack(self):
-        _check(lib().cmb_sage_pack_weights(_ptr(self.w_self), _ptr(self.w_neigh), self.feat_dim,
-                                           self.out_dim, _ptr(self.w_img), self.w_img.numel(),
-                                           _stream()))
+        pack = lib().cmb_sage_hidden_pack_weights if self.hidden else lib().cmb_sage_pack_weights
+        _check(pack(_ptr(self.w_self), _ptr(self.w_neigh), self.feat_dim, self.out_dim,
+                    _ptr(self.w_img), self.w_img.numel(), _stream()))
 
     def backward_workspace(self) -> torch.Tensor:
         if getattr(self, "_bws", None) is None:

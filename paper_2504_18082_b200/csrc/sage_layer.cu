@@ -667,6 +667,201 @@ __global__ void __launch_bounds__(256) k_sage_bwd_reduce(const float* __restrict
   }
 }
 
+// ----------------------------------------------------------------- NEXT-4 hidden layers
+// Layers after the first (reading R29): the input is the previous layer's output Yp (bf16,
+// [n_{h+1} x Fin], row = local src id of hop h; the dst rows d < n_h are its prefix), so
+//     Y[d] = sigma( Yp[d] W_self + mean_{e in row d of hop h} Yp[idx[e]] W_neigh + b ).
+// K = 2 Fin = 512 at the paper's hidden dim (256) does not fit in shared memory next to
+// its weights, so every 128-row tile runs two K phases (self, then neighbour mean), each staging
+// its A half (128 x Fin bf16, 64 KB) and its W half (Fin x Fo bf16, 128 KB; from L2) before
+// Fin/16 tcgen05 MMAs accumulate into the same TMEM columns.  One lane owns 8 columns (one
+// 16-byte load per row); the neighbour mean is summed in fp32 in CSR order.
+__device__ __forceinline__ uint4 ldg16_or_zero(const uint4* p, bool pred) {
+  uint4 r;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\tmov.b32 %2, 0;\n\tmov.b32 %3, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "r"(static_cast<int>(pred)));
+  return r;
+}
+__device__ __forceinline__ void add_bf16x8(float (&acc)[8], const uint4& v) {
+  const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(p[i]);
+    acc[2 * i] = __fadd_rn(acc[2 * i], f.x);
+    acc[2 * i + 1] = __fadd_rn(acc[2 * i + 1], f.y);
+  }
+}
+inline size_t hid_smem_bytes(int kin, int fo) {
+  return 1024 + static_cast<size_t>(kin) * kM * kAtomBytes + static_cast<size_t>(kin) * fo * kAtomBytes +
+         64 + static_cast<size_t>(fo) * 4;
+}
+
+template <int DMAX>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_sage_hidden(const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                  const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
+                  const uint4* __restrict__ yp, int64_t yp_ld8, int kin,
+                  const uint4* __restrict__ w_img, const float* __restrict__ bias, int fo,
+                  int tmem_cols, int relu, int out_bf16, void* __restrict__ out, int64_t out_ld) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
+  const uint32_t abytes = static_cast<uint32_t>(kin) * kM * kAtomBytes;
+  const uint32_t wbytes = static_cast<uint32_t>(kin) * fo * kAtomBytes;  // one half
+  uint8_t* sA = smem;
+  uint8_t* sW = sA + abytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sW + wbytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  float* sbias = reinterpret_cast<float*>(bar + 8);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr unsigned kFull = 0xffffffffu;
+  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
+  const int64_t ntiles = (n_dst + kM - 1) / kM;
+  for (int i = tid; i < fo; i += kThreads) sbias[i] = bias ? __ldg(bias + i) : 0.f;
+  if (tid == 0) {
+    mbar_init(saddr(bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     saddr(tmem_slot)),
+                 "r"(tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t idesc = idesc_bf16(kM, fo);
+  const uint32_t sA_addr = saddr(sA), sW_addr = saddr(sW);
+  const bool col = lane < kin * 8;  // lane owns columns 8*lane .. 8*lane+7
+  const uint64_t pol_stream = l2_evict_first();
+  uint32_t phase = 0;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t rbase = tile * kM + warp * kRowsPerWarp;
+    const int64_t rem = n_dst - rbase;
+    const int nr = rem <= 0 ? 0 : (rem >= kRowsPerWarp ? kRowsPerWarp : static_cast<int>(rem));
+    const int32_t ip = (lane <= nr && nr > 0) ? __ldg(indptr + rbase + lane) : 0;
+    for (int h = 0; h < 2; ++h) {
+      // ---- A half h: self rows (h = 0) or neighbour means (h = 1), bf16, swizzled
+#pragma unroll 2
+      for (int k = 0; k < kRowsPerWarp; ++k) {
+        const int r = warp * kRowsPerWarp + k;
+        uint4 a = make_uint4(0u, 0u, 0u, 0u);
+        if (h == 0) {
+          a = ldg16_or_zero(yp + (rbase + k) * yp_ld8 + lane, k < nr && col);
+        } else {
+          const int32_t lo = __shfl_sync(kFull, ip, k);
+          const int32_t hi = __shfl_sync(kFull, ip, k + 1);
+          const int deg = k < nr ? hi - lo : 0;
+          const int32_t my = lane < deg ? __ldg(idx + lo + lane) : 0;
+          float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          for (int j0 = 0; j0 < deg; j0 += DMAX) {
+            uint4 v[DMAX];
+#pragma unroll
+            for (int j = 0; j < DMAX; ++j) {
+              const int32_t s = __shfl_sync(kFull, my, (j0 + j) & 31);
+              v[j] = ldg16_or_zero(yp + static_cast<int64_t>(s) * yp_ld8 + lane, col && j0 + j < deg);
+            }
+#pragma unroll
+            for (int j = 0; j < DMAX; ++j)
+              if (j0 + j < deg) add_bf16x8(acc, v[j]);
+          }
+          if (deg > 0) {
+            const float y = __frcp_rn(static_cast<float>(deg));
+            uint32_t p[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[2 * i] * y, acc[2 * i + 1] * y);
+              p[i] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
+            a = make_uint4(p[0], p[1], p[2], p[3]);
+          }
+        }
+        if (col && k < nr) {
+          const int atom = lane >> 3, j = lane & 7;
+          *reinterpret_cast<uint4*>(sA + atom * (kM * kAtomBytes) + (r >> 3) * 1024 + (r & 7) * 128 +
+                                    ((j ^ (r & 7)) << 4)) = a;
+        }
+      }
+      // ---- W half h (from L2)
+      const uint4* wsrc = w_img + static_cast<size_t>(h) * (wbytes / 16);
+      for (uint32_t i = tid; i < wbytes / 16; i += kThreads)
+        reinterpret_cast<uint4*>(sW)[i] = __ldg(wsrc + i);
+      fence_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        for (int st = 0; st < kin * 4; ++st) {
+          const uint32_t atom = static_cast<uint32_t>(st >> 2);
+          const uint32_t koff = static_cast<uint32_t>(st & 3) * 32u;
+          mma_bf16(tmem, sw128_desc(sA_addr + atom * (kM * kAtomBytes) + koff),
+                   sw128_desc(sW_addr + atom * (fo * kAtomBytes) + koff), idesc,
+                   (h > 0 || st > 0) ? 1u : 0u);
+        }
+        mma_commit(saddr(bar));
+      }
+      mbar_wait(saddr(bar), phase);  // A / W free again, accumulator complete after h = 1
+      phase ^= 1;
+      tc_fence_after();
+      __syncthreads();
+    }
+    // ---- epilogue (as the first layer's)
+    {
+      const int q = warp & 3;
+      const int64_t row = tile * kM + q * 32 + lane;
+      const bool live = row < n_dst;
+      for (int ch = warp >> 2; ch < fo / 16; ch += kWarps / 4) {
+        uint32_t v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(ch * 16), v);
+        tmem_ld_wait();
+        float y[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          y[i] = __fadd_rn(__uint_as_float(v[i]), sbias[ch * 16 + i]);
+          if (relu) y[i] = fmaxf(y[i], 0.f);
+        }
+        if (live) {
+          if (out_bf16) {
+            uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + row * out_ld +
+                                                ch * 16);
+            uint32_t p[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[2 * i], y[2 * i + 1]);
+              p[i] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
+            st16_hint(o, make_uint4(p[0], p[1], p[2], p[3]), pol_stream);
+            st16_hint(o + 1, make_uint4(p[4], p[5], p[6], p[7]), pol_stream);
+          } else {
+            uint4* o = reinterpret_cast<uint4*>(static_cast<float*>(out) + row * out_ld + ch * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              st16_hint(o + i, make_uint4(__float_as_uint(y[4 * i]), __float_as_uint(y[4 * i + 1]),
+                                          __float_as_uint(y[4 * i + 2]), __float_as_uint(y[4 * i + 3])),
+                        pol_stream);
+          }
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(tmem_cols)
+                 : "memory");
+  }
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace sl
@@ -863,6 +1058,74 @@ cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* b, int3
   const int64_t nout = 2ll * F * out_dim + out_dim;
   sl::k_sage_bwd_reduce<<<static_cast<int>((nout + 31) / 32), 256, 0, s>>>(
       part, part_db, grid, F, kh, out_dim, dw, db);
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+size_t cmb_sage_hidden_weights_bytes(int32_t in_dim, int32_t out_dim) {
+  if (in_dim < 64 || in_dim > 256 || in_dim % 64 || out_dim < 16 || out_dim > 256 || out_dim % 16)
+    return 0;
+  return sl::w_img_bytes(in_dim / 64, out_dim);
+}
+
+cmb_status cmb_sage_hidden_pack_weights(const float* w_self, const float* w_neigh, int32_t in_dim,
+                                        int32_t out_dim, void* w_img, size_t w_img_bytes,
+                                        void* stream) {
+  CMB_ARG(w_self && w_neigh && w_img, "cmb_sage_hidden_pack_weights: null argument");
+  const size_t need = cmb_sage_hidden_weights_bytes(in_dim, out_dim);
+  CMB_ARG(need != 0, "cmb_sage_hidden_pack_weights: need in_dim in {64, 128, 192, 256} and "
+                     "out_dim in [16, 256], a multiple of 16 (got %d, %d)", in_dim, out_dim);
+  CMB_ARG(w_img_bytes >= need && sl::aligned16(w_img),
+          "cmb_sage_hidden_pack_weights: w_img smaller than %zu bytes or unaligned", need);
+  cmb_status st = require_sm100();
+  if (st != CMB_OK) return st;
+  const int kh = in_dim / 64;
+  const int64_t total = static_cast<int64_t>(2 * kh * 64) * out_dim;
+  sl::k_pack_weights<<<static_cast<int>((total + 255) / 256), 256, 0,
+                       static_cast<cudaStream_t>(stream)>>>(
+      w_self, w_neigh, in_dim, out_dim, kh, static_cast<__nv_bfloat16*>(w_img));
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+cmb_status cmb_sage_hidden_forward(const cmb_blocks* b, int32_t hop, int64_t n_dst_cap,
+                                   const void* y_prev, int64_t y_prev_ld, int32_t in_dim,
+                                   const void* w_img, const float* bias, int32_t out_dim,
+                                   int32_t relu, int32_t out_bf16, void* out, int64_t out_ld,
+                                   void* stream) {
+  CMB_ARG(b && y_prev && w_img && out, "cmb_sage_hidden_forward: null argument");
+  CMB_ARG(hop >= 0 && hop < CMB_MAX_HOPS && b->indptr[hop] && b->indices[hop],
+          "cmb_sage_hidden_forward: bad hop");
+  CMB_ARG(cmb_sage_hidden_weights_bytes(in_dim, out_dim) != 0,
+          "cmb_sage_hidden_forward: need in_dim in {64, 128, 192, 256}, out_dim in [16, 256] and "
+          "a multiple of 16 (got %d, %d)", in_dim, out_dim);
+  CMB_ARG(y_prev_ld >= in_dim && y_prev_ld % 8 == 0 && sl::aligned16(y_prev),
+          "cmb_sage_hidden_forward: y_prev rows must be 16-byte aligned bf16, ld >= in_dim");
+  CMB_ARG(out_ld >= out_dim && out_ld % (out_bf16 ? 8 : 4) == 0 && sl::aligned16(out),
+          "cmb_sage_hidden_forward: out_ld must be >= out_dim and keep rows 16-byte aligned");
+  CMB_ARG(sl::aligned16(w_img), "cmb_sage_hidden_forward: w_img must be 16-byte aligned");
+  CMB_ARG(n_dst_cap >= 0, "cmb_sage_hidden_forward: bad n_dst_cap");
+  if (n_dst_cap == 0) return CMB_OK;
+  cmb_status st = require_sm100();
+  if (st != CMB_OK) return st;
+  int dev = 0, sms = 0;
+  CMB_CUDA(cudaGetDevice(&dev));
+  CMB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int kin = in_dim / 64;
+  const int cols = out_dim <= 32 ? 32 : out_dim <= 64 ? 64 : out_dim <= 128 ? 128 : 256;
+  const size_t smem = sl::hid_smem_bytes(kin, out_dim);
+  static bool configured = false;
+  if (!configured) {
+    CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_hidden<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sl::hid_smem_bytes(4, 256))));
+    configured = true;
+  }
+  const int64_t tiles = (n_dst_cap + sl::kM - 1) / sl::kM;
+  const int grid = static_cast<int>(tiles < sms ? tiles : sms);
+  sl::k_sage_hidden<8><<<grid, sl::kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      b->indptr[hop], b->indices[hop], b->sizes + hop, n_dst_cap,
+      static_cast<const uint4*>(y_prev), y_prev_ld / 8, kin, static_cast<const uint4*>(w_img), bias,
+      out_dim, cols, relu, out_bf16, out, out_ld);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
 }

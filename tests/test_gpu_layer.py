@@ -269,3 +269,60 @@ def test_gcn_layer_parity(name, factor, fo, relu, out_bf16):
     tol = 2.0 ** -7 * Aabs + (2.0 ** -8 * np.abs(Y) if out_bf16 else 0.0)
     err = np.abs(y[:nd].float().cpu().numpy().astype(np.float64) - Y)
     assert np.all(err <= tol + 1e-30), float(np.max(err - tol))
+
+
+# ---------------------------------------------------------------- the 3-layer model (R26, R29)
+def _prop(T, ip, ix, nd):
+    """Elementwise bound of a layer input error T through (self row, neighbour mean)."""
+    return T[:nd], oracle.sage_mean64(ip, ix, T)
+
+
+@pytest.mark.parametrize("name,factor", [("tiny", None), ("products", 0.01)])
+def test_three_layer_forward(name, factor):
+    """Layer 1 fused with the gather, layers 2 and 3 on the previous layer's bf16 output, the last
+    without activation and with a class-sized output (48).  The oracle chain runs in fp64; the
+    bound of each layer is its own R26/R29 term plus the previous layer's bound propagated
+    through |W| (ReLU is 1-Lipschitz)."""
+    b, prep, g = _bundle(name, factor)
+    cfg = b.cfg
+    F, L = cfg.feat_dim, len(cfg.fanouts)
+    gen = torch.Generator().manual_seed(31)
+    dims = [F] + [256] * (L - 1) + [48]
+    Ws = [(torch.randn(dims[i], dims[i + 1], generator=gen) / np.sqrt(dims[i]),
+           torch.randn(dims[i], dims[i + 1], generator=gen) / np.sqrt(dims[i]),
+           torch.randn(dims[i + 1], generator=gen) * 0.1) for i in range(L)]
+    order = oracle.order_roots(b.train, b.comm, cfg.num_communities, oracle.MODE_RAND, 0.0, SEED, 0)
+    roots = oracle.batch_roots(order, cfg.batch_size, 0)
+    sampler = cmb.Sampler(g, len(roots), cfg.fanouts)
+    sampler.sample(torch.from_numpy(roots).cuda(), cfg.p_intra, SEED, 0)
+    ref = oracle.run_batch(prep, b.X, F, roots, cfg.fanouts, cfg.p_intra, SEED, 0)
+    # GPU chain
+    ys = []
+    for l in range(L):
+        ws, wn, bias = Ws[l]
+        last = l == L - 1
+        layer = cmb.SageLayer(ws, wn, bias, relu=not last, out_bf16=not last, hidden=l > 0)
+        ys.append(sampler.sage_layer(layer) if l == 0 else
+                  sampler.sage_hidden(layer, L - 1 - l, ys[-1]))
+    torch.cuda.synchronize()
+    assert sampler.status() == 0
+    # oracle chain with propagated bounds
+    X = ref["X_in"][:, :F].astype(np.float64)
+    Y, T = None, None
+    for l in range(L):
+        h = L - 1 - l
+        ip, ix, nd = ref["indptr"][h], ref["indices"][h], ref["n"][h]
+        ws, wn, bias = (t.double().numpy() for t in Ws[l])
+        last = l == L - 1
+        src = X if l == 0 else Y
+        Xd, Hn = src[:nd], oracle.sage_mean64(ip, ix, src)
+        Yn = oracle.sage_conv(Xd, Hn, ws, wn, bias, relu=not last)
+        S = np.abs(Xd) @ np.abs(ws) + np.abs(Hn) @ np.abs(wn) + np.abs(bias)[None, :]
+        tol = 2.0 ** -7 * S + (0.0 if last else 2.0 ** -8 * np.abs(Yn))
+        if T is not None:
+            Td, Tn = _prop(T, ip, ix, nd)
+            tol = tol + Td @ np.abs(ws) + Tn @ np.abs(wn) + 2.0 ** -7 * (Td @ np.abs(ws) + Tn @ np.abs(wn))
+        got = ys[l][:nd].float().cpu().numpy().astype(np.float64)
+        err = np.abs(got - Yn)
+        assert np.all(err <= tol + 1e-30), (l, float(np.max(err - tol)))
+        Y, T = Yn, tol

@@ -204,3 +204,21 @@ def test_gcn_brute_force_and_identities(tiny_prep, tiny_bundle):
         rows = np.nonzero(deg == k)[0]
         ys = oracle.sage_conv(X[rows], H64[rows], W / (k + 1), k * W / (k + 1))
         assert np.allclose(y[rows], ys, rtol=1e-12, atol=1e-12)
+
+
+def test_sage_mean64_matches_the_c_oracle(tiny_prep, tiny_bundle):
+    """The numpy fp64 mean used for the hidden layers (R29) equals the C oracle's fp64 shadow of
+    a5 on the same (fp32) inputs, including empty rows."""
+    from gen import CONFIGS
+    cfg = CONFIGS["tiny"]
+    order = oracle.order_roots(tiny_bundle.train, tiny_bundle.comm, cfg.num_communities,
+                               oracle.MODE_NORAND, 0.0, 5, 0)
+    ref = oracle.run_batch(tiny_prep, tiny_bundle.X, cfg.feat_dim,
+                           oracle.batch_roots(order, cfg.batch_size, 0), cfg.fanouts, 1.0, 5, 0)
+    for h in range(len(cfg.fanouts)):
+        ip, ix = ref["indptr"][h], ref["indices"][h]
+        Xs = ref["X_in"][: ref["n"][h + 1]]
+        _, h64 = oracle.sage_mean(ip, ix, Xs)
+        assert np.array_equal(oracle.sage_mean64(ip, ix, Xs), h64)
+    assert np.array_equal(oracle.sage_mean64([0, 0, 2], [1, 2], np.array([[1.0], [2.0], [6.0]])),
+                          np.array([[0.0], [4.0]]))
