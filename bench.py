@@ -552,6 +552,15 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
     ws = torch.randn(F, fo, generator=gen) / np.sqrt(F)
     wn = torch.randn(F, fo, generator=gen) / np.sqrt(F)
     layer = cmb.SageLayer(ws, wn, torch.zeros(fo), relu=True, out_bf16=True, device=graph.device)
+    # the rest of the paper's 3-layer GraphSAGE: hidden 256 -> 256, last layer 256 -> 48
+    # (ogbn-products' 47 classes rounded up to 16), run on hops L-2 .. 0 (reading R29)
+    hidden = []
+    for l in range(1, len(cfg.fanouts)):
+        fout = 48 if l == len(cfg.fanouts) - 1 else fo
+        hidden.append(cmb.SageLayer(torch.randn(fo, fout, generator=gen) / np.sqrt(fo),
+                                    torch.randn(fo, fout, generator=gen) / np.sqrt(fo),
+                                    torch.zeros(fout), relu=fout == fo, out_bf16=fout == fo,
+                                    device=graph.device, hidden=True))
     p = cfg.p_intra if args.p is None else args.p
     pipe = cmb.MiniBatchPipeline(graph, torch.from_numpy(bundle.train), cfg.batch_size,
                                  cfg.fanouts, mode=args.mode, mix=args.mix, p=p, seed=args.seed)
@@ -560,7 +569,13 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
     out = layer.alloc_out(smp.n_cap[L - 1])
     s = torch.cuda.current_stream()
     n = min(n_batches, pipe.n_batches)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(n)]
+
+    def rest_of_model():
+        y = out
+        for l, hl in enumerate(hidden):
+            y = smp.sage_hidden(hl, L - 2 - l, y)
+        return y
     gen_dy = torch.Generator(device=graph.device).manual_seed(2)
     dy = (torch.randn(smp.n_cap[L - 1], fo, generator=gen_dy, device=graph.device) * 0.01
           ).to(torch.bfloat16)
@@ -569,6 +584,7 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
         smp.sample(pipe.batch_roots(warm), p, args.seed, warm)
         smp.sage_layer(layer, out)
         smp.sage_layer_backward(layer, dy, out)
+        rest_of_model()
         smp.gather_aggregate()
     torch.cuda.synchronize()
     for k in range(n):
@@ -576,6 +592,8 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
         ev[k][0].record(s)
         smp.sage_layer(layer, out)
         ev[k][1].record(s)
+        rest_of_model()
+        ev[k][4].record(s)
         smp.gather_aggregate()
         ev[k][2].record(s)
         smp.sage_layer_backward(layer, dy, out)   # weight gradients of the same batch
@@ -584,7 +602,8 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
     torch.cuda.synchronize()
     assert smp.status() == 0
     t_layer = np.array([e[0].elapsed_time(e[1]) for e in ev])
-    t_agg = np.array([e[1].elapsed_time(e[2]) for e in ev])
+    t_agg = np.array([e[4].elapsed_time(e[2]) for e in ev])
+    t_rest = np.array([e[1].elapsed_time(e[4]) for e in ev])
     t_bwd = np.array([e[2].elapsed_time(e[3]) for e in ev])
     sz = sizes.cpu().numpy()
     nL, nd, ed = sz[:, L], sz[:, L - 1], sz[:, L + 1 + L - 1]
@@ -601,6 +620,8 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
     return {"kernel": "k_sage_layer (a4+a5+SAGEConv layer 1, tcgen05 bf16, cmb_sage_layer_forward)",
             "out_dim": fo, "out_dtype": "bf16", "relu": True, "batches": int(n),
             "layer_ms": float(np.mean(t_layer)), "gather_aggregate_ms_same_batches": float(np.mean(t_agg)),
+            "layers_2_to_L_ms": float(np.mean(t_rest)),
+            "model_forward_ms": float(np.mean(t_layer) + np.mean(t_rest)),
             "dst_rows_per_batch": float(nd.mean()), "unique_input_rows_per_batch": float(nL.mean()),
             "algorithmic_bytes_per_launch": float(np.mean(alg)),
             "roofline": {"bound": "hbm", "achieved": gbps, "peak": peak, "peak_source": peak_src,

@@ -102,6 +102,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
   }
 }
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+// global -> shared bulk copy (TMA engine, no registers) completing on an mbarrier; the image is
+// moved in 32-KB pieces, the barrier expects the whole byte count
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  mbar_expect_tx(bar, bytes);
+  for (uint32_t off = 0; off < bytes; off += 32768u) {
+    const uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(dst + off),
+        "l"(static_cast<const char*>(src) + off), "r"(n), "r"(bar)
+        : "memory");
+  }
+}
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -335,13 +353,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t ntiles = (n_dst + kM - 1) / kM;
   const uint64_t pol_keep = l2_evict_last(), pol_stream = l2_evict_first();
 
-  // weight image and bias -> shared memory, once per launch
-  for (uint32_t i = tid; i < wbytes / 16; i += kThreads)
-    reinterpret_cast<uint4*>(sW)[i] = __ldg(w_img + i);
+  // weight image -> shared memory once per launch by a bulk copy (waited for by the MMA thread
+  // before the first MMA, so it lands while the first tile is gathered); bias by plain loads
+  const uint32_t wbar = saddr(bar + 2);
   for (int i = tid; i < fo; i += kThreads) sbias[i] = bias ? __ldg(bias + i) : 0.f;
   if (tid == 0) {
     mbar_init(saddr(bar), 1);
+    mbar_init(wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    bulk_g2s(saddr(sW), w_img, wbytes, wbar);
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -384,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // ---------------------------------------------------------------- 2. MMA (one thread)
     if (tid == 0) {
+      if (tile == blockIdx.x) mbar_wait(wbar, 0);  // the weight image has landed
       tc_fence_after();
       uint32_t acc_flag = 0;
       for (int h = 0; h < halves; ++h) {
@@ -445,6 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ga.advance();
   }
 
+  if (tid == 0 && ntiles <= blockIdx.x) mbar_wait(wbar, 0);  // no tile: the copy must still land
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
@@ -721,9 +743,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr unsigned kFull = 0xffffffffu;
   const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
   const int64_t ntiles = (n_dst + kM - 1) / kM;
+  const uint32_t wbar = saddr(bar + 2);
+  uint32_t wphase = 0;
   for (int i = tid; i < fo; i += kThreads) sbias[i] = bias ? __ldg(bias + i) : 0.f;
   if (tid == 0) {
     mbar_init(saddr(bar), 1);
+    mbar_init(wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -747,68 +772,105 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t rbase = tile * kM + warp * kRowsPerWarp;
     const int64_t rem = n_dst - rbase;
     const int nr = rem <= 0 ? 0 : (rem >= kRowsPerWarp ? kRowsPerWarp : static_cast<int>(rem));
+    // phase 0 = the neighbour half (A = bf16 neighbour means, W half 1), phase 1 = the self half
+    // (A = the dst rows of Yp, W half 0); each W half is bulk-copied from L2 while A is built
     const int32_t ip = (lane <= nr && nr > 0) ? __ldg(indptr + rbase + lane) : 0;
-    for (int h = 0; h < 2; ++h) {
-      // ---- A half h: self rows (h = 0) or neighbour means (h = 1), bf16, swizzled
-#pragma unroll 2
-      for (int k = 0; k < kRowsPerWarp; ++k) {
-        const int r = warp * kRowsPerWarp + k;
-        uint4 a = make_uint4(0u, 0u, 0u, 0u);
-        if (h == 0) {
-          a = ldg16_or_zero(yp + (rbase + k) * yp_ld8 + lane, k < nr && col);
-        } else {
+    for (int ph = 0; ph < 2; ++ph) {
+      if (tid == 0) bulk_g2s(saddr(sW), w_img + (ph == 0 ? wbytes / 16 : 0), wbytes, wbar);
+      if (ph == 0) {
+        // edge ids of all 8 rows first (one round trip), then two rows at a time, each row's
+        // edges in chunks of DMAX loads issued together, summed in fp32 in CSR order
+        int32_t g[kRowsPerWarp];
+#pragma unroll
+        for (int k = 0; k < kRowsPerWarp; ++k) {
           const int32_t lo = __shfl_sync(kFull, ip, k);
           const int32_t hi = __shfl_sync(kFull, ip, k + 1);
-          const int deg = k < nr ? hi - lo : 0;
-          const int32_t my = lane < deg ? __ldg(idx + lo + lane) : 0;
-          float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          for (int j0 = 0; j0 < deg; j0 += DMAX) {
-            uint4 v[DMAX];
+          g[k] = (k < nr && lane < hi - lo) ? __ldg(idx + lo + lane) : 0;
+        }
 #pragma unroll
-            for (int j = 0; j < DMAX; ++j) {
-              const int32_t s = __shfl_sync(kFull, my, (j0 + j) & 31);
-              v[j] = ldg16_or_zero(yp + static_cast<int64_t>(s) * yp_ld8 + lane, col && j0 + j < deg);
-            }
+        for (int k0 = 0; k0 < kRowsPerWarp; k0 += 2) {
+          int deg[2];
+          float acc[2][8];
 #pragma unroll
-            for (int j = 0; j < DMAX; ++j)
-              if (j0 + j < deg) add_bf16x8(acc, v[j]);
+          for (int u = 0; u < 2; ++u) {
+            const int k = k0 + u;
+            const int32_t lo = __shfl_sync(kFull, ip, k);
+            const int32_t hi = __shfl_sync(kFull, ip, k + 1);
+            deg[u] = k < nr ? hi - lo : 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
           }
-          if (deg > 0) {
-            const float y = __frcp_rn(static_cast<float>(deg));
-            uint32_t p[4];
+          const int dm = deg[0] > deg[1] ? deg[0] : deg[1];
+          for (int j0 = 0; j0 < dm; j0 += DMAX) {
+            uint4 v[2][DMAX];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[2 * i] * y, acc[2 * i + 1] * y);
-              p[i] = *reinterpret_cast<const uint32_t*>(&b2);
+            for (int u = 0; u < 2; ++u) {
+#pragma unroll
+              for (int j = 0; j < DMAX; ++j) {
+                const int32_t e = __shfl_sync(kFull, g[k0 + u], (j0 + j) & 31);
+                v[u][j] = ldg16_or_zero(yp + static_cast<int64_t>(e) * yp_ld8 + lane,
+                                        col && j0 + j < deg[u]);
+              }
             }
-            a = make_uint4(p[0], p[1], p[2], p[3]);
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+              for (int j = 0; j < DMAX; ++j)
+                if (j0 + j < deg[u]) add_bf16x8(acc[u], v[u][j]);
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int k = k0 + u;
+            uint4 m = make_uint4(0u, 0u, 0u, 0u);
+            if (deg[u] > 0) {
+              const float y = __frcp_rn(static_cast<float>(deg[u]));
+              uint32_t pk[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const __nv_bfloat162 b2 =
+                    __floats2bfloat162_rn(acc[u][2 * i] * y, acc[u][2 * i + 1] * y);
+                pk[i] = *reinterpret_cast<const uint32_t*>(&b2);
+              }
+              m = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+            if (col && k < nr) {
+              const int r = warp * kRowsPerWarp + k, atom = lane >> 3, j = lane & 7;
+              *reinterpret_cast<uint4*>(sA + atom * (kM * kAtomBytes) + (r >> 3) * 1024 +
+                                        (r & 7) * 128 + ((j ^ (r & 7)) << 4)) = m;
+            }
           }
         }
-        if (col && k < nr) {
-          const int atom = lane >> 3, j = lane & 7;
-          *reinterpret_cast<uint4*>(sA + atom * (kM * kAtomBytes) + (r >> 3) * 1024 + (r & 7) * 128 +
-                                    ((j ^ (r & 7)) << 4)) = a;
+      } else {
+        uint4 sv[kRowsPerWarp];
+#pragma unroll
+        for (int k = 0; k < kRowsPerWarp; ++k)
+          sv[k] = ldg16_or_zero(yp + (rbase + k) * yp_ld8 + lane, k < nr && col);
+#pragma unroll
+        for (int k = 0; k < kRowsPerWarp; ++k) {
+          if (col && k < nr) {
+            const int r = warp * kRowsPerWarp + k, atom = lane >> 3, j = lane & 7;
+            *reinterpret_cast<uint4*>(sA + atom * (kM * kAtomBytes) + (r >> 3) * 1024 +
+                                      (r & 7) * 128 + ((j ^ (r & 7)) << 4)) = sv[k];
+          }
         }
       }
-      // ---- W half h (from L2)
-      const uint4* wsrc = w_img + static_cast<size_t>(h) * (wbytes / 16);
-      for (uint32_t i = tid; i < wbytes / 16; i += kThreads)
-        reinterpret_cast<uint4*>(sW)[i] = __ldg(wsrc + i);
       fence_async_smem();
       __syncthreads();
       if (tid == 0) {
+        mbar_wait(wbar, wphase);
         tc_fence_after();
         for (int st = 0; st < kin * 4; ++st) {
           const uint32_t atom = static_cast<uint32_t>(st >> 2);
           const uint32_t koff = static_cast<uint32_t>(st & 3) * 32u;
           mma_bf16(tmem, sw128_desc(sA_addr + atom * (kM * kAtomBytes) + koff),
                    sw128_desc(sW_addr + atom * (fo * kAtomBytes) + koff), idesc,
-                   (h > 0 || st > 0) ? 1u : 0u);
+                   (ph > 0 || st > 0) ? 1u : 0u);
         }
         mma_commit(saddr(bar));
       }
-      mbar_wait(saddr(bar), phase);  // A / W free again, accumulator complete after h = 1
+      mbar_wait(saddr(bar), phase);  // A / W free again, accumulator complete after phase 1
       phase ^= 1;
+      wphase ^= 1;
       tc_fence_after();
       __syncthreads();
     }
