@@ -57,3 +57,30 @@ def test_sm100a_code_in_library(cmb):
     r = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", cmb.LIB_PATH],
                        capture_output=True, text=True)
     assert "sm_100a" in r.stdout
+
+
+def test_layer_entry_points_host_checks(cmb):
+    """NEXT-4 sizes and host-checked errors (no device work): image sizes follow the
+    swizzle-atom layout, unsupported shapes report 0 / CMB_ERR_INVALID_ARGUMENT."""
+    L = cmb.lib()
+    # first layer: 2 halves x ceil(F/64) atoms x Fo rows x 128 B
+    assert L.cmb_sage_weights_bytes(100, 256) == 2 * 2 * 256 * 128
+    assert L.cmb_sage_weights_bytes(16, 48) == 2 * 1 * 48 * 128
+    assert L.cmb_sage_weights_bytes(129, 256) == 0          # K = 2F must stay <= 256
+    assert L.cmb_sage_weights_bytes(100, 40) == 0           # Fo % 16
+    assert L.cmb_gcn_weights_bytes(100, 256) == 2 * 256 * 128
+    assert L.cmb_sage_hidden_weights_bytes(256, 256) == 2 * 4 * 256 * 128
+    assert L.cmb_sage_hidden_weights_bytes(100, 256) == 0   # in_dim multiple of 64
+    assert L.cmb_sage_backward_workspace_bytes(100, 48) == 0   # backward: power-of-two Fo
+    assert L.cmb_sage_backward_workspace_bytes(100, 256) == 160 * (256 + 1) * 256 * 4
+    for call in (lambda: L.cmb_sage_pack_weights(None, None, 100, 256, None, 0, None),
+                 lambda: L.cmb_sage_layer_forward(None, None, 3, 0, None, None, 256, 1, 0, None,
+                                                  0, None),
+                 lambda: L.cmb_gcn_layer_forward(None, None, 3, 0, None, None, 256, 1, 0, None,
+                                                 0, None),
+                 lambda: L.cmb_sage_hidden_forward(None, 1, 0, None, 0, 256, None, None, 256, 1,
+                                                   1, None, 0, None),
+                 lambda: L.cmb_sage_layer_backward(None, None, 3, 0, None, 0, None, 0, 256, None,
+                                                   None, None, 0, None)):
+        assert call() == 1
+        assert b"null" in L.cmb_last_error_message()
