@@ -70,39 +70,51 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.max_mhz = None
+        self.error = None
         self._stop = threading.Event()
         self._t = None
+        self._h = None
+        try:  # NVML opened in the caller's thread; a failure is reported, not hidden
+            import pynvml
+            self._nv = pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.error = f"{type(e).__name__}: {e}"
+
+    def _sample(self):
+        try:
+            sm = self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM)
+            rs = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            self.rows.append((sm, rs))
+        except Exception as e:  # noqa: BLE001
+            self.error = f"{type(e).__name__}: {e}"
 
     def _run(self):
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-        except Exception:
-            return
         while not self._stop.is_set():
-            try:
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append((sm, rs))
-            except Exception:
-                pass
+            self._sample()
             self._stop.wait(0.005)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
-        time.sleep(0.02)
+        if self._h is not None:
+            self._sample()  # at least one sample per region, however short
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+            time.sleep(0.02)
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t is not None:
+            self._t.join()
+        if self._h is not None:
+            self._sample()
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"],
+                    "error": self.error}
         sm = [r[0] for r in self.rows]
         reasons = sorted({n for _, rs in self.rows for n, bit in self.REASONS.items() if rs & bit})
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,

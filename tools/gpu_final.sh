@@ -11,4 +11,6 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_ga
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_sample_persistent -s 3 -c 1 -o gpurun_out/final/prof_sampler_products python bench.py --steps 10 --warmup 3 --no-extra --cpu-seconds 1 > /dev/null 2>&1
 timeout 1800 python bench.py --config papers100m --steps 200 --cpu-seconds 20 > gpurun_out/final/bench_papers100m.json 2> gpurun_out/final/bench_papers100m.err
 timeout 900 ncu --set full --clock-control none -k regex:k_gather_mean_row -s 5 -c 1 -o gpurun_out/final/prof_row_papers python bench.py --config papers100m --steps 10 --warmup 3 --no-extra --cpu-seconds 1 > /dev/null 2>&1
-echo done
+
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_sage_layer -s 8 -c 2 -o gpurun_out/final/prof_layer_products python bench.py --steps 4 --warmup 3 --no-extra --layer --cpu-seconds 1 > /dev/null 2>&1
+echo done2
