@@ -217,6 +217,8 @@ struct ATileGather {
   int nr;
   int32_t nip, nself, ng[kRowsPerWarp];  // next tile
   int nnr;
+  float4 ps[RIF], pv[RIF][DMAX];  // the first row group of the current tile, loaded ahead
+  int pdeg[RIF];
 
   __device__ __forceinline__ void load_head(int64_t tile, int32_t& ip_, int32_t& self_, int& nr_) {
     const int64_t rbase = tile * kM + warp * kRowsPerWarp;
@@ -248,7 +250,29 @@ struct ATileGather {
   // gathers the current tile into sA (rows past n_dst: skipped, or zero-filled if zero_dead) and
   // starts loading the indices of tile `next`.  gcn: one half only, the row of the self-loop,
   // row-normalised adjacency (X_dst + sum of the edge rows) / (deg + 1) (reading R28)
-  __device__ __forceinline__ void build(int64_t next, uint8_t* sA, bool zero_dead, bool gcn = false) {
+  // issues the loads of the current tile's first row group into ps / pv (build(pre = true)
+  // consumes them): lets a kernel keep loads in flight across its MMA wait and epilogue
+  __device__ __forceinline__ void issue_group0() {
+    constexpr unsigned kFull = 0xffffffffu;
+    const bool col_data = lane < ((F + 3) >> 2);
+#pragma unroll
+    for (int u = 0; u < RIF; ++u) {
+      const int32_t lo = __shfl_sync(kFull, ip, u);
+      const int32_t hi = __shfl_sync(kFull, ip, u + 1);
+      pdeg[u] = u < nr ? hi - lo : 0;
+      const int32_t sv = __shfl_sync(kFull, self, u);
+      int32_t gj[DMAX];
+#pragma unroll
+      for (int j = 0; j < DMAX; ++j) gj[j] = __shfl_sync(kFull, g[u], j);
+      const bool live = u < nr && col_data;
+      ps[u] = ldg4_or_zero(x + static_cast<int64_t>(sv) * ld4 + lane, live, pol);
+#pragma unroll
+      for (int j = 0; j < DMAX; ++j)
+        pv[u][j] = ldg4_or_zero(x + static_cast<int64_t>(gj[j]) * ld4 + lane, live && j < pdeg[u], pol);
+    }
+  }
+  __device__ __forceinline__ void build(int64_t next, uint8_t* sA, bool zero_dead, bool gcn = false,
+                                        bool pre = false) {
     constexpr unsigned kFull = 0xffffffffu;
     const int f4 = (F + 3) >> 2;
     const int c0 = lane * 4;             // this lane's 4 columns of each half
@@ -260,25 +284,35 @@ struct ATileGather {
     for (int k0 = 0; k0 < kRowsPerWarp; k0 += RIF) {
       float4 s[RIF], v[RIF][DMAX];
       int deg[RIF];
-      int32_t sv[RIF], gj[RIF][DMAX];
+      if (k0 == 0 && pre) {
 #pragma unroll
-      for (int u = 0; u < RIF; ++u) {  // all shuffles first, then every load back to back
-        const int k = k0 + u;
-        const int32_t lo = __shfl_sync(kFull, ip, k);
-        const int32_t hi = __shfl_sync(kFull, ip, k + 1);
-        deg[u] = k < nr ? hi - lo : 0;
-        sv[u] = __shfl_sync(kFull, self, k);
+        for (int u = 0; u < RIF; ++u) {
+          s[u] = ps[u];
+          deg[u] = pdeg[u];
 #pragma unroll
-        for (int j = 0; j < DMAX; ++j) gj[u][j] = __shfl_sync(kFull, g[k], j);
-      }
+          for (int j = 0; j < DMAX; ++j) v[u][j] = pv[u][j];
+        }
+      } else {
+        int32_t sv[RIF], gj[RIF][DMAX];
 #pragma unroll
-      for (int u = 0; u < RIF; ++u) {
-        const bool live = k0 + u < nr && col_data;
-        s[u] = ldg4_or_zero(x + static_cast<int64_t>(sv[u]) * ld4 + lane, live, pol);
+        for (int u = 0; u < RIF; ++u) {  // all shuffles first, then every load back to back
+          const int k = k0 + u;
+          const int32_t lo = __shfl_sync(kFull, ip, k);
+          const int32_t hi = __shfl_sync(kFull, ip, k + 1);
+          deg[u] = k < nr ? hi - lo : 0;
+          sv[u] = __shfl_sync(kFull, self, k);
 #pragma unroll
-        for (int j = 0; j < DMAX; ++j)
-          v[u][j] = ldg4_or_zero(x + static_cast<int64_t>(gj[u][j]) * ld4 + lane,
-                                 live && j < deg[u], pol);
+          for (int j = 0; j < DMAX; ++j) gj[u][j] = __shfl_sync(kFull, g[k], j);
+        }
+#pragma unroll
+        for (int u = 0; u < RIF; ++u) {
+          const bool live = k0 + u < nr && col_data;
+          s[u] = ldg4_or_zero(x + static_cast<int64_t>(sv[u]) * ld4 + lane, live, pol);
+#pragma unroll
+          for (int j = 0; j < DMAX; ++j)
+            v[u][j] = ldg4_or_zero(x + static_cast<int64_t>(gj[u][j]) * ld4 + lane,
+                                   live && j < deg[u], pol);
+        }
       }
       if (k0 == 0) load_edges(nip, nnr, ng);  // next tile's edge ids, behind this group's loads
 #pragma unroll
@@ -395,10 +429,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   ga.lane = lane;
   ga.pol = pol_keep;
   ga.start(blockIdx.x);
+  ga.issue_group0();
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     // ---------------------------------------------------------------- 1. gather -> A (bf16)
-    ga.build(tile + gridDim.x, sA, false, halves == 1);
+    ga.build(tile + gridDim.x, sA, false, halves == 1, /*pre=*/true);
     fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core (async proxy)
     __syncthreads();
 
@@ -419,6 +454,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mma_commit(saddr(bar));
     }
+    ga.advance();       // the next tile's first row group loads while the MMAs run and the
+    ga.issue_group0();  // accumulator is drained (A is rewritten only after the next sync)
     mbar_wait(saddr(bar), phase);
     phase ^= 1;
     tc_fence_after();
@@ -463,7 +500,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();  // TMEM drained and A free before the next tile overwrites them
-    ga.advance();
   }
 
   if (tid == 0 && ntiles <= blockIdx.x) mbar_wait(wbar, 0);  // no tile: the copy must still land
