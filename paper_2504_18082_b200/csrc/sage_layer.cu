@@ -764,7 +764,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
                   const uint4* __restrict__ yp, int64_t yp_ld8, int kin,
                   const uint4* __restrict__ w_img, const float* __restrict__ bias, int fo,
-                  int tmem_cols, int relu, int out_bf16, void* __restrict__ out, int64_t out_ld) {
+                  int tmem_cols, int relu, int out_bf16, void* __restrict__ out, int64_t out_ld,
+                  int rows_per_tile) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   const uint32_t abytes = static_cast<uint32_t>(kin) * kM * kAtomBytes;
@@ -778,7 +779,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr unsigned kFull = 0xffffffffu;
   const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
-  const int64_t ntiles = (n_dst + kM - 1) / kM;
+  // R = rows_per_tile (32, 64 or 128) real rows per 128-row MMA tile: a layer with few dst rows
+  // (the last layer: 1024 roots) is spread over more CTAs, R / 16 rows per warp
+  const int R = rows_per_tile, rpw = R / kWarps;
+  const int64_t ntiles = (n_dst + R - 1) / R;
   const uint32_t wbar = saddr(bar + 2);
   uint32_t wphase = 0;
   for (int i = tid; i < fo; i += kThreads) sbias[i] = bias ? __ldg(bias + i) : 0.f;
@@ -805,9 +809,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t phase = 0;
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t rbase = tile * kM + warp * kRowsPerWarp;
+    const int64_t rbase = tile * R + warp * rpw;
     const int64_t rem = n_dst - rbase;
-    const int nr = rem <= 0 ? 0 : (rem >= kRowsPerWarp ? kRowsPerWarp : static_cast<int>(rem));
+    const int nr = rem <= 0 ? 0 : (rem >= rpw ? rpw : static_cast<int>(rem));
     // phase 0 = the neighbour half (A = bf16 neighbour means, W half 1), phase 1 = the self half
     // (A = the dst rows of Yp, W half 0); each W half is bulk-copied from L2 while A is built
     const int32_t ip = (lane <= nr && nr > 0) ? __ldg(indptr + rbase + lane) : 0;
@@ -870,7 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               m = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
             if (col && k < nr) {
-              const int r = warp * kRowsPerWarp + k, atom = lane >> 3, j = lane & 7;
+              const int r = warp * rpw + k, atom = lane >> 3, j = lane & 7;
               *reinterpret_cast<uint4*>(sA + atom * (kM * kAtomBytes) + (r >> 3) * 1024 +
                                         (r & 7) * 128 + ((j ^ (r & 7)) << 4)) = m;
             }
@@ -884,7 +888,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < kRowsPerWarp; ++k) {
           if (col && k < nr) {
-            const int r = warp * kRowsPerWarp + k, atom = lane >> 3, j = lane & 7;
+            const int r = warp * rpw + k, atom = lane >> 3, j = lane & 7;
             *reinterpret_cast<uint4*>(sA + atom * (kM * kAtomBytes) + (r >> 3) * 1024 +
                                       (r & 7) * 128 + ((j ^ (r & 7)) << 4)) = sv[k];
           }
@@ -913,8 +917,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- epilogue (as the first layer's)
     {
       const int q = warp & 3;
-      const int64_t row = tile * kM + q * 32 + lane;
-      const bool live = row < n_dst;
+      const int64_t row = tile * R + q * 32 + lane;
+      const bool live = q * 32 + lane < R && row < n_dst;
       for (int ch = warp >> 2; ch < fo / 16; ch += kWarps / 4) {
         uint32_t v[16];
         tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(ch * 16), v);
@@ -1218,12 +1222,15 @@ cmb_status cmb_sage_hidden_forward(const cmb_blocks* b, int32_t hop, int64_t n_d
                                   static_cast<int>(sl::hid_smem_bytes(4, 256))));
     configured = true;
   }
-  const int64_t tiles = (n_dst_cap + sl::kM - 1) / sl::kM;
+  // fewer real rows per tile when the layer has fewer than one 128-row tile per SM
+  int R = 128;
+  while (R > 32 && (n_dst_cap + R - 1) / R < sms) R >>= 1;
+  const int64_t tiles = (n_dst_cap + R - 1) / R;
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
   sl::k_sage_hidden<8><<<grid, sl::kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
       b->indptr[hop], b->indices[hop], b->sizes + hop, n_dst_cap,
       static_cast<const uint4*>(y_prev), y_prev_ld / 8, kin, static_cast<const uint4*>(w_img), bias,
-      out_dim, cols, relu, out_bf16, out, out_ld);
+      out_dim, cols, relu, out_bf16, out, out_ld, R);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
 }
