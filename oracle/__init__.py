@@ -300,3 +300,17 @@ def sage_mean64(indptr_h, idx, Xsrc) -> np.ndarray:
     nz = deg > 0
     H[nz] /= deg[nz, None]
     return H
+
+
+def sage_mean_backward(indptr_h, idx, dH, n_src) -> np.ndarray:
+    """Backward of a5's mean through the transposed block (NEXT-4 "transposed-block scatter-add",
+    reading R30), fp64: H = M X with M[d, idx[e]] += 1/deg_d for e in row d (R12), so
+    dX = M^T dH, i.e. dX[idx[e], :] += dH[d, :] / deg_d for every edge e of row d; rows of X that
+    no edge references get 0.  Returns dX [n_src, F]."""
+    ip = np.asarray(indptr_h, dtype=np.int64)
+    G = np.asarray(dH, dtype=np.float64)
+    deg = np.diff(ip)
+    dX = np.zeros((int(n_src), G.shape[1]), dtype=np.float64)
+    rows = np.repeat(np.arange(ip.shape[0] - 1), deg)
+    np.add.at(dX, np.asarray(idx, dtype=np.int64), G[rows] / deg[rows, None])
+    return dX

@@ -222,3 +222,31 @@ def test_sage_mean64_matches_the_c_oracle(tiny_prep, tiny_bundle):
         assert np.array_equal(oracle.sage_mean64(ip, ix, Xs), h64)
     assert np.array_equal(oracle.sage_mean64([0, 0, 2], [1, 2], np.array([[1.0], [2.0], [6.0]])),
                           np.array([[0.0], [4.0]]))
+
+
+# ---------------------------------------------------------------- a5 backward (reading R30)
+def test_mean_backward_is_the_adjoint(tiny_prep, tiny_bundle):
+    """<mean(X), G> == <X, mean^T(G)> for random X, G on real sampled blocks of every hop -- the
+    defining property of the transposed-block scatter-add, independent of how either side sums."""
+    from gen import CONFIGS
+    cfg = CONFIGS["tiny"]
+    order = oracle.order_roots(tiny_bundle.train, tiny_bundle.comm, cfg.num_communities,
+                               oracle.MODE_RAND, 0.0, 9, 0)
+    ref = oracle.sample_blocks(tiny_prep, oracle.batch_roots(order, cfg.batch_size, 0),
+                               cfg.fanouts, 0.7, 9, 0)
+    rng = np.random.default_rng(4)
+    for h in range(len(cfg.fanouts)):
+        ip, ix = ref["indptr"][h], ref["indices"][h]
+        n_src, n_dst = ref["n"][h + 1], ref["n"][h]
+        X = rng.standard_normal((n_src, 7))
+        G = rng.standard_normal((n_dst, 7))
+        lhs = np.sum(oracle.sage_mean64(ip, ix, X) * G)
+        rhs = np.sum(X * oracle.sage_mean_backward(ip, ix, G, n_src))
+        assert abs(lhs - rhs) <= 1e-10 * (1 + abs(lhs))
+
+
+def test_mean_backward_worked_example():
+    """Rows: d0 -> {1, 2}, d1 -> {2}, d2 -> {} over 4 src rows; dH = [[2], [3], [5]]:
+    dX[1] = 2/2 = 1, dX[2] = 2/2 + 3/1 = 4, dX[0] = dX[3] = 0 (d2 has no edges)."""
+    dX = oracle.sage_mean_backward([0, 2, 3, 3], [1, 2, 2], np.array([[2.0], [3.0], [5.0]]), 4)
+    assert np.array_equal(dX, np.array([[0.0], [1.0], [4.0], [0.0]]))
