@@ -617,6 +617,23 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
     t_agg = np.array([e[4].elapsed_time(e[2]) for e in ev])
     t_rest = np.array([e[1].elapsed_time(e[4]) for e in ev])
     t_bwd = np.array([e[2].elapsed_time(e[3]) for e in ev])
+    # R30: the aggregation's backward on layer 2's block (hop L-2) at the hidden width: dX of the
+    # layer-1 outputs (n_{L-1} x 256 fp32) += M^T dH (n_{L-2} x 256), for the last batch sampled
+    hb = max(0, L - 2)
+    ndh, nsh = int(sz[-1, hb]), int(sz[-1, hb + 1])
+    dH = torch.randn(max(1, smp.n_cap[hb]), fo, device=graph.device)
+    dX = torch.zeros(max(1, smp.n_cap[hb + 1]), fo, device=graph.device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cmb.sage_mean_backward(smp.indptr[hb], smp.indices[hb], smp.sizes[hb:hb + 1], dH, dX)
+    reps = 20
+    e0.record(s)
+    for _ in range(reps):
+        cmb.sage_mean_backward(smp.indptr[hb], smp.indices[hb], smp.sizes[hb:hb + 1], dH, dX)
+    e1.record(s)
+    torch.cuda.synchronize()
+    t_mb = e0.elapsed_time(e1) / reps
+    eh = int(sz[-1, L + 1 + hb])
+    alg_mb = ndh * fo * 4 + 4 * (ndh + 1) + 4 * eh + 2 * nsh * fo * 4
     sz = sizes.cpu().numpy()
     nL, nd, ed = sz[:, L], sz[:, L - 1], sz[:, L + 1 + L - 1]
     alg = nL * 4 * F + 4 * (nd + 1) + 4 * ed + 4 * nd + nd * 2 * fo
@@ -639,6 +656,13 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
             "roofline": {"bound": "hbm", "achieved": gbps, "peak": peak, "peak_source": peak_src,
                          "unit": "GB/s", "frac": gbps / peak},
             "tensor_tflops": float(np.mean(flops) / (np.mean(t_layer) * 1e-3) / 1e12),
+            "mean_backward_hidden": {
+                "kernel": "k_sage_mean_bwd (cmb_sage_mean_backward, R30), hop L-2 at width 256",
+                "dst_rows": ndh, "src_rows": nsh, "edges": eh, "ms": float(t_mb),
+                "algorithmic_bytes": float(alg_mb),
+                "roofline": {"bound": "hbm", "achieved": float(alg_mb / (t_mb * 1e-3) / 1e9),
+                             "peak": peak, "unit": "GB/s",
+                             "frac": float(alg_mb / (t_mb * 1e-3) / 1e9 / peak)}},
             "backward": {"kernels": "k_sage_layer_bwd + k_sage_bwd_reduce (cmb_sage_layer_backward)",
                          "ms": float(np.mean(t_bwd)),
                          "algorithmic_bytes_per_call": float(np.mean(alg_b)),

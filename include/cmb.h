@@ -427,6 +427,17 @@ CMB_API cmb_status cmb_sage_hidden_forward(const cmb_blocks* blocks, int32_t hop
                                            int32_t out_bf16, void* out, int64_t out_ld,
                                            void* stream);
 
+/* NEXT-4 aggregation backward (reading R30, the "transposed-block scatter-add"):
+ *     dX[indices[e], :] += dH[d, :] / deg_d   for every edge e of row d < *n_dst_dev,
+ * i.e. dX += M^T dH for the mean H = M X of cmb_sage_mean_aggregate.  ADDS into dx (zero it, or
+ * pass a buffer that already holds the self path's gradient).  dh: device fp32 [n_dst x ld];
+ * dx: device fp32 [n_src x ld]; rows 16-B aligned (ld % 4 == 0); columns >= feat_dim untouched.
+ * fp32 vector reductions in no fixed order: |error| <= (c_s + 2) 2^-24 (M^T |dH|)[s]. */
+CMB_API cmb_status cmb_sage_mean_backward(const int32_t* indptr, const int32_t* indices,
+                                          const int64_t* n_dst_dev, int64_t n_dst_cap,
+                                          const float* dh, int64_t dh_ld, int32_t feat_dim,
+                                          float* dx, int64_t dx_ld, void* stream);
+
 /* NEXT-4 backward (reading R27): weight gradients of the same layer for one batch,
  *     dZ = dY * 1[Y > 0] (y != NULL; y = NULL: dZ = dY),
  *     dW_self = X_dst^T dZ,  dW_neigh = H^T dZ,  db = sum_d dZ[d, :],

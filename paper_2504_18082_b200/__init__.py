@@ -53,7 +53,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sage_backward_workspace_bytes", "cmb_sage_layer_backward",
            "cmb_gcn_weights_bytes", "cmb_gcn_pack_weights", "cmb_gcn_layer_forward",
            "cmb_sage_hidden_weights_bytes", "cmb_sage_hidden_pack_weights",
-           "cmb_sage_hidden_forward",
+           "cmb_sage_hidden_forward", "cmb_sage_mean_backward",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -102,6 +102,17 @@ class BatchFeatures(ctypes.Structure):
 
 MAX_BATCHES_PER_LAUNCH = 4
 LAW_A, LAW_SLOT = 0, 1  # Knob-2 laws (include/cmb.h cmb_sample_law)
+
+
+def sage_mean_backward(indptr: torch.Tensor, indices: torch.Tensor, n_dst: torch.Tensor,
+                       dh: torch.Tensor, dx: torch.Tensor, feat_dim: Optional[int] = None):
+    """NEXT-4 (R30): dx[indices[e]] += dh[d] / deg_d over the transposed block (adds into dx).
+    n_dst: device int64 [1] count (e.g. a Sampler's sizes[h:h+1])."""
+    F = int(dh.shape[1] if feat_dim is None else feat_dim)
+    _check(lib().cmb_sage_mean_backward(_ptr(indptr), _ptr(indices), _ptr(n_dst),
+                                        int(indptr.shape[0] - 1), _ptr(dh), dh.stride(0), F,
+                                        _ptr(dx), dx.stride(0), _stream()))
+    return dx
 
 
 def _law(law) -> int:
@@ -166,6 +177,7 @@ def lib():
             "cmb_sage_backward_workspace_bytes": (SZ, [I32, I32]),
             "cmb_gcn_weights_bytes": (SZ, [I32, I32]),
             "cmb_sage_hidden_weights_bytes": (SZ, [I32, I32]),
+            "cmb_sage_mean_backward": (I32, [P, P, P, I64, P, I64, I32, P, I64, P]),
             "cmb_sage_hidden_pack_weights": (I32, [P, P, I32, I32, P, SZ, P]),
             "cmb_sage_hidden_forward": (I32, [ctypes.POINTER(Blocks), I32, I64, P, I64, I32, P, P,
                                               I32, I32, I32, P, I64, P]),

@@ -964,6 +964,57 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ----------------------------------------------------------------- NEXT-4: a5 backward (R30)
+// dX[idx[e]] += dH[d] / deg_d over the transposed block: one warp per dst row (grid stride), the
+// row's edge ids lane-parallel, lane c scaling float4 column c of dH[d] by RN(1/deg) once and
+// adding it into every src row with a vector fp32 reduction (one REDG.F32x4 per edge per lane,
+// resolved at L2 -- no read-modify-write round trip in the SM).
+__device__ __forceinline__ void red_add4(float* p, const float4& v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__global__ void __launch_bounds__(256) k_sage_mean_bwd(const int32_t* __restrict__ indptr,
+                                                       const int32_t* __restrict__ idx,
+                                                       const int64_t* __restrict__ n_dst_dev,
+                                                       int64_t n_dst_cap, const float* __restrict__ dh,
+                                                       int64_t dh_ld, int F, float* __restrict__ dx,
+                                                       int64_t dx_ld) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
+  const int lane = threadIdx.x & 31;
+  const int64_t W = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int f4 = (F + 3) >> 2;
+  for (int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < n_dst;
+       row += W) {
+    const int32_t e0 = __ldg(indptr + row), e1 = __ldg(indptr + row + 1);
+    const int deg = e1 - e0;
+    if (deg <= 0) continue;  // warp-uniform
+    const float y = __frcp_rn(static_cast<float>(deg));
+    for (int eb = 0; eb < deg; eb += 32) {  // sampled rows have deg <= 32: one pass
+      const int32_t my = eb + lane < deg ? __ldg(idx + e0 + eb + lane) : 0;
+      const int ne = deg - eb < 32 ? deg - eb : 32;
+      for (int c0 = 0; c0 < f4; c0 += 32) {
+        const int c = c0 + lane;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c < f4) {
+          v = __ldg(reinterpret_cast<const float4*>(dh + row * dh_ld) + c);
+          v = make_float4(v.x * y, v.y * y, v.z * y, v.w * y);
+          if (4 * c + 4 > F) {  // the columns past F stay untouched (added as 0)
+            if (4 * c + 1 >= F) v.y = 0.f;
+            if (4 * c + 2 >= F) v.z = 0.f;
+            if (4 * c + 3 >= F) v.w = 0.f;
+          }
+        }
+        for (int j = 0; j < ne; ++j) {
+          const int32_t s = __shfl_sync(kFull, my, j);
+          if (c < f4) red_add4(dx + static_cast<int64_t>(s) * dx_ld + 4 * c, v);
+        }
+      }
+    }
+  }
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace sl
@@ -1231,6 +1282,29 @@ cmb_status cmb_sage_hidden_forward(const cmb_blocks* b, int32_t hop, int64_t n_d
       b->indptr[hop], b->indices[hop], b->sizes + hop, n_dst_cap,
       static_cast<const uint4*>(y_prev), y_prev_ld / 8, kin, static_cast<const uint4*>(w_img), bias,
       out_dim, cols, relu, out_bf16, out, out_ld, R);
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+cmb_status cmb_sage_mean_backward(const int32_t* indptr, const int32_t* indices,
+                                  const int64_t* n_dst_dev, int64_t n_dst_cap, const float* dh,
+                                  int64_t dh_ld, int32_t feat_dim, float* dx, int64_t dx_ld,
+                                  void* stream) {
+  CMB_ARG(indptr && indices && n_dst_dev && dh && dx, "cmb_sage_mean_backward: null argument");
+  CMB_ARG(feat_dim >= 1 && dh_ld >= feat_dim && dx_ld >= feat_dim && dh_ld % 4 == 0 &&
+              dx_ld % 4 == 0 && sl::aligned16(dh) && sl::aligned16(dx),
+          "cmb_sage_mean_backward: rows must be 16-byte aligned fp32 with ld >= feat_dim");
+  CMB_ARG(n_dst_cap >= 0, "cmb_sage_mean_backward: bad n_dst_cap");
+  if (n_dst_cap == 0) return CMB_OK;
+  cmb_status st = require_sm100();
+  if (st != CMB_OK) return st;
+  int dev = 0, sms = 0;
+  CMB_CUDA(cudaGetDevice(&dev));
+  CMB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t want = (n_dst_cap + 7) / 8;
+  const int grid = static_cast<int>(want < 8ll * sms ? (want > 0 ? want : 1) : 8ll * sms);
+  sl::k_sage_mean_bwd<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      indptr, indices, n_dst_dev, n_dst_cap, dh, dh_ld, feat_dim, dx, dx_ld);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
 }

@@ -326,3 +326,35 @@ def test_three_layer_forward(name, factor):
         err = np.abs(got - Yn)
         assert np.all(err <= tol + 1e-30), (l, float(np.max(err - tol)))
         Y, T = Yn, tol
+
+
+# ---------------------------------------------------------------- a5 backward (reading R30)
+@pytest.mark.parametrize("name,factor,F,ld", [("tiny", None, 16, 16), ("products", 0.01, 100, 100),
+                                              ("products", 0.01, 7, 8), ("arxiv", None, 256, 256)])
+def test_mean_backward_parity(name, factor, F, ld):
+    """dX += M^T dH on every hop of a sampled batch (the GPU's blocks are bit-exact with the
+    oracle's, tested above); dx starts at 1 to check that the kernel adds into it."""
+    b, prep, g = _bundle(name, factor)
+    cfg = b.cfg
+    order = oracle.order_roots(b.train, b.comm, cfg.num_communities, oracle.MODE_RAND, 0.0, SEED, 0)
+    roots = oracle.batch_roots(order, cfg.batch_size, 0)
+    sampler = cmb.Sampler(g, len(roots), cfg.fanouts)
+    sampler.sample(torch.from_numpy(roots).cuda(), cfg.p_intra, SEED, 0)
+    ref = oracle.sample_blocks(prep, roots, cfg.fanouts, cfg.p_intra, SEED, 0)
+    gen = torch.Generator().manual_seed(17)
+    for h in range(len(cfg.fanouts)):
+        nd, ns = ref["n"][h], ref["n"][h + 1]
+        dH = torch.randn(nd, ld, generator=gen)
+        dx = torch.ones(ns, ld, device="cuda")
+        cmb.sage_mean_backward(sampler.indptr[h], sampler.indices[h], sampler.sizes[h:h + 1],
+                               dH.cuda(), dx, F)
+        torch.cuda.synchronize()
+        ip, ix = ref["indptr"][h], ref["indices"][h]
+        want = 1.0 + oracle.sage_mean_backward(ip, ix, dH[:, :F].double().numpy(), ns)
+        S = oracle.sage_mean_backward(ip, ix, np.abs(dH[:, :F].double().numpy()), ns)
+        cnt = np.bincount(np.asarray(ix, dtype=np.int64), minlength=ns)[:, None]
+        got = dx.cpu().double().numpy()
+        err = np.abs(got[:, :F] - want)
+        tol = (cnt + 2) * 2.0 ** -24 * (S + 1.0) + 2.0 ** -126
+        assert np.all(err <= tol), (h, float(np.max(err - tol)))
+        assert np.all(got[:, F:] == 1.0)   # columns past feat_dim untouched
