@@ -620,7 +620,8 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
     # R30: the aggregation's backward on layer 2's block (hop L-2) at the hidden width: dX of the
     # layer-1 outputs (n_{L-1} x 256 fp32) += M^T dH (n_{L-2} x 256), for the last batch sampled
     hb = max(0, L - 2)
-    ndh, nsh = int(sz[-1, hb]), int(sz[-1, hb + 1])
+    szl = sizes[-1].cpu().numpy()
+    ndh, nsh = int(szl[hb]), int(szl[hb + 1])
     dH = torch.randn(max(1, smp.n_cap[hb]), fo, device=graph.device)
     dX = torch.zeros(max(1, smp.n_cap[hb + 1]), fo, device=graph.device)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -632,7 +633,7 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
     e1.record(s)
     torch.cuda.synchronize()
     t_mb = e0.elapsed_time(e1) / reps
-    eh = int(sz[-1, L + 1 + hb])
+    eh = int(szl[L + 1 + hb])
     alg_mb = ndh * fo * 4 + 4 * (ndh + 1) + 4 * eh + 2 * nsh * fo * 4
     sz = sizes.cpu().numpy()
     nL, nd, ed = sz[:, L], sz[:, L - 1], sz[:, L + 1 + L - 1]
