@@ -441,14 +441,17 @@ def run_e2e(args, pipe, cfg, stream, K, W, world, rank):
     dev = pipe.sampler.sizes.device
     B = cfg.batch_size
     order_host = torch.empty(pipe.orderer.n, dtype=torch.int32, pin_memory=True)
-    roots_dev = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(G)]
-    sizes_host = torch.empty(G, 2 * L + 1, dtype=torch.int64, pin_memory=True)
+    # two slots: the host enqueues launch group k+1 while the device runs group k, then waits for
+    # group k's sizes only (one group in flight, the way a training loop overlaps its data path)
+    roots_dev = [[torch.empty(B, dtype=torch.int32, device=dev) for _ in range(G)] for _ in range(2)]
+    sizes_host = [torch.empty(G, 2 * L + 1, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
     h2d = d2h = 0
     epoch_cache = {}
 
-    def steps(t0, count):
+    def enqueue(t0, count, slot):
         """Steps t0 .. t0+count-1 (one sampler launch): per batch a pinned H2D copy of its
-        roots, then per batch a D2H copy of its sizes, consumed by the host after one sync."""
+        roots, the step, then a D2H copy of its sizes into the slot; returns the count."""
         nonlocal h2d, d2h
         gbs = [t * world + rank for t in range(t0, t0 + count)]
         roots = []
@@ -461,30 +464,44 @@ def run_e2e(args, pipe, cfg, stream, K, W, world, rank):
                 epoch_cache["epoch"] = epoch
                 d2h += order_host.numel() * 4
             lo, hi = b * B, min((b + 1) * B, pipe.orderer.n)
-            r = roots_dev[i][: hi - lo]
+            r = roots_dev[slot][i][: hi - lo]
             r.copy_(order_host[lo:hi], non_blocking=True)
             h2d += (hi - lo) * 4
             roots.append(r)
         ss = pipe.step_group(gbs, roots=roots)
-        for i, s in enumerate(ss):
-            sizes_host[i].copy_(s.sizes, non_blocking=True)
-            d2h += sizes_host.shape[1] * 8
-        torch.cuda.current_stream().synchronize()
-        return [int(sizes_host[i, L]) for i in range(count)]  # the host consumes the results
+        for i, smp in enumerate(ss):
+            sizes_host[slot][i].copy_(smp.sizes, non_blocking=True)
+            d2h += sizes_host[slot].shape[1] * 8
+        done[slot].record()
+        return count
 
-    for t in range(0, W, G):
-        steps(t, min(G, W - t))
+    def consume(slot, count):
+        done[slot].synchronize()
+        return [int(sizes_host[slot][i, L]) for i in range(count)]  # the host reads the results
+
+    def run(t_first, n_steps):
+        groups = [(t_first + k, min(G, n_steps - k)) for k in range(0, n_steps, G)]
+        pending = None
+        for gi, (t0, cnt) in enumerate(groups):
+            enqueue(t0, cnt, gi & 1)
+            if pending is not None:
+                consume(*pending)
+            pending = (gi & 1, cnt)
+        if pending is not None:
+            consume(*pending)
+
+    run(0, W)
     h2d = d2h = 0
     epoch_cache.clear()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for k in range(0, K, G):
-        steps(W + k, min(G, K - k))
+    run(W, K)
     el = time.perf_counter() - t0
     return {"value": K * world / el, "unit": "batches/s",
             "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
             "note": f"per step: pinned H2D of the batch's roots and D2H of its sizes read by the "
-                    f"host (one sync per launch group of {G} batches), sample+relabel+gather+"
+                    f"host (launch groups of {G} batches, one group in flight: the host enqueues "
+                    f"group k+1 before it waits for group k's sizes), sample+relabel+gather+"
                     f"aggregate on the GPU; the epoch's Knob-1 order is computed on the GPU and "
                     f"read back once per epoch inside the region (wall clock, rank-local x world)"}
 
