@@ -455,6 +455,30 @@ CMB_API cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks*
                                            int64_t y_ld, int32_t out_dim, float* dw, float* db,
                                            void* workspace, size_t workspace_bytes, void* stream);
 
+/* NEXT-4 hidden-layer backward (reading R31 = R27 applied to the R29 layer): weight
+ * gradients of a layer >= 2 on hop `hop` of the blocks, whose input is the previous layer's
+ * bf16 output y_prev (rows = local src ids of the hop, the dst rows d < n_hop its prefix):
+ *     dZ = dY * 1[Y > 0] (y != NULL; y = NULL: dZ = dY),
+ *     dW_self = y_prev[0:n_dst]^T dZ,  dW_neigh = H^T dZ,  db = sum_d dZ[d, :],
+ * H = the neighbour means exactly as cmb_sage_hidden_forward builds them (fp32 sum in CSR order
+ * times RN(1/deg), rounded to bf16).  bf16 operands, fp32 accumulation per CTA on the tensor
+ * cores, fp64 sum of the per-CTA partials (deterministic).  y_prev: device bf16 [n_src x ld]
+ * (ld % 8 == 0, ld >= in_dim, 16-B aligned); dy, y: device bf16 [n_dst x ld] (same rules with
+ * out_dim); dw: device fp32 [2 x in_dim x out_dim] (dW_self then dW_neigh, row-major like W);
+ * db: device fp32 [out_dim].  in_dim in {64, 128, 192, 256}; out_dim a power of two in
+ * [16, 256].  workspace: device, >= cmb_sage_hidden_backward_workspace_bytes (partials; the
+ * library never allocates).  n_dst = min(sizes[hop], n_dst_cap).  Host-checked errors return
+ * CMB_ERR_INVALID_ARGUMENT before any launch.
+ * Accuracy: |dW - exact| <= 2^-7 * |A|^T |dZ|, |db - exact| <= 2^-12 * sum |dZ| (R31). */
+CMB_API size_t cmb_sage_hidden_backward_workspace_bytes(int32_t in_dim, int32_t out_dim);
+CMB_API cmb_status cmb_sage_hidden_backward(const cmb_blocks* blocks, int32_t hop,
+                                            int64_t n_dst_cap, const void* y_prev,
+                                            int64_t y_prev_ld, int32_t in_dim, const void* dy,
+                                            int64_t dy_ld, const void* y, int64_t y_ld,
+                                            int32_t out_dim, float* dw, float* db,
+                                            void* workspace, size_t workspace_bytes,
+                                            void* stream);
+
 /* ------------------------------------------------------------------ status */
 /* Synchronises `stream`, returns (and clears) the sticky device status word of a
  * graph / order / sample workspace. */

@@ -54,6 +54,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_gcn_weights_bytes", "cmb_gcn_pack_weights", "cmb_gcn_layer_forward",
            "cmb_sage_hidden_weights_bytes", "cmb_sage_hidden_pack_weights",
            "cmb_sage_hidden_forward", "cmb_sage_mean_backward",
+           "cmb_sage_hidden_backward_workspace_bytes", "cmb_sage_hidden_backward",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -186,6 +187,9 @@ def lib():
                                             I32, P, I64, P]),
             "cmb_sage_layer_backward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, I64, P, I64,
                                               I32, P, P, P, SZ, P]),
+            "cmb_sage_hidden_backward_workspace_bytes": (SZ, [I32, I32]),
+            "cmb_sage_hidden_backward": (I32, [ctypes.POINTER(Blocks), I32, I64, P, I64, I32, P,
+                                               I64, P, I64, I32, P, P, P, SZ, P]),
             "cmb_get_device_status": (I32, [P, P]),
             "cmb_status_string": (ctypes.c_char_p, [I32]),
             "cmb_last_error_message": (ctypes.c_char_p, []),
@@ -494,6 +498,25 @@ class Sampler:
             _ptr(db), _ptr(ws), ws.numel(), _stream()))
         return dw[0], dw[1], db
 
+    def sage_hidden_backward(self, layer: "SageLayer", hop: int, y_prev: torch.Tensor,
+                             dy: torch.Tensor, y: Optional[torch.Tensor] = None):
+        """NEXT-4 hidden-layer backward (R31) on hop `hop` of the last sampled batch: y_prev =
+        the layer's bf16 input (the previous layer's output), dY (bf16 [>= n_hop, out_dim]) and,
+        for a ReLU layer, its output Y (bf16) -> (dW_self [F, out], dW_neigh, db) fp32."""
+        if not layer.hidden:
+            raise ValueError("layer was packed as a first layer; use SageLayer(..., hidden=True)")
+        if any(t is not None and t.dtype != torch.bfloat16 for t in (y_prev, dy, y)):
+            raise ValueError("y_prev, dy and y must be bf16")
+        F, fo = layer.feat_dim, layer.out_dim
+        ws = layer.backward_workspace()
+        dw = torch.empty(2, F, fo, dtype=torch.float32, device=layer.device)
+        db = torch.empty(fo, dtype=torch.float32, device=layer.device)
+        _check(lib().cmb_sage_hidden_backward(
+            ctypes.byref(self._blocks), int(hop), self.n_cap[hop], _ptr(y_prev), y_prev.stride(0),
+            F, _ptr(dy), dy.stride(0), _ptr(y), 0 if y is None else y.stride(0), fo, _ptr(dw),
+            _ptr(db), _ptr(ws), ws.numel(), _stream()))
+        return dw[0], dw[1], db
+
     def alloc_features_ld(self, ld: int):
         if self.x_in is None or self.x_in.stride(0) != ld:
             dev = self.graph.device
@@ -536,7 +559,8 @@ class SageLayer:
 
     def backward_workspace(self) -> torch.Tensor:
         if getattr(self, "_bws", None) is None:
-            n = lib().cmb_sage_backward_workspace_bytes(self.feat_dim, self.out_dim)
+            n = (lib().cmb_sage_hidden_backward_workspace_bytes if self.hidden else
+                 lib().cmb_sage_backward_workspace_bytes)(self.feat_dim, self.out_dim)
             if n == 0:
                 raise ValueError(f"backward needs out_dim a power of two in [16, 256] "
                                  f"(got {self.out_dim})")

@@ -758,6 +758,96 @@ inline size_t hid_smem_bytes(int kin, int fo) {
          64 + static_cast<size_t>(fo) * 4;
 }
 
+// One K half of a hidden layer's A tile in shared memory (K-major SWIZZLE_128B, one 16-KB atom per
+// 64 columns): ph 0 = the bf16 neighbour means of the warp's rows rbase .. rbase + nr - 1 (edge
+// ids of all its rows first, then two rows at a time, each row's edges in chunks of DMAX loads
+// issued together, summed in fp32 in CSR order, times RN(1/deg)); ph 1 = those rows of Yp.  The
+// warp's rows nr .. rpw - 1 (past n_dst) are written as zeros, so a tile never holds stale rows.
+template <int DMAX>
+__device__ __forceinline__ void hid_build_half(int ph, const int32_t* __restrict__ idx,
+                                               const uint4* __restrict__ yp, int64_t yp_ld8,
+                                               int32_t ip, int64_t rbase, int nr, int rpw,
+                                               int warp, int lane, bool col, uint8_t* sA) {
+  constexpr unsigned kFull = 0xffffffffu;
+  if (ph == 0) {
+    // edge ids of all 8 rows first (one round trip), then two rows at a time, each row's
+    // edges in chunks of DMAX loads issued together, summed in fp32 in CSR order
+    int32_t g[kRowsPerWarp];
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const int32_t lo = __shfl_sync(kFull, ip, k);
+      const int32_t hi = __shfl_sync(kFull, ip, k + 1);
+      g[k] = (k < nr && lane < hi - lo) ? __ldg(idx + lo + lane) : 0;
+    }
+#pragma unroll
+    for (int k0 = 0; k0 < kRowsPerWarp; k0 += 2) {
+      int deg[2];
+      float acc[2][8];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = k0 + u;
+        const int32_t lo = __shfl_sync(kFull, ip, k);
+        const int32_t hi = __shfl_sync(kFull, ip, k + 1);
+        deg[u] = k < nr ? hi - lo : 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
+      }
+      const int dm = deg[0] > deg[1] ? deg[0] : deg[1];
+      for (int j0 = 0; j0 < dm; j0 += DMAX) {
+        uint4 v[2][DMAX];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+#pragma unroll
+          for (int j = 0; j < DMAX; ++j) {
+            const int32_t e = __shfl_sync(kFull, g[k0 + u], (j0 + j) & 31);
+            v[u][j] = ldg16_or_zero(yp + static_cast<int64_t>(e) * yp_ld8 + lane,
+                                    col && j0 + j < deg[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int j = 0; j < DMAX; ++j)
+            if (j0 + j < deg[u]) add_bf16x8(acc[u], v[u][j]);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = k0 + u;
+        uint4 m = make_uint4(0u, 0u, 0u, 0u);
+        if (deg[u] > 0) {
+          const float y = __frcp_rn(static_cast<float>(deg[u]));
+          uint32_t pk[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const __nv_bfloat162 b2 =
+                __floats2bfloat162_rn(acc[u][2 * i] * y, acc[u][2 * i + 1] * y);
+            pk[i] = *reinterpret_cast<const uint32_t*>(&b2);
+          }
+          m = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+        if (col && k < rpw) {
+          const int r = warp * rpw + k, atom = lane >> 3, j = lane & 7;
+          *reinterpret_cast<uint4*>(sA + atom * (kM * kAtomBytes) + (r >> 3) * 1024 +
+                                    (r & 7) * 128 + ((j ^ (r & 7)) << 4)) = m;
+        }
+      }
+    }
+  } else {
+    uint4 sv[kRowsPerWarp];
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k)
+      sv[k] = ldg16_or_zero(yp + (rbase + k) * yp_ld8 + lane, k < nr && col);
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      if (col && k < rpw) {
+        const int r = warp * rpw + k, atom = lane >> 3, j = lane & 7;
+        *reinterpret_cast<uint4*>(sA + atom * (kM * kAtomBytes) + (r >> 3) * 1024 +
+                                  (r & 7) * 128 + ((j ^ (r & 7)) << 4)) = sv[k];
+      }
+    }
+  }
+}
+
 template <int DMAX>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sage_hidden(const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
@@ -817,83 +907,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int32_t ip = (lane <= nr && nr > 0) ? __ldg(indptr + rbase + lane) : 0;
     for (int ph = 0; ph < 2; ++ph) {
       if (tid == 0) bulk_g2s(saddr(sW), w_img + (ph == 0 ? wbytes / 16 : 0), wbytes, wbar);
-      if (ph == 0) {
-        // edge ids of all 8 rows first (one round trip), then two rows at a time, each row's
-        // edges in chunks of DMAX loads issued together, summed in fp32 in CSR order
-        int32_t g[kRowsPerWarp];
-#pragma unroll
-        for (int k = 0; k < kRowsPerWarp; ++k) {
-          const int32_t lo = __shfl_sync(kFull, ip, k);
-          const int32_t hi = __shfl_sync(kFull, ip, k + 1);
-          g[k] = (k < nr && lane < hi - lo) ? __ldg(idx + lo + lane) : 0;
-        }
-#pragma unroll
-        for (int k0 = 0; k0 < kRowsPerWarp; k0 += 2) {
-          int deg[2];
-          float acc[2][8];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int k = k0 + u;
-            const int32_t lo = __shfl_sync(kFull, ip, k);
-            const int32_t hi = __shfl_sync(kFull, ip, k + 1);
-            deg[u] = k < nr ? hi - lo : 0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
-          }
-          const int dm = deg[0] > deg[1] ? deg[0] : deg[1];
-          for (int j0 = 0; j0 < dm; j0 += DMAX) {
-            uint4 v[2][DMAX];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-#pragma unroll
-              for (int j = 0; j < DMAX; ++j) {
-                const int32_t e = __shfl_sync(kFull, g[k0 + u], (j0 + j) & 31);
-                v[u][j] = ldg16_or_zero(yp + static_cast<int64_t>(e) * yp_ld8 + lane,
-                                        col && j0 + j < deg[u]);
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-#pragma unroll
-              for (int j = 0; j < DMAX; ++j)
-                if (j0 + j < deg[u]) add_bf16x8(acc[u], v[u][j]);
-          }
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int k = k0 + u;
-            uint4 m = make_uint4(0u, 0u, 0u, 0u);
-            if (deg[u] > 0) {
-              const float y = __frcp_rn(static_cast<float>(deg[u]));
-              uint32_t pk[4];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const __nv_bfloat162 b2 =
-                    __floats2bfloat162_rn(acc[u][2 * i] * y, acc[u][2 * i + 1] * y);
-                pk[i] = *reinterpret_cast<const uint32_t*>(&b2);
-              }
-              m = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            }
-            if (col && k < nr) {
-              const int r = warp * rpw + k, atom = lane >> 3, j = lane & 7;
-              *reinterpret_cast<uint4*>(sA + atom * (kM * kAtomBytes) + (r >> 3) * 1024 +
-                                        (r & 7) * 128 + ((j ^ (r & 7)) << 4)) = m;
-            }
-          }
-        }
-      } else {
-        uint4 sv[kRowsPerWarp];
-#pragma unroll
-        for (int k = 0; k < kRowsPerWarp; ++k)
-          sv[k] = ldg16_or_zero(yp + (rbase + k) * yp_ld8 + lane, k < nr && col);
-#pragma unroll
-        for (int k = 0; k < kRowsPerWarp; ++k) {
-          if (col && k < nr) {
-            const int r = warp * rpw + k, atom = lane >> 3, j = lane & 7;
-            *reinterpret_cast<uint4*>(sA + atom * (kM * kAtomBytes) + (r >> 3) * 1024 +
-                                      (r & 7) * 128 + ((j ^ (r & 7)) << 4)) = sv[k];
-          }
-        }
-      }
+      hid_build_half<DMAX>(ph, idx, yp, yp_ld8, ip, rbase, nr, rpw, warp, lane, col, sA);
       fence_async_smem();
       __syncthreads();
       if (tid == 0) {
@@ -960,6 +974,172 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(tmem_cols)
+                 : "memory");
+  }
+}
+
+// ----------------------------------------------------------------- NEXT-4: hidden backward (R31)
+// Weight gradients of a hidden layer (reading R31 = R27 on the R29 layer):
+//     dZ = dY * 1[Y > 0],  dW_self = Yp[0:n_dst]^T dZ,  dW_neigh = H^T dZ,  db = sum_d dZ[d],
+// H = the bf16 neighbour means the forward builds.  As in k_sage_layer_bwd the reduction runs over
+// the dst rows (M = features, N = Fo, K = rows; A read MN-major from the forward's K-major image,
+// dZ staged MN-major).  One half's accumulator ([kin2*64 x Fo] fp32 = kin2/2 M blocks of Fo TMEM
+// columns, 512 at Fin = Fo = 256) is all TMEM holds, so every CTA makes two passes over its tiles
+// -- neighbour half, then self half -- and drains TMEM into its partial between them; partials
+// are summed in fp64 by k_sage_bwd_reduce (deterministic).  R real rows per 128-row tile as in the
+// forward; the rest of the tile is zero in A and in dZ.
+inline size_t hid_bwd_smem_bytes(int kin2, int fo) {
+  return 1024 + static_cast<size_t>(kin2) * kM * kAtomBytes + b_bytes(fo) + 64 +
+         static_cast<size_t>(fo) * 4;
+}
+
+template <int DMAX>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_sage_hidden_bwd(const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                      const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
+                      const uint4* __restrict__ yp, int64_t yp_ld8, int kin,
+                      const __nv_bfloat16* __restrict__ dy, int64_t dy_ld,
+                      const __nv_bfloat16* __restrict__ y, int64_t y_ld, int fo, int tmem_alloc,
+                      int rows_per_tile, float* __restrict__ part, float* __restrict__ part_db) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
+  const int kin2 = (kin + 1) & ~1;  // atoms of the A image (whole 128-feature M blocks)
+  const uint32_t abytes = static_cast<uint32_t>(kin2) * kM * kAtomBytes;
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + abytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sB + b_bytes(fo));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  float* sdb = reinterpret_cast<float*>(bar + 8);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
+  const int R = rows_per_tile, rpw = R / kWarps;
+  const int64_t ntiles = (n_dst + R - 1) / R;
+  const int m_all = 2 * kin2 * 64;
+  const int nmb = kin2 / 2;  // M blocks of one half
+
+  // A and dZ start as zeros: rows R..127 of a tile and the padding atom are never written
+  for (uint32_t i = tid; i < (abytes + b_bytes(fo)) / 16; i += kThreads)
+    reinterpret_cast<uint4*>(sA)[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (int i = tid; i < fo; i += kThreads) sdb[i] = 0.f;
+  if (tid == 0) {
+    mbar_init(saddr(bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     saddr(tmem_slot)),
+                 "r"(tmem_alloc)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int cpr = fo / 8;  // dZ staging: thread owns 8-column chunk c of rows tid / cpr + i*rstep
+  const int c = tid % cpr;
+  const int rstep = kThreads / cpr;
+  float dbacc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dbacc[i] = 0.f;
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
+                         (static_cast<uint32_t>(fo >> 3) << 17) | (static_cast<uint32_t>(kM >> 4) << 24);
+  const uint32_t sA_addr = saddr(sA), sB_addr = saddr(sB);
+  const bool col = lane < kin * 8;
+  uint32_t phase = 0;
+
+  for (int ph = 0; ph < 2; ++ph) {  // ph 0: neighbour half (dW_neigh), ph 1: self half (dW_self)
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int64_t rbase = tile * R + warp * rpw;
+      const int64_t rem = n_dst - rbase;
+      const int nr = rem <= 0 ? 0 : (rem >= rpw ? rpw : static_cast<int>(rem));
+      const int32_t ip = (ph == 0 && lane <= nr && nr > 0) ? __ldg(indptr + rbase + lane) : 0;
+      hid_build_half<DMAX>(ph, idx, yp, yp_ld8, ip, rbase, nr, rpw, warp, lane, col, sA);
+      for (int r = tid / cpr; r < R; r += rstep) {
+        const int64_t row = tile * R + r;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (row < n_dst) {
+          v = __ldg(reinterpret_cast<const uint4*>(dy + row * dy_ld) + c);
+          if (y) {
+            const uint4 m = __ldg(reinterpret_cast<const uint4*>(y + row * y_ld) + c);
+            const uint32_t* mw = reinterpret_cast<const uint32_t*>(&m);
+            uint32_t* vw = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {  // keep dY where Y > 0 (bf16 sign bit clear, nonzero)
+              const uint32_t lo = mw[i] & 0xFFFFu, hi = mw[i] >> 16;
+              const uint32_t keep = ((lo != 0u && !(lo & 0x8000u)) ? 0xFFFFu : 0u) |
+                                    ((hi != 0u && !(hi & 0x8000u)) ? 0xFFFF0000u : 0u);
+              vw[i] &= keep;
+            }
+          }
+          if (ph == 0) {
+            const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f2 = __bfloat1622float2(p2[i]);
+              dbacc[2 * i] += f2.x;
+              dbacc[2 * i + 1] += f2.y;
+            }
+          }
+        }
+        const uint32_t off = static_cast<uint32_t>(c >> 3) * (kM * kAtomBytes) + (r >> 3) * 1024 +
+                             (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(sB + off) = v;
+      }
+      fence_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        for (int mb = 0; mb < nmb; ++mb) {
+          for (int ks = 0; ks < kM / 16; ++ks) {
+            const uint64_t da = sw128_mn_desc(sA_addr + (2 * mb) * (kM * kAtomBytes) + ks * 2048,
+                                              kM * kAtomBytes);
+            const uint64_t db = sw128_mn_desc(sB_addr + ks * 2048, kM * kAtomBytes);
+            mma_bf16(tmem + static_cast<uint32_t>(mb * fo), da, db, idesc,
+                     (it > 0 || ks > 0) ? 1u : 0u);
+          }
+        }
+        mma_commit(saddr(bar));
+      }
+      mbar_wait(saddr(bar), phase);  // A and dZ may be overwritten once the MMAs have read them
+      phase ^= 1;
+      tc_fence_after();
+      __syncthreads();
+    }
+    // drain this half's accumulator into the CTA's partial (half h = 1 - ph in the reduce's order)
+    const int h = 1 - ph;
+    const int q = warp & 3;
+    for (int mb = 0; mb < nmb; ++mb) {
+      const int m = h * kin2 * 64 + mb * kM + q * 32 + lane;
+      float* dst = part + (static_cast<int64_t>(blockIdx.x) * m_all + m) * fo;
+      for (int ch = warp >> 2; ch < fo / 16; ch += kWarps / 4) {
+        uint32_t v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) +
+                      static_cast<uint32_t>(mb * fo + ch * 16), v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          reinterpret_cast<float4*>(dst + ch * 16)[i] =
+              it > 0 ? make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                   __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    tc_fence_before();  // the next pass's MMAs overwrite the columns just read
+    __syncthreads();
+    tc_fence_after();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) atomicAdd(&sdb[c * 8 + i], dbacc[i]);
+  __syncthreads();
+  for (int i = tid; i < fo; i += kThreads) part_db[static_cast<int64_t>(blockIdx.x) * fo + i] = sdb[i];
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(tmem_alloc)
                  : "memory");
   }
 }
@@ -1282,6 +1462,68 @@ cmb_status cmb_sage_hidden_forward(const cmb_blocks* b, int32_t hop, int64_t n_d
       b->indptr[hop], b->indices[hop], b->sizes + hop, n_dst_cap,
       static_cast<const uint4*>(y_prev), y_prev_ld / 8, kin, static_cast<const uint4*>(w_img), bias,
       out_dim, cols, relu, out_bf16, out, out_ld, R);
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+size_t cmb_sage_hidden_backward_workspace_bytes(int32_t in_dim, int32_t out_dim) {
+  if (cmb_sage_hidden_weights_bytes(in_dim, out_dim) == 0 || (out_dim & (out_dim - 1))) return 0;
+  const size_t kin2 = ((in_dim / 64) + 1) & ~1;
+  return static_cast<size_t>(sl::kMaxBwdCtas) * (2 * kin2 * 64 + 1) * out_dim * sizeof(float);
+}
+
+cmb_status cmb_sage_hidden_backward(const cmb_blocks* b, int32_t hop, int64_t n_dst_cap,
+                                    const void* y_prev, int64_t y_prev_ld, int32_t in_dim,
+                                    const void* dy, int64_t dy_ld, const void* y, int64_t y_ld,
+                                    int32_t out_dim, float* dw, float* db, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+  CMB_ARG(b && y_prev && dy && dw && db && workspace, "cmb_sage_hidden_backward: null argument");
+  CMB_ARG(hop >= 0 && hop < CMB_MAX_HOPS && b->indptr[hop] && b->indices[hop],
+          "cmb_sage_hidden_backward: bad hop");
+  const size_t need = cmb_sage_hidden_backward_workspace_bytes(in_dim, out_dim);
+  CMB_ARG(need != 0, "cmb_sage_hidden_backward: need in_dim in {64, 128, 192, 256} and out_dim a "
+                     "power of two in [16, 256] (got %d, %d)", in_dim, out_dim);
+  CMB_ARG(workspace_bytes >= need && sl::aligned16(workspace),
+          "cmb_sage_hidden_backward: workspace < %zu bytes or unaligned", need);
+  CMB_ARG(y_prev_ld >= in_dim && y_prev_ld % 8 == 0 && sl::aligned16(y_prev),
+          "cmb_sage_hidden_backward: y_prev rows must be 16-byte aligned bf16, ld >= in_dim");
+  CMB_ARG(dy_ld >= out_dim && dy_ld % 8 == 0 && sl::aligned16(dy) &&
+              (!y || (y_ld >= out_dim && y_ld % 8 == 0 && sl::aligned16(y))),
+          "cmb_sage_hidden_backward: dy / y rows must be 16-byte aligned bf16 with ld >= out_dim");
+  CMB_ARG(n_dst_cap >= 0, "cmb_sage_hidden_backward: bad n_dst_cap");
+  cmb_status st = require_sm100();
+  if (st != CMB_OK) return st;
+  int dev = 0, sms = 0;
+  CMB_CUDA(cudaGetDevice(&dev));
+  CMB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int kin = in_dim / 64, kin2 = (kin + 1) & ~1;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int R = 128;
+  while (R > 32 && (n_dst_cap + R - 1) / R < sms) R >>= 1;
+  const int64_t tiles = (n_dst_cap + R - 1) / R;
+  int grid = static_cast<int>(tiles < sms ? tiles : sms);
+  if (grid > sl::kMaxBwdCtas) grid = sl::kMaxBwdCtas;
+  float* part = static_cast<float*>(workspace);
+  float* part_db = part + static_cast<size_t>(sl::kMaxBwdCtas) * 2 * kin2 * 64 * out_dim;
+  if (grid > 0) {
+    int alloc = 32;
+    while (alloc < (kin2 / 2) * out_dim) alloc <<= 1;
+    static bool configured = false;
+    if (!configured) {
+      CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_hidden_bwd<8>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sl::hid_bwd_smem_bytes(4, 256))));
+      configured = true;
+    }
+    sl::k_sage_hidden_bwd<8><<<grid, sl::kThreads, sl::hid_bwd_smem_bytes(kin2, out_dim), s>>>(
+        b->indptr[hop], b->indices[hop], b->sizes + hop, n_dst_cap,
+        static_cast<const uint4*>(y_prev), y_prev_ld / 8, kin, static_cast<const __nv_bfloat16*>(dy),
+        dy_ld, static_cast<const __nv_bfloat16*>(y), y_ld, out_dim, alloc, R, part, part_db);
+    CMB_CUDA(cudaGetLastError());
+  }
+  const int64_t nout = 2ll * in_dim * out_dim + out_dim;
+  sl::k_sage_bwd_reduce<<<static_cast<int>((nout + 31) / 32), 256, 0, s>>>(
+      part, part_db, grid, in_dim, kin2, out_dim, dw, db);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
 }

@@ -358,3 +358,68 @@ def test_mean_backward_parity(name, factor, F, ld):
         tol = (cnt + 2) * 2.0 ** -24 * (S + 1.0) + 2.0 ** -126
         assert np.all(err <= tol), (h, float(np.max(err - tol)))
         assert np.all(got[:, F:] == 1.0)   # columns past feat_dim untouched
+
+
+# ---------------------------------------------------------------- hidden backward (reading R31)
+@pytest.mark.parametrize("name,factor,hop,fin,ld,fo,relu", [
+    ("tiny", None, 0, 64, 64, 64, True),           # 64 dst rows: 32-row tiles, padding atom
+    ("products", 0.01, 1, 256, 264, 256, True),    # layer 2 at the paper's widths, padded rows
+    ("products", 0.01, 0, 192, 192, 128, False),   # odd atom count, no activation
+    ("arxiv", None, 1, 256, 256, 256, True),
+    ("products", None, 1, 256, 256, 256, True),    # full-size layer 2: 16K dst rows
+    ("products", None, 0, 256, 256, 64, True),     # full-size layer 3: 1024 roots, 32-row tiles
+])
+def test_hidden_backward_parity(name, factor, hop, fin, ld, fo, relu):
+    """Weight gradients of a hidden layer (R31) on a sampled batch's hop against
+    oracle.sage_conv_backward on (Yp[0:n_dst], sage_mean64(Yp)); Yp, dY and Y are bf16 test
+    inputs, the same values on both sides (Y only decides the ReLU mask)."""
+    b, prep, g = _bundle(name, factor)
+    cfg = b.cfg
+    order = oracle.order_roots(b.train, b.comm, cfg.num_communities, oracle.MODE_RAND, 0.0, SEED, 0)
+    roots = oracle.batch_roots(order, cfg.batch_size, 1)
+    sampler = cmb.Sampler(g, len(roots), cfg.fanouts)
+    sampler.sample(torch.from_numpy(roots).cuda(), cfg.p_intra, SEED, 1)
+    ref = oracle.sample_blocks(prep, roots, cfg.fanouts, cfg.p_intra, SEED, 1)
+    nd, ns = ref["n"][hop], ref["n"][hop + 1]
+    ip, ix = ref["indptr"][hop], ref["indices"][hop]
+    gen = torch.Generator().manual_seed(23 + hop)
+    yp = (torch.randn(sampler.n_cap[hop + 1], ld, generator=gen) * 0.5).to(torch.bfloat16)
+    dY = (torch.randn(nd, fo, generator=gen) * 0.01).to(torch.bfloat16)
+    Y = torch.randn(nd, fo, generator=gen)
+    Y[torch.rand(nd, fo, generator=gen) < 0.1] = 0.0   # exact zeros are masked out too
+    Y = Y.to(torch.bfloat16)
+    dy_d = torch.zeros(sampler.n_cap[hop], fo, dtype=torch.bfloat16, device="cuda")
+    dy_d[:nd] = dY.cuda()
+    y_d = None
+    if relu:
+        y_d = torch.zeros_like(dy_d)
+        y_d[:nd] = Y.cuda()
+    layer = cmb.SageLayer(torch.zeros(fin, fo), torch.zeros(fin, fo), relu=relu, out_bf16=True,
+                          hidden=True)
+    dws, dwn, db = sampler.sage_hidden_backward(layer, hop, yp.cuda(), dy_d, y_d)
+    torch.cuda.synchronize()
+    assert sampler.status() == 0
+    Yp = yp[:ns, :fin].double().numpy()
+    Xd, H = Yp[:nd], oracle.sage_mean64(ip, ix, Yp)
+    dZ = dY.double().numpy()
+    if relu:
+        dZ = dZ * (Y.double().numpy() > 0)
+    rs, rn, rb = oracle.sage_conv_backward(Xd, H, dZ)
+    for got, want, A in ((dws, rs, Xd), (dwn, rn, H)):
+        S = np.abs(A).T @ np.abs(dZ)
+        err = np.abs(got.double().cpu().numpy() - want)
+        assert np.all(err <= 2.0 ** -7 * S + 1e-30), float(np.max(err - 2.0 ** -7 * S))
+    errb = np.abs(db.double().cpu().numpy() - rb)
+    assert np.all(errb <= 2.0 ** -12 * np.abs(dZ).sum(0) + 1e-30), float(np.max(errb))
+
+
+def test_hidden_backward_errors():
+    layer = cmb.SageLayer(torch.zeros(256, 48), torch.zeros(256, 48), hidden=True)
+    with pytest.raises(ValueError):   # needs a power-of-two out_dim
+        layer.backward_workspace()
+    first = cmb.SageLayer(torch.zeros(64, 64), torch.zeros(64, 64))
+    b, prep, g = _bundle("tiny")
+    sampler = cmb.Sampler(g, 8, b.cfg.fanouts)
+    z = torch.zeros(8, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):   # a first-layer weight image is not a hidden layer's
+        sampler.sage_hidden_backward(first, 0, z, z)

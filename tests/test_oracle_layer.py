@@ -250,3 +250,50 @@ def test_mean_backward_worked_example():
     dX[1] = 2/2 = 1, dX[2] = 2/2 + 3/1 = 4, dX[0] = dX[3] = 0 (d2 has no edges)."""
     dX = oracle.sage_mean_backward([0, 2, 3, 3], [1, 2, 2], np.array([[2.0], [3.0], [5.0]]), 4)
     assert np.array_equal(dX, np.array([[0.0], [1.0], [4.0], [0.0]]))
+
+
+# ---------------------------------------------------------------- hidden backward (reading R31)
+@pytest.mark.parametrize("relu", [False, True])
+def test_hidden_backward_matches_finite_differences(tiny_prep, tiny_bundle, relu):
+    """R31: the weight gradients of a hidden layer are R27's on (Yp[0:n_dst], mean of Yp over the
+    hop's block).  Central differences of the hidden forward chain (sage_mean64 -> sage_conv)
+    on a real sampled block of the tiny graph, a check that does not reuse the transpose."""
+    from gen import CONFIGS
+    cfg = CONFIGS["tiny"]
+    order = oracle.order_roots(tiny_bundle.train, tiny_bundle.comm, cfg.num_communities,
+                               oracle.MODE_RAND, 0.0, 7, 0)
+    roots = oracle.batch_roots(order, cfg.batch_size, 0)
+    blk = oracle.sample_blocks(tiny_prep, roots, cfg.fanouts, cfg.p_intra, 7, 0)
+    h = 0
+    ip, ix = blk["indptr"][h], blk["indices"][h]
+    nd, ns = blk["n"][h], blk["n"][h + 1]
+    rng = np.random.default_rng(11)
+    Fin, Fo = 3, 2
+    Yp = rng.standard_normal((ns, Fin))
+    Ws, Wn, b = rng.standard_normal((Fin, Fo)), rng.standard_normal((Fin, Fo)), rng.standard_normal(Fo)
+    G = rng.standard_normal((nd, Fo))
+
+    def loss():
+        Y = oracle.sage_conv(Yp[:nd], oracle.sage_mean64(ip, ix, Yp), Ws, Wn, b, relu=relu)
+        return float(np.sum(G * Y))
+
+    H = oracle.sage_mean64(ip, ix, Yp)
+    Y = oracle.sage_conv(Yp[:nd], H, Ws, Wn, b, relu=relu)
+    dWs, dWn, db = oracle.sage_conv_backward(Yp[:nd], H, G, Y, relu=relu)
+    eps = 1e-6
+    for W, dW in ((Ws, dWs), (Wn, dWn)):
+        for i in range(Fin):
+            for j in range(Fo):
+                W[i, j] += eps
+                lp = loss()
+                W[i, j] -= 2 * eps
+                lm = loss()
+                W[i, j] += eps
+                assert abs((lp - lm) / (2 * eps) - dW[i, j]) <= 1e-6 * (1 + abs(dW[i, j]))
+    for j in range(Fo):
+        b[j] += eps
+        lp = loss()
+        b[j] -= 2 * eps
+        lm = loss()
+        b[j] += eps
+        assert abs((lp - lm) / (2 * eps) - db[j]) <= 1e-6 * (1 + abs(db[j]))
