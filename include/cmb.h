@@ -467,8 +467,10 @@ CMB_API cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks*
  * out_dim); dw: device fp32 [2 x in_dim x out_dim] (dW_self then dW_neigh, row-major like W);
  * db: device fp32 [out_dim].  in_dim in {64, 128, 192, 256}; out_dim a power of two in
  * [16, 256].  workspace: device, >= cmb_sage_hidden_backward_workspace_bytes (partials; the
- * library never allocates).  n_dst = min(sizes[hop], n_dst_cap).  Host-checked errors return
- * CMB_ERR_INVALID_ARGUMENT before any launch.
+ * library never allocates).  n_dst = min(sizes[hop], n_dst_cap).  dz_out (optional, NULL to
+ * skip): device bf16 [n_dst x dz_ld] receives the masked dZ (bit-exact dY * 1[Y > 0]), the
+ * operand of cmb_sage_hidden_input_grad -- written by the same kernel, no extra pass.
+ * Host-checked errors return CMB_ERR_INVALID_ARGUMENT before any launch.
  * Accuracy: |dW - exact| <= 2^-7 * |A|^T |dZ|, |db - exact| <= 2^-12 * sum |dZ| (R31). */
 CMB_API size_t cmb_sage_hidden_backward_workspace_bytes(int32_t in_dim, int32_t out_dim);
 CMB_API cmb_status cmb_sage_hidden_backward(const cmb_blocks* blocks, int32_t hop,
@@ -477,7 +479,32 @@ CMB_API cmb_status cmb_sage_hidden_backward(const cmb_blocks* blocks, int32_t ho
                                             int64_t dy_ld, const void* y, int64_t y_ld,
                                             int32_t out_dim, float* dw, float* db,
                                             void* workspace, size_t workspace_bytes,
-                                            void* stream);
+                                            void* dz_out, int64_t dz_ld, void* stream);
+
+/* NEXT-4 hidden-layer input gradient (reading R32): the gradient that flows into the
+ * layer's input Yp (the previous layer's output) through both of its paths,
+ *     dX = P^T (dZ W_self^T) + M^T (dZ W_neigh^T),
+ * P = the dst-prefix selection (dX[d] gets dZ[d] W_self^T for d < n_dst) and M^T = the
+ * transposed-block scatter of cmb_sage_mean_backward (dX[idx[e]] += dH[d] / deg_d).  Three
+ * launches: the tensor-core layer kernel in its self-only form twice (A = dZ, B = the packed
+ * W_self^T, then W_neigh^T; fp32 out: dX rows < n_dst, dH), then the scatter into dX.
+ * wt_img: cmb_sage_hidden_pack_weights_t of the layer's W_self, W_neigh ([in_dim x out_dim]
+ * fp32 row-major, as for the forward), cmb_sage_hidden_weights_t_bytes bytes.
+ * dz: device bf16 [n_dst x dz_ld], dz_ld >= out_dim rounded up to 64, columns out_dim.. zero
+ * (cmb_sage_hidden_backward's dz_out).  dx: device fp32 [n_src_cap x dx_ld], OVERWRITTEN (zeroed
+ * first); dh: device fp32 scratch [n_dst_cap x dh_ld].  ld % 4 == 0, 16-B aligned.
+ * in_dim in [16, 256] a multiple of 16; out_dim in [1, 256].
+ * Accuracy: |dX - exact| <= 2^-7 * (P^T |dZ||W_self|^T + M^T |dZ||W_neigh|^T) (R32). */
+CMB_API size_t cmb_sage_hidden_weights_t_bytes(int32_t in_dim, int32_t out_dim);
+CMB_API cmb_status cmb_sage_hidden_pack_weights_t(const float* w_self, const float* w_neigh,
+                                                  int32_t in_dim, int32_t out_dim, void* wt_img,
+                                                  size_t wt_img_bytes, void* stream);
+CMB_API cmb_status cmb_sage_hidden_input_grad(const cmb_blocks* blocks, int32_t hop,
+                                              int64_t n_dst_cap, int64_t n_src_cap,
+                                              const void* dz, int64_t dz_ld, int32_t out_dim,
+                                              const void* wt_img, int32_t in_dim, float* dx,
+                                              int64_t dx_ld, float* dh, int64_t dh_ld,
+                                              void* stream);
 
 /* ------------------------------------------------------------------ status */
 /* Synchronises `stream`, returns (and clears) the sticky device status word of a

@@ -314,3 +314,17 @@ def sage_mean_backward(indptr_h, idx, dH, n_src) -> np.ndarray:
     rows = np.repeat(np.arange(ip.shape[0] - 1), deg)
     np.add.at(dX, np.asarray(idx, dtype=np.int64), G[rows] / deg[rows, None])
     return dX
+
+
+def sage_hidden_input_grad(indptr_h, idx, dZ, W_self, W_neigh, n_src) -> np.ndarray:
+    """Gradient into a hidden layer's input Yp (NEXT-4 backward of layers 2-3, reading R32), fp64:
+    the layer (R29) reads Yp through its dst-prefix rows (Yp[d] W_self, d < n_dst: the dst list
+    is the prefix of the src list, R8) and through the neighbour mean (M Yp) W_neigh, so by the
+    chain rule dYp = P^T (dZ W_self^T) + M^T (dZ W_neigh^T), with M^T = sage_mean_backward (R30).
+    dZ = dY * sigma'(Z) is an input.  Returns dYp [n_src, Fin]."""
+    G = np.asarray(dZ, dtype=np.float64)
+    Ws = np.asarray(W_self, dtype=np.float64)
+    Wn = np.asarray(W_neigh, dtype=np.float64)
+    dX = sage_mean_backward(indptr_h, idx, G @ Wn.T, n_src)
+    dX[:G.shape[0]] += G @ Ws.T
+    return dX

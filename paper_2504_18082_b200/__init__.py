@@ -55,6 +55,8 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sage_hidden_weights_bytes", "cmb_sage_hidden_pack_weights",
            "cmb_sage_hidden_forward", "cmb_sage_mean_backward",
            "cmb_sage_hidden_backward_workspace_bytes", "cmb_sage_hidden_backward",
+           "cmb_sage_hidden_weights_t_bytes", "cmb_sage_hidden_pack_weights_t",
+           "cmb_sage_hidden_input_grad",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -189,7 +191,11 @@ def lib():
                                               I32, P, P, P, SZ, P]),
             "cmb_sage_hidden_backward_workspace_bytes": (SZ, [I32, I32]),
             "cmb_sage_hidden_backward": (I32, [ctypes.POINTER(Blocks), I32, I64, P, I64, I32, P,
-                                               I64, P, I64, I32, P, P, P, SZ, P]),
+                                               I64, P, I64, I32, P, P, P, SZ, P, I64, P]),
+            "cmb_sage_hidden_weights_t_bytes": (SZ, [I32, I32]),
+            "cmb_sage_hidden_pack_weights_t": (I32, [P, P, I32, I32, P, SZ, P]),
+            "cmb_sage_hidden_input_grad": (I32, [ctypes.POINTER(Blocks), I32, I64, I64, P, I64, I32,
+                                                 P, I32, P, I64, P, I64, P]),
             "cmb_get_device_status": (I32, [P, P]),
             "cmb_status_string": (ctypes.c_char_p, [I32]),
             "cmb_last_error_message": (ctypes.c_char_p, []),
@@ -499,10 +505,12 @@ class Sampler:
         return dw[0], dw[1], db
 
     def sage_hidden_backward(self, layer: "SageLayer", hop: int, y_prev: torch.Tensor,
-                             dy: torch.Tensor, y: Optional[torch.Tensor] = None):
+                             dy: torch.Tensor, y: Optional[torch.Tensor] = None,
+                             dz_out: Optional[torch.Tensor] = None):
         """NEXT-4 hidden-layer backward (R31) on hop `hop` of the last sampled batch: y_prev =
         the layer's bf16 input (the previous layer's output), dY (bf16 [>= n_hop, out_dim]) and,
-        for a ReLU layer, its output Y (bf16) -> (dW_self [F, out], dW_neigh, db) fp32."""
+        for a ReLU layer, its output Y (bf16) -> (dW_self [F, out], dW_neigh, db) fp32.
+        dz_out (bf16 [>= n_hop, >= out_dim]) receives the masked dZ for sage_hidden_input_grad."""
         if not layer.hidden:
             raise ValueError("layer was packed as a first layer; use SageLayer(..., hidden=True)")
         if any(t is not None and t.dtype != torch.bfloat16 for t in (y_prev, dy, y)):
@@ -514,8 +522,27 @@ class Sampler:
         _check(lib().cmb_sage_hidden_backward(
             ctypes.byref(self._blocks), int(hop), self.n_cap[hop], _ptr(y_prev), y_prev.stride(0),
             F, _ptr(dy), dy.stride(0), _ptr(y), 0 if y is None else y.stride(0), fo, _ptr(dw),
-            _ptr(db), _ptr(ws), ws.numel(), _stream()))
+            _ptr(db), _ptr(ws), ws.numel(), _ptr(dz_out),
+            0 if dz_out is None else dz_out.stride(0), _stream()))
         return dw[0], dw[1], db
+
+    def sage_hidden_input_grad(self, layer: "SageLayer", hop: int, dz: torch.Tensor,
+                               dx: Optional[torch.Tensor] = None):
+        """NEXT-4 (R32): gradient into a hidden layer's input Yp from dZ (bf16 [>= n_hop, ld],
+        ld >= out_dim rounded up to 64, padding columns zero) -> dX fp32 [n_cap[hop+1], in_dim]
+        (rows >= n_{hop+1} zero)."""
+        if not layer.hidden or dz.dtype != torch.bfloat16:
+            raise ValueError("needs a hidden SageLayer and a bf16 dz")
+        F, fo = layer.feat_dim, layer.out_dim
+        wt = layer.transposed_image()
+        if dx is None:
+            dx = torch.empty(self.n_cap[hop + 1], F, dtype=torch.float32, device=layer.device)
+        dh = torch.empty(max(1, self.n_cap[hop]), F, dtype=torch.float32, device=layer.device)
+        _check(lib().cmb_sage_hidden_input_grad(
+            ctypes.byref(self._blocks), int(hop), self.n_cap[hop], self.n_cap[hop + 1], _ptr(dz),
+            dz.stride(0), fo, _ptr(wt), F, _ptr(dx), dx.stride(0), _ptr(dh), dh.stride(0),
+            _stream()))
+        return dx
 
     def alloc_features_ld(self, ld: int):
         if self.x_in is None or self.x_in.stride(0) != ld:
@@ -553,9 +580,24 @@ class SageLayer:
         self.repack()
 
     def repack(self):
+        self._wt = None  # the transposed image follows the weights
         pack = lib().cmb_sage_hidden_pack_weights if self.hidden else lib().cmb_sage_pack_weights
         _check(pack(_ptr(self.w_self), _ptr(self.w_neigh), self.feat_dim, self.out_dim,
                     _ptr(self.w_img), self.w_img.numel(), _stream()))
+
+    def transposed_image(self) -> torch.Tensor:
+        """bf16 image of (W_self^T, W_neigh^T) for the input-gradient GEMMs (R32); rebuilt by
+        repack()."""
+        if getattr(self, "_wt", None) is None:
+            n = lib().cmb_sage_hidden_weights_t_bytes(self.feat_dim, self.out_dim)
+            if n == 0:
+                raise ValueError(f"input gradient needs in_dim in [16, 256] a multiple of 16 "
+                                 f"(got {self.feat_dim})")
+            self._wt = torch.empty(n, dtype=torch.uint8, device=self.device)
+            _check(lib().cmb_sage_hidden_pack_weights_t(
+                _ptr(self.w_self), _ptr(self.w_neigh), self.feat_dim, self.out_dim,
+                _ptr(self._wt), self._wt.numel(), _stream()))
+        return self._wt
 
     def backward_workspace(self) -> torch.Tensor:
         if getattr(self, "_bws", None) is None:

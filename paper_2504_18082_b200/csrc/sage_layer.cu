@@ -181,8 +181,11 @@ __device__ __forceinline__ uint2 pack_bf16x4(float4 v) {
 // ----------------------------------------------------------------- weight packing
 // w_img[element (n, k)] = bf16(W_h[c][n]) for k = half h, column c < F; 0 for the padding columns.
 // w_neigh == NULL: one half only (the GCN form, W = w_self)
+// trans != 0: the halves are the transposes of row-major [fo x F] matrices (w[n * F + c]), the
+// image of the input-gradient GEMM dZ W^T of a hidden layer (K = its out_dim, N = its in_dim)
 __global__ void k_pack_weights(const float* __restrict__ w_self, const float* __restrict__ w_neigh,
-                               int F, int fo, int kh, __nv_bfloat16* __restrict__ img) {
+                               int F, int fo, int kh, __nv_bfloat16* __restrict__ img,
+                               int trans = 0) {
   const int kcols = kh * 64;
   const int64_t total = static_cast<int64_t>((w_neigh ? 2 : 1) * kcols) * fo;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -191,7 +194,9 @@ __global__ void k_pack_weights(const float* __restrict__ w_self, const float* __
     const int k = static_cast<int>(i / fo);
     const int h = k / kcols, c = k % kcols;
     float v = 0.f;
-    if (c < F) v = (h == 0 ? w_self : w_neigh)[static_cast<int64_t>(c) * fo + n];
+    if (c < F)
+      v = (h == 0 ? w_self : w_neigh)[trans ? static_cast<int64_t>(n) * F + c
+                                            : static_cast<int64_t>(c) * fo + n];
     img[sw128_off(n, h, c, kh, fo) >> 1] = __float2bfloat16_rn(v);
   }
 }
@@ -855,7 +860,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const uint4* __restrict__ yp, int64_t yp_ld8, int kin,
                   const uint4* __restrict__ w_img, const float* __restrict__ bias, int fo,
                   int tmem_cols, int relu, int out_bf16, void* __restrict__ out, int64_t out_ld,
-                  int rows_per_tile) {
+                  int rows_per_tile, int halves = 2) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   const uint32_t abytes = static_cast<uint32_t>(kin) * kM * kAtomBytes;
@@ -905,7 +910,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // phase 0 = the neighbour half (A = bf16 neighbour means, W half 1), phase 1 = the self half
     // (A = the dst rows of Yp, W half 0); each W half is bulk-copied from L2 while A is built
     const int32_t ip = (lane <= nr && nr > 0) ? __ldg(indptr + rbase + lane) : 0;
-    for (int ph = 0; ph < 2; ++ph) {
+    // halves == 1: the self phase only, against the image's first half (input gradients, R32)
+    const int ph0 = halves == 1 ? 1 : 0;
+    for (int ph = ph0; ph < 2; ++ph) {
       if (tid == 0) bulk_g2s(saddr(sW), w_img + (ph == 0 ? wbytes / 16 : 0), wbytes, wbar);
       hid_build_half<DMAX>(ph, idx, yp, yp_ld8, ip, rbase, nr, rpw, warp, lane, col, sA);
       fence_async_smem();
@@ -918,7 +925,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t koff = static_cast<uint32_t>(st & 3) * 32u;
           mma_bf16(tmem, sw128_desc(sA_addr + atom * (kM * kAtomBytes) + koff),
                    sw128_desc(sW_addr + atom * (fo * kAtomBytes) + koff), idesc,
-                   (ph > 0 || st > 0) ? 1u : 0u);
+                   (ph > ph0 || st > 0) ? 1u : 0u);
         }
         mma_commit(saddr(bar));
       }
@@ -1000,7 +1007,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const uint4* __restrict__ yp, int64_t yp_ld8, int kin,
                       const __nv_bfloat16* __restrict__ dy, int64_t dy_ld,
                       const __nv_bfloat16* __restrict__ y, int64_t y_ld, int fo, int tmem_alloc,
-                      int rows_per_tile, float* __restrict__ part, float* __restrict__ part_db) {
+                      int rows_per_tile, float* __restrict__ part, float* __restrict__ part_db,
+                      __nv_bfloat16* __restrict__ dz_out, int64_t dz_ld) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   const int kin2 = (kin + 1) & ~1;  // atoms of the A image (whole 128-feature M blocks)
@@ -1076,6 +1084,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (ph == 0) {
+            if (dz_out)  // the masked dZ, the A operand of the input-gradient GEMMs (R32)
+              *reinterpret_cast<uint4*>(dz_out + row * dz_ld + c * 8) = v;
             const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -1476,8 +1486,11 @@ cmb_status cmb_sage_hidden_backward(const cmb_blocks* b, int32_t hop, int64_t n_
                                     const void* y_prev, int64_t y_prev_ld, int32_t in_dim,
                                     const void* dy, int64_t dy_ld, const void* y, int64_t y_ld,
                                     int32_t out_dim, float* dw, float* db, void* workspace,
-                                    size_t workspace_bytes, void* stream) {
+                                    size_t workspace_bytes, void* dz_out, int64_t dz_ld,
+                                    void* stream) {
   CMB_ARG(b && y_prev && dy && dw && db && workspace, "cmb_sage_hidden_backward: null argument");
+  CMB_ARG(!dz_out || (dz_ld >= out_dim && dz_ld % 8 == 0 && sl::aligned16(dz_out)),
+          "cmb_sage_hidden_backward: dz_out rows must be 16-byte aligned bf16 with ld >= out_dim");
   CMB_ARG(hop >= 0 && hop < CMB_MAX_HOPS && b->indptr[hop] && b->indices[hop],
           "cmb_sage_hidden_backward: bad hop");
   const size_t need = cmb_sage_hidden_backward_workspace_bytes(in_dim, out_dim);
@@ -1518,12 +1531,97 @@ cmb_status cmb_sage_hidden_backward(const cmb_blocks* b, int32_t hop, int64_t n_
     sl::k_sage_hidden_bwd<8><<<grid, sl::kThreads, sl::hid_bwd_smem_bytes(kin2, out_dim), s>>>(
         b->indptr[hop], b->indices[hop], b->sizes + hop, n_dst_cap,
         static_cast<const uint4*>(y_prev), y_prev_ld / 8, kin, static_cast<const __nv_bfloat16*>(dy),
-        dy_ld, static_cast<const __nv_bfloat16*>(y), y_ld, out_dim, alloc, R, part, part_db);
+        dy_ld, static_cast<const __nv_bfloat16*>(y), y_ld, out_dim, alloc, R, part, part_db,
+        static_cast<__nv_bfloat16*>(dz_out), dz_ld);
     CMB_CUDA(cudaGetLastError());
   }
   const int64_t nout = 2ll * in_dim * out_dim + out_dim;
   sl::k_sage_bwd_reduce<<<static_cast<int>((nout + 31) / 32), 256, 0, s>>>(
       part, part_db, grid, in_dim, kin2, out_dim, dw, db);
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+cmb_status cmb_sage_hidden_pack_weights_t(const float* w_self, const float* w_neigh,
+                                          int32_t in_dim, int32_t out_dim, void* wt_img,
+                                          size_t wt_img_bytes, void* stream) {
+  CMB_ARG(w_self && w_neigh && wt_img, "cmb_sage_hidden_pack_weights_t: null argument");
+  CMB_ARG(in_dim >= 16 && in_dim <= 256 && in_dim % 16 == 0 && out_dim >= 1 && out_dim <= 256,
+          "cmb_sage_hidden_pack_weights_t: need in_dim in [16, 256] a multiple of 16 and "
+          "1 <= out_dim <= 256 (got %d, %d)", in_dim, out_dim);
+  const int kt = (out_dim + 63) / 64;  // K = out_dim, padded to whole 64-column atoms
+  const size_t need = sl::w_img_bytes(kt, in_dim);
+  CMB_ARG(wt_img_bytes >= need && sl::aligned16(wt_img),
+          "cmb_sage_hidden_pack_weights_t: wt_img smaller than %zu bytes or unaligned", need);
+  cmb_status st = require_sm100();
+  if (st != CMB_OK) return st;
+  const int64_t total = static_cast<int64_t>(2 * kt * 64) * in_dim;
+  sl::k_pack_weights<<<static_cast<int>((total + 255) / 256), 256, 0,
+                       static_cast<cudaStream_t>(stream)>>>(
+      w_self, w_neigh, out_dim, in_dim, kt, static_cast<__nv_bfloat16*>(wt_img), 1);
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+size_t cmb_sage_hidden_weights_t_bytes(int32_t in_dim, int32_t out_dim) {
+  if (in_dim < 16 || in_dim > 256 || in_dim % 16 || out_dim < 1 || out_dim > 256) return 0;
+  return sl::w_img_bytes((out_dim + 63) / 64, in_dim);
+}
+
+cmb_status cmb_sage_hidden_input_grad(const cmb_blocks* b, int32_t hop, int64_t n_dst_cap,
+                                      int64_t n_src_cap, const void* dz, int64_t dz_ld,
+                                      int32_t out_dim, const void* wt_img, int32_t in_dim,
+                                      float* dx, int64_t dx_ld, float* dh, int64_t dh_ld,
+                                      void* stream) {
+  CMB_ARG(b && dz && wt_img && dx && dh, "cmb_sage_hidden_input_grad: null argument");
+  CMB_ARG(hop >= 0 && hop < CMB_MAX_HOPS && b->indptr[hop] && b->indices[hop],
+          "cmb_sage_hidden_input_grad: bad hop");
+  CMB_ARG(cmb_sage_hidden_weights_t_bytes(in_dim, out_dim) != 0,
+          "cmb_sage_hidden_input_grad: need in_dim in [16, 256] a multiple of 16 and "
+          "1 <= out_dim <= 256 (got %d, %d)", in_dim, out_dim);
+  const int kt = (out_dim + 63) / 64;
+  CMB_ARG(dz_ld >= kt * 64 && dz_ld % 8 == 0 && sl::aligned16(dz),
+          "cmb_sage_hidden_input_grad: dz rows must be 16-byte aligned bf16 with ld >= "
+          "out_dim rounded up to 64 (columns out_dim.. zero)");
+  CMB_ARG(dx_ld >= in_dim && dx_ld % 4 == 0 && sl::aligned16(dx) && dh_ld >= in_dim &&
+              dh_ld % 4 == 0 && sl::aligned16(dh),
+          "cmb_sage_hidden_input_grad: dx / dh rows must be 16-byte aligned fp32, ld >= in_dim");
+  CMB_ARG(n_dst_cap >= 0 && n_src_cap >= n_dst_cap, "cmb_sage_hidden_input_grad: bad capacities");
+  cmb_status st = require_sm100();
+  if (st != CMB_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CMB_CUDA(cudaMemsetAsync(dx, 0, static_cast<size_t>(n_src_cap) * dx_ld * sizeof(float), s));
+  if (n_dst_cap == 0) return CMB_OK;
+  int dev = 0, sms = 0;
+  CMB_CUDA(cudaGetDevice(&dev));
+  CMB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  static bool configured = false;
+  if (!configured) {
+    CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_hidden<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sl::hid_smem_bytes(4, 256))));
+    configured = true;
+  }
+  int R = 128;
+  while (R > 32 && (n_dst_cap + R - 1) / R < sms) R >>= 1;
+  const int64_t tiles = (n_dst_cap + R - 1) / R;
+  const int grid = static_cast<int>(tiles < sms ? tiles : sms);
+  const int cols = in_dim <= 32 ? 32 : in_dim <= 64 ? 64 : in_dim <= 128 ? 128 : 256;
+  const size_t smem = sl::hid_smem_bytes(kt, in_dim);
+  const uint4* wt = static_cast<const uint4*>(wt_img);
+  const size_t half16 = sl::w_img_bytes(kt, in_dim, 1) / 16;
+  // dX[d] = dZ[d] W_self^T for d < n_dst (stored); dH = dZ W_neigh^T; dX += M^T dH (R30)
+  sl::k_sage_hidden<8><<<grid, sl::kThreads, smem, s>>>(
+      b->indptr[hop], b->indices[hop], b->sizes + hop, n_dst_cap, static_cast<const uint4*>(dz),
+      dz_ld / 8, kt, wt, nullptr, in_dim, cols, 0, 0, dx, dx_ld, R, 1);
+  CMB_CUDA(cudaGetLastError());
+  sl::k_sage_hidden<8><<<grid, sl::kThreads, smem, s>>>(
+      b->indptr[hop], b->indices[hop], b->sizes + hop, n_dst_cap, static_cast<const uint4*>(dz),
+      dz_ld / 8, kt, wt + half16, nullptr, in_dim, cols, 0, 0, dh, dh_ld, R, 1);
+  CMB_CUDA(cudaGetLastError());
+  const int64_t want = (n_dst_cap + 7) / 8;
+  const int mgrid = static_cast<int>(want < 8ll * sms ? want : 8ll * sms);
+  sl::k_sage_mean_bwd<<<mgrid, 256, 0, s>>>(b->indptr[hop], b->indices[hop], b->sizes + hop,
+                                            n_dst_cap, dh, dh_ld, in_dim, dx, dx_ld);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
 }

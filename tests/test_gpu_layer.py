@@ -396,9 +396,12 @@ def test_hidden_backward_parity(name, factor, hop, fin, ld, fo, relu):
         y_d[:nd] = Y.cuda()
     layer = cmb.SageLayer(torch.zeros(fin, fo), torch.zeros(fin, fo), relu=relu, out_bf16=True,
                           hidden=True)
-    dws, dwn, db = sampler.sage_hidden_backward(layer, hop, yp.cuda(), dy_d, y_d)
+    dz_d = torch.full((sampler.n_cap[hop], fo), float("nan"), dtype=torch.bfloat16, device="cuda")
+    dws, dwn, db = sampler.sage_hidden_backward(layer, hop, yp.cuda(), dy_d, y_d, dz_out=dz_d)
     torch.cuda.synchronize()
     assert sampler.status() == 0
+    mz = torch.where(Y > 0, dY, torch.zeros_like(dY)) if relu else dY   # R31's dZ, bit for bit
+    assert torch.equal(dz_d[:nd].cpu().view(torch.int16), mz.view(torch.int16))
     Yp = yp[:ns, :fin].double().numpy()
     Xd, H = Yp[:nd], oracle.sage_mean64(ip, ix, Yp)
     dZ = dY.double().numpy()
@@ -423,3 +426,46 @@ def test_hidden_backward_errors():
     z = torch.zeros(8, 64, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ValueError):   # a first-layer weight image is not a hidden layer's
         sampler.sage_hidden_backward(first, 0, z, z)
+
+
+# ---------------------------------------------------------------- hidden input gradient (R32)
+@pytest.mark.parametrize("name,factor,hop,fin,fo", [
+    ("tiny", None, 0, 64, 64),
+    ("products", 0.01, 1, 256, 256),     # layer 2's input gradient at the paper's widths
+    ("products", 0.01, 0, 128, 64),      # layer 3 (1024-root batches scaled down)
+    ("arxiv", None, 1, 256, 256),
+    ("products", None, 1, 256, 256),     # full size: 16K dst rows, ~145K src rows
+])
+def test_hidden_input_grad_parity(name, factor, hop, fin, fo):
+    """dYp = P^T dZ W_self^T + M^T dZ W_neigh^T (R32) against oracle.sage_hidden_input_grad;
+    every row of the output past n_src is zero."""
+    b, prep, g = _bundle(name, factor)
+    cfg = b.cfg
+    order = oracle.order_roots(b.train, b.comm, cfg.num_communities, oracle.MODE_RAND, 0.0, SEED, 0)
+    roots = oracle.batch_roots(order, cfg.batch_size, 1)
+    sampler = cmb.Sampler(g, len(roots), cfg.fanouts)
+    sampler.sample(torch.from_numpy(roots).cuda(), cfg.p_intra, SEED, 1)
+    ref = oracle.sample_blocks(prep, roots, cfg.fanouts, cfg.p_intra, SEED, 1)
+    nd, ns = ref["n"][hop], ref["n"][hop + 1]
+    ip, ix = ref["indptr"][hop], ref["indices"][hop]
+    gen = torch.Generator().manual_seed(41 + hop)
+    ws = torch.randn(fin, fo, generator=gen) / np.sqrt(fo)
+    wn = torch.randn(fin, fo, generator=gen) / np.sqrt(fo)
+    dZ = (torch.randn(nd, fo, generator=gen) * 0.01).to(torch.bfloat16)
+    ld = ((fo + 63) // 64) * 64
+    dz_d = torch.zeros(sampler.n_cap[hop], ld, dtype=torch.bfloat16, device="cuda")
+    dz_d[:nd, :fo] = dZ.cuda()
+    layer = cmb.SageLayer(ws, wn, hidden=True)
+    dx = torch.full((sampler.n_cap[hop + 1], fin), float("nan"), device="cuda")
+    sampler.sage_hidden_input_grad(layer, hop, dz_d, dx)
+    torch.cuda.synchronize()
+    assert sampler.status() == 0
+    Z = dZ.double().numpy()
+    want = oracle.sage_hidden_input_grad(ip, ix, Z, ws.double().numpy(), wn.double().numpy(), ns)
+    S = oracle.sage_hidden_input_grad(ip, ix, np.abs(Z), np.abs(ws.double().numpy()),
+                                      np.abs(wn.double().numpy()), ns)
+    got = dx.cpu().double().numpy()
+    err = np.abs(got[:ns] - want)
+    tol = 2.0 ** -7 * S + 1e-30
+    assert np.all(err <= tol), float(np.max(err - tol))
+    assert np.all(got[ns:] == 0.0)

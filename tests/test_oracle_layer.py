@@ -297,3 +297,43 @@ def test_hidden_backward_matches_finite_differences(tiny_prep, tiny_bundle, relu
         lm = loss()
         b[j] += eps
         assert abs((lp - lm) / (2 * eps) - db[j]) <= 1e-6 * (1 + abs(db[j]))
+
+
+# ---------------------------------------------------------------- hidden input gradient (R32)
+@pytest.mark.parametrize("relu", [False, True])
+def test_hidden_input_grad_matches_finite_differences(tiny_prep, tiny_bundle, relu):
+    """R32: dYp of L = sum(G * sigma(Yp[:nd] W_self + mean(Yp) W_neigh + b)) by central
+    differences in every entry of Yp on a real sampled block (hop 1 of tiny: shared and unused
+    src rows, an independent check of both the prefix path and the transposed block)."""
+    from gen import CONFIGS
+    cfg = CONFIGS["tiny"]
+    order = oracle.order_roots(tiny_bundle.train, tiny_bundle.comm, cfg.num_communities,
+                               oracle.MODE_RAND, 0.0, 7, 0)
+    roots = oracle.batch_roots(order, cfg.batch_size, 0)[:6]
+    blk = oracle.sample_blocks(tiny_prep, roots, cfg.fanouts, cfg.p_intra, 7, 0)
+    h = 1
+    ip, ix = blk["indptr"][h], blk["indices"][h]
+    nd, ns = blk["n"][h], blk["n"][h + 1]
+    rng = np.random.default_rng(13)
+    Fin, Fo = 2, 3
+    Yp = rng.standard_normal((ns + 2, Fin))   # two rows past n_src: no gradient may reach them
+    Ws, Wn, b = rng.standard_normal((Fin, Fo)), rng.standard_normal((Fin, Fo)), rng.standard_normal(Fo)
+    G = rng.standard_normal((nd, Fo))
+
+    def fwd():
+        return oracle.sage_conv(Yp[:nd], oracle.sage_mean64(ip, ix, Yp[:ns]), Ws, Wn, b, relu=relu)
+
+    Y = fwd()
+    dZ = G * (Y > 0) if relu else G
+    dX = oracle.sage_hidden_input_grad(ip, ix, dZ, Ws, Wn, ns)
+    assert dX.shape == (ns, Fin)
+    eps = 1e-6
+    for i in range(ns + 2):
+        for j in range(Fin):
+            Yp[i, j] += eps
+            lp = float(np.sum(G * fwd()))
+            Yp[i, j] -= 2 * eps
+            lm = float(np.sum(G * fwd()))
+            Yp[i, j] += eps
+            want = dX[i, j] if i < ns else 0.0
+            assert abs((lp - lm) / (2 * eps) - want) <= 1e-6 * (1 + abs(want)), (i, j)
