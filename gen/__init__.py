@@ -9,5 +9,5 @@ set -- from numpy's PCG64 generator keyed by ``gen_seed``.
 See DESIGN.md "Input recipe" for the shapes and the
 paper passages each shape follows (Table 2).
 """
-from .configs import CONFIGS, GraphConfig, scaled  # noqa: F401
-from .planted import Bundle, generate, make_features  # noqa: F401
+from .configs import CONFIGS, NUM_CLASSES, GraphConfig, num_classes, scaled  # noqa: F401
+from .planted import Bundle, generate, make_features, make_labels  # noqa: F401

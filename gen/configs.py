@@ -67,3 +67,12 @@ def scaled(cfg: GraphConfig, factor: float, name: str = None) -> GraphConfig:
     return replace(cfg, name=name or f"{cfg.name}@{factor:g}", num_nodes=n,
                    nnz_target=int(n * min(deg, 0.5 * (n - 1))), num_communities=c,
                    comm_size_range=(lo, hi), n_train=ntr)
+
+
+# class counts of the paper's datasets (Table 2: ogbn-arxiv 40, reddit 41,
+# ogbn-products 47, ogbn-papers100M 172); tiny is a test size
+NUM_CLASSES = {"tiny": 8, "arxiv": 40, "reddit": 41, "products": 47, "papers100m": 172}
+
+
+def num_classes(cfg: GraphConfig) -> int:
+    return NUM_CLASSES.get(cfg.name.split("@")[0].split("_")[0], 8)

@@ -292,3 +292,15 @@ def feature_rows(bundle: Bundle, rows) -> np.ndarray:
     if bundle.X is not None:
         return bundle.X[np.asarray(rows, dtype=np.int64), : cfg.feat_dim]
     return make_features(cfg, np.asarray(rows, dtype=np.int64))[:, : cfg.feat_dim]
+
+
+def make_labels(bundle: "Bundle", num_classes: int) -> np.ndarray:
+    """Synthetic node labels for the training step (NEXT-4): int32 [N] in [0, num_classes),
+    homophilous like the paper's datasets -- the community id mod C, replaced by a uniform class
+    for 20 % of the nodes (PCG64 stream 7 of the config's seed)."""
+    rng = _rng(bundle.cfg.gen_seed, 7)
+    n = bundle.comm.shape[0]
+    lab = (bundle.comm.astype(np.int64) % num_classes).astype(np.int32)
+    flip = rng.random(n) < 0.2
+    lab[flip] = rng.integers(0, num_classes, int(flip.sum()), dtype=np.int32)
+    return lab

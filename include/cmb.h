@@ -443,16 +443,18 @@ CMB_API cmb_status cmb_sage_mean_backward(const int32_t* indptr, const int32_t* 
  *     dW_self = X_dst^T dZ,  dW_neigh = H^T dZ,  db = sum_d dZ[d, :],
  * with [X_dst | H] recomputed from the feature table exactly as the forward builds it (bf16
  * operands, fp32 accumulation on the tensor cores per CTA, fp64 sum of the per-CTA partials:
- * deterministic).  dy, y: device bf16 [n_{L-1} x out_dim], row stride dy_ld / y_ld elements
- * (multiples of 8, 16-B aligned).  dw: device fp32 [2 x F x out_dim] (dW_self then dW_neigh,
+ * deterministic).  dy: device [n_{L-1} x out_dim], bf16 (dy_f32 = 0) or fp32 (dy_f32 = 1:
+ * e.g. cmb_sage_hidden_input_grad's dX, rounded to bf16 as it is staged); y: device bf16; row
+ * strides dy_ld / y_ld elements (16-B aligned rows).  dw: device fp32 [2 x F x out_dim] (dW_self then dW_neigh,
  * row-major like the forward's W); db: device fp32 [out_dim].  out_dim: a power of two in
  * [16, 256]; F <= 128.  workspace: device, >= cmb_sage_backward_workspace_bytes (partials).
  * Accuracy: |dW - exact| <= 2^-7 * |A|^T |dZ|, |db - exact| <= 2^-12 * sum |dZ| (R27). */
 CMB_API size_t cmb_sage_backward_workspace_bytes(int32_t feat_dim, int32_t out_dim);
 CMB_API cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* blocks,
                                            int32_t n_hops, int64_t n_last_dst_cap,
-                                           const void* dy, int64_t dy_ld, const void* y,
-                                           int64_t y_ld, int32_t out_dim, float* dw, float* db,
+                                           const void* dy, int64_t dy_ld, int32_t dy_f32,
+                                           const void* y, int64_t y_ld, int32_t out_dim,
+                                           float* dw, float* db,
                                            void* workspace, size_t workspace_bytes, void* stream);
 
 /* NEXT-4 hidden-layer backward (reading R31 = R27 applied to the R29 layer): weight
@@ -463,8 +465,8 @@ CMB_API cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks*
  * H = the neighbour means exactly as cmb_sage_hidden_forward builds them (fp32 sum in CSR order
  * times RN(1/deg), rounded to bf16).  bf16 operands, fp32 accumulation per CTA on the tensor
  * cores, fp64 sum of the per-CTA partials (deterministic).  y_prev: device bf16 [n_src x ld]
- * (ld % 8 == 0, ld >= in_dim, 16-B aligned); dy, y: device bf16 [n_dst x ld] (same rules with
- * out_dim); dw: device fp32 [2 x in_dim x out_dim] (dW_self then dW_neigh, row-major like W);
+ * (ld % 8 == 0, ld >= in_dim, 16-B aligned); dy: device [n_dst x ld], bf16 or (dy_f32 = 1) fp32
+ * rounded to bf16 as it is staged; y: device bf16 [n_dst x ld] (16-B aligned rows, ld >= out_dim); dw: device fp32 [2 x in_dim x out_dim] (dW_self then dW_neigh, row-major like W);
  * db: device fp32 [out_dim].  in_dim in {64, 128, 192, 256}; out_dim a power of two in
  * [16, 256].  workspace: device, >= cmb_sage_hidden_backward_workspace_bytes (partials; the
  * library never allocates).  n_dst = min(sizes[hop], n_dst_cap).  dz_out (optional, NULL to
@@ -476,7 +478,8 @@ CMB_API size_t cmb_sage_hidden_backward_workspace_bytes(int32_t in_dim, int32_t 
 CMB_API cmb_status cmb_sage_hidden_backward(const cmb_blocks* blocks, int32_t hop,
                                             int64_t n_dst_cap, const void* y_prev,
                                             int64_t y_prev_ld, int32_t in_dim, const void* dy,
-                                            int64_t dy_ld, const void* y, int64_t y_ld,
+                                            int64_t dy_ld, int32_t dy_f32, const void* y,
+                                            int64_t y_ld,
                                             int32_t out_dim, float* dw, float* db,
                                             void* workspace, size_t workspace_bytes,
                                             void* dz_out, int64_t dz_ld, void* stream);
@@ -505,6 +508,34 @@ CMB_API cmb_status cmb_sage_hidden_input_grad(const cmb_blocks* blocks, int32_t 
                                               const void* wt_img, int32_t in_dim, float* dx,
                                               int64_t dx_ld, float* dh, int64_t dh_ld,
                                               void* stream);
+
+/* NEXT-4 loss (reading R33; "minimizing the loss between the labels
+ * ... and the node embeddings of the last layer"): softmax cross-entropy of the last layer's
+ * logits, mean over the batch's n = min(*n_dev, n_cap) roots (the prefix of `nodes`):
+ *     *loss = (1/n) sum_i [ logsumexp(Y[i, 0:C]) - Y[i, label_i] ],  label_i = node_labels[nodes[i]],
+ *     dY[i, c] = (softmax(Y[i])_c - 1[c == label_i]) / n  (bf16; columns C .. dy_cols-1 = 0).
+ * logits: device fp32 [n x ld]; node_labels: device int32 [N]; nodes: the batch's node list
+ * (device); n_dev: device int64 (cmb_blocks sizes[0]); dy: device bf16 [n x dy_ld]; loss:
+ * device fp64 scalar (summed in a fixed order: deterministic); status: device int32 word or
+ * NULL, set to CMB_ERR_INVALID_ARGUMENT if a label is outside [0, C) (that row is skipped).
+ * 1 <= C <= 256.  Accuracy (fp32 softmax): |dY - exact| <= 2^-8 |dY| + 2^-20 / n,
+ * |loss - exact| <= 2^-20 * mean_i (|max_c Y[i, c]| + 1). */
+CMB_API cmb_status cmb_softmax_xent(const float* logits, int64_t ld, const int32_t* node_labels,
+                                    const int32_t* nodes, const int64_t* n_dev, int64_t n_cap,
+                                    int32_t num_classes, void* dy, int64_t dy_ld, int32_t dy_cols,
+                                    double* loss, int32_t* status, void* stream);
+
+/* NEXT-4 optimizer step (reading R34; DGL's GraphSAGE defaults, lr 1e-3,
+ * weight decay 5e-4 -- Adam in that example): on n fp32 parameters (flat, device, 16-B aligned,
+ * n % 4 == 0), with the step's gradient g and the moment buffers m, v (zero before step 1):
+ *     g' = g + wd w;  m = b1 m + (1 - b1) g';  v = b2 v + (1 - b2) g'^2;
+ *     w -= lr (m / (1 - b1^step)) / (sqrt(v / (1 - b2^step)) + eps).
+ * Hyper-parameters in fp64: 1 - beta and the bias corrections are formed in fp64 and rounded
+ * once (1 - 0.999f would be off by 1.3e-5).  Updates w, m, v in place.  fp32 arithmetic: |w - exact| <= 2^-22 |w| + 2^-18 lr (|u| + 1),
+ * u the exact update direction. */
+CMB_API cmb_status cmb_adam_step(float* w, const float* g, float* m, float* v, int64_t n,
+                                 double lr, double beta1, double beta2, double eps,
+                                 double weight_decay, int32_t step, void* stream);
 
 /* ------------------------------------------------------------------ status */
 /* Synchronises `stream`, returns (and clears) the sticky device status word of a

@@ -328,3 +328,40 @@ def sage_hidden_input_grad(indptr_h, idx, dZ, W_self, W_neigh, n_src) -> np.ndar
     dX = sage_mean_backward(indptr_h, idx, G @ Wn.T, n_src)
     dX[:G.shape[0]] += G @ Ws.T
     return dX
+
+
+def softmax_xent(Y, labels):
+    """The training loss (NEXT-4, reading R33), fp64: PAPER.md P:503 trains the layer parameters
+    "by minimizing the loss between the labels of all labeled nodes and the node embeddings of
+    the last layer"; the loss of DGL's GraphSAGE node classification is the softmax cross-entropy,
+    averaged over the batch's n roots:
+        loss = (1/n) sum_i [ log sum_c exp(Y[i, c]) - Y[i, label_i] ],
+        dY[i, c] = (exp(Y[i, c]) / sum_c' exp(Y[i, c']) - 1[c == label_i]) / n.
+    Y: [n, C] logits; labels: [n] ints in [0, C).  Returns (loss, dY)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    lab = np.asarray(labels, dtype=np.int64)
+    n = Y.shape[0]
+    if n == 0:
+        return 0.0, np.zeros_like(Y)
+    m = Y.max(axis=1, keepdims=True)
+    e = np.exp(Y - m)
+    s = e.sum(axis=1, keepdims=True)
+    lse = (m + np.log(s))[:, 0]
+    loss = float(np.mean(lse - Y[np.arange(n), lab]))
+    dY = e / s
+    dY[np.arange(n), lab] -= 1.0
+    return loss, dY / n
+
+
+def adam_step(w, g, m, v, step, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=5e-4):
+    """One optimizer step (NEXT-4, reading R34), fp64: Adam with L2 weight decay added to the
+    gradient (torch.optim.Adam semantics; DGL's GraphSAGE defaults lr = 1e-3, weight decay 5e-4,
+    PAPER.md P:774):  g' = g + wd w;  m = b1 m + (1 - b1) g';  v = b2 v + (1 - b2) g'^2;
+    w = w - lr (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps).  Returns new (w, m, v)."""
+    w = np.asarray(w, dtype=np.float64)
+    gp = np.asarray(g, dtype=np.float64) + weight_decay * w
+    m = beta1 * np.asarray(m, dtype=np.float64) + (1.0 - beta1) * gp
+    v = beta2 * np.asarray(v, dtype=np.float64) + (1.0 - beta2) * gp * gp
+    mh = m / (1.0 - beta1 ** step)
+    vh = v / (1.0 - beta2 ** step)
+    return w - lr * mh / (np.sqrt(vh) + eps), m, v

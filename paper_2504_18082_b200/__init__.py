@@ -56,7 +56,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sage_hidden_forward", "cmb_sage_mean_backward",
            "cmb_sage_hidden_backward_workspace_bytes", "cmb_sage_hidden_backward",
            "cmb_sage_hidden_weights_t_bytes", "cmb_sage_hidden_pack_weights_t",
-           "cmb_sage_hidden_input_grad",
+           "cmb_sage_hidden_input_grad", "cmb_softmax_xent", "cmb_adam_step",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -187,12 +187,15 @@ def lib():
             "cmb_gcn_pack_weights": (I32, [P, I32, I32, P, SZ, P]),
             "cmb_gcn_layer_forward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, P, I32, I32,
                                             I32, P, I64, P]),
-            "cmb_sage_layer_backward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, I64, P, I64,
-                                              I32, P, P, P, SZ, P]),
+            "cmb_sage_layer_backward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, I64, I32, P,
+                                              I64, I32, P, P, P, SZ, P]),
             "cmb_sage_hidden_backward_workspace_bytes": (SZ, [I32, I32]),
             "cmb_sage_hidden_backward": (I32, [ctypes.POINTER(Blocks), I32, I64, P, I64, I32, P,
-                                               I64, P, I64, I32, P, P, P, SZ, P, I64, P]),
+                                               I64, I32, P, I64, I32, P, P, P, SZ, P, I64, P]),
             "cmb_sage_hidden_weights_t_bytes": (SZ, [I32, I32]),
+            "cmb_softmax_xent": (I32, [P, I64, P, P, P, I64, I32, P, I64, I32, P, P, P]),
+            "cmb_adam_step": (I32, [P, P, P, P, I64, ctypes.c_double, ctypes.c_double,
+                                    ctypes.c_double, ctypes.c_double, ctypes.c_double, I32, P]),
             "cmb_sage_hidden_pack_weights_t": (I32, [P, P, I32, I32, P, SZ, P]),
             "cmb_sage_hidden_input_grad": (I32, [ctypes.POINTER(Blocks), I32, I64, I64, P, I64, I32,
                                                  P, I32, P, I64, P, I64, P]),
@@ -227,6 +230,36 @@ def _dev_tensor(t, dtype, device):
     if not isinstance(t, torch.Tensor):
         t = torch.as_tensor(t)
     return t.to(device=device, dtype=dtype).contiguous()
+
+
+def _grad_out(dw, db, F, fo, device):
+    """Gradient outputs of a layer backward: caller-given views ([2, F, fo] and [fo] fp32,
+    contiguous) or fresh tensors."""
+    if dw is None:
+        dw = torch.empty(2, F, fo, dtype=torch.float32, device=device)
+    if db is None:
+        db = torch.empty(fo, dtype=torch.float32, device=device)
+    if tuple(dw.shape) != (2, F, fo) or not dw.is_contiguous() or dw.dtype != torch.float32 or \
+            tuple(db.shape) != (fo,) or db.dtype != torch.float32:
+        raise ValueError("dw must be contiguous fp32 [2, F, out_dim], db fp32 [out_dim]")
+    return dw, db
+
+
+def softmax_xent(logits: torch.Tensor, node_labels: torch.Tensor, nodes: torch.Tensor,
+                 n_dev: torch.Tensor, num_classes: int, dy: torch.Tensor, loss: torch.Tensor,
+                 status: Optional[torch.Tensor] = None):
+    """NEXT-4 loss (R33): softmax cross-entropy over the batch's roots (the prefix of `nodes`,
+    n = n_dev[0]) -> loss (device fp64 [1]) and dY (bf16, columns >= num_classes zero)."""
+    _check(lib().cmb_softmax_xent(_ptr(logits), logits.stride(0), _ptr(node_labels), _ptr(nodes),
+                                  _ptr(n_dev), dy.shape[0], int(num_classes), _ptr(dy),
+                                  dy.stride(0), dy.shape[1], _ptr(loss), _ptr(status), _stream()))
+
+
+def adam_step(w: torch.Tensor, g: torch.Tensor, m: torch.Tensor, v: torch.Tensor, step: int,
+              lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=5e-4):
+    """NEXT-4 optimizer step (R34) on flat fp32 buffers, in place."""
+    _check(lib().cmb_adam_step(_ptr(w), _ptr(g), _ptr(m), _ptr(v), w.numel(), lr, beta1, beta2,
+                               eps, weight_decay, int(step), _stream()))
 
 
 def _workspace(nbytes: int, device) -> torch.Tensor:
@@ -489,39 +522,43 @@ class Sampler:
         return out
 
     def sage_layer_backward(self, layer: "SageLayer", dy: torch.Tensor,
-                            y: Optional[torch.Tensor] = None):
+                            y: Optional[torch.Tensor] = None, dw: Optional[torch.Tensor] = None,
+                            db: Optional[torch.Tensor] = None):
         """NEXT-4 backward for the last sampled batch: dY (bf16 [>= n_{L-1}, out_dim]) and, for a
         ReLU layer, its output Y (bf16) -> (dW_self [F, out_dim], dW_neigh, db) fp32."""
-        if dy.dtype != torch.bfloat16 or (y is not None and y.dtype != torch.bfloat16):
-            raise ValueError("dy and y must be bf16")
+        if dy.dtype not in (torch.bfloat16, torch.float32) or (
+                y is not None and y.dtype != torch.bfloat16):
+            raise ValueError("dy must be bf16 or fp32, y bf16")
         F, fo = layer.feat_dim, layer.out_dim
         ws = layer.backward_workspace()
-        dw = torch.empty(2, F, fo, dtype=torch.float32, device=layer.device)
-        db = torch.empty(fo, dtype=torch.float32, device=layer.device)
+        dw, db = _grad_out(dw, db, F, fo, layer.device)
         _check(lib().cmb_sage_layer_backward(
             self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
-            _ptr(dy), dy.stride(0), _ptr(y), 0 if y is None else y.stride(0), fo, _ptr(dw),
-            _ptr(db), _ptr(ws), ws.numel(), _stream()))
+            _ptr(dy), dy.stride(0), int(dy.dtype == torch.float32), _ptr(y),
+            0 if y is None else y.stride(0), fo, _ptr(dw), _ptr(db), _ptr(ws), ws.numel(),
+            _stream()))
         return dw[0], dw[1], db
 
     def sage_hidden_backward(self, layer: "SageLayer", hop: int, y_prev: torch.Tensor,
                              dy: torch.Tensor, y: Optional[torch.Tensor] = None,
-                             dz_out: Optional[torch.Tensor] = None):
+                             dz_out: Optional[torch.Tensor] = None,
+                             dw: Optional[torch.Tensor] = None, db: Optional[torch.Tensor] = None):
         """NEXT-4 hidden-layer backward (R31) on hop `hop` of the last sampled batch: y_prev =
         the layer's bf16 input (the previous layer's output), dY (bf16 [>= n_hop, out_dim]) and,
         for a ReLU layer, its output Y (bf16) -> (dW_self [F, out], dW_neigh, db) fp32.
         dz_out (bf16 [>= n_hop, >= out_dim]) receives the masked dZ for sage_hidden_input_grad."""
         if not layer.hidden:
             raise ValueError("layer was packed as a first layer; use SageLayer(..., hidden=True)")
-        if any(t is not None and t.dtype != torch.bfloat16 for t in (y_prev, dy, y)):
-            raise ValueError("y_prev, dy and y must be bf16")
+        if any(t is not None and t.dtype != torch.bfloat16 for t in (y_prev, y)) or \
+                dy.dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError("y_prev and y must be bf16, dy bf16 or fp32")
         F, fo = layer.feat_dim, layer.out_dim
         ws = layer.backward_workspace()
-        dw = torch.empty(2, F, fo, dtype=torch.float32, device=layer.device)
-        db = torch.empty(fo, dtype=torch.float32, device=layer.device)
+        dw, db = _grad_out(dw, db, F, fo, layer.device)
         _check(lib().cmb_sage_hidden_backward(
             ctypes.byref(self._blocks), int(hop), self.n_cap[hop], _ptr(y_prev), y_prev.stride(0),
-            F, _ptr(dy), dy.stride(0), _ptr(y), 0 if y is None else y.stride(0), fo, _ptr(dw),
+            F, _ptr(dy), dy.stride(0), int(dy.dtype == torch.float32), _ptr(y),
+            0 if y is None else y.stride(0), fo, _ptr(dw),
             _ptr(db), _ptr(ws), ws.numel(), _ptr(dz_out),
             0 if dz_out is None else dz_out.stride(0), _stream()))
         return dw[0], dw[1], db
@@ -612,6 +649,112 @@ class SageLayer:
     def alloc_out(self, rows: int) -> torch.Tensor:
         dt = torch.bfloat16 if self.out_bf16 else torch.float32
         return torch.empty(max(1, rows), self.out_dim, dtype=dt, device=self.device)
+
+
+class GraphSAGE:
+    """NEXT-4: the paper's L-layer GraphSAGE (3 layers, hidden 256, DGL defaults
+    lr 1e-3, weight decay 5e-4) trained on the sampled blocks of a Sampler, every stage in this
+    library's kernels: layer 1 fused with a4 + a5 (R26), hidden layers (R29), softmax
+    cross-entropy (R33), weight gradients (R27, R31), input gradients of the hidden layers (R32),
+    Adam (R34), weight images repacked.  All parameters live in ONE flat fp32 buffer (per layer
+    [W_self | W_neigh | b]) with matching gradient and moment buffers, so the optimizer is one
+    launch.  The last layer's width is num_classes rounded up to a power of two >= 16 (the padded
+    columns start at zero and stay zero: no gradient reaches them)."""
+
+    def __init__(self, feat_dim: int, num_classes: int, hidden: int = 256, num_layers: int = 3,
+                 seed: int = 0, lr=1e-3, weight_decay=5e-4, device=None):
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        out = 16
+        while out < num_classes:
+            out *= 2
+        self.dims = [feat_dim] + [hidden] * (num_layers - 1) + [out]
+        self.num_classes, self.L = int(num_classes), num_layers
+        self.lr, self.weight_decay, self.step_count = lr, weight_decay, 0
+        sizes = [2 * self.dims[l] * self.dims[l + 1] + self.dims[l + 1] for l in range(num_layers)]
+        self.offsets = [sum(sizes[:l]) for l in range(num_layers + 1)]
+        n = self.offsets[-1]
+        gen = torch.Generator().manual_seed(seed)
+        host = torch.zeros(n)
+        for l in range(num_layers):   # Glorot-uniform weights, zero bias (DGL's SAGEConv init)
+            fi, fo = self.dims[l], self.dims[l + 1]
+            a = (6.0 / (fi + fo)) ** 0.5
+            w = (torch.rand(2, fi, fo, generator=gen) * 2 - 1) * a
+            if l == num_layers - 1:
+                w[:, :, num_classes:] = 0.0
+            host[self.offsets[l]:self.offsets[l] + 2 * fi * fo] = w.reshape(-1)
+        self.params = host.to(dev)
+        self.grads = torch.zeros(n, device=dev)
+        self.m = torch.zeros(n, device=dev)
+        self.v = torch.zeros(n, device=dev)
+        self.layers = []
+        for l in range(num_layers):
+            ws, wn, b = self._views(self.params, l)
+            last = l == num_layers - 1
+            self.layers.append(SageLayer(ws, wn, b, relu=not last, out_bf16=not last,
+                                         device=dev, hidden=l > 0))
+        self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._bufs = {}
+        self.device = dev
+
+    def _views(self, flat, l):
+        fi, fo = self.dims[l], self.dims[l + 1]
+        o = self.offsets[l]
+        return (flat[o:o + fi * fo].view(fi, fo), flat[o + fi * fo:o + 2 * fi * fo].view(fi, fo),
+                flat[o + 2 * fi * fo:o + 2 * fi * fo + fo])
+
+    def _buf(self, key, rows, cols, dtype):
+        t = self._bufs.get(key)
+        if t is None or t.shape[0] < rows:
+            t = torch.zeros(max(1, rows), cols, dtype=dtype, device=self.device)
+            self._bufs[key] = t
+        return t
+
+    def forward(self, sampler: "Sampler"):
+        """Activations of every layer for the last sampled batch: [Y1, .., YL] (YL = fp32
+        logits [n_cap[0], out], the others bf16)."""
+        L = self.L
+        if sampler.L != L:
+            raise ValueError(f"sampler has {sampler.L} hops, the model {L} layers")
+        ys = []
+        for l, layer in enumerate(self.layers):
+            h = L - 1 - l
+            out = self._buf(("y", l), sampler.n_cap[h], layer.out_dim,
+                            torch.bfloat16 if layer.out_bf16 else torch.float32)
+            ys.append(sampler.sage_layer(layer, out) if l == 0 else
+                      sampler.sage_hidden(layer, h, ys[-1], out))
+        return ys
+
+    def train_step(self, sampler: "Sampler", node_labels: torch.Tensor) -> torch.Tensor:
+        """One training step on the last sampled batch: forward, loss, backward, Adam, repack.
+        Returns the device fp64 loss tensor (no host synchronisation)."""
+        L = self.L
+        ys = self.forward(sampler)
+        fo = self.dims[-1]
+        dy = self._buf("dyL", sampler.n_cap[0], fo, torch.bfloat16)
+        softmax_xent(ys[-1], node_labels, sampler.nodes, sampler.sizes[0:1], self.num_classes,
+                     dy[:sampler.n_cap[0]], self.loss, self.status)
+        for l in range(L - 1, -1, -1):
+            h = L - 1 - l
+            layer = self.layers[l]
+            g_ws, g_wn, g_b = self._views(self.grads, l)
+            dw = self.grads[self.offsets[l]:self.offsets[l] + 2 * g_ws.numel()].view(2, *g_ws.shape)
+            y = ys[l] if layer.relu else None
+            if l == 0:
+                sampler.sage_layer_backward(layer, dy, y, dw=dw, db=g_b)
+            else:
+                dz = self._buf(("dz", l), sampler.n_cap[h], ((layer.out_dim + 63) // 64) * 64,
+                               torch.bfloat16)
+                sampler.sage_hidden_backward(layer, h, ys[l - 1], dy, y, dz_out=dz, dw=dw, db=g_b)
+                dy = sampler.sage_hidden_input_grad(
+                    layer, h, dz, self._buf(("dx", l), sampler.n_cap[h + 1], layer.feat_dim,
+                                            torch.float32)[:sampler.n_cap[h + 1]])
+        self.step_count += 1
+        adam_step(self.params, self.grads, self.m, self.v, self.step_count, self.lr,
+                  weight_decay=self.weight_decay)
+        for layer in self.layers:
+            layer.repack()
+        return self.loss
 
 
 class GcnLayer:

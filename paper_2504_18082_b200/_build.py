@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libcmb.so")
 SOURCES = ["capi.cu", "graph.cu", "order.cu", "sample.cu", "features.cu", "shard.cu", "peer.cu", "runtime.cu", "cache.cu", "reorder.cu",
-           "sage_layer.cu"]
+           "sage_layer.cu", "train.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v",

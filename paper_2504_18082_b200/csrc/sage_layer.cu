@@ -541,12 +541,25 @@ __device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t addr, uint32_t lbo) {
          (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
 }
 
+// 8 columns (8c .. 8c+7) of row `row` of dY as bf16: a bf16 dY is loaded as is; an fp32 one (the
+// input gradient of the next layer, R32, accumulated in fp32) is rounded to bf16 here, so the
+// chain needs no cast pass
+__device__ __forceinline__ uint4 load_dy8(const void* dy, int dy_f32, int64_t row, int64_t ld,
+                                          int c) {
+  if (!dy_f32)
+    return __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(dy) + row * ld) + c);
+  const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(dy) + row * ld) + 2 * c;
+  const float4 a = __ldg(p), b = __ldg(p + 1);
+  const uint2 lo = pack_bf16x4(a), hi = pack_bf16x4(b);
+  return make_uint4(lo.x, lo.y, hi.x, hi.y);
+}
+
 template <int DMAX, int RIF>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sage_layer_bwd(const int32_t* __restrict__ indptr, const int32_t* __restrict__ gid,
                      const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
                      const float4* __restrict__ x, int64_t ld4, const int32_t* __restrict__ map,
-                     int F, int kh, const __nv_bfloat16* __restrict__ dy, int64_t dy_ld,
+                     int F, int kh, const void* __restrict__ dy, int64_t dy_ld, int dy_f32,
                      const __nv_bfloat16* __restrict__ y, int64_t y_ld, int fo, int tmem_alloc,
                      float* __restrict__ part, float* __restrict__ part_db) {
   extern __shared__ uint8_t smem_raw[];
@@ -615,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t row = tile * kM + r;
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
       if (row < n_dst) {
-        v = __ldg(reinterpret_cast<const uint4*>(dy + row * dy_ld) + c);
+        v = load_dy8(dy, dy_f32, row, dy_ld, c);
         if (y) {
           const uint4 m = __ldg(reinterpret_cast<const uint4*>(y + row * y_ld) + c);
           const uint32_t* mw = reinterpret_cast<const uint32_t*>(&m);
@@ -1005,7 +1018,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_sage_hidden_bwd(const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
                       const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
                       const uint4* __restrict__ yp, int64_t yp_ld8, int kin,
-                      const __nv_bfloat16* __restrict__ dy, int64_t dy_ld,
+                      const void* __restrict__ dy, int64_t dy_ld, int dy_f32,
                       const __nv_bfloat16* __restrict__ y, int64_t y_ld, int fo, int tmem_alloc,
                       int rows_per_tile, float* __restrict__ part, float* __restrict__ part_db,
                       __nv_bfloat16* __restrict__ dz_out, int64_t dz_ld) {
@@ -1070,7 +1083,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t row = tile * R + r;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         if (row < n_dst) {
-          v = __ldg(reinterpret_cast<const uint4*>(dy + row * dy_ld) + c);
+          v = load_dy8(dy, dy_f32, row, dy_ld, c);
           if (y) {
             const uint4 m = __ldg(reinterpret_cast<const uint4*>(y + row * y_ld) + c);
             const uint32_t* mw = reinterpret_cast<const uint32_t*>(&m);
@@ -1338,7 +1351,7 @@ size_t cmb_sage_backward_workspace_bytes(int32_t feat_dim, int32_t out_dim) {
 
 cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
                                    int64_t n_last_dst_cap, const void* dy, int64_t dy_ld,
-                                   const void* y, int64_t y_ld, int32_t out_dim, float* dw,
+                                   int32_t dy_f32, const void* y, int64_t y_ld, int32_t out_dim, float* dw,
                                    float* db, void* workspace, size_t workspace_bytes,
                                    void* stream) {
   CMB_ARG(g && b && dy && dw && db && workspace, "cmb_sage_layer_backward: null argument");
@@ -1353,9 +1366,10 @@ cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* b, int3
   CMB_ARG(b->last_src_ids != nullptr, "cmb_sage_layer_backward: blocks->last_src_ids is required");
   CMB_ARG(g->d.ld % 4 == 0 && sl::aligned16(g->d.x),
           "cmb_sage_layer_backward: feature rows must be 16-byte aligned (ld %% 4 == 0)");
-  CMB_ARG(dy_ld >= out_dim && dy_ld % 8 == 0 && sl::aligned16(dy) &&
+  CMB_ARG(dy_ld >= out_dim && dy_ld % (dy_f32 ? 4 : 8) == 0 && sl::aligned16(dy) &&
               (!y || (y_ld >= out_dim && y_ld % 8 == 0 && sl::aligned16(y))),
-          "cmb_sage_layer_backward: dy / y rows must be 16-byte aligned bf16 with ld >= out_dim");
+          "cmb_sage_layer_backward: dy (bf16 or fp32) / y (bf16) rows must be 16-byte aligned "
+          "with ld >= out_dim");
   CMB_ARG(n_last_dst_cap >= 0 && n_last_dst_cap <= b->nodes_cap,
           "cmb_sage_layer_backward: bad n_last_dst_cap");
   const int L = n_hops;
@@ -1389,7 +1403,7 @@ cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* b, int3
 #define CMB_BWD_ARGS                                                                          \
   b->indptr[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,                     \
       reinterpret_cast<const float4*>(g->d.x), g->d.ld / 4, b->nodes, F, kh,                 \
-      static_cast<const __nv_bfloat16*>(dy), dy_ld, static_cast<const __nv_bfloat16*>(y), y_ld, \
+      dy, dy_ld, dy_f32, static_cast<const __nv_bfloat16*>(y), y_ld,                         \
       out_dim, alloc, part, part_db
     if (dmax <= 5)
       sl::k_sage_layer_bwd<5, 2><<<grid, sl::kThreads, smem, s>>>(CMB_BWD_ARGS);
@@ -1484,8 +1498,8 @@ size_t cmb_sage_hidden_backward_workspace_bytes(int32_t in_dim, int32_t out_dim)
 
 cmb_status cmb_sage_hidden_backward(const cmb_blocks* b, int32_t hop, int64_t n_dst_cap,
                                     const void* y_prev, int64_t y_prev_ld, int32_t in_dim,
-                                    const void* dy, int64_t dy_ld, const void* y, int64_t y_ld,
-                                    int32_t out_dim, float* dw, float* db, void* workspace,
+                                    const void* dy, int64_t dy_ld, int32_t dy_f32, const void* y,
+                                    int64_t y_ld, int32_t out_dim, float* dw, float* db, void* workspace,
                                     size_t workspace_bytes, void* dz_out, int64_t dz_ld,
                                     void* stream) {
   CMB_ARG(b && y_prev && dy && dw && db && workspace, "cmb_sage_hidden_backward: null argument");
@@ -1500,9 +1514,10 @@ cmb_status cmb_sage_hidden_backward(const cmb_blocks* b, int32_t hop, int64_t n_
           "cmb_sage_hidden_backward: workspace < %zu bytes or unaligned", need);
   CMB_ARG(y_prev_ld >= in_dim && y_prev_ld % 8 == 0 && sl::aligned16(y_prev),
           "cmb_sage_hidden_backward: y_prev rows must be 16-byte aligned bf16, ld >= in_dim");
-  CMB_ARG(dy_ld >= out_dim && dy_ld % 8 == 0 && sl::aligned16(dy) &&
+  CMB_ARG(dy_ld >= out_dim && dy_ld % (dy_f32 ? 4 : 8) == 0 && sl::aligned16(dy) &&
               (!y || (y_ld >= out_dim && y_ld % 8 == 0 && sl::aligned16(y))),
-          "cmb_sage_hidden_backward: dy / y rows must be 16-byte aligned bf16 with ld >= out_dim");
+          "cmb_sage_hidden_backward: dy (bf16 or fp32) / y (bf16) rows must be 16-byte aligned "
+          "with ld >= out_dim");
   CMB_ARG(n_dst_cap >= 0, "cmb_sage_hidden_backward: bad n_dst_cap");
   cmb_status st = require_sm100();
   if (st != CMB_OK) return st;
@@ -1530,8 +1545,8 @@ cmb_status cmb_sage_hidden_backward(const cmb_blocks* b, int32_t hop, int64_t n_
     }
     sl::k_sage_hidden_bwd<8><<<grid, sl::kThreads, sl::hid_bwd_smem_bytes(kin2, out_dim), s>>>(
         b->indptr[hop], b->indices[hop], b->sizes + hop, n_dst_cap,
-        static_cast<const uint4*>(y_prev), y_prev_ld / 8, kin, static_cast<const __nv_bfloat16*>(dy),
-        dy_ld, static_cast<const __nv_bfloat16*>(y), y_ld, out_dim, alloc, R, part, part_db,
+        static_cast<const uint4*>(y_prev), y_prev_ld / 8, kin, dy, dy_ld, dy_f32,
+        static_cast<const __nv_bfloat16*>(y), y_ld, out_dim, alloc, R, part, part_db,
         static_cast<__nv_bfloat16*>(dz_out), dz_ld);
     CMB_CUDA(cudaGetLastError());
   }

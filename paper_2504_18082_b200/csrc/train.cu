@@ -1,0 +1,170 @@
+// train.cu -- NEXT-4: the loss and the optimizer step that close one training
+// step of the paper's 3-layer GraphSAGE.  PAPER.md P:503: "The goal of training is to learn the
+// layer parameters W^1 .. W^{L-1} by minimizing the loss between the labels of all labeled nodes
+// and the node embeddings of the last layer"; DGL's GraphSAGE defaults, learning rate 1e-3,
+// weight decay 5e-4.  Readings R33 (softmax cross-entropy, mean over the batch's roots) and R34
+// (Adam with L2 weight decay added to the gradient, DGL's optimizer) in DESIGN.md.
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace cmb {
+namespace tr {
+
+constexpr int kXentThreads = 1024;
+constexpr unsigned kFull = 0xffffffffu;
+
+// R33: for root i < n (label_i = node_labels[nodes[i]]; the roots are the prefix of `nodes`),
+//     loss = (1/n) sum_i [ lse_i - Y[i, label_i] ],  lse_i = m_i + log sum_c exp(Y[i, c] - m_i),
+//     dY[i, c] = (exp(Y[i, c] - lse_i) - 1[c == label_i]) / n     (c < C; columns C.. of dY = 0).
+// One block: warp w owns rows w, w + 32, ...; lane j columns j, j + 32, ... (C <= 256).  Row max
+// and sum by shuffles in fp32; the per-row losses are summed in fp64 per warp in row order and
+// the 32 warp sums in warp order by thread 0 (deterministic).  A label outside [0, C) sets the
+// status word (CMB_ERR_INVALID_ARGUMENT) and contributes nothing.
+__global__ void __launch_bounds__(kXentThreads)
+    k_xent(const float* __restrict__ logits, int64_t ld, const int32_t* __restrict__ node_labels,
+           const int32_t* __restrict__ nodes, const int64_t* __restrict__ n_dev, int64_t n_cap,
+           int C, __nv_bfloat16* __restrict__ dy, int64_t dy_ld, int dy_cols,
+           double* __restrict__ loss, int32_t* __restrict__ status) {
+  __shared__ double wsum[kXentThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = min(*n_dev, n_cap);
+  const float inv_n = n > 0 ? 1.0f / static_cast<float>(n) : 0.f;
+  double acc = 0.0;
+  for (int64_t i = warp; i < n; i += kXentThreads / 32) {
+    const int32_t lab = __ldg(node_labels + __ldg(nodes + i));
+    const bool ok = lab >= 0 && lab < C;
+    if (!ok && lane == 0 && status) atomicCAS(status, 0, CMB_ERR_INVALID_ARGUMENT);
+    float y[8];
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = lane + 32 * k;
+      y[k] = c < C ? __ldg(logits + i * ld + c) : -INFINITY;
+      m = fmaxf(m, y[k]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += lane + 32 * k < C ? expf(y[k] - m) : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    const float lse = m + logf(s);
+    float ylab = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (lane + 32 * k == lab) ylab = y[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ylab += __shfl_xor_sync(kFull, ylab, o);
+    if (lane == 0 && ok) acc += static_cast<double>(lse) - static_cast<double>(ylab);
+    for (int c = lane; c < dy_cols; c += 32) {
+      float g = 0.f;
+      if (c < C && ok) {
+        const int k = c >> 5;  // c = lane + 32 k
+        float yc = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          if (kk == k) yc = y[kk];
+        g = (expf(yc - lse) - (c == lab ? 1.f : 0.f)) * inv_n;
+      }
+      dy[i * dy_ld + c] = __float2bfloat16_rn(g);
+    }
+  }
+  if (lane == 0) wsum[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kXentThreads / 32; ++w) t += wsum[w];
+    *loss = n > 0 ? t / static_cast<double>(n) : 0.0;
+  }
+}
+
+// R34: Adam (torch.optim.Adam semantics, the optimizer of DGL's GraphSAGE example) with L2 weight
+// decay added to the gradient, on a flat fp32 parameter buffer:
+//     g = dW + wd * w;  m = b1 m + (1 - b1) g;  v = b2 v + (1 - b2) g^2;
+//     w -= lr * (m * c1) / (sqrt(v * c2) + eps),  c1 = 1 / (1 - b1^t), c2 = 1 / (1 - b2^t).
+// 1 - b1, 1 - b2 and the bias corrections are computed on the host in fp64 and rounded once
+// (1 - 0.999f in fp32 would be off by 1.3e-5 relative).  HBM-bound elementwise (16 bytes read +
+// 12 written per parameter), float4 per thread.
+__global__ void __launch_bounds__(256)
+    k_adam(float4* __restrict__ w, const float4* __restrict__ g, float4* __restrict__ m,
+           float4* __restrict__ v, int64_t n4, float lr, float b1, float b2, float omb1,
+           float omb2, float eps, float wd, float c1, float c2) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 W = w[i], G = __ldg(g + i), M = m[i], V = v[i];
+    float* pw = &W.x;
+    const float* pg = &G.x;
+    float* pm = &M.x;
+    float* pv = &V.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float gk = __fmaf_rn(wd, pw[k], pg[k]);
+      pm[k] = __fmaf_rn(b1, pm[k], omb1 * gk);
+      pv[k] = __fmaf_rn(b2, pv[k], omb2 * gk * gk);
+      const float den = __fsqrt_rn(pv[k] * c2) + eps;
+      pw[k] = pw[k] - lr * __fdiv_rn(pm[k] * c1, den);
+    }
+    w[i] = W;
+    m[i] = M;
+    v[i] = V;
+  }
+}
+
+}  // namespace tr
+}  // namespace cmb
+
+using namespace cmb;
+
+extern "C" {
+
+cmb_status cmb_softmax_xent(const float* logits, int64_t ld, const int32_t* node_labels,
+                            const int32_t* nodes, const int64_t* n_dev, int64_t n_cap,
+                            int32_t num_classes, void* dy, int64_t dy_ld, int32_t dy_cols,
+                            double* loss, int32_t* status, void* stream) {
+  CMB_ARG(logits && node_labels && nodes && n_dev && dy && loss, "cmb_softmax_xent: null argument");
+  CMB_ARG(num_classes >= 1 && num_classes <= 256 && dy_cols >= num_classes && ld >= num_classes &&
+              dy_ld >= dy_cols && n_cap >= 0,
+          "cmb_softmax_xent: need 1 <= num_classes <= 256 <= ..., dy_cols >= num_classes, "
+          "ld / dy_ld >= their widths (got C=%d, dy_cols=%d)", num_classes, dy_cols);
+  cmb_status st = require_sm100();
+  if (st != CMB_OK) return st;
+  tr::k_xent<<<1, tr::kXentThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      logits, ld, node_labels, nodes, n_dev, n_cap, num_classes,
+      static_cast<__nv_bfloat16*>(dy), dy_ld, dy_cols, loss, status);
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+cmb_status cmb_adam_step(float* w, const float* g, float* m, float* v, int64_t n, double lr,
+                         double beta1, double beta2, double eps, double weight_decay, int32_t step,
+                         void* stream) {
+  CMB_ARG(w && g && m && v, "cmb_adam_step: null argument");
+  CMB_ARG(n >= 0 && n % 4 == 0 && step >= 1 && beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 &&
+              beta2 < 1.0,
+          "cmb_adam_step: need n %% 4 == 0, step >= 1, betas in [0, 1)");
+  CMB_ARG(((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g) |
+            reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15u) == 0,
+          "cmb_adam_step: buffers must be 16-byte aligned");
+  if (n == 0) return CMB_OK;
+  cmb_status st = require_sm100();
+  if (st != CMB_OK) return st;
+  const double c1 = 1.0 / (1.0 - std::pow(beta1, step));
+  const double c2 = 1.0 / (1.0 - std::pow(beta2, step));
+  const int64_t n4 = n / 4;
+  const int grid = static_cast<int>(n4 / 256 + 1 < 148 * 8 ? n4 / 256 + 1 : 148 * 8);
+  tr::k_adam<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<float4*>(w), reinterpret_cast<const float4*>(g),
+      reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n4, static_cast<float>(lr),
+      static_cast<float>(beta1), static_cast<float>(beta2), static_cast<float>(1.0 - beta1),
+      static_cast<float>(1.0 - beta2), static_cast<float>(eps), static_cast<float>(weight_decay),
+      static_cast<float>(c1), static_cast<float>(c2));
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+}  // extern "C"

@@ -73,6 +73,12 @@ def test_layer_entry_points_host_checks(cmb):
     assert L.cmb_sage_hidden_weights_bytes(100, 256) == 0   # in_dim multiple of 64
     assert L.cmb_sage_backward_workspace_bytes(100, 48) == 0   # backward: power-of-two Fo
     assert L.cmb_sage_backward_workspace_bytes(100, 256) == 160 * (256 + 1) * 256 * 4
+    assert L.cmb_sage_hidden_backward_workspace_bytes(256, 256) == 160 * (512 + 1) * 256 * 4
+    assert L.cmb_sage_hidden_backward_workspace_bytes(192, 64) == 160 * (512 + 1) * 64 * 4
+    assert L.cmb_sage_hidden_backward_workspace_bytes(256, 48) == 0   # power-of-two Fo
+    assert L.cmb_sage_hidden_weights_t_bytes(256, 64) == 2 * 1 * 256 * 128   # K = 64, N = 256
+    assert L.cmb_sage_hidden_weights_t_bytes(256, 48) == 2 * 1 * 256 * 128   # K padded to 64
+    assert L.cmb_sage_hidden_weights_t_bytes(100, 64) == 0   # N = in_dim multiple of 16
     for call in (lambda: L.cmb_sage_pack_weights(None, None, 100, 256, None, 0, None),
                  lambda: L.cmb_sage_layer_forward(None, None, 3, 0, None, None, 256, 1, 0, None,
                                                   0, None),
@@ -80,7 +86,12 @@ def test_layer_entry_points_host_checks(cmb):
                                                  0, None),
                  lambda: L.cmb_sage_hidden_forward(None, 1, 0, None, 0, 256, None, None, 256, 1,
                                                    1, None, 0, None),
-                 lambda: L.cmb_sage_layer_backward(None, None, 3, 0, None, 0, None, 0, 256, None,
-                                                   None, None, 0, None)):
+                 lambda: L.cmb_sage_layer_backward(None, None, 3, 0, None, 0, 0, None, 0, 256,
+                                                   None, None, None, 0, None),
+                 lambda: L.cmb_sage_hidden_backward(None, 1, 0, None, 0, 256, None, 0, 0, None,
+                                                    0, 256, None, None, None, 0, None, 0, None),
+                 lambda: L.cmb_sage_hidden_pack_weights_t(None, None, 256, 64, None, 0, None),
+                 lambda: L.cmb_sage_hidden_input_grad(None, 0, 0, 0, None, 0, 64, None, 256,
+                                                      None, 0, None, 0, None)):
         assert call() == 1
         assert b"null" in L.cmb_last_error_message()
