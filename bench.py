@@ -379,6 +379,7 @@ def run_cmb(args, bundle):
         extra = knob_points(bundle, graph, cfg, args, K, flush)
     if (not args.no_extra or args.layer) and world == 1:
         layer = layer_point(bundle, graph, cfg, args)
+        layer["train_step"] = train_point(bundle, graph, cfg, args)
 
     if rank == 0:
         peak, peak_src = measured_peak_hbm()
@@ -687,6 +688,62 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
                          "roofline": {"bound": "hbm", "achieved": gbps_b, "peak": peak,
                                       "unit": "GB/s", "frac": gbps_b / peak},
                          "tensor_tflops": float(np.mean(flops) / (np.mean(t_bwd) * 1e-3) / 1e12)}}
+
+
+def train_point(bundle, graph, cfg, args, n_batches=48):
+    """NEXT-4 (R26-R34): one training step of the paper's 3-layer GraphSAGE (hidden
+    256, Adam lr 1e-3, weight decay 5e-4) per mini-batch -- sample (a2 + a3), forward (layer 1
+    fused with a4 + a5, hidden layers), softmax cross-entropy, every gradient, Adam, repack --
+    timed with CUDA events per batch at the paper's per-epoch comparison points (p = 0.5:
+    RAND, COMM-RAND-MIX-50 %, MIX-0 %, NORAND; P:822-825 report 1.09x / 1.32x / 1.69x per-epoch
+    TRAINING speedups on A100, averaged over 4 datasets -- context, not a target)."""
+    import torch
+    import paper_2504_18082_b200 as cmb
+    from gen import make_labels, num_classes
+    if cfg.feat_dim > 128:
+        return {"skipped": f"feat_dim {cfg.feat_dim} > 128 (layer 1 keeps K = 2F <= 256 resident)"}
+    C = num_classes(cfg)
+    labels = torch.from_numpy(make_labels(bundle, C)).to(graph.device)
+    s = torch.cuda.current_stream()
+    points = []
+    paper = {("rand", 0.0): None, ("comm", 0.5): 1.09, ("comm", 0.0): 1.32, ("norand", 0.0): 1.69}
+    for (mode, mix), ctx in paper.items():
+        pipe = cmb.MiniBatchPipeline(graph, torch.from_numpy(bundle.train), cfg.batch_size,
+                                     cfg.fanouts, mode=mode, mix=mix, p=0.5, seed=args.seed)
+        pipe.start_epoch(0)
+        smp = pipe.sampler
+        model = cmb.GraphSAGE(cfg.feat_dim, C, num_layers=len(cfg.fanouts), seed=1,
+                              device=graph.device)
+        n = min(n_batches, pipe.n_batches)
+        for w in range(3):
+            smp.sample(pipe.batch_roots(w), 0.5, args.seed, w)
+            model.train_step(smp, labels)
+        torch.cuda.synchronize()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n)]
+        losses = torch.zeros(n, dtype=torch.float64, device=graph.device)
+        for k in range(n):
+            ev[k][0].record(s)
+            smp.sample(pipe.batch_roots(k), 0.5, args.seed, k)
+            ev[k][1].record(s)
+            losses[k:k + 1].copy_(model.train_step(smp, labels))
+            ev[k][2].record(s)
+        torch.cuda.synchronize()
+        assert smp.status() == 0 and int(model.status.item()) == 0
+        t_s = np.array([e[0].elapsed_time(e[1]) for e in ev])
+        t_t = np.array([e[1].elapsed_time(e[2]) for e in ev])
+        per = float(np.mean(t_s + t_t))
+        points.append({"knob1": mode + (f"(k={mix})" if mode == "comm" else ""), "p_intra": 0.5,
+                       "train_batches_per_s": 1e3 / per, "sample_ms": float(np.mean(t_s)),
+                       "train_step_ms": float(np.mean(t_t)),
+                       "ms_per_epoch": per * pipe.n_batches, "batches_per_epoch": pipe.n_batches,
+                       "loss_first_last": [float(losses[0]), float(losses[-1])],
+                       "paper_per_epoch_training_speedup_context": ctx})
+    base = points[0]["ms_per_epoch"]
+    for pt in points:
+        pt["per_epoch_speedup_vs_rand"] = base / pt["ms_per_epoch"]
+    return {"model": f"GraphSAGE {len(cfg.fanouts)} layers, hidden 256, {C} classes, Adam",
+            "timed": f"{n_batches} consecutive batches of epoch 0 per point (events around sample "
+                     f"and around train_step, host enqueue included)", "points": points}
 
 
 def main():

@@ -208,3 +208,22 @@ def test_train_step_matches_the_oracle_chain(name, factor):
     # padded logit columns: no gradient reaches them, their parameters stay zero
     assert np.all(views(got_g, L - 1)[0][:, C:] == 0.0)
     assert np.all(views(got_p, L - 1)[0][:, C:] == 0.0)
+
+
+def test_training_fits_one_batch():
+    """Sanity of the whole step as an optimizer: repeated steps on ONE batch (tiny graph) must
+    drive its loss down (the classic overfit-a-batch check; a sign error anywhere in the chain
+    makes the loss rise)."""
+    cfg = CONFIGS["tiny"]
+    b = generate(cfg)
+    C = num_classes(cfg)
+    g = cmb.Graph.from_bundle(b)
+    model = cmb.GraphSAGE(cfg.feat_dim, C, num_layers=len(cfg.fanouts), seed=5, lr=1e-2,
+                          weight_decay=0.0)
+    order = oracle.order_roots(b.train, b.comm, cfg.num_communities, oracle.MODE_RAND, 0.0, SEED, 0)
+    roots = oracle.batch_roots(order, cfg.batch_size, 0)
+    sampler = cmb.Sampler(g, len(roots), cfg.fanouts)
+    sampler.sample(torch.from_numpy(roots).cuda(), cfg.p_intra, SEED, 0)
+    labels = torch.from_numpy(make_labels(b, C)).cuda()
+    losses = [float(model.train_step(sampler, labels).item()) for _ in range(40)]
+    assert losses[0] > 1.0 and losses[-1] < 0.25 * losses[0], losses
