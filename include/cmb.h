@@ -516,14 +516,16 @@ CMB_API cmb_status cmb_sage_hidden_input_grad(const cmb_blocks* blocks, int32_t 
  *     dY[i, c] = (softmax(Y[i])_c - 1[c == label_i]) / n  (bf16; columns C .. dy_cols-1 = 0).
  * logits: device fp32 [n x ld]; node_labels: device int32 [N]; nodes: the batch's node list
  * (device); n_dev: device int64 (cmb_blocks sizes[0]); dy: device bf16 [n x dy_ld]; loss:
- * device fp64 scalar (summed in a fixed order: deterministic); status: device int32 word or
+ * device fp64 scalar (per-root terms in row_loss, device fp64 scratch [n_cap], summed in a fixed
+ * order by a second launch: deterministic); dy_cols <= 256; status: device int32 word or
  * NULL, set to CMB_ERR_INVALID_ARGUMENT if a label is outside [0, C) (that row is skipped).
  * 1 <= C <= 256.  Accuracy (fp32 softmax): |dY - exact| <= 2^-8 |dY| + 2^-20 / n,
  * |loss - exact| <= 2^-20 * mean_i (|max_c Y[i, c]| + 1). */
 CMB_API cmb_status cmb_softmax_xent(const float* logits, int64_t ld, const int32_t* node_labels,
                                     const int32_t* nodes, const int64_t* n_dev, int64_t n_cap,
                                     int32_t num_classes, void* dy, int64_t dy_ld, int32_t dy_cols,
-                                    double* loss, int32_t* status, void* stream);
+                                    double* loss, double* row_loss, int32_t* status,
+                                    void* stream);
 
 /* NEXT-4 optimizer step (reading R34; DGL's GraphSAGE defaults, lr 1e-3,
  * weight decay 5e-4 -- Adam in that example): on n fp32 parameters (flat, device, 16-B aligned,

@@ -193,7 +193,7 @@ def lib():
             "cmb_sage_hidden_backward": (I32, [ctypes.POINTER(Blocks), I32, I64, P, I64, I32, P,
                                                I64, I32, P, I64, I32, P, P, P, SZ, P, I64, P]),
             "cmb_sage_hidden_weights_t_bytes": (SZ, [I32, I32]),
-            "cmb_softmax_xent": (I32, [P, I64, P, P, P, I64, I32, P, I64, I32, P, P, P]),
+            "cmb_softmax_xent": (I32, [P, I64, P, P, P, I64, I32, P, I64, I32, P, P, P, P]),
             "cmb_adam_step": (I32, [P, P, P, P, I64, ctypes.c_double, ctypes.c_double,
                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, I32, P]),
             "cmb_sage_hidden_pack_weights_t": (I32, [P, P, I32, I32, P, SZ, P]),
@@ -247,12 +247,15 @@ def _grad_out(dw, db, F, fo, device):
 
 def softmax_xent(logits: torch.Tensor, node_labels: torch.Tensor, nodes: torch.Tensor,
                  n_dev: torch.Tensor, num_classes: int, dy: torch.Tensor, loss: torch.Tensor,
-                 status: Optional[torch.Tensor] = None):
+                 status: Optional[torch.Tensor] = None, row_loss: Optional[torch.Tensor] = None):
     """NEXT-4 loss (R33): softmax cross-entropy over the batch's roots (the prefix of `nodes`,
     n = n_dev[0]) -> loss (device fp64 [1]) and dY (bf16, columns >= num_classes zero)."""
+    if row_loss is None or row_loss.numel() < dy.shape[0]:
+        row_loss = torch.empty(max(1, dy.shape[0]), dtype=torch.float64, device=dy.device)
     _check(lib().cmb_softmax_xent(_ptr(logits), logits.stride(0), _ptr(node_labels), _ptr(nodes),
                                   _ptr(n_dev), dy.shape[0], int(num_classes), _ptr(dy),
-                                  dy.stride(0), dy.shape[1], _ptr(loss), _ptr(status), _stream()))
+                                  dy.stride(0), dy.shape[1], _ptr(loss), _ptr(row_loss),
+                                  _ptr(status), _stream()))
 
 
 def adam_step(w: torch.Tensor, g: torch.Tensor, m: torch.Tensor, v: torch.Tensor, step: int,
@@ -733,7 +736,8 @@ class GraphSAGE:
         fo = self.dims[-1]
         dy = self._buf("dyL", sampler.n_cap[0], fo, torch.bfloat16)
         softmax_xent(ys[-1], node_labels, sampler.nodes, sampler.sizes[0:1], self.num_classes,
-                     dy[:sampler.n_cap[0]], self.loss, self.status)
+                     dy[:sampler.n_cap[0]], self.loss, self.status,
+                     self._buf("row_loss", sampler.n_cap[0], 1, torch.float64)[:, 0])
         for l in range(L - 1, -1, -1):
             h = L - 1 - l
             layer = self.layers[l]

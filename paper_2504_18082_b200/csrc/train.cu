@@ -20,66 +20,72 @@ constexpr unsigned kFull = 0xffffffffu;
 // R33: for root i < n (label_i = node_labels[nodes[i]]; the roots are the prefix of `nodes`),
 //     loss = (1/n) sum_i [ lse_i - Y[i, label_i] ],  lse_i = m_i + log sum_c exp(Y[i, c] - m_i),
 //     dY[i, c] = (exp(Y[i, c] - lse_i) - 1[c == label_i]) / n     (c < C; columns C.. of dY = 0).
-// One block: warp w owns rows w, w + 32, ...; lane j columns j, j + 32, ... (C <= 256).  Row max
-// and sum by shuffles in fp32; the per-row losses are summed in fp64 per warp in row order and
-// the 32 warp sums in warp order by thread 0 (deterministic).  A label outside [0, C) sets the
-// status word (CMB_ERR_INVALID_ARGUMENT) and contributes nothing.
-__global__ void __launch_bounds__(kXentThreads)
-    k_xent(const float* __restrict__ logits, int64_t ld, const int32_t* __restrict__ node_labels,
-           const int32_t* __restrict__ nodes, const int64_t* __restrict__ n_dev, int64_t n_cap,
-           int C, __nv_bfloat16* __restrict__ dy, int64_t dy_ld, int dy_cols,
-           double* __restrict__ loss, int32_t* __restrict__ status) {
-  __shared__ double wsum[kXentThreads / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// k_xent_rows: one warp per root (a row is one latency chain: loads, max and sum shuffles, log),
+// lane j owning columns j, j + 32, ... (C <= 256); the row's loss term goes to row_loss[i] (fp64).
+// k_xent_sum: one block sums row_loss in a fixed order (thread t: rows t, t + 1024, ... in
+// order; then the 1024 partials in order by thread 0) -- deterministic.  A label outside [0, C)
+// sets the status word (CMB_ERR_INVALID_ARGUMENT); that row contributes nothing.
+constexpr int kRowWarps = 8;
+__global__ void __launch_bounds__(kRowWarps * 32)
+    k_xent_rows(const float* __restrict__ logits, int64_t ld, const int32_t* __restrict__ node_labels,
+                const int32_t* __restrict__ nodes, const int64_t* __restrict__ n_dev, int64_t n_cap,
+                int C, __nv_bfloat16* __restrict__ dy, int64_t dy_ld, int dy_cols,
+                double* __restrict__ row_loss, int32_t* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
   const int64_t n = min(*n_dev, n_cap);
-  const float inv_n = n > 0 ? 1.0f / static_cast<float>(n) : 0.f;
-  double acc = 0.0;
-  for (int64_t i = warp; i < n; i += kXentThreads / 32) {
-    const int32_t lab = __ldg(node_labels + __ldg(nodes + i));
-    const bool ok = lab >= 0 && lab < C;
-    if (!ok && lane == 0 && status) atomicCAS(status, 0, CMB_ERR_INVALID_ARGUMENT);
-    float y[8];
-    float m = -INFINITY;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kRowWarps + (threadIdx.x >> 5);
+  if (i >= n) return;  // warp-uniform
+  const float inv_n = 1.0f / static_cast<float>(n);
+  const int32_t lab = __ldg(node_labels + __ldg(nodes + i));
+  const bool ok = lab >= 0 && lab < C;
+  if (!ok && lane == 0 && status) atomicCAS(status, 0, CMB_ERR_INVALID_ARGUMENT);
+  float y[8];
+  float m = -INFINITY;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int c = lane + 32 * k;
-      y[k] = c < C ? __ldg(logits + i * ld + c) : -INFINITY;
-      m = fmaxf(m, y[k]);
-    }
+  for (int k = 0; k < 8; ++k) {
+    const int c = lane + 32 * k;
+    y[k] = c < C ? __ldg(logits + i * ld + c) : -INFINITY;
+    m = fmaxf(m, y[k]);
+  }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
-    float s = 0.f;
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+  float s = 0.f, ylab = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s += lane + 32 * k < C ? expf(y[k] - m) : 0.f;
+  for (int k = 0; k < 8; ++k) {
+    s += lane + 32 * k < C ? expf(y[k] - m) : 0.f;
+    if (lane + 32 * k == lab) ylab = y[k];
+  }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-    const float lse = m + logf(s);
-    float ylab = 0.f;
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(kFull, s, o);
+    ylab += __shfl_xor_sync(kFull, ylab, o);
+  }
+  const float lse = m + logf(s);
+  if (lane == 0) row_loss[i] = ok ? static_cast<double>(lse) - static_cast<double>(ylab) : 0.0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (lane + 32 * k == lab) ylab = y[k];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ylab += __shfl_xor_sync(kFull, ylab, o);
-    if (lane == 0 && ok) acc += static_cast<double>(lse) - static_cast<double>(ylab);
-    for (int c = lane; c < dy_cols; c += 32) {
+  for (int k = 0; k < 8; ++k) {
+    const int c = lane + 32 * k;
+    if (c < dy_cols) {
       float g = 0.f;
-      if (c < C && ok) {
-        const int k = c >> 5;  // c = lane + 32 k
-        float yc = 0.f;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          if (kk == k) yc = y[kk];
-        g = (expf(yc - lse) - (c == lab ? 1.f : 0.f)) * inv_n;
-      }
+      if (c < C && ok) g = (expf(y[k] - lse) - (c == lab ? 1.f : 0.f)) * inv_n;
       dy[i * dy_ld + c] = __float2bfloat16_rn(g);
     }
   }
-  if (lane == 0) wsum[warp] = acc;
+}
+
+__global__ void __launch_bounds__(kXentThreads)
+    k_xent_sum(const double* __restrict__ row_loss, const int64_t* __restrict__ n_dev,
+               int64_t n_cap, double* __restrict__ loss) {
+  __shared__ double part[kXentThreads];
+  const int64_t n = min(*n_dev, n_cap);
+  double t = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += kXentThreads) t += row_loss[i];
+  part[threadIdx.x] = t;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < kXentThreads / 32; ++w) t += wsum[w];
-    *loss = n > 0 ? t / static_cast<double>(n) : 0.0;
+    double a = 0.0;
+    for (int w = 0; w < kXentThreads; ++w) a += part[w];
+    *loss = n > 0 ? a / static_cast<double>(n) : 0.0;
   }
 }
 
@@ -125,17 +131,25 @@ extern "C" {
 cmb_status cmb_softmax_xent(const float* logits, int64_t ld, const int32_t* node_labels,
                             const int32_t* nodes, const int64_t* n_dev, int64_t n_cap,
                             int32_t num_classes, void* dy, int64_t dy_ld, int32_t dy_cols,
-                            double* loss, int32_t* status, void* stream) {
-  CMB_ARG(logits && node_labels && nodes && n_dev && dy && loss, "cmb_softmax_xent: null argument");
-  CMB_ARG(num_classes >= 1 && num_classes <= 256 && dy_cols >= num_classes && ld >= num_classes &&
+                            double* loss, double* row_loss, int32_t* status, void* stream) {
+  CMB_ARG(logits && node_labels && nodes && n_dev && dy && loss && row_loss,
+          "cmb_softmax_xent: null argument");
+  CMB_ARG(num_classes >= 1 && num_classes <= 256 && dy_cols >= num_classes && dy_cols <= 256 &&
+              ld >= num_classes &&
               dy_ld >= dy_cols && n_cap >= 0,
           "cmb_softmax_xent: need 1 <= num_classes <= 256 <= ..., dy_cols >= num_classes, "
           "ld / dy_ld >= their widths (got C=%d, dy_cols=%d)", num_classes, dy_cols);
   cmb_status st = require_sm100();
   if (st != CMB_OK) return st;
-  tr::k_xent<<<1, tr::kXentThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      logits, ld, node_labels, nodes, n_dev, n_cap, num_classes,
-      static_cast<__nv_bfloat16*>(dy), dy_ld, dy_cols, loss, status);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n_cap > 0) {
+    tr::k_xent_rows<<<static_cast<int>((n_cap + tr::kRowWarps - 1) / tr::kRowWarps),
+                      tr::kRowWarps * 32, 0, s>>>(logits, ld, node_labels, nodes, n_dev, n_cap,
+                                                  num_classes, static_cast<__nv_bfloat16*>(dy),
+                                                  dy_ld, dy_cols, row_loss, status);
+    CMB_CUDA(cudaGetLastError());
+  }
+  tr::k_xent_sum<<<1, tr::kXentThreads, 0, s>>>(row_loss, n_dev, n_cap, loss);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
 }
