@@ -457,6 +457,29 @@ CMB_API cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks*
                                            float* dw, float* db,
                                            void* workspace, size_t workspace_bytes, void* stream);
 
+/* NEXT-4 forward with the A tile saved for the backward ("saved operand"):
+ * cmb_sage_layer_forward that also writes every 128-row tile's operand image [X_dst | H] (bf16,
+ * the tensor cores' K-major 128-B-swizzled layout, rows past n_{L-1} zero) to a_save with the TMA
+ * engine while the MMAs run; cmb_sage_layer_backward_saved then loads those images (one bulk
+ * copy per tile) instead of re-gathering the feature rows -- same arithmetic, same results, bit
+ * for bit.  a_save: device, >= cmb_sage_saved_a_bytes(F, n_last_dst_cap) bytes (64 KB per tile
+ * at F <= 128), 16-B aligned, caller-owned; valid until the next forward on it.  The SAGE form
+ * only (not GCN). */
+CMB_API size_t cmb_sage_saved_a_bytes(int32_t feat_dim, int64_t n_last_dst_cap);
+CMB_API cmb_status cmb_sage_layer_forward_save(const cmb_graph* g, const cmb_blocks* blocks,
+                                               int32_t n_hops, int64_t n_last_dst_cap,
+                                               const void* w_img, const float* bias,
+                                               int32_t out_dim, int32_t relu, int32_t out_bf16,
+                                               void* out, int64_t out_ld, void* a_save,
+                                               size_t a_save_bytes, void* stream);
+CMB_API cmb_status cmb_sage_layer_backward_saved(const cmb_graph* g, const cmb_blocks* blocks,
+                                                 int32_t n_hops, int64_t n_last_dst_cap,
+                                                 const void* a_saved, size_t a_saved_bytes,
+                                                 const void* dy, int64_t dy_ld, int32_t dy_f32,
+                                                 const void* y, int64_t y_ld, int32_t out_dim,
+                                                 float* dw, float* db, void* workspace,
+                                                 size_t workspace_bytes, void* stream);
+
 /* NEXT-4 hidden-layer backward (reading R31 = R27 applied to the R29 layer): weight
  * gradients of a layer >= 2 on hop `hop` of the blocks, whose input is the previous layer's
  * bf16 output y_prev (rows = local src ids of the hop, the dst rows d < n_hop its prefix):

@@ -57,6 +57,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sage_hidden_backward_workspace_bytes", "cmb_sage_hidden_backward",
            "cmb_sage_hidden_weights_t_bytes", "cmb_sage_hidden_pack_weights_t",
            "cmb_sage_hidden_input_grad", "cmb_softmax_xent", "cmb_adam_step",
+           "cmb_sage_saved_a_bytes", "cmb_sage_layer_forward_save", "cmb_sage_layer_backward_saved",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -193,6 +194,11 @@ def lib():
             "cmb_sage_hidden_backward": (I32, [ctypes.POINTER(Blocks), I32, I64, P, I64, I32, P,
                                                I64, I32, P, I64, I32, P, P, P, SZ, P, I64, P]),
             "cmb_sage_hidden_weights_t_bytes": (SZ, [I32, I32]),
+            "cmb_sage_saved_a_bytes": (SZ, [I32, I64]),
+            "cmb_sage_layer_forward_save": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, P, I32,
+                                                  I32, I32, P, I64, P, SZ, P]),
+            "cmb_sage_layer_backward_saved": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, SZ, P,
+                                                    I64, I32, P, I64, I32, P, P, P, SZ, P]),
             "cmb_softmax_xent": (I32, [P, I64, P, P, P, I64, I32, P, I64, I32, P, P, P, P]),
             "cmb_adam_step": (I32, [P, P, P, P, I64, ctypes.c_double, ctypes.c_double,
                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, I32, P]),
@@ -487,11 +493,27 @@ class Sampler:
             _ptr(x_in), x_in.stride(0), _ptr(h), h.stride(0), _ptr(cache.stats), _stream()))
         return x_in, h
 
-    def sage_layer(self, layer: "SageLayer", out: Optional[torch.Tensor] = None):
+    def saved_a_buffer(self) -> torch.Tensor:
+        """Device buffer for the layer-1 operand tiles saved by sage_layer(save_a=True)."""
+        n = lib().cmb_sage_saved_a_bytes(self.graph.feat_dim, self.n_cap[self.L - 1])
+        if getattr(self, "_a_save", None) is None or self._a_save.numel() < n:
+            self._a_save = torch.empty(max(16, n), dtype=torch.uint8, device=self.graph.device)
+        return self._a_save
+
+    def sage_layer(self, layer: "SageLayer", out: Optional[torch.Tensor] = None,
+                   save_a: bool = False):
         """NEXT-4: a4 + a5 fused with the first GraphSAGE layer for the last sampled batch ->
-        Y [n_cap[L-1], out_dim] (rows < n_{L-1} valid), fp32 or bf16 as the layer says."""
+        Y [n_cap[L-1], out_dim] (rows < n_{L-1} valid), fp32 or bf16 as the layer says.
+        save_a: also keep the operand tiles for sage_layer_backward(saved=True)."""
         if out is None:
             out = layer.alloc_out(self.n_cap[self.L - 1])
+        if save_a:
+            a = self.saved_a_buffer()
+            _check(lib().cmb_sage_layer_forward_save(
+                self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
+                _ptr(layer.w_img), _ptr(layer.bias), layer.out_dim, int(layer.relu),
+                int(layer.out_bf16), _ptr(out), out.stride(0), _ptr(a), a.numel(), _stream()))
+            return out
         _check(lib().cmb_sage_layer_forward(
             self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
             _ptr(layer.w_img), _ptr(layer.bias), layer.out_dim, int(layer.relu),
@@ -526,7 +548,7 @@ class Sampler:
 
     def sage_layer_backward(self, layer: "SageLayer", dy: torch.Tensor,
                             y: Optional[torch.Tensor] = None, dw: Optional[torch.Tensor] = None,
-                            db: Optional[torch.Tensor] = None):
+                            db: Optional[torch.Tensor] = None, saved: bool = False):
         """NEXT-4 backward for the last sampled batch: dY (bf16 [>= n_{L-1}, out_dim]) and, for a
         ReLU layer, its output Y (bf16) -> (dW_self [F, out_dim], dW_neigh, db) fp32."""
         if dy.dtype not in (torch.bfloat16, torch.float32) or (
@@ -535,6 +557,14 @@ class Sampler:
         F, fo = layer.feat_dim, layer.out_dim
         ws = layer.backward_workspace()
         dw, db = _grad_out(dw, db, F, fo, layer.device)
+        if saved:   # the operand tiles of the last sage_layer(save_a=True) on this batch
+            a = self.saved_a_buffer()
+            _check(lib().cmb_sage_layer_backward_saved(
+                self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
+                _ptr(a), a.numel(), _ptr(dy), dy.stride(0), int(dy.dtype == torch.float32),
+                _ptr(y), 0 if y is None else y.stride(0), fo, _ptr(dw), _ptr(db), _ptr(ws),
+                ws.numel(), _stream()))
+            return dw[0], dw[1], db
         _check(lib().cmb_sage_layer_backward(
             self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
             _ptr(dy), dy.stride(0), int(dy.dtype == torch.float32), _ptr(y),
@@ -699,6 +729,9 @@ class GraphSAGE:
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self._bufs = {}
         self.device = dev
+        # layer 1's operand tiles are saved by the forward and reloaded by the backward instead
+        # of re-gathering the feature rows; False re-gathers (same results)
+        self.save_a = True
 
     def _views(self, flat, l):
         fi, fo = self.dims[l], self.dims[l + 1]
@@ -724,7 +757,7 @@ class GraphSAGE:
             h = L - 1 - l
             out = self._buf(("y", l), sampler.n_cap[h], layer.out_dim,
                             torch.bfloat16 if layer.out_bf16 else torch.float32)
-            ys.append(sampler.sage_layer(layer, out) if l == 0 else
+            ys.append(sampler.sage_layer(layer, out, save_a=self.save_a) if l == 0 else
                       sampler.sage_hidden(layer, h, ys[-1], out))
         return ys
 
@@ -745,7 +778,7 @@ class GraphSAGE:
             dw = self.grads[self.offsets[l]:self.offsets[l] + 2 * g_ws.numel()].view(2, *g_ws.shape)
             y = ys[l] if layer.relu else None
             if l == 0:
-                sampler.sage_layer_backward(layer, dy, y, dw=dw, db=g_b)
+                sampler.sage_layer_backward(layer, dy, y, dw=dw, db=g_b, saved=self.save_a)
             else:
                 dz = self._buf(("dz", l), sampler.n_cap[h], ((layer.out_dim + 63) // 64) * 64,
                                torch.bfloat16)

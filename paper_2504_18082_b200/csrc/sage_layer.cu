@@ -120,6 +120,24 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         : "memory");
   }
 }
+// shared -> global bulk copy (TMA engine) in 32-KB pieces, one bulk group; the source may be
+// overwritten after bulk_s2g_wait_read()
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+  for (uint32_t off = 0; off < bytes; off += 32768u) {
+    const uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                     static_cast<char*>(dst) + off),
+                 "r"(src + off), "r"(n)
+                 : "memory");
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_s2g_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_s2g_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -377,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                  const float4* __restrict__ x, int64_t ld4, const int32_t* __restrict__ map,
                  int F, int kh, const uint4* __restrict__ w_img, const float* __restrict__ bias,
                  int fo, int tmem_cols, int relu, int out_bf16, void* __restrict__ out,
-                 int64_t out_ld, int halves) {
+                 int64_t out_ld, int halves, uint8_t* __restrict__ a_save = nullptr) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   const uint32_t wbytes = w_img_bytes(kh, fo, halves);
@@ -438,9 +456,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     // ---------------------------------------------------------------- 1. gather -> A (bf16)
-    ga.build(tile + gridDim.x, sA, false, halves == 1, /*pre=*/true);
+    ga.build(tile + gridDim.x, sA, a_save != nullptr, halves == 1, /*pre=*/true);
     fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core (async proxy)
     __syncthreads();
+    // the built A tile (the exact operand image, dead rows zero) -> HBM for the backward, by the
+    // TMA engine while the MMAs and the epilogue run (R27: the backward reads it back instead of
+    // re-gathering the feature rows)
+    if (a_save && tid == 32)
+      bulk_s2g(a_save + tile * static_cast<int64_t>(a_bytes(kh)), sA_addr, a_bytes(kh));
 
     // ---------------------------------------------------------------- 2. MMA (one thread)
     if (tid == 0) {
@@ -503,9 +526,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (a_save && tid == 32) bulk_s2g_wait_read();  // the saved tile has left shared memory
     tc_fence_before();
     __syncthreads();  // TMEM drained and A free before the next tile overwrites them
   }
+  if (a_save && tid == 32) bulk_s2g_wait_all();
 
   if (tid == 0 && ntiles <= blockIdx.x) mbar_wait(wbar, 0);  // no tile: the copy must still land
   __syncthreads();
@@ -561,7 +586,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const float4* __restrict__ x, int64_t ld4, const int32_t* __restrict__ map,
                      int F, int kh, const void* __restrict__ dy, int64_t dy_ld, int dy_f32,
                      const __nv_bfloat16* __restrict__ y, int64_t y_ld, int fo, int tmem_alloc,
-                     float* __restrict__ part, float* __restrict__ part_db) {
+                     float* __restrict__ part, float* __restrict__ part_db,
+                     const uint8_t* __restrict__ a_saved = nullptr) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   uint8_t* sA = smem;
@@ -607,7 +633,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   ga.warp = warp;
   ga.lane = lane;
   ga.pol = pol_keep;
-  ga.start(blockIdx.x);
+  if (!a_saved) ga.start(blockIdx.x);
+  const uint32_t lbar = saddr(bar + 2);  // a_saved: the tile image's bulk load
+  uint32_t lphase = 0;
+  if (a_saved && tid == 0) {
+    mbar_init(lbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
 
   // dZ staging: thread owns the 8-column chunk c = tid % (fo/8) of rows tid / (fo/8) + i*step
   const int cpr = fo / 8;           // chunks per row (a power of two dividing kThreads)
@@ -623,7 +656,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t phase = 0;
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    ga.build(tile + gridDim.x, sA, true);
+    if (a_saved) {  // the forward's A tile: one bulk load, overlapped with the dZ staging below
+      if (tid == 0)
+        bulk_g2s(sA_addr, a_saved + tile * static_cast<int64_t>(a_bytes(kh)), a_bytes(kh), lbar);
+    } else {
+      ga.build(tile + gridDim.x, sA, true);
+    }
     for (int r = tid / cpr; r < kM; r += rstep) {
       const int64_t row = tile * kM + r;
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
@@ -653,6 +691,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                            (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4);
       *reinterpret_cast<uint4*>(sB + off) = v;
     }
+    if (a_saved) {
+      mbar_wait(lbar, lphase);
+      lphase ^= 1;
+    }
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -672,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     phase ^= 1;
     tc_fence_after();
     __syncthreads();
-    ga.advance();
+    if (!a_saved) ga.advance();
   }
 
   // ---------------------------------------------------------------- partials
@@ -695,8 +737,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  {  // db: the per-thread column sums added in a fixed order (deterministic; dZ's tile is free)
+    float* buf = reinterpret_cast<float*>(sB);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) atomicAdd(&sdb[c * 8 + i], dbacc[i]);
+    for (int i = 0; i < 8; ++i) buf[(tid / cpr) * fo + c * 8 + i] = dbacc[i];
+    __syncthreads();
+    for (int i = tid; i < fo; i += kThreads) {
+      float t = 0.f;
+      for (int j = 0; j < rstep; ++j) t += buf[j * fo + i];
+      sdb[i] = t;
+    }
+  }
   tc_fence_before();
   __syncthreads();
   for (int i = tid; i < fo; i += kThreads) part_db[static_cast<int64_t>(blockIdx.x) * fo + i] = sdb[i];
@@ -1155,8 +1206,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
   }
+  {  // db: the per-thread column sums added in a fixed order (deterministic; dZ's tile is free)
+    float* buf = reinterpret_cast<float*>(sB);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) atomicAdd(&sdb[c * 8 + i], dbacc[i]);
+    for (int i = 0; i < 8; ++i) buf[(tid / cpr) * fo + c * 8 + i] = dbacc[i];
+    __syncthreads();
+    for (int i = tid; i < fo; i += kThreads) {
+      float t = 0.f;
+      for (int j = 0; j < rstep; ++j) t += buf[j * fo + i];
+      sdb[i] = t;
+    }
+  }
   __syncthreads();
   for (int i = tid; i < fo; i += kThreads) part_db[static_cast<int64_t>(blockIdx.x) * fo + i] = sdb[i];
   if (warp == 0) {
@@ -1254,7 +1314,8 @@ cmb_status cmb_sage_pack_weights(const float* w_self, const float* w_neigh, int3
 static cmb_status layer_forward(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
                                 int64_t n_last_dst_cap, const void* w_img, const float* bias,
                                 int32_t out_dim, int32_t relu, int32_t out_bf16, void* out,
-                                int64_t out_ld, void* stream, int halves) {
+                                int64_t out_ld, void* stream, int halves,
+                                void* a_save = nullptr) {
   CMB_ARG(g && b && w_img && out, "cmb_sage_layer_forward: null argument");
   CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_sage_layer_forward: bad n_hops");
   CMB_ARG(g->d.x != nullptr, "cmb_sage_layer_forward: graph has no feature table");
@@ -1293,7 +1354,8 @@ static cmb_status layer_forward(const cmb_graph* g, const cmb_blocks* b, int32_t
 #define CMB_LAYER_ARGS                                                                        \
   b->indptr[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,                     \
       reinterpret_cast<const float4*>(g->d.x), g->d.ld / 4, b->nodes, F, kh,                 \
-      static_cast<const uint4*>(w_img), bias, out_dim, cols, relu, out_bf16, out, out_ld, halves
+      static_cast<const uint4*>(w_img), bias, out_dim, cols, relu, out_bf16, out, out_ld, halves, \
+      static_cast<uint8_t*>(a_save)
   if (dmax <= 5)
     sl::k_sage_layer<5, 2><<<grid, sl::kThreads, smem, s>>>(CMB_LAYER_ARGS);
   else
@@ -1309,6 +1371,24 @@ cmb_status cmb_sage_layer_forward(const cmb_graph* g, const cmb_blocks* b, int32
                                   int64_t out_ld, void* stream) {
   return layer_forward(g, b, n_hops, n_last_dst_cap, w_img, bias, out_dim, relu, out_bf16, out,
                        out_ld, stream, 2);
+}
+
+size_t cmb_sage_saved_a_bytes(int32_t feat_dim, int64_t n_last_dst_cap) {
+  if (feat_dim < 1 || feat_dim > 128 || n_last_dst_cap < 0) return 0;
+  return static_cast<size_t>((n_last_dst_cap + sl::kM - 1) / sl::kM) * sl::a_bytes((feat_dim + 63) / 64);
+}
+
+cmb_status cmb_sage_layer_forward_save(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                       int64_t n_last_dst_cap, const void* w_img,
+                                       const float* bias, int32_t out_dim, int32_t relu,
+                                       int32_t out_bf16, void* out, int64_t out_ld, void* a_save,
+                                       size_t a_save_bytes, void* stream) {
+  CMB_ARG(a_save && g, "cmb_sage_layer_forward_save: null argument");
+  const size_t need = cmb_sage_saved_a_bytes(g->d.f, n_last_dst_cap);
+  CMB_ARG(a_save_bytes >= need && sl::aligned16(a_save),
+          "cmb_sage_layer_forward_save: a_save smaller than %zu bytes or unaligned", need);
+  return layer_forward(g, b, n_hops, n_last_dst_cap, w_img, bias, out_dim, relu, out_bf16, out,
+                       out_ld, stream, 2, a_save);
 }
 
 size_t cmb_gcn_weights_bytes(int32_t feat_dim, int32_t out_dim) {
@@ -1349,11 +1429,11 @@ size_t cmb_sage_backward_workspace_bytes(int32_t feat_dim, int32_t out_dim) {
   return static_cast<size_t>(sl::kMaxBwdCtas) * (2 * kh * 64 + 1) * out_dim * sizeof(float);
 }
 
-cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
-                                   int64_t n_last_dst_cap, const void* dy, int64_t dy_ld,
-                                   int32_t dy_f32, const void* y, int64_t y_ld, int32_t out_dim, float* dw,
-                                   float* db, void* workspace, size_t workspace_bytes,
-                                   void* stream) {
+static cmb_status layer_backward(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                 int64_t n_last_dst_cap, const void* dy, int64_t dy_ld,
+                                 int32_t dy_f32, const void* y, int64_t y_ld, int32_t out_dim,
+                                 float* dw, float* db, void* workspace, size_t workspace_bytes,
+                                 void* stream, const void* a_saved) {
   CMB_ARG(g && b && dy && dw && db && workspace, "cmb_sage_layer_backward: null argument");
   CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_sage_layer_backward: bad n_hops");
   CMB_ARG(g->d.x != nullptr, "cmb_sage_layer_backward: graph has no feature table");
@@ -1404,7 +1484,7 @@ cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* b, int3
   b->indptr[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,                     \
       reinterpret_cast<const float4*>(g->d.x), g->d.ld / 4, b->nodes, F, kh,                 \
       dy, dy_ld, dy_f32, static_cast<const __nv_bfloat16*>(y), y_ld,                         \
-      out_dim, alloc, part, part_db
+      out_dim, alloc, part, part_db, static_cast<const uint8_t*>(a_saved)
     if (dmax <= 5)
       sl::k_sage_layer_bwd<5, 2><<<grid, sl::kThreads, smem, s>>>(CMB_BWD_ARGS);
     else
@@ -1417,6 +1497,29 @@ cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* b, int3
       part, part_db, grid, F, kh, out_dim, dw, db);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
+}
+
+cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                   int64_t n_last_dst_cap, const void* dy, int64_t dy_ld,
+                                   int32_t dy_f32, const void* y, int64_t y_ld, int32_t out_dim,
+                                   float* dw, float* db, void* workspace, size_t workspace_bytes,
+                                   void* stream) {
+  return layer_backward(g, b, n_hops, n_last_dst_cap, dy, dy_ld, dy_f32, y, y_ld, out_dim, dw, db,
+                        workspace, workspace_bytes, stream, nullptr);
+}
+
+cmb_status cmb_sage_layer_backward_saved(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                         int64_t n_last_dst_cap, const void* a_saved,
+                                         size_t a_saved_bytes, const void* dy, int64_t dy_ld,
+                                         int32_t dy_f32, const void* y, int64_t y_ld,
+                                         int32_t out_dim, float* dw, float* db, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
+  CMB_ARG(a_saved && g, "cmb_sage_layer_backward_saved: null argument");
+  const size_t need = cmb_sage_saved_a_bytes(g->d.f, n_last_dst_cap);
+  CMB_ARG(a_saved_bytes >= need && sl::aligned16(a_saved),
+          "cmb_sage_layer_backward_saved: a_saved smaller than %zu bytes or unaligned", need);
+  return layer_backward(g, b, n_hops, n_last_dst_cap, dy, dy_ld, dy_f32, y, y_ld, out_dim, dw, db,
+                        workspace, workspace_bytes, stream, a_saved);
 }
 
 size_t cmb_sage_hidden_weights_bytes(int32_t in_dim, int32_t out_dim) {

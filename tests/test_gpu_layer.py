@@ -469,3 +469,33 @@ def test_hidden_input_grad_parity(name, factor, hop, fin, fo):
     tol = 2.0 ** -7 * S + 1e-30
     assert np.all(err <= tol), float(np.max(err - tol))
     assert np.all(got[ns:] == 0.0)
+
+
+# ---------------------------------------------------------------- saved operand tiles (§7)
+@pytest.mark.parametrize("name,factor,relu", [("tiny", None, True), ("products", 0.01, True),
+                                              ("arxiv", None, False), ("products", None, True)])
+def test_layer_saved_operand_is_bit_exact(name, factor, relu):
+    """The forward that saves its operand tiles returns the same Y, and the backward that reloads
+    them returns the same dW / db, bit for bit, as the re-gathering pair (same operand bytes, same
+    MMAs, same reduction order); the R27 bound is checked on the re-gathering pair above."""
+    b, prep, g = _bundle(name, factor)
+    cfg = b.cfg
+    F, L, fo = cfg.feat_dim, len(cfg.fanouts), 256
+    ws, wn, bias = _weights(F, fo, 5)
+    layer = cmb.SageLayer(ws, wn, bias, relu=relu, out_bf16=True)
+    order = oracle.order_roots(b.train, b.comm, cfg.num_communities, oracle.MODE_RAND, 0.0, SEED, 0)
+    roots = oracle.batch_roots(order, cfg.batch_size, 1)
+    sampler = cmb.Sampler(g, len(roots), cfg.fanouts)
+    sampler.sample(torch.from_numpy(roots).cuda(), cfg.p_intra, SEED, 1)
+    y0 = sampler.sage_layer(layer).clone()
+    y1 = sampler.sage_layer(layer, save_a=True)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    dy = torch.randn(sampler.n_cap[L - 1], fo, generator=gen, device="cuda") * 0.01   # fp32 dY
+    r0 = [t.clone() for t in sampler.sage_layer_backward(layer, dy, y1 if relu else None)]
+    r1 = sampler.sage_layer_backward(layer, dy, y1 if relu else None, saved=True)
+    torch.cuda.synchronize()
+    assert sampler.status() == 0
+    nd = int(sampler.sizes[L - 1].item())
+    assert torch.equal(y0[:nd].view(torch.int16), y1[:nd].view(torch.int16))
+    for a, c in zip(r0, r1):
+        assert torch.equal(a.view(torch.int32), c.view(torch.int32))
