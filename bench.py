@@ -752,6 +752,9 @@ def main():
         return 0  # the reference arm runs on rank 0 only; the other ranks exit without work
     from gen import CONFIGS, generate
     cfg = CONFIGS[args.config]
+    if os.environ.get("CMB_FEAT_LD"):  # layout experiments: feature row stride in floats
+        import dataclasses
+        cfg = dataclasses.replace(cfg, feat_ld=int(os.environ["CMB_FEAT_LD"]))
     bundle = generate(cfg)
     if args.impl == "reference":
         return run_reference(args, bundle)
