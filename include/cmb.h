@@ -562,6 +562,29 @@ CMB_API cmb_status cmb_adam_step(float* w, const float* g, float* m, float* v, i
                                  double lr, double beta1, double beta2, double eps,
                                  double weight_decay, int32_t step, void* stream);
 
+/* One GraphSAGE layer's slice of the flat parameter buffer and its bf16 operand images, for
+ * cmb_adam_step_pack: parameters [offset, offset + 2 in_dim out_dim + out_dim) of the buffer are
+ * [W_self | W_neigh | b] (row-major [in_dim x out_dim] each); img: the forward weight image
+ * (cmb_sage_pack_weights / cmb_sage_hidden_pack_weights layout, kh = ceil(in_dim / 64));
+ * img_t: NULL or the transposed image of cmb_sage_hidden_pack_weights_t (kt = ceil(out_dim/64)). */
+typedef struct {
+  int64_t offset;
+  int32_t in_dim, out_dim;
+  void* img;
+  void* img_t;
+} cmb_layer_pack;
+
+/* cmb_adam_step fused with the repack of the updated weights: every W element is written, as
+ * bf16, into its layer's forward image and (img_t != NULL) its transposed image in the same pass
+ * -- one launch instead of one Adam launch plus one packer launch per image.  The images'
+ * padding (columns >= in_dim / out_dim) must already be zero (it is never written).  n_layers
+ * <= 8; layers must tile [0, n) in order. */
+CMB_API cmb_status cmb_adam_step_pack(float* w, const float* g, float* m, float* v, int64_t n,
+                                      double lr, double beta1, double beta2, double eps,
+                                      double weight_decay, int32_t step,
+                                      const cmb_layer_pack* layers, int32_t n_layers,
+                                      void* stream);
+
 /* ------------------------------------------------------------------ status */
 /* Synchronises `stream`, returns (and clears) the sticky device status word of a
  * graph / order / sample workspace. */

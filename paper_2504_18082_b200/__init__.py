@@ -58,6 +58,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sage_hidden_weights_t_bytes", "cmb_sage_hidden_pack_weights_t",
            "cmb_sage_hidden_input_grad", "cmb_softmax_xent", "cmb_adam_step",
            "cmb_sage_saved_a_bytes", "cmb_sage_layer_forward_save", "cmb_sage_layer_backward_saved",
+           "cmb_adam_step_pack",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -88,6 +89,12 @@ class Batch(ctypes.Structure):
     _fields_ = [("roots", ctypes.c_void_p), ("n_roots", ctypes.c_int64),
                 ("batch_id", ctypes.c_uint32), ("out", ctypes.POINTER(Blocks)),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
+
+
+class LayerPack(ctypes.Structure):
+    """cmb_layer_pack (include/cmb.h)."""
+    _fields_ = [("offset", ctypes.c_int64), ("in_dim", ctypes.c_int32), ("out_dim", ctypes.c_int32),
+                ("img", ctypes.c_void_p), ("img_t", ctypes.c_void_p)]
 
 
 class FeatureCacheDesc(ctypes.Structure):
@@ -195,6 +202,9 @@ def lib():
                                                I64, I32, P, I64, I32, P, P, P, SZ, P, I64, P]),
             "cmb_sage_hidden_weights_t_bytes": (SZ, [I32, I32]),
             "cmb_sage_saved_a_bytes": (SZ, [I32, I64]),
+            "cmb_adam_step_pack": (I32, [P, P, P, P, I64, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_double, ctypes.c_double, I32,
+                                         ctypes.POINTER(LayerPack), I32, P]),
             "cmb_sage_layer_forward_save": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, P, I32,
                                                   I32, I32, P, I64, P, SZ, P]),
             "cmb_sage_layer_backward_saved": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, SZ, P,
@@ -787,10 +797,15 @@ class GraphSAGE:
                     layer, h, dz, self._buf(("dx", l), sampler.n_cap[h + 1], layer.feat_dim,
                                             torch.float32)[:sampler.n_cap[h + 1]])
         self.step_count += 1
-        adam_step(self.params, self.grads, self.m, self.v, self.step_count, self.lr,
-                  weight_decay=self.weight_decay)
-        for layer in self.layers:
-            layer.repack()
+        # Adam and the repack of every weight image (forward and transposed) in one launch
+        packs = (LayerPack * L)()
+        for l, layer in enumerate(self.layers):
+            wt = layer.transposed_image() if layer.hidden else None
+            packs[l] = LayerPack(self.offsets[l], layer.feat_dim, layer.out_dim,
+                                 layer.w_img.data_ptr(), None if wt is None else wt.data_ptr())
+        _check(lib().cmb_adam_step_pack(
+            _ptr(self.params), _ptr(self.grads), _ptr(self.m), _ptr(self.v), self.params.numel(),
+            self.lr, 0.9, 0.999, 1e-8, self.weight_decay, self.step_count, packs, L, _stream()))
         return self.loss
 
 

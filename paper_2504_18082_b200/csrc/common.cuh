@@ -110,6 +110,17 @@ struct DevGraph {
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
+// byte offset of element (row r, column c of half h) in a K-major SWIZZLE_128B bf16 operand image
+// (the tcgen05 canonical layout) whose 128-byte-wide atoms hold `rows` rows each (atom = h*kh +
+// c/64; 8-row groups 1 KB apart; 16-byte chunk j of row r stored at chunk j ^ (r & 7)).  Used by
+// the layer kernels, the weight packer and the fused Adam + repack.
+__host__ __device__ inline uint32_t sw128_off(int r, int h, int c, int kh, int rows) {
+  const int atom = h * kh + (c >> 6);
+  const int j = (c & 63) >> 3;
+  return static_cast<uint32_t>(atom) * rows * 128u + (r >> 3) * 1024 + (r & 7) * 128 +
+         ((j ^ (r & 7)) << 4) + ((c & 7) << 1);
+}
+
 }  // namespace cmb
 
 struct cmb_graph {

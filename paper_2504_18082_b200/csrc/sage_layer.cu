@@ -50,14 +50,7 @@ inline size_t smem_bytes(int kh, int fo) {
   return 1024 /*alignment slack*/ + w_img_bytes(kh, fo) + a_bytes(kh) + 64 /*barrier, tmem slot*/ +
          static_cast<size_t>(fo) * 4 /*bias*/;
 }
-// byte offset of element (row r, column c of half h) in a K-major SWIZZLE_128B operand image whose
-// atoms hold `rows` rows each (atom = h*kh + c/64)
-__host__ __device__ inline uint32_t sw128_off(int r, int h, int c, int kh, int rows) {
-  const int atom = h * kh + (c >> 6);
-  const int j = (c & 63) >> 3;
-  return static_cast<uint32_t>(atom) * rows * kAtomBytes + (r >> 3) * 1024 + (r & 7) * 128 +
-         ((j ^ (r & 7)) << 4) + ((c & 7) << 1);
-}
+// sw128_off (common.cuh): byte offset of an element in the K-major SWIZZLE_128B operand image
 
 // ----------------------------------------------------------------- PTX wrappers (tcgen05, mbarrier)
 __device__ __forceinline__ uint32_t saddr(const void* p) {

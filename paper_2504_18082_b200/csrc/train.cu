@@ -121,6 +121,49 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// cmb_adam_step_pack: the Adam update of k_adam, then every updated W element rounded to bf16
+// and stored at its place in the layer's forward image (row n = output column, K column c, half
+// h) and transposed image (row c, K column n, half h).  Element-per-thread over the flat buffer.
+constexpr int kMaxPackLayers = 8;
+struct PackTable {
+  int n_layers;
+  int64_t offset[kMaxPackLayers + 1];
+  int in_dim[kMaxPackLayers], out_dim[kMaxPackLayers];
+  __nv_bfloat16* img[kMaxPackLayers];
+  __nv_bfloat16* img_t[kMaxPackLayers];
+};
+
+__global__ void __launch_bounds__(256)
+    k_adam_pack(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
+                float* __restrict__ v, int64_t n, float lr, float b1, float b2, float omb1,
+                float omb2, float eps, float wd, float c1, float c2,
+                const __grid_constant__ PackTable t) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float gk = __fmaf_rn(wd, w[i], __ldg(g + i));
+    const float mk = __fmaf_rn(b1, m[i], omb1 * gk);
+    const float vk = __fmaf_rn(b2, v[i], omb2 * gk * gk);
+    const float den = __fsqrt_rn(vk * c2) + eps;
+    const float wk = w[i] - lr * __fdiv_rn(mk * c1, den);
+    w[i] = wk;
+    m[i] = mk;
+    v[i] = vk;
+    int l = 0;
+    while (l + 1 < t.n_layers && i >= t.offset[l + 1]) ++l;
+    const int F = t.in_dim[l], fo = t.out_dim[l];
+    const int64_t j = i - t.offset[l];
+    const int64_t per = static_cast<int64_t>(F) * fo;
+    if (j < 2 * per) {  // a weight (the bias has no image)
+      const int h = static_cast<int>(j / per);
+      const int r = static_cast<int>(j - h * per);
+      const int c = r / fo, o = r - c * fo;
+      const __nv_bfloat16 bv = __float2bfloat16_rn(wk);
+      t.img[l][sw128_off(o, h, c, (F + 63) / 64, fo) >> 1] = bv;
+      if (t.img_t[l]) t.img_t[l][sw128_off(c, h, o, (fo + 63) / 64, F) >> 1] = bv;
+    }
+  }
+}
+
 }  // namespace tr
 }  // namespace cmb
 
@@ -177,6 +220,47 @@ cmb_status cmb_adam_step(float* w, const float* g, float* m, float* v, int64_t n
       static_cast<float>(beta1), static_cast<float>(beta2), static_cast<float>(1.0 - beta1),
       static_cast<float>(1.0 - beta2), static_cast<float>(eps), static_cast<float>(weight_decay),
       static_cast<float>(c1), static_cast<float>(c2));
+  CMB_CUDA(cudaGetLastError());
+  return CMB_OK;
+}
+
+cmb_status cmb_adam_step_pack(float* w, const float* g, float* m, float* v, int64_t n, double lr,
+                              double beta1, double beta2, double eps, double weight_decay,
+                              int32_t step, const cmb_layer_pack* layers, int32_t n_layers,
+                              void* stream) {
+  CMB_ARG(w && g && m && v && layers, "cmb_adam_step_pack: null argument");
+  CMB_ARG(n >= 0 && step >= 1 && beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0 &&
+              n_layers >= 1 && n_layers <= tr::kMaxPackLayers,
+          "cmb_adam_step_pack: need step >= 1, betas in [0, 1), 1 <= n_layers <= 8");
+  tr::PackTable t{};
+  t.n_layers = n_layers;
+  int64_t at = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    const cmb_layer_pack& L = layers[l];
+    CMB_ARG(L.offset == at && L.in_dim >= 1 && L.in_dim <= 256 && L.out_dim >= 16 &&
+                L.out_dim <= 256 && L.out_dim % 16 == 0 && L.img,
+            "cmb_adam_step_pack: layer %d: offsets must tile the buffer in order, 1 <= in_dim <= "
+            "256, out_dim in [16, 256] a multiple of 16, img non-null", l);
+    t.offset[l] = L.offset;
+    t.in_dim[l] = L.in_dim;
+    t.out_dim[l] = L.out_dim;
+    t.img[l] = static_cast<__nv_bfloat16*>(L.img);
+    t.img_t[l] = static_cast<__nv_bfloat16*>(L.img_t);
+    at += 2ll * L.in_dim * L.out_dim + L.out_dim;
+  }
+  CMB_ARG(at == n, "cmb_adam_step_pack: the layers cover %lld parameters, n = %lld",
+          static_cast<long long>(at), static_cast<long long>(n));
+  t.offset[n_layers] = n;
+  if (n == 0) return CMB_OK;
+  cmb_status st = require_sm100();
+  if (st != CMB_OK) return st;
+  const double c1 = 1.0 / (1.0 - std::pow(beta1, step));
+  const double c2 = 1.0 / (1.0 - std::pow(beta2, step));
+  const int grid = static_cast<int>(n / 256 + 1 < 148 * 8 ? n / 256 + 1 : 148 * 8);
+  tr::k_adam_pack<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      w, g, m, v, n, static_cast<float>(lr), static_cast<float>(beta1), static_cast<float>(beta2),
+      static_cast<float>(1.0 - beta1), static_cast<float>(1.0 - beta2), static_cast<float>(eps),
+      static_cast<float>(weight_decay), static_cast<float>(c1), static_cast<float>(c2), t);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
 }

@@ -227,3 +227,34 @@ def test_training_fits_one_batch():
     labels = torch.from_numpy(make_labels(b, C)).cuda()
     losses = [float(model.train_step(sampler, labels).item()) for _ in range(40)]
     assert losses[0] > 1.0 and losses[-1] < 0.25 * losses[0], losses
+
+
+def test_fused_adam_repack_equals_adam_then_pack():
+    """cmb_adam_step_pack (one launch) = cmb_adam_step + a fresh pack of every image, bit for
+    bit: parameters, moments, forward images and transposed images after three steps."""
+    cfg = scaled(CONFIGS["products"], 0.01)
+    b = generate(cfg)
+    C = num_classes(cfg)
+    g = cmb.Graph.from_bundle(b)
+    L = len(cfg.fanouts)
+    labels = torch.from_numpy(make_labels(b, C)).cuda()
+    order = oracle.order_roots(b.train, b.comm, cfg.num_communities, oracle.MODE_RAND, 0.0, SEED, 0)
+    sampler = cmb.Sampler(g, cfg.batch_size, cfg.fanouts)
+    model = cmb.GraphSAGE(cfg.feat_dim, C, num_layers=L, seed=2)
+    for k in range(3):
+        roots = oracle.batch_roots(order, cfg.batch_size, k % 2)   # the scaled graph has 2
+        sampler.sample(torch.from_numpy(roots).cuda(), cfg.p_intra, SEED, k)
+        p_before, m_before, v_before = (t.clone() for t in (model.params, model.m, model.v))
+        model.train_step(sampler, labels)
+        # the unfused reference from the same state and gradients
+        w, m, v = p_before.clone(), m_before.clone(), v_before.clone()
+        cmb.adam_step(w, model.grads, m, v, model.step_count, model.lr,
+                      weight_decay=model.weight_decay)
+        for got, want in ((model.params, w), (model.m, m), (model.v, v)):
+            assert torch.equal(got.view(torch.int32), want.view(torch.int32))
+        for layer in model.layers:
+            ref = cmb.SageLayer(layer.w_self, layer.w_neigh, layer.bias, hidden=layer.hidden)
+            assert torch.equal(layer.w_img, ref.w_img)
+            if layer.hidden:
+                assert torch.equal(layer.transposed_image(), ref.transposed_image())
+    torch.cuda.synchronize()
