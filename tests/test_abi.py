@@ -79,6 +79,9 @@ def test_layer_entry_points_host_checks(cmb):
     assert L.cmb_sage_hidden_weights_t_bytes(256, 64) == 2 * 1 * 256 * 128   # K = 64, N = 256
     assert L.cmb_sage_hidden_weights_t_bytes(256, 48) == 2 * 1 * 256 * 128   # K padded to 64
     assert L.cmb_sage_hidden_weights_t_bytes(100, 64) == 0   # N = in_dim multiple of 16
+    assert L.cmb_sage_saved_a_bytes(100, 180_224) == 1408 * 2 * 2 * 128 * 128   # 64 KB per tile
+    assert L.cmb_sage_saved_a_bytes(16, 1) == 2 * 1 * 128 * 128
+    assert L.cmb_sage_saved_a_bytes(129, 10) == 0
     for call in (lambda: L.cmb_sage_pack_weights(None, None, 100, 256, None, 0, None),
                  lambda: L.cmb_sage_layer_forward(None, None, 3, 0, None, None, 256, 1, 0, None,
                                                   0, None),
@@ -92,6 +95,16 @@ def test_layer_entry_points_host_checks(cmb):
                                                     0, 256, None, None, None, 0, None, 0, None),
                  lambda: L.cmb_sage_hidden_pack_weights_t(None, None, 256, 64, None, 0, None),
                  lambda: L.cmb_sage_hidden_input_grad(None, 0, 0, 0, None, 0, 64, None, 256,
-                                                      None, 0, None, 0, None)):
+                                                      None, 0, None, 0, None),
+                 lambda: L.cmb_sage_layer_forward_save(None, None, 3, 0, None, None, 256, 1, 1,
+                                                       None, 0, None, 0, None),
+                 lambda: L.cmb_sage_layer_backward_saved(None, None, 3, 0, None, 0, None, 0, 0,
+                                                         None, 0, 256, None, None, None, 0, None),
+                 lambda: L.cmb_softmax_xent(None, 64, None, None, None, 0, 47, None, 64, 64, None,
+                                            None, None, None),
+                 lambda: L.cmb_adam_step(None, None, None, None, 4, 1e-3, 0.9, 0.999, 1e-8, 0.0,
+                                         1, None),
+                 lambda: L.cmb_adam_step_pack(None, None, None, None, 4, 1e-3, 0.9, 0.999, 1e-8,
+                                              0.0, 1, None, 1, None)):
         assert call() == 1
         assert b"null" in L.cmb_last_error_message()
