@@ -655,15 +655,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
       ga.build(tile + gridDim.x, sA, true);
     }
-    for (int r = tid / cpr; r < kM; r += rstep) {
-      const int64_t row = tile * kM + r;
-      uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (row < n_dst) {
-        v = load_dy8(dy, dy_f32, row, dy_ld, c);
+    // dZ staging, four of the thread's rows at a time: all their loads first (one round trip),
+    // then mask, column sums and the swizzled shared-memory stores
+    for (int r0 = tid / cpr; r0 < kM; r0 += 4 * rstep) {
+      uint4 v[4], m[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + u * rstep;
+        const int64_t row = tile * kM + r;
+        const bool live = r < kM && row < n_dst;
+        v[u] = live ? load_dy8(dy, dy_f32, row, dy_ld, c) : make_uint4(0u, 0u, 0u, 0u);
+        m[u] = (live && y) ? __ldg(reinterpret_cast<const uint4*>(y + row * y_ld) + c)
+                           : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + u * rstep;
+        if (r >= kM) break;
         if (y) {
-          const uint4 m = __ldg(reinterpret_cast<const uint4*>(y + row * y_ld) + c);
-          const uint32_t* mw = reinterpret_cast<const uint32_t*>(&m);
-          uint32_t* vw = reinterpret_cast<uint32_t*>(&v);
+          const uint32_t* mw = reinterpret_cast<const uint32_t*>(&m[u]);
+          uint32_t* vw = reinterpret_cast<uint32_t*>(&v[u]);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {  // keep dY where Y > 0 (bf16 sign bit clear, nonzero)
             const uint32_t lo = mw[i] & 0xFFFFu, hi = mw[i] >> 16;
@@ -672,17 +683,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             vw[i] &= keep;
           }
         }
-        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 4; ++i) {  // dead rows are zero: adding them changes nothing
           const float2 f2 = __bfloat1622float2(p2[i]);
           dbacc[2 * i] += f2.x;
           dbacc[2 * i + 1] += f2.y;
         }
+        const uint32_t off = static_cast<uint32_t>(c >> 3) * (kM * kAtomBytes) + (r >> 3) * 1024 +
+                             (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(sB + off) = v[u];
       }
-      const uint32_t off = static_cast<uint32_t>(c >> 3) * (kM * kAtomBytes) + (r >> 3) * 1024 +
-                           (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4);
-      *reinterpret_cast<uint4*>(sB + off) = v;
     }
     if (a_saved) {
       mbar_wait(lbar, lphase);
