@@ -1134,15 +1134,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nr = rem <= 0 ? 0 : (rem >= rpw ? rpw : static_cast<int>(rem));
       const int32_t ip = (ph == 0 && lane <= nr && nr > 0) ? __ldg(indptr + rbase + lane) : 0;
       hid_build_half<DMAX>(ph, idx, yp, yp_ld8, ip, rbase, nr, rpw, warp, lane, col, sA);
-      for (int r = tid / cpr; r < R; r += rstep) {
-        const int64_t row = tile * R + r;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (row < n_dst) {
-          v = load_dy8(dy, dy_f32, row, dy_ld, c);
+      // four of the thread's rows at a time: all their loads first, then mask / dZ out / sums
+      for (int r0 = tid / cpr; r0 < R; r0 += 4 * rstep) {
+        uint4 v[4], m[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = r0 + u * rstep;
+          const int64_t row = tile * R + r;
+          const bool live = r < R && row < n_dst;
+          v[u] = live ? load_dy8(dy, dy_f32, row, dy_ld, c) : make_uint4(0u, 0u, 0u, 0u);
+          m[u] = (live && y) ? __ldg(reinterpret_cast<const uint4*>(y + row * y_ld) + c)
+                             : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = r0 + u * rstep;
+          if (r >= R) break;
+          const int64_t row = tile * R + r;
           if (y) {
-            const uint4 m = __ldg(reinterpret_cast<const uint4*>(y + row * y_ld) + c);
-            const uint32_t* mw = reinterpret_cast<const uint32_t*>(&m);
-            uint32_t* vw = reinterpret_cast<uint32_t*>(&v);
+            const uint32_t* mw = reinterpret_cast<const uint32_t*>(&m[u]);
+            uint32_t* vw = reinterpret_cast<uint32_t*>(&v[u]);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {  // keep dY where Y > 0 (bf16 sign bit clear, nonzero)
               const uint32_t lo = mw[i] & 0xFFFFu, hi = mw[i] >> 16;
@@ -1151,10 +1162,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               vw[i] &= keep;
             }
           }
-          if (ph == 0) {
+          if (ph == 0 && row < n_dst) {
             if (dz_out)  // the masked dZ, the A operand of the input-gradient GEMMs (R32)
-              *reinterpret_cast<uint4*>(dz_out + row * dz_ld + c * 8) = v;
-            const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+              *reinterpret_cast<uint4*>(dz_out + row * dz_ld + c * 8) = v[u];
+            const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const float2 f2 = __bfloat1622float2(p2[i]);
@@ -1162,10 +1173,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               dbacc[2 * i + 1] += f2.y;
             }
           }
+          const uint32_t off = static_cast<uint32_t>(c >> 3) * (kM * kAtomBytes) + (r >> 3) * 1024 +
+                               (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4);
+          *reinterpret_cast<uint4*>(sB + off) = v[u];
         }
-        const uint32_t off = static_cast<uint32_t>(c >> 3) * (kM * kAtomBytes) + (r >> 3) * 1024 +
-                             (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4);
-        *reinterpret_cast<uint4*>(sB + off) = v;
       }
       fence_async_smem();
       __syncthreads();
