@@ -368,6 +368,7 @@ def test_mean_backward_parity(name, factor, F, ld):
     ("arxiv", None, 1, 256, 256, 256, True),
     ("products", None, 1, 256, 256, 256, True),    # full-size layer 2: 16K dst rows
     ("products", None, 0, 256, 256, 64, True),     # full-size layer 3: 1024 roots, 32-row tiles
+    ("arxiv", None, 0, 128, 128, 128, True),       # fp32 dY (as the training step passes it)
 ])
 def test_hidden_backward_parity(name, factor, hop, fin, ld, fo, relu):
     """Weight gradients of a hidden layer (R31) on a sampled batch's hop against
@@ -397,6 +398,8 @@ def test_hidden_backward_parity(name, factor, hop, fin, ld, fo, relu):
     layer = cmb.SageLayer(torch.zeros(fin, fo), torch.zeros(fin, fo), relu=relu, out_bf16=True,
                           hidden=True)
     dz_d = torch.full((sampler.n_cap[hop], fo), float("nan"), dtype=torch.bfloat16, device="cuda")
+    if name == "arxiv" and hop == 0:   # the fp32 dY path: the same (bf16-exact) values in fp32
+        dy_d = dy_d.float()
     dws, dwn, db = sampler.sage_hidden_backward(layer, hop, yp.cuda(), dy_d, y_d, dz_out=dz_d)
     torch.cuda.synchronize()
     assert sampler.status() == 0
@@ -429,8 +432,30 @@ def test_hidden_backward_errors():
 
 
 # ---------------------------------------------------------------- hidden input gradient (R32)
+class _TLayer:
+    """Only what sage_hidden_input_grad needs, for widths the hidden forward does not take
+    (in_dim not a multiple of 64): the transposed image packed by cmb_sage_hidden_pack_weights_t."""
+
+    def __init__(self, ws, wn):
+        import ctypes
+        self.hidden, self.feat_dim, self.out_dim = True, int(ws.shape[0]), int(ws.shape[1])
+        self.device = torch.device("cuda")
+        self.w_self, self.w_neigh = ws.cuda().contiguous(), wn.cuda().contiguous()
+        n = cmb.lib().cmb_sage_hidden_weights_t_bytes(self.feat_dim, self.out_dim)
+        assert n > 0
+        self._wt = torch.zeros(n, dtype=torch.uint8, device="cuda")
+        assert cmb.lib().cmb_sage_hidden_pack_weights_t(
+            ctypes.c_void_p(self.w_self.data_ptr()), ctypes.c_void_p(self.w_neigh.data_ptr()),
+            self.feat_dim, self.out_dim, ctypes.c_void_p(self._wt.data_ptr()), n, None) == 0
+
+    def transposed_image(self):
+        return self._wt
+
+
 @pytest.mark.parametrize("name,factor,hop,fin,fo", [
     ("tiny", None, 0, 64, 64),
+    ("tiny", None, 1, 192, 32),          # K = 32 padded to one 64-column atom (zero columns)
+    ("products", 0.01, 1, 48, 16),       # N = 48 (not a multiple of 64), K = 16
     ("products", 0.01, 1, 256, 256),     # layer 2's input gradient at the paper's widths
     ("products", 0.01, 0, 128, 64),      # layer 3 (1024-root batches scaled down)
     ("arxiv", None, 1, 256, 256),
@@ -455,7 +480,7 @@ def test_hidden_input_grad_parity(name, factor, hop, fin, fo):
     ld = ((fo + 63) // 64) * 64
     dz_d = torch.zeros(sampler.n_cap[hop], ld, dtype=torch.bfloat16, device="cuda")
     dz_d[:nd, :fo] = dZ.cuda()
-    layer = cmb.SageLayer(ws, wn, hidden=True)
+    layer = cmb.SageLayer(ws, wn, hidden=True) if fin % 64 == 0 else _TLayer(ws, wn)
     dx = torch.full((sampler.n_cap[hop + 1], fin), float("nan"), device="cuda")
     sampler.sage_hidden_input_grad(layer, hop, dz_d, dx)
     torch.cuda.synchronize()
