@@ -928,7 +928,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const uint4* __restrict__ yp, int64_t yp_ld8, int kin,
                   const uint4* __restrict__ w_img, const float* __restrict__ bias, int fo,
                   int tmem_cols, int relu, int out_bf16, void* __restrict__ out, int64_t out_ld,
-                  int rows_per_tile, int halves = 2) {
+                  int rows_per_tile, int halves = 2, void* __restrict__ out2 = nullptr,
+                  int64_t out2_ld = 0) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   const uint32_t abytes = static_cast<uint32_t>(kin) * kM * kAtomBytes;
@@ -978,22 +979,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     // phase 0 = the neighbour half (A = bf16 neighbour means, W half 1), phase 1 = the self half
     // (A = the dst rows of Yp, W half 0); each W half is bulk-copied from L2 while A is built
     const int32_t ip = (lane <= nr && nr > 0) ? __ldg(indptr + rbase + lane) : 0;
-    // halves == 1: the self phase only, against the image's first half (input gradients, R32)
+    // halves == 1: the self phase only, against the image's first half (input gradients, R32);
+    // dual (halves == 1, out2 != NULL): A = the self rows built once, multiplied by the image's
+    // first half into TMEM columns [0, fo) and by its second half into [fo, 2 fo) -> out, out2
     const int ph0 = halves == 1 ? 1 : 0;
-    for (int ph = ph0; ph < 2; ++ph) {
-      if (tid == 0) bulk_g2s(saddr(sW), w_img + (ph == 0 ? wbytes / 16 : 0), wbytes, wbar);
-      hid_build_half<DMAX>(ph, idx, yp, yp_ld8, ip, rbase, nr, rpw, warp, lane, col, sA);
+    const bool dual = halves == 1 && out2 != nullptr;
+    for (int k = 0; k < (dual ? 2 : 2 - ph0); ++k) {
+      const int ph = dual ? 1 : ph0 + k;
+      const int whalf = dual ? k : (ph == 0 ? 1 : 0);
+      if (tid == 0) bulk_g2s(saddr(sW), w_img + whalf * (wbytes / 16), wbytes, wbar);
+      if (!(dual && k == 1))
+        hid_build_half<DMAX>(ph, idx, yp, yp_ld8, ip, rbase, nr, rpw, warp, lane, col, sA);
       fence_async_smem();
       __syncthreads();
       if (tid == 0) {
         mbar_wait(wbar, wphase);
         tc_fence_after();
+        const uint32_t dcol = dual ? static_cast<uint32_t>(k * fo) : 0u;
         for (int st = 0; st < kin * 4; ++st) {
           const uint32_t atom = static_cast<uint32_t>(st >> 2);
           const uint32_t koff = static_cast<uint32_t>(st & 3) * 32u;
-          mma_bf16(tmem, sw128_desc(sA_addr + atom * (kM * kAtomBytes) + koff),
+          mma_bf16(tmem + dcol, sw128_desc(sA_addr + atom * (kM * kAtomBytes) + koff),
                    sw128_desc(sW_addr + atom * (fo * kAtomBytes) + koff), idesc,
-                   (ph > ph0 || st > 0) ? 1u : 0u);
+                   ((!dual && ph > ph0) || st > 0) ? 1u : 0u);
         }
         mma_commit(saddr(bar));
       }
@@ -1003,14 +1011,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       __syncthreads();
     }
-    // ---- epilogue (as the first layer's)
-    {
+    // ---- epilogue (as the first layer's; dual: both accumulators, to out and out2)
+    for (int qo = 0; qo < (dual ? 2 : 1); ++qo) {
+      void* const dst = qo ? out2 : out;
+      const int64_t dst_ld = qo ? out2_ld : out_ld;
       const int q = warp & 3;
       const int64_t row = tile * R + q * 32 + lane;
       const bool live = q * 32 + lane < R && row < n_dst;
       for (int ch = warp >> 2; ch < fo / 16; ch += kWarps / 4) {
         uint32_t v[16];
-        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(ch * 16), v);
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) +
+                      static_cast<uint32_t>(qo * fo + ch * 16), v);
         tmem_ld_wait();
         float y[16];
 #pragma unroll
@@ -1020,7 +1031,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (live) {
           if (out_bf16) {
-            uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + row * out_ld +
+            uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(dst) + row * dst_ld +
                                                 ch * 16);
             uint32_t p[8];
 #pragma unroll
@@ -1031,7 +1042,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             st16_hint(o, make_uint4(p[0], p[1], p[2], p[3]), pol_stream);
             st16_hint(o + 1, make_uint4(p[4], p[5], p[6], p[7]), pol_stream);
           } else {
-            uint4* o = reinterpret_cast<uint4*>(static_cast<float*>(out) + row * out_ld + ch * 16);
+            uint4* o = reinterpret_cast<uint4*>(static_cast<float*>(dst) + row * dst_ld + ch * 16);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
               st16_hint(o + i, make_uint4(__float_as_uint(y[4 * i]), __float_as_uint(y[4 * i + 1]),
@@ -1738,18 +1749,15 @@ cmb_status cmb_sage_hidden_input_grad(const cmb_blocks* b, int32_t hop, int64_t 
   while (R > 32 && (n_dst_cap + R - 1) / R < sms) R >>= 1;
   const int64_t tiles = (n_dst_cap + R - 1) / R;
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
-  const int cols = in_dim <= 32 ? 32 : in_dim <= 64 ? 64 : in_dim <= 128 ? 128 : 256;
+  int cols = 32;  // two accumulators of in_dim columns each
+  while (cols < 2 * in_dim) cols <<= 1;
   const size_t smem = sl::hid_smem_bytes(kt, in_dim);
-  const uint4* wt = static_cast<const uint4*>(wt_img);
-  const size_t half16 = sl::w_img_bytes(kt, in_dim, 1) / 16;
-  // dX[d] = dZ[d] W_self^T for d < n_dst (stored); dH = dZ W_neigh^T; dX += M^T dH (R30)
+  // dX[d] = dZ[d] W_self^T for d < n_dst (stored) and dH = dZ W_neigh^T in ONE launch (A = dZ
+  // staged once, the two image halves into two TMEM accumulators); then dX += M^T dH (R30)
   sl::k_sage_hidden<8><<<grid, sl::kThreads, smem, s>>>(
       b->indptr[hop], b->indices[hop], b->sizes + hop, n_dst_cap, static_cast<const uint4*>(dz),
-      dz_ld / 8, kt, wt, nullptr, in_dim, cols, 0, 0, dx, dx_ld, R, 1);
-  CMB_CUDA(cudaGetLastError());
-  sl::k_sage_hidden<8><<<grid, sl::kThreads, smem, s>>>(
-      b->indptr[hop], b->indices[hop], b->sizes + hop, n_dst_cap, static_cast<const uint4*>(dz),
-      dz_ld / 8, kt, wt + half16, nullptr, in_dim, cols, 0, 0, dh, dh_ld, R, 1);
+      dz_ld / 8, kt, static_cast<const uint4*>(wt_img), nullptr, in_dim, cols, 0, 0, dx, dx_ld, R,
+      1, dh, dh_ld);
   CMB_CUDA(cudaGetLastError());
   const int64_t want = (n_dst_cap + 7) / 8;
   const int mgrid = static_cast<int>(want < 8ll * sms ? want : 8ll * sms);

@@ -14,7 +14,6 @@
 namespace cmb {
 namespace tr {
 
-constexpr int kXentThreads = 1024;
 constexpr unsigned kFull = 0xffffffffu;
 
 // R33: for root i < n (label_i = node_labels[nodes[i]]; the roots are the prefix of `nodes`),
@@ -22,8 +21,7 @@ constexpr unsigned kFull = 0xffffffffu;
 //     dY[i, c] = (exp(Y[i, c] - lse_i) - 1[c == label_i]) / n     (c < C; columns C.. of dY = 0).
 // k_xent_rows: one warp per root (a row is one latency chain: loads, max and sum shuffles, log),
 // lane j owning columns j, j + 32, ... (C <= 256); the row's loss term goes to row_loss[i] (fp64).
-// k_xent_sum: one block sums row_loss in a fixed order (thread t: rows t, t + 1024, ... in
-// order; then the 1024 partials in order by thread 0) -- deterministic.  A label outside [0, C)
+// k_xent_sum: one block sums row_loss in a fixed order (below) -- deterministic.  A label outside [0, C)
 // sets the status word (CMB_ERR_INVALID_ARGUMENT); that row contributes nothing.
 constexpr int kRowWarps = 8;
 __global__ void __launch_bounds__(kRowWarps * 32)
@@ -73,18 +71,23 @@ __global__ void __launch_bounds__(kRowWarps * 32)
   }
 }
 
-__global__ void __launch_bounds__(kXentThreads)
+constexpr int kSumThreads = 256;
+__global__ void __launch_bounds__(kSumThreads)
     k_xent_sum(const double* __restrict__ row_loss, const int64_t* __restrict__ n_dev,
                int64_t n_cap, double* __restrict__ loss) {
-  __shared__ double part[kXentThreads];
+  // fixed order: thread t adds rows t, t + 256, ... in order; a fixed xor-shuffle tree per warp;
+  // thread 0 adds the 8 warp sums in warp order (deterministic, no serial 1024-term loop)
+  __shared__ double wsum[kSumThreads / 32];
   const int64_t n = min(*n_dev, n_cap);
   double t = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += kXentThreads) t += row_loss[i];
-  part[threadIdx.x] = t;
+  for (int64_t i = threadIdx.x; i < n; i += kSumThreads) t += row_loss[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = t;
   __syncthreads();
   if (threadIdx.x == 0) {
     double a = 0.0;
-    for (int w = 0; w < kXentThreads; ++w) a += part[w];
+    for (int w = 0; w < kSumThreads / 32; ++w) a += wsum[w];
     *loss = n > 0 ? a / static_cast<double>(n) : 0.0;
   }
 }
@@ -192,7 +195,7 @@ cmb_status cmb_softmax_xent(const float* logits, int64_t ld, const int32_t* node
                                                   dy_ld, dy_cols, row_loss, status);
     CMB_CUDA(cudaGetLastError());
   }
-  tr::k_xent_sum<<<1, tr::kXentThreads, 0, s>>>(row_loss, n_dev, n_cap, loss);
+  tr::k_xent_sum<<<1, tr::kSumThreads, 0, s>>>(row_loss, n_dev, n_cap, loss);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
 }
