@@ -25,7 +25,7 @@ from typing import List, Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcmb.so")
+LIB_PATH = os.environ.get("CMB_LIB_PATH") or os.path.join(_HERE, "libcmb.so")  # override: A/B builds
 MAX_HOPS = 8
 MAX_FANOUT = 32
 

@@ -92,9 +92,16 @@ __global__ void k_gather_scalar(const float* __restrict__ x, int64_t ld,
 // L2 cache-policy hints (createpolicy): feature rows are loaded evict_last (a row referenced
 // by several dst rows of the batch should survive until its next use -- the paper's L2 reuse),
 // outputs (X_in, H) are stored evict_first (written once, never re-read by this kernel).
+// fraction of the feature-row loads marked evict_last (the rest evict_normal); 1.0 by default
+#ifndef CMB_KEEP_FRAC
+#define CMB_KEEP_FRAC 1.0
+#endif
+#define CMB_STR2(x) #x
+#define CMB_STR(x) CMB_STR2(x)
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, " CMB_STR(CMB_KEEP_FRAC) ";"
+               : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
