@@ -8,11 +8,13 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2504_18082_b200 as cmb  # noqa: E402
-from gen import CONFIGS, generate, make_labels, num_classes  # noqa: E402
+from gen import CONFIGS, generate, make_labels, num_classes, scaled  # noqa: E402
 
 
 def main():
     cfg = CONFIGS[os.environ.get("CFG", "products")]
+    if os.environ.get("SCALE"):
+        cfg = scaled(cfg, float(os.environ["SCALE"]))
     b = generate(cfg)
     g = cmb.Graph.from_bundle(b)
     C = num_classes(cfg)
@@ -22,13 +24,13 @@ def main():
     smp = pipe.sampler
     model = cmb.GraphSAGE(cfg.feat_dim, C, num_layers=len(cfg.fanouts), seed=1)
     K = int(os.environ.get("K", "20"))
-    for k in range(3):
+    for k in range(min(3, pipe.n_batches)):
         smp.sample(pipe.batch_roots(k), 0.5, 42, k)
         model.train_step(smp, labels)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for k in range(K):
-        smp.sample(pipe.batch_roots(k), 0.5, 42, k)
+        smp.sample(pipe.batch_roots(k % pipe.n_batches), 0.5, 42, k)
         model.train_step(smp, labels)
     t1 = time.perf_counter()
     torch.cuda.synchronize()
