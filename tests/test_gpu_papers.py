@@ -5,9 +5,9 @@ come from the same counter formula on the host (gen.planted.feature_rows), so X_
 X[nodes[i]] byte for byte and H must equal the oracle's CSR-order fp32 mean.
 
 * ``test_papers_scaled`` (default): 1 % of the nodes, same degree / mu / F / fanouts.
-* ``test_papers_full`` (opt-in, CMB_TEST_PAPERS=1, ~10 min of generation on the box): the full
-  111M-node, 3.2G-entry CSR -- positions beyond 2^31 exercise the int64 CSR offsets of every
-  kernel -- one batch compared in full (blocks, X_in, H)."""
+* ``test_papers_full`` (default; ~4 min, mostly generation): the full 111M-node, 3.2G-entry
+  CSR -- positions beyond 2^31 exercise the int64 CSR offsets of every kernel -- batches
+  compared in full (blocks, X_in, H).  CMB_TEST_PAPERS=0 skips it."""
 import os
 
 import numpy as np
@@ -64,8 +64,7 @@ def test_papers_scaled():
     _run(scaled(CONFIGS["papers100m"], 0.01), [(0, 0.5), (5, 1.0)])
 
 
-@pytest.mark.skipif(os.environ.get("CMB_TEST_PAPERS") != "1",
-                    reason="full papers100M generation takes ~10 min; set CMB_TEST_PAPERS=1")
+@pytest.mark.skipif(os.environ.get("CMB_TEST_PAPERS") == "0", reason="CMB_TEST_PAPERS=0")
 def test_papers_full():
     b, out = _run(CONFIGS["papers100m"], [(3, 0.5)])
     assert b.indptr[-1] > 2 ** 31  # the int64 CSR offsets are exercised

@@ -214,7 +214,9 @@ def test_arxiv_full_size():
 
 
 def test_products_full_size_launch_config():
-    """BASELINE configs[3] at full size in the bench's launch configuration."""
+    """BASELINE configs[3] at full size, one batch per sampler launch (all SMs on one batch).
+    The bench's own launch configuration (4 batches per launch) is tested batch by batch over a
+    whole epoch in test_gpu_headline.py."""
     b, prep, g = _bundle("products")
     cfg = b.cfg
     s = cmb.Sampler(g, cfg.batch_size, cfg.fanouts)
