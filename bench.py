@@ -9,11 +9,19 @@ relabel (a2, a3) and the fused input-feature gather + GraphSAGE-mean aggregation
 region and at every epoch boundary inside it (it is once per epoch).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cmb|reference]
+                  [--config products|papers100m|...] [--shard none|ipc|a2a]
   torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+
+`--gpus N` without a torchrun environment re-launches itself under
+`python -m torch.distributed.run --nproc-per-node N` (one rank per GPU, NCCL).
 
 Multi-GPU: batches are independent units (reading R22): rank r runs global
 batches r, r+N, r+2N, ... with the graph and features replicated; there is no
-per-batch collective (weak scaling).  Rank 0 prints one JSON line.
+per-batch collective (weak scaling).  `--shard ipc|a2a` row-shards the feature table
+over the ranks instead (a6, the papers100M layout of BASELINE.json configs[4]): `ipc` reads
+remote rows inside the fused gather through CUDA-IPC-mapped peer shards (NEXT-1, NVLink on a
+multi-GPU node), `a2a` exchanges ids and rows with NCCL all-to-all (shard.ShardedFeatures).
+Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -53,7 +61,41 @@ def parse():
                          "(auto: on when features + CSR < 4x L2)")
     ap.add_argument("--batches-per-launch", type=int, default=4,
                     help="batches sampled per persistent-sampler launch (1..4)")
+    ap.add_argument("--shard", default="none", choices=["none", "ipc", "a2a"],
+                    help="row-shard the feature table over the ranks (a6): ipc = one-sided "
+                         "gather of peer shards mapped by CUDA IPC, a2a = NCCL all-to-all")
+    ap.add_argument("--cpu-workers", type=int, default=0,
+                    help="threads of the batch-parallel oracle baseline (0 = all host cores)")
     return ap.parse_args()
+
+
+def relaunch(args):
+    """`--gpus N` outside a torchrun environment: start N ranks (one per GPU) under
+    torch.distributed.run on this node and return its exit status (rank 0 prints the line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def host_cpu():
+    """(logical cores, CPU model) of this host."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
 
 
 METRIC = "mini-batches/s"
@@ -193,6 +235,57 @@ def oracle_batches(bundle, mode, mix, p, seed, budget_s, max_batches=None, law=0
     return done, el, edges
 
 
+def oracle_parallel(bundle, mode, mix, p, seed, n_batches=None, budget_s=None, workers=0, law=0,
+                    first=0):
+    """Batch-parallel oracle (SURVEY.md §8(d) mode 2): consecutive batches of epoch 0 run by a
+    pool of `workers` threads, each batch the same plain single-threaded C functions (they
+    release the GIL; batches are independent by reading R11).  Stops after `n_batches`, or once
+    `budget_s` of wall time has passed.  Returns (batches, seconds, edges, threads)."""
+    from concurrent.futures import FIRST_COMPLETED, ThreadPoolExecutor, wait
+    import oracle
+    cfg = bundle.cfg
+    workers = workers or (os.cpu_count() or 1)
+    prep = oracle.graph_prep(bundle)
+    modes = {"rand": oracle.MODE_RAND, "norand": oracle.MODE_NORAND, "comm": oracle.MODE_COMM,
+             "comm_static": oracle.MODE_COMM_STATIC}
+    t0 = time.perf_counter()
+    order = oracle.order_roots(bundle.train, bundle.comm, cfg.num_communities, modes[mode], mix,
+                               seed, 0)
+    nb = (order.shape[0] + cfg.batch_size - 1) // cfg.batch_size
+    scratch = [np.full(prep.num_nodes, -1, dtype=np.int32) for _ in range(workers)]
+    free = list(range(workers))
+
+    def one(b):
+        slot = free.pop()
+        try:
+            r = oracle_step(prep, bundle, oracle.batch_roots(order, cfg.batch_size, b % nb), p,
+                            seed, b % nb, scratch[slot], law)
+            return sum(r["e"])
+        finally:
+            free.append(slot)
+
+    done = edges = 0
+    nxt = first
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        live = set()
+        while True:
+            stop = (n_batches is not None and nxt - first >= n_batches) or \
+                   (budget_s is not None and time.perf_counter() - t0 >= budget_s)
+            while not stop and len(live) < workers:
+                live.add(ex.submit(one, nxt))
+                nxt += 1
+                stop = n_batches is not None and nxt - first >= n_batches
+            if not live:
+                break
+            fin, live = wait(live, return_when=FIRST_COMPLETED)
+            for f in fin:
+                edges += f.result()
+                done += 1
+            if stop and not live:
+                break
+    return done, time.perf_counter() - t0, edges, workers
+
+
 def run_reference(args, bundle):
     import torch
     rank = int(os.environ.get("RANK", "0"))
@@ -215,21 +308,24 @@ def run_reference(args, bundle):
 
     for w in range(args.warmup):
         step(w)
-    t0 = time.perf_counter()
-    edges = 0
-    for k in range(args.steps):
-        edges += sum(step(args.warmup + k)["e"])
-    el = time.perf_counter() - t0
-    val = args.steps / el
+    # the K timed steps (one batch each) run batch-parallel over the host's cores
+    done, el, edges, workers = oracle_parallel(bundle, args.mode, args.mix, p, args.seed,
+                                               n_batches=args.steps, workers=args.cpu_workers,
+                                               law=0 if args.law == "A" else 1, first=args.warmup)
+    cores, model = host_cpu()
+    val = done / el
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "batches/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000 * el / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(args, cfg, bundle, p),
             "sampled_edges_per_s": edges / el,
-            "cpu_baseline": {"value": val, "unit": "batches/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} consecutive batches of epoch 0, one per step, "
-                                       f"single-threaded plain-C oracle (oracle/oracle.c)"},
+            "cpu_baseline": {"value": val, "unit": "batches/s", "cores": workers, "kind": "oracle",
+                             "host_cores": cores, "cpu_model": model,
+                             "sample": f"{args.steps} consecutive batches of epoch 0 (one per "
+                                       f"step), batch-parallel over {workers} threads, each batch "
+                                       f"the single-threaded plain-C oracle (oracle/oracle.c), "
+                                       f"a1 included"},
             "e2e": {"value": val, "unit": "batches/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -256,7 +352,10 @@ def workload_config(args, cfg, bundle, p, flush=False):
                       bundle.nnz * 4 / 1e6)) if flush else
                   "no flush: inputs larger than L2 (X %.0f MB, CSR %.0f MB > 126 MB)"
                   % (cfg.num_nodes * cfg.feat_ld * 4 / 1e6, bundle.nnz * 4 / 1e6),
-            "parallelism": f"dp{args.gpus} (batches round-robin over ranks, graph replicated)"}
+            "parallelism": (f"dp{int(os.environ.get('WORLD_SIZE', '1'))} (batches round-robin over "
+                            f"ranks, graph replicated" +
+                            (", features replicated)" if args.shard == "none" else
+                             f", feature rows sharded over the ranks, {args.shard} exchange)"))}
 
 
 # ------------------------------------------------------------------ gpu leg
@@ -272,26 +371,34 @@ def count_launches(fn):
     return len(ours), sorted(set(ours))
 
 
+def init_ranks():
+    """One process per GPU (torchrun environment, else a single rank): (world, rank, local,
+    backend, device).  CMB_DIST_BACKEND=gloo (+ more ranks than GPUs) only to exercise the
+    multi-rank flow on a single-GPU box."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("CMB_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1 and not dist.is_initialized():
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return world, rank, local, backend, dev
+
+
 def run_cmb(args, bundle):
     import torch
     import torch.distributed as dist
     import paper_2504_18082_b200 as cmb
     from paper_2504_18082_b200 import dist as cmb_dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # one process per GPU; CMB_DIST_BACKEND=gloo (+ more ranks than GPUs) only to exercise the
-    # multi-rank flow on a single-GPU box
-    backend = os.environ.get("CMB_DIST_BACKEND", "nccl")
-    local = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
+    world, rank, local, backend, dev = init_ranks()
     cfg = bundle.cfg
     p = cfg.p_intra if args.p is None else args.p
     L = len(cfg.fanouts)
@@ -388,11 +495,7 @@ def run_cmb(args, bundle):
         traffic = ncu_traffic(cfg.name, knob)
         cpu = None
         if world == 1:
-            done, el, ed = oracle_batches(bundle, args.mode, args.mix, p, args.seed, args.cpu_seconds,
-                                          law=0 if args.law == "A" else 1)
-            cpu = {"value": done / el, "unit": "batches/s", "cores": 1, "kind": "oracle",
-                   "sample": f"first {done} batches of epoch 0 of the same workload/knobs "
-                             f"({el:.1f} s, single-threaded plain-C oracle, a1 included)"}
+            cpu = cpu_baseline(args, bundle, p)
         value = total_batches / (ms_max * 1e-3)
         line = {
             "metric": METRIC, "value": value, "unit": "batches/s", "n_gpus": world,
@@ -420,11 +523,198 @@ def run_cmb(args, bundle):
                                     "kernels": kernel_names},
             "clocks": clk.summary(),
             "knob_points": extra,
+            "knob_pearson_time_vs_feature_bytes": knob_pearson(extra, cfg) if extra else None,
             "next4_layer": layer,
             "graph_meta": {k: (float(v) if isinstance(v, (np.floating, float)) else v)
                            for k, v in bundle.meta.items()},
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline(args, bundle, p):
+    """§8(d): the oracle as it stands, timed on this host's cores on a bounded sample of the same
+    workload -- batch-parallel over all cores (the headline `value`) and on one core."""
+    law = 0 if args.law == "A" else 1
+    d1, el1, _ = oracle_batches(bundle, args.mode, args.mix, p, args.seed, args.cpu_seconds / 3,
+                                law=law)
+    dn, eln, _, workers = oracle_parallel(bundle, args.mode, args.mix, p, args.seed,
+                                          budget_s=args.cpu_seconds, workers=args.cpu_workers,
+                                          law=law)
+    cores, model = host_cpu()
+    return {"value": dn / eln, "unit": "batches/s", "cores": workers, "kind": "oracle",
+            "host_cores": cores, "cpu_model": model,
+            "sample": f"first {dn} batches of epoch 0 of the same workload/knobs in {eln:.1f} s, "
+                      f"batch-parallel over {workers} threads, each batch the single-threaded "
+                      f"plain-C oracle (oracle/oracle.c), a1 included",
+            "single_core": {"value": d1 / el1, "unit": "batches/s", "cores": 1,
+                            "sample": f"first {d1} batches of epoch 0, one thread, {el1:.1f} s"}}
+
+
+def run_sharded(args, bundle):
+    """a6 / NEXT-1 at N ranks: the feature table row-sharded over the ranks (rank r owns rows
+    [r*S, (r+1)*S), S = ceil(N / W), generated in place on its GPU), graph replicated.  Per launch
+    group: one sampler launch for up to 4 batches, then per batch the input-feature gather +
+    aggregate from the sharded table -- `ipc`: the fused kernel reading remote rows from the
+    peers' shards mapped by CUDA IPC (cmb_gather_aggregate_sharded, no host sync, no staging);
+    `a2a`: ids and rows exchanged with NCCL all-to-all (shard.ShardedFeatures; its variable
+    splits need the counts on the host: one device->host read per batch, that arm's cost), then
+    the unfused a5 over X_in.  A spot check against the generator's row formula follows."""
+    import torch
+    import torch.distributed as dist
+    import paper_2504_18082_b200 as cmb
+    from paper_2504_18082_b200 import dist as cmb_dist
+    from paper_2504_18082_b200.shard import ShardedFeatures
+    from gen.device import feature_table
+    from gen.planted import feature_rows
+
+    world, rank, local, backend, dev = init_ranks()
+    cfg = bundle.cfg
+    p = cfg.p_intra if args.p is None else args.p
+    L, F, N, B = len(cfg.fanouts), cfg.feat_dim, cfg.num_nodes, cfg.batch_size
+    S = (N + world - 1) // world
+    r0, r1 = rank * S, min(N, (rank + 1) * S)
+    x_local = feature_table(bundle, dev, r0, r1)
+    graph = cmb.Graph.from_bundle(bundle, device=dev, validate=True, features=False)
+    G = max(1, min(args.batches_per_launch, cmb.MAX_BATCHES_PER_LAUNCH))
+    pipe = cmb.MiniBatchPipeline(graph, torch.from_numpy(bundle.train), B, cfg.fanouts,
+                                 mode=args.mode, mix=args.mix, p=p, seed=args.seed, law=args.law)
+    samplers = [pipe.sampler] + [cmb.Sampler(graph, B, cfg.fanouts) for _ in range(G - 1)]
+    nb = pipe.n_batches
+    if args.shard == "ipc":
+        table = (cmb.ShardTable.exchange(x_local, N, F, rank, world) if world > 1 else
+                 cmb.ShardTable([x_local], N, F))
+
+        def gather(s):
+            return s.gather_aggregate_sharded(table)
+    else:
+        sf = ShardedFeatures(x_local, N, F, world, rank)
+
+        def gather(s):
+            x_in, h = s.alloc_features_ld(x_local.stride(0))
+            n = int(s.sizes[L].item())   # the a2a splits need host-side counts
+            sf.gather(s.nodes, n, x_in)
+            cmb.sage_mean_aggregate(s.indptr[L - 1], s.indices[L - 1], s.sizes[L - 1:L], x_in, F,
+                                    h, n_dst_cap=s.n_cap[L - 1])
+            return x_in, h
+
+    def gbatch(t):
+        return cmb_dist.global_batch(rank, world, t)
+
+    def group(t0, cnt, ev=None):
+        ids = [gbatch(t) for t in range(t0, t0 + cnt)]
+        roots = []
+        for gb in ids:
+            e, bb = divmod(gb, nb)
+            if pipe.epoch != e:
+                roots = [r.clone() for r in roots]
+                pipe.start_epoch(e)
+            roots.append(pipe.batch_roots(bb))
+        if ev:
+            ev[0].record()
+        cmb.sample_multi(samplers[:cnt], roots, ids, p, args.seed, args.law)
+        if ev:
+            ev[1].record()
+        for i, s in enumerate(samplers[:cnt]):
+            gather(s)
+        if ev:
+            ev[2].record()
+        return samplers[:cnt]
+
+    K, W = args.steps, args.warmup
+    for t in range(0, W, G):
+        group(t, min(G, W - t))
+    torch.cuda.synchronize()
+    sizes_log = torch.zeros(K, 2 * L + 1, dtype=torch.int64, device=dev)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(0, K, G)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start.record()
+        for gi, k0 in enumerate(range(0, K, G)):
+            cnt = min(G, K - k0)
+            ss = group(W + k0, cnt, evs[gi])
+            for i, s in enumerate(ss):
+                sizes_log[k0 + i].copy_(s.sizes, non_blocking=True)
+        end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    samp = sum(e[0].elapsed_time(e[1]) for e in evs) / K
+    gat = sum(e[1].elapsed_time(e[2]) for e in evs) / K
+    sz = sizes_log.cpu().numpy()
+    n_h, e_h = sz[:, : L + 1], sz[:, L + 1:]
+    alg = float(np.mean([algorithmic_bytes(n_h[k], e_h[k], F, L) for k in range(K)]))
+    # remote share of the last batch's unique input rows (the rows read over NVLink / exchanged)
+    s_last = ss[-1]
+    nl = int(sz[K - 1, L])
+    remote = cmb_dist.remote_fraction(s_last.nodes, nl, rank, S)
+    # spot check against the generator's row formula (input generation, not the method): X_in
+    # rows byte-identical to X[nodes], H rows = fp64 mean of their X_in rows within 1e-5
+    rng = np.random.default_rng(rank)
+    x_in, h = s_last.x_in, s_last.h
+    nodes = s_last.nodes[:nl].cpu().numpy()
+    pick = rng.choice(nl, size=min(nl, 2048), replace=False)
+    ok_x = bool(np.array_equal(x_in[torch.from_numpy(pick).to(dev), :F].cpu().numpy(),
+                               feature_rows(bundle, nodes[pick])))
+    ip = s_last.indptr[L - 1][: int(sz[K - 1, L - 1]) + 1].cpu().numpy().astype(np.int64)
+    ix = s_last.indices[L - 1][: int(sz[K - 1, L + 1 + L - 1])].cpu().numpy()
+    rows = rng.choice(ip.shape[0] - 1, size=min(ip.shape[0] - 1, 256), replace=False)
+    xin_h = x_in[: nl, :F].cpu().numpy()
+    hh = h[: ip.shape[0] - 1, :F].cpu().numpy()
+    ok_h = True
+    for d in rows:
+        a, b_ = ip[d], ip[d + 1]
+        want = xin_h[ix[a:b_]].astype(np.float64).mean(0) if b_ > a else np.zeros(F)
+        scale = np.abs(xin_h[ix[a:b_]]).astype(np.float64).mean(0) if b_ > a else np.zeros(F)
+        ok_h &= bool(np.all(np.abs(hh[d] - want) <= 1e-5 * np.maximum(np.abs(want), scale) + 1e-30))
+    ok = torch.tensor([int(ok_x and ok_h)], dtype=torch.int64, device=dev)
+    ms_max, (tot_edges, tot_batches, n_ok) = cmb_dist.reduce_timing(
+        ms, [float(e_h.sum()), float(K), float(ok.item())],
+        device=dev if backend == "nccl" else None)
+    if int(n_ok) != world:
+        raise RuntimeError(f"sharded gather spot check failed on {world - int(n_ok)} rank(s)")
+    if rank == 0:
+        peak, peak_src = measured_peak_hbm()
+        achieved = alg / (gat * 1e-3) / 1e9
+        remote_bytes = remote * float(np.mean(n_h[:, L])) * 4 * F
+        line = {
+            "metric": METRIC, "value": tot_batches / (ms_max * 1e-3), "unit": "batches/s",
+            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_max / K,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": workload_config(args, cfg, bundle, p),
+            "sampled_edges_per_s": tot_edges / (ms_max * 1e-3),
+            "stage_ms_per_step": {"sample_relabel": samp, "gather_aggregate_sharded": gat},
+            "unique_input_rows_per_batch": float(n_h[:, L].mean()),
+            "roofline": {"bound": "hbm" if world == 1 else "nvlink",
+                         "kernel": ("k_gather_mean_row<ShardedRows> (cmb_gather_aggregate_sharded)"
+                                    if args.shard == "ipc" else
+                                    "NCCL all-to-all exchange + k_gather_v4 / k_scatter_rows + "
+                                    "k_gather_mean_pipe"),
+                         "achieved": achieved, "peak": peak, "peak_source": peak_src,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "algorithmic_bytes_per_launch": alg},
+            "nvlink": {"remote_row_fraction": remote,
+                       "remote_bytes_per_batch": remote_bytes,
+                       "remote_gbps": remote_bytes / (gat * 1e-3) / 1e9,
+                       "peak_gbps_per_direction_spec": 900.0,
+                       "note": "ranks on distinct GPUs read remote rows over NVLink; ranks that "
+                               "share one GPU (a functional dry run) read them from the same HBM"},
+            "spot_check": {"x_in_rows": int(pick.shape[0]), "h_rows": int(rows.shape[0]),
+                           "ok_all_ranks": True},
+            "cpu_baseline": None, "e2e": None,
+            "gpu_launches": None,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if args.shard == "ipc" and world > 1:
+        table.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -563,6 +853,18 @@ def knob_points(bundle, graph, cfg, args, K, flush=False):
                     "gather_aggregate_ms": float(np.mean(agg)),
                     "gather_aggregate_alg_gbps": float(np.mean(alg) / (np.mean(agg) * 1e-3) / 1e9)})
     return pts
+
+
+def knob_pearson(pts, cfg):
+    """The paper's correlation (§6.3): Pearson r between the per-epoch time and
+    the per-epoch input-feature volume (unique input rows x 4F bytes x batches) across the knob
+    points."""
+    t = np.array([q["ms_per_epoch"] for q in pts], dtype=np.float64)
+    x = np.array([q["unique_input_rows"] * 4 * cfg.feat_dim for q in pts], dtype=np.float64)
+    if t.shape[0] < 3 or np.std(t) == 0 or np.std(x) == 0:
+        return None
+    return {"r": float(np.corrcoef(t, x)[0, 1]), "points": int(t.shape[0]),
+            "x": "unique input-feature bytes per batch", "y": "ms per epoch (a1-a5)"}
 
 
 def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
@@ -762,14 +1064,23 @@ def main():
     args = parse()
     if args.impl == "reference" and int(os.environ.get("RANK", "0")) != 0:
         return 0  # the reference arm runs on rank 0 only; the other ranks exit without work
+    if args.impl == "cmb" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     from gen import CONFIGS, generate
     cfg = CONFIGS[args.config]
-    if os.environ.get("CMB_FEAT_LD"):  # layout experiments: feature row stride in floats
-        import dataclasses
-        cfg = dataclasses.replace(cfg, feat_ld=int(os.environ["CMB_FEAT_LD"]))
+    if args.impl == "cmb" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # ranks start together; rank 0 generates (or loads) the bundle first, the others then
+        # read the generator's on-disk cache instead of generating it concurrently
+        import torch.distributed as dist
+        world, rank = init_ranks()[:2]
+        if rank == 0:
+            generate(cfg, features=False)
+        dist.barrier()
     bundle = generate(cfg)
     if args.impl == "reference":
         return run_reference(args, bundle)
+    if args.shard != "none":
+        return run_sharded(args, bundle)
     return run_cmb(args, bundle)
 
 

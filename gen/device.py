@@ -21,13 +21,18 @@ def _shr(z: torch.Tensor, s: int) -> torch.Tensor:
     return (z >> s) & ((1 << (64 - s)) - 1)
 
 
-def device_features(cfg, device, chunk_rows: int = 1 << 20) -> torch.Tensor:
+def device_features(cfg, device, chunk_rows: int = 1 << 20, row_begin: int = 0,
+                    row_end: int = None) -> torch.Tensor:
+    """Rows [row_begin, row_end) of the table (default: all of it) -- a row shard is generated
+    in place on its own GPU."""
     n, f, ld = cfg.num_nodes, cfg.feat_dim, cfg.feat_ld
-    X = torch.zeros(n, ld, dtype=torch.float32, device=device)
+    row_end = n if row_end is None else min(n, int(row_end))
+    row_begin = min(int(row_begin), row_end)
+    X = torch.zeros(max(1, row_end - row_begin), ld, dtype=torch.float32, device=device)
     base = (cfg.gen_seed * _SM_GAMMA) % (1 << 64)
     cols = torch.arange(f, dtype=torch.int64, device=device)
-    for r0 in range(0, n, chunk_rows):
-        r1 = min(n, r0 + chunk_rows)
+    for r0 in range(row_begin, row_end, chunk_rows):
+        r1 = min(row_end, r0 + chunk_rows)
         v = torch.arange(r0, r1, dtype=torch.int64, device=device)
         z = v[:, None] * f + cols[None, :]
         z = z + _i64((base + _SM_GAMMA) % (1 << 64))
@@ -35,11 +40,16 @@ def device_features(cfg, device, chunk_rows: int = 1 << 20) -> torch.Tensor:
         z = (z ^ _shr(z, 27)) * _i64(_SM_M2)
         z = z ^ _shr(z, 31)
         k = _shr(z, 40).to(torch.float32)
-        X[r0:r1, :f] = k * (2.0 ** -23) - 1.0
+        X[r0 - row_begin:r1 - row_begin, :f] = k * (2.0 ** -23) - 1.0
     return X
 
 
-def feature_table(bundle: Bundle, device) -> torch.Tensor:
+def feature_table(bundle: Bundle, device, row_begin: int = 0, row_end: int = None) -> torch.Tensor:
+    """The bundle's feature table on `device`, or its rows [row_begin, row_end) (a shard)."""
+    n = bundle.cfg.num_nodes
+    row_end = n if row_end is None else min(n, int(row_end))
     if bundle.X is not None:
-        return torch.from_numpy(bundle.X).to(device)
-    return device_features(bundle.cfg, device)
+        if row_begin == 0 and row_end == n:
+            return torch.from_numpy(bundle.X).to(device)
+        return torch.from_numpy(bundle.X[row_begin:max(row_end, row_begin + 1)]).to(device)
+    return device_features(bundle.cfg, device, row_begin=row_begin, row_end=row_end)

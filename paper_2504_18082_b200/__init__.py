@@ -902,8 +902,14 @@ class ShardTable:
     def exchange(cls, x_local: torch.Tensor, num_nodes: int, feat_dim: int, rank: int, world: int,
                  group=None):
         """Collective: every rank exports its shard, all-gathers the handles and maps the
-        peers' shards (CUDA IPC; NVLink on a multi-GPU node)."""
+        peers' shards (CUDA IPC; NVLink on a multi-GPU node).
+
+        Ownership: the producer's stream is synchronised before the handle is published, so a
+        peer never maps a shard whose fill is still pending; every rank must keep its shard
+        allocated and unchanged until ``close()`` (a collective: it unmaps the peers' shards and
+        then waits at a barrier, so no rank returns from it while a peer may still read)."""
         import torch.distributed as tdist
+        torch.cuda.current_stream(x_local.device).synchronize()  # the shard's bytes are final
         h = (ctypes.c_char * 64)()
         off = ctypes.c_uint64()
         _check(lib().cmb_ipc_export(ctypes.c_void_p(x_local.data_ptr()), h, ctypes.byref(off)))
@@ -922,12 +928,23 @@ class ShardTable:
                                       ctypes.byref(p), ctypes.byref(b)))
             ptrs.append(int(p.value))
             bases.append(int(b.value))
-        return cls(ptrs, num_nodes, feat_dim, shard_ld=x_local.stride(0), mapped_bases=bases)
+        t = cls(ptrs, num_nodes, feat_dim, shard_ld=x_local.stride(0), mapped_bases=bases)
+        t._group, t._collective = group, True
+        return t
 
     def close(self):
+        """Unmap the peers' shards.  For a table built by ``exchange`` this is a collective:
+        the device work reading the shards is finished first, then all ranks meet at a barrier,
+        after which each owner may free or overwrite its own shard."""
+        if self._mapped or getattr(self, "_collective", False):
+            torch.cuda.synchronize()
         for b in self._mapped:
             _check(lib().cmb_ipc_close(ctypes.c_void_p(b)))
         self._mapped = []
+        if getattr(self, "_collective", False):
+            import torch.distributed as tdist
+            tdist.barrier(group=self._group)
+            self._collective = False
 
 
 def sample_multi(samplers: Sequence["Sampler"], roots: Sequence[torch.Tensor],

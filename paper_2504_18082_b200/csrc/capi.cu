@@ -1,6 +1,9 @@
 // capi.cu -- error plumbing, status queries and capacity helpers of the cmb C ABI.
 #include <cstdarg>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "common.cuh"
 
@@ -29,6 +32,21 @@ cmb_status require_sm100() {
     set_error("device %d has compute capability %d.x; this library is built for sm_100a (B200)",
               dev, major);
     return CMB_ERR_UNSUPPORTED_DEVICE;
+  }
+  return CMB_OK;
+}
+
+cmb_status ensure_dyn_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  CMB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{kernel, dev}];
+  if (have < bytes) {
+    CMB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(bytes)));
+    have = bytes;
   }
   return CMB_OK;
 }

@@ -17,6 +17,15 @@ namespace cmb {
 void set_error(const char* fmt, ...);
 cmb_status cuda_fail(cudaError_t e, const char* what);
 cmb_status require_sm100();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device setting: applied once per
+// (kernel, current device) pair, thread-safe (capi.cu).
+cmb_status ensure_dyn_smem(const void* kernel, size_t bytes);
+#define CMB_SMEM(kernel, bytes)                                                             \
+  do {                                                                                      \
+    const cmb_status st_ = ::cmb::ensure_dyn_smem(reinterpret_cast<const void*>(kernel),    \
+                                                  static_cast<size_t>(bytes));              \
+    if (st_ != CMB_OK) return st_;                                                          \
+  } while (0)
 
 #define CMB_CUDA(call)                                        \
   do {                                                        \
@@ -128,9 +137,4 @@ struct cmb_graph {
   int32_t* status;  // graph workspace header
   int device;
   int num_sms;
-  // TMA descriptor of the feature table for tile::gather4 row loads (2D: W columns x N rows,
-  // box W x 1); has_xmap = 0 when the layout does not allow it (W > 256 or unaligned)
-  alignas(64) CUtensorMap xmap;
-  int has_xmap;
-  int xmap_w;  // columns per row fetched by TMA (F rounded up to a 16-byte multiple)
 };

@@ -92,16 +92,9 @@ __global__ void k_gather_scalar(const float* __restrict__ x, int64_t ld,
 // L2 cache-policy hints (createpolicy): feature rows are loaded evict_last (a row referenced
 // by several dst rows of the batch should survive until its next use -- the paper's L2 reuse),
 // outputs (X_in, H) are stored evict_first (written once, never re-read by this kernel).
-// fraction of the feature-row loads marked evict_last (the rest evict_normal); 1.0 by default
-#ifndef CMB_KEEP_FRAC
-#define CMB_KEEP_FRAC 1.0
-#endif
-#define CMB_STR2(x) #x
-#define CMB_STR(x) CMB_STR2(x)
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, " CMB_STR(CMB_KEEP_FRAC) ";"
-               : "=l"(p));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -129,15 +122,12 @@ __global__ void __launch_bounds__(256, (LPR == 16 && NV == 2 && CH == 2) ? 4 : 1
     const int32_t* __restrict__ gid, const int64_t* __restrict__ n_dst_dev, int64_t n_dst_cap,
     const float4* __restrict__ src, int64_t src_ld4, const int32_t* __restrict__ map, int f4,
     float4* __restrict__ out, int64_t out_ld4, float4* __restrict__ x_in, int64_t x_in_ld4,
-    const uint32_t* __restrict__ new_mask, int hint) {
+    const uint32_t* __restrict__ new_mask) {
   constexpr unsigned kFull = 0xffffffffu;
   constexpr int GPW = 32 / LPR;  // lane groups (dst rows) per warp
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
-  auto LD = [&](const float4* p) { return hint ? ldg4_hint(p, pol_keep) : ldg4(p); };
-  auto ST = [&](float4* p, const float4& v) {
-    if (hint) st4_hint(p, v, pol_stream);
-    else *p = v;
-  };
+  auto LD = [&](const float4* p) { return ldg4_hint(p, pol_keep); };
+  auto ST = [&](float4* p, const float4& v) { st4_hint(p, v, pol_stream); };
   const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
   const int lane = threadIdx.x % LPR;
   // Warp-uniform walk: the GPW groups of a warp take rows rb + q (q = group in the warp) and all
@@ -256,7 +246,6 @@ __global__ void __launch_bounds__(256, (LPR == 16 && NV == 2 && CH == 2) ? 4 : 1
 }  // namespace
 }  // namespace cmb
 
-#include "gather_tma.cuh"
 #include "gather_row.cuh"
 #include "cache.cuh"
 
@@ -333,20 +322,6 @@ cmb_status gather_dispatch(const float* x, int64_t ld, int f, const int32_t* ids
   return CMB_OK;
 }
 
-// CMB_AGG_KERNEL selects the fused a4+a5 form for A/B runs: unset / w = warp per row
-// (gather_row.cuh, the default), p = the 16-lane pipelined form, g = TMA tile::gather4
-// (gather_tma.cuh).  All compute identical bytes.
-int agg_kernel_form() {
-  static const int v = [] {
-    const char* e = std::getenv("CMB_AGG_KERNEL");
-    if (e && e[0] == 'p') return 3;
-    if (e && e[0] == 'g') return 5;
-    if (e && e[0] == 'w') return 7;
-    return 0;
-  }();
-  return v;
-}
-
 template <int LPR, int NV, int CH>
 void launch_mean(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
                  const int32_t* gid, const int64_t* n_dev, int64_t n_cap, const float* src,
@@ -356,22 +331,12 @@ void launch_mean(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* 
   // pipelined row form: a persistent-style grid (a few blocks per SM, grid-stride rows) so
   // every group walks many rows and its look-ahead pipeline stays full
   int64_t want = (n_cap + gpb - 1) / gpb;
-  // CMB_AGG_BLOCKS_PER_SM caps the grid so the kernel can share the SMs with a concurrently
-  // running sampler of the next batch (overlapped pipeline)
-  static const int bps = [] {
-    const char* e = std::getenv("CMB_AGG_BLOCKS_PER_SM");
-    return e ? std::atoi(e) : 8;
-  }();
-  const int64_t cap_grid = static_cast<int64_t>(sms) * (bps > 0 ? bps : 8);
+  const int64_t cap_grid = static_cast<int64_t>(sms) * 8;
   const int grid = static_cast<int>(want < cap_grid ? (want > 0 ? want : 1) : cap_grid);
-  static const int hint = [] {  // CMB_AGG_HINT=0 disables the L2 cache-policy hints
-    const char* e = std::getenv("CMB_AGG_HINT");
-    return e ? std::atoi(e) : 1;
-  }();
   k_gather_mean_pipe<LPR, NV, CH><<<grid, 256, 0, s>>>(
       indptr, idx, gid, n_dev, n_cap, reinterpret_cast<const float4*>(src), src_ld / 4, map, f4,
       reinterpret_cast<float4*>(out), out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4,
-      mask, hint);
+      mask);
 }
 
 // the default fused form: one warp per dst row (gather_row.cuh).  DMAX = edge rows issued per
@@ -382,36 +347,20 @@ cmb_status launch_row(int sms, cudaStream_t s, const int32_t* indptr, const int3
                       const int32_t* gid, const int64_t* n_dev, int64_t n_cap, const Rows& rows,
                       const int32_t* map, int f4, float* out, int64_t out_ld, float* x_in,
                       int64_t x_in_ld, const uint32_t* mask, int deg_hint) {
-  static const int dmax_env = [] {
-    const char* e = std::getenv("CMB_ROW_DMAX");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int dmax = dmax_env > 0 ? dmax_env : (deg_hint < 6 ? deg_hint : 6);
-  static const int bps = [] {  // 4 resident 256-thread blocks per SM (64 registers)
-    const char* e = std::getenv("CMB_AGG_BLOCKS_PER_SM");
-    return e ? std::atoi(e) : 4;
-  }();
+  const int dmax = deg_hint < 6 ? deg_hint : 6;
   const int64_t want = (n_cap + 7) / 8;  // 8 warps (rows) per 256-thread block
-  const int64_t cap = static_cast<int64_t>(sms) * (bps > 0 ? bps : 8);
+  const int64_t cap = static_cast<int64_t>(sms) * 4;  // 4 resident blocks per SM (64 registers)
   const int grid = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
-  static const int minb = [] {
-    const char* e = std::getenv("CMB_ROW_MINB");
-    return e ? std::atoi(e) : 4;
-  }();
 #define CMB_ROWK(D_)                                                                          \
-  if (minb == 5) CMB_ROWK2(D_, 5); else CMB_ROWK2(D_, 4)
-#define CMB_ROWK2(D_, M_)                                                                     \
-  if (f4 > 32) CMB_ROWK3(D_, M_, true); else CMB_ROWK3(D_, M_, false)
-#define CMB_ROWK3(D_, M_, W_)                                                                 \
-  k_gather_mean_row<D_, M_, W_, Rows><<<grid, 256, 0, s>>>(                                   \
+  if (f4 > 32) CMB_ROWK3(D_, true); else CMB_ROWK3(D_, false)
+#define CMB_ROWK3(D_, W_)                                                                     \
+  k_gather_mean_row<D_, 4, W_, Rows><<<grid, 256, 0, s>>>(                                    \
       indptr, idx, gid, n_dev, n_cap, rows, map, f4, reinterpret_cast<float4*>(out),          \
       out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4, mask)
   if (dmax <= 4) { CMB_ROWK(4); }
   else if (dmax <= 5) { CMB_ROWK(5); }
-  else if (dmax <= 6) { CMB_ROWK(6); }
-  else { CMB_ROWK(8); }
+  else { CMB_ROWK(6); }
 #undef CMB_ROWK
-#undef CMB_ROWK2
 #undef CMB_ROWK3
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
@@ -426,8 +375,7 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_
   const int f4 = (f + 3) / 4;
   const bool vec = aligned16(src) && aligned16(out) && src_ld % 4 == 0 && out_ld % 4 == 0 &&
                    (!x_in || (aligned16(x_in) && x_in_ld % 4 == 0));
-  const int form = agg_kernel_form();
-  if (vec && x_in && gid && (form == 0 || form == 7))
+  if (vec && x_in && gid)
     return launch_row(sms, s, indptr, idx, gid, n_dev, n_cap,
                       DenseRows{reinterpret_cast<const float4*>(src), src_ld / 4}, map, f4, out,
                       out_ld, x_in, x_in_ld, mask, deg_hint);
@@ -447,28 +395,9 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_
     case 16: CMB_MEAN(16, 1, 8); break;
     default:
       if (f4 <= 32) {
-        // default (measured best on B200, products F = 100): 16 lanes x 2 float4 per row,
-        // two dst rows per warp, 2 edges in flight per lane; env knobs for A/B runs
-        static const int ch = [] {
-          const char* e = std::getenv("CMB_AGG_CH");
-          return e ? std::atoi(e) : 2;
-        }();
-        static const int lp = [] {
-          const char* e = std::getenv("CMB_AGG_LPR");
-          return e ? std::atoi(e) : 16;
-        }();
-        if (lp == 16) {
-          if (ch == 4) CMB_MEAN(16, 2, 4);
-          else CMB_MEAN(16, 2, 2);
-        } else if (lp == 8) {
-          CMB_MEAN(8, 4, 2);
-        } else if (ch == 8) {
-          CMB_MEAN(32, 1, 8);
-        } else if (ch == 6) {
-          CMB_MEAN(32, 1, 6);
-        } else {
-          CMB_MEAN(32, 1, 4);
-        }
+        // measured best on B200 (products F = 100): 16 lanes x 2 float4 per row, two dst rows
+        // per warp, 2 edges in flight per lane
+        CMB_MEAN(16, 2, 2);
       } else if (f4 <= 64) CMB_MEAN(32, 2, 4);
       else if (f4 <= 128) CMB_MEAN(32, 4, 2);
       else CMB_MEAN(32, 5, 2);  // F = 602 -> 151 float4 = 32 x 5 (column tiles beyond)
@@ -611,46 +540,6 @@ cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t
   CMB_ARG(n_last_dst_cap <= nodes_cap, "cmb_gather_aggregate: n_last_dst_cap > nodes_cap");
   const int L = n_hops;
   const int f4 = (g->d.f + 3) / 4;
-  if (agg_kernel_form() == 5 && g->has_xmap && f4 <= 64 && (x_in_ld % 4) == 0 &&
-      (h_ld % 4) == 0 && aligned16(x_in) && aligned16(h_out)) {
-    // TMA tile::gather4 form
-    const uint32_t rb = static_cast<uint32_t>(g->xmap_w) * 4u;
-    static const int stages_env = [] {
-      const char* e = std::getenv("CMB_TMA_STAGES");
-      return e ? std::atoi(e) : 2;
-    }();
-    int stages = stages_env < 1 ? 1 : (stages_env > 8 ? 8 : stages_env);
-    while (stages > 1 && tma::smem_bytes(rb, stages) > 227 * 1024) --stages;
-    const size_t smem = tma::smem_bytes(rb, stages);
-    const void* fn = f4 <= 32 ? reinterpret_cast<const void*>(&k_gather_mean_tma<1>)
-                              : reinterpret_cast<const void*>(&k_gather_mean_tma<2>);
-    static size_t configured[2] = {0, 0};
-    int per_sm = 1;
-    if (configured[f4 > 32] < smem) {
-      CMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      configured[f4 > 32] = smem;
-    }
-    CMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, tma::kWarps * 32, smem));
-    if (per_sm < 1) per_sm = 1;
-    const int64_t windows = (n_last_dst_cap + tma::kRows - 1) / tma::kRows;
-    const int64_t want = (windows + tma::kWarps - 1) / tma::kWarps;
-    const int64_t cap = static_cast<int64_t>(g->num_sms) * per_sm;
-    const int grid = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int64_t* nd = b->sizes + (L - 1);
-    if (f4 <= 32)
-      k_gather_mean_tma<1><<<grid, tma::kWarps * 32, smem, s>>>(
-          g->xmap, stages, b->indptr[L - 1], b->indices[L - 1], b->last_src_ids, nd,
-          n_last_dst_cap, b->nodes, f4, rb, reinterpret_cast<float4*>(h_out), h_ld / 4,
-          reinterpret_cast<float4*>(x_in), x_in_ld / 4, b->new_src_mask);
-    else
-      k_gather_mean_tma<2><<<grid, tma::kWarps * 32, smem, s>>>(
-          g->xmap, stages, b->indptr[L - 1], b->indices[L - 1], b->last_src_ids, nd,
-          n_last_dst_cap, b->nodes, f4, rb, reinterpret_cast<float4*>(h_out), h_ld / 4,
-          reinterpret_cast<float4*>(x_in), x_in_ld / 4, b->new_src_mask);
-    CMB_CUDA(cudaGetLastError());
-    return CMB_OK;
-  }
   return mean_dispatch(b->indptr[L - 1], b->indices[L - 1], b->last_src_ids, b->sizes + (L - 1),
                        n_last_dst_cap, g->d.x, g->d.ld, b->nodes, g->d.f, h_out, h_ld, x_in,
                        x_in_ld, b->new_src_mask, g->num_sms, static_cast<cudaStream_t>(stream),

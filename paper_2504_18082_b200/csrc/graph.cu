@@ -33,15 +33,19 @@ __global__ void k_comm_offsets(const int32_t* __restrict__ comm, int64_t n, int3
   }
 }
 
-// Strictly ascending rows with ids in [0, n): one warp per row.
+// indptr[0] == 0, indptr[n] == nnz, rows inside [0, nnz), strictly ascending with ids in
+// [0, n): one warp per row (a row whose offsets leave [0, nnz) is flagged before any read).
 __global__ void k_validate_rows(const int64_t* __restrict__ indptr,
-                                const int32_t* __restrict__ indices, int64_t n, int32_t* status) {
+                                const int32_t* __restrict__ indices, int64_t n, int64_t nnz,
+                                int32_t* status) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (warp == 0 && lane == 0 && (indptr[0] != 0 || indptr[n] != nnz))
+    raise_status(status, CMB_ERR_INVALID_GRAPH);
   for (int64_t v = warp; v < n; v += nwarps) {
     const int64_t rs = indptr[v], re = indptr[v + 1];
-    bool bad = re < rs;
+    bool bad = re < rs || rs < 0 || re > nnz;
     for (int64_t e = rs + lane; e < re && !bad; e += 32) {
       const int32_t u = indices[e];
       bad |= (u < 0) || (u >= n) || (e + 1 < re && indices[e + 1] <= u);
@@ -90,45 +94,6 @@ GraphWs carve_graph_ws(void* base, int64_t n, int32_t ncomm, size_t* bytes) {
   return w;
 }
 
-// TMA descriptor of the feature table for tile::gather4 (cp.async.bulk.tensor.2d ... gather4):
-// a 2D fp32 tensor of ld columns x N rows, box W x 1 with W = F rounded up to a 16-byte
-// multiple (W <= 256 and W <= ld).  The L2 promotion (fetch granularity from DRAM) is
-// CMB_TMA_L2PROMO = 0 none, 64, 128 (default) or 256.  Obtained through the runtime's
-// driver entry point so the library needs no link-time libcuda.
-void make_feature_tensor_map(cmb_graph* g) {
-  const int64_t w = (g->d.f + 3) / 4 * 4;
-  if (w > 256 || w > g->d.ld || (g->d.ld * 4) % 16 != 0 ||
-      (reinterpret_cast<uintptr_t>(g->d.x) & 15) != 0)
-    return;
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-      fn == nullptr)
-    return;
-  auto encode = reinterpret_cast<CUresult(CUDAAPI*)(
-      CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
-      const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-      CUtensorMapL2promotion, CUtensorMapFloatOOBfill)>(fn);
-  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-  if (const char* e = std::getenv("CMB_TMA_L2PROMO")) {
-    const int v = std::atoi(e);
-    promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-          : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-          : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                     : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-  }
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g->d.ld), static_cast<cuuint64_t>(g->d.n)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g->d.ld) * 4};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(w), 1u};
-  const cuuint32_t estr[2] = {1u, 1u};
-  if (encode(&g->xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(g->d.x), dims,
-             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
-    g->has_xmap = 1;
-    g->xmap_w = static_cast<int>(w);
-  }
-}
-
 }  // namespace
 }  // namespace cmb
 
@@ -175,7 +140,8 @@ cmb_status cmb_load_graph(const cmb_graph_desc* d, void* stream, cmb_graph** out
                                       &w.hdr->status);
   CMB_CUDA(cudaGetLastError());
   if (d->validate) {
-    k_validate_rows<<<grid, 256, 0, s>>>(d->indptr, d->indices, d->num_nodes, &w.hdr->status);
+    k_validate_rows<<<grid, 256, 0, s>>>(d->indptr, d->indices, d->num_nodes, d->num_edges,
+                                         &w.hdr->status);
     CMB_CUDA(cudaGetLastError());
     int32_t hs = 0;
     CMB_CUDA(cudaMemcpyAsync(&hs, &w.hdr->status, 4, cudaMemcpyDeviceToHost, s));
@@ -213,9 +179,6 @@ cmb_status cmb_load_graph(const cmb_graph_desc* d, void* stream, cmb_graph** out
   g->status = &w.hdr->status;
   g->device = dev;
   g->num_sms = sms;
-  g->has_xmap = 0;
-  g->xmap_w = 0;
-  if (d->features) make_feature_tensor_map(g);
   *out = g;
   return CMB_OK;
 }

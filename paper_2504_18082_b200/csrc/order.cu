@@ -18,26 +18,34 @@
 namespace cmb {
 namespace {
 
-__global__ void k_root_keys(const int32_t* __restrict__ train, int64_t n, uint64_t seed,
-                            uint32_t epoch, uint64_t* __restrict__ keys,
+__global__ void k_root_keys(const int32_t* __restrict__ train, int64_t n, int64_t num_nodes,
+                            uint64_t seed, uint32_t epoch, uint64_t* __restrict__ keys,
                             int32_t* __restrict__ vals, int32_t* status) {
   const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t v = train[i];
-    if (i > 0 && train[i - 1] >= v) raise_status(status, CMB_ERR_INVALID_INPUT);
+    if ((i > 0 && train[i - 1] >= v) || v < 0 || v >= num_nodes)
+      raise_status(status, CMB_ERR_INVALID_INPUT);
     keys[i] = lo64(philox4x32_10(0u, static_cast<uint32_t>(v), kTagRoot << 24, epoch, k0, k1));
     vals[i] = static_cast<int32_t>(i);  // train position; ascending -> ties keep v order
   }
 }
 
+// community of train id v; an id outside [0, N) (already flagged by k_root_keys) reads node 0
+__device__ __forceinline__ int32_t comm_of(const int32_t* __restrict__ comm, int32_t v,
+                                           int64_t num_nodes) {
+  return comm[(v >= 0 && v < num_nodes) ? v : 0];
+}
+
 // flag[i] = 1 where a new training community starts (train ascending + comm
 // non-decreasing => comm[train[i]] non-decreasing).
 __global__ void k_comm_flags(const int32_t* __restrict__ train, const int32_t* __restrict__ comm,
-                             int64_t n, int32_t* __restrict__ flag) {
+                             int64_t n, int64_t num_nodes, int32_t* __restrict__ flag) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    flag[i] = (i == 0 || comm[train[i]] != comm[train[i - 1]]) ? 1 : 0;
+    flag[i] = (i == 0 || comm_of(comm, train[i], num_nodes) !=
+                             comm_of(comm, train[i - 1], num_nodes)) ? 1 : 0;
   }
 }
 
@@ -50,13 +58,13 @@ __global__ void k_comm_pad(int32_t ncomm, uint64_t* __restrict__ ckey, int32_t* 
 
 __global__ void k_comm_keys(const int32_t* __restrict__ train, const int32_t* __restrict__ comm,
                             const int32_t* __restrict__ flag, const int32_t* __restrict__ cpos,
-                            int64_t n, uint64_t seed, uint32_t epoch,
+                            int64_t n, int64_t num_nodes, uint64_t seed, uint32_t epoch,
                             uint64_t* __restrict__ ckey) {
   const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (!flag[i]) continue;
-    const int32_t c = comm[train[i]];
+    const int32_t c = comm_of(comm, train[i], num_nodes);
     ckey[cpos[i] - 1] = lo64(philox4x32_10(0u, static_cast<uint32_t>(c), kTagComm << 24, epoch,
                                            k0, k1));
   }
@@ -221,21 +229,22 @@ cmb_status cmb_order_roots(const cmb_graph* g, const int32_t* train_ids, int64_t
   const int grid = g->num_sms * 4, blk = 256;
   const int ni = static_cast<int>(n_train);
   size_t tb = w.temp_bytes;
-  k_root_keys<<<grid, blk, 0, s>>>(train_ids, n_train, seed, epoch, w.k0, w.v0, &w.hdr->status);
+  k_root_keys<<<grid, blk, 0, s>>>(train_ids, n_train, g->d.n, seed, epoch, w.k0, w.v0,
+                                   &w.hdr->status);
   CMB_CUDA(cudaGetLastError());
   // sort train positions by key(v) (stable: equal keys keep ascending v)
   CMB_CUDA(cub::DeviceRadixSort::SortPairs(w.temp, tb, w.k0, w.k1, w.v0, w.v1, ni, 0, 64, s));
   const int32_t* pos = w.v1;
   if (mode == CMB_ROOTS_COMM || mode == CMB_ROOTS_COMM_STATIC) {
     const int32_t C = g->d.ncomm;
-    k_comm_flags<<<grid, blk, 0, s>>>(train_ids, g->d.comm, n_train, w.flag);
+    k_comm_flags<<<grid, blk, 0, s>>>(train_ids, g->d.comm, n_train, g->d.n, w.flag);
     CMB_CUDA(cudaGetLastError());
     tb = w.temp_bytes;
     CMB_CUDA(cub::DeviceScan::InclusiveSum(w.temp, tb, w.flag, w.cpos, ni, s));
     if (mode == CMB_ROOTS_COMM) {
       k_comm_pad<<<ceil_div(C, blk), blk, 0, s>>>(C, w.ck0, w.cv0);
-      k_comm_keys<<<grid, blk, 0, s>>>(train_ids, g->d.comm, w.flag, w.cpos, n_train, seed,
-                                       epoch, w.ck0);
+      k_comm_keys<<<grid, blk, 0, s>>>(train_ids, g->d.comm, w.flag, w.cpos, n_train, g->d.n,
+                                       seed, epoch, w.ck0);
       CMB_CUDA(cudaGetLastError());
       tb = w.temp_bytes;
       CMB_CUDA(

@@ -1367,16 +1367,8 @@ static cmb_status layer_forward(const cmb_graph* g, const cmb_blocks* b, int32_t
   const int64_t tiles = (n_last_dst_cap + sl::kM - 1) / sl::kM;
   const int grid = static_cast<int>(tiles < g->num_sms ? tiles : g->num_sms);
   const int dmax = static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap);  // max fanout
-  static bool configured = false;
-  if (!configured) {
-    CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_layer<5, 2>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem_max)));
-    CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_layer<10, 2>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem_max)));
-    configured = true;
-  }
+  CMB_SMEM((&sl::k_sage_layer<5, 2>), smem_max);
+  CMB_SMEM((&sl::k_sage_layer<10, 2>), smem_max);
 #define CMB_LAYER_ARGS                                                                        \
   b->indptr[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,                     \
       reinterpret_cast<const float4*>(g->d.x), g->d.ld / 4, b->nodes, F, kh,                 \
@@ -1484,10 +1476,6 @@ static cmb_status layer_backward(const cmb_graph* g, const cmb_blocks* b, int32_
   const int64_t tiles = (n_last_dst_cap + sl::kM - 1) / sl::kM;
   int grid = static_cast<int>(tiles < g->num_sms ? tiles : g->num_sms);
   if (grid > sl::kMaxBwdCtas) grid = sl::kMaxBwdCtas;
-  if (const char* e = std::getenv("CMB_BWD_GRID")) {  // debugging: fewer CTAs, more tiles each
-    const int gm = std::atoi(e);
-    if (gm > 0 && gm < grid) grid = gm;
-  }
   float* part = static_cast<float*>(workspace);
   float* part_db = part + static_cast<size_t>(sl::kMaxBwdCtas) * 2 * kh * 64 * out_dim;
   if (grid > 0) {
@@ -1495,16 +1483,8 @@ static cmb_status layer_backward(const cmb_graph* g, const cmb_blocks* b, int32_
     int alloc = 32;
     while (alloc < cols) alloc <<= 1;
     const size_t smem = sl::bwd_smem_bytes(kh, out_dim);
-    static bool configured = false;
-    if (!configured) {
-      CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_layer_bwd<5, 2>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sl::bwd_smem_bytes(2, 256))));
-      CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_layer_bwd<10, 2>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sl::bwd_smem_bytes(2, 256))));
-      configured = true;
-    }
+    CMB_SMEM((&sl::k_sage_layer_bwd<5, 2>), sl::bwd_smem_bytes(2, 256));
+    CMB_SMEM((&sl::k_sage_layer_bwd<10, 2>), sl::bwd_smem_bytes(2, 256));
     const int dmax = static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap);
 #define CMB_BWD_ARGS                                                                          \
   b->indptr[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,                     \
@@ -1600,12 +1580,7 @@ cmb_status cmb_sage_hidden_forward(const cmb_blocks* b, int32_t hop, int64_t n_d
   const int kin = in_dim / 64;
   const int cols = out_dim <= 32 ? 32 : out_dim <= 64 ? 64 : out_dim <= 128 ? 128 : 256;
   const size_t smem = sl::hid_smem_bytes(kin, out_dim);
-  static bool configured = false;
-  if (!configured) {
-    CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_hidden<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sl::hid_smem_bytes(4, 256))));
-    configured = true;
-  }
+  CMB_SMEM((&sl::k_sage_hidden<8>), sl::hid_smem_bytes(4, 256));
   // fewer real rows per tile when the layer has fewer than one 128-row tile per SM
   int R = 128;
   while (R > 32 && (n_dst_cap + R - 1) / R < sms) R >>= 1;
@@ -1665,13 +1640,7 @@ cmb_status cmb_sage_hidden_backward(const cmb_blocks* b, int32_t hop, int64_t n_
   if (grid > 0) {
     int alloc = 32;
     while (alloc < (kin2 / 2) * out_dim) alloc <<= 1;
-    static bool configured = false;
-    if (!configured) {
-      CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_hidden_bwd<8>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sl::hid_bwd_smem_bytes(4, 256))));
-      configured = true;
-    }
+    CMB_SMEM((&sl::k_sage_hidden_bwd<8>), sl::hid_bwd_smem_bytes(4, 256));
     sl::k_sage_hidden_bwd<8><<<grid, sl::kThreads, sl::hid_bwd_smem_bytes(kin2, out_dim), s>>>(
         b->indptr[hop], b->indices[hop], b->sizes + hop, n_dst_cap,
         static_cast<const uint4*>(y_prev), y_prev_ld / 8, kin, dy, dy_ld, dy_f32,
@@ -1739,12 +1708,7 @@ cmb_status cmb_sage_hidden_input_grad(const cmb_blocks* b, int32_t hop, int64_t 
   int dev = 0, sms = 0;
   CMB_CUDA(cudaGetDevice(&dev));
   CMB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  static bool configured = false;
-  if (!configured) {
-    CMB_CUDA(cudaFuncSetAttribute(&sl::k_sage_hidden<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sl::hid_smem_bytes(4, 256))));
-    configured = true;
-  }
+  CMB_SMEM((&sl::k_sage_hidden<8>), sl::hid_smem_bytes(4, 256));
   int R = 128;
   while (R > 32 && (n_dst_cap + R - 1) / R < sms) R >>= 1;
   const int64_t tiles = (n_dst_cap + R - 1) / R;

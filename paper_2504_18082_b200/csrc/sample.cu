@@ -3,8 +3,6 @@
 // of sample_persist.cuh (one launch per batch, all hops, grid barriers between phases).
 #include <cub/cub.cuh>
 
-#include <cstdlib>
-
 #include "sample_dev.cuh"
 #include "sample_persist.cuh"
 
@@ -24,7 +22,6 @@ struct SampleWs {
   unsigned* tag_ctr;         // [1] batch tag of the last batch
   unsigned long long* map;   // [N] tagged dedup map
   uint32_t* scan;            // [max e_cap]
-  int64_t* pick;             // [max e_cap]
 };
 
 SampleWs carve_sample_ws(void* base, int64_t n_roots, const int32_t* fanouts, int32_t L,
@@ -43,17 +40,8 @@ SampleWs carve_sample_ws(void* base, int64_t n_roots, const int32_t* fanouts, in
   w.tag_ctr = c.take<unsigned>(1);
   w.map = c.take<unsigned long long>(static_cast<size_t>(num_nodes));
   w.scan = c.take<uint32_t>(static_cast<size_t>(max_e) + 1);
-  w.pick = c.take<int64_t>(static_cast<size_t>(max_e) + 1);
   if (bytes) *bytes = c.bytes();
   return w;
-}
-
-int sampler_threads() {
-  static const int pb = [] {
-    const char* e = std::getenv("CMB_SAMPLER_THREADS");
-    return (e && std::atoi(e) == 512) ? 512 : 1024;
-  }();
-  return pb;
 }
 
 void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t n_roots,
@@ -80,53 +68,25 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
   a.map = w.map;
   a.tag_ctr = w.tag_ctr;
   a.scan = w.scan;
-  a.pick = w.pick;
   a.pub = w.pub;
   a.bar = w.bar;
   a.prof = w.prof;
   a.status = &w.hdr->status;
-  // CMB_PICK_DEDUP=1 warp-deduplicates the first-occurrence marks with match_any before the
-  // atomics (fewer same-address atomics on hub nodes); off by default: the MATCH costs more than
-  // it saves on the products-shaped graphs (sampler 86 vs 88 us per batch)
-  static const int dedup = [] {
-    const char* e = std::getenv("CMB_PICK_DEDUP");
-    return e ? std::atoi(e) : 0;
-  }();
-  a.dedup = dedup;
   a.law = law;
-  static const int fuse = [] {  // CMB_FUSE_PICKS=0: separate coalesced picks pass (A/B knob)
-    const char* e = std::getenv("CMB_FUSE_PICKS");
-    return e ? std::atoi(e) : 1;
-  }();
-  a.fuse_picks = fuse;
-  static const int check = [] {  // CMB_MARK_CHECK (A/B knob)
-    const char* e = std::getenv("CMB_MARK_CHECK");
-    return e ? std::atoi(e) : 1;
-  }();
-  a.mark_check = check;
 }
 
+// One 1024-thread block per SM (64 registers: the whole register file), co-resident by
+// construction.  (A 512-thread form measured 101 vs 78 us per batch and was removed.)
 cmb_status launch_persistent(const cmb_graph* g, pst::PMulti& m, cudaStream_t s) {
-  const int pb = sampler_threads();
-  int grid = g->num_sms;  // one block per SM: co-resident by construction
+  constexpr int kPB = 1024;
+  int grid = g->num_sms;
   if (grid > kMaxPersistBlocks) grid = kMaxPersistBlocks;
   grid -= grid % m.nb;    // equal virtual grids per batch
   void* args[] = {&m};
-  const void* fn;
-  size_t smem;
-  if (pb == 512) {
-    fn = reinterpret_cast<const void*>(&pst::k_sample_persistent<512>);
-    smem = pst::smem_bytes<512>();
-  } else {
-    fn = reinterpret_cast<const void*>(&pst::k_sample_persistent<1024>);
-    smem = pst::smem_bytes<1024>();
-  }
-  static bool configured[2] = {false, false};
-  if (!configured[pb == 512]) {
-    CMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured[pb == 512] = true;
-  }
-  CMB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(pb), args, smem, s));
+  const void* fn = reinterpret_cast<const void*>(&pst::k_sample_persistent<kPB>);
+  const size_t smem = pst::smem_bytes<kPB>();
+  CMB_SMEM(fn, smem);
+  CMB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kPB), args, smem, s));
   return CMB_OK;
 }
 

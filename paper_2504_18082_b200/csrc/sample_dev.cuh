@@ -36,5 +36,13 @@ __device__ __forceinline__ RowInfo row_info(const DevGraph& g, int32_t v, uint32
   return r;
 }
 
+// the same for an id that may be out of [0, N) (a caller's root): such a row has no neighbours
+// (the root insertion raised CMB_ERR_INVALID_INPUT)
+__device__ __forceinline__ RowInfo row_info_checked(const DevGraph& g, int32_t v, uint32_t wi,
+                                                    uint32_t wo) {
+  if (static_cast<uint32_t>(v) >= static_cast<uint64_t>(g.n)) return RowInfo{0, 0, 0, 0, 0u, 0u};
+  return row_info(g, v, wi, wo);
+}
+
 }  // namespace smp
 }  // namespace cmb

@@ -7,17 +7,17 @@
 // by earlier batches read as empty and the map is never cleared:
 //     value = kFinal | id          node u has local id `id` (dst nodes, relabelled nodes)
 //           = kMarkerTop - e       e = smallest edge position seen so far for new node u
-// "First occurrence" is then ONE fire-and-forget 64-bit atomicMax per warp-deduplicated edge:
-// a newer tag beats a stale entry, final ids beat markers, smaller e beats larger e.
+// "First occurrence" is then ONE fire-and-forget 64-bit atomicMax per edge (skipped when the
+// entry already holds a winning value): a newer tag beats a stale entry, final ids beat markers,
+// smaller e beats larger e.
 //
 // Phases of hop h:
-//  A  [relabel(h-1)] + count + prefix + positions + picks
+//  A  [relabel(h-1)] + count + prefix + positions/picks/marks
 //     block b owns dst rows [b*R, (b+1)*R): row info cached in shared memory; counts; block scan;
 //     single-pass cross-block prefix (publish own total, add the totals of blocks < b);
 //     positions: the urn + Floyd draws of each row (one thread per row for f <= 16, G-lane
-//     groups otherwise) write the absolute CSR index of each pick; picks: one thread per pick
-//     loads indices[pos] (all random loads of the hop independent).
-//  B  mark: warp-deduplicated atomicMax(map[u], tag | kMarkerTop - e)
+//     groups otherwise); each pick loads indices[pos] right away and marks its first occurrence
+//     with atomicMax(map[u], tag | kMarkerTop - e)
 //  C  flag + prefix + assign: first occurrences (map[u] == tag | kMarkerTop - e) get
 //     id = n_h + global flag scan - 1: map[u] := tag | kFinal | id, nodes[id] := u
 // then (after the barrier) relabel(h): indices[e] := id(map[u]), fused into hop h+1's A.
@@ -63,15 +63,11 @@ struct PArgs {
   unsigned long long* map;  // [N] tagged direct dedup map (see above)
   unsigned* tag_ctr;        // [1] last batch tag used with this workspace
   uint32_t* scan;           // [max e_cap] flag << 31 | block-local inclusive flag scan
-  int64_t* pick;            // [max e_cap] absolute CSR index of each pick
   unsigned long long* pub;  // [2][kMaxBlocks] tagged block aggregates
   unsigned* bar;            // [0] arrivals, [1] generation
   uint64_t* prof;           // [kMaxBlocks][64] per-block %globaltimer at sub-step boundaries
   int32_t* status;
-  int dedup;                // warp-deduplicate the marks (match_any) before the atomics
   int law;                  // Knob-2 law: 0 = successive weighted w/o replacement, 1 = slot
-  int fuse_picks;           // load + mark each pick in the positions step (else a picks pass)
-  int mark_check;           // fused marks: load the entry first, atomic only if it can win
 };
 
 // Per-block sub-step timeline (profiling aid, one store per sub-step per block):
@@ -194,31 +190,25 @@ __device__ void phase_relabel(const PArgs& a, int h) {
 }
 
 // ---- the picks of one row: rank k (ascending position) at absolute CSR index p
-
-// PosEmit: record the CSR index (a separate picks pass loads and marks the neighbours).
-struct PosEmit {
-  int64_t* o;
-  __device__ __forceinline__ void put(int k, int64_t p) const { o[k] = p; }
-};
-// PickEmit (default): load the neighbour id right away, write it to the block and mark its
-// first occurrence -- atomicMax(map[u], tag | kMarkerTop - e), a fire-and-forget reduction;
-// final entries (roots, earlier hops) always beat markers, smaller e beats larger e.  The
-// random CSR loads then overlap with the Philox work of the other rows of the phase instead of
-// forming a pass of their own, and the pick array round trip disappears.
+// PickEmit: load the neighbour id right away, write it to the block and mark its first
+// occurrence -- atomicMax(map[u], tag | kMarkerTop - e), a fire-and-forget reduction; final
+// entries (roots, earlier hops) always beat markers, smaller e beats larger e.  The random CSR
+// loads then overlap with the Philox work of the other rows of the phase instead of forming a
+// pass of their own.  (Tried and removed: a separate coalesced picks pass through a pick-position
+// array, 91 vs 84 us per batch; warp-deduplicating the marks with match_any, 88 vs 86 us.)
 struct PickEmit {
   const int32_t* ind;
   int32_t* out;                // block indices of this row's first pick
   unsigned long long* map;
   unsigned long long tag;
   uint32_t e0;                 // absolute edge index of the row's first pick
-  int check;                   // read the entry first; skip the atomic if it cannot win
   __device__ __forceinline__ void put(int k, int64_t p) const {
     const uint32_t u = static_cast<uint32_t>(__ldg(ind + p));
     out[k] = static_cast<int32_t>(u);
     const unsigned long long m = tag | (kMarkerTop - (e0 + static_cast<uint32_t>(k)));
-    // a node picked by many rows (hubs; every pick of a community at p = 1) would otherwise
-    // queue one same-address atomic per pick in L2
-    if (!check || __ldcg(map + u) < m) atomicMax(map + u, m);
+    // read the entry first: a node picked by many rows (hubs; every pick of a community at
+    // p = 1) would otherwise queue one same-address atomic per pick in L2
+    if (__ldcg(map + u) < m) atomicMax(map + u, m);
   }
 };
 
@@ -405,7 +395,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
     int32_t v = 0;
     if (i < hi) {
       v = __ldcg(dst + i);
-      r = row_info(a.g, v, a.wi, a.wo);
+      r = row_info_checked(a.g, v, a.wi, a.wo);
       const int64_t m = r.ni_e + r.no_e;
       c = static_cast<int32_t>(m < f ? m : f);
       if (a.law == 1 && f < m) c = slot_count(v, h, f, a.wi, r.ni_e, r.no_e, a.k0, a.k1, a.batch);
@@ -447,7 +437,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       off = rc.off[k];
     } else {
       v = __ldcg(dst + i);
-      const RowInfo r = row_info(a.g, v, a.wi, a.wo);
+      const RowInfo r = row_info_checked(a.g, v, a.wi, a.wo);
       rs = r.rs;
       deg = r.deg;
       rlo = r.lo;
@@ -465,23 +455,13 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       fetch(i, v, rs, deg, rlo, rhi, off);
       a.indptr[h][i] = base + off;
       const uint32_t e0 = static_cast<uint32_t>(base + off);
-      if (a.fuse_picks) {
-        const PickEmit em{a.g.indices, a.indices[h] + e0, a.map, tag, e0, a.mark_check};
-        if (f <= 8)
-          row_positions_thread<8>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
-                                  a.law);
-        else
-          row_positions_thread<16>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch,
-                                   em, a.law);
-      } else {
-        const PosEmit em{a.pick + e0};
-        if (f <= 8)
-          row_positions_thread<8>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
-                                  a.law);
-        else
-          row_positions_thread<16>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch,
-                                   em, a.law);
-      }
+      const PickEmit em{a.g.indices, a.indices[h] + e0, a.map, tag, e0};
+      if (f <= 8)
+        row_positions_thread<8>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
+                                a.law);
+      else
+        row_positions_thread<16>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
+                                 a.law);
     }
   } else {
     const int lane = threadIdx.x & (G - 1);
@@ -494,52 +474,13 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       fetch(i, v, rs, deg, rlo, rhi, off);
       if (lane == 0) a.indptr[h][i] = base + off;
       const uint32_t e0 = static_cast<uint32_t>(base + off);
-      if (a.fuse_picks)
-        row_positions_group<G>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, lane,
-                               gmask,
-                               PickEmit{a.g.indices, a.indices[h] + e0, a.map, tag, e0,
-                                        a.mark_check},
-                               a.law);
-      else
-        row_positions_group<G>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, lane,
-                               gmask, PosEmit{a.pick + e0}, a.law);
+      row_positions_group<G>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, lane,
+                             gmask, PickEmit{a.g.indices, a.indices[h] + e0, a.map, tag, e0},
+                             a.law);
     }
   }
   __syncthreads();
   CMB_PROF(a, pk);
-  if (a.fuse_picks) return;  // picks and marks were emitted with the positions
-  // (3) picks + mark: the block's edges are the contiguous range [base, base + run); each
-  // picked neighbour u is written out and its first occurrence marked right away:
-  // warp-deduplicated atomicMax(map[u], tag | kMarkerTop - e) (fire-and-forget reductions).
-  // Final entries (roots, earlier hops) always beat markers, so no ordering is needed with
-  // the root insertion of hop 0 or across blocks.
-  const int32_t* __restrict__ ind = a.g.indices;
-  int32_t* __restrict__ out = a.indices[h];
-  const int64_t e1 = (int64_t)base + run;
-  const int lane = threadIdx.x & 31;
-  constexpr int U = 8;
-  for (int64_t w0 = base + (threadIdx.x & ~31); w0 < e1; w0 += U * PB) {  // warp-uniform
-    int64_t p[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = w0 + lane + u * PB;
-      p[u] = e < e1 ? __ldcg(a.pick + e) : 0;
-    }
-    uint32_t val[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      val[u] = (w0 + lane + u * PB < e1) ? static_cast<uint32_t>(__ldg(ind + p[u])) : kEmpty - lane;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = w0 + lane + u * PB;
-      const unsigned peers = a.dedup ? __match_any_sync(0xffffffffu, val[u]) : (1u << lane);
-      if (e < e1) {
-        out[e] = static_cast<int32_t>(val[u]);
-        if (lane == __ffs(peers) - 1)  // lowest lane = smallest e of the duplicates
-          atomicMax(a.map + val[u], tag | (kMarkerTop - static_cast<uint32_t>(e)));
-      }
-    }
-  }
 }
 
 // flags + prefix + assign
@@ -616,6 +557,11 @@ __device__ __forceinline__ void run_batch(const PArgs& a) {
   for (int64_t i = vblk() * (int64_t)PB + threadIdx.x; i < a.n_roots;
        i += (int64_t)vgrid() * PB) {
     const uint32_t u = static_cast<uint32_t>(a.roots[i]);
+    if (u >= static_cast<uint64_t>(a.g.n)) {  // out of range: error; the row samples nothing and
+      raise_status(a.status, CMB_ERR_INVALID_INPUT);  // node 0 stands in for it in the outputs, so
+      a.nodes[i] = 0;                                 // every later read stays inside the graph
+      continue;
+    }
     a.nodes[i] = static_cast<int32_t>(u);
     const unsigned long long old = atomicExch(a.map + u, tag | kFinal | static_cast<uint32_t>(i));
     // duplicate root <=> the entry already holds a final id of THIS batch (a marker of this

@@ -97,8 +97,12 @@ class ShardedFeatures:
         counts, send_ids, perm = self.ops.plan(nodes, n_dev, n_cap, self.S, self.world)
         recv_counts = torch.empty_like(counts)
         self._a2a(recv_counts, counts, [1] * self.world, [1] * self.world)
-        sc = [int(c) for c in counts.cpu().tolist()]
-        rc = [int(c) for c in recv_counts.cpu().tolist()]
+        # NCCL's all-to-all takes its variable splits on the host: ONE device->host read of both
+        # count vectors per batch is this protocol's synchronisation cost (the one-sided form,
+        # cmb_gather_aggregate_sharded, has none)
+        both = torch.cat([counts, recv_counts]).cpu().tolist()
+        sc = [int(c) for c in both[: self.world]]
+        rc = [int(c) for c in both[self.world:]]
         req = torch.empty(sum(rc), dtype=torch.int32, device=dev)
         self._a2a(req, send_ids[: sum(sc)].contiguous(), rc, sc)
         rows = torch.empty(sum(rc), self.x.stride(0), dtype=self.x.dtype, device=dev)
