@@ -286,6 +286,18 @@ CMB_API cmb_status cmb_community_order(const int64_t* indptr, const int32_t* ind
                                        size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------ step executor */
+/* a4 + a5 exactly as cmb_gather_aggregate (same results, byte for byte), the dst rows of hop
+ * L-1 visited in the order dst_order[0 .. n_{L-1}) (device int32, a permutation of
+ * [0, n_{L-1})): rows of nearby node ids processed together re-read the src rows they share
+ * while those are still in L2 (the paper's reuse mechanism).  Only the schedule
+ * changes: every X_in / H row is the one cmb_gather_aggregate writes.  Requires 16-B aligned rows
+ * (ld % 4 == 0). */
+CMB_API cmb_status cmb_gather_aggregate_ordered(const cmb_graph* g, const cmb_blocks* blocks,
+                                                int32_t n_hops, int64_t n_last_dst_cap,
+                                                int64_t nodes_cap, const int32_t* dst_order,
+                                                float* x_in, int64_t x_in_ld, float* h_out,
+                                                int64_t h_ld, void* stream);
+
 /* Where cmb_step_group writes the a4 + a5 outputs of one batch (see cmb_gather_aggregate). */
 typedef struct {
   float* x_in;
@@ -408,6 +420,18 @@ CMB_API cmb_status cmb_gcn_layer_forward(const cmb_graph* g, const cmb_blocks* b
                                          const void* w_img, const float* bias, int32_t out_dim,
                                          int32_t relu, int32_t out_bf16, void* out,
                                          int64_t out_ld, void* stream);
+/* Its weight gradients (reading R35; the chain rule on Eq. (1)):
+ * dZ = dY * 1[Y > 0] (y = the forward's bf16 output, or NULL for an identity layer),
+ * dW = (A' X_in)^T dZ -> dw fp32 [F x Fo] row-major, db = sum_d dZ[d] -> db fp32 [Fo].  The
+ * aggregate rows are rebuilt from the feature table exactly as the forward builds them (bf16),
+ * the products accumulate in fp32 on the tensor cores per CTA and the CTA partials are summed
+ * in fp64 in a fixed order (deterministic).  Arguments, limits and workspace
+ * (cmb_sage_backward_workspace_bytes) as cmb_sage_layer_backward. */
+CMB_API cmb_status cmb_gcn_layer_backward(const cmb_graph* g, const cmb_blocks* blocks,
+                                          int32_t n_hops, int64_t n_last_dst_cap, const void* dy,
+                                          int64_t dy_ld, int32_t dy_f32, const void* y,
+                                          int64_t y_ld, int32_t out_dim, float* dw, float* db,
+                                          void* workspace, size_t workspace_bytes, void* stream);
 
 /* NEXT-4 hidden layers (reading R29): layer l >= 2 of the model on hop h = L - l:
  *     Y[d] = sigma( Yp[d] W_self + mean_{e in row d of hop h} Yp[indices[h][e]] W_neigh + b ),

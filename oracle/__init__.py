@@ -287,6 +287,33 @@ def gcn_conv(indptr_h, idx, X_in, W, bias=None, relu=False) -> np.ndarray:
     return Y
 
 
+def gcn_aggregate64(indptr_h, idx, X_in) -> np.ndarray:
+    """Row d of A' X_in for the GCN form (reading R28): (X_in[d] + sum_{e in row d}
+    X_in[idx[e]]) / (deg_d + 1), fp64 -- the aggregate gcn_conv multiplies by W."""
+    ip = np.asarray(indptr_h, dtype=np.int64)
+    ix = np.asarray(idx, dtype=np.int64)
+    X = np.asarray(X_in, dtype=np.float64)
+    n_dst = ip.shape[0] - 1
+    deg = np.diff(ip)
+    S = X[:n_dst].copy()
+    np.add.at(S, np.repeat(np.arange(n_dst), deg), X[ix])
+    return S / (deg + 1.0)[:, None]
+
+
+def gcn_conv_backward(indptr_h, idx, X_in, dY, Y=None, relu=False):
+    """Weight gradients of the GCN form of the layer (NEXT-4, reading R35), fp64.
+
+    For Y = sigma(Z), Z = G W + b with G = A' X_in (gcn_conv, reading R28) and an upstream dY:
+    dZ = dY * sigma'(Z) (ReLU: 1[Y > 0] on the given Y), dW = G^T dZ, db = sum_d dZ[d, :] -- the
+    chain rule on Eq. (1); the features get no gradient.  Returns (dW, db).
+    """
+    G = gcn_aggregate64(indptr_h, idx, X_in)
+    dZ = np.asarray(dY, dtype=np.float64)
+    if relu:
+        dZ = dZ * (np.asarray(Y, dtype=np.float64) > 0)
+    return G.T @ dZ, dZ.sum(axis=0)
+
+
 def sage_mean64(indptr_h, idx, Xsrc) -> np.ndarray:
     """a5's mean (reading R12: neighbours only, 0 for an empty row) on fp64 inputs, for
     the hidden layers of the model (reading R29), whose inputs are the previous layer's outputs:

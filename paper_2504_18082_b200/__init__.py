@@ -43,7 +43,8 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sample_workspace_bytes", "cmb_sample_blocks", "cmb_sample_blocks_law",
            "cmb_sample_blocks_multi",
            "cmb_gather_features",
-           "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_shard_plan_workspace_bytes",
+           "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_gather_aggregate_ordered",
+           "cmb_shard_plan_workspace_bytes",
            "cmb_shard_plan", "cmb_gather_rows", "cmb_scatter_rows",
            "cmb_gather_aggregate_sharded", "cmb_ipc_export", "cmb_ipc_open", "cmb_ipc_close",
            "cmb_step_group", "cmb_feature_cache_bytes", "cmb_feature_cache_init",
@@ -52,6 +53,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sage_weights_bytes", "cmb_sage_pack_weights", "cmb_sage_layer_forward",
            "cmb_sage_backward_workspace_bytes", "cmb_sage_layer_backward",
            "cmb_gcn_weights_bytes", "cmb_gcn_pack_weights", "cmb_gcn_layer_forward",
+           "cmb_gcn_layer_backward",
            "cmb_sage_hidden_weights_bytes", "cmb_sage_hidden_pack_weights",
            "cmb_sage_hidden_forward", "cmb_sage_mean_backward",
            "cmb_sage_hidden_backward_workspace_bytes", "cmb_sage_hidden_backward",
@@ -163,6 +165,8 @@ def lib():
             "cmb_sage_mean_aggregate": (I32, [P, P, P, I64, P, I64, P, I32, P, I64, P]),
             "cmb_gather_aggregate": (I32, [P, ctypes.POINTER(Blocks), I32, I64, I64, P, I64, P,
                                            I64, P]),
+            "cmb_gather_aggregate_ordered": (I32, [P, ctypes.POINTER(Blocks), I32, I64, I64, P, P,
+                                                   I64, P, I64, P]),
             "cmb_shard_plan_workspace_bytes": (SZ, [I64]),
             "cmb_shard_plan": (I32, [P, P, I64, I64, I32, P, P, P, P, SZ, P]),
             "cmb_gather_rows": (I32, [P, I64, I64, I32, P, P, I64, P, I64, P]),
@@ -197,6 +201,8 @@ def lib():
                                             I32, P, I64, P]),
             "cmb_sage_layer_backward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, I64, I32, P,
                                               I64, I32, P, P, P, SZ, P]),
+            "cmb_gcn_layer_backward": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, I64, I32, P,
+                                             I64, I32, P, P, P, SZ, P]),
             "cmb_sage_hidden_backward_workspace_bytes": (SZ, [I32, I32]),
             "cmb_sage_hidden_backward": (I32, [ctypes.POINTER(Blocks), I32, I64, P, I64, I32, P,
                                                I64, I32, P, I64, I32, P, P, P, SZ, P, I64, P]),
@@ -476,9 +482,17 @@ class Sampler:
                                  device=g.device)
         return self.x_in, self.h
 
-    def gather_aggregate(self):
-        """a4 + a5 fused for the last sampled batch -> (X_in [n_L, ld], H [n_{L-1}, ld])."""
+    def gather_aggregate(self, dst_order: Optional[torch.Tensor] = None):
+        """a4 + a5 fused for the last sampled batch -> (X_in [n_L, ld], H [n_{L-1}, ld]).
+        dst_order (device int32 permutation of the n_{L-1} dst rows): the visiting order
+        (cmb_gather_aggregate_ordered); same bytes."""
         x_in, h = self.alloc_features()
+        if dst_order is not None:
+            _check(lib().cmb_gather_aggregate_ordered(
+                self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
+                self.n_cap[self.L], _ptr(dst_order), _ptr(x_in), x_in.stride(0), _ptr(h),
+                h.stride(0), _stream()))
+            return x_in, h
         _check(lib().cmb_gather_aggregate(self.graph.handle, ctypes.byref(self._blocks), self.L,
                                           self.n_cap[self.L - 1], self.n_cap[self.L], _ptr(x_in),
                                           x_in.stride(0), _ptr(h), h.stride(0), _stream()))
@@ -555,6 +569,24 @@ class Sampler:
             _ptr(layer.w_img), _ptr(layer.bias), layer.out_dim, int(layer.relu),
             int(layer.out_bf16), _ptr(out), out.stride(0), _stream()))
         return out
+
+    def gcn_layer_backward(self, layer: "GcnLayer", dy: torch.Tensor,
+                           y: Optional[torch.Tensor] = None):
+        """NEXT-4 GCN backward (R35) for the last sampled batch: dY (bf16 or fp32
+        [>= n_{L-1}, out_dim]) and, for a ReLU layer, its bf16 output Y -> (dW [F, out], db)."""
+        if dy.dtype not in (torch.bfloat16, torch.float32) or (
+                y is not None and y.dtype != torch.bfloat16):
+            raise ValueError("dy must be bf16 or fp32, y bf16")
+        F, fo = layer.feat_dim, layer.out_dim
+        ws = layer.backward_workspace()
+        dw = torch.empty(F, fo, dtype=torch.float32, device=layer.device)
+        db = torch.empty(fo, dtype=torch.float32, device=layer.device)
+        _check(lib().cmb_gcn_layer_backward(
+            self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
+            _ptr(dy), dy.stride(0), int(dy.dtype == torch.float32), _ptr(y),
+            0 if y is None else y.stride(0), fo, _ptr(dw), _ptr(db), _ptr(ws), ws.numel(),
+            _stream()))
+        return dw, db
 
     def sage_layer_backward(self, layer: "SageLayer", dy: torch.Tensor,
                             y: Optional[torch.Tensor] = None, dw: Optional[torch.Tensor] = None,
@@ -830,6 +862,15 @@ class GcnLayer:
     def alloc_out(self, rows: int) -> torch.Tensor:
         dt = torch.bfloat16 if self.out_bf16 else torch.float32
         return torch.empty(max(1, rows), self.out_dim, dtype=dt, device=self.device)
+
+    def backward_workspace(self) -> torch.Tensor:
+        if getattr(self, "_bws", None) is None:
+            n = lib().cmb_sage_backward_workspace_bytes(self.feat_dim, self.out_dim)
+            if n == 0:
+                raise ValueError(f"backward needs out_dim a power of two in [16, 256] "
+                                 f"(got {self.out_dim})")
+            self._bws = torch.empty(n, dtype=torch.uint8, device=self.device)
+        return self._bws
 
 
 class FeatureCache:

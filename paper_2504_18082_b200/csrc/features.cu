@@ -346,7 +346,8 @@ template <class Rows>
 cmb_status launch_row(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
                       const int32_t* gid, const int64_t* n_dev, int64_t n_cap, const Rows& rows,
                       const int32_t* map, int f4, float* out, int64_t out_ld, float* x_in,
-                      int64_t x_in_ld, const uint32_t* mask, int deg_hint) {
+                      int64_t x_in_ld, const uint32_t* mask, int deg_hint,
+                      const int32_t* order = nullptr) {
   const int dmax = deg_hint < 6 ? deg_hint : 6;
   const int64_t want = (n_cap + 7) / 8;  // 8 warps (rows) per 256-thread block
   const int64_t cap = static_cast<int64_t>(sms) * 4;  // 4 resident blocks per SM (64 registers)
@@ -356,7 +357,7 @@ cmb_status launch_row(int sms, cudaStream_t s, const int32_t* indptr, const int3
 #define CMB_ROWK3(D_, W_)                                                                     \
   k_gather_mean_row<D_, 4, W_, Rows><<<grid, 256, 0, s>>>(                                    \
       indptr, idx, gid, n_dev, n_cap, rows, map, f4, reinterpret_cast<float4*>(out),          \
-      out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4, mask)
+      out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4, mask, order)
   if (dmax <= 4) { CMB_ROWK(4); }
   else if (dmax <= 5) { CMB_ROWK(5); }
   else { CMB_ROWK(6); }
@@ -527,6 +528,29 @@ cmb_status cmb_cache_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, i
                     w.slot_i, (feat_dim + 3) / 4, h_out, h_ld, x_in, x_in_ld, b->new_src_mask,
                     n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
                                        : 8);
+}
+
+cmb_status cmb_gather_aggregate_ordered(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                        int64_t n_last_dst_cap, int64_t nodes_cap,
+                                        const int32_t* dst_order, float* x_in, int64_t x_in_ld,
+                                        float* h_out, int64_t h_ld, void* stream) {
+  CMB_ARG(g && b && x_in && h_out && dst_order, "cmb_gather_aggregate_ordered: null argument");
+  CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_gather_aggregate_ordered: bad n_hops");
+  CMB_ARG(g->d.x != nullptr, "cmb_gather_aggregate_ordered: graph has no feature table");
+  CMB_ARG(b->new_src_mask && b->last_src_ids,
+          "cmb_gather_aggregate_ordered: blocks->new_src_mask and last_src_ids are required");
+  CMB_ARG(x_in_ld >= g->d.f && h_ld >= g->d.f && x_in_ld % 4 == 0 && h_ld % 4 == 0 &&
+              g->d.ld % 4 == 0 && aligned16(x_in) && aligned16(h_out) && aligned16(g->d.x),
+          "cmb_gather_aggregate_ordered: rows must be 16-B aligned");
+  CMB_ARG(n_last_dst_cap <= nodes_cap, "cmb_gather_aggregate_ordered: n_last_dst_cap > nodes_cap");
+  const int L = n_hops;
+  return launch_row(g->num_sms, static_cast<cudaStream_t>(stream), b->indptr[L - 1],
+                    b->indices[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,
+                    DenseRows{reinterpret_cast<const float4*>(g->d.x), g->d.ld / 4}, b->nodes,
+                    (g->d.f + 3) / 4, h_out, h_ld, x_in, x_in_ld, b->new_src_mask,
+                    n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
+                                       : 8,
+                    dst_order);
 }
 
 cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,

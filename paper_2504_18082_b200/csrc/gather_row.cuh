@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256, MINB)
                       int64_t n_dst_cap, const __grid_constant__ Rows rows,
                       const int32_t* __restrict__ map, int f4, float4* __restrict__ out,
                       int64_t out_ld4, float4* __restrict__ x_in, int64_t x_in_ld4,
-                      const uint32_t* __restrict__ new_mask) {
+                      const uint32_t* __restrict__ new_mask, const int32_t* __restrict__ order) {
   constexpr unsigned kFull = 0xffffffffu;
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
   const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
@@ -63,14 +63,18 @@ __global__ void __launch_bounds__(256, MINB)
   const int64_t W = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
 
-  struct A { int32_t e0, e1, self; };
+  // slot k of the walk processes dst row d = order[k] (a permutation of [0, n_dst): rows of
+  // nearby ids together, so the src rows they share are re-read while still in L2) or k
+  struct A { int32_t e0, e1, self, d; };
   struct B { int32_t g, l, first; };
-  auto loadA = [&](int64_t row) {
-    A a{0, 0, 0};
-    if (row < n_dst) {
-      a.e0 = __ldg(indptr + row);
-      a.e1 = __ldg(indptr + row + 1);
-      a.self = __ldg(map + row);
+  auto loadA = [&](int64_t k) {
+    A a{0, 0, 0, 0};
+    if (k < n_dst) {
+      const int32_t d = order ? __ldg(order + k) : static_cast<int32_t>(k);
+      a.d = d;
+      a.e0 = __ldg(indptr + d);
+      a.e1 = __ldg(indptr + d + 1);
+      a.self = __ldg(map + d);
     }
     return a;
   };
@@ -128,8 +132,8 @@ __global__ void __launch_bounds__(256, MINB)
         h.z = div_small(acc.z, d, y);
         h.w = div_small(acc.w, d, y);
       }
-      st4_hint(out + row * out_ld4 + c0 + lane, h, pol_stream);
-      st4_hint(x_in + row * x_in_ld4 + c0 + lane, sv, pol_stream);
+      st4_hint(out + static_cast<int64_t>(ac.d) * out_ld4 + c0 + lane, h, pol_stream);
+      st4_hint(x_in + static_cast<int64_t>(ac.d) * x_in_ld4 + c0 + lane, sv, pol_stream);
     }
     }
     ac = an;

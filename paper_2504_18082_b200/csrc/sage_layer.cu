@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      int F, int kh, const void* __restrict__ dy, int64_t dy_ld, int dy_f32,
                      const __nv_bfloat16* __restrict__ y, int64_t y_ld, int fo, int tmem_alloc,
                      float* __restrict__ part, float* __restrict__ part_db,
-                     const uint8_t* __restrict__ a_saved = nullptr) {
+                     const uint8_t* __restrict__ a_saved = nullptr, int gcn = 0) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   uint8_t* sA = smem;
@@ -594,7 +594,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t ntiles = (n_dst + kM - 1) / kM;
   const uint64_t pol_keep = l2_evict_last();
   const int m_all = 2 * kh * 64;
-  const int nmb = m_all / kM;  // M = 128 blocks of feature rows (= kh)
+  // M = 128 blocks of feature rows (= kh); the GCN form (reading R35) has one operand half, the
+  // aggregate A'X_in in atoms [0, kh): its blocks cover them (an odd kh's last block also spans
+  // the first atom of the unused half, whose output rows are never reduced)
+  const int nmb = gcn ? (kh + 1) / 2 : m_all / kM;
 
   for (int i = tid; i < fo; i += kThreads) sdb[i] = 0.f;
   if (tid == 0) {
@@ -653,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (tid == 0)
         bulk_g2s(sA_addr, a_saved + tile * static_cast<int64_t>(a_bytes(kh)), a_bytes(kh), lbar);
     } else {
-      ga.build(tile + gridDim.x, sA, true);
+      ga.build(tile + gridDim.x, sA, true, gcn != 0);
     }
     // dZ staging, four of the thread's rows at a time: all their loads first (one round trip),
     // then mask, column sums and the swizzled shared-memory stores
@@ -770,10 +773,10 @@ __global__ void __launch_bounds__(256) k_sage_bwd_reduce(const float* __restrict
                                                          const float* __restrict__ part_db,
                                                          int nparts, int F, int kh, int fo,
                                                          float* __restrict__ dw,
-                                                         float* __restrict__ db) {
+                                                         float* __restrict__ db, int halves = 2) {
   __shared__ double red[8][32];
   const int m_all = 2 * kh * 64;
-  const int64_t nw = 2ll * F * fo;
+  const int64_t nw = static_cast<int64_t>(halves) * F * fo;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * 32 + lane;
   double s = 0.0;
@@ -1451,7 +1454,7 @@ static cmb_status layer_backward(const cmb_graph* g, const cmb_blocks* b, int32_
                                  int64_t n_last_dst_cap, const void* dy, int64_t dy_ld,
                                  int32_t dy_f32, const void* y, int64_t y_ld, int32_t out_dim,
                                  float* dw, float* db, void* workspace, size_t workspace_bytes,
-                                 void* stream, const void* a_saved) {
+                                 void* stream, const void* a_saved, int gcn = 0) {
   CMB_ARG(g && b && dy && dw && db && workspace, "cmb_sage_layer_backward: null argument");
   CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_sage_layer_backward: bad n_hops");
   CMB_ARG(g->d.x != nullptr, "cmb_sage_layer_backward: graph has no feature table");
@@ -1490,7 +1493,7 @@ static cmb_status layer_backward(const cmb_graph* g, const cmb_blocks* b, int32_
   b->indptr[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,                     \
       reinterpret_cast<const float4*>(g->d.x), g->d.ld / 4, b->nodes, F, kh,                 \
       dy, dy_ld, dy_f32, static_cast<const __nv_bfloat16*>(y), y_ld,                         \
-      out_dim, alloc, part, part_db, static_cast<const uint8_t*>(a_saved)
+      out_dim, alloc, part, part_db, static_cast<const uint8_t*>(a_saved), gcn
     if (dmax <= 5)
       sl::k_sage_layer_bwd<5, 2><<<grid, sl::kThreads, smem, s>>>(CMB_BWD_ARGS);
     else
@@ -1498,9 +1501,10 @@ static cmb_status layer_backward(const cmb_graph* g, const cmb_blocks* b, int32_
 #undef CMB_BWD_ARGS
     CMB_CUDA(cudaGetLastError());
   }
-  const int64_t nout = 2ll * F * out_dim + out_dim;
+  const int halves = gcn ? 1 : 2;
+  const int64_t nout = static_cast<int64_t>(halves) * F * out_dim + out_dim;
   sl::k_sage_bwd_reduce<<<static_cast<int>((nout + 31) / 32), 256, 0, s>>>(
-      part, part_db, grid, F, kh, out_dim, dw, db);
+      part, part_db, grid, F, kh, out_dim, dw, db, halves);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
 }
@@ -1526,6 +1530,15 @@ cmb_status cmb_sage_layer_backward_saved(const cmb_graph* g, const cmb_blocks* b
           "cmb_sage_layer_backward_saved: a_saved smaller than %zu bytes or unaligned", need);
   return layer_backward(g, b, n_hops, n_last_dst_cap, dy, dy_ld, dy_f32, y, y_ld, out_dim, dw, db,
                         workspace, workspace_bytes, stream, a_saved);
+}
+
+cmb_status cmb_gcn_layer_backward(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
+                                  int64_t n_last_dst_cap, const void* dy, int64_t dy_ld,
+                                  int32_t dy_f32, const void* y, int64_t y_ld, int32_t out_dim,
+                                  float* dw, float* db, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
+  return layer_backward(g, b, n_hops, n_last_dst_cap, dy, dy_ld, dy_f32, y, y_ld, out_dim, dw, db,
+                        workspace, workspace_bytes, stream, nullptr, 1);
 }
 
 size_t cmb_sage_hidden_weights_bytes(int32_t in_dim, int32_t out_dim) {

@@ -27,3 +27,20 @@ def test_hash_feature_values():
     assert abs(float(X[:, :F].mean())) < 0.01        # ~U[-1, 1)
     assert abs(float(X[:, :F].std()) - 1 / np.sqrt(3)) < 0.01
     assert torch.from_numpy(X).isfinite().all()
+
+
+def test_device_feature_shards_concatenate_to_the_table():
+    # bench.py --shard: rank r generates rows [r*S, (r+1)*S) in place; the shards are the table
+    from types import SimpleNamespace
+    from gen.device import feature_table
+    cfg = scaled(CONFIGS["papers100m"], 0.0002)
+    full = device_features(cfg, "cpu", chunk_rows=1000).numpy()
+    W = 3
+    S = (cfg.num_nodes + W - 1) // W
+    parts = [device_features(cfg, "cpu", chunk_rows=1000, row_begin=r * S,
+                             row_end=(r + 1) * S).numpy() for r in range(W)]
+    assert np.concatenate(parts).tobytes() == full.tobytes()
+    host = SimpleNamespace(cfg=scaled(CONFIGS["products"], 0.001), X=None)
+    host.X = make_features(host.cfg)
+    sh = feature_table(host, "cpu", 10, 25).numpy()
+    assert sh.tobytes() == host.X[10:25].tobytes()

@@ -271,6 +271,54 @@ def test_gcn_layer_parity(name, factor, fo, relu, out_bf16):
     assert np.all(err <= tol + 1e-30), float(np.max(err - tol))
 
 
+@pytest.mark.parametrize("name,factor,fo,relu", [
+    ("tiny", None, 64, True),        # F = 16: kh = 1, the M block spans an unused atom
+    ("tiny", None, 256, False),
+    ("products", 0.01, 256, True),   # F = 100: kh = 2, one M block
+    ("arxiv", None, 128, False),     # F = 128
+    ("products", None, 256, True),   # full size
+])
+def test_gcn_layer_backward_parity(name, factor, fo, relu):
+    """GCN weight gradients (reading R35) against oracle.gcn_conv_backward on the oracle's own
+    block and X_in, within the R27 bound 2^-7 |A'X|^T |dZ| (dW) and 2^-12 sum |dZ| (db)."""
+    b, prep, g = _bundle(name, factor)
+    F, L = b.cfg.feat_dim, len(b.cfg.fanouts)
+    gen = torch.Generator().manual_seed(17)
+    W = torch.randn(F, fo, generator=gen) / np.sqrt(F)
+    bias = torch.randn(fo, generator=gen) * 0.1
+    layer = cmb.GcnLayer(W, bias, relu=relu, out_bf16=True)
+    order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_COMM, 0.5,
+                               SEED, 0)
+    roots = oracle.batch_roots(order, b.cfg.batch_size, 2)
+    sampler = cmb.Sampler(g, len(roots), b.cfg.fanouts)
+    sampler.sample(torch.from_numpy(roots).cuda(), b.cfg.p_intra, SEED, 2)
+    ref = oracle.run_batch(prep, b.X, F, roots, b.cfg.fanouts, b.cfg.p_intra, SEED, 2)
+    nd = ref["n"][L - 1]
+    ip, ix = ref["indptr"][L - 1], ref["indices"][L - 1]
+    X = ref["X_in"][:, :F].astype(np.float64)
+    dY = (torch.randn(nd, fo, generator=gen) * 0.01).to(torch.bfloat16)
+    Yo = torch.from_numpy(oracle.gcn_conv(ip, ix, X, W.double().numpy(), bias.double().numpy(),
+                                          relu=True)).to(torch.bfloat16)
+    dy_d = torch.zeros(sampler.n_cap[L - 1], fo, dtype=torch.bfloat16, device="cuda")
+    dy_d[:nd] = dY.cuda()
+    y_d = None
+    if relu:
+        y_d = torch.zeros_like(dy_d)
+        y_d[:nd] = Yo.cuda()
+    dw, db = sampler.gcn_layer_backward(layer, dy_d, y_d)
+    torch.cuda.synchronize()
+    assert sampler.status() == 0
+    dZ = dY.double().numpy()
+    if relu:
+        dZ = dZ * (Yo.double().numpy() > 0)
+    rw, rb = oracle.gcn_conv_backward(ip, ix, X, dZ)
+    S = np.abs(oracle.gcn_aggregate64(ip, ix, X)).T @ np.abs(dZ)
+    err = np.abs(dw.double().cpu().numpy() - rw)
+    assert np.all(err <= 2.0 ** -7 * S + 1e-30), float(np.max(err - 2.0 ** -7 * S))
+    errb = np.abs(db.double().cpu().numpy() - rb)
+    assert np.all(errb <= 2.0 ** -12 * np.abs(dZ).sum(0) + 1e-30), float(np.max(errb))
+
+
 # ---------------------------------------------------------------- the 3-layer model (R26, R29)
 def _prop(T, ip, ix, nd):
     """Elementwise bound of a layer input error T through (self row, neighbour mean)."""

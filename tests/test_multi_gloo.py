@@ -6,6 +6,7 @@ work runs on the CPU oracle, which stands in for the GPU step here."""
 import hashlib
 import os
 import socket
+import sys
 import time
 
 import numpy as np
@@ -132,3 +133,24 @@ def test_remote_fraction_counts_foreign_rows():
     assert cmb_dist.remote_fraction(nodes, 5, 0, 10) == 3 / 5    # rows 10, 15, 19 are rank 1's
     assert cmb_dist.remote_fraction(nodes, 6, 1, 10) == 3 / 6
     assert cmb_dist.remote_fraction(nodes, 0, 0, 10) == 0.0
+
+
+def test_bench_relaunches_under_torchrun(monkeypatch):
+    """`python bench.py --gpus N` outside torchrun starts N ranks through torch.distributed.run
+    on 127.0.0.1 with the same arguments (the driver's command form)."""
+    import bench
+    seen = {}
+
+    def fake_call(cmd, env=None):
+        seen["cmd"], seen["env"] = cmd, env
+        return 0
+
+    monkeypatch.setattr(bench.subprocess, "call", fake_call)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "7"])
+    assert bench.main() == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "7"]
+    assert os.path.basename(cmd[cmd.index("--master-addr=127.0.0.1") + 2]) == "bench.py"

@@ -206,6 +206,61 @@ def test_gcn_brute_force_and_identities(tiny_prep, tiny_bundle):
         assert np.allclose(y[rows], ys, rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("relu", [False, True])
+def test_gcn_backward_matches_finite_differences(tiny_prep, tiny_bundle, relu):
+    """GCN weight gradients (reading R35) against central differences of the GCN forward oracle
+    (gcn_conv) on a real sampled block -- the transpose formula is not reused."""
+    from gen import CONFIGS
+    cfg = CONFIGS["tiny"]
+    order = oracle.order_roots(tiny_bundle.train, tiny_bundle.comm, cfg.num_communities,
+                               oracle.MODE_COMM, 0.5, 4, 0)
+    ref = oracle.run_batch(tiny_prep, tiny_bundle.X, cfg.feat_dim,
+                           oracle.batch_roots(order, cfg.batch_size, 1), cfg.fanouts,
+                           cfg.p_intra, 4, 1)
+    L = len(cfg.fanouts)
+    ip, ix, X = ref["indptr"][L - 1], ref["indices"][L - 1], ref["X_in"].astype(np.float64)
+    nd, F, Fo = ip.shape[0] - 1, cfg.feat_dim, 5
+    rng = np.random.default_rng(11)
+    W, b, Gup = rng.standard_normal((F, Fo)), rng.standard_normal(Fo), rng.standard_normal((nd, Fo))
+    Y = oracle.gcn_conv(ip, ix, X, W, b, relu=relu)
+    dW, db = oracle.gcn_conv_backward(ip, ix, X, Gup, Y, relu=relu)
+
+    def loss():
+        return float(np.sum(Gup * oracle.gcn_conv(ip, ix, X, W, b, relu=relu)))
+
+    eps = 1e-6
+    for i in range(0, F, 3):
+        for j in range(Fo):
+            W[i, j] += eps
+            lp = loss()
+            W[i, j] -= 2 * eps
+            lm = loss()
+            W[i, j] += eps
+            assert abs((lp - lm) / (2 * eps) - dW[i, j]) <= 1e-6 * (1 + abs(dW[i, j]))
+    for j in range(Fo):
+        b[j] += eps
+        lp = loss()
+        b[j] -= 2 * eps
+        lm = loss()
+        b[j] += eps
+        assert abs((lp - lm) / (2 * eps) - db[j]) <= 1e-6 * (1 + abs(db[j]))
+
+
+def test_gcn_backward_worked_example():
+    """The worked block of test_gcn_worked_example: A' X = [[2, 1], [-1, 4]].  With dY = ones:
+    dW = (A'X)^T 1 = [[1, 1, 1], [5, 5, 5]], db = [2, 2, 2].  With the ReLU outputs
+    Y = [[2, 1, 4], [0, 4, 0]] only (0, *) and (1, 1) pass: dW = [[2, 1, 2], [1, 5, 1]],
+    db = [1, 2, 1]."""
+    X = np.array([[1, 2], [-1, 4], [3, 0], [2, 1]], dtype=np.float64)
+    dW, db = oracle.gcn_conv_backward([0, 2, 2], [2, 3], X, np.ones((2, 3)))
+    assert np.array_equal(dW, np.array([[1, 1, 1], [5, 5, 5]], dtype=np.float64))
+    assert np.array_equal(db, np.array([2, 2, 2], dtype=np.float64))
+    Y = np.array([[2, 1, 4], [0, 4, 0]], dtype=np.float64)
+    dW, db = oracle.gcn_conv_backward([0, 2, 2], [2, 3], X, np.ones((2, 3)), Y, relu=True)
+    assert np.array_equal(dW, np.array([[2, 1, 2], [1, 5, 1]], dtype=np.float64))
+    assert np.array_equal(db, np.array([1, 2, 1], dtype=np.float64))
+
+
 def test_sage_mean64_matches_the_c_oracle(tiny_prep, tiny_bundle):
     """The numpy fp64 mean used for the hidden layers (R29) equals the C oracle's fp64 shadow of
     a5 on the same (fp32) inputs, including empty rows."""
