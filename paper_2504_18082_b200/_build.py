@@ -26,14 +26,18 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, out=None, defines=()):
+    """Build libcmb.so (or, for layout experiments, `out` with extra -D `defines` in its own
+    object directory; the product library is always built without them)."""
+    so = out or SO
+    if not force and not defines and so == SO and not _stale():
         return SO
-    bdir = os.path.join(HERE, "build")
+    bdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(
+        d.replace("=", "") for d in defines))
     os.makedirs(bdir, exist_ok=True)
     def one(src):
         obj = os.path.join(bdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         with open(os.path.join(bdir, src + ".ptxas.log"), "w") as fh:
             fh.write(r.stdout + r.stderr)
@@ -50,11 +54,11 @@ def build(force=False, verbose=False):
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    tmp = SO + ".tmp"
+    tmp = so + ".tmp"
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp,
                            *objs, "-lcudart"])
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, so)
+    return so
 
 
 if __name__ == "__main__":

@@ -92,6 +92,9 @@ __global__ void k_gather_scalar(const float* __restrict__ x, int64_t ld,
 // L2 cache-policy hints (createpolicy): feature rows are loaded evict_last (a row referenced
 // by several dst rows of the batch should survive until its next use -- the paper's L2 reuse),
 // outputs (X_in, H) are stored evict_first (written once, never re-read by this kernel).
+#ifndef CMB_ROW_MINB
+#define CMB_ROW_MINB 4
+#endif
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -107,6 +110,20 @@ __device__ __forceinline__ float4 ldg4_hint(const float4* p, uint64_t pol) {
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                : "l"(p), "l"(pol));
+  return r;
+}
+// predicated 16-byte load whose destination is zeroed inside the same asm block: a C
+// `pred ? load : 0` leaves a select after the load that waits on its scoreboard, which holds the
+// NEXT load's shuffle and address back until this one has returned (the row's loads then leave
+// in two round trips instead of one)
+__device__ __forceinline__ float4 ldg4_pred(const float4* p, bool pred, uint64_t pol) {
+  float4 r;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\tmov.b32 %2, 0;\n\tmov.b32 %3, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %6;\n\t}"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p), "r"(static_cast<int>(pred)), "l"(pol));
   return r;
 }
 __device__ __forceinline__ void st4_hint(float4* p, const float4& v, uint64_t pol) {
@@ -350,12 +367,14 @@ cmb_status launch_row(int sms, cudaStream_t s, const int32_t* indptr, const int3
                       const int32_t* order = nullptr) {
   const int dmax = deg_hint < 6 ? deg_hint : 6;
   const int64_t want = (n_cap + 7) / 8;  // 8 warps (rows) per 256-thread block
-  const int64_t cap = static_cast<int64_t>(sms) * 4;  // 4 resident blocks per SM (64 registers)
+  // CMB_ROW_MINB resident 256-thread blocks per SM (4: 64 registers); a compile-time constant for
+  // layout experiments (tools/), never a run-time switch
+  const int64_t cap = static_cast<int64_t>(sms) * CMB_ROW_MINB;
   const int grid = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
 #define CMB_ROWK(D_)                                                                          \
   if (f4 > 32) CMB_ROWK3(D_, true); else CMB_ROWK3(D_, false)
 #define CMB_ROWK3(D_, W_)                                                                     \
-  k_gather_mean_row<D_, 4, W_, Rows><<<grid, 256, 0, s>>>(                                    \
+  k_gather_mean_row<D_, CMB_ROW_MINB, W_, Rows><<<grid, 256, 0, s>>>(                                    \
       indptr, idx, gid, n_dev, n_cap, rows, map, f4, reinterpret_cast<float4*>(out),          \
       out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4, mask, order)
   if (dmax <= 4) { CMB_ROWK(4); }
@@ -378,7 +397,9 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_
                    (!x_in || (aligned16(x_in) && x_in_ld % 4 == 0));
   if (vec && x_in && gid)
     return launch_row(sms, s, indptr, idx, gid, n_dev, n_cap,
-                      DenseRows{reinterpret_cast<const float4*>(src), src_ld / 4}, map, f4, out,
+                      DenseRows{reinterpret_cast<const float4*>(src),
+                                static_cast<uint32_t>(src_ld / 4)},
+                      map, f4, out,
                       out_ld, x_in, x_in_ld, mask, deg_hint);
   if (!vec) {
     k_sage_mean_scalar<<<sms * 8, 256, 0, s>>>(indptr, idx, n_dev, n_cap, src, src_ld, map, f,
@@ -480,7 +501,7 @@ cmb_status cmb_gather_aggregate_sharded(const cmb_graph* g, const cmb_blocks* b,
     CMB_ARG(shards[r] && aligned16(shards[r]), "cmb_gather_aggregate_sharded: shard %d", r);
     rows.base[r] = reinterpret_cast<const float4*>(shards[r]);
   }
-  rows.ld4 = shard_ld / 4;
+  rows.ld4 = static_cast<uint32_t>(shard_ld / 4);
   rows.rows_per_shard = static_cast<uint32_t>(rows_per_shard);
   rows.inv = ((1ull << 32) + rows_per_shard - 1) / rows_per_shard;
   const int L = n_hops;
@@ -524,7 +545,8 @@ cmb_status cmb_cache_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, i
   // each edge's src node, map = slot of each node of the batch)
   return launch_row(g->num_sms, s, b->indptr[L - 1], b->indices[L - 1], w.gslot,
                     b->sizes + (L - 1), n_last_dst_cap,
-                    DenseRows{reinterpret_cast<const float4*>(c->cache_rows), c->cache_ld / 4},
+                    DenseRows{reinterpret_cast<const float4*>(c->cache_rows),
+                              static_cast<uint32_t>(c->cache_ld / 4)},
                     w.slot_i, (feat_dim + 3) / 4, h_out, h_ld, x_in, x_in_ld, b->new_src_mask,
                     n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
                                        : 8);
@@ -546,7 +568,9 @@ cmb_status cmb_gather_aggregate_ordered(const cmb_graph* g, const cmb_blocks* b,
   const int L = n_hops;
   return launch_row(g->num_sms, static_cast<cudaStream_t>(stream), b->indptr[L - 1],
                     b->indices[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,
-                    DenseRows{reinterpret_cast<const float4*>(g->d.x), g->d.ld / 4}, b->nodes,
+                    DenseRows{reinterpret_cast<const float4*>(g->d.x),
+                              static_cast<uint32_t>(g->d.ld / 4)},
+                    b->nodes,
                     (g->d.f + 3) / 4, h_out, h_ld, x_in, x_in_ld, b->new_src_mask,
                     n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
                                        : 8,

@@ -29,22 +29,22 @@ __device__ __forceinline__ float div_small(float a, float d, float y) {
 // over NVLink inside the kernel -- no staging copy, no separate collective.
 struct DenseRows {
   const float4* base;
-  int64_t ld4;
+  uint32_t ld4;  // row stride in float4 (one IMAD.WIDE.U32 per row address)
   __device__ __forceinline__ const float4* row(int32_t v) const {
-    return base + static_cast<int64_t>(v) * ld4;
+    return base + static_cast<uint64_t>(static_cast<uint32_t>(v)) * ld4;
   }
 };
 constexpr int kMaxShards = 8;
 struct ShardedRows {
   const float4* base[kMaxShards];
-  int64_t ld4;
+  uint32_t ld4;
   uint64_t inv;  // ceil(2^32 / rows_per_shard): owner = (v * inv) >> 32, at most 1 too high
   uint32_t rows_per_shard;
   __device__ __forceinline__ const float4* row(int32_t v) const {
     const uint32_t u = static_cast<uint32_t>(v);
     uint32_t r = static_cast<uint32_t>((static_cast<uint64_t>(u) * inv) >> 32);
     if (static_cast<uint64_t>(r) * rows_per_shard > u) --r;
-    return base[r] + static_cast<int64_t>(u - r * rows_per_shard) * ld4;
+    return base[r] + static_cast<uint64_t>(u - r * rows_per_shard) * ld4;
   }
 };
 
@@ -101,14 +101,20 @@ __global__ void __launch_bounds__(256, MINB)
     // column chunks of 32 float4 (one for F <= 128; wide rows, e.g. F = 602, take several)
     for (int c0 = 0; c0 < (WIDE ? f4 : 1); c0 += 32) {
     const bool col = c0 + lane < f4;
-    const float4 sv = col ? ldg4_hint(rows.row(ac.self) + c0 + lane, pol_keep) : zero;
+    // every load is unconditional (no select or zeroing after it: a predicated or selected
+    // load leaves a register move that waits on its scoreboard and holds the next load's
+    // address back, splitting a row's loads over two round trips): lanes past F re-read the
+    // row's last float4 (same request), slots past deg re-read the self row (an L2 hit); only
+    // the first deg values are summed and only lanes < F/4 store
+    const int cl = col ? c0 + lane : f4 - 1;
+    const float4 sv = ldg4_hint(rows.row(ac.self) + cl, pol_keep);
     float4 acc = zero;
     for (int base = 0; base < deg; base += DMAX) {
       float4 v[DMAX];
 #pragma unroll
       for (int j = 0; j < DMAX; ++j) {
         const int32_t g = __shfl_sync(kFull, bc.g, (base + j) & 31);
-        v[j] = (col && base + j < deg) ? ldg4_hint(rows.row(g) + c0 + lane, pol_keep) : zero;
+        v[j] = ldg4_hint(rows.row(base + j < deg ? g : ac.self) + cl, pol_keep);
       }
 #pragma unroll
       for (int j = 0; j < DMAX; ++j) {
