@@ -30,6 +30,7 @@ using namespace smp;
 
 constexpr int kMaxBlocks = 4096;
 constexpr int kRowCap = 3072;  // dst rows per block cached in shared memory
+constexpr int kTiles = 8;      // edge tiles per block whose flags are loaded before scanning
 constexpr uint32_t kFinal = 0x80000000u;
 constexpr uint32_t kMarkerTop = 0x7FFFFFFFu;
 
@@ -163,48 +164,28 @@ __device__ __forceinline__ void range_of(int64_t n, int64_t align, int64_t& lo, 
   if (hi > n) hi = n;
 }
 
-// 8 consecutive int32 of p starting at e0 (a multiple of 8), entries at or past n read as 0:
-// two 16-byte loads when the run is whole and 16-byte aligned, else scalar loads
-__device__ __forceinline__ void ld8(const int32_t* p, int64_t e0, int64_t n, int32_t (&v)[8]) {
-  if (e0 + 8 <= n && (reinterpret_cast<uintptr_t>(p + e0) & 15) == 0) {
-    const int4 x = __ldcg(reinterpret_cast<const int4*>(p + e0));
-    const int4 y = __ldcg(reinterpret_cast<const int4*>(p + e0) + 1);
-    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-    v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
-  } else {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = e0 + k < n ? __ldcg(p + e0 + k) : 0;
-  }
-}
-__device__ __forceinline__ void st8(int32_t* p, int64_t e0, int64_t n, const int32_t (&v)[8]) {
-  if (e0 + 8 <= n && (reinterpret_cast<uintptr_t>(p + e0) & 15) == 0) {
-    reinterpret_cast<int4*>(p + e0)[0] = make_int4(v[0], v[1], v[2], v[3]);
-    reinterpret_cast<int4*>(p + e0)[1] = make_int4(v[4], v[5], v[6], v[7]);
-  } else {
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (e0 + k < n) p[e0 + k] = v[k];
-  }
-}
-
-// relabel of hop h (all entries final): indices[e] := local id of its node.  A thread owns 8
-// consecutive edges per round: their ids in two vector loads, then all 8 map lookups in flight.
+// relabel of hop h (all entries final): indices[e] := local id of its node
 template <int PB>
 __device__ void phase_relabel(const PArgs& a, int h) {
   const int64_t e_h = __ldcg(a.sizes + a.L + 1 + h);
   int32_t* gid = (h == a.L - 1) ? a.last_src : nullptr;
   int32_t* ind = a.indices[h];
-  const int64_t stride = (int64_t)vgrid() * PB * 8;
-  for (int64_t e0 = (vblk() * (int64_t)PB + threadIdx.x) * 8; e0 < e_h; e0 += stride) {
-    int32_t u[8], l[8];
-    ld8(ind, e0, e_h, u);
-    unsigned long long v[8];
+  const int64_t stride = (int64_t)vgrid() * PB;
+  for (int64_t e0 = vblk() * (int64_t)PB + threadIdx.x; e0 < e_h; e0 += 4 * stride) {
+    int32_t u[4];
+    unsigned long long v[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = __ldcg(a.map + u[k]);  // past e_h: u = 0, harmless
+    for (int k = 0; k < 4; ++k) u[k] = e0 + k * stride < e_h ? __ldcg(ind + e0 + k * stride) : 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) l[k] = static_cast<int32_t>(static_cast<uint32_t>(v[k]) & ~kFinal);
-    if (gid) st8(gid, e0, e_h, u);
-    st8(ind, e0, e_h, l);
+    for (int k = 0; k < 4; ++k) v[k] = e0 + k * stride < e_h ? __ldcg(a.map + u[k]) : 0ull;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t e = e0 + k * stride;
+      if (e < e_h) {
+        if (gid) gid[e] = u[k];
+        ind[e] = static_cast<int32_t>(static_cast<uint32_t>(v[k]) & ~kFinal);
+      }
+    }
   }
 }
 
@@ -228,40 +209,6 @@ struct PickEmit {
     // read the entry first: a node picked by many rows (hubs; every pick of a community at
     // p = 1) would otherwise queue one same-address atomic per pick in L2
     if (__ldcg(map + u) < m) atomicMax(map + u, m);
-  }
-  // all picks of one row at once (thread-per-row form): pick s at CSR offset rs + pos[s] has
-  // rank rk[s]; every neighbour load is issued before any is used, then every map load, so a
-  // row costs two memory round trips instead of two per pick
-  // (SORTED: pos is already ascending, rank = slot; else rank = number of smaller positions)
-  template <int FM, bool SORTED>
-  __device__ __forceinline__ void put_all(int tot, int64_t rs, const uint32_t (&pos)[FM]) const {
-#pragma unroll
-    for (int c = 0; c < FM; c += 8) {  // chunks of 8 picks bound the registers in flight
-      if (c >= tot) break;
-      int32_t u[8];
-#pragma unroll
-      for (int s = 0; s < 8; ++s) u[s] = __ldg(ind + rs + (c + s < tot ? pos[c + s] : pos[c]));
-      uint32_t rk[8];
-#pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        uint32_t r = c + s;
-        if (!SORTED) {
-          r = 0;
-#pragma unroll
-          for (int q = 0; q < FM; ++q) r += (q < tot) && pos[q] < pos[c + s];
-        }
-        rk[s] = r;
-        if (c + s < tot) out[r] = u[s];
-      }
-      unsigned long long cur[8];
-#pragma unroll
-      for (int s = 0; s < 8; ++s) cur[s] = __ldcg(map + u[s]);
-#pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        const unsigned long long m = tag | (kMarkerTop - (e0 + rk[s]));
-        if (c + s < tot && cur[s] < m) atomicMax(map + u[s], m);
-      }
-    }
   }
 };
 
@@ -367,17 +314,7 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
                                                      const Emit& em, int law) {
   const int64_t ni = static_cast<int64_t>(hi) - lo;
   const int64_t ni_e = wi ? ni : 0, no_e = wo ? deg - ni : 0;
-  if (f >= ni_e + no_e) {  // take-all (reading R4): every eligible position, ascending
-    const int m = static_cast<int>(ni_e + no_e);
-    uint32_t pos[FM];
-#pragma unroll
-    for (int s = 0; s < FM; ++s) {
-      const uint32_t q = static_cast<uint32_t>(s);
-      pos[s] = (ni_e && no_e) ? q : ni_e ? lo + q : (q < lo ? q : hi + (q - lo));
-    }
-    em.template put_all<FM, true>(m, rs, pos);
-    return;
-  }
+  if (take_all(rs, deg, lo, hi, ni_e, no_e, f, 0, 1, em)) return;
   uint64_t r23[FM];
   uint64_t ri = static_cast<uint64_t>(ni_e), ro = static_cast<uint64_t>(no_e);
   int K = 0, kd = 0;
@@ -429,7 +366,15 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
       pos[s] = s < K ? lo + q : (q < lo ? q : hi + (q - lo));
     }
   }
-  em.template put_all<FM, false>(tot, rs, pos);  // emitted in ascending position order
+#pragma unroll
+  for (int s = 0; s < FM; ++s) {  // ascending emit by rank
+    if (s < tot) {
+      int rank = 0;
+#pragma unroll
+      for (int q = 0; q < FM; ++q) rank += (q < tot) && pos[q] < pos[s];
+      em.put(rank, rs + pos[s]);
+    }
+  }
 }
 
 template <int PB, int G>
@@ -441,58 +386,34 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   int64_t lo, hi;
   range_of(n_h, 1, lo, hi);
   RowCache& rc = sm.rows;
-  // (1) counts, block scan, cached row info.  A thread owns RPT consecutive rows per round: the
-  // row ids, then all their CSR offsets and intra bounds are loaded before any is used (one
-  // scan per PB * RPT rows); an id outside [0, N) (a caller's bad root, already flagged) reads
-  // node 0's row and is given no neighbours
-  constexpr int RPT = 4;
+  // (1) counts, block scan, cached row info
   int32_t run = 0;
-  for (int64_t t0 = lo; t0 < hi; t0 += static_cast<int64_t>(PB) * RPT) {
-    const int64_t i0 = t0 + static_cast<int64_t>(threadIdx.x) * RPT;
-    int32_t v[RPT];
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) v[q] = i0 + q < hi ? __ldcg(dst + i0 + q) : -1;
-    int64_t rs[RPT], re[RPT];
-    uint2 bd[RPT];
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int32_t vv = static_cast<uint32_t>(v[q]) < static_cast<uint64_t>(a.g.n) ? v[q] : 0;
-      rs[q] = __ldg(a.g.indptr + vv);
-      re[q] = __ldg(a.g.indptr + vv + 1);
-      bd[q] = __ldg(a.g.bounds + vv);
-    }
-    int32_t c[RPT], s = 0;
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const bool ok = static_cast<uint32_t>(v[q]) < static_cast<uint64_t>(a.g.n);
-      if (!ok) re[q] = rs[q], bd[q] = make_uint2(0u, 0u);
-      const int64_t ni = static_cast<int64_t>(bd[q].y) - bd[q].x;
-      const int64_t ni_e = a.wi ? ni : 0, no_e = a.wo ? (re[q] - rs[q]) - ni : 0;
-      const int64_t m = ni_e + no_e;
-      c[q] = static_cast<int32_t>(m < f ? m : f);
-      if (a.law == 1 && f < m) c[q] = slot_count(v[q], h, f, a.wi, ni_e, no_e, a.k0, a.k1, a.batch);
-      s += c[q];
+  for (int64_t t0 = lo; t0 < hi; t0 += PB) {
+    const int64_t i = t0 + threadIdx.x;
+    int32_t c = 0;
+    RowInfo r{};
+    int32_t v = 0;
+    if (i < hi) {
+      v = __ldcg(dst + i);
+      r = row_info_checked(a.g, v, a.wi, a.wo);
+      const int64_t m = r.ni_e + r.no_e;
+      c = static_cast<int32_t>(m < f ? m : f);
+      if (a.law == 1 && f < m) c = slot_count(v, h, f, a.wi, r.ni_e, r.no_e, a.k0, a.k1, a.batch);
     }
     int32_t ex, agg;
-    cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(s, ex, agg);
+    cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(c, ex, agg);
     __syncthreads();
-    int32_t off = run + ex;
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int64_t i = i0 + q;
-      if (i < hi) {
-        const int64_t k = i - lo;
-        a.indptr[h][i] = off;
-        if (k < kRowCap) {
-          rc.rs[k] = rs[q];
-          rc.deg[k] = static_cast<uint32_t>(re[q] - rs[q]);
-          rc.lo[k] = bd[q].x;
-          rc.hi[k] = bd[q].y;
-          rc.v[k] = v[q];
-          rc.off[k] = off;
-        }
+    if (i < hi) {
+      const int64_t k = i - lo;
+      a.indptr[h][i] = run + ex;
+      if (k < kRowCap) {
+        rc.rs[k] = r.rs;
+        rc.deg[k] = static_cast<uint32_t>(r.deg);
+        rc.lo[k] = r.lo;
+        rc.hi[k] = r.hi;
+        rc.v[k] = v;
+        rc.off[k] = run + ex;
       }
-      off += c[q];
     }
     run += agg;
   }
@@ -562,9 +483,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   CMB_PROF(a, pk);
 }
 
-// flags + prefix + assign.  A thread owns 8 consecutive edges per round (the block's range is
-// 32-aligned, so 4 threads fill one new-src mask word): ids in two vector loads, all 8 map
-// lookups in flight, one block scan per PB * 8 edges.
+// flags + prefix + assign
 template <int PB>
 __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
                                   unsigned long long tag) {
@@ -575,55 +494,42 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   uint32_t* mask = (h == a.L - 1) ? a.mask : nullptr;
   const int32_t* nbr = a.indices[h];
   int32_t run = 0;
-  for (int64_t c0 = lo; c0 < hi; c0 += static_cast<int64_t>(PB) * 8) {
-    const int64_t e0 = c0 + static_cast<int64_t>(threadIdx.x) * 8;
-    int32_t u[8];
-    ld8(nbr, e0, hi, u);
-    unsigned long long mv[8];
+  for (int64_t c0 = lo; c0 < hi; c0 += (int64_t)kTiles * PB) {
+    bool fl[kTiles];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) mv[k] = __ldcg(a.map + u[k]);
-    uint32_t fl = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      fl |= (e0 + k < hi && mv[k] == (tag | (kMarkerTop - static_cast<uint32_t>(e0 + k))))
-                ? (1u << k) : 0u;
-    int32_t ex, agg;
-    cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(__popc(fl), ex, agg);
-    __syncthreads();
-    int32_t sc[8];
-    int32_t acc = run + ex;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {  // flag << 31 | block-local inclusive flag count
-      acc += (fl >> k) & 1u;
-      sc[k] = static_cast<int32_t>(((fl >> k) & 1u) << 31 | static_cast<uint32_t>(acc));
+    for (int k = 0; k < kTiles; ++k) {  // all loads of up to kTiles tiles in flight
+      const int64_t e = c0 + k * PB + threadIdx.x;
+      fl[k] = e < hi && __ldcg(a.map + __ldcg(nbr + e)) ==
+                            (tag | (kMarkerTop - static_cast<uint32_t>(e)));
     }
-    st8(reinterpret_cast<int32_t*>(a.scan), e0, hi, sc);
-    if (mask) {  // edges e0 .. e0+7 are bits 8 * (thread % 4) .. of word e0 / 32
-      uint32_t w = fl << (8 * (threadIdx.x & 3));
-      w |= __shfl_xor_sync(0xffffffffu, w, 1);
-      w |= __shfl_xor_sync(0xffffffffu, w, 2);
-      if ((threadIdx.x & 3) == 0 && e0 < hi) mask[e0 >> 5] = w;
+#pragma unroll
+    for (int k = 0; k < kTiles; ++k) {
+      const int64_t t0 = c0 + k * PB;
+      if (t0 >= hi) break;
+      const int64_t e = t0 + threadIdx.x;
+      int32_t inc, agg;
+      cub::BlockScan<int32_t, PB>(sm.cub.scan).InclusiveSum(fl[k] ? 1 : 0, inc, agg);
+      __syncthreads();
+      if (e < hi) a.scan[e] = (fl[k] ? 0x80000000u : 0u) | static_cast<uint32_t>(run + inc);
+      if (mask) {
+        const unsigned word = __ballot_sync(0xffffffffu, fl[k]);
+        if ((threadIdx.x & 31) == 0 && e < hi) mask[e >> 5] = word;
+      }
+      run += agg;
     }
-    run += agg;
   }
   CMB_PROF(a, pk);
   const int32_t base =
       publish_and_prefix<PB>(a.pub + kMaxBlocks, static_cast<unsigned>(h + 1), run, sm);
   CMB_PROF(a, pk);
   if (vblk() == vgrid() - 1 && threadIdx.x == 0) a.sizes[h + 1] = n_h + base + run;
-  for (int64_t e0 = lo + static_cast<int64_t>(threadIdx.x) * 8; e0 < hi;
-       e0 += static_cast<int64_t>(PB) * 8) {
-    int32_t sc[8], u[8];
-    ld8(reinterpret_cast<const int32_t*>(a.scan), e0, hi, sc);
-    ld8(nbr, e0, hi, u);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (sc[k] < 0) {  // flag bit 31: first occurrence -> the next local id
-        const uint32_t id =
-            static_cast<uint32_t>(n_h + base + (static_cast<uint32_t>(sc[k]) & 0x7fffffffu) - 1);
-        a.nodes[id] = u[k];
-        a.map[u[k]] = tag | kFinal | id;
-      }
+  for (int64_t e = lo + threadIdx.x; e < hi; e += PB) {
+    const uint32_t sc = __ldcg(a.scan + e);
+    if (sc & 0x80000000u) {
+      const uint32_t id = static_cast<uint32_t>(n_h + base + (sc & 0x7fffffffu) - 1);
+      const int32_t u = __ldcg(nbr + e);
+      a.nodes[id] = u;
+      a.map[u] = tag | kFinal | id;
     }
   }
 }
