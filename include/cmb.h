@@ -160,6 +160,15 @@ typedef struct {
                                           every edge of hop L-1 (= nodes[indices[L-1][e]]; lets
                                           cmb_gather_aggregate skip the relabel-map lookup)      */
   int64_t* sizes;                      /* [2L+1]: n_0..n_L then e_0..e_{L-1}                  */
+  int32_t* dst_order;                  /* optional (NULL): [n_cap[L-1]] the sampler writes a
+                                          permutation of [0, n_{L-1}) grouping the dst rows of
+                                          hop L-1 by node-id bucket (v >> s, at most 4096
+                                          buckets; order inside a bucket unspecified) and the
+                                          a4 + a5 calls visit the rows in that order, so rows
+                                          of one community, which share most of their src rows
+                                          (P:683-691), are processed together and re-read those
+                                          rows from L2.  Results do not depend
+                                          on it: every output row is the same, byte for byte. */
 } cmb_blocks;
 
 /* Capacity bounds (host): n_cap[0] = n_roots, e_cap[h] = n_cap[h] * f_h,
@@ -286,18 +295,6 @@ CMB_API cmb_status cmb_community_order(const int64_t* indptr, const int32_t* ind
                                        size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------ step executor */
-/* a4 + a5 exactly as cmb_gather_aggregate (same results, byte for byte), the dst rows of hop
- * L-1 visited in the order dst_order[0 .. n_{L-1}) (device int32, a permutation of
- * [0, n_{L-1})): rows of nearby node ids processed together re-read the src rows they share
- * while those are still in L2 (the paper's reuse mechanism).  Only the schedule
- * changes: every X_in / H row is the one cmb_gather_aggregate writes.  Requires 16-B aligned rows
- * (ld % 4 == 0). */
-CMB_API cmb_status cmb_gather_aggregate_ordered(const cmb_graph* g, const cmb_blocks* blocks,
-                                                int32_t n_hops, int64_t n_last_dst_cap,
-                                                int64_t nodes_cap, const int32_t* dst_order,
-                                                float* x_in, int64_t x_in_ld, float* h_out,
-                                                int64_t h_ld, void* stream);
-
 /* Where cmb_step_group writes the a4 + a5 outputs of one batch (see cmb_gather_aggregate). */
 typedef struct {
   float* x_in;

@@ -43,8 +43,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sample_workspace_bytes", "cmb_sample_blocks", "cmb_sample_blocks_law",
            "cmb_sample_blocks_multi",
            "cmb_gather_features",
-           "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_gather_aggregate_ordered",
-           "cmb_shard_plan_workspace_bytes",
+           "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_shard_plan_workspace_bytes",
            "cmb_shard_plan", "cmb_gather_rows", "cmb_scatter_rows",
            "cmb_gather_aggregate_sharded", "cmb_ipc_export", "cmb_ipc_open", "cmb_ipc_close",
            "cmb_step_group", "cmb_feature_cache_bytes", "cmb_feature_cache_init",
@@ -84,7 +83,8 @@ class Blocks(ctypes.Structure):
     _fields_ = [("nodes", ctypes.c_void_p), ("nodes_cap", ctypes.c_int64),
                 ("indptr", ctypes.c_void_p * MAX_HOPS), ("indices", ctypes.c_void_p * MAX_HOPS),
                 ("indices_cap", ctypes.c_int64 * MAX_HOPS), ("new_src_mask", ctypes.c_void_p),
-                ("last_src_ids", ctypes.c_void_p), ("sizes", ctypes.c_void_p)]
+                ("last_src_ids", ctypes.c_void_p), ("sizes", ctypes.c_void_p),
+                ("dst_order", ctypes.c_void_p)]
 
 
 class Batch(ctypes.Structure):
@@ -165,8 +165,6 @@ def lib():
             "cmb_sage_mean_aggregate": (I32, [P, P, P, I64, P, I64, P, I32, P, I64, P]),
             "cmb_gather_aggregate": (I32, [P, ctypes.POINTER(Blocks), I32, I64, I64, P, I64, P,
                                            I64, P]),
-            "cmb_gather_aggregate_ordered": (I32, [P, ctypes.POINTER(Blocks), I32, I64, I64, P, P,
-                                                   I64, P, I64, P]),
             "cmb_shard_plan_workspace_bytes": (SZ, [I64]),
             "cmb_shard_plan": (I32, [P, P, I64, I64, I32, P, P, P, P, SZ, P]),
             "cmb_gather_rows": (I32, [P, I64, I64, I32, P, P, I64, P, I64, P]),
@@ -444,6 +442,10 @@ class Sampler:
         b.new_src_mask = self.mask.data_ptr()
         b.last_src_ids = self.last_src_ids.data_ptr()
         b.sizes = self.sizes.data_ptr()
+        # the visiting order of the last hop's dst rows, written by the sampler and used by the
+        # a4 + a5 calls (include/cmb.h cmb_blocks.dst_order; results do not depend on it)
+        self.dst_order = torch.empty(max(1, self.n_cap[L - 1]), dtype=torch.int32, device=dev)
+        b.dst_order = self.dst_order.data_ptr()
         self._blocks = b
         self.x_in = None
         self.h = None
@@ -482,17 +484,9 @@ class Sampler:
                                  device=g.device)
         return self.x_in, self.h
 
-    def gather_aggregate(self, dst_order: Optional[torch.Tensor] = None):
-        """a4 + a5 fused for the last sampled batch -> (X_in [n_L, ld], H [n_{L-1}, ld]).
-        dst_order (device int32 permutation of the n_{L-1} dst rows): the visiting order
-        (cmb_gather_aggregate_ordered); same bytes."""
+    def gather_aggregate(self):
+        """a4 + a5 fused for the last sampled batch -> (X_in [n_L, ld], H [n_{L-1}, ld])."""
         x_in, h = self.alloc_features()
-        if dst_order is not None:
-            _check(lib().cmb_gather_aggregate_ordered(
-                self.graph.handle, ctypes.byref(self._blocks), self.L, self.n_cap[self.L - 1],
-                self.n_cap[self.L], _ptr(dst_order), _ptr(x_in), x_in.stride(0), _ptr(h),
-                h.stride(0), _stream()))
-            return x_in, h
         _check(lib().cmb_gather_aggregate(self.graph.handle, ctypes.byref(self._blocks), self.L,
                                           self.n_cap[self.L - 1], self.n_cap[self.L], _ptr(x_in),
                                           x_in.stride(0), _ptr(h), h.stride(0), _stream()))
@@ -662,6 +656,10 @@ class Sampler:
             self.x_in = torch.empty(self.n_cap[self.L], ld, dtype=torch.float32, device=dev)
             self.h = torch.empty(self.n_cap[self.L - 1], ld, dtype=torch.float32, device=dev)
         return self.x_in, self.h
+
+    def set_dst_order(self, enabled: bool):
+        """Let the sampler write (and the a4 + a5 calls use) the dst visiting order, or not."""
+        self._blocks.dst_order = self.dst_order.data_ptr() if enabled else None
 
     def status(self):
         return lib().cmb_get_device_status(_ptr(self.workspace), _stream())

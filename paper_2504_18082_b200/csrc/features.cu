@@ -390,7 +390,8 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_
                          const int64_t* n_dev, int64_t n_cap, const float* src, int64_t src_ld,
                          const int32_t* map, int f, float* out, int64_t out_ld, float* x_in,
                          int64_t x_in_ld, const uint32_t* mask, int sms, cudaStream_t s,
-                         int32_t* status = nullptr, int deg_hint = 8) {
+                         int32_t* status = nullptr, int deg_hint = 8,
+                         const int32_t* order = nullptr) {
   if (n_cap <= 0) return CMB_OK;
   const int f4 = (f + 3) / 4;
   const bool vec = aligned16(src) && aligned16(out) && src_ld % 4 == 0 && out_ld % 4 == 0 &&
@@ -400,7 +401,7 @@ cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_
                       DenseRows{reinterpret_cast<const float4*>(src),
                                 static_cast<uint32_t>(src_ld / 4)},
                       map, f4, out,
-                      out_ld, x_in, x_in_ld, mask, deg_hint);
+                      out_ld, x_in, x_in_ld, mask, deg_hint, order);
   if (!vec) {
     k_sage_mean_scalar<<<sms * 8, 256, 0, s>>>(indptr, idx, n_dev, n_cap, src, src_ld, map, f,
                                                out, out_ld, x_in, x_in_ld, mask);
@@ -509,7 +510,8 @@ cmb_status cmb_gather_aggregate_sharded(const cmb_graph* g, const cmb_blocks* b,
                     b->indices[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap, rows,
                     b->nodes, (feat_dim + 3) / 4, h_out, h_ld, x_in, x_in_ld, b->new_src_mask,
                     n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
-                                       : 8);
+                                       : 8,
+                    b->dst_order);
 }
 
 cmb_status cmb_cache_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
@@ -549,32 +551,8 @@ cmb_status cmb_cache_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, i
                               static_cast<uint32_t>(c->cache_ld / 4)},
                     w.slot_i, (feat_dim + 3) / 4, h_out, h_ld, x_in, x_in_ld, b->new_src_mask,
                     n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
-                                       : 8);
-}
-
-cmb_status cmb_gather_aggregate_ordered(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
-                                        int64_t n_last_dst_cap, int64_t nodes_cap,
-                                        const int32_t* dst_order, float* x_in, int64_t x_in_ld,
-                                        float* h_out, int64_t h_ld, void* stream) {
-  CMB_ARG(g && b && x_in && h_out && dst_order, "cmb_gather_aggregate_ordered: null argument");
-  CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_gather_aggregate_ordered: bad n_hops");
-  CMB_ARG(g->d.x != nullptr, "cmb_gather_aggregate_ordered: graph has no feature table");
-  CMB_ARG(b->new_src_mask && b->last_src_ids,
-          "cmb_gather_aggregate_ordered: blocks->new_src_mask and last_src_ids are required");
-  CMB_ARG(x_in_ld >= g->d.f && h_ld >= g->d.f && x_in_ld % 4 == 0 && h_ld % 4 == 0 &&
-              g->d.ld % 4 == 0 && aligned16(x_in) && aligned16(h_out) && aligned16(g->d.x),
-          "cmb_gather_aggregate_ordered: rows must be 16-B aligned");
-  CMB_ARG(n_last_dst_cap <= nodes_cap, "cmb_gather_aggregate_ordered: n_last_dst_cap > nodes_cap");
-  const int L = n_hops;
-  return launch_row(g->num_sms, static_cast<cudaStream_t>(stream), b->indptr[L - 1],
-                    b->indices[L - 1], b->last_src_ids, b->sizes + (L - 1), n_last_dst_cap,
-                    DenseRows{reinterpret_cast<const float4*>(g->d.x),
-                              static_cast<uint32_t>(g->d.ld / 4)},
-                    b->nodes,
-                    (g->d.f + 3) / 4, h_out, h_ld, x_in, x_in_ld, b->new_src_mask,
-                    n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
                                        : 8,
-                    dst_order);
+                    b->dst_order);
 }
 
 cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
@@ -593,7 +571,8 @@ cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t
                        x_in_ld, b->new_src_mask, g->num_sms, static_cast<cudaStream_t>(stream),
                        g->status,
                        n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
-                                          : 8);
+                                          : 8,
+                       b->dst_order);
 }
 
 }  // extern "C"

@@ -18,6 +18,8 @@ struct SampleWs {
   WsHeader* hdr;
   unsigned* bar;             // grid barrier {arrivals, generation}
   unsigned long long* pub;   // [2][kMaxPersistBlocks] tagged block aggregates
+  uint32_t* hist;            // [kOrderBuckets] dst rows of hop L-1 per node-id bucket
+  uint32_t* cursor;          // [kOrderBuckets] rows placed so far per bucket
   uint64_t* prof;            // [kMaxPersistBlocks][64] sub-step timeline
   unsigned* tag_ctr;         // [1] batch tag of the last batch
   unsigned long long* map;   // [N] tagged dedup map
@@ -36,6 +38,8 @@ SampleWs carve_sample_ws(void* base, int64_t n_roots, const int32_t* fanouts, in
   w.hdr = c.take<WsHeader>(1);
   w.bar = c.take<unsigned>(64);
   w.pub = c.take<unsigned long long>(2 * kMaxPersistBlocks);  // follows bar contiguously
+  w.hist = c.take<uint32_t>(pst::kOrderBuckets);               // then hist, cursor: the
+  w.cursor = c.take<uint32_t>(pst::kOrderBuckets);             // per-batch memset clears all
   w.prof = c.take<uint64_t>(static_cast<size_t>(kMaxPersistBlocks) * 64);
   w.tag_ctr = c.take<unsigned>(1);
   w.map = c.take<unsigned long long>(static_cast<size_t>(num_nodes));
@@ -71,6 +75,12 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
   a.pub = w.pub;
   a.bar = w.bar;
   a.prof = w.prof;
+  a.hist = w.hist;
+  a.cursor = w.cursor;
+  a.order = out->dst_order;
+  int bits = 0;
+  while ((int64_t{1} << bits) < g->d.n) ++bits;
+  a.order_shift = bits > pst::kOrderBits ? bits - pst::kOrderBits : 0;
   a.status = &w.hdr->status;
   a.law = law;
 }
@@ -170,9 +180,10 @@ cmb_status cmb_sample_blocks_multi(const cmb_graph* g, const cmb_batch* batches,
     SampleWs w = carve_sample_ws(b.workspace, b.n_roots, fanouts, n_hops, g->d.n, nullptr);
     fill_args(m.a[i], g, b.roots, b.n_roots, fanouts, n_hops, wi, wo, k0, k1, b.batch_id, b.out,
               w, law);
-    // barrier state + tagged aggregates (contiguous) are cleared for every batch
+    // barrier state, tagged aggregates and the dst-order buckets (contiguous) are cleared for
+    // every batch
     CMB_CUDA(cudaMemsetAsync(w.bar, 0,
-                             reinterpret_cast<char*>(w.pub + 2 * kMaxPersistBlocks) -
+                             reinterpret_cast<char*>(w.cursor + pst::kOrderBuckets) -
                                  reinterpret_cast<char*>(w.bar),
                              s));
   }

@@ -31,6 +31,8 @@ using namespace smp;
 constexpr int kMaxBlocks = 4096;
 constexpr int kRowCap = 3072;  // dst rows per block cached in shared memory
 constexpr int kTiles = 8;      // edge tiles per block whose flags are loaded before scanning
+constexpr int kOrderBits = 12;                 // dst-order buckets: at most 2^12 node-id ranges
+constexpr int kOrderBuckets = 1 << kOrderBits;
 constexpr uint32_t kFinal = 0x80000000u;
 constexpr uint32_t kMarkerTop = 0x7FFFFFFFu;
 
@@ -66,6 +68,10 @@ struct PArgs {
   unsigned long long* pub;  // [2][kMaxBlocks] tagged block aggregates
   unsigned* bar;            // [0] arrivals, [1] generation
   uint64_t* prof;           // [kMaxBlocks][64] per-block %globaltimer at sub-step boundaries
+  uint32_t* hist;           // [kOrderBuckets] dst rows of hop L-1 per bucket v >> order_shift
+  uint32_t* cursor;         // [kOrderBuckets] rows of each bucket placed so far
+  int32_t* order;           // optional [n_{L-1}]: the visiting order of the last hop's dst rows
+  int order_shift;
   int32_t* status;
   int law;                  // Knob-2 law: 0 = successive weighted w/o replacement, 1 = slot
 };
@@ -396,6 +402,11 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
     if (i < hi) {
       v = __ldcg(dst + i);
       r = row_info_checked(a.g, v, a.wi, a.wo);
+      if (a.order && h == a.L - 1)  // an out-of-range root (flagged) counts in bucket 0
+        atomicAdd(a.hist + (static_cast<uint32_t>(v) < static_cast<uint64_t>(a.g.n)
+                                ? static_cast<uint32_t>(v) >> a.order_shift
+                                : 0u),
+                  1u);
       const int64_t m = r.ni_e + r.no_e;
       c = static_cast<int32_t>(m < f ? m : f);
       if (a.law == 1 && f < m) c = slot_count(v, h, f, a.wi, r.ni_e, r.no_e, a.k0, a.k1, a.batch);
@@ -483,6 +494,40 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   CMB_PROF(a, pk);
 }
 
+// The visiting order of the last hop's dst rows (blocks.dst_order): after the grid barrier
+// that follows the count step every bucket count is final; each block scans the counts and
+// places its own dst rows (the count step's row range) at bucket offset + atomic cursor.
+template <int PB>
+__device__ void place_dst_rows(const PArgs& a, int h, int64_t n_h, Smem<PB>& sm) {
+  static_assert(kOrderBuckets % PB == 0, "buckets per thread");
+  constexpr int BPT = kOrderBuckets / PB;
+  uint32_t* off = reinterpret_cast<uint32_t*>(&sm.rows);  // the row cache is free in this phase
+  uint32_t c[BPT];
+  int32_t s = 0;
+#pragma unroll
+  for (int q = 0; q < BPT; ++q) {
+    c[q] = __ldcg(a.hist + threadIdx.x * BPT + q);
+    s += static_cast<int32_t>(c[q]);
+  }
+  int32_t ex;
+  cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(s, ex);
+#pragma unroll
+  for (int q = 0; q < BPT; ++q) {
+    off[threadIdx.x * BPT + q] = static_cast<uint32_t>(ex);
+    ex += static_cast<int32_t>(c[q]);
+  }
+  __syncthreads();
+  const int32_t* dst = h == 0 ? a.roots : a.nodes;
+  int64_t lo, hi;
+  range_of(n_h, 1, lo, hi);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += PB) {
+    const uint32_t v = static_cast<uint32_t>(__ldcg(dst + i));
+    const uint32_t b = v < static_cast<uint64_t>(a.g.n) ? v >> a.order_shift : 0u;
+    a.order[off[b] + atomicAdd(a.cursor + b, 1u)] = static_cast<int32_t>(i);
+  }
+  __syncthreads();
+}
+
 // flags + prefix + assign
 template <int PB>
 __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
@@ -493,6 +538,7 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   range_of(e_h, 32, lo, hi);
   uint32_t* mask = (h == a.L - 1) ? a.mask : nullptr;
   const int32_t* nbr = a.indices[h];
+  if (a.order && h == a.L - 1) place_dst_rows<PB>(a, h, n_h, sm);
   int32_t run = 0;
   for (int64_t c0 = lo; c0 < hi; c0 += (int64_t)kTiles * PB) {
     bool fl[kTiles];

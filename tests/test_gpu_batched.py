@@ -64,3 +64,34 @@ def test_batched_pipeline_matches_sequential(small):
         assert s.nodes[: n[3]].cpu().numpy().tobytes() == nodes.tobytes()
         assert s.x_in[: n[3]].cpu().numpy().tobytes() == xin.tobytes()
         assert s.h[: n[2]].cpu().numpy().tobytes() == hh.tobytes()
+
+
+@pytest.mark.parametrize("nb", [1, 4])
+def test_dst_order_is_a_bucketed_permutation(small, nb):
+    """cmb_blocks.dst_order: the sampler writes a permutation of the last hop's dst rows whose
+    node ids (v >> s, s = max(0, bits(N) - 12)) are non-decreasing by bucket; the fused gather's
+    bytes do not depend on it (checked against the natural order)."""
+    b, prep, g = small
+    fan = (15, 10, 5)
+    L = len(fan)
+    order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_RAND, 0, SEED, 0)
+    samplers = [cmb.Sampler(g, 256, fan) for _ in range(nb)]
+    roots = [torch.from_numpy(oracle.batch_roots(order, 256, i)).cuda() for i in range(nb)]
+    cmb.sample_multi(samplers, roots, list(range(nb)), 0.9, SEED)
+    torch.cuda.synchronize()
+    N = b.cfg.num_nodes
+    shift = max(0, int(N - 1).bit_length() - 12)
+    for s in samplers:
+        assert s.status() == 0
+        n = int(s.sizes[L - 1].item())
+        o = s.dst_order[:n].cpu().numpy()
+        assert np.array_equal(np.sort(o), np.arange(n))
+        bucket = s.nodes[:n].cpu().numpy()[o] >> shift
+        assert np.all(np.diff(bucket) >= 0)
+        x1, h1 = (t.clone() for t in s.gather_aggregate())
+        s.set_dst_order(False)
+        x0, h0 = s.gather_aggregate()
+        s.set_dst_order(True)
+        torch.cuda.synchronize()
+        nl = int(s.sizes[L].item())
+        assert torch.equal(x0[:nl], x1[:nl]) and torch.equal(h0[:n], h1[:n])

@@ -1,9 +1,9 @@
-"""Does the visiting order of the last hop's dst rows change the fused gather's DRAM traffic?
-products-shaped input: per batch, the fused a4 + a5 kernel in the natural order and with
-dst_order = (a) rows sorted by node id, (b) sorted by id >> SHIFT buckets (stable), (c) a random
-permutation (control).  Checks the bytes are identical to the natural order's, prints the mean
-kernel time per order (CUDA events).  Under ncu, -k regex:k_gather_mean_row gives the DRAM
-bytes of each launch (launch order: natural, sorted, bucketed, random per batch)."""
+"""Does the visiting order of the last hop's dst rows change the fused gather's time / DRAM
+traffic?  products-shaped input: per batch (sampled with the dst order on), the fused a4 + a5
+kernel in the natural order, in the sampler's bucketed order (cmb_blocks.dst_order) and through
+the one-shard ShardedRows map.  Checks the bytes are identical, prints the mean kernel time per
+form (CUDA events).  Under ncu, -k regex:k_gather_mean_row gives the DRAM bytes of each launch
+(launch order per batch: natural, sampler_order, sharded1)."""
 import json
 import os
 import sys
@@ -18,7 +18,6 @@ from gen import CONFIGS, generate  # noqa: E402
 def main():
     cfg = CONFIGS[os.environ.get("CFG", "products")]
     K = int(os.environ.get("K", "24"))
-    shift = int(os.environ.get("SHIFT", "10"))
     b = generate(cfg)
     g = cmb.Graph.from_bundle(b)
     L = len(cfg.fanouts)
@@ -29,26 +28,21 @@ def main():
                                      mode=mode, mix=mix, p=p)
         pipe.start_epoch(0)
         s = pipe.sampler
-        t = {k: [] for k in ("natural", "sorted", "bucketed", "random", "sharded1")}
+        t = {k: [] for k in ("natural", "sampler_order", "sharded1")}
         table = cmb.ShardTable([g.features], cfg.num_nodes, cfg.feat_dim)
         same = True
-        gen = torch.Generator(device="cuda").manual_seed(0)
         for k in range(K):
+            s.set_dst_order(True)
             s.sample(pipe.batch_roots(k), p, 42, k)
             n = int(s.sizes[L - 1].item())
-            nodes = s.nodes[:n]
-            orders = {"natural": None,
-                      "sorted": torch.argsort(nodes, stable=True).to(torch.int32),
-                      "bucketed": torch.argsort(nodes >> shift, stable=True).to(torch.int32),
-                      "random": torch.randperm(n, device="cuda", generator=gen).to(torch.int32),
-                      "sharded1": "sharded1"}
             ref = None
-            for name, o in orders.items():
+            for name in t:
+                s.set_dst_order(name == "sampler_order")
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 torch.cuda.synchronize()
                 e0.record()
-                x_in, h = (s.gather_aggregate_sharded(table) if isinstance(o, str) else
-                           s.gather_aggregate(o))
+                x_in, h = (s.gather_aggregate_sharded(table) if name == "sharded1" else
+                           s.gather_aggregate())
                 e1.record()
                 torch.cuda.synchronize()
                 if k >= 2:
@@ -59,6 +53,7 @@ def main():
                     ref = cur
                 else:
                     same &= bool(torch.equal(ref[0], cur[0]) and torch.equal(ref[1], cur[1]))
+            s.set_dst_order(True)
         out[f"{mode}({mix})|{p}"] = {k: sum(v) / len(v) for k, v in t.items()}
         out[f"{mode}({mix})|{p}"]["bytes_identical"] = same
     print(json.dumps(out))
