@@ -213,7 +213,9 @@ CMB_API cmb_status cmb_sample_blocks_law(const cmb_graph* g, const int32_t* root
  * bound phases of small hops overlap across batches.  Each batch has its own roots, batch id,
  * output blocks and workspace (workspaces must be distinct); results are identical to
  * calling cmb_sample_blocks once per batch. */
+#ifndef CMB_MAX_BATCHES_PER_LAUNCH
 #define CMB_MAX_BATCHES_PER_LAUNCH 4
+#endif
 typedef struct {
   const int32_t* roots; /* device int32[n_roots], distinct */
   int64_t n_roots;
