@@ -4,6 +4,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <cstdio>
@@ -51,6 +52,17 @@ static_assert(sizeof(WsHeader) == 256, "header is one 256-byte line");
 __device__ __forceinline__ void raise_status(int32_t* st, int32_t code) {
   atomicCAS(st, 0, code);  // first error wins
 }
+
+// ---------------------------------------------------------------- tracing
+// NVTX range around every entry point of the path (host enqueue span of one stage; nsys / ncu
+// --nvtx show them per stage).  Header-only NVTX3: a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define CMB_NVTX(name) ::cmb::NvtxRange cmb_nvtx_range_(name)
 
 // ---------------------------------------------------------------- workspace carving
 struct Carver {

@@ -439,6 +439,7 @@ extern "C" {
 
 cmb_status cmb_gather_features(const cmb_graph* g, const int32_t* node_ids, const int64_t* n_dev,
                                int64_t n_cap, float* out, int64_t out_ld, void* stream) {
+  CMB_NVTX("cmb.a4.gather_features");
   CMB_ARG(g && node_ids && n_dev && out, "cmb_gather_features: null argument");
   CMB_ARG(g->d.x != nullptr, "cmb_gather_features: graph has no feature table");
   CMB_ARG(n_cap >= 0 && out_ld >= g->d.f, "cmb_gather_features: n_cap < 0 or out_ld < F");
@@ -449,6 +450,7 @@ cmb_status cmb_gather_features(const cmb_graph* g, const int32_t* node_ids, cons
 cmb_status cmb_gather_rows(const float* x, int64_t ld, int64_t row0, int32_t feat_dim,
                            const int32_t* ids, const int64_t* n_dev, int64_t n_cap, float* out,
                            int64_t out_ld, void* stream) {
+  CMB_NVTX("cmb.a6.gather_rows");
   CMB_ARG(x && ids && n_dev && out, "cmb_gather_rows: null argument");
   CMB_ARG(feat_dim >= 1 && ld >= feat_dim && out_ld >= feat_dim && n_cap >= 0 && row0 >= 0,
           "cmb_gather_rows: bad feat_dim / ld / n_cap / row0");
@@ -464,6 +466,7 @@ cmb_status cmb_sage_mean_aggregate(const int32_t* indptr, const int32_t* indices
                                    const int64_t* n_dst_dev, int64_t n_dst_cap, const float* src,
                                    int64_t src_ld, const int32_t* src_map, int32_t feat_dim,
                                    float* out, int64_t out_ld, void* stream) {
+  CMB_NVTX("cmb.a5.sage_mean_aggregate");
   CMB_ARG(indptr && indices && n_dst_dev && src && out, "cmb_sage_mean_aggregate: null argument");
   CMB_ARG(feat_dim >= 1 && src_ld >= feat_dim && out_ld >= feat_dim && n_dst_cap >= 0,
           "cmb_sage_mean_aggregate: bad feat_dim / ld / n_dst_cap");
@@ -481,6 +484,7 @@ cmb_status cmb_gather_aggregate_sharded(const cmb_graph* g, const cmb_blocks* b,
                                         int64_t rows_per_shard, int64_t shard_ld, int32_t feat_dim,
                                         float* x_in, int64_t x_in_ld, float* h_out, int64_t h_ld,
                                         void* stream) {
+  CMB_NVTX("cmb.a4a5.gather_aggregate_sharded");
   CMB_ARG(g && b && shards && x_in && h_out, "cmb_gather_aggregate_sharded: null argument");
   CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_gather_aggregate_sharded: bad n_hops");
   CMB_ARG(world >= 1 && world <= kMaxShards, "cmb_gather_aggregate_sharded: world %d outside [1, %d]",
@@ -519,6 +523,7 @@ cmb_status cmb_cache_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, i
                                       const cmb_feature_cache* c, int32_t feat_dim,
                                       uint32_t batch_tag, float* x_in, int64_t x_in_ld,
                                       float* h_out, int64_t h_ld, int64_t* stats, void* stream) {
+  CMB_NVTX("cmb.a4a5.cache_gather_aggregate");
   CMB_ARG(g && b && c && x_in && h_out, "cmb_cache_gather_aggregate: null argument");
   CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_cache_gather_aggregate: bad n_hops");
   CMB_ARG(c->workspace && c->host_x && c->cache_rows, "cmb_cache_gather_aggregate: bad cache");
@@ -558,6 +563,7 @@ cmb_status cmb_cache_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, i
 cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
                                 int64_t n_last_dst_cap, int64_t nodes_cap, float* x_in,
                                 int64_t x_in_ld, float* h_out, int64_t h_ld, void* stream) {
+  CMB_NVTX("cmb.a4a5.gather_aggregate");
   CMB_ARG(g && b && x_in && h_out, "cmb_gather_aggregate: null argument");
   CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_gather_aggregate: bad n_hops");
   CMB_ARG(g->d.x != nullptr, "cmb_gather_aggregate: graph has no feature table");

@@ -108,6 +108,7 @@ size_t cmb_graph_workspace_bytes(int64_t num_nodes, int32_t num_communities) {
 }
 
 cmb_status cmb_load_graph(const cmb_graph_desc* d, void* stream, cmb_graph** out) {
+  CMB_NVTX("cmb.a0.load_graph");
   CMB_ARG(d != nullptr && out != nullptr, "cmb_load_graph: null desc/out");
   *out = nullptr;
   CMB_ARG(d->num_nodes > 0 && d->num_nodes < (int64_t(1) << 31),

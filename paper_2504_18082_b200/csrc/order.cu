@@ -209,6 +209,7 @@ cmb_status cmb_order_roots(const cmb_graph* g, const int32_t* train_ids, int64_t
                            cmb_roots_mode mode, double mix_fraction, uint64_t seed, uint32_t epoch,
                            int32_t* out_order, void* workspace, size_t workspace_bytes,
                            void* stream) {
+  CMB_NVTX("cmb.a1.order_roots");
   CMB_ARG(g && train_ids && out_order, "cmb_order_roots: null graph/train_ids/out_order");
   CMB_ARG(n_train >= 1 && n_train <= g->d.n, "cmb_order_roots: n_train %lld outside [1, N]",
           (long long)n_train);

@@ -107,6 +107,7 @@ cmb_status cmb_community_order(const int64_t* indptr, const int32_t* indices,
                                int32_t num_communities, int32_t* perm, int32_t* inv,
                                int64_t* indptr_out, int32_t* indices_out, int32_t* community_out,
                                void* workspace, size_t workspace_bytes, void* stream) {
+  CMB_NVTX("cmb.next2.community_order");
   CMB_ARG(indptr && community && perm && inv && indptr_out && community_out &&
               (nnz == 0 || (indices && indices_out)),
           "cmb_community_order: null argument");

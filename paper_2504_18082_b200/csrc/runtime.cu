@@ -14,6 +14,7 @@ cmb_status cmb_step_group(const cmb_graph* g, const cmb_batch* batches,
                           const cmb_batch_features* feats, int32_t n_batches,
                           const int32_t* fanouts, int32_t n_hops, double p_intra, int32_t law,
                           uint64_t seed, void* const* events, void* stream) {
+  CMB_NVTX("cmb.step_group");
   CMB_ARG(g && batches && feats && fanouts, "cmb_step_group: null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto rec = [&](int i) -> cmb_status {

@@ -1390,6 +1390,7 @@ cmb_status cmb_sage_layer_forward(const cmb_graph* g, const cmb_blocks* b, int32
                                   int64_t n_last_dst_cap, const void* w_img, const float* bias,
                                   int32_t out_dim, int32_t relu, int32_t out_bf16, void* out,
                                   int64_t out_ld, void* stream) {
+  CMB_NVTX("cmb.next4.sage_layer_forward");
   return layer_forward(g, b, n_hops, n_last_dst_cap, w_img, bias, out_dim, relu, out_bf16, out,
                        out_ld, stream, 2);
 }
@@ -1404,6 +1405,7 @@ cmb_status cmb_sage_layer_forward_save(const cmb_graph* g, const cmb_blocks* b, 
                                        const float* bias, int32_t out_dim, int32_t relu,
                                        int32_t out_bf16, void* out, int64_t out_ld, void* a_save,
                                        size_t a_save_bytes, void* stream) {
+  CMB_NVTX("cmb.next4.sage_layer_forward_save");
   CMB_ARG(a_save && g, "cmb_sage_layer_forward_save: null argument");
   const size_t need = cmb_sage_saved_a_bytes(g->d.f, n_last_dst_cap);
   CMB_ARG(a_save_bytes >= need && sl::aligned16(a_save),
@@ -1440,6 +1442,7 @@ cmb_status cmb_gcn_layer_forward(const cmb_graph* g, const cmb_blocks* b, int32_
                                  int64_t n_last_dst_cap, const void* w_img, const float* bias,
                                  int32_t out_dim, int32_t relu, int32_t out_bf16, void* out,
                                  int64_t out_ld, void* stream) {
+  CMB_NVTX("cmb.next4.gcn_layer_forward");
   return layer_forward(g, b, n_hops, n_last_dst_cap, w_img, bias, out_dim, relu, out_bf16, out,
                        out_ld, stream, 1);
 }
@@ -1514,6 +1517,7 @@ cmb_status cmb_sage_layer_backward(const cmb_graph* g, const cmb_blocks* b, int3
                                    int32_t dy_f32, const void* y, int64_t y_ld, int32_t out_dim,
                                    float* dw, float* db, void* workspace, size_t workspace_bytes,
                                    void* stream) {
+  CMB_NVTX("cmb.next4.sage_layer_backward");
   return layer_backward(g, b, n_hops, n_last_dst_cap, dy, dy_ld, dy_f32, y, y_ld, out_dim, dw, db,
                         workspace, workspace_bytes, stream, nullptr);
 }
@@ -1524,6 +1528,7 @@ cmb_status cmb_sage_layer_backward_saved(const cmb_graph* g, const cmb_blocks* b
                                          int32_t dy_f32, const void* y, int64_t y_ld,
                                          int32_t out_dim, float* dw, float* db, void* workspace,
                                          size_t workspace_bytes, void* stream) {
+  CMB_NVTX("cmb.next4.sage_layer_backward_saved");
   CMB_ARG(a_saved && g, "cmb_sage_layer_backward_saved: null argument");
   const size_t need = cmb_sage_saved_a_bytes(g->d.f, n_last_dst_cap);
   CMB_ARG(a_saved_bytes >= need && sl::aligned16(a_saved),
@@ -1537,6 +1542,7 @@ cmb_status cmb_gcn_layer_backward(const cmb_graph* g, const cmb_blocks* b, int32
                                   int32_t dy_f32, const void* y, int64_t y_ld, int32_t out_dim,
                                   float* dw, float* db, void* workspace, size_t workspace_bytes,
                                   void* stream) {
+  CMB_NVTX("cmb.next4.gcn_layer_backward");
   return layer_backward(g, b, n_hops, n_last_dst_cap, dy, dy_ld, dy_f32, y, y_ld, out_dim, dw, db,
                         workspace, workspace_bytes, stream, nullptr, 1);
 }
@@ -1572,6 +1578,7 @@ cmb_status cmb_sage_hidden_forward(const cmb_blocks* b, int32_t hop, int64_t n_d
                                    const void* w_img, const float* bias, int32_t out_dim,
                                    int32_t relu, int32_t out_bf16, void* out, int64_t out_ld,
                                    void* stream) {
+  CMB_NVTX("cmb.next4.sage_hidden_forward");
   CMB_ARG(b && y_prev && w_img && out, "cmb_sage_hidden_forward: null argument");
   CMB_ARG(hop >= 0 && hop < CMB_MAX_HOPS && b->indptr[hop] && b->indices[hop],
           "cmb_sage_hidden_forward: bad hop");
@@ -1619,6 +1626,7 @@ cmb_status cmb_sage_hidden_backward(const cmb_blocks* b, int32_t hop, int64_t n_
                                     int64_t y_ld, int32_t out_dim, float* dw, float* db, void* workspace,
                                     size_t workspace_bytes, void* dz_out, int64_t dz_ld,
                                     void* stream) {
+  CMB_NVTX("cmb.next4.sage_hidden_backward");
   CMB_ARG(b && y_prev && dy && dw && db && workspace, "cmb_sage_hidden_backward: null argument");
   CMB_ARG(!dz_out || (dz_ld >= out_dim && dz_ld % 8 == 0 && sl::aligned16(dz_out)),
           "cmb_sage_hidden_backward: dz_out rows must be 16-byte aligned bf16 with ld >= out_dim");
@@ -1699,6 +1707,7 @@ cmb_status cmb_sage_hidden_input_grad(const cmb_blocks* b, int32_t hop, int64_t 
                                       int32_t out_dim, const void* wt_img, int32_t in_dim,
                                       float* dx, int64_t dx_ld, float* dh, int64_t dh_ld,
                                       void* stream) {
+  CMB_NVTX("cmb.next4.sage_hidden_input_grad");
   CMB_ARG(b && dz && wt_img && dx && dh, "cmb_sage_hidden_input_grad: null argument");
   CMB_ARG(hop >= 0 && hop < CMB_MAX_HOPS && b->indptr[hop] && b->indices[hop],
           "cmb_sage_hidden_input_grad: bad hop");
@@ -1748,6 +1757,7 @@ cmb_status cmb_sage_mean_backward(const int32_t* indptr, const int32_t* indices,
                                   const int64_t* n_dst_dev, int64_t n_dst_cap, const float* dh,
                                   int64_t dh_ld, int32_t feat_dim, float* dx, int64_t dx_ld,
                                   void* stream) {
+  CMB_NVTX("cmb.next4.sage_mean_backward");
   CMB_ARG(indptr && indices && n_dst_dev && dh && dx, "cmb_sage_mean_backward: null argument");
   CMB_ARG(feat_dim >= 1 && dh_ld >= feat_dim && dx_ld >= feat_dim && dh_ld % 4 == 0 &&
               dx_ld % 4 == 0 && sl::aligned16(dh) && sl::aligned16(dx),

@@ -149,6 +149,7 @@ size_t cmb_sample_workspace_bytes(int64_t n_roots, const int32_t* fanouts, int32
 cmb_status cmb_sample_blocks_multi(const cmb_graph* g, const cmb_batch* batches,
                                    int32_t n_batches, const int32_t* fanouts, int32_t n_hops,
                                    double p_intra, int32_t law, uint64_t seed, void* stream) {
+  CMB_NVTX("cmb.a2a3.sample_relabel");
   CMB_ARG(g && batches && fanouts, "cmb_sample_blocks: null graph/batches/fanouts");
   CMB_ARG(n_batches >= 1 && n_batches <= CMB_MAX_BATCHES_PER_LAUNCH,
           "cmb_sample_blocks_multi: n_batches %d outside [1, %d]", n_batches,

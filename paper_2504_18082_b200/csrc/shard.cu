@@ -118,6 +118,7 @@ cmb_status cmb_shard_plan(const int32_t* nodes, const int64_t* n_dev, int64_t n_
                           int64_t rows_per_shard, int32_t world, int64_t* counts,
                           int32_t* send_ids, int32_t* perm, void* workspace,
                           size_t workspace_bytes, void* stream) {
+  CMB_NVTX("cmb.a6.shard_plan");
   CMB_ARG(nodes && n_dev && counts && send_ids && perm, "cmb_shard_plan: null argument");
   CMB_ARG(n_cap >= 1 && n_cap < (int64_t(1) << 31), "cmb_shard_plan: n_cap outside [1, 2^31)");
   CMB_ARG(world >= 1 && world <= 1024 && rows_per_shard >= 1,
@@ -152,6 +153,7 @@ cmb_status cmb_gather_rows(const float* x, int64_t ld, int64_t row0, int32_t fea
 cmb_status cmb_scatter_rows(const float* rows, int64_t rows_ld, const int32_t* perm,
                             const int64_t* n_dev, int64_t n_cap, int32_t feat_dim, float* out,
                             int64_t out_ld, void* stream) {
+  CMB_NVTX("cmb.a6.scatter_rows");
   CMB_ARG(rows && perm && n_dev && out, "cmb_scatter_rows: null argument");
   CMB_ARG(feat_dim >= 1 && rows_ld >= feat_dim && out_ld >= feat_dim && n_cap >= 0,
           "cmb_scatter_rows: bad feat_dim / ld / n_cap");

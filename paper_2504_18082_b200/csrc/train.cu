@@ -178,6 +178,7 @@ cmb_status cmb_softmax_xent(const float* logits, int64_t ld, const int32_t* node
                             const int32_t* nodes, const int64_t* n_dev, int64_t n_cap,
                             int32_t num_classes, void* dy, int64_t dy_ld, int32_t dy_cols,
                             double* loss, double* row_loss, int32_t* status, void* stream) {
+  CMB_NVTX("cmb.next4.softmax_xent");
   CMB_ARG(logits && node_labels && nodes && n_dev && dy && loss && row_loss,
           "cmb_softmax_xent: null argument");
   CMB_ARG(num_classes >= 1 && num_classes <= 256 && dy_cols >= num_classes && dy_cols <= 256 &&
@@ -203,6 +204,7 @@ cmb_status cmb_softmax_xent(const float* logits, int64_t ld, const int32_t* node
 cmb_status cmb_adam_step(float* w, const float* g, float* m, float* v, int64_t n, double lr,
                          double beta1, double beta2, double eps, double weight_decay, int32_t step,
                          void* stream) {
+  CMB_NVTX("cmb.next4.adam_step");
   CMB_ARG(w && g && m && v, "cmb_adam_step: null argument");
   CMB_ARG(n >= 0 && n % 4 == 0 && step >= 1 && beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 &&
               beta2 < 1.0,
@@ -231,6 +233,7 @@ cmb_status cmb_adam_step_pack(float* w, const float* g, float* m, float* v, int6
                               double beta1, double beta2, double eps, double weight_decay,
                               int32_t step, const cmb_layer_pack* layers, int32_t n_layers,
                               void* stream) {
+  CMB_NVTX("cmb.next4.adam_step_pack");
   CMB_ARG(w && g && m && v && layers, "cmb_adam_step_pack: null argument");
   CMB_ARG(n >= 0 && step >= 1 && beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0 &&
               n_layers >= 1 && n_layers <= tr::kMaxPackLayers,
