@@ -875,15 +875,18 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
     (indptr, last-hop src ids, dst ids) and Y (n_{L-1} * 2 Fo); flops 2 * n_{L-1} * 2F * Fo."""
     import torch
     import paper_2504_18082_b200 as cmb
-    if cfg.feat_dim > 128:
-        return {"skipped": f"feat_dim {cfg.feat_dim} > 128 (the fused layer keeps K = 2F <= 256 "
-                           f"resident; see DESIGN.md)"}
     L = len(cfg.fanouts)
     F = cfg.feat_dim
+    wide = F > 128   # the fused layer keeps K = 2F <= 256 resident; wider rows: cmb_sage_dense_*
     gen = torch.Generator().manual_seed(1)
     ws = torch.randn(F, fo, generator=gen) / np.sqrt(F)
     wn = torch.randn(F, fo, generator=gen) / np.sqrt(F)
-    layer = cmb.SageLayer(ws, wn, torch.zeros(fo), relu=True, out_bf16=True, device=graph.device)
+    if wide:
+        layer = cmb.DenseSageLayer(ws, wn, torch.zeros(fo), relu=True, out_bf16=True,
+                                   device=graph.device)
+    else:
+        layer = cmb.SageLayer(ws, wn, torch.zeros(fo), relu=True, out_bf16=True,
+                              device=graph.device)
     # the rest of the paper's 3-layer GraphSAGE (P:770): hidden 256 -> 256, last layer 256 -> 48
     # (ogbn-products' 47 classes rounded up to 16), run on hops L-2 .. 0 (reading R29)
     hidden = []
@@ -912,23 +915,30 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
     dy = (torch.randn(smp.n_cap[L - 1], fo, generator=gen_dy, device=graph.device) * 0.01
           ).to(torch.bfloat16)
     sizes = torch.zeros(n, 2 * L + 1, dtype=torch.int64, device=graph.device)
+    def fwd():
+        return smp.sage_dense_layer(layer, out) if wide else smp.sage_layer(layer, out)
+
+    def bwd():   # weight gradients of the same batch
+        return (smp.sage_dense_backward(layer, dy, out) if wide else
+                smp.sage_layer_backward(layer, dy, out))
+
     for warm in range(3):
         smp.sample(pipe.batch_roots(warm), p, args.seed, warm)
-        smp.sage_layer(layer, out)
-        smp.sage_layer_backward(layer, dy, out)
+        fwd()
+        bwd()
         rest_of_model()
         smp.gather_aggregate()
     torch.cuda.synchronize()
     for k in range(n):
         smp.sample(pipe.batch_roots(k), p, args.seed, k)
         ev[k][0].record(s)
-        smp.sage_layer(layer, out)
+        fwd()
         ev[k][1].record(s)
         rest_of_model()
         ev[k][4].record(s)
         smp.gather_aggregate()
         ev[k][2].record(s)
-        smp.sage_layer_backward(layer, dy, out)   # weight gradients of the same batch
+        bwd()
         ev[k][3].record(s)
         sizes[k].copy_(smp.sizes, non_blocking=True)
     torch.cuda.synchronize()
@@ -967,7 +977,12 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
     part = 148 * (2 * kh * 64 + 1) * fo * 4
     alg_b = nL * 4 * F + 4 * (nd + 1) + 4 * ed + 4 * nd + 2 * nd * 2 * fo + 2 * part + 4 * (2 * F + 1) * fo
     gbps_b = float(np.mean(alg_b) / (np.mean(t_bwd) * 1e-3) / 1e9)
-    return {"kernel": "k_sage_layer (a4+a5+SAGEConv layer 1, tcgen05 bf16, cmb_sage_layer_forward)",
+    if wide:  # unfused: the a4 + a5 bytes (X_in + H written, then read back as the GEMM operand)
+        alg = alg + nL * 4 * F + nd * 4 * F + 2 * nd * 2 * 4 * F
+    return {"kernel": ("a4+a5 fused gather + cmb_sage_dense_forward (bf16 pack, cuBLASLt bf16 "
+                       "GEMM, epilogue): F > 128" if wide else
+                       "k_sage_layer (a4+a5+SAGEConv layer 1, tcgen05 bf16, "
+                       "cmb_sage_layer_forward)"),
             "out_dim": fo, "out_dtype": "bf16", "relu": True, "batches": int(n),
             "layer_ms": float(np.mean(t_layer)), "gather_aggregate_ms_same_batches": float(np.mean(t_agg)),
             "layers_2_to_L_ms": float(np.mean(t_rest)),
@@ -984,7 +999,9 @@ def layer_point(bundle, graph, cfg, args, n_batches=64, fo=256):
                 "roofline": {"bound": "hbm", "achieved": float(alg_mb / (t_mb * 1e-3) / 1e9),
                              "peak": peak, "unit": "GB/s",
                              "frac": float(alg_mb / (t_mb * 1e-3) / 1e9 / peak)}},
-            "backward": {"kernels": "k_sage_layer_bwd + k_sage_bwd_reduce (cmb_sage_layer_backward)",
+            "backward": {"kernels": ("cmb_sage_dense_backward (bf16 pack, mask, cuBLASLt bf16 GEMM "
+                                     "A^T dZ, fixed-order db)" if wide else
+                                     "k_sage_layer_bwd + k_sage_bwd_reduce (cmb_sage_layer_backward)"),
                          "ms": float(np.mean(t_bwd)),
                          "algorithmic_bytes_per_call": float(np.mean(alg_b)),
                          "roofline": {"bound": "hbm", "achieved": gbps_b, "peak": peak,
@@ -1002,8 +1019,6 @@ def train_point(bundle, graph, cfg, args, n_batches=48):
     import torch
     import paper_2504_18082_b200 as cmb
     from gen import make_labels, num_classes
-    if cfg.feat_dim > 128:
-        return {"skipped": f"feat_dim {cfg.feat_dim} > 128 (layer 1 keeps K = 2F <= 256 resident)"}
     C = num_classes(cfg)
     labels = torch.from_numpy(make_labels(bundle, C)).to(graph.device)
     s = torch.cuda.current_stream()

@@ -432,6 +432,40 @@ CMB_API cmb_status cmb_gcn_layer_backward(const cmb_graph* g, const cmb_blocks* 
                                           int64_t y_ld, int32_t out_dim, float* dw, float* db,
                                           void* workspace, size_t workspace_bytes, void* stream);
 
+/* NEXT-4 for wide feature rows (F > 128: Reddit's F = 602), where the fused layer
+ * cannot keep K = 2F resident: the same layer (reading R26) and weight gradients (reading R27)
+ * computed from the a4 + a5 outputs of cmb_gather_aggregate, x_dst = X_in (rows < n = n_dev[0]
+ * <= n_rows_cap, ld x_ld) and h = H (ld h_ld), fp32 device.  Operands are rounded to bf16 (as in
+ * the fused layer, same bounds), the two dense products run as cuBLASLt bf16 GEMMs with fp32
+ * accumulation (the library's only library GEMM), packing / bias / ReLU / mask / dW unpack /
+ * fixed-order db are this library's kernels.
+ *   cmb_sage_dense_pack_weights: w_self, w_neigh fp32 [F x Fo] row-major -> the bf16 image
+ *     (cmb_sage_dense_weights_bytes; Fo a multiple of 8).
+ *   cmb_sage_dense_forward: out[r] = sigma(x_dst[r] W_self + h[r] W_neigh + bias) for r < n
+ *     (bf16 or fp32, ld out_ld), rows n .. n_rows_cap zero.
+ *   cmb_sage_dense_backward: dZ = dY * 1[Y > 0] (y = the forward's bf16 output; NULL = identity),
+ *     dw fp32 [2][F][Fo] = (X_dst^T dZ, H^T dZ), db fp32 [Fo] = sum_r dZ[r] (fp64, fixed order).
+ * workspace: cmb_sage_dense_workspace_bytes(n_rows_cap, F, Fo) bytes, 256-B aligned, caller owned
+ * (it holds the bf16 operand image, the fp32 product, dZ and cuBLASLt's scratch). */
+CMB_API size_t cmb_sage_dense_weights_bytes(int32_t feat_dim, int32_t out_dim);
+CMB_API size_t cmb_sage_dense_workspace_bytes(int64_t n_rows_cap, int32_t feat_dim,
+                                              int32_t out_dim);
+CMB_API cmb_status cmb_sage_dense_pack_weights(const float* w_self, const float* w_neigh,
+                                               int32_t feat_dim, int32_t out_dim, void* w_img,
+                                               size_t w_img_bytes, void* stream);
+CMB_API cmb_status cmb_sage_dense_forward(const float* x_dst, int64_t x_ld, const float* h,
+                                          int64_t h_ld, const int64_t* n_dev, int64_t n_rows_cap,
+                                          int32_t feat_dim, const void* w_img, const float* bias,
+                                          int32_t out_dim, int32_t relu, int32_t out_bf16,
+                                          void* out, int64_t out_ld, void* workspace,
+                                          size_t workspace_bytes, void* stream);
+CMB_API cmb_status cmb_sage_dense_backward(const float* x_dst, int64_t x_ld, const float* h,
+                                           int64_t h_ld, const int64_t* n_dev,
+                                           int64_t n_rows_cap, int32_t feat_dim, const void* dy,
+                                           int64_t dy_ld, int32_t dy_f32, const void* y,
+                                           int64_t y_ld, int32_t out_dim, float* dw, float* db,
+                                           void* workspace, size_t workspace_bytes, void* stream);
+
 /* NEXT-4 hidden layers (reading R29): layer l >= 2 of the model on hop h = L - l:
  *     Y[d] = sigma( Yp[d] W_self + mean_{e in row d of hop h} Yp[indices[h][e]] W_neigh + b ),
  * d < n_h (device count blocks->sizes[h] <= n_dst_cap).  y_prev: device bf16 [n_{h+1} x in_dim]
@@ -589,12 +623,15 @@ CMB_API cmb_status cmb_adam_step(float* w, const float* g, float* m, float* v, i
  * cmb_adam_step_pack: parameters [offset, offset + 2 in_dim out_dim + out_dim) of the buffer are
  * [W_self | W_neigh | b] (row-major [in_dim x out_dim] each); img: the forward weight image
  * (cmb_sage_pack_weights / cmb_sage_hidden_pack_weights layout, kh = ceil(in_dim / 64));
- * img_t: NULL or the transposed image of cmb_sage_hidden_pack_weights_t (kt = ceil(out_dim/64)). */
+ * img_t: NULL or the transposed image of cmb_sage_hidden_pack_weights_t (kt = ceil(out_dim/64)).
+ * dense = 1: img is a cmb_sage_dense_pack_weights image instead (wide first layer, in_dim may
+ * exceed 256; img_t must be NULL). */
 typedef struct {
   int64_t offset;
   int32_t in_dim, out_dim;
   void* img;
   void* img_t;
+  int32_t dense;
 } cmb_layer_pack;
 
 /* cmb_adam_step fused with the repack of the updated weights: every W element is written, as

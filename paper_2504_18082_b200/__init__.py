@@ -59,7 +59,8 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sage_hidden_weights_t_bytes", "cmb_sage_hidden_pack_weights_t",
            "cmb_sage_hidden_input_grad", "cmb_softmax_xent", "cmb_adam_step",
            "cmb_sage_saved_a_bytes", "cmb_sage_layer_forward_save", "cmb_sage_layer_backward_saved",
-           "cmb_adam_step_pack",
+           "cmb_adam_step_pack", "cmb_sage_dense_weights_bytes", "cmb_sage_dense_workspace_bytes",
+           "cmb_sage_dense_pack_weights", "cmb_sage_dense_forward", "cmb_sage_dense_backward",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
 
@@ -96,7 +97,7 @@ class Batch(ctypes.Structure):
 class LayerPack(ctypes.Structure):
     """cmb_layer_pack (include/cmb.h)."""
     _fields_ = [("offset", ctypes.c_int64), ("in_dim", ctypes.c_int32), ("out_dim", ctypes.c_int32),
-                ("img", ctypes.c_void_p), ("img_t", ctypes.c_void_p)]
+                ("img", ctypes.c_void_p), ("img_t", ctypes.c_void_p), ("dense", ctypes.c_int32)]
 
 
 class FeatureCacheDesc(ctypes.Structure):
@@ -219,6 +220,13 @@ def lib():
             "cmb_sage_hidden_pack_weights_t": (I32, [P, P, I32, I32, P, SZ, P]),
             "cmb_sage_hidden_input_grad": (I32, [ctypes.POINTER(Blocks), I32, I64, I64, P, I64, I32,
                                                  P, I32, P, I64, P, I64, P]),
+            "cmb_sage_dense_weights_bytes": (SZ, [I32, I32]),
+            "cmb_sage_dense_workspace_bytes": (SZ, [I64, I32, I32]),
+            "cmb_sage_dense_pack_weights": (I32, [P, P, I32, I32, P, SZ, P]),
+            "cmb_sage_dense_forward": (I32, [P, I64, P, I64, P, I64, I32, P, P, I32, I32, I32, P,
+                                             I64, P, SZ, P]),
+            "cmb_sage_dense_backward": (I32, [P, I64, P, I64, P, I64, I32, P, I64, I32, P, I64,
+                                              I32, P, P, P, SZ, P]),
             "cmb_get_device_status": (I32, [P, P]),
             "cmb_status_string": (ctypes.c_char_p, [I32]),
             "cmb_last_error_message": (ctypes.c_char_p, []),
@@ -564,6 +572,40 @@ class Sampler:
             int(layer.out_bf16), _ptr(out), out.stride(0), _stream()))
         return out
 
+    def sage_dense_layer(self, layer: "DenseSageLayer", out: Optional[torch.Tensor] = None):
+        """NEXT-4 for wide rows (F > 128): a4 + a5 (cmb_gather_aggregate) for the last sampled
+        batch, then the layer on its X_in / H (cmb_sage_dense_forward) -> Y [n_cap[L-1], out]."""
+        cap = self.n_cap[self.L - 1]
+        if out is None:
+            out = layer.alloc_out(cap)
+        x_in, h = self.gather_aggregate()
+        ws = layer.workspace(cap)
+        _check(lib().cmb_sage_dense_forward(
+            _ptr(x_in), x_in.stride(0), _ptr(h), h.stride(0), _ptr(self.sizes[self.L - 1:self.L]),
+            cap, layer.feat_dim, _ptr(layer.w_img), _ptr(layer.bias), layer.out_dim,
+            int(layer.relu), int(layer.out_bf16), _ptr(out), out.stride(0), _ptr(ws), ws.numel(),
+            _stream()))
+        return out
+
+    def sage_dense_backward(self, layer: "DenseSageLayer", dy: torch.Tensor,
+                            y: Optional[torch.Tensor] = None, dw: Optional[torch.Tensor] = None,
+                            db: Optional[torch.Tensor] = None):
+        """Weight gradients of sage_dense_layer on the X_in / H of the last gather (R27)."""
+        if dy.dtype not in (torch.bfloat16, torch.float32) or (
+                y is not None and y.dtype != torch.bfloat16):
+            raise ValueError("dy must be bf16 or fp32, y bf16")
+        F, fo = layer.feat_dim, layer.out_dim
+        cap = self.n_cap[self.L - 1]
+        dw, db = _grad_out(dw, db, F, fo, layer.device)
+        ws = layer.workspace(cap)
+        x_in, h = self.x_in, self.h
+        _check(lib().cmb_sage_dense_backward(
+            _ptr(x_in), x_in.stride(0), _ptr(h), h.stride(0), _ptr(self.sizes[self.L - 1:self.L]),
+            cap, F, _ptr(dy), dy.stride(0), int(dy.dtype == torch.float32), _ptr(y),
+            0 if y is None else y.stride(0), fo, _ptr(dw), _ptr(db), _ptr(ws), ws.numel(),
+            _stream()))
+        return dw[0], dw[1], db
+
     def gcn_layer_backward(self, layer: "GcnLayer", dy: torch.Tensor,
                            y: Optional[torch.Tensor] = None):
         """NEXT-4 GCN backward (R35) for the last sampled batch: dY (bf16 or fp32
@@ -724,6 +766,49 @@ class SageLayer:
         return torch.empty(max(1, rows), self.out_dim, dtype=dt, device=self.device)
 
 
+class DenseSageLayer:
+    """NEXT-4 first layer for wide feature rows (F > 128, e.g. Reddit's 602; include/cmb.h
+    cmb_sage_dense_*): the weights [F, out_dim] (Y = X W) packed once into a bf16 image; the
+    layer runs on the a4 + a5 outputs of the fused gather."""
+
+    def __init__(self, w_self: torch.Tensor, w_neigh: torch.Tensor, bias=None, relu=True,
+                 out_bf16=False, device=None):
+        F, fo = int(w_self.shape[0]), int(w_self.shape[1])
+        if tuple(w_neigh.shape) != (F, fo):
+            raise ValueError("w_self and w_neigh must both be [F, out_dim]")
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        nbytes = lib().cmb_sage_dense_weights_bytes(F, fo)
+        if nbytes == 0:
+            raise ValueError(f"unsupported dense layer shape F={F}, out_dim={fo}")
+        self.feat_dim, self.out_dim = F, fo
+        self.relu, self.out_bf16 = bool(relu), bool(out_bf16)
+        self.hidden = False
+        self.w_self = _dev_tensor(w_self, torch.float32, dev)
+        self.w_neigh = _dev_tensor(w_neigh, torch.float32, dev)
+        self.bias = None if bias is None else _dev_tensor(bias, torch.float32, dev)
+        self.w_img = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        self.device = dev
+        self._ws = {}
+        self.repack()
+
+    def repack(self):
+        _check(lib().cmb_sage_dense_pack_weights(_ptr(self.w_self), _ptr(self.w_neigh),
+                                                 self.feat_dim, self.out_dim, _ptr(self.w_img),
+                                                 self.w_img.numel(), _stream()))
+
+    def workspace(self, rows_cap: int) -> torch.Tensor:
+        ws = self._ws.get(rows_cap)
+        if ws is None:
+            n = lib().cmb_sage_dense_workspace_bytes(rows_cap, self.feat_dim, self.out_dim)
+            ws = _workspace(n, self.device)
+            self._ws[rows_cap] = ws
+        return ws
+
+    def alloc_out(self, rows: int) -> torch.Tensor:
+        dt = torch.bfloat16 if self.out_bf16 else torch.float32
+        return torch.empty(max(1, rows), self.out_dim, dtype=dt, device=self.device)
+
+
 class GraphSAGE:
     """NEXT-4: the paper's L-layer GraphSAGE (3 layers, hidden 256, DGL defaults
     lr 1e-3, weight decay 5e-4) trained on the sampled blocks of a Sampler, every stage in this
@@ -763,6 +848,10 @@ class GraphSAGE:
         for l in range(num_layers):
             ws, wn, b = self._views(self.params, l)
             last = l == num_layers - 1
+            if l == 0 and feat_dim > 128:  # wide rows: the unfused dense first layer
+                self.layers.append(DenseSageLayer(ws, wn, b, relu=not last, out_bf16=not last,
+                                                  device=dev))
+                continue
             self.layers.append(SageLayer(ws, wn, b, relu=not last, out_bf16=not last,
                                          device=dev, hidden=l > 0))
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -797,6 +886,9 @@ class GraphSAGE:
             h = L - 1 - l
             out = self._buf(("y", l), sampler.n_cap[h], layer.out_dim,
                             torch.bfloat16 if layer.out_bf16 else torch.float32)
+            if l == 0 and isinstance(layer, DenseSageLayer):
+                ys.append(sampler.sage_dense_layer(layer, out))
+                continue
             ys.append(sampler.sage_layer(layer, out, save_a=self.save_a) if l == 0 else
                       sampler.sage_hidden(layer, h, ys[-1], out))
         return ys
@@ -817,7 +909,9 @@ class GraphSAGE:
             g_ws, g_wn, g_b = self._views(self.grads, l)
             dw = self.grads[self.offsets[l]:self.offsets[l] + 2 * g_ws.numel()].view(2, *g_ws.shape)
             y = ys[l] if layer.relu else None
-            if l == 0:
+            if l == 0 and isinstance(layer, DenseSageLayer):
+                sampler.sage_dense_backward(layer, dy, y, dw=dw, db=g_b)
+            elif l == 0:
                 sampler.sage_layer_backward(layer, dy, y, dw=dw, db=g_b, saved=self.save_a)
             else:
                 dz = self._buf(("dz", l), sampler.n_cap[h], ((layer.out_dim + 63) // 64) * 64,
@@ -832,7 +926,8 @@ class GraphSAGE:
         for l, layer in enumerate(self.layers):
             wt = layer.transposed_image() if layer.hidden else None
             packs[l] = LayerPack(self.offsets[l], layer.feat_dim, layer.out_dim,
-                                 layer.w_img.data_ptr(), None if wt is None else wt.data_ptr())
+                                 layer.w_img.data_ptr(), None if wt is None else wt.data_ptr(),
+                                 int(isinstance(layer, DenseSageLayer)))
         _check(lib().cmb_adam_step_pack(
             _ptr(self.params), _ptr(self.grads), _ptr(self.m), _ptr(self.v), self.params.numel(),
             self.lr, 0.9, 0.999, 1e-8, self.weight_decay, self.step_count, packs, L, _stream()))

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libcmb.so")
 SOURCES = ["capi.cu", "graph.cu", "order.cu", "sample.cu", "features.cu", "shard.cu", "peer.cu", "runtime.cu", "cache.cu", "reorder.cu",
-           "sage_layer.cu", "train.cu"]
+           "sage_layer.cu", "train.cu", "dense.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v",
@@ -56,7 +56,7 @@ def build(force=False, verbose=False, out=None, defines=()):
         objs.append(obj)
     tmp = so + ".tmp"
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp,
-                           *objs, "-lcudart"])
+                           *objs, "-lcudart", "-lcublasLt"])
     os.replace(tmp, so)
     return so
 

@@ -134,6 +134,7 @@ struct PackTable {
   int in_dim[kMaxPackLayers], out_dim[kMaxPackLayers];
   __nv_bfloat16* img[kMaxPackLayers];
   __nv_bfloat16* img_t[kMaxPackLayers];
+  int dense[kMaxPackLayers];  // img in the dense.cu layout: row (h * Fp + c), column o
 };
 
 __global__ void __launch_bounds__(256)
@@ -161,6 +162,11 @@ __global__ void __launch_bounds__(256)
       const int r = static_cast<int>(j - h * per);
       const int c = r / fo, o = r - c * fo;
       const __nv_bfloat16 bv = __float2bfloat16_rn(wk);
+      if (t.dense[l]) {
+        const int64_t fp = (F + 7) / 8 * 8;
+        t.img[l][(h * fp + c) * fo + o] = bv;
+        continue;
+      }
       t.img[l][sw128_off(o, h, c, (F + 63) / 64, fo) >> 1] = bv;
       if (t.img_t[l]) t.img_t[l][sw128_off(c, h, o, (fo + 63) / 64, F) >> 1] = bv;
     }
@@ -243,15 +249,18 @@ cmb_status cmb_adam_step_pack(float* w, const float* g, float* m, float* v, int6
   int64_t at = 0;
   for (int l = 0; l < n_layers; ++l) {
     const cmb_layer_pack& L = layers[l];
-    CMB_ARG(L.offset == at && L.in_dim >= 1 && L.in_dim <= 256 && L.out_dim >= 16 &&
-                L.out_dim <= 256 && L.out_dim % 16 == 0 && L.img,
+    CMB_ARG(L.offset == at && L.in_dim >= 1 && (L.dense || L.in_dim <= 256) &&
+                L.out_dim >= 16 && L.out_dim <= 256 && L.out_dim % 16 == 0 && L.img &&
+                (!L.dense || !L.img_t),
             "cmb_adam_step_pack: layer %d: offsets must tile the buffer in order, 1 <= in_dim <= "
-            "256, out_dim in [16, 256] a multiple of 16, img non-null", l);
+            "256 (any for a dense image), out_dim in [16, 256] a multiple of 16, img non-null, "
+            "no transposed image with a dense one", l);
     t.offset[l] = L.offset;
     t.in_dim[l] = L.in_dim;
     t.out_dim[l] = L.out_dim;
     t.img[l] = static_cast<__nv_bfloat16*>(L.img);
     t.img_t[l] = static_cast<__nv_bfloat16*>(L.img_t);
+    t.dense[l] = L.dense ? 1 : 0;
     at += 2ll * L.in_dim * L.out_dim + L.out_dim;
   }
   CMB_ARG(at == n, "cmb_adam_step_pack: the layers cover %lld parameters, n = %lld",

@@ -238,6 +238,60 @@ def test_layer_backward_edge_cases():
         layer.backward_workspace()
 
 
+# ---------------------------------------------------------------- wide rows (cmb_sage_dense_*)
+@pytest.mark.parametrize("name,factor,fo,relu,out_bf16", [
+    ("reddit", 0.01, 256, True, True),       # F = 602 (ld 604): the case the fused layer can't hold
+    ("reddit", 0.01, 64, False, False),
+    ("products", 0.01, 256, True, True),     # F = 100: the same layer through the unfused path
+])
+def test_dense_layer_parity(name, factor, fo, relu, out_bf16):
+    """NEXT-4 for F > 128 (R26 / R27 on the a4 + a5 outputs, bf16 operands, cuBLASLt GEMMs):
+    forward within the R26 bound, weight gradients within the R27 bound, rows past n zero."""
+    b, prep, g = _bundle(name, factor)
+    cfg = b.cfg
+    F, L = cfg.feat_dim, len(cfg.fanouts)
+    ws, wn, bias = _weights(F, fo, 9)
+    layer = cmb.DenseSageLayer(ws, wn, bias, relu=relu, out_bf16=out_bf16)
+    order = oracle.order_roots(b.train, b.comm, cfg.num_communities, oracle.MODE_RAND, 0.0, SEED, 0)
+    roots = oracle.batch_roots(order, cfg.batch_size, 1)
+    sampler = cmb.Sampler(g, len(roots), cfg.fanouts)
+    sampler.sample(torch.from_numpy(roots).cuda(), cfg.p_intra, SEED, 1)
+    y = sampler.sage_dense_layer(layer)
+    torch.cuda.synchronize()
+    assert sampler.status() == 0
+    ref = oracle.run_batch(prep, b.X, F, roots, cfg.fanouts, cfg.p_intra, SEED, 1)
+    nd = ref["n"][L - 1]
+    _check(y[:nd].float().cpu().numpy().astype(np.float64), ref, nd, F, ws, wn, bias, relu,
+           out_bf16)
+    assert torch.all(y[nd:] == 0)
+    # backward on the same batch: dY bf16 test input, Y the oracle's bf16 forward (mask source)
+    Xd = ref["X_in"][:nd, :F].astype(np.float64)
+    H = ref["H64"][:, :F]
+    gen = torch.Generator().manual_seed(4)
+    dY = (torch.randn(nd, fo, generator=gen) * 0.01).to(torch.bfloat16)
+    Yo = torch.from_numpy(oracle.sage_conv(Xd, H, ws.double().numpy(), wn.double().numpy(),
+                                           bias.double().numpy(), relu=True)).to(torch.bfloat16)
+    cap = sampler.n_cap[L - 1]
+    dy_d = torch.zeros(cap, fo, dtype=torch.bfloat16, device="cuda")
+    dy_d[:nd] = dY.cuda()
+    y_d = None
+    if relu:
+        y_d = torch.zeros_like(dy_d)
+        y_d[:nd] = Yo.cuda()
+    dws, dwn, db = sampler.sage_dense_backward(layer, dy_d, y_d)
+    torch.cuda.synchronize()
+    dZ = dY.double().numpy()
+    if relu:
+        dZ = dZ * (Yo.double().numpy() > 0)
+    rs, rn, rb = oracle.sage_conv_backward(Xd, H, dZ)
+    for got, ref_, A in ((dws, rs, Xd), (dwn, rn, H)):
+        S = np.abs(A).T @ np.abs(dZ)
+        err = np.abs(got.double().cpu().numpy() - ref_)
+        assert np.all(err <= 2.0 ** -7 * S + 1e-30), float(np.max(err - 2.0 ** -7 * S))
+    errb = np.abs(db.double().cpu().numpy() - rb)
+    assert np.all(errb <= 2.0 ** -12 * np.abs(dZ).sum(0) + 1e-30), float(np.max(errb))
+
+
 # ---------------------------------------------------------------- GCN variant (reading R28)
 @pytest.mark.parametrize("name,factor,fo,relu,out_bf16", [
     ("tiny", None, 64, True, False),

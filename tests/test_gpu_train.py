@@ -101,7 +101,8 @@ def _bf16(t):
     return t.to(torch.bfloat16).float().cpu().double().numpy()
 
 
-@pytest.mark.parametrize("name,factor", [("tiny", None), ("products", 0.01), ("arxiv", None)])
+@pytest.mark.parametrize("name,factor", [("tiny", None), ("products", 0.01), ("arxiv", None),
+                                         ("reddit", 0.01)])
 def test_train_step_matches_the_oracle_chain(name, factor):
     """One step of the model (layers = hops) on a RAND batch, in two parts.
     (1) Plumbing, elementwise: every layer's weight gradient equals oracle.sage_conv_backward on
