@@ -343,10 +343,11 @@ def test_gcn_layer_backward_parity(name, factor, fo, relu):
     layer = cmb.GcnLayer(W, bias, relu=relu, out_bf16=True)
     order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_COMM, 0.5,
                                SEED, 0)
-    roots = oracle.batch_roots(order, b.cfg.batch_size, 2)
+    roots = oracle.batch_roots(order, b.cfg.batch_size, 1)   # every config has >= 2 batches
+    assert len(roots) > 0
     sampler = cmb.Sampler(g, len(roots), b.cfg.fanouts)
-    sampler.sample(torch.from_numpy(roots).cuda(), b.cfg.p_intra, SEED, 2)
-    ref = oracle.run_batch(prep, b.X, F, roots, b.cfg.fanouts, b.cfg.p_intra, SEED, 2)
+    sampler.sample(torch.from_numpy(roots).cuda(), b.cfg.p_intra, SEED, 1)
+    ref = oracle.run_batch(prep, b.X, F, roots, b.cfg.fanouts, b.cfg.p_intra, SEED, 1)
     nd = ref["n"][L - 1]
     ip, ix = ref["indptr"][L - 1], ref["indices"][L - 1]
     X = ref["X_in"][:, :F].astype(np.float64)
