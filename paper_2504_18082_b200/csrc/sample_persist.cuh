@@ -458,7 +458,10 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   };
   // thread per row when the block has many rows (every thread busy); G-lane groups when the
   // rows are few (small hops: spread each row's f draws over lanes instead)
-  if (f <= 16 && (hi - lo) * G > PB) {
+#ifndef CMB_SAMPLER_ROWS_PER_THREAD  // rows per thread above which a thread takes a whole row
+#define CMB_SAMPLER_ROWS_PER_THREAD 0  // (layout experiments only; 0: whenever G-lane groups
+#endif                                 // would need more than one pass over the block's rows)
+  if (f <= 16 && (hi - lo) * G > PB && (hi - lo) > static_cast<int64_t>(PB) * CMB_SAMPLER_ROWS_PER_THREAD) {
     for (int64_t i = lo + threadIdx.x; i < hi; i += PB) {
       int32_t v, off;
       int64_t rs, deg;
@@ -620,6 +623,10 @@ __device__ __forceinline__ void run_batch(const PArgs& a) {
     if (h > 0) phase_relabel<PB>(a, h - 1);
     CMB_PROF(a, pk);                                  // +0 relabel(h-1)
     const int f = a.fan[h];
+#if defined(CMB_SAMPLER_G8)
+    if (f <= 8) phase_count_sample<PB, 8>(a, h, sm, pk, tag);
+    else
+#endif
     if (f <= 16) phase_count_sample<PB, 16>(a, h, sm, pk, tag);
     else phase_count_sample<PB, 32>(a, h, sm, pk, tag);  // +1 count, +2 prefix, +3 positions
     CMB_PROF(a, pk);                                  // +4 picks + marks
