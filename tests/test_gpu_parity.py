@@ -285,6 +285,54 @@ def test_capacity_and_argument_errors():
     assert s2.status() == 0          # sticky word cleared by the read
 
 
+def test_out_of_range_ids_are_flagged_not_followed():
+    """A root id outside [0, N) (or negative) sets CMB_ERR_INVALID_INPUT and is never used as an
+    address: its row samples nothing, node 0 stands in for it in the outputs, the fused gather
+    stays inside the table, and the other roots' rows are unaffected.  Train ids outside [0, N)
+    in the root order are flagged the same way."""
+    b, prep, g = _bundle("tiny")
+    cfg = b.cfg
+    N = cfg.num_nodes
+    s = cmb.Sampler(g, 8, (5, 5))
+    good = b.train[:3].astype(np.int32)
+    for bad in (N, N + 12345, -7, 2 ** 31 - 1):
+        roots = np.array([good[0], bad, good[1], good[2]], dtype=np.int32)
+        view = s.sample(torch.from_numpy(roots).cuda(), 0.9, SEED, 3)
+        x_in, h = s.gather_aggregate()
+        torch.cuda.synchronize()
+        assert s.status() == 7
+        n, e = view.host_sizes()
+        nodes = view.nodes[: n[-1]].cpu().numpy()
+        assert nodes[1] == 0 and np.all((nodes >= 0) & (nodes < N))
+        ip0 = view.indptr[0][: n[0] + 1].cpu().numpy()
+        assert ip0[2] - ip0[1] == 0           # the bad root's row is empty
+        # the first root's picks depend only on (root, hop, batch): the oracle's, in global ids
+        ref = oracle.sample_blocks(prep, good[:1], (5,), 0.9, SEED, 3)
+        got = nodes[view.indices[0][: ip0[1]].cpu().numpy()]
+        assert np.array_equal(got, ref["nbr"][0])
+    ro = cmb.RootOrderer(g, torch.tensor([1, 5, N + 3], dtype=torch.int32))
+    ro.order("comm", 0.5, SEED, 0)
+    torch.cuda.synchronize()
+    assert ro.status() == 7
+
+
+def test_load_graph_checks_row_offsets():
+    """validate=1: indptr[0] != 0 or indptr[N] != nnz (a tail past the index array) is rejected
+    before any row is read."""
+    from conftest import star_graph
+    ip, ix, comm, C, hub = star_graph(3, 2, 2)
+    bad = ip.copy()
+    bad[-1] += 5                      # the last row claims entries past nnz
+    with pytest.raises(cmb.CmbError) as ei:
+        cmb.Graph(bad, ix, comm, C)
+    assert ei.value.code == 2
+    bad = ip.copy()
+    bad[0] = 1
+    with pytest.raises(cmb.CmbError) as ei:
+        cmb.Graph(bad, ix, comm, C)
+    assert ei.value.code == 2
+
+
 def test_deterministic_repeat():
     b, prep, g = _bundle("products", 0.01)
     s = cmb.Sampler(g, 512, (15, 10, 5))

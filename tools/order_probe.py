@@ -19,7 +19,8 @@ def main():
     cfg = CONFIGS[os.environ.get("CFG", "products")]
     K = int(os.environ.get("K", "24"))
     b = generate(cfg)
-    g = cmb.Graph.from_bundle(b)
+    from gen.device import feature_table
+    g = cmb.Graph.from_bundle(b, features=feature_table(b, "cuda"))
     L = len(cfg.fanouts)
     out = {}
     for mode, mix, p in ((os.environ.get("MODE", "rand"), float(os.environ.get("MIX", "0")),
