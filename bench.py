@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--shard", default="none", choices=["none", "ipc", "a2a"],
                     help="row-shard the feature table over the ranks (a6): ipc = one-sided "
                          "gather of peer shards mapped by CUDA IPC, a2a = NCCL all-to-all")
+    ap.add_argument("--dst-order", default="on", choices=["on", "off"],
+                    help="let the sampler write the last hop's dst visiting order for the fused "
+                         "gather (cmb_blocks.dst_order; same bytes either way) -- A/B switch")
     ap.add_argument("--cpu-workers", type=int, default=0,
                     help="threads of the batch-parallel oracle baseline (0 = all host cores)")
     return ap.parse_args()
@@ -345,6 +348,7 @@ def workload_config(args, cfg, bundle, p, flush=False):
             "num_nodes": cfg.num_nodes, "nnz": int(bundle.nnz), "feat_dim": cfg.feat_dim,
             "batch": cfg.batch_size, "fanouts_hop_order": list(cfg.fanouts),
             "knob1": args.mode + (f"(k={args.mix})" if args.mode.startswith("comm") else ""),
+            "dst_order": args.dst_order,
             "p_intra": p, "knob2_law": args.law, "seed": args.seed,
             "l2": ("L2 flushed (256 MB write) before every launch group of %d batches; "
                    "ms = sum of the groups' device events (X %.0f MB, CSR %.0f MB)"
@@ -409,6 +413,8 @@ def run_cmb(args, bundle):
     pipe = cmb.BatchedPipeline(graph, torch.from_numpy(bundle.train), cfg.batch_size,
                                cfg.fanouts, mode=args.mode, mix=args.mix, p=p, seed=args.seed,
                                nb=G, law=args.law)
+    for smp in pipe.samplers:
+        smp.set_dst_order(args.dst_order == "on")
     nb = pipe.n_batches
     stream = torch.cuda.current_stream()
     K, W = args.steps, args.warmup
