@@ -464,8 +464,7 @@ def run_cmb(args, bundle):
             evlog.append({"sample": (evs[0], evs[1]),
                           "gather": [(evs[2 + 2 * i], evs[3 + 2 * i]) for i in range(cnt)]})
             n_groups += 1
-            for i, s in enumerate(ss):
-                sizes_log[k0 + i].copy_(s.sizes, non_blocking=True)
+            sizes_log[k0:k0 + cnt].copy_(pipe.group_sizes[:cnt], non_blocking=True)
         end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -765,10 +764,9 @@ def run_e2e(args, pipe, cfg, stream, K, W, world, rank):
             r.copy_(order_host[lo:hi], non_blocking=True)
             h2d += (hi - lo) * 4
             roots.append(r)
-        ss = pipe.step_group(gbs, roots=roots)
-        for i, smp in enumerate(ss):
-            sizes_host[slot][i].copy_(smp.sizes, non_blocking=True)
-            d2h += sizes_host[slot].shape[1] * 8
+        pipe.step_group(gbs, roots=roots)
+        sizes_host[slot][:count].copy_(pipe.group_sizes[:count], non_blocking=True)
+        d2h += count * sizes_host[slot].shape[1] * 8
         done[slot].record()
         return count
 

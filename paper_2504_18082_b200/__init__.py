@@ -1182,6 +1182,12 @@ class BatchedPipeline(MiniBatchPipeline):
             raise ValueError(f"nb must be in [1, {MAX_BATCHES_PER_LAUNCH}]")
         self.samplers = [self.sampler] + [Sampler(graph, self.batch_size, fanouts)
                                           for _ in range(self.nb - 1)]
+        # the samplers' size vectors as rows of one tensor: a group's sizes are one copy away
+        L = self.sampler.L
+        self.group_sizes = torch.zeros(self.nb, 2 * L + 1, dtype=torch.int64, device=graph.device)
+        for i, s in enumerate(self.samplers):
+            s.sizes = self.group_sizes[i]
+            s._blocks.sizes = s.sizes.data_ptr()
         # step-executor argument arrays, filled once (per group only roots / ids change)
         self._batches = (Batch * self.nb)()
         self._feats = (BatchFeatures * self.nb)()

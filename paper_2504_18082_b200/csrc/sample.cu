@@ -11,15 +11,17 @@ namespace {
 
 constexpr int kMaxPersistBlocks = pst::kMaxBlocks;
 
-// Workspace layout (all 256-B aligned).  The caller zero-initialises it once: the status
-// word, the tag counter and the tagged dedup map start at zero and are kept consistent by the
-// kernel itself from then on (a workspace belongs to one graph).
+// Workspace layout (all 256-B aligned).  The caller zero-initialises it once: the status word,
+// the grid-barrier words, the tagged block aggregates, the tag counter, the tagged dedup map and
+// the dst-order buckets start at zero and the kernel leaves them consistent after every batch
+// (the barrier's arrival count returns to 0, aggregates and map entries are tagged by batch, the
+// buckets are cleared after use) -- no per-batch memset.  A workspace belongs to one graph.
 struct SampleWs {
   WsHeader* hdr;
   unsigned* bar;             // grid barrier {arrivals, generation}
   unsigned long long* pub;   // [2][kMaxPersistBlocks] tagged block aggregates
-  uint32_t* hist;            // [kOrderBuckets] dst rows of hop L-1 per node-id bucket
-  uint32_t* cursor;          // [kOrderBuckets] rows placed so far per bucket
+  uint32_t* hist;            // [kOrderBuckets] dst rows of hop L-1 per node-id bucket, then
+  uint32_t* cursor;          // [kOrderBuckets] rows placed so far per bucket (contiguous)
   uint64_t* prof;            // [kMaxPersistBlocks][64] sub-step timeline
   unsigned* tag_ctr;         // [1] batch tag of the last batch
   unsigned long long* map;   // [N] tagged dedup map
@@ -38,8 +40,8 @@ SampleWs carve_sample_ws(void* base, int64_t n_roots, const int32_t* fanouts, in
   w.hdr = c.take<WsHeader>(1);
   w.bar = c.take<unsigned>(64);
   w.pub = c.take<unsigned long long>(2 * kMaxPersistBlocks);  // follows bar contiguously
-  w.hist = c.take<uint32_t>(pst::kOrderBuckets);               // then hist, cursor: the
-  w.cursor = c.take<uint32_t>(pst::kOrderBuckets);             // per-batch memset clears all
+  w.hist = c.take<uint32_t>(2 * pst::kOrderBuckets);
+  w.cursor = w.hist + pst::kOrderBuckets;
   w.prof = c.take<uint64_t>(static_cast<size_t>(kMaxPersistBlocks) * 64);
   w.tag_ctr = c.take<unsigned>(1);
   w.map = c.take<unsigned long long>(static_cast<size_t>(num_nodes));
@@ -181,12 +183,6 @@ cmb_status cmb_sample_blocks_multi(const cmb_graph* g, const cmb_batch* batches,
     SampleWs w = carve_sample_ws(b.workspace, b.n_roots, fanouts, n_hops, g->d.n, nullptr);
     fill_args(m.a[i], g, b.roots, b.n_roots, fanouts, n_hops, wi, wo, k0, k1, b.batch_id, b.out,
               w, law);
-    // barrier state, tagged aggregates and the dst-order buckets (contiguous) are cleared for
-    // every batch
-    CMB_CUDA(cudaMemsetAsync(w.bar, 0,
-                             reinterpret_cast<char*>(w.cursor + pst::kOrderBuckets) -
-                                 reinterpret_cast<char*>(w.bar),
-                             s));
   }
   return launch_persistent(g, m, s);
 }

@@ -137,6 +137,12 @@ struct Smem {
   RowCache rows;
 };
 
+// The tag of a published aggregate: this batch's map tag and the hop, so entries left by earlier
+// batches or hops never match and the array needs no clearing between batches.
+__device__ __forceinline__ unsigned pub_tag(unsigned long long tag, int h) {
+  return (static_cast<unsigned>(tag >> 32) << 4) | static_cast<unsigned>(h + 1);
+}
+
 // Block b publishes its aggregate (tagged) and adds the aggregates of blocks [0, b) as they
 // appear.  Every block publishes before it waits -> the wait always ends.  Only the numbers
 // are exchanged, so relaxed accesses suffice.
@@ -429,7 +435,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
     run += agg;
   }
   CMB_PROF(a, pk);
-  const int32_t base = publish_and_prefix<PB>(a.pub, static_cast<unsigned>(h + 1), run, sm);
+  const int32_t base = publish_and_prefix<PB>(a.pub, pub_tag(tag, h), run, sm);
   CMB_PROF(a, pk);
   if (vblk() == vgrid() - 1 && threadIdx.x == 0) {
     a.indptr[h][n_h] = base + run;
@@ -569,7 +575,7 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   }
   CMB_PROF(a, pk);
   const int32_t base =
-      publish_and_prefix<PB>(a.pub + kMaxBlocks, static_cast<unsigned>(h + 1), run, sm);
+      publish_and_prefix<PB>(a.pub + kMaxBlocks, pub_tag(tag, h), run, sm);
   CMB_PROF(a, pk);
   if (vblk() == vgrid() - 1 && threadIdx.x == 0) a.sizes[h + 1] = n_h + base + run;
   for (int64_t e = lo + threadIdx.x; e < hi; e += PB) {
@@ -639,6 +645,8 @@ __device__ __forceinline__ void run_batch(const PArgs& a) {
     CMB_PROF(a, pk);                                  // +9 barrier
   }
   phase_relabel<PB>(a, a.L - 1);
+  if (a.order && vblk() == 0)  // the dst-order buckets, used up (grid barrier above): cleared
+    for (int i = threadIdx.x; i < 2 * kOrderBuckets; i += PB) a.hist[i] = 0u;  // (hist, cursor)
   CMB_PROF(a, pk);
 }
 
