@@ -306,10 +306,20 @@ typedef struct {
   int64_t n_last_dst_cap; /* n_cap[L-1] of the batch's blocks */
   int64_t nodes_cap;      /* n_cap[L]                         */
 } cmb_batch_features;
+/* a4 + a5 of n_batches (<= CMB_MAX_BATCHES_PER_LAUNCH) sampled batches in ONE launch: exactly
+ * cmb_gather_aggregate of each (same outputs, byte for byte), their dst rows walked as one
+ * sequence so the batches share the launch (no gap and no tail between them).  blocks[j] and
+ * feats[j] as cmb_gather_aggregate's arguments; every batch needs new_src_mask and
+ * last_src_ids, 16-B aligned output rows and a 16-B aligned feature table. */
+CMB_API cmb_status cmb_gather_aggregate_multi(const cmb_graph* g, const cmb_blocks* const* blocks,
+                                              const cmb_batch_features* feats, int32_t n_batches,
+                                              int32_t n_hops, void* stream);
 /* One launch group of the step, enqueued by ONE call: cmb_sample_blocks_multi over the
- * n_batches batches, then cmb_gather_aggregate of each (same arguments and results as calling
- * them in that order).  events: NULL, or 2 + 2 * n_batches cudaEvent_t (entries may be NULL)
- * recorded on `stream` before/after the sampler launch and before/after every gather. */
+ * n_batches batches, then cmb_gather_aggregate_multi over them (same results as
+ * cmb_gather_aggregate of each).  events: NULL, or 2 + 2 * n_batches cudaEvent_t (entries may be
+ * NULL) recorded on `stream` before/after the sampler launch and around the gather launch:
+ * events[2], events[3] bracket it, events[4 ..] are recorded at its end (so per-batch gather
+ * times sum to the launch's). */
 CMB_API cmb_status cmb_step_group(const cmb_graph* g, const cmb_batch* batches,
                                   const cmb_batch_features* feats, int32_t n_batches,
                                   const int32_t* fanouts, int32_t n_hops, double p_intra,

@@ -43,7 +43,8 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sample_workspace_bytes", "cmb_sample_blocks", "cmb_sample_blocks_law",
            "cmb_sample_blocks_multi",
            "cmb_gather_features",
-           "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_shard_plan_workspace_bytes",
+           "cmb_sage_mean_aggregate", "cmb_gather_aggregate", "cmb_gather_aggregate_multi",
+           "cmb_shard_plan_workspace_bytes",
            "cmb_shard_plan", "cmb_gather_rows", "cmb_scatter_rows",
            "cmb_gather_aggregate_sharded", "cmb_ipc_export", "cmb_ipc_open", "cmb_ipc_close",
            "cmb_step_group", "cmb_feature_cache_bytes", "cmb_feature_cache_init",

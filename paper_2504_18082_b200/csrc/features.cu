@@ -356,16 +356,16 @@ void launch_mean(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* 
       mask);
 }
 
-// the default fused form: one warp per dst row (gather_row.cuh).  DMAX = edge rows issued per
-// round: the block's fanout (deg_hint = e_cap / n_cap) clamped to [4, 6] (8 spills at 64
-// registers: reddit's fanout-10 block runs best at 6, 178 vs 212 us)
+// the default fused form: one warp per dst row (gather_row.cuh), all batches of the set in one
+// launch.  DMAX = edge rows issued per round: the block's fanout (deg_hint = e_cap / n_cap)
+// clamped to [4, 6] (8 spills at 64 registers: reddit's fanout-10 block runs best at 6, 178 vs
+// 212 us)
 template <class Rows>
-cmb_status launch_row(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
-                      const int32_t* gid, const int64_t* n_dev, int64_t n_cap, const Rows& rows,
-                      const int32_t* map, int f4, float* out, int64_t out_ld, float* x_in,
-                      int64_t x_in_ld, const uint32_t* mask, int deg_hint,
-                      const int32_t* order = nullptr) {
+cmb_status launch_rows(int sms, cudaStream_t s, const GatherSet& set, const Rows& rows, int f4,
+                       int deg_hint) {
   const int dmax = deg_hint < 6 ? deg_hint : 6;
+  int64_t n_cap = 0;
+  for (int j = 0; j < set.nb; ++j) n_cap += set.n_dst_cap[j];
   const int64_t want = (n_cap + 7) / 8;  // 8 warps (rows) per 256-thread block
   // CMB_ROW_MINB resident 256-thread blocks per SM (4: 64 registers); a compile-time constant for
   // layout experiments (tools/), never a run-time switch
@@ -374,9 +374,7 @@ cmb_status launch_row(int sms, cudaStream_t s, const int32_t* indptr, const int3
 #define CMB_ROWK(D_)                                                                          \
   if (f4 > 32) CMB_ROWK3(D_, true); else CMB_ROWK3(D_, false)
 #define CMB_ROWK3(D_, W_)                                                                     \
-  k_gather_mean_row<D_, CMB_ROW_MINB, W_, Rows><<<grid, 256, 0, s>>>(                                    \
-      indptr, idx, gid, n_dev, n_cap, rows, map, f4, reinterpret_cast<float4*>(out),          \
-      out_ld / 4, reinterpret_cast<float4*>(x_in), x_in_ld / 4, mask, order)
+  k_gather_mean_row<D_, CMB_ROW_MINB, W_, Rows><<<grid, 256, 0, s>>>(set, rows, f4)
   if (dmax <= 4) { CMB_ROWK(4); }
   else if (dmax <= 5) { CMB_ROWK(5); }
   else { CMB_ROWK(6); }
@@ -384,6 +382,37 @@ cmb_status launch_row(int sms, cudaStream_t s, const int32_t* indptr, const int3
 #undef CMB_ROWK3
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
+}
+
+// one batch's operands as entry j of a set
+void set_batch(GatherSet& set, int j, const int32_t* indptr, const int32_t* idx,
+               const int32_t* gid, const int64_t* n_dev, int64_t n_cap, const int32_t* map,
+               float* out, int64_t out_ld, float* x_in, int64_t x_in_ld, const uint32_t* mask,
+               const int32_t* order) {
+  set.indptr[j] = indptr;
+  set.idx[j] = idx;
+  set.gid[j] = gid;
+  set.n_dst_dev[j] = n_dev;
+  set.n_dst_cap[j] = n_cap;
+  set.map[j] = map;
+  set.mask[j] = mask;
+  set.order[j] = order;
+  set.out[j] = reinterpret_cast<float4*>(out);
+  set.out_ld4[j] = out_ld / 4;
+  set.x_in[j] = reinterpret_cast<float4*>(x_in);
+  set.x_in_ld4[j] = x_in_ld / 4;
+}
+
+template <class Rows>
+cmb_status launch_row(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* idx,
+                      const int32_t* gid, const int64_t* n_dev, int64_t n_cap, const Rows& rows,
+                      const int32_t* map, int f4, float* out, int64_t out_ld, float* x_in,
+                      int64_t x_in_ld, const uint32_t* mask, int deg_hint,
+                      const int32_t* order = nullptr) {
+  GatherSet set{};
+  set.nb = 1;
+  set_batch(set, 0, indptr, idx, gid, n_dev, n_cap, map, out, out_ld, x_in, x_in_ld, mask, order);
+  return launch_rows(sms, s, set, rows, f4, deg_hint);
 }
 
 cmb_status mean_dispatch(const int32_t* indptr, const int32_t* idx, const int32_t* gid,
@@ -558,6 +587,40 @@ cmb_status cmb_cache_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, i
                     n_last_dst_cap > 0 ? static_cast<int>(b->indices_cap[L - 1] / n_last_dst_cap)
                                        : 8,
                     b->dst_order);
+}
+
+cmb_status cmb_gather_aggregate_multi(const cmb_graph* g, const cmb_blocks* const* blocks,
+                                      const cmb_batch_features* feats, int32_t n_batches,
+                                      int32_t n_hops, void* stream) {
+  CMB_NVTX("cmb.a4a5.gather_aggregate_multi");
+  CMB_ARG(g && blocks && feats, "cmb_gather_aggregate_multi: null argument");
+  CMB_ARG(n_batches >= 1 && n_batches <= kMaxGatherBatches,
+          "cmb_gather_aggregate_multi: n_batches %d outside [1, %d]", n_batches,
+          kMaxGatherBatches);
+  CMB_ARG(n_hops >= 1 && n_hops <= CMB_MAX_HOPS, "cmb_gather_aggregate_multi: bad n_hops");
+  CMB_ARG(g->d.x != nullptr && g->d.ld % 4 == 0 && aligned16(g->d.x),
+          "cmb_gather_aggregate_multi: needs a 16-B aligned feature table (ld %% 4 == 0)");
+  const int L = n_hops;
+  GatherSet set{};
+  set.nb = n_batches;
+  int deg_hint = 8;
+  for (int j = 0; j < n_batches; ++j) {
+    const cmb_blocks* b = blocks[j];
+    const cmb_batch_features& f = feats[j];
+    CMB_ARG(b && f.x_in && f.h_out && b->new_src_mask && b->last_src_ids,
+            "cmb_gather_aggregate_multi: batch %d: null blocks / outputs / mask / src ids", j);
+    CMB_ARG(f.x_in_ld >= g->d.f && f.h_ld >= g->d.f && f.x_in_ld % 4 == 0 && f.h_ld % 4 == 0 &&
+                aligned16(f.x_in) && aligned16(f.h_out) && f.n_last_dst_cap <= f.nodes_cap,
+            "cmb_gather_aggregate_multi: batch %d: outputs must be 16-B aligned rows, ld >= F", j);
+    set_batch(set, j, b->indptr[L - 1], b->indices[L - 1], b->last_src_ids, b->sizes + (L - 1),
+              f.n_last_dst_cap, b->nodes, f.h_out, f.h_ld, f.x_in, f.x_in_ld, b->new_src_mask,
+              b->dst_order);
+    if (f.n_last_dst_cap > 0) deg_hint = static_cast<int>(b->indices_cap[L - 1] / f.n_last_dst_cap);
+  }
+  return launch_rows(g->num_sms, static_cast<cudaStream_t>(stream), set,
+                     DenseRows{reinterpret_cast<const float4*>(g->d.x),
+                               static_cast<uint32_t>(g->d.ld / 4)},
+                     (g->d.f + 3) / 4, deg_hint);
 }
 
 cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,

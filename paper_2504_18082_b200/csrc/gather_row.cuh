@@ -48,45 +48,79 @@ struct ShardedRows {
   }
 };
 
+// The a4 + a5 operands of up to kMaxGatherBatches independent batches, walked as ONE sequence of
+// dst rows (one launch per launch group instead of one per batch: no launch gap and no tail
+// between the batches).  Batch j's rows are slots [pre_j, pre_{j+1}) of the walk, pre from the
+// device counts n_dst_dev[j] (capped at n_dst_cap[j]).
+constexpr int kMaxGatherBatches = CMB_MAX_BATCHES_PER_LAUNCH;
+struct GatherSet {
+  int nb;
+  const int32_t* indptr[kMaxGatherBatches];  // hop L-1 block: [n_dst + 1]
+  const int32_t* idx[kMaxGatherBatches];     // local src id per edge
+  const int32_t* gid[kMaxGatherBatches];     // global src id per edge
+  const int64_t* n_dst_dev[kMaxGatherBatches];
+  int64_t n_dst_cap[kMaxGatherBatches];
+  const int32_t* map[kMaxGatherBatches];     // nodes: row id of dst node d
+  const uint32_t* mask[kMaxGatherBatches];   // first-occurrence bits per edge
+  const int32_t* order[kMaxGatherBatches];   // visiting order of the dst rows, or NULL
+  float4* out[kMaxGatherBatches];            // H
+  int64_t out_ld4[kMaxGatherBatches];
+  float4* x_in[kMaxGatherBatches];           // X_in
+  int64_t x_in_ld4[kMaxGatherBatches];
+};
+
 template <int DMAX, int MINB, bool WIDE, class Rows>
 __global__ void __launch_bounds__(256, MINB)
-    k_gather_mean_row(const int32_t* __restrict__ indptr, const int32_t* __restrict__ idx,
-                      const int32_t* __restrict__ gid, const int64_t* __restrict__ n_dst_dev,
-                      int64_t n_dst_cap, const __grid_constant__ Rows rows,
-                      const int32_t* __restrict__ map, int f4, float4* __restrict__ out,
-                      int64_t out_ld4, float4* __restrict__ x_in, int64_t x_in_ld4,
-                      const uint32_t* __restrict__ new_mask, const int32_t* __restrict__ order) {
+    k_gather_mean_row(const __grid_constant__ GatherSet S, const __grid_constant__ Rows rows,
+                      int f4) {
   constexpr unsigned kFull = 0xffffffffu;
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
-  const int64_t n_dst = min(*n_dst_dev, n_dst_cap);
+  __shared__ int32_t pre[kMaxGatherBatches + 1];
+  if (threadIdx.x == 0) {
+    int32_t t = 0;
+    pre[0] = 0;
+    for (int j = 0; j < kMaxGatherBatches; ++j) {
+      if (j < S.nb) t += static_cast<int32_t>(min(*S.n_dst_dev[j], S.n_dst_cap[j]));
+      pre[j + 1] = t;
+    }
+  }
+  __syncthreads();
+  const int64_t n_dst = pre[kMaxGatherBatches];
   const int lane = threadIdx.x & 31;
   const int64_t W = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
 
-  // slot k of the walk processes dst row d = order[k] (a permutation of [0, n_dst): rows of
-  // nearby ids together, so the src rows they share are re-read while still in L2) or k
-  struct A { int32_t e0, e1, self, d; };
+  // slot k of the walk: batch b, dst row d = order_b[k - pre_b] (a permutation of the batch's
+  // rows: rows of nearby ids together, so the src rows they share are re-read while still in
+  // L2) or k - pre_b
+  struct A { int32_t e0, e1, self, d, b; };
   struct B { int32_t g, l, first; };
   auto loadA = [&](int64_t k) {
-    A a{0, 0, 0, 0};
+    A a{0, 0, 0, 0, 0};
     if (k < n_dst) {
-      const int32_t d = order ? __ldg(order + k) : static_cast<int32_t>(k);
+      const int32_t kk = static_cast<int32_t>(k);
+      int b = 0;
+#pragma unroll
+      for (int j = 1; j < kMaxGatherBatches; ++j) b += kk >= pre[j];
+      const int32_t r = kk - pre[b];
+      const int32_t d = S.order[b] ? __ldg(S.order[b] + r) : r;
+      a.b = b;
       a.d = d;
-      a.e0 = __ldg(indptr + d);
-      a.e1 = __ldg(indptr + d + 1);
-      a.self = __ldg(map + d);
+      a.e0 = __ldg(S.indptr[b] + d);
+      a.e1 = __ldg(S.indptr[b] + d + 1);
+      a.self = __ldg(S.map[b] + d);
     }
     return a;
   };
   auto loadB = [&](const A& a) {
-    B b{0, 0, 0};
+    B v{0, 0, 0};
     const int32_t e = a.e0 + lane;
     if (e < a.e1) {
-      b.l = __ldg(idx + e);
-      b.g = __ldg(gid + e);
-      b.first = static_cast<int>((__ldg(new_mask + (e >> 5)) >> (e & 31)) & 1u);
+      v.l = __ldg(S.idx[a.b] + e);
+      v.g = __ldg(S.gid[a.b] + e);
+      v.first = static_cast<int>((__ldg(S.mask[a.b] + (e >> 5)) >> (e & 31)) & 1u);
     }
-    return b;
+    return v;
   };
 
   int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -98,6 +132,8 @@ __global__ void __launch_bounds__(256, MINB)
     const B bn = loadB(an);
     const int deg = ac.e1 - ac.e0;
     const unsigned firsts = __ballot_sync(kFull, bc.first);
+    float4* const x_in = S.x_in[ac.b];
+    const int64_t x_in_ld4 = S.x_in_ld4[ac.b];
     // column chunks of 32 float4 (one for F <= 128; wide rows, e.g. F = 602, take several)
     for (int c0 = 0; c0 < (WIDE ? f4 : 1); c0 += 32) {
     const bool col = c0 + lane < f4;
@@ -138,7 +174,8 @@ __global__ void __launch_bounds__(256, MINB)
         h.z = div_small(acc.z, d, y);
         h.w = div_small(acc.w, d, y);
       }
-      st4_hint(out + static_cast<int64_t>(ac.d) * out_ld4 + c0 + lane, h, pol_stream);
+      st4_hint(S.out[ac.b] + static_cast<int64_t>(ac.d) * S.out_ld4[ac.b] + c0 + lane, h,
+               pol_stream);
       st4_hint(x_in + static_cast<int64_t>(ac.d) * x_in_ld4 + c0 + lane, sv, pol_stream);
     }
     }
