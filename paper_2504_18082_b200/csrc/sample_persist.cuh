@@ -476,6 +476,15 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       a.indptr[h][i] = base + off;
       const uint32_t e0 = static_cast<uint32_t>(base + off);
       const PickEmit em{a.g.indices, a.indices[h] + e0, a.map, tag, e0};
+#if defined(CMB_SAMPLER_EXACT_FM)  // layout experiment: slot arrays sized to the exact fanout
+      if (f == 5)
+        row_positions_thread<5>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
+                                a.law);
+      else if (f == 10)
+        row_positions_thread<10>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
+                                 a.law);
+      else
+#endif
       if (f <= 8)
         row_positions_thread<8>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
                                 a.law);
