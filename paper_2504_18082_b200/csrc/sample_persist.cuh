@@ -476,21 +476,24 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       a.indptr[h][i] = base + off;
       const uint32_t e0 = static_cast<uint32_t>(base + off);
       const PickEmit em{a.g.indices, a.indices[h] + e0, a.map, tag, e0};
-#if defined(CMB_SAMPLER_EXACT_FM)  // layout experiment: slot arrays sized to the exact fanout
-      if (f == 5)
-        row_positions_thread<5>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
-                                a.law);
-      else if (f == 10)
-        row_positions_thread<10>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
-                                 a.law);
-      else
-#endif
-      if (f <= 8)
-        row_positions_thread<8>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
-                                a.law);
-      else
-        row_positions_thread<16>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em,
-                                 a.law);
+      // the slot arrays are sized to the fanout: an unrolled slot a row does not use still
+      // issues its (predicated) Philox rounds -- exact sizes for the per-row fanouts of the
+      // BASELINE configs' big hops (5, 10) cut the sampler 3.5 % on products (f = 5 was an
+      // 8-slot form); other fanouts round up to 8 or 16 slots (more exact sizes spill)
+      switch (f) {
+#define CMB_ROWPOS(FM_)                                                                      \
+    row_positions_thread<FM_>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em, \
+                              a.law);                                                        \
+    break;
+        case 5: CMB_ROWPOS(5)
+        case 10: CMB_ROWPOS(10)
+        default:
+          if (f <= 8) {
+            CMB_ROWPOS(8)
+          }
+          CMB_ROWPOS(16)
+#undef CMB_ROWPOS
+      }
     }
   } else {
     const int lane = threadIdx.x & (G - 1);
