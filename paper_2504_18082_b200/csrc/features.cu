@@ -81,7 +81,7 @@ __global__ void k_gather_scalar(const float* __restrict__ x, int64_t ld,
   }
 }
 
-// Pipelined row form (the unfused a5 path; CMB_AGG_KERNEL=p for the fused one): one group of
+// Pipelined row form (the kernel of the unfused cmb_sage_mean_aggregate): one group of
 // LPR lanes per dst row, rows visited with
 // a grid stride, and the index chain of the rows AHEAD is issued before the feature loads of
 // the current row: stage A (row i+2G) loads indptr pair + self node id, stage B (row i+G)
