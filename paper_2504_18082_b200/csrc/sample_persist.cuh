@@ -36,6 +36,51 @@ constexpr int kOrderBuckets = 1 << kOrderBits;
 constexpr uint32_t kFinal = 0x80000000u;
 constexpr uint32_t kMarkerTop = 0x7FFFFFFFu;
 
+// Accesses to the tagged dedup map.  CMB_MAP_EVICT_LAST (layout experiment) marks them L2
+// evict_last, so the maps of a launch group's workspaces survive the gathers that stream through
+// L2 between two sampler launches.
+#if defined(CMB_MAP_EVICT_LAST)
+__device__ __forceinline__ uint64_t map_pol() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long map_ld(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.global.cg.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(map_pol()));
+  return v;
+}
+__device__ __forceinline__ void map_st(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(map_pol())
+               : "memory");
+}
+__device__ __forceinline__ void map_max(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.global.max.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(map_pol())
+               : "memory");
+}
+__device__ __forceinline__ unsigned long long map_exch(unsigned long long* p,
+                                                       unsigned long long v) {
+  unsigned long long o;
+  asm volatile("atom.global.exch.L2::cache_hint.b64 %0, [%1], %2, %3;"
+               : "=l"(o)
+               : "l"(p), "l"(v), "l"(map_pol())
+               : "memory");
+  return o;
+}
+#else
+__device__ __forceinline__ unsigned long long map_ld(const unsigned long long* p) {
+  return __ldcg(p);
+}
+__device__ __forceinline__ void map_st(unsigned long long* p, unsigned long long v) { *p = v; }
+__device__ __forceinline__ void map_max(unsigned long long* p, unsigned long long v) {
+  atomicMax(p, v);
+}
+__device__ __forceinline__ unsigned long long map_exch(unsigned long long* p,
+                                                       unsigned long long v) {
+  return atomicExch(p, v);
+}
+#endif
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -189,7 +234,7 @@ __device__ void phase_relabel(const PArgs& a, int h) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) u[k] = e0 + k * stride < e_h ? __ldcg(ind + e0 + k * stride) : 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = e0 + k * stride < e_h ? __ldcg(a.map + u[k]) : 0ull;
+    for (int k = 0; k < 4; ++k) v[k] = e0 + k * stride < e_h ? map_ld(a.map + u[k]) : 0ull;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t e = e0 + k * stride;
@@ -220,7 +265,7 @@ struct PickEmit {
     const unsigned long long m = tag | (kMarkerTop - (e0 + static_cast<uint32_t>(k)));
     // read the entry first: a node picked by many rows (hubs; every pick of a community at
     // p = 1) would otherwise queue one same-address atomic per pick in L2
-    if (__ldcg(map + u) < m) atomicMax(map + u, m);
+    if (map_ld(map + u) < m) map_max(map + u, m);
   }
 };
 
@@ -566,7 +611,7 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
 #pragma unroll
     for (int k = 0; k < kTiles; ++k) {  // all loads of up to kTiles tiles in flight
       const int64_t e = c0 + k * PB + threadIdx.x;
-      fl[k] = e < hi && __ldcg(a.map + __ldcg(nbr + e)) ==
+      fl[k] = e < hi && map_ld(a.map + __ldcg(nbr + e)) ==
                             (tag | (kMarkerTop - static_cast<uint32_t>(e)));
     }
 #pragma unroll
@@ -596,7 +641,7 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       const uint32_t id = static_cast<uint32_t>(n_h + base + (sc & 0x7fffffffu) - 1);
       const int32_t u = __ldcg(nbr + e);
       a.nodes[id] = u;
-      a.map[u] = tag | kFinal | id;
+      map_st(a.map + u, tag | kFinal | id);
     }
   }
 }
@@ -630,7 +675,7 @@ __device__ __forceinline__ void run_batch(const PArgs& a) {
       continue;
     }
     a.nodes[i] = static_cast<int32_t>(u);
-    const unsigned long long old = atomicExch(a.map + u, tag | kFinal | static_cast<uint32_t>(i));
+    const unsigned long long old = map_exch(a.map + u, tag | kFinal | static_cast<uint32_t>(i));
     // duplicate root <=> the entry already holds a final id of THIS batch (a marker of this
     // batch -- hop-0 picks run concurrently -- is not a duplicate: the final id replaces it)
     if ((old & 0xffffffff00000000ull) == tag && (static_cast<uint32_t>(old) & kFinal))
