@@ -97,11 +97,7 @@ __global__ void k_gather_scalar(const float* __restrict__ x, int64_t ld,
 #endif
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
-#if defined(CMB_GATHER_EVICT_NORMAL)  // layout experiment: feature rows loaded evict_normal
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-#else
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-#endif
   return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {

@@ -36,10 +36,11 @@ constexpr int kOrderBuckets = 1 << kOrderBits;
 constexpr uint32_t kFinal = 0x80000000u;
 constexpr uint32_t kMarkerTop = 0x7FFFFFFFu;
 
-// Accesses to the tagged dedup map.  CMB_MAP_EVICT_LAST (layout experiment) marks them L2
-// evict_last, so the maps of a launch group's workspaces survive the gathers that stream through
-// L2 between two sampler launches.
-#if defined(CMB_MAP_EVICT_LAST)
+// Accesses to the tagged dedup map are marked L2 evict_last: the maps of a launch group's
+// workspaces (4 x 19.6 MB on products) then survive the gathers that stream ~2.4 GB through L2
+// between two sampler launches, and a batch's first touches of map entries hit L2 instead of
+// DRAM (sampler 81.0 -> 76.6 us per batch, gather 108.9 -> 109.4: 190.7 -> 186.9 us per step;
+// evict_normal feature loads in the gather instead: 188.0).
 __device__ __forceinline__ uint64_t map_pol() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -54,6 +55,7 @@ __device__ __forceinline__ void map_st(unsigned long long* p, unsigned long long
   asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(map_pol())
                : "memory");
 }
+// atomicMax without a result (a reduction), same policy
 __device__ __forceinline__ void map_max(unsigned long long* p, unsigned long long v) {
   asm volatile("red.global.max.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(map_pol())
                : "memory");
@@ -67,19 +69,6 @@ __device__ __forceinline__ unsigned long long map_exch(unsigned long long* p,
                : "memory");
   return o;
 }
-#else
-__device__ __forceinline__ unsigned long long map_ld(const unsigned long long* p) {
-  return __ldcg(p);
-}
-__device__ __forceinline__ void map_st(unsigned long long* p, unsigned long long v) { *p = v; }
-__device__ __forceinline__ void map_max(unsigned long long* p, unsigned long long v) {
-  atomicMax(p, v);
-}
-__device__ __forceinline__ unsigned long long map_exch(unsigned long long* p,
-                                                       unsigned long long v) {
-  return atomicExch(p, v);
-}
-#endif
 
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
