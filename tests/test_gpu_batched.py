@@ -95,3 +95,27 @@ def test_dst_order_is_a_bucketed_permutation(small, nb):
         torch.cuda.synchronize()
         nl = int(s.sizes[L].item())
         assert torch.equal(x0[:nl], x1[:nl]) and torch.equal(h0[:n], h1[:n])
+
+
+def test_step_group_unaligned_rows_fall_back_per_batch():
+    """cmb_step_group with feature rows that are not 16-byte multiples (F = ld = 15): the
+    one-launch gather needs vector rows, so each batch goes through cmb_gather_aggregate's
+    scalar path -- same bytes as the oracle."""
+    from gen import CONFIGS
+    b = generate(CONFIGS["tiny"])
+    F = 15
+    X = np.ascontiguousarray(b.X[:, :F])
+    g = cmb.Graph(b.indptr, b.indices, b.comm, b.cfg.num_communities, torch.from_numpy(X), F)
+    prep = oracle.graph_prep(b)
+    pipe = cmb.BatchedPipeline(g, torch.from_numpy(b.train), 64, (5, 5), mode="rand", p=0.9,
+                               nb=3)
+    ss = pipe.step_group([0, 1, 2])
+    torch.cuda.synchronize()
+    order = oracle.order_roots(b.train, b.comm, b.cfg.num_communities, oracle.MODE_RAND, 0.0,
+                               42, 0)
+    for bb, s in enumerate(ss):
+        assert s.status() == 0
+        ref = oracle.run_batch(prep, X, F, oracle.batch_roots(order, 64, bb), (5, 5), 0.9, 42, bb)
+        n = s.sizes.cpu().tolist()
+        assert s.x_in[: n[2], :F].cpu().numpy().tobytes() == ref["X_in"].tobytes()
+        assert s.h[: n[1], :F].cpu().numpy().tobytes() == ref["H"].tobytes()
