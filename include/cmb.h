@@ -286,8 +286,10 @@ CMB_API cmb_status cmb_scatter_rows(const float* rows, int64_t rows_ld, const in
  * inv[old] = new; row i of the output is old row perm[i] renamed through inv and sorted;
  * community_out[i] = community[perm[i]] (non-decreasing, ready for cmb_load_graph).  All
  * arrays are device, caller-allocated: perm / inv / community_out [N], indptr_out [N+1],
- * indices_out [nnz].  N and nnz < 2^31.  Feature rows and train ids follow the permutation
- * (e.g. cmb_gather_rows with perm; train_new = sort(inv[train])). */
+ * indices_out [nnz].  N < 2^31; nnz of any size (above 2^31 - 1 entries the rows are sorted in
+ * chunks of <= 2^30 entries, whose boundaries are read back to the host once: the call then
+ * synchronises the stream; a single row must stay below 2^30 entries).  Feature rows and train
+ * ids follow the permutation (e.g. cmb_gather_rows with perm; train_new = sort(inv[train])). */
 CMB_API size_t cmb_community_order_workspace_bytes(int64_t num_nodes, int64_t nnz);
 CMB_API cmb_status cmb_community_order(const int64_t* indptr, const int32_t* indices,
                                        const int32_t* community, int64_t num_nodes, int64_t nnz,

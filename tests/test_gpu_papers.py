@@ -70,3 +70,37 @@ def test_papers_full():
     assert b.indptr[-1] > 2 ** 31  # the int64 CSR offsets are exercised
     n, e = out[0]
     print("papers100M batch 3: n =", n, "e =", e)
+
+
+@pytest.mark.skipif(os.environ.get("CMB_TEST_PAPERS") == "0", reason="CMB_TEST_PAPERS=0")
+def test_papers_community_order_beyond_int32():
+    """NEXT-2 (iii) at papers100M scale (3.2G CSR entries > 2^31 - 1: the row sort runs in
+    chunks).  Input: the community-ordered graph with its two halves (split at a community
+    boundary) swapped -- node v of the first half becomes v + |B|, of the second v - |A| -- so
+    the communities are out of order and every row's neighbour ids are unsorted.  Reading R25
+    (new order = (community, old id)) must give back the original graph exactly: perm = the
+    swap, indptr / indices / communities identical to the generated ones."""
+    cfg = CONFIGS["papers100m"]
+    b = generate(cfg, features=False)
+    n, nnz, C = cfg.num_nodes, int(b.indptr[-1]), cfg.num_communities
+    assert nnz > 2 ** 31
+    cut = int(np.searchsorted(b.comm, C // 2))       # first node of community C/2
+    e0 = int(b.indptr[cut])
+    dev = torch.device("cuda")
+    ip = torch.from_numpy(b.indptr).to(dev)
+    ix = torch.from_numpy(b.indices).to(dev)
+    cm = torch.from_numpy(b.comm).to(dev)
+    nb_ = n - cut                                      # |B|
+    ip_in = torch.cat([ip[cut:] - e0, ip[1:cut + 1] + (nnz - e0)])
+    cm_in = torch.cat([cm[cut:], cm[:cut]])
+    ix_in = torch.cat([ix[e0:], ix[:e0]])
+    step = 1 << 28
+    for s0 in range(0, nnz, step):                     # rename in place, chunk by chunk
+        t = ix_in[s0:s0 + step]
+        t.copy_(torch.where(t < cut, t + nb_, t - cut))
+    perm, inv, ip2, ix2, cm2 = cmb.community_order(ip_in, ix_in, cm_in, C, device=dev)
+    torch.cuda.synchronize()
+    want_perm = torch.cat([torch.arange(nb_, n, device=dev), torch.arange(0, nb_, device=dev)])
+    assert torch.equal(perm.long(), want_perm)
+    assert torch.equal(ip2, ip) and torch.equal(cm2, cm)
+    assert torch.equal(ix2, ix)
