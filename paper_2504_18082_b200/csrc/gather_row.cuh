@@ -130,11 +130,14 @@ __global__ void __launch_bounds__(256, MINB)
     B v{0, 0, 0};
     const int32_t e = a.e0 + lane;
     if (e < a.e1) {
-      if (RELABEL) {  // l = the raw map word (kFinal | local id), masked where it is used: the
-        const int32_t u = __ldcg(S.idx[a.b] + e);  // lookup completes behind a row's loads
+      if (RELABEL) {
+        const int32_t u = __ldcg(S.idx[a.b] + e);
         v.first = static_cast<int>((__ldg(S.mask[a.b] + (e >> 5)) >> (e & 31)) & 1u);
-        v.l = static_cast<int32_t>(static_cast<uint32_t>(ld_map_keep(S.dmap[a.b] + u)));
+        v.l = static_cast<int32_t>(static_cast<uint32_t>(ld_map_keep(S.dmap[a.b] + u)) &
+                                   0x7FFFFFFFu);
         v.g = u;
+        const_cast<int32_t*>(S.idx[a.b])[e] = v.l;   // hop L-1's relabel (a3)
+        const_cast<int32_t*>(S.gid[a.b])[e] = u;     // last_src_ids
       } else {
         v.l = __ldg(S.idx[a.b] + e);
         v.g = __ldg(S.gid[a.b] + e);
@@ -173,17 +176,12 @@ __global__ void __launch_bounds__(256, MINB)
         const int32_t g = __shfl_sync(kFull, bc.g, (base + j) & 31);
         v[j] = ldg4_hint(rows.row(base + j < deg ? g : ac.self) + cl, pol_keep);
       }
-      if (RELABEL && c0 == 0 && base == 0 && lane < deg) {  // after this row's loads: the
-        const int32_t e = ac.e0 + lane;                        // relabel of its edges (a3)
-        const_cast<int32_t*>(S.idx[ac.b])[e] = bc.l & 0x7FFFFFFF;
-        const_cast<int32_t*>(S.gid[ac.b])[e] = bc.g;           // and last_src_ids
-      }
 #pragma unroll
       for (int j = 0; j < DMAX; ++j) {
         if (base + j < deg) {
           add4(acc, v[j]);
           if ((firsts >> (base + j)) & 1u) {  // first occurrence of a new src node
-            const int32_t l = __shfl_sync(kFull, bc.l, base + j) & 0x7FFFFFFF;
+            const int32_t l = __shfl_sync(kFull, bc.l, base + j);
             if (col)
               st4_hint(x_in + static_cast<int64_t>(l) * x_in_ld4 + c0 + lane, v[j], pol_stream);
           }
