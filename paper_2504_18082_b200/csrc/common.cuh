@@ -144,21 +144,6 @@ __host__ __device__ inline uint32_t sw128_off(int r, int h, int c, int kh, int r
 
 }  // namespace cmb
 
-// Internal (not exported) pieces of the step executor (runtime.cu): the sampler with the last
-// hop's relabel left to the one-launch gather (sample.cu), the sampler workspace's dedup map,
-// and that gather (features.cu).
-namespace cmb {
-cmb_status sample_multi(const cmb_graph* g, const cmb_batch* batches, int32_t n_batches,
-                        const int32_t* fanouts, int32_t n_hops, double p_intra, int32_t law,
-                        uint64_t seed, void* stream, int defer_last_relabel);
-const unsigned long long* sample_ws_map(const cmb_graph* g, const cmb_batch& b,
-                                        const int32_t* fanouts, int32_t n_hops);
-cmb_status gather_aggregate_multi(const cmb_graph* g, const cmb_blocks* const* blocks,
-                                  const cmb_batch_features* feats, int32_t n_batches,
-                                  int32_t n_hops, const unsigned long long* const* relabel_maps,
-                                  void* stream);
-}  // namespace cmb
-
 struct cmb_graph {
   cmb::DevGraph d;
   int32_t* status;  // graph workspace header

@@ -360,7 +360,7 @@ void launch_mean(int sms, cudaStream_t s, const int32_t* indptr, const int32_t* 
 // launch.  DMAX = edge rows issued per round: the block's fanout (deg_hint = e_cap / n_cap)
 // clamped to [4, 6] (8 spills at 64 registers: reddit's fanout-10 block runs best at 6, 178 vs
 // 212 us)
-template <class Rows, bool RELABEL = false>
+template <class Rows>
 cmb_status launch_rows(int sms, cudaStream_t s, const GatherSet& set, const Rows& rows, int f4,
                        int deg_hint) {
   const int dmax = deg_hint < 6 ? deg_hint : 6;
@@ -374,7 +374,7 @@ cmb_status launch_rows(int sms, cudaStream_t s, const GatherSet& set, const Rows
 #define CMB_ROWK(D_)                                                                          \
   if (f4 > 32) CMB_ROWK3(D_, true); else CMB_ROWK3(D_, false)
 #define CMB_ROWK3(D_, W_)                                                                     \
-  k_gather_mean_row<D_, CMB_ROW_MINB, W_, RELABEL, Rows><<<grid, 256, 0, s>>>(set, rows, f4)
+  k_gather_mean_row<D_, CMB_ROW_MINB, W_, Rows><<<grid, 256, 0, s>>>(set, rows, f4)
   if (dmax <= 4) { CMB_ROWK(4); }
   else if (dmax <= 5) { CMB_ROWK(5); }
   else { CMB_ROWK(6); }
@@ -592,16 +592,6 @@ cmb_status cmb_cache_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, i
 cmb_status cmb_gather_aggregate_multi(const cmb_graph* g, const cmb_blocks* const* blocks,
                                       const cmb_batch_features* feats, int32_t n_batches,
                                       int32_t n_hops, void* stream) {
-  return cmb::gather_aggregate_multi(g, blocks, feats, n_batches, n_hops, nullptr, stream);
-}
-
-}  // extern "C"
-
-cmb_status cmb::gather_aggregate_multi(const cmb_graph* g, const cmb_blocks* const* blocks,
-                                       const cmb_batch_features* feats, int32_t n_batches,
-                                       int32_t n_hops,
-                                       const unsigned long long* const* relabel_maps,
-                                       void* stream) {
   CMB_NVTX("cmb.a4a5.gather_aggregate_multi");
   CMB_ARG(g && blocks && feats, "cmb_gather_aggregate_multi: null argument");
   CMB_ARG(n_batches >= 1 && n_batches <= kMaxGatherBatches,
@@ -625,17 +615,13 @@ cmb_status cmb::gather_aggregate_multi(const cmb_graph* g, const cmb_blocks* con
     set_batch(set, j, b->indptr[L - 1], b->indices[L - 1], b->last_src_ids, b->sizes + (L - 1),
               f.n_last_dst_cap, b->nodes, f.h_out, f.h_ld, f.x_in, f.x_in_ld, b->new_src_mask,
               b->dst_order);
-    set.dmap[j] = relabel_maps ? relabel_maps[j] : nullptr;
     if (f.n_last_dst_cap > 0) deg_hint = static_cast<int>(b->indices_cap[L - 1] / f.n_last_dst_cap);
   }
-  const DenseRows rows{reinterpret_cast<const float4*>(g->d.x), static_cast<uint32_t>(g->d.ld / 4)};
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (relabel_maps)
-    return launch_rows<DenseRows, true>(g->num_sms, s, set, rows, (g->d.f + 3) / 4, deg_hint);
-  return launch_rows(g->num_sms, s, set, rows, (g->d.f + 3) / 4, deg_hint);
+  return launch_rows(g->num_sms, static_cast<cudaStream_t>(stream), set,
+                     DenseRows{reinterpret_cast<const float4*>(g->d.x),
+                               static_cast<uint32_t>(g->d.ld / 4)},
+                     (g->d.f + 3) / 4, deg_hint);
 }
-
-extern "C" {
 
 cmb_status cmb_gather_aggregate(const cmb_graph* g, const cmb_blocks* b, int32_t n_hops,
                                 int64_t n_last_dst_cap, int64_t nodes_cap, float* x_in,

@@ -67,23 +67,9 @@ struct GatherSet {
   int64_t out_ld4[kMaxGatherBatches];
   float4* x_in[kMaxGatherBatches];           // X_in
   int64_t x_in_ld4[kMaxGatherBatches];
-  // RELABEL form (cmb_step_group): idx still holds the sampler's GLOBAL neighbour ids; the walk
-  // looks each up in the batch's dedup map (final entries: kFinal | local id), writes the local
-  // id back to idx and the global one to gid (last_src_ids) -- the sampler's last relabel pass,
-  // done here where the rows are read anyway
-  const unsigned long long* dmap[kMaxGatherBatches];
 };
 
-// the dedup map's lines are kept in L2 (evict_last, as the sampler marks them)
-__device__ __forceinline__ unsigned long long ld_map_keep(const unsigned long long* p) {
-  unsigned long long v;
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile("ld.global.cg.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
-  return v;
-}
-
-template <int DMAX, int MINB, bool WIDE, bool RELABEL, class Rows>
+template <int DMAX, int MINB, bool WIDE, class Rows>
 __global__ void __launch_bounds__(256, MINB)
     k_gather_mean_row(const __grid_constant__ GatherSet S, const __grid_constant__ Rows rows,
                       int f4) {
@@ -130,19 +116,9 @@ __global__ void __launch_bounds__(256, MINB)
     B v{0, 0, 0};
     const int32_t e = a.e0 + lane;
     if (e < a.e1) {
-      if (RELABEL) {
-        const int32_t u = __ldcg(S.idx[a.b] + e);
-        v.first = static_cast<int>((__ldg(S.mask[a.b] + (e >> 5)) >> (e & 31)) & 1u);
-        v.l = static_cast<int32_t>(static_cast<uint32_t>(ld_map_keep(S.dmap[a.b] + u)) &
-                                   0x7FFFFFFFu);
-        v.g = u;
-        const_cast<int32_t*>(S.idx[a.b])[e] = v.l;   // hop L-1's relabel (a3)
-        const_cast<int32_t*>(S.gid[a.b])[e] = u;     // last_src_ids
-      } else {
-        v.l = __ldg(S.idx[a.b] + e);
-        v.g = __ldg(S.gid[a.b] + e);
-        v.first = static_cast<int>((__ldg(S.mask[a.b] + (e >> 5)) >> (e & 31)) & 1u);
-      }
+      v.l = __ldg(S.idx[a.b] + e);
+      v.g = __ldg(S.gid[a.b] + e);
+      v.first = static_cast<int>((__ldg(S.mask[a.b] + (e >> 5)) >> (e & 31)) & 1u);
     }
     return v;
   };

@@ -21,33 +21,25 @@ cmb_status cmb_step_group(const cmb_graph* g, const cmb_batch* batches,
     if (events && events[i]) CMB_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s));
     return CMB_OK;
   };
-  // the a4 + a5 of every batch of the group in ONE launch (one walk over all their dst rows)
-  // when every operand is 16-byte aligned; that launch also does the last hop's relabel, which
-  // the sampler then skips (the per-batch events bracket the launch: the first batch's pair
-  // spans it, the others are recorded at its end).  Otherwise the sampler relabels and each
-  // batch gets one cmb_gather_aggregate (its scalar path handles unaligned rows).
-  auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-  bool one_launch = g->d.x && a16(g->d.x) && g->d.ld % 4 == 0 && n_batches >= 1 &&
-                    n_batches <= CMB_MAX_BATCHES_PER_LAUNCH;
-  for (int i = 0; i < n_batches && one_launch; ++i)
-    one_launch = a16(feats[i].x_in) && a16(feats[i].h_out) && feats[i].x_in_ld % 4 == 0 &&
-                 feats[i].h_ld % 4 == 0 && batches[i].out && batches[i].out->new_src_mask &&
-                 batches[i].out->last_src_ids;
   cmb_status st = rec(0);
   if (st != CMB_OK) return st;
-  st = sample_multi(g, batches, n_batches, fanouts, n_hops, p_intra, law, seed, stream,
-                    one_launch ? 1 : 0);
+  st = cmb_sample_blocks_multi(g, batches, n_batches, fanouts, n_hops, p_intra, law, seed, stream);
   if (st != CMB_OK) return st;
   if ((st = rec(1)) != CMB_OK) return st;
+  // the a4 + a5 of every batch of the group in ONE launch (one walk over all their dst rows)
+  // when every operand is 16-byte aligned (the per-batch events bracket that launch: the first
+  // batch's pair spans it, the others are recorded at its end); otherwise one
+  // cmb_gather_aggregate per batch (its scalar path handles unaligned rows)
+  auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  bool one_launch = g->d.x && a16(g->d.x) && g->d.ld % 4 == 0;
+  for (int i = 0; i < n_batches && one_launch; ++i)
+    one_launch = a16(feats[i].x_in) && a16(feats[i].h_out) && feats[i].x_in_ld % 4 == 0 &&
+                 feats[i].h_ld % 4 == 0;
   if (one_launch) {
     if ((st = rec(2)) != CMB_OK) return st;
     const cmb_blocks* blocks[CMB_MAX_BATCHES_PER_LAUNCH];
-    const unsigned long long* maps[CMB_MAX_BATCHES_PER_LAUNCH];
-    for (int i = 0; i < n_batches; ++i) {
-      blocks[i] = batches[i].out;
-      maps[i] = sample_ws_map(g, batches[i], fanouts, n_hops);
-    }
-    st = gather_aggregate_multi(g, blocks, feats, n_batches, n_hops, maps, stream);
+    for (int i = 0; i < n_batches; ++i) blocks[i] = batches[i].out;
+    st = cmb_gather_aggregate_multi(g, blocks, feats, n_batches, n_hops, stream);
     if (st != CMB_OK) return st;
     for (int i = 0; i < n_batches; ++i) {
       if (i > 0 && (st = rec(2 + 2 * i)) != CMB_OK) return st;

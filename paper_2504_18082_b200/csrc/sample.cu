@@ -85,7 +85,6 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
   a.order_shift = bits > pst::kOrderBits ? bits - pst::kOrderBits : 0;
   a.status = &w.hdr->status;
   a.law = law;
-  a.defer_last_relabel = 0;
 }
 
 // One 1024-thread block per SM (64 registers: the whole register file), co-resident by
@@ -152,21 +151,6 @@ size_t cmb_sample_workspace_bytes(int64_t n_roots, const int32_t* fanouts, int32
 cmb_status cmb_sample_blocks_multi(const cmb_graph* g, const cmb_batch* batches,
                                    int32_t n_batches, const int32_t* fanouts, int32_t n_hops,
                                    double p_intra, int32_t law, uint64_t seed, void* stream) {
-  return cmb::sample_multi(g, batches, n_batches, fanouts, n_hops, p_intra, law, seed, stream, 0);
-}
-
-}  // extern "C"
-
-namespace cmb {
-
-const unsigned long long* sample_ws_map(const cmb_graph* g, const cmb_batch& b,
-                                        const int32_t* fanouts, int32_t n_hops) {
-  return carve_sample_ws(b.workspace, b.n_roots, fanouts, n_hops, g->d.n, nullptr).map;
-}
-
-cmb_status sample_multi(const cmb_graph* g, const cmb_batch* batches, int32_t n_batches,
-                        const int32_t* fanouts, int32_t n_hops, double p_intra, int32_t law,
-                        uint64_t seed, void* stream, int defer_last_relabel) {
   CMB_NVTX("cmb.a2a3.sample_relabel");
   CMB_ARG(g && batches && fanouts, "cmb_sample_blocks: null graph/batches/fanouts");
   CMB_ARG(n_batches >= 1 && n_batches <= CMB_MAX_BATCHES_PER_LAUNCH,
@@ -199,14 +183,9 @@ cmb_status sample_multi(const cmb_graph* g, const cmb_batch* batches, int32_t n_
     SampleWs w = carve_sample_ws(b.workspace, b.n_roots, fanouts, n_hops, g->d.n, nullptr);
     fill_args(m.a[i], g, b.roots, b.n_roots, fanouts, n_hops, wi, wo, k0, k1, b.batch_id, b.out,
               w, law);
-    m.a[i].defer_last_relabel = defer_last_relabel;
   }
   return launch_persistent(g, m, s);
 }
-
-}  // namespace cmb
-
-extern "C" {
 
 cmb_status cmb_sample_blocks(const cmb_graph* g, const int32_t* roots, int64_t n_roots,
                              const int32_t* fanouts, int32_t n_hops, double p_intra, uint64_t seed,

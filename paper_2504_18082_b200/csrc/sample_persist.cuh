@@ -108,7 +108,6 @@ struct PArgs {
   int order_shift;
   int32_t* status;
   int law;                  // Knob-2 law: 0 = successive weighted w/o replacement, 1 = slot
-  int defer_last_relabel;   // 1: hop L-1's relabel is done by the one-launch gather (step group)
 };
 
 // Per-block sub-step timeline (profiling aid, one store per sub-step per block):
@@ -691,7 +690,7 @@ __device__ __forceinline__ void run_batch(const PArgs& a) {
     grid_barrier(a.bar, gen);
     CMB_PROF(a, pk);                                  // +9 barrier
   }
-  if (!a.defer_last_relabel) phase_relabel<PB>(a, a.L - 1);
+  phase_relabel<PB>(a, a.L - 1);
   if (a.order && vblk() == 0)  // the dst-order buckets, used up (grid barrier above): cleared
     for (int i = threadIdx.x; i < 2 * kOrderBuckets; i += PB) a.hist[i] = 0u;  // (hist, cursor)
   CMB_PROF(a, pk);
