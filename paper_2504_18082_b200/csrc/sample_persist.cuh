@@ -30,7 +30,6 @@ using namespace smp;
 
 constexpr int kMaxBlocks = 4096;
 constexpr int kRowCap = 3072;  // dst rows per block cached in shared memory
-constexpr int kTiles = 8;      // edge tiles per block whose flags are loaded before scanning
 constexpr int kOrderBits = 12;                 // dst-order buckets: at most 2^12 node-id ranges
 constexpr int kOrderBuckets = 1 << kOrderBits;
 constexpr uint32_t kFinal = 0x80000000u;
@@ -549,6 +548,30 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   CMB_PROF(a, pk);
 }
 
+// 8 consecutive int32 of p starting at e0 (a multiple of 8), entries at or past n read as 0:
+// two 16-byte loads when the run is whole and 16-byte aligned, else scalar loads
+__device__ __forceinline__ void ld8(const int32_t* p, int64_t e0, int64_t n, int32_t (&v)[8]) {
+  if (e0 + 8 <= n && (reinterpret_cast<uintptr_t>(p + e0) & 15) == 0) {
+    const int4 x = __ldcg(reinterpret_cast<const int4*>(p + e0));
+    const int4 y = __ldcg(reinterpret_cast<const int4*>(p + e0) + 1);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = e0 + k < n ? __ldcg(p + e0 + k) : 0;
+  }
+}
+__device__ __forceinline__ void st8(int32_t* p, int64_t e0, int64_t n, const int32_t (&v)[8]) {
+  if (e0 + 8 <= n && (reinterpret_cast<uintptr_t>(p + e0) & 15) == 0) {
+    reinterpret_cast<int4*>(p + e0)[0] = make_int4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<int4*>(p + e0)[1] = make_int4(v[4], v[5], v[6], v[7]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (e0 + k < n) p[e0 + k] = v[k];
+  }
+}
+
 // The visiting order of the last hop's dst rows (blocks.dst_order): after the grid barrier
 // that follows the count step every bucket count is final; each block scans the counts and
 // places its own dst rows (the count step's row range) at bucket offset + atomic cursor.
@@ -575,10 +598,23 @@ __device__ void place_dst_rows(const PArgs& a, int h, int64_t n_h, Smem<PB>& sm)
   const int32_t* dst = h == 0 ? a.roots : a.nodes;
   int64_t lo, hi;
   range_of(n_h, 1, lo, hi);
-  for (int64_t i = lo + threadIdx.x; i < hi; i += PB) {
-    const uint32_t v = static_cast<uint32_t>(__ldcg(dst + i));
-    const uint32_t b = v < static_cast<uint64_t>(a.g.n) ? v >> a.order_shift : 0u;
-    a.order[off[b] + atomicAdd(a.cursor + b, 1u)] = static_cast<int32_t>(i);
+  constexpr int U = 4;  // rows per thread per round: their atomics in flight together
+  for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += static_cast<int64_t>(U) * PB) {
+    uint32_t b[U], pos[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + static_cast<int64_t>(u) * PB;
+      const uint32_t v = i < hi ? static_cast<uint32_t>(__ldcg(dst + i)) : 0u;
+      b[u] = v < static_cast<uint64_t>(a.g.n) ? v >> a.order_shift : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      pos[u] = i0 + static_cast<int64_t>(u) * PB < hi ? atomicAdd(a.cursor + b[u], 1u) : 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + static_cast<int64_t>(u) * PB;
+      if (i < hi) a.order[off[b[u]] + pos[u]] = static_cast<int32_t>(i);
+    }
   }
   __syncthreads();
 }
@@ -594,43 +630,59 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   uint32_t* mask = (h == a.L - 1) ? a.mask : nullptr;
   const int32_t* nbr = a.indices[h];
   if (a.order && h == a.L - 1) place_dst_rows<PB>(a, h, n_h, sm);
+  // a thread owns 8 consecutive edges per round (the block's range is 32-aligned, so 4 threads
+  // fill one new-src mask word): their ids in two vector loads, all 8 map lookups in flight,
+  // one block scan per PB * 8 edges
   int32_t run = 0;
-  for (int64_t c0 = lo; c0 < hi; c0 += (int64_t)kTiles * PB) {
-    bool fl[kTiles];
+  for (int64_t c0 = lo; c0 < hi; c0 += static_cast<int64_t>(PB) * 8) {
+    const int64_t e0 = c0 + static_cast<int64_t>(threadIdx.x) * 8;
+    int32_t u[8];
+    ld8(nbr, e0, hi, u);
+    unsigned long long mv[8];
 #pragma unroll
-    for (int k = 0; k < kTiles; ++k) {  // all loads of up to kTiles tiles in flight
-      const int64_t e = c0 + k * PB + threadIdx.x;
-      fl[k] = e < hi && map_ld(a.map + __ldcg(nbr + e)) ==
-                            (tag | (kMarkerTop - static_cast<uint32_t>(e)));
-    }
+    for (int k = 0; k < 8; ++k) mv[k] = map_ld(a.map + u[k]);  // past hi: u = 0, harmless
+    uint32_t fl = 0;
 #pragma unroll
-    for (int k = 0; k < kTiles; ++k) {
-      const int64_t t0 = c0 + k * PB;
-      if (t0 >= hi) break;
-      const int64_t e = t0 + threadIdx.x;
-      int32_t inc, agg;
-      cub::BlockScan<int32_t, PB>(sm.cub.scan).InclusiveSum(fl[k] ? 1 : 0, inc, agg);
-      __syncthreads();
-      if (e < hi) a.scan[e] = (fl[k] ? 0x80000000u : 0u) | static_cast<uint32_t>(run + inc);
-      if (mask) {
-        const unsigned word = __ballot_sync(0xffffffffu, fl[k]);
-        if ((threadIdx.x & 31) == 0 && e < hi) mask[e >> 5] = word;
-      }
-      run += agg;
+    for (int k = 0; k < 8; ++k)
+      fl |= (e0 + k < hi && mv[k] == (tag | (kMarkerTop - static_cast<uint32_t>(e0 + k))))
+                ? (1u << k) : 0u;
+    int32_t ex, agg;
+    cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(__popc(fl), ex, agg);
+    __syncthreads();
+    int32_t sc[8];
+    int32_t acc = run + ex;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {  // flag << 31 | block-local inclusive flag count
+      acc += (fl >> k) & 1u;
+      sc[k] = static_cast<int32_t>(((fl >> k) & 1u) << 31 | static_cast<uint32_t>(acc));
     }
+    st8(reinterpret_cast<int32_t*>(a.scan), e0, hi, sc);
+    if (mask) {  // edges e0 .. e0+7 are bits 8 * (thread % 4) .. of word e0 / 32
+      uint32_t w = fl << (8 * (threadIdx.x & 3));
+      w |= __shfl_xor_sync(0xffffffffu, w, 1);
+      w |= __shfl_xor_sync(0xffffffffu, w, 2);
+      if ((threadIdx.x & 3) == 0 && e0 < hi) mask[e0 >> 5] = w;
+    }
+    run += agg;
   }
   CMB_PROF(a, pk);
   const int32_t base =
       publish_and_prefix<PB>(a.pub + kMaxBlocks, pub_tag(tag, h), run, sm);
   CMB_PROF(a, pk);
   if (vblk() == vgrid() - 1 && threadIdx.x == 0) a.sizes[h + 1] = n_h + base + run;
-  for (int64_t e = lo + threadIdx.x; e < hi; e += PB) {
-    const uint32_t sc = __ldcg(a.scan + e);
-    if (sc & 0x80000000u) {
-      const uint32_t id = static_cast<uint32_t>(n_h + base + (sc & 0x7fffffffu) - 1);
-      const int32_t u = __ldcg(nbr + e);
-      a.nodes[id] = u;
-      map_st(a.map + u, tag | kFinal | id);
+  for (int64_t e0 = lo + static_cast<int64_t>(threadIdx.x) * 8; e0 < hi;
+       e0 += static_cast<int64_t>(PB) * 8) {
+    int32_t sc[8], u[8];
+    ld8(reinterpret_cast<const int32_t*>(a.scan), e0, hi, sc);
+    ld8(nbr, e0, hi, u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (sc[k] < 0) {  // flag bit 31: a first occurrence -> the next local id
+        const uint32_t id =
+            static_cast<uint32_t>(n_h + base + (static_cast<uint32_t>(sc[k]) & 0x7fffffffu) - 1);
+        a.nodes[id] = u[k];
+        map_st(a.map + u[k], tag | kFinal | id);
+      }
     }
   }
 }
