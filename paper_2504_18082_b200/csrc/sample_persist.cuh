@@ -431,60 +431,39 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   int64_t lo, hi;
   range_of(n_h, 1, lo, hi);
   RowCache& rc = sm.rows;
-  // (1) counts, block scan, cached row info.  A thread owns RPT consecutive rows per round: the
-  // row ids, then all their CSR offsets and intra bounds are loaded before any is used (one
-  // scan per PB * RPT rows); an id outside [0, N) (a caller's bad root, already flagged) reads
-  // node 0's row and is given no neighbours
-  constexpr int RPT = 4;
+  // (1) counts, block scan, cached row info
   int32_t run = 0;
-  for (int64_t t0 = lo; t0 < hi; t0 += static_cast<int64_t>(PB) * RPT) {
-    const int64_t i0 = t0 + static_cast<int64_t>(threadIdx.x) * RPT;
-    int32_t v[RPT];
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) v[q] = i0 + q < hi ? __ldcg(dst + i0 + q) : -1;
-    int64_t rs[RPT], re[RPT];
-    uint2 bd[RPT];
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int32_t vv = static_cast<uint32_t>(v[q]) < static_cast<uint64_t>(a.g.n) ? v[q] : 0;
-      rs[q] = __ldg(a.g.indptr + vv);
-      re[q] = __ldg(a.g.indptr + vv + 1);
-      bd[q] = __ldg(a.g.bounds + vv);
-    }
-    int32_t c[RPT], s = 0;
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const bool ok = static_cast<uint32_t>(v[q]) < static_cast<uint64_t>(a.g.n);
-      if (!ok) re[q] = rs[q], bd[q] = make_uint2(0u, 0u);
-      if (a.order && h == a.L - 1 && i0 + q < hi)  // an out-of-range root counts in bucket 0
-        atomicAdd(a.hist + (ok ? static_cast<uint32_t>(v[q]) >> a.order_shift : 0u), 1u);
-      const int64_t ni = static_cast<int64_t>(bd[q].y) - bd[q].x;
-      const int64_t ni_e = a.wi ? ni : 0, no_e = a.wo ? (re[q] - rs[q]) - ni : 0;
-      const int64_t m = ni_e + no_e;
-      c[q] = static_cast<int32_t>(m < f ? m : f);
-      if (a.law == 1 && f < m) c[q] = slot_count(v[q], h, f, a.wi, ni_e, no_e, a.k0, a.k1, a.batch);
-      s += c[q];
+  for (int64_t t0 = lo; t0 < hi; t0 += PB) {
+    const int64_t i = t0 + threadIdx.x;
+    int32_t c = 0;
+    RowInfo r{};
+    int32_t v = 0;
+    if (i < hi) {
+      v = __ldcg(dst + i);
+      r = row_info_checked(a.g, v, a.wi, a.wo);
+      if (a.order && h == a.L - 1)  // an out-of-range root (flagged) counts in bucket 0
+        atomicAdd(a.hist + (static_cast<uint32_t>(v) < static_cast<uint64_t>(a.g.n)
+                                ? static_cast<uint32_t>(v) >> a.order_shift
+                                : 0u),
+                  1u);
+      const int64_t m = r.ni_e + r.no_e;
+      c = static_cast<int32_t>(m < f ? m : f);
+      if (a.law == 1 && f < m) c = slot_count(v, h, f, a.wi, r.ni_e, r.no_e, a.k0, a.k1, a.batch);
     }
     int32_t ex, agg;
-    cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(s, ex, agg);
+    cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(c, ex, agg);
     __syncthreads();
-    int32_t off = run + ex;
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int64_t i = i0 + q;
-      if (i < hi) {
-        const int64_t k = i - lo;
-        a.indptr[h][i] = off;
-        if (k < kRowCap) {
-          rc.rs[k] = rs[q];
-          rc.deg[k] = static_cast<uint32_t>(re[q] - rs[q]);
-          rc.lo[k] = bd[q].x;
-          rc.hi[k] = bd[q].y;
-          rc.v[k] = v[q];
-          rc.off[k] = off;
-        }
+    if (i < hi) {
+      const int64_t k = i - lo;
+      a.indptr[h][i] = run + ex;
+      if (k < kRowCap) {
+        rc.rs[k] = r.rs;
+        rc.deg[k] = static_cast<uint32_t>(r.deg);
+        rc.lo[k] = r.lo;
+        rc.hi[k] = r.hi;
+        rc.v[k] = v;
+        rc.off[k] = run + ex;
       }
-      off += c[q];
     }
     run += agg;
   }
