@@ -255,6 +255,32 @@ struct PickEmit {
     // p = 1) would otherwise queue one same-address atomic per pick in L2
     if (map_ld(map + u) < m) map_max(map + u, m);
   }
+  // all picks of a row at once (thread-per-row form, FM <= 8): every neighbour load, then every
+  // map load, then the reductions -- two round trips per row instead of two per pick
+  template <int FM>
+  __device__ __forceinline__ void put_row(int tot, int64_t rs, const uint32_t (&pos)[FM]) const {
+    if (tot <= 0) return;
+    uint32_t u[FM], rk[FM];
+#pragma unroll
+    for (int s = 0; s < FM; ++s)
+      u[s] = static_cast<uint32_t>(__ldg(ind + rs + (s < tot ? pos[s] : pos[0])));
+#pragma unroll
+    for (int s = 0; s < FM; ++s) {
+      uint32_t r = 0;
+#pragma unroll
+      for (int q = 0; q < FM; ++q) r += (q < tot) && pos[q] < pos[s];
+      rk[s] = r;
+      if (s < tot) out[r] = static_cast<int32_t>(u[s]);
+    }
+    unsigned long long cur[FM];
+#pragma unroll
+    for (int s = 0; s < FM; ++s) cur[s] = map_ld(map + u[s]);
+#pragma unroll
+    for (int s = 0; s < FM; ++s) {
+      const unsigned long long m = tag | (kMarkerTop - (e0 + rk[s]));
+      if (s < tot && cur[s] < m) map_max(map + u[s], m);
+    }
+  }
 };
 
 // take-all (reading R4): every eligible position, ascending; returns true if taken
@@ -411,13 +437,17 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
       pos[s] = s < K ? lo + q : (q < lo ? q : hi + (q - lo));
     }
   }
+  if constexpr (FM <= 8) {
+    em.template put_row<FM>(tot, rs, pos);  // ascending emit by rank, loads batched
+  } else {
 #pragma unroll
-  for (int s = 0; s < FM; ++s) {  // ascending emit by rank
-    if (s < tot) {
-      int rank = 0;
+    for (int s = 0; s < FM; ++s) {  // ascending emit by rank
+      if (s < tot) {
+        int rank = 0;
 #pragma unroll
-      for (int q = 0; q < FM; ++q) rank += (q < tot) && pos[q] < pos[s];
-      em.put(rank, rs + pos[s]);
+        for (int q = 0; q < FM; ++q) rank += (q < tot) && pos[q] < pos[s];
+        em.put(rank, rs + pos[s]);
+      }
     }
   }
 }
