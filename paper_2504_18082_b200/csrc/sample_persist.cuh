@@ -255,6 +255,9 @@ struct PickEmit {
     // p = 1) would otherwise queue one same-address atomic per pick in L2
     if (map_ld(map + u) < m) map_max(map + u, m);
   }
+#ifndef CMB_PUT_ROW_MAX
+#define CMB_PUT_ROW_MAX 8  // widest slot form whose picks are emitted as one batch
+#endif
   // all picks of a row at once (thread-per-row form, FM <= 8): every neighbour load, then every
   // map load, then the reductions -- two round trips per row instead of two per pick
   template <int FM>
@@ -437,7 +440,7 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
       pos[s] = s < K ? lo + q : (q < lo ? q : hi + (q - lo));
     }
   }
-  if constexpr (FM <= 8) {
+  if constexpr (FM <= CMB_PUT_ROW_MAX) {
     em.template put_row<FM>(tot, rs, pos);  // ascending emit by rank, loads batched
   } else {
 #pragma unroll
