@@ -256,9 +256,9 @@ struct PickEmit {
     if (map_ld(map + u) < m) map_max(map + u, m);
   }
 #ifndef CMB_PUT_ROW_MAX
-#define CMB_PUT_ROW_MAX 8  // widest slot form whose picks are emitted as one batch
+#define CMB_PUT_ROW_MAX 10  // widest slot form whose picks are emitted as one batch (16: spills)
 #endif
-  // all picks of a row at once (thread-per-row form, FM <= 8): every neighbour load, then every
+  // all picks of a row at once (thread-per-row form, FM <= 10): every neighbour load, then every
   // map load, then the reductions -- two round trips per row instead of two per pick
   template <int FM>
   __device__ __forceinline__ void put_row(int tot, int64_t rs, const uint32_t (&pos)[FM]) const {
