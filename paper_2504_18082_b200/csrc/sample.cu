@@ -23,13 +23,23 @@ struct SampleWs {
   uint32_t* hist;            // [kOrderBuckets] dst rows of hop L-1 per node-id bucket, then
   uint32_t* cursor;          // [kOrderBuckets] rows placed so far per bucket (contiguous)
   uint64_t* prof;            // [kMaxPersistBlocks][64] sub-step timeline
-  unsigned* tag_ctr;         // [1] batch tag of the last batch
-  unsigned long long* map;   // [N] tagged dedup map
+  unsigned* tag_ctr;         // [1] batches sampled with this workspace
+  void* map;                 // [N] tagged dedup map: 32-bit words, or 64-bit (wide_map)
   uint32_t* scan;            // [max e_cap]
 };
 
+// A batch needs 64-bit map words when one of its local ids or edge positions may reach 2^24
+// (the 32-bit word's value field; sample_persist.cuh MapWord).
+bool wide_map(int64_t n_roots, const int32_t* fanouts, int32_t L, int64_t num_nodes) {
+  int64_t n_cap[CMB_MAX_HOPS + 1], e_cap[CMB_MAX_HOPS];
+  cmb_blocks_capacity(n_roots, fanouts, L, num_nodes, n_cap, e_cap);
+  bool wide = n_cap[L] > static_cast<int64_t>(pst::MapWord<uint32_t>::kVal);
+  for (int h = 0; h < L; ++h) wide |= e_cap[h] > static_cast<int64_t>(pst::MapWord<uint32_t>::kVal);
+  return wide;
+}
+
 SampleWs carve_sample_ws(void* base, int64_t n_roots, const int32_t* fanouts, int32_t L,
-                         int64_t num_nodes, size_t* bytes) {
+                         int64_t num_nodes, bool wide, size_t* bytes) {
   int64_t n_cap[CMB_MAX_HOPS + 1], e_cap[CMB_MAX_HOPS];
   cmb_blocks_capacity(n_roots, fanouts, L, num_nodes, n_cap, e_cap);
   int64_t max_e = 0;
@@ -43,8 +53,11 @@ SampleWs carve_sample_ws(void* base, int64_t n_roots, const int32_t* fanouts, in
   w.hist = c.take<uint32_t>(2 * pst::kOrderBuckets);
   w.cursor = w.hist + pst::kOrderBuckets;
   w.prof = c.take<uint64_t>(static_cast<size_t>(kMaxPersistBlocks) * 64);
-  w.tag_ctr = c.take<unsigned>(1);
-  w.map = c.take<unsigned long long>(static_cast<size_t>(num_nodes));
+  w.tag_ctr = c.take<unsigned>(2);  // {batch counter, map width of the last batch}
+  if (wide)
+    w.map = c.take<unsigned long long>(static_cast<size_t>(num_nodes));
+  else
+    w.map = c.take<unsigned>(static_cast<size_t>(num_nodes));
   w.scan = c.take<uint32_t>(static_cast<size_t>(max_e) + 1);
   if (bytes) *bytes = c.bytes();
   return w;
@@ -80,6 +93,7 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
   a.hist = w.hist;
   a.cursor = w.cursor;
   a.order = out->dst_order;
+  a.chunks = out->dst_order ? out->dst_chunks : nullptr;
   int bits = 0;
   while ((int64_t{1} << bits) < g->d.n) ++bits;
   a.order_shift = bits > pst::kOrderBits ? bits - pst::kOrderBits : 0;
@@ -89,13 +103,14 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
 
 // One 1024-thread block per SM (64 registers: the whole register file), co-resident by
 // construction.  (A 512-thread form measured 101 vs 78 us per batch and was removed.)
-cmb_status launch_persistent(const cmb_graph* g, pst::PMulti& m, cudaStream_t s) {
+cmb_status launch_persistent(const cmb_graph* g, pst::PMulti& m, bool wide, cudaStream_t s) {
   constexpr int kPB = 1024;
   int grid = g->num_sms;
   if (grid > kMaxPersistBlocks) grid = kMaxPersistBlocks;
   grid -= grid % m.nb;    // equal virtual grids per batch
   void* args[] = {&m};
-  const void* fn = reinterpret_cast<const void*>(&pst::k_sample_persistent<kPB>);
+  const void* fn = wide ? reinterpret_cast<const void*>(&pst::k_sample_persistent<kPB, uint64_t>)
+                        : reinterpret_cast<const void*>(&pst::k_sample_persistent<kPB, uint32_t>);
   const size_t smem = pst::smem_bytes<kPB>();
   CMB_SMEM(fn, smem);
   CMB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kPB), args, smem, s));
@@ -105,7 +120,7 @@ cmb_status launch_persistent(const cmb_graph* g, pst::PMulti& m, cudaStream_t s)
 // host-checkable validation of one batch (capacities, workspace)
 cmb_status check_batch(const cmb_graph* g, const int32_t* roots, int64_t n_roots,
                        const int32_t* fanouts, int n_hops, const cmb_blocks* out,
-                       const void* workspace, size_t workspace_bytes) {
+                       const void* workspace, size_t workspace_bytes, bool wide) {
   CMB_ARG(roots && out, "cmb_sample_blocks: null roots/out");
   CMB_ARG(n_roots >= 1 && n_roots <= g->d.n, "cmb_sample_blocks: n_roots %lld outside [1, N]",
           (long long)n_roots);
@@ -127,7 +142,8 @@ cmb_status check_batch(const cmb_graph* g, const int32_t* roots, int64_t n_roots
     CMB_ARG(e_cap[h] < (int64_t(1) << 31) - 1, "cmb_sample_blocks: hop %d capacity exceeds int32",
             h);
   }
-  const size_t need = cmb_sample_workspace_bytes(n_roots, fanouts, n_hops, g->d.n);
+  size_t need = 0;  // the launch's map width (wide if any batch of it needs 64-bit words)
+  carve_sample_ws(nullptr, n_roots, fanouts, n_hops, g->d.n, wide, &need);
   CMB_ARG(workspace && workspace_bytes >= need && (reinterpret_cast<uintptr_t>(workspace) & 255) == 0,
           "cmb_sample_blocks: workspace must be 256-B aligned and >= %zu bytes", need);
   return CMB_OK;
@@ -144,7 +160,8 @@ size_t cmb_sample_workspace_bytes(int64_t n_roots, const int32_t* fanouts, int32
                                   int64_t num_nodes) {
   if (!fanouts || n_hops < 1 || n_hops > CMB_MAX_HOPS) return 0;
   size_t b = 0;
-  carve_sample_ws(nullptr, n_roots, fanouts, n_hops, num_nodes, &b);
+  carve_sample_ws(nullptr, n_roots, fanouts, n_hops, num_nodes,
+                  wide_map(n_roots, fanouts, n_hops, num_nodes), &b);
   return b;
 }
 
@@ -163,10 +180,13 @@ cmb_status cmb_sample_blocks_multi(const cmb_graph* g, const cmb_batch* batches,
   for (int h = 0; h < n_hops; ++h)
     CMB_ARG(fanouts[h] >= 1 && fanouts[h] <= CMB_MAX_FANOUT,
             "cmb_sample_blocks: fanout[%d] = %d outside [1, %d]", h, fanouts[h], CMB_MAX_FANOUT);
+  bool wide = false;
+  for (int i = 0; i < n_batches; ++i)
+    wide |= wide_map(batches[i].n_roots, fanouts, n_hops, g->d.n);
   for (int i = 0; i < n_batches; ++i) {
     const cmb_status st = check_batch(g, batches[i].roots, batches[i].n_roots, fanouts, n_hops,
                                       batches[i].out, batches[i].workspace,
-                                      batches[i].workspace_bytes);
+                                      batches[i].workspace_bytes, wide);
     if (st != CMB_OK) return st;
     for (int j = 0; j < i; ++j)
       CMB_ARG(batches[j].workspace != batches[i].workspace,
@@ -180,11 +200,11 @@ cmb_status cmb_sample_blocks_multi(const cmb_graph* g, const cmb_batch* batches,
   m.nb = n_batches;
   for (int i = 0; i < n_batches; ++i) {
     const cmb_batch& b = batches[i];
-    SampleWs w = carve_sample_ws(b.workspace, b.n_roots, fanouts, n_hops, g->d.n, nullptr);
+    SampleWs w = carve_sample_ws(b.workspace, b.n_roots, fanouts, n_hops, g->d.n, wide, nullptr);
     fill_args(m.a[i], g, b.roots, b.n_roots, fanouts, n_hops, wi, wo, k0, k1, b.batch_id, b.out,
               w, law);
   }
-  return launch_persistent(g, m, s);
+  return launch_persistent(g, m, wide, s);
 }
 
 cmb_status cmb_sample_blocks(const cmb_graph* g, const int32_t* roots, int64_t n_roots,

@@ -1,15 +1,21 @@
 // sample_persist.cuh -- the persistent cooperative schedule of a2 + a3 (included by sample.cu).
 //
 // One launch per batch, one block per SM (cooperative launch: all blocks co-resident), grid
-// barriers between the phases of a hop.  Dedup uses a DIRECT map over node ids (uint64[N] in
-// the workspace; L2-resident for N up to ~15M) instead of a hash table.  An entry is
-// (batch tag << 32) | value, the tag being a per-workspace batch counter, so entries written
-// by earlier batches read as empty and the map is never cleared:
+// barriers between the phases of a hop.  Dedup uses a DIRECT map over node ids (one word per
+// node in the workspace) instead of a hash table.  An entry is tag | value, the tag being a
+// per-workspace batch counter in the word's top bits, so entries written by earlier batches
+// read as empty and the map is never cleared between batches:
 //     value = kFinal | id          node u has local id `id` (dst nodes, relabelled nodes)
 //           = kMarkerTop - e       e = smallest edge position seen so far for new node u
-// "First occurrence" is then ONE fire-and-forget 64-bit atomicMax per edge (skipped when the
-// entry already holds a winning value): a newer tag beats a stale entry, final ids beat markers,
+// "First occurrence" is then ONE fire-and-forget atomicMax per edge (skipped when the entry
+// already holds a winning value): a newer tag beats a stale entry, final ids beat markers,
 // smaller e beats larger e.
+// Map words (MapWord<W>): 32-bit (7-bit tag, 24-bit values: every id and edge position of the
+// batch below 2^24 -- the BASELINE configs need <= 1.1M) whenever the batch's capacities allow,
+// else 64-bit (32-bit tag, 31-bit values).  The 32-bit tag wraps after 127 batches: the batch
+// that takes tag 1 clears the map first (one extra grid barrier every 127 batches).  Half the
+// bytes per entry halves the map's footprint (9.8 instead of 19.6 MB per workspace on products),
+// so the four maps of a launch group stay L2-resident across the gathers between two launches.
 //
 // Phases of hop h:
 //  A  [relabel(h-1)] + count + prefix + positions/picks/marks
@@ -32,8 +38,28 @@ constexpr int kMaxBlocks = 4096;
 constexpr int kRowCap = 3072;  // dst rows per block cached in shared memory
 constexpr int kOrderBits = 12;                 // dst-order buckets: at most 2^12 node-id ranges
 constexpr int kOrderBuckets = 1 << kOrderBits;
-constexpr uint32_t kFinal = 0x80000000u;
-constexpr uint32_t kMarkerTop = 0x7FFFFFFFu;
+
+// the two map word layouts: tag in the top bits, then the final flag, then the value
+template <class W>
+struct MapWord;
+template <>
+struct MapWord<uint32_t> {
+  using T = unsigned;
+  static constexpr int kShift = 25;
+  static constexpr unsigned kFinal = 1u << 24;
+  static constexpr unsigned kMarkerTop = (1u << 24) - 1u;
+  static constexpr unsigned kVal = (1u << 24) - 1u;
+  static constexpr unsigned kTagMax = 127u;  // tags 1..127, then clear + wrap
+};
+template <>
+struct MapWord<uint64_t> {
+  using T = unsigned long long;
+  static constexpr int kShift = 32;
+  static constexpr unsigned long long kFinal = 0x80000000ull;
+  static constexpr unsigned long long kMarkerTop = 0x7FFFFFFFull;
+  static constexpr unsigned long long kVal = 0x7FFFFFFFull;
+  static constexpr unsigned kTagMax = 0xFFFFFFFFu;  // never wraps in practice
+};
 
 // Accesses to the tagged dedup map are marked L2 evict_last: the maps of a launch group's
 // workspaces (4 x 19.6 MB on products) then survive the gathers that stream ~2.4 GB through L2
@@ -50,13 +76,26 @@ __device__ __forceinline__ unsigned long long map_ld(const unsigned long long* p
   asm volatile("ld.global.cg.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(map_pol()));
   return v;
 }
+__device__ __forceinline__ unsigned map_ld(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(map_pol()));
+  return v;
+}
 __device__ __forceinline__ void map_st(unsigned long long* p, unsigned long long v) {
   asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(map_pol())
+               : "memory");
+}
+__device__ __forceinline__ void map_st(unsigned* p, unsigned v) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(map_pol())
                : "memory");
 }
 // atomicMax without a result (a reduction), same policy
 __device__ __forceinline__ void map_max(unsigned long long* p, unsigned long long v) {
   asm volatile("red.global.max.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(map_pol())
+               : "memory");
+}
+__device__ __forceinline__ void map_max(unsigned* p, unsigned v) {
+  asm volatile("red.global.max.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(map_pol())
                : "memory");
 }
 __device__ __forceinline__ unsigned long long map_exch(unsigned long long* p,
@@ -65,6 +104,14 @@ __device__ __forceinline__ unsigned long long map_exch(unsigned long long* p,
   asm volatile("atom.global.exch.L2::cache_hint.b64 %0, [%1], %2, %3;"
                : "=l"(o)
                : "l"(p), "l"(v), "l"(map_pol())
+               : "memory");
+  return o;
+}
+__device__ __forceinline__ unsigned map_exch(unsigned* p, unsigned v) {
+  unsigned o;
+  asm volatile("atom.global.exch.L2::cache_hint.b32 %0, [%1], %2, %3;"
+               : "=r"(o)
+               : "l"(p), "r"(v), "l"(map_pol())
                : "memory");
   return o;
 }
@@ -95,8 +142,8 @@ struct PArgs {
   uint32_t* mask;
   int32_t* last_src;
   int64_t* sizes;
-  unsigned long long* map;  // [N] tagged direct dedup map (see above)
-  unsigned* tag_ctr;        // [1] last batch tag used with this workspace
+  void* map;                // [N] tagged direct dedup map (see above), MapWord<W>::T words
+  unsigned* tag_ctr;        // [1] batches sampled with this workspace so far
   uint32_t* scan;           // [max e_cap] flag << 31 | block-local inclusive flag scan
   unsigned long long* pub;  // [2][kMaxBlocks] tagged block aggregates
   unsigned* bar;            // [0] arrivals, [1] generation
@@ -104,6 +151,7 @@ struct PArgs {
   uint32_t* hist;           // [kOrderBuckets] dst rows of hop L-1 per bucket v >> order_shift
   uint32_t* cursor;         // [kOrderBuckets] rows of each bucket placed so far
   int32_t* order;           // optional [n_{L-1}]: the visiting order of the last hop's dst rows
+  int32_t* chunks;          // optional [CMB_ORDER_CHUNKS + 1]: chunk starts in order, then n_{L-1}
   int order_shift;
   int32_t* status;
   int law;                  // Knob-2 law: 0 = successive weighted w/o replacement, 1 = slot
@@ -172,8 +220,8 @@ struct Smem {
 
 // The tag of a published aggregate: this batch's map tag and the hop, so entries left by earlier
 // batches or hops never match and the array needs no clearing between batches.
-__device__ __forceinline__ unsigned pub_tag(unsigned long long tag, int h) {
-  return (static_cast<unsigned>(tag >> 32) << 4) | static_cast<unsigned>(h + 1);
+__device__ __forceinline__ unsigned pub_tag(unsigned ctr, int h) {
+  return (ctr << 4) | static_cast<unsigned>(h + 1);
 }
 
 // Block b publishes its aggregate (tagged) and adds the aggregates of blocks [0, b) as they
@@ -210,25 +258,28 @@ __device__ __forceinline__ void range_of(int64_t n, int64_t align, int64_t& lo, 
 }
 
 // relabel of hop h (all entries final): indices[e] := local id of its node
-template <int PB>
+template <int PB, class W>
 __device__ void phase_relabel(const PArgs& a, int h) {
+  using M = MapWord<W>;
+  using T = typename M::T;
+  const T* map = static_cast<const T*>(a.map);
   const int64_t e_h = __ldcg(a.sizes + a.L + 1 + h);
   int32_t* gid = (h == a.L - 1) ? a.last_src : nullptr;
   int32_t* ind = a.indices[h];
   const int64_t stride = (int64_t)vgrid() * PB;
   for (int64_t e0 = vblk() * (int64_t)PB + threadIdx.x; e0 < e_h; e0 += 4 * stride) {
     int32_t u[4];
-    unsigned long long v[4];
+    T v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) u[k] = e0 + k * stride < e_h ? __ldcg(ind + e0 + k * stride) : 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = e0 + k * stride < e_h ? map_ld(a.map + u[k]) : 0ull;
+    for (int k = 0; k < 4; ++k) v[k] = e0 + k * stride < e_h ? map_ld(map + u[k]) : T(0);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t e = e0 + k * stride;
       if (e < e_h) {
         if (gid) gid[e] = u[k];
-        ind[e] = static_cast<int32_t>(static_cast<uint32_t>(v[k]) & ~kFinal);
+        ind[e] = static_cast<int32_t>(v[k] & M::kVal);
       }
     }
   }
@@ -241,16 +292,19 @@ __device__ void phase_relabel(const PArgs& a, int h) {
 // loads then overlap with the Philox work of the other rows of the phase instead of forming a
 // pass of their own.  (Tried and removed: a separate coalesced picks pass through a pick-position
 // array, 91 vs 84 us per batch; warp-deduplicating the marks with match_any, 88 vs 86 us.)
+template <class W>
 struct PickEmit {
+  using M = MapWord<W>;
+  using T = typename M::T;
   const int32_t* ind;
   int32_t* out;                // block indices of this row's first pick
-  unsigned long long* map;
-  unsigned long long tag;
+  T* map;
+  T tag;
   uint32_t e0;                 // absolute edge index of the row's first pick
   __device__ __forceinline__ void put(int k, int64_t p) const {
     const uint32_t u = static_cast<uint32_t>(__ldg(ind + p));
     out[k] = static_cast<int32_t>(u);
-    const unsigned long long m = tag | (kMarkerTop - (e0 + static_cast<uint32_t>(k)));
+    const T m = tag | (M::kMarkerTop - (e0 + static_cast<uint32_t>(k)));
     // read the entry first: a node picked by many rows (hubs; every pick of a community at
     // p = 1) would otherwise queue one same-address atomic per pick in L2
     if (map_ld(map + u) < m) map_max(map + u, m);
@@ -275,12 +329,12 @@ struct PickEmit {
       rk[s] = r;
       if (s < tot) out[r] = static_cast<int32_t>(u[s]);
     }
-    unsigned long long cur[FM];
+    T cur[FM];
 #pragma unroll
     for (int s = 0; s < FM; ++s) cur[s] = map_ld(map + u[s]);
 #pragma unroll
     for (int s = 0; s < FM; ++s) {
-      const unsigned long long m = tag | (kMarkerTop - (e0 + rk[s]));
+      const T m = tag | (M::kMarkerTop - (e0 + rk[s]));
       if (s < tot && cur[s] < m) map_max(map + u[s], m);
     }
   }
@@ -455,9 +509,10 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
   }
 }
 
-template <int PB, int G>
+template <int PB, int G, class W>
 __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
-                                   unsigned long long tag) {
+                                   typename MapWord<W>::T tag, unsigned ctr) {
+  using T = typename MapWord<W>::T;
   const int64_t n_h = h == 0 ? a.n_roots : __ldcg(a.sizes + h);
   const int32_t* dst = h == 0 ? a.roots : a.nodes;
   const int f = a.fan[h];
@@ -501,7 +556,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
     run += agg;
   }
   CMB_PROF(a, pk);
-  const int32_t base = publish_and_prefix<PB>(a.pub, pub_tag(tag, h), run, sm);
+  const int32_t base = publish_and_prefix<PB>(a.pub, pub_tag(ctr, h), run, sm);
   CMB_PROF(a, pk);
   if (vblk() == vgrid() - 1 && threadIdx.x == 0) {
     a.indptr[h][n_h] = base + run;
@@ -541,7 +596,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       fetch(i, v, rs, deg, rlo, rhi, off);
       a.indptr[h][i] = base + off;
       const uint32_t e0 = static_cast<uint32_t>(base + off);
-      const PickEmit em{a.g.indices, a.indices[h] + e0, a.map, tag, e0};
+      const PickEmit<W> em{a.g.indices, a.indices[h] + e0, static_cast<T*>(a.map), tag, e0};
       // the slot arrays are sized to the fanout: an unrolled slot a row does not use still
       // issues its (predicated) Philox rounds -- exact sizes for the per-row fanouts of the
       // BASELINE configs' big hops (5, 10) cut the sampler 3.5 % on products (f = 5 was an
@@ -573,7 +628,9 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       if (lane == 0) a.indptr[h][i] = base + off;
       const uint32_t e0 = static_cast<uint32_t>(base + off);
       row_positions_group<G>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, lane,
-                             gmask, PickEmit{a.g.indices, a.indices[h] + e0, a.map, tag, e0},
+                             gmask,
+                             PickEmit<W>{a.g.indices, a.indices[h] + e0, static_cast<T*>(a.map),
+                                         tag, e0},
                              a.law);
     }
   }
@@ -628,6 +685,12 @@ __device__ void place_dst_rows(const PArgs& a, int h, int64_t n_h, Smem<PB>& sm)
     ex += static_cast<int32_t>(c[q]);
   }
   __syncthreads();
+  static_assert(kOrderBuckets % CMB_ORDER_CHUNKS == 0, "whole buckets per chunk");
+  if (a.chunks && vblk() == 0)  // chunk c = buckets [c * Q, (c + 1) * Q): where it starts
+    for (int c = threadIdx.x; c <= CMB_ORDER_CHUNKS; c += PB)
+      a.chunks[c] = c < CMB_ORDER_CHUNKS
+                        ? static_cast<int32_t>(off[c * (kOrderBuckets / CMB_ORDER_CHUNKS)])
+                        : static_cast<int32_t>(n_h);
   const int32_t* dst = h == 0 ? a.roots : a.nodes;
   int64_t lo, hi;
   range_of(n_h, 1, lo, hi);
@@ -653,9 +716,12 @@ __device__ void place_dst_rows(const PArgs& a, int h, int64_t n_h, Smem<PB>& sm)
 }
 
 // flags + prefix + assign
-template <int PB>
+template <int PB, class W>
 __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
-                                  unsigned long long tag) {
+                                  typename MapWord<W>::T tag, unsigned ctr) {
+  using M = MapWord<W>;
+  using T = typename M::T;
+  T* map = static_cast<T*>(a.map);
   const int64_t n_h = h == 0 ? a.n_roots : __ldcg(a.sizes + h);
   const int64_t e_h = __ldcg(a.sizes + a.L + 1 + h);
   int64_t lo, hi;
@@ -671,13 +737,13 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
     const int64_t e0 = c0 + static_cast<int64_t>(threadIdx.x) * 8;
     int32_t u[8];
     ld8(nbr, e0, hi, u);
-    unsigned long long mv[8];
+    T mv[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) mv[k] = map_ld(a.map + u[k]);  // past hi: u = 0, harmless
+    for (int k = 0; k < 8; ++k) mv[k] = map_ld(map + u[k]);  // past hi: u = 0, harmless
     uint32_t fl = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      fl |= (e0 + k < hi && mv[k] == (tag | (kMarkerTop - static_cast<uint32_t>(e0 + k))))
+      fl |= (e0 + k < hi && mv[k] == (tag | (M::kMarkerTop - static_cast<uint32_t>(e0 + k))))
                 ? (1u << k) : 0u;
     int32_t ex, agg;
     cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(__popc(fl), ex, agg);
@@ -700,7 +766,7 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   }
   CMB_PROF(a, pk);
   const int32_t base =
-      publish_and_prefix<PB>(a.pub + kMaxBlocks, pub_tag(tag, h), run, sm);
+      publish_and_prefix<PB>(a.pub + kMaxBlocks, pub_tag(ctr, h), run, sm);
   CMB_PROF(a, pk);
   if (vblk() == vgrid() - 1 && threadIdx.x == 0) a.sizes[h + 1] = n_h + base + run;
   for (int64_t e0 = lo + static_cast<int64_t>(threadIdx.x) * 8; e0 < hi;
@@ -714,7 +780,7 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
         const uint32_t id =
             static_cast<uint32_t>(n_h + base + (static_cast<uint32_t>(sc[k]) & 0x7fffffffu) - 1);
         a.nodes[id] = u[k];
-        map_st(a.map + u[k], tag | kFinal | id);
+        map_st(map + u[k], tag | M::kFinal | id);
       }
     }
   }
@@ -726,19 +792,35 @@ struct PMulti {
   PArgs a[kMaxNB];
 };
 
-template <int PB>
+template <int PB, class W>
 __device__ __forceinline__ void run_batch(const PArgs& a) {
+  using M = MapWord<W>;
+  using T = typename M::T;
+  T* map = static_cast<T*>(a.map);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<PB>& sm = *reinterpret_cast<Smem<PB>*>(smem_raw);
-  __shared__ unsigned gen_s, tag_s;
+  __shared__ unsigned gen_s, ctr_s, width_s;
+  constexpr unsigned kWidth = sizeof(T);
   if (threadIdx.x == 0) {
     gen_s = ld_acquire(a.bar + 1);
-    tag_s = __ldcg(a.tag_ctr) + 1u;  // this batch's map tag (published by block 0 below)
+    ctr_s = __ldcg(a.tag_ctr) + 1u;  // this batch's counter (published by block 0 below)
+    width_s = __ldcg(a.tag_ctr + 1);  // map word bytes of the workspace's last batch (0: none)
   }
   __syncthreads();
   unsigned gen = gen_s;
-  const unsigned long long tag = static_cast<unsigned long long>(tag_s) << 32;
+  const unsigned ctr = ctr_s;
+  // map tag 1..kTagMax; the batch that (re)starts at tag 1 clears the map first, so no entry of
+  // an earlier cycle can beat this cycle's markers (the workspace starts zeroed: counter 0), and
+  // so does a batch whose map width differs from the previous batch's on this workspace
+  const unsigned tagv = (ctr - 1u) % M::kTagMax + 1u;
+  const T tag = static_cast<T>(tagv) << M::kShift;
   int pk = 0;
+  if ((tagv == 1u && ctr > 1u) || (width_s != 0u && width_s != kWidth)) {
+    const int64_t n = a.g.n;
+    for (int64_t i = vblk() * (int64_t)PB + threadIdx.x; i < n; i += (int64_t)vgrid() * PB)
+      map[i] = T(0);
+    grid_barrier(a.bar, gen);
+  }
   CMB_PROF(a, pk);
   for (int64_t i = vblk() * (int64_t)PB + threadIdx.x; i < a.n_roots;
        i += (int64_t)vgrid() * PB) {
@@ -749,39 +831,42 @@ __device__ __forceinline__ void run_batch(const PArgs& a) {
       continue;
     }
     a.nodes[i] = static_cast<int32_t>(u);
-    const unsigned long long old = map_exch(a.map + u, tag | kFinal | static_cast<uint32_t>(i));
+    const T old = map_exch(map + u, tag | M::kFinal | static_cast<uint32_t>(i));
     // duplicate root <=> the entry already holds a final id of THIS batch (a marker of this
     // batch -- hop-0 picks run concurrently -- is not a duplicate: the final id replaces it)
-    if ((old & 0xffffffff00000000ull) == tag && (static_cast<uint32_t>(old) & kFinal))
+    if ((old >> M::kShift) == tagv && (old & M::kFinal))
       raise_status(a.status, CMB_ERR_INVALID_INPUT);
   }
   if (vblk() == 0 && threadIdx.x == 0) a.sizes[0] = a.n_roots;
   for (int h = 0; h < a.L; ++h) {
-    if (h > 0) phase_relabel<PB>(a, h - 1);
+    if (h > 0) phase_relabel<PB, W>(a, h - 1);
     CMB_PROF(a, pk);                                  // +0 relabel(h-1)
     const int f = a.fan[h];
 #if defined(CMB_SAMPLER_G8)
-    if (f <= 8) phase_count_sample<PB, 8>(a, h, sm, pk, tag);
+    if (f <= 8) phase_count_sample<PB, 8, W>(a, h, sm, pk, tag, ctr);
     else
 #endif
-    if (f <= 16) phase_count_sample<PB, 16>(a, h, sm, pk, tag);
-    else phase_count_sample<PB, 32>(a, h, sm, pk, tag);  // +1 count, +2 prefix, +3 positions
+    if (f <= 16) phase_count_sample<PB, 16, W>(a, h, sm, pk, tag, ctr);
+    else phase_count_sample<PB, 32, W>(a, h, sm, pk, tag, ctr);  // +1 count, +2 prefix, +3 positions
     CMB_PROF(a, pk);                                  // +4 picks + marks
     grid_barrier(a.bar, gen);
     CMB_PROF(a, pk);                                  // +5 barrier (marks final)
-    if (h == 0 && vblk() == 0 && threadIdx.x == 0) *a.tag_ctr = tag_s;  // all have read it
-    phase_flag_assign<PB>(a, h, sm, pk, tag);         // +6 flag scan, +7 prefix
+    if (h == 0 && vblk() == 0 && threadIdx.x == 0) {  // all blocks have read them
+      a.tag_ctr[0] = ctr;
+      a.tag_ctr[1] = kWidth;
+    }
+    phase_flag_assign<PB, W>(a, h, sm, pk, tag, ctr); // +6 flag scan, +7 prefix
     CMB_PROF(a, pk);                                  // +8 assign
     grid_barrier(a.bar, gen);
     CMB_PROF(a, pk);                                  // +9 barrier
   }
-  phase_relabel<PB>(a, a.L - 1);
+  phase_relabel<PB, W>(a, a.L - 1);
   if (a.order && vblk() == 0)  // the dst-order buckets, used up (grid barrier above): cleared
     for (int i = threadIdx.x; i < 2 * kOrderBuckets; i += PB) a.hist[i] = 0u;  // (hist, cursor)
   CMB_PROF(a, pk);
 }
 
-template <int PB>
+template <int PB, class W>
 __global__ void __launch_bounds__(PB, 1024 / PB)
     k_sample_persistent(const __grid_constant__ PMulti m) {
   const int nb = m.nb;
@@ -791,7 +876,7 @@ __global__ void __launch_bounds__(PB, 1024 / PB)
     g_vgrid = (gridDim.x - grp + nb - 1) / nb;
   }
   __syncthreads();
-  run_batch<PB>(m.a[grp]);
+  run_batch<PB, W>(m.a[grp]);
 }
 
 template <int PB>
