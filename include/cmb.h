@@ -104,7 +104,8 @@ typedef struct {
 } cmb_graph_desc;
 
 /* Bytes of graph workspace: community offsets int32[C+1] + per-row intra segment
- * uint32x2[N] + status word. */
+ * uint32x2[N] + a packed 16-byte row record per node (row start, degree and intra segment,
+ * so the sampler reads one random sector per row instead of two or three) + status word. */
 CMB_API size_t cmb_graph_workspace_bytes(int64_t num_nodes, int32_t num_communities);
 
 /* a0: builds the per-row intra-community segment [lo, hi) of every row (the
@@ -175,6 +176,14 @@ typedef struct {
  * n_cap[h+1] = min(num_nodes, n_cap[h] + e_cap[h]).  n_cap has n_hops+1 entries. */
 CMB_API void cmb_blocks_capacity(int64_t n_roots, const int32_t* fanouts, int32_t n_hops,
                          int64_t num_nodes, int64_t* n_cap, int64_t* e_cap);
+/* Bytes of sampler workspace for batches of up to n_roots roots: device, 256-B aligned,
+ * zero-filled ONCE by the caller and then owned by the sampler (no per-batch memset): grid
+ * barrier words, tagged block aggregates, a batch counter and a direct dedup map of one word per
+ * node -- 32-bit words (7-bit batch tag: the batch that wraps the tag clears the map) when every
+ * local id and edge position of a batch of this capacity is below 2^24, else 64-bit words.  A
+ * workspace may serve batches of either width (a width change clears the map); one launch
+ * uses one width for all its batches, so a workspace sized for the narrow width must not be
+ * combined with a batch that needs the wide one (CMB_ERR_INVALID_ARGUMENT). */
 CMB_API size_t cmb_sample_workspace_bytes(int64_t n_roots, const int32_t* fanouts, int32_t n_hops,
                                   int64_t num_nodes);
 /* Samples an n_hops-hop sub-graph from `roots` (device int32[n_roots], distinct).

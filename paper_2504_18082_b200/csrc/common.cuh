@@ -115,6 +115,7 @@ __device__ __forceinline__ uint64_t hi64(const PhiloxOut& w) {
 }
 
 // Graph as seen by kernels.
+constexpr uint32_t kRecDegSlow = 0xFFFFFFu;  // row record degree field: "read indptr / bounds"
 struct DevGraph {
   int64_t n;
   int64_t nnz;
@@ -124,6 +125,8 @@ struct DevGraph {
   int32_t ncomm;
   const int32_t* cbeg;   // [C+1]
   const uint2* bounds;   // [N] (lo, hi) row offsets of the intra segment
+  const uint4* rec;      // [N] or NULL: packed row record (graph.cu k_intra_bounds): row start,
+                         // degree and intra segment of v in ONE 16-byte load
   const float* x;
   int32_t f;
   int64_t ld;

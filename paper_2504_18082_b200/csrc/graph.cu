@@ -64,10 +64,15 @@ __device__ __forceinline__ int64_t lower_bound(const int32_t* __restrict__ a, in
 }
 
 // (lo, hi) = row offsets of the first neighbour >= cbeg[c(v)] and >= cbeg[c(v)+1].
+// With `rec`, also the packed row record the sampler reads instead of indptr[v], indptr[v+1]
+// and bounds[v] (two or three random 32-B sectors -> one): x = row start bits 0..31,
+// y = start bits 32..39 | degree << 8, z = lo, w = hi; a row of degree >= 2^24 - 1 stores the
+// degree field 0xFFFFFF (read the three arrays instead).  Used when nnz < 2^40.
 __global__ void k_intra_bounds(const int64_t* __restrict__ indptr,
                                const int32_t* __restrict__ indices,
                                const int32_t* __restrict__ comm, const int32_t* __restrict__ cbeg,
-                               int32_t ncomm, int64_t n, uint2* __restrict__ bounds) {
+                               int32_t ncomm, int64_t n, uint2* __restrict__ bounds,
+                               uint4* __restrict__ rec) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t rs = indptr[v], re = indptr[v + 1];
@@ -75,6 +80,13 @@ __global__ void k_intra_bounds(const int64_t* __restrict__ indptr,
     const int64_t a = lower_bound(indices, rs, re, cbeg[c]);
     const int64_t b = lower_bound(indices, a, re, cbeg[c + 1]);
     bounds[v] = make_uint2(static_cast<uint32_t>(a - rs), static_cast<uint32_t>(b - rs));
+    if (rec) {
+      const uint64_t deg = static_cast<uint64_t>(re - rs);
+      const uint32_t df = deg < kRecDegSlow ? static_cast<uint32_t>(deg) : kRecDegSlow;
+      rec[v] = make_uint4(static_cast<uint32_t>(rs),
+                          (static_cast<uint32_t>(static_cast<uint64_t>(rs) >> 32) & 0xFFu) | (df << 8),
+                          static_cast<uint32_t>(a - rs), static_cast<uint32_t>(b - rs));
+    }
   }
 }
 
@@ -82,6 +94,7 @@ struct GraphWs {
   WsHeader* hdr;
   int32_t* cbeg;
   uint2* bounds;
+  uint4* rec;
 };
 
 GraphWs carve_graph_ws(void* base, int64_t n, int32_t ncomm, size_t* bytes) {
@@ -90,6 +103,7 @@ GraphWs carve_graph_ws(void* base, int64_t n, int32_t ncomm, size_t* bytes) {
   w.hdr = c.take<WsHeader>(1);
   w.cbeg = c.take<int32_t>(static_cast<size_t>(ncomm) + 1);
   w.bounds = c.take<uint2>(static_cast<size_t>(n));
+  w.rec = c.take<uint4>(static_cast<size_t>(n));
   if (bytes) *bytes = c.bytes();
   return w;
 }
@@ -131,6 +145,7 @@ cmb_status cmb_load_graph(const cmb_graph_desc* d, void* stream, cmb_graph** out
   if (st != CMB_OK) return st;
 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool use_rec = d->num_edges < (int64_t(1) << 40);  // the record's 40-bit row start
   GraphWs w = carve_graph_ws(d->workspace, d->num_nodes, d->num_communities, nullptr);
   CMB_CUDA(cudaMemsetAsync(w.hdr, 0, sizeof(WsHeader), s));
   int dev = 0, sms = 148;
@@ -155,7 +170,7 @@ cmb_status cmb_load_graph(const cmb_graph_desc* d, void* stream, cmb_graph** out
   }
   k_intra_bounds<<<grid, 256, 0, s>>>(d->indptr, d->indices, d->community, w.cbeg,
                                       d->num_communities, d->num_nodes,
-                                      w.bounds);
+                                      w.bounds, use_rec ? w.rec : nullptr);
   CMB_CUDA(cudaGetLastError());
 
   // 64-byte aligned (the embedded CUtensorMap requires it)
@@ -174,6 +189,7 @@ cmb_status cmb_load_graph(const cmb_graph_desc* d, void* stream, cmb_graph** out
   g->d.ncomm = d->num_communities;
   g->d.cbeg = w.cbeg;
   g->d.bounds = w.bounds;
+  g->d.rec = use_rec ? w.rec : nullptr;
   g->d.x = d->features;
   g->d.f = d->features ? d->feat_dim : 0;
   g->d.ld = d->features ? d->feat_ld : 0;

@@ -93,7 +93,6 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
   a.hist = w.hist;
   a.cursor = w.cursor;
   a.order = out->dst_order;
-  a.chunks = out->dst_order ? out->dst_chunks : nullptr;
   int bits = 0;
   while ((int64_t{1} << bits) < g->d.n) ++bits;
   a.order_shift = bits > pst::kOrderBits ? bits - pst::kOrderBits : 0;

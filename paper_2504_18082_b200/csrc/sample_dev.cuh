@@ -25,12 +25,23 @@ struct RowInfo {
 __device__ __forceinline__ RowInfo row_info(const DevGraph& g, int32_t v, uint32_t wi,
                                             uint32_t wo) {
   RowInfo r;
-  r.rs = __ldg(g.indptr + v);
-  r.deg = __ldg(g.indptr + v + 1) - r.rs;
-  const uint2 b = __ldg(g.bounds + v);
-  r.lo = b.x;
-  r.hi = b.y;
-  const int64_t ni = static_cast<int64_t>(b.y) - b.x;
+  uint32_t df = kRecDegSlow;
+  if (g.rec) {  // one 16-byte load (graph.cu k_intra_bounds packs it)
+    const uint4 q = __ldg(g.rec + v);
+    df = q.y >> 8;
+    r.rs = static_cast<int64_t>(q.x) | (static_cast<int64_t>(q.y & 0xFFu) << 32);
+    r.deg = df;
+    r.lo = q.z;
+    r.hi = q.w;
+  }
+  if (df == kRecDegSlow) {  // no record, or a row too long for its degree field
+    r.rs = __ldg(g.indptr + v);
+    r.deg = __ldg(g.indptr + v + 1) - r.rs;
+    const uint2 b = __ldg(g.bounds + v);
+    r.lo = b.x;
+    r.hi = b.y;
+  }
+  const int64_t ni = static_cast<int64_t>(r.hi) - r.lo;
   r.ni_e = wi ? ni : 0;
   r.no_e = wo ? r.deg - ni : 0;
   return r;

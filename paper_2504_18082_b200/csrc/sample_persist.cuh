@@ -35,7 +35,10 @@ namespace pst {
 using namespace smp;
 
 constexpr int kMaxBlocks = 4096;
-constexpr int kRowCap = 3072;  // dst rows per block cached in shared memory
+#ifndef CMB_ROW_CAP  // layout experiments only (tools/gpu_variant_ab.sh)
+#define CMB_ROW_CAP 3072
+#endif
+constexpr int kRowCap = CMB_ROW_CAP;  // dst rows per block cached in shared memory
 constexpr int kOrderBits = 12;                 // dst-order buckets: at most 2^12 node-id ranges
 constexpr int kOrderBuckets = 1 << kOrderBits;
 
@@ -151,7 +154,6 @@ struct PArgs {
   uint32_t* hist;           // [kOrderBuckets] dst rows of hop L-1 per bucket v >> order_shift
   uint32_t* cursor;         // [kOrderBuckets] rows of each bucket placed so far
   int32_t* order;           // optional [n_{L-1}]: the visiting order of the last hop's dst rows
-  int32_t* chunks;          // optional [CMB_ORDER_CHUNKS + 1]: chunk starts in order, then n_{L-1}
   int order_shift;
   int32_t* status;
   int law;                  // Knob-2 law: 0 = successive weighted w/o replacement, 1 = slot
@@ -330,8 +332,16 @@ struct PickEmit {
       if (s < tot) out[r] = static_cast<int32_t>(u[s]);
     }
     T cur[FM];
+#ifndef CMB_MARK_PRECHECK  // layout experiments only
+#define CMB_MARK_PRECHECK 1
+#endif
+#if CMB_MARK_PRECHECK
 #pragma unroll
     for (int s = 0; s < FM; ++s) cur[s] = map_ld(map + u[s]);
+#else
+#pragma unroll
+    for (int s = 0; s < FM; ++s) cur[s] = 0;
+#endif
 #pragma unroll
     for (int s = 0; s < FM; ++s) {
       const T m = tag | (M::kMarkerTop - (e0 + rk[s]));
@@ -434,17 +444,18 @@ __device__ __forceinline__ void row_positions_group(int32_t v, int64_t rs, int64
 
 // one thread per row (f <= FM): the same draws with every loop statically unrolled over FM
 // slots (register arrays, predicated on s < f) -- no shuffles, 32 rows per warp.
+// (32-bit row quantities: a row's degree is below N < 2^31; fewer registers, fewer spills)
 template <int FM, class Emit>
-__device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int64_t deg,
+__device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, uint32_t deg,
                                                      uint32_t lo, uint32_t hi, int hop, int f,
                                                      uint32_t wi, uint32_t wo, uint32_t k0,
                                                      uint32_t k1, uint32_t batch,
                                                      const Emit& em, int law) {
-  const int64_t ni = static_cast<int64_t>(hi) - lo;
-  const int64_t ni_e = wi ? ni : 0, no_e = wo ? deg - ni : 0;
+  const uint32_t ni = hi - lo;
+  const uint32_t ni_e = wi ? ni : 0u, no_e = wo ? deg - ni : 0u;
   if (take_all(rs, deg, lo, hi, ni_e, no_e, f, 0, 1, em)) return;
   uint64_t r23[FM];
-  uint64_t ri = static_cast<uint64_t>(ni_e), ro = static_cast<uint64_t>(no_e);
+  uint32_t ri = ni_e, ro = no_e;
   int K = 0, kd = 0;
   const uint32_t c2 = (kTagSample << 24) | static_cast<uint32_t>(hop);
 #pragma unroll
@@ -455,8 +466,8 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
                                         batch, k0, k1);
       r23[s] = hi64(w);
       kd += (lo64(w) >> 48) < wi;  // slot law: slot s intra iff unif(r01, 65536) < P16
-      const uint64_t wri = wi * ri;
-      if (__umul64hi(lo64(w), wri + wo * ro) < wri) {
+      const uint64_t wri = static_cast<uint64_t>(wi) * ri;
+      if (__umul64hi(lo64(w), wri + static_cast<uint64_t>(wo) * ro) < wri) {
         ++K;
         --ri;
       } else {
@@ -466,8 +477,8 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
   }
   int kb = f - K;
   if (law == 1) {
-    K = kd < ni_e ? kd : static_cast<int>(ni_e);
-    kb = f - kd < no_e ? f - kd : static_cast<int>(no_e);
+    K = kd < static_cast<int64_t>(ni_e) ? kd : static_cast<int>(ni_e);
+    kb = f - kd < static_cast<int64_t>(no_e) ? f - kd : static_cast<int>(no_e);
   }
   const int tot = K + kb;  // picks of this row (f under law A)
   uint32_t pos[FM];
@@ -476,10 +487,10 @@ __device__ __forceinline__ void row_positions_thread(int32_t v, int64_t rs, int6
     pos[s] = kEmpty;
     if (s < tot) {
       const bool in = s < K;
-      const uint64_t n_cls = in ? static_cast<uint64_t>(ni_e) : static_cast<uint64_t>(no_e);
+      const uint32_t n_cls = in ? ni_e : no_e;
       const int k_cls = in ? K : kb;
       const int t = in ? s : s - K;
-      const uint32_t j = static_cast<uint32_t>(n_cls - static_cast<uint64_t>(k_cls) + t);
+      const uint32_t j = n_cls - static_cast<uint32_t>(k_cls) + static_cast<uint32_t>(t);
       const uint32_t r = static_cast<uint32_t>(__umul64hi(r23[s], static_cast<uint64_t>(j) + 1u));
       bool hit = false;
 #pragma unroll
@@ -589,7 +600,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
 #define CMB_SAMPLER_ROWS_PER_THREAD 0  // (layout experiments only; 0: whenever G-lane groups
 #endif                                 // would need more than one pass over the block's rows)
   if (f <= 16 && (hi - lo) * G > PB && (hi - lo) > static_cast<int64_t>(PB) * CMB_SAMPLER_ROWS_PER_THREAD) {
-    for (int64_t i = lo + threadIdx.x; i < hi; i += PB) {
+    for (int32_t i = static_cast<int32_t>(lo) + threadIdx.x; i < hi; i += PB) {
       int32_t v, off;
       int64_t rs, deg;
       uint32_t rlo, rhi;
@@ -603,7 +614,8 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
       // 8-slot form); other fanouts round up to 8 or 16 slots (more exact sizes spill)
       switch (f) {
 #define CMB_ROWPOS(FM_)                                                                      \
-    row_positions_thread<FM_>(v, rs, deg, rlo, rhi, h, f, a.wi, a.wo, a.k0, a.k1, a.batch, em, \
+    row_positions_thread<FM_>(v, rs, static_cast<uint32_t>(deg), rlo, rhi, h, f, a.wi, a.wo,   \
+                              a.k0, a.k1, a.batch, em,                                       \
                               a.law);                                                        \
     break;
         case 5: CMB_ROWPOS(5)
@@ -685,12 +697,6 @@ __device__ void place_dst_rows(const PArgs& a, int h, int64_t n_h, Smem<PB>& sm)
     ex += static_cast<int32_t>(c[q]);
   }
   __syncthreads();
-  static_assert(kOrderBuckets % CMB_ORDER_CHUNKS == 0, "whole buckets per chunk");
-  if (a.chunks && vblk() == 0)  // chunk c = buckets [c * Q, (c + 1) * Q): where it starts
-    for (int c = threadIdx.x; c <= CMB_ORDER_CHUNKS; c += PB)
-      a.chunks[c] = c < CMB_ORDER_CHUNKS
-                        ? static_cast<int32_t>(off[c * (kOrderBuckets / CMB_ORDER_CHUNKS)])
-                        : static_cast<int32_t>(n_h);
   const int32_t* dst = h == 0 ? a.roots : a.nodes;
   int64_t lo, hi;
   range_of(n_h, 1, lo, hi);
