@@ -59,8 +59,9 @@ def parse():
     ap.add_argument("--flush-l2", default="auto", choices=["auto", "on", "off"],
                     help="write 256 MB before every launch group and time only the groups "
                          "(auto: on when features + CSR < 4x L2)")
-    ap.add_argument("--batches-per-launch", type=int, default=4,
-                    help="batches sampled per persistent-sampler launch (1..4)")
+    ap.add_argument("--batches-per-launch", type=int, default=None,
+                    help="batches sampled per persistent-sampler launch (1..8; default "
+                         "cmb.DEFAULT_BATCHES_PER_LAUNCH = 6, measured best on products)")
     ap.add_argument("--shard", default="none", choices=["none", "ipc", "a2a"],
                     help="row-shard the feature table over the ranks (a6): ipc = one-sided "
                          "gather of peer shards mapped by CUDA IPC, a2a = NCCL all-to-all")
@@ -69,7 +70,11 @@ def parse():
                          "gather (cmb_blocks.dst_order; same bytes either way) -- A/B switch")
     ap.add_argument("--cpu-workers", type=int, default=0,
                     help="threads of the batch-parallel oracle baseline (0 = all host cores)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.batches_per_launch is None:
+        from paper_2504_18082_b200 import DEFAULT_BATCHES_PER_LAUNCH  # (no library load)
+        args.batches_per_launch = DEFAULT_BATCHES_PER_LAUNCH
+    return args
 
 
 def relaunch(args):

@@ -223,7 +223,7 @@ CMB_API cmb_status cmb_sample_blocks_law(const cmb_graph* g, const int32_t* root
  * output blocks and workspace (workspaces must be distinct); results are identical to
  * calling cmb_sample_blocks once per batch. */
 #ifndef CMB_MAX_BATCHES_PER_LAUNCH
-#define CMB_MAX_BATCHES_PER_LAUNCH 4
+#define CMB_MAX_BATCHES_PER_LAUNCH 8
 #endif
 typedef struct {
   const int32_t* roots; /* device int32[n_roots], distinct */

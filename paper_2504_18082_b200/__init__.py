@@ -115,7 +115,10 @@ class BatchFeatures(ctypes.Structure):
                 ("nodes_cap", ctypes.c_int64)]
 
 
-MAX_BATCHES_PER_LAUNCH = 4
+MAX_BATCHES_PER_LAUNCH = 8
+# batches per sampler launch of the benchmarked step (bench.py default; products: 166 us per batch
+# at 6 vs 169 at 4 and 171 at 8 -- 148 SMs split into 6 virtual grids of 24 blocks)
+DEFAULT_BATCHES_PER_LAUNCH = 6
 LAW_A, LAW_SLOT = 0, 1  # Knob-2 laws (include/cmb.h cmb_sample_law)
 
 

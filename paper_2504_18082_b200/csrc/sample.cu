@@ -19,7 +19,7 @@ constexpr int kMaxPersistBlocks = pst::kMaxBlocks;
 struct SampleWs {
   WsHeader* hdr;
   unsigned* bar;             // grid barrier {arrivals, generation}
-  unsigned long long* pub;   // [2][kMaxPersistBlocks] tagged block aggregates
+  unsigned long long* pub;   // [3][kMaxPersistBlocks] tagged block aggregates / bases
   uint32_t* hist;            // [kOrderBuckets] dst rows of hop L-1 per node-id bucket, then
   uint32_t* cursor;          // [kOrderBuckets] rows placed so far per bucket (contiguous)
   uint64_t* prof;            // [kMaxPersistBlocks][64] sub-step timeline
@@ -49,7 +49,8 @@ SampleWs carve_sample_ws(void* base, int64_t n_roots, const int32_t* fanouts, in
   SampleWs w;
   w.hdr = c.take<WsHeader>(1);
   w.bar = c.take<unsigned>(64);
-  w.pub = c.take<unsigned long long>(2 * kMaxPersistBlocks);  // follows bar contiguously
+  // [3][kMaxPersistBlocks]: count and flag aggregates, then the last hop's block bases
+  w.pub = c.take<unsigned long long>(3 * kMaxPersistBlocks);  // follows bar contiguously
   w.hist = c.take<uint32_t>(2 * pst::kOrderBuckets);
   w.cursor = w.hist + pst::kOrderBuckets;
   w.prof = c.take<uint64_t>(static_cast<size_t>(kMaxPersistBlocks) * 64);

@@ -148,7 +148,7 @@ struct PArgs {
   void* map;                // [N] tagged direct dedup map (see above), MapWord<W>::T words
   unsigned* tag_ctr;        // [1] batches sampled with this workspace so far
   uint32_t* scan;           // [max e_cap] flag << 31 | block-local inclusive flag scan
-  unsigned long long* pub;  // [2][kMaxBlocks] tagged block aggregates
+  unsigned long long* pub;  // [3][kMaxBlocks] tagged block aggregates, last-hop block bases
   unsigned* bar;            // [0] arrivals, [1] generation
   uint64_t* prof;           // [kMaxBlocks][64] per-block %globaltimer at sub-step boundaries
   uint32_t* hist;           // [kOrderBuckets] dst rows of hop L-1 per bucket v >> order_shift
@@ -180,6 +180,14 @@ __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long l
 }
 __device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // Generation-counting grid barrier (all blocks co-resident).
@@ -303,19 +311,19 @@ struct PickEmit {
   T* map;
   T tag;
   uint32_t e0;                 // absolute edge index of the row's first pick
+  // (reading the entry first and skipping the reduction when it already holds a winning value,
+  // against hub contention at p = 1, measured no better at MIX-0 / NORAND p = 1 and 1.9 us per
+  // batch slower at RAND: removed)
   __device__ __forceinline__ void put(int k, int64_t p) const {
     const uint32_t u = static_cast<uint32_t>(__ldg(ind + p));
     out[k] = static_cast<int32_t>(u);
-    const T m = tag | (M::kMarkerTop - (e0 + static_cast<uint32_t>(k)));
-    // read the entry first: a node picked by many rows (hubs; every pick of a community at
-    // p = 1) would otherwise queue one same-address atomic per pick in L2
-    if (map_ld(map + u) < m) map_max(map + u, m);
+    map_max(map + u, tag | (M::kMarkerTop - (e0 + static_cast<uint32_t>(k))));
   }
 #ifndef CMB_PUT_ROW_MAX
 #define CMB_PUT_ROW_MAX 10  // widest slot form whose picks are emitted as one batch (16: spills)
 #endif
-  // all picks of a row at once (thread-per-row form, FM <= 10): every neighbour load, then every
-  // map load, then the reductions -- two round trips per row instead of two per pick
+  // all picks of a row at once (thread-per-row form, FM <= 10): every neighbour load, then the
+  // reductions -- one round trip per row instead of one per pick
   template <int FM>
   __device__ __forceinline__ void put_row(int tot, int64_t rs, const uint32_t (&pos)[FM]) const {
     if (tot <= 0) return;
@@ -331,22 +339,9 @@ struct PickEmit {
       rk[s] = r;
       if (s < tot) out[r] = static_cast<int32_t>(u[s]);
     }
-    T cur[FM];
-#ifndef CMB_MARK_PRECHECK  // layout experiments only
-#define CMB_MARK_PRECHECK 1
-#endif
-#if CMB_MARK_PRECHECK
 #pragma unroll
-    for (int s = 0; s < FM; ++s) cur[s] = map_ld(map + u[s]);
-#else
-#pragma unroll
-    for (int s = 0; s < FM; ++s) cur[s] = 0;
-#endif
-#pragma unroll
-    for (int s = 0; s < FM; ++s) {
-      const T m = tag | (M::kMarkerTop - (e0 + rk[s]));
-      if (s < tot && cur[s] < m) map_max(map + u[s], m);
-    }
+    for (int s = 0; s < FM; ++s)
+      if (s < tot) map_max(map + u[s], tag | (M::kMarkerTop - (e0 + rk[s])));
   }
 };
 
@@ -724,7 +719,7 @@ __device__ void place_dst_rows(const PArgs& a, int h, int64_t n_h, Smem<PB>& sm)
 // flags + prefix + assign
 template <int PB, class W>
 __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
-                                  typename MapWord<W>::T tag, unsigned ctr) {
+                                  typename MapWord<W>::T tag, unsigned ctr, bool fuse) {
   using M = MapWord<W>;
   using T = typename M::T;
   T* map = static_cast<T*>(a.map);
@@ -732,6 +727,12 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   const int64_t e_h = __ldcg(a.sizes + a.L + 1 + h);
   int64_t lo, hi;
   range_of(e_h, 32, lo, hi);
+  // fuse (last hop, 32-bit words): the relabel of this hop is done here, not in a pass after one
+  // more grid barrier.  Every edge's entry is final after the marks: its own marker (a first
+  // occurrence), a final id (a node of an earlier hop) or the marker of the first occurrence w.
+  // The scan word then records that: flag << 31 | count, 1 << 30 | id, or w; the assign loop
+  // turns w into id(w) = n_h + base(block of w) + count(w) - 1 from the blocks' published bases.
+  unsigned long long* bases = a.pub + 2 * kMaxBlocks;
   uint32_t* mask = (h == a.L - 1) ? a.mask : nullptr;
   const int32_t* nbr = a.indices[h];
   if (a.order && h == a.L - 1) place_dst_rows<PB>(a, h, n_h, sm);
@@ -760,6 +761,10 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
     for (int k = 0; k < 8; ++k) {  // flag << 31 | block-local inclusive flag count
       acc += (fl >> k) & 1u;
       sc[k] = static_cast<int32_t>(((fl >> k) & 1u) << 31 | static_cast<uint32_t>(acc));
+      if (fuse && !((fl >> k) & 1u))  // not a first occurrence: the node's id, or its first edge
+        sc[k] = static_cast<int32_t>(
+            (mv[k] & M::kFinal) ? (1u << 30) | static_cast<uint32_t>(mv[k] & M::kVal)
+                                : M::kMarkerTop - static_cast<uint32_t>(mv[k] & M::kVal));
     }
     st8(reinterpret_cast<int32_t*>(a.scan), e0, hi, sc);
     if (mask) {  // edges e0 .. e0+7 are bits 8 * (thread % 4) .. of word e0 / 32
@@ -771,10 +776,48 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
     run += agg;
   }
   CMB_PROF(a, pk);
+  if (fuse) __threadfence();  // this thread's scan words before the block's base (below)
   const int32_t base =
       publish_and_prefix<PB>(a.pub + kMaxBlocks, pub_tag(ctr, h), run, sm);
   CMB_PROF(a, pk);
   if (vblk() == vgrid() - 1 && threadIdx.x == 0) a.sizes[h + 1] = n_h + base + run;
+  if (fuse) {
+    if (threadIdx.x == 0)  // the block's base, tagged like the aggregates (no clearing needed)
+      st_release64(bases + vblk(), (static_cast<unsigned long long>(pub_tag(ctr, h)) << 32) |
+                                       static_cast<uint32_t>(base));
+    int64_t per = (e_h + vgrid() - 1) / vgrid();  // range_of's block size
+    per = (per + 31) / 32 * 32;
+    int32_t* ind = a.indices[h];
+    for (int64_t e0 = lo + static_cast<int64_t>(threadIdx.x) * 8; e0 < hi;
+         e0 += static_cast<int64_t>(PB) * 8) {
+      int32_t sc[8], u[8], id[8];
+      ld8(reinterpret_cast<const int32_t*>(a.scan), e0, hi, sc);
+      ld8(nbr, e0, hi, u);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t c = static_cast<uint32_t>(sc[k]);
+        if (c >> 31) {  // a first occurrence -> the next local id
+          id[k] = static_cast<int32_t>(n_h + base + (c & 0x7fffffffu) - 1);
+          if (e0 + k < hi) a.nodes[id[k]] = u[k];
+        } else if (c >> 30) {  // a node of an earlier hop
+          id[k] = static_cast<int32_t>(c & 0x3fffffffu);
+        } else if (e0 + k >= hi) {
+          id[k] = 0;
+        } else {  // the id given to edge c, the node's first occurrence (maybe another block's)
+          const int b = static_cast<int>(c / per);
+          const unsigned want = pub_tag(ctr, h);
+          unsigned long long v;
+          while (((v = ld_acquire64(bases + b)) >> 32) != want) {
+          }
+          const uint32_t cw = static_cast<uint32_t>(__ldcg(a.scan + c)) & 0x7fffffffu;
+          id[k] = static_cast<int32_t>(n_h + static_cast<int64_t>(v & 0xffffffffu) + cw - 1);
+        }
+      }
+      st8(ind, e0, hi, id);
+      st8(a.last_src, e0, hi, u);
+    }
+    return;
+  }
   for (int64_t e0 = lo + static_cast<int64_t>(threadIdx.x) * 8; e0 < hi;
        e0 += static_cast<int64_t>(PB) * 8) {
     int32_t sc[8], u[8];
@@ -827,6 +870,11 @@ __device__ __forceinline__ void run_batch(const PArgs& a) {
       map[i] = T(0);
     grid_barrier(a.bar, gen);
   }
+  // the dst-order buckets start empty: cleared here, before the grid barrier that precedes the
+  // last hop's count step (one more barrier when that count step is hop 0's)
+  if (a.order && vblk() == 0)
+    for (int i = threadIdx.x; i < 2 * kOrderBuckets; i += PB) a.hist[i] = 0u;  // (hist, cursor)
+  if (a.order && a.L == 1) grid_barrier(a.bar, gen);
   CMB_PROF(a, pk);
   for (int64_t i = vblk() * (int64_t)PB + threadIdx.x; i < a.n_roots;
        i += (int64_t)vgrid() * PB) {
@@ -861,14 +909,15 @@ __device__ __forceinline__ void run_batch(const PArgs& a) {
       a.tag_ctr[0] = ctr;
       a.tag_ctr[1] = kWidth;
     }
-    phase_flag_assign<PB, W>(a, h, sm, pk, tag, ctr); // +6 flag scan, +7 prefix
-    CMB_PROF(a, pk);                                  // +8 assign
+    // the last hop with 32-bit words relabels inside its assign step (no barrier, no pass)
+    const bool fuse = sizeof(T) == 4 && h == a.L - 1;
+    phase_flag_assign<PB, W>(a, h, sm, pk, tag, ctr, fuse);  // +6 flag scan, +7 prefix
+    CMB_PROF(a, pk);                                  // +8 assign (+ relabel if fused)
+    if (fuse) break;
     grid_barrier(a.bar, gen);
     CMB_PROF(a, pk);                                  // +9 barrier
   }
-  phase_relabel<PB, W>(a, a.L - 1);
-  if (a.order && vblk() == 0)  // the dst-order buckets, used up (grid barrier above): cleared
-    for (int i = threadIdx.x; i < 2 * kOrderBuckets; i += PB) a.hist[i] = 0u;  // (hist, cursor)
+  if (sizeof(T) != 4) phase_relabel<PB, W>(a, a.L - 1);
   CMB_PROF(a, pk);
 }
 

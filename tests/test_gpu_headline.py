@@ -1,9 +1,9 @@
 """GPU parity of the EXACT benchmarked path (bench.py's default run), every batch of an epoch.
 
 bench.py times products-shaped input (BASELINE.json configs[3], full size) through
-``BatchedPipeline.step_group`` -> ``cmb_step_group``: one cooperative sampler launch for 4
-batches (the SMs split into 4 virtual grids of num_sms / 4 blocks) followed by the fused
-gather + aggregate of each batch.  This file runs that same call, with the same pipeline
+``BatchedPipeline.step_group`` -> ``cmb_step_group``: one cooperative sampler launch for
+``cmb.DEFAULT_BATCHES_PER_LAUNCH`` = 6 batches (the SMs split into 6 virtual grids of 24 blocks)
+followed by the ONE fused gather + aggregate launch over all of them.  This file runs that same call, with the same pipeline
 object and the same global batch ids (epoch 0: 0 .. n_batches - 1, the last group ragged),
 and compares EVERY batch of epoch 0 with the oracle:
 
@@ -73,7 +73,7 @@ def test_bench_launch_config_every_batch_of_epoch0(mode, k, p):
     b, prep, g = _products()
     cfg = b.cfg
     L, F, B = len(cfg.fanouts), cfg.feat_dim, cfg.batch_size
-    G = cmb.MAX_BATCHES_PER_LAUNCH  # bench.py --batches-per-launch default (4)
+    G = cmb.DEFAULT_BATCHES_PER_LAUNCH  # bench.py --batches-per-launch default (6)
     pipe = cmb.BatchedPipeline(g, torch.from_numpy(b.train), B, cfg.fanouts, mode=mode, mix=k,
                                p=p, seed=SEED, nb=G)
     nb = pipe.n_batches
@@ -103,7 +103,7 @@ def test_bench_launch_config_every_batch_of_epoch0(mode, k, p):
         return got["n"]
 
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    vgrid = (sms - sms % G) // G  # blocks per batch in a 4-batch launch (sample.cu)
+    vgrid = (sms - sms % G) // G  # blocks per batch in a G-batch launch (sample.cu)
     sizes = {}
     with ThreadPoolExecutor(max_workers=workers) as ex:
         futs = []

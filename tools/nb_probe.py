@@ -17,8 +17,10 @@ def main():
     cfg = CONFIGS["products"]
     b = generate(cfg)
     g = cmb.Graph.from_bundle(b)
-    pipe = cmb.BatchedPipeline(g, torch.from_numpy(b.train), cfg.batch_size, cfg.fanouts, p=0.5,
-                               nb=nb)
+    mode = os.environ.get("MODE", "rand")  # Knob-1 (env MODE, MIX, P)
+    pipe = cmb.BatchedPipeline(g, torch.from_numpy(b.train), cfg.batch_size, cfg.fanouts,
+                               mode=mode, mix=float(os.environ.get("MIX", "0")),
+                               p=float(os.environ.get("P", "0.5")), nb=nb)
     K = 400 // nb * nb
     for t in range(0, 8 * nb, nb):
         pipe.step_group(list(range(t, t + nb)))

@@ -15,7 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2504_18082_b200 as cmb  # noqa: E402
 from gen import CONFIGS, generate  # noqa: E402
 
-PROF_OFFSET = 98816          # carve order: header 256, barrier 256, pub 2*4096*8, dst-order
+PROF_OFFSET = 131584         # carve order: header 256, barrier 256, pub 3*4096*8, dst-order
                              # hist + cursor 2*4096*4 (sample.cu)
 SUB = ["relabel(h-1)", "count", "prefix", "positions", "picks+mark", "barrierA",
        "flag_scan", "prefix2", "assign", "barrierC"]
@@ -31,10 +31,10 @@ def main():
                                mode=os.environ.get("MODE", "rand"),
                                mix=float(os.environ.get("MIX", "0")), p=p, nb=nb)
     L = len(cfg.fanouts)
-    npts = 2 + 10 * L
+    npts = 1 + 10 * L  # 32-bit map words: the last hop relabels inside its assign step
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     nblk = (sms - sms % nb) // nb  # virtual blocks of batch 0 of each launch
-    labels = [f"h{h}.{s}" for h in range(L) for s in SUB] + ["relabel(L-1)"]
+    labels = [f"h{h}.{s}" for h in range(L) for s in SUB][:-1] + ["end"]
     crit, mean, mx = [], [], []
     pipe.start_epoch(0)
     for t in range(25):
