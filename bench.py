@@ -428,9 +428,10 @@ def run_cmb(args, bundle):
     def gbatch(t):  # global batch id of this rank's t-th step (round-robin, reading R22)
         return cmb_dist.global_batch(rank, world, t)
 
-    def group(t0, count, events=None):
-        """Steps t0 .. t0+count-1 of this rank: one sampler launch + `count` gather launches."""
-        return pipe.step_group([gbatch(t) for t in range(t0, t0 + count)], events=events)
+    def group(t0, count, events=None, sizes_out=None):
+        """Steps t0 .. t0+count-1 of this rank: one sampler launch + one gather launch."""
+        return pipe.step_group([gbatch(t) for t in range(t0, t0 + count)], events=events,
+                               sizes_out=sizes_out)
 
     # warm-up (also compiles nothing: the library is prebuilt)
     for t in range(0, W, G):
@@ -465,11 +466,10 @@ def run_cmb(args, bundle):
             evs = evpool[k0 // G]
             if flush:
                 scrub.fill_(k0 & 0xFF)   # evicts the previous group's lines from L2
-            ss = group(W + k0, cnt, evs)
+            ss = group(W + k0, cnt, evs, sizes_log[k0:k0 + cnt])  # sizes written in place
             evlog.append({"sample": (evs[0], evs[1]),
                           "gather": [(evs[2 + 2 * i], evs[3 + 2 * i]) for i in range(cnt)]})
             n_groups += 1
-            sizes_log[k0:k0 + cnt].copy_(pipe.group_sizes[:cnt], non_blocking=True)
         end.record(stream)
         torch.cuda.synchronize()
     if world > 1:

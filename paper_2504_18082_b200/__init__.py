@@ -1212,9 +1212,11 @@ class BatchedPipeline(MiniBatchPipeline):
         return evs
 
     def step_group(self, gbs: Sequence[int], roots: Optional[Sequence[torch.Tensor]] = None,
-                   events=None):
+                   events=None, sizes_out: Optional[torch.Tensor] = None):
         """Run the global batches `gbs` (at most nb) with one sampler launch, then the fused
-        gather + aggregate of each.  `roots` optionally overrides the epoch order.  If `events`
+        gather + aggregate of each.  `roots` optionally overrides the epoch order; `sizes_out`
+        (int64 [>= n, 2L+1], device) receives the batches' size vectors instead of group_sizes
+        (no copy kernel per group).  If `events`
         is a dict, ('sample' -> (start, end)) and ('gather' -> [(start, end), ...]) CUDA events
         are recorded around the launches.  Returns the samplers used (one per batch)."""
         gbs = [int(x) for x in gbs]
@@ -1254,8 +1256,20 @@ class BatchedPipeline(MiniBatchPipeline):
         if ev_list is not None:
             evp = (ctypes.c_void_p * (2 + 2 * n))(*[e.cuda_event for e in ev_list[: 2 + 2 * n]])
         s0 = ss[0]
-        _check(lib().cmb_step_group(self.graph.handle, self._batches, self._feats, n, s0._f, s0.L,
-                                    float(self.p), self.law, int(self.seed), evp, _stream()))
+        if sizes_out is not None:  # this group's size vectors straight into the caller's rows
+            if (sizes_out.dtype != torch.int64 or sizes_out.shape[0] < n or
+                    sizes_out.shape[1] != 2 * s0.L + 1 or not sizes_out.is_contiguous()):
+                raise ValueError("sizes_out: contiguous int64 [>= n, 2L+1]")
+            for i, s in enumerate(ss):
+                s._blocks.sizes = sizes_out[i].data_ptr()
+        try:
+            _check(lib().cmb_step_group(self.graph.handle, self._batches, self._feats, n, s0._f,
+                                        s0.L, float(self.p), self.law, int(self.seed), evp,
+                                        _stream()))
+        finally:  # the launches captured the pointers; later calls use group_sizes again
+            if sizes_out is not None:
+                for s in ss:
+                    s._blocks.sizes = s.sizes.data_ptr()
         return ss
 
 

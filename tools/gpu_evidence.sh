@@ -22,5 +22,5 @@ done
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_sage_layer -s 4 -c 1 \
   -o $out/full_k_sage_layer python bench.py --steps 8 --warmup 4 --no-extra --layer \
   --cpu-seconds 1 > /dev/null 2>> $out/ncu.err
-NB=4 timeout 300 python tools/profile_sampler.py > $out/sampler_timeline.json 2>> $out/ncu.err
+NB=6 timeout 300 python tools/profile_sampler.py > $out/sampler_timeline.json 2>> $out/ncu.err
 echo done
