@@ -225,6 +225,7 @@ struct Smem {
     typename cub::BlockReduce<int32_t, PB>::TempStorage reduce;
   } cub;
   int32_t bc;
+  int32_t next;  // positions step: the next unclaimed row chunk of the block
   RowCache rows;
 };
 
@@ -525,6 +526,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   int64_t lo, hi;
   range_of(n_h, 1, lo, hi);
   RowCache& rc = sm.rows;
+  if (threadIdx.x == 0) sm.next = 0;  // read after publish_and_prefix's barrier
   // (1) counts, block scan, cached row info
   int32_t run = 0;
   for (int64_t t0 = lo; t0 < hi; t0 += PB) {
@@ -595,7 +597,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
 #define CMB_SAMPLER_ROWS_PER_THREAD 0  // (layout experiments only; 0: whenever G-lane groups
 #endif                                 // would need more than one pass over the block's rows)
   if (f <= 16 && (hi - lo) * G > PB && (hi - lo) > static_cast<int64_t>(PB) * CMB_SAMPLER_ROWS_PER_THREAD) {
-    for (int32_t i = static_cast<int32_t>(lo) + threadIdx.x; i < hi; i += PB) {
+    auto row = [&](int32_t i) {
       int32_t v, off;
       int64_t rs, deg;
       uint32_t rlo, rhi;
@@ -622,7 +624,26 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
           CMB_ROWPOS(16)
 #undef CMB_ROWPOS
       }
+    };
+#ifndef CMB_DYN_ROWS  // layout experiments only
+#define CMB_DYN_ROWS 0
+#endif
+#if CMB_DYN_ROWS
+    // warps claim 32-row chunks from a block counter: a warp whose rows come back early takes
+    // more, so the block's barrier after this step waits less for its slowest warp
+    const int32_t nrows = static_cast<int32_t>(hi - lo);
+    const int wl = threadIdx.x & 31;
+    for (;;) {
+      int32_t c0 = 0;
+      if (wl == 0) c0 = atomicAdd(&sm.next, 32);
+      c0 = __shfl_sync(0xffffffffu, c0, 0);
+      if (c0 >= nrows) break;
+      const int32_t i = static_cast<int32_t>(lo) + c0 + wl;
+      if (i < hi) row(i);
     }
+#else
+    for (int32_t i = static_cast<int32_t>(lo) + threadIdx.x; i < hi; i += PB) row(i);
+#endif
   } else {
     const int lane = threadIdx.x & (G - 1);
     const int wl = threadIdx.x & 31;
@@ -736,29 +757,36 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   uint32_t* mask = (h == a.L - 1) ? a.mask : nullptr;
   const int32_t* nbr = a.indices[h];
   if (a.order && h == a.L - 1) place_dst_rows<PB>(a, h, n_h, sm);
-  // a thread owns 8 consecutive edges per round (the block's range is 32-aligned, so 4 threads
-  // fill one new-src mask word): their ids in two vector loads, all 8 map lookups in flight,
-  // one block scan per PB * 8 edges
+  // a thread owns EPT consecutive edges per round (the block's range is 32-aligned, so 32 / EPT
+  // threads fill one new-src mask word): their ids in vector loads, all EPT map lookups in
+  // flight, one block scan per PB * EPT edges
+#ifndef CMB_FLAG_EPT  // layout experiments only: 8 or 16
+#define CMB_FLAG_EPT 8
+#endif
+  constexpr int EPT = CMB_FLAG_EPT;
+  static_assert(EPT == 8 || EPT == 16, "edges per thread in the flag step");
   int32_t run = 0;
-  for (int64_t c0 = lo; c0 < hi; c0 += static_cast<int64_t>(PB) * 8) {
-    const int64_t e0 = c0 + static_cast<int64_t>(threadIdx.x) * 8;
-    int32_t u[8];
-    ld8(nbr, e0, hi, u);
-    T mv[8];
+  for (int64_t c0 = lo; c0 < hi; c0 += static_cast<int64_t>(PB) * EPT) {
+    const int64_t e0 = c0 + static_cast<int64_t>(threadIdx.x) * EPT;
+    int32_t u[EPT];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) mv[k] = map_ld(map + u[k]);  // past hi: u = 0, harmless
+    for (int q = 0; q < EPT; q += 8)
+      ld8(nbr, e0 + q, hi, *reinterpret_cast<int32_t(*)[8]>(u + q));
+    T mv[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) mv[k] = map_ld(map + u[k]);  // past hi: u = 0, harmless
     uint32_t fl = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < EPT; ++k)
       fl |= (e0 + k < hi && mv[k] == (tag | (M::kMarkerTop - static_cast<uint32_t>(e0 + k))))
                 ? (1u << k) : 0u;
     int32_t ex, agg;
     cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(__popc(fl), ex, agg);
     __syncthreads();
-    int32_t sc[8];
+    int32_t sc[EPT];
     int32_t acc = run + ex;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {  // flag << 31 | block-local inclusive flag count
+    for (int k = 0; k < EPT; ++k) {  // flag << 31 | block-local inclusive flag count
       acc += (fl >> k) & 1u;
       sc[k] = static_cast<int32_t>(((fl >> k) & 1u) << 31 | static_cast<uint32_t>(acc));
       if (fuse && !((fl >> k) & 1u))  // not a first occurrence: the node's id, or its first edge
@@ -766,12 +794,16 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
             (mv[k] & M::kFinal) ? (1u << 30) | static_cast<uint32_t>(mv[k] & M::kVal)
                                 : M::kMarkerTop - static_cast<uint32_t>(mv[k] & M::kVal));
     }
-    st8(reinterpret_cast<int32_t*>(a.scan), e0, hi, sc);
-    if (mask) {  // edges e0 .. e0+7 are bits 8 * (thread % 4) .. of word e0 / 32
-      uint32_t w = fl << (8 * (threadIdx.x & 3));
-      w |= __shfl_xor_sync(0xffffffffu, w, 1);
-      w |= __shfl_xor_sync(0xffffffffu, w, 2);
-      if ((threadIdx.x & 3) == 0 && e0 < hi) mask[e0 >> 5] = w;
+#pragma unroll
+    for (int q = 0; q < EPT; q += 8)
+      st8(reinterpret_cast<int32_t*>(a.scan), e0 + q, hi,
+          *reinterpret_cast<const int32_t(*)[8]>(sc + q));
+    if (mask) {  // edges e0 .. e0+EPT-1 are bits EPT * (thread % (32 / EPT)) .. of word e0 / 32
+      constexpr int TPW = 32 / EPT;
+      uint32_t w = fl << (EPT * (threadIdx.x & (TPW - 1)));
+#pragma unroll
+      for (int o = 1; o < TPW; o <<= 1) w |= __shfl_xor_sync(0xffffffffu, w, o);
+      if ((threadIdx.x & (TPW - 1)) == 0 && e0 < hi) mask[e0 >> 5] = w;
     }
     run += agg;
   }
