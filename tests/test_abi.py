@@ -108,3 +108,34 @@ def test_layer_entry_points_host_checks(cmb):
                                               0.0, 1, None, 1, None)):
         assert call() == 1
         assert b"null" in L.cmb_last_error_message()
+
+
+def test_sample_workspace_map_width(cmb):
+    """cmb_sample_workspace_bytes (host only): the dedup map takes 4 bytes per node while every
+    local id and edge position of the batch's capacity stays below 2^24, 8 bytes beyond (the
+    workspace layout is otherwise a function of the largest hop's edge capacity)."""
+    L = cmb.lib()
+    N = 734_708
+    fan = (32, 32)
+    f = (ctypes.c_int32 * 2)(*fan)
+
+    def nbytes(r):
+        return L.cmb_sample_workspace_bytes(r, f, 2, N)
+
+    def max_e(r):
+        n_cap, e_cap = cmb.blocks_capacity(r, fan, N)
+        return max(e_cap), n_cap[-1]
+
+    lim = (1 << 24) - 1
+    # the largest narrow batch and the smallest wide one (capacity grows with n_roots)
+    lo, hi = 1, N  # binary search: max(max_e(lo)) <= lim < max(max_e(hi))
+    while hi - lo > 1:
+        mid = (lo + hi) // 2
+        lo, hi = (mid, hi) if max(max_e(mid)) <= lim else (lo, mid)
+    narrow, wide = lo, hi
+    assert max(max_e(narrow)) <= lim < max(max_e(wide))
+    d_scan = 4 * (max_e(wide)[0] - max_e(narrow)[0])
+    d = nbytes(wide) - nbytes(narrow)
+    assert abs(d - (4 * N + d_scan)) <= 512, (d, 4 * N + d_scan)   # 256-B aligned pieces
+    d_narrow = nbytes(narrow) - nbytes(narrow - 1)
+    assert abs(d_narrow - 4 * (max_e(narrow)[0] - max_e(narrow - 1)[0])) <= 512
