@@ -102,10 +102,14 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
 }
 
 // One 1024-thread block per SM (64 registers: the whole register file), co-resident by
-// construction.  (A 512-thread form measured 101 vs 78 us per batch and was removed.)
+// construction.  (One 512-thread block per SM measured 101 vs 78 us per batch.)  Layout
+// experiments: CMB_SAMPLER_PB = 512 runs TWO 512-thread blocks per SM, of different batches.
+#ifndef CMB_SAMPLER_PB
+#define CMB_SAMPLER_PB 1024
+#endif
 cmb_status launch_persistent(const cmb_graph* g, pst::PMulti& m, bool wide, cudaStream_t s) {
-  constexpr int kPB = 1024;
-  int grid = g->num_sms;
+  constexpr int kPB = CMB_SAMPLER_PB;
+  int grid = g->num_sms * (1024 / kPB);
   if (grid > kMaxPersistBlocks) grid = kMaxPersistBlocks;
   grid -= grid % m.nb;    // equal virtual grids per batch
   void* args[] = {&m};
