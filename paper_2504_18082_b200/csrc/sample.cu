@@ -102,8 +102,9 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
 }
 
 // One 1024-thread block per SM (64 registers: the whole register file), co-resident by
-// construction.  (One 512-thread block per SM measured 101 vs 78 us per batch.)  Layout
-// experiments: CMB_SAMPLER_PB = 512 runs TWO 512-thread blocks per SM, of different batches.
+// construction.  (One 512-thread block per SM measured 101 vs 78 us per batch; TWO 512-thread
+// blocks per SM, of different batches -- CMB_SAMPLER_PB = 512, a layout experiment -- 172 vs
+// 164 us per step at 6 batches per launch.)
 #ifndef CMB_SAMPLER_PB
 #define CMB_SAMPLER_PB 1024
 #endif
