@@ -105,6 +105,22 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// the L2 policy of the fused gather's feature-row loads (layout experiments: CMB_ROW_POLICY
+// 1 = evict_normal, 2 = evict_first; 0, the product, = evict_last)
+#ifndef CMB_ROW_POLICY
+#define CMB_ROW_POLICY 0
+#endif
+__device__ __forceinline__ uint64_t policy_rows() {
+  uint64_t p;
+#if CMB_ROW_POLICY == 1
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+#elif CMB_ROW_POLICY == 2
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#else
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
+}
 __device__ __forceinline__ float4 ldg4_hint(const float4* p, uint64_t pol) {
   float4 r;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"

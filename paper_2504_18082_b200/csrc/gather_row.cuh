@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256, MINB)
     k_gather_mean_row(const __grid_constant__ GatherSet S, const __grid_constant__ Rows rows,
                       int f4) {
   constexpr unsigned kFull = 0xffffffffu;
-  const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+  const uint64_t pol_keep = policy_rows(), pol_stream = policy_evict_first();
   __shared__ int32_t pre[kMaxGatherBatches + 1];
   if (threadIdx.x == 0) {
     int32_t t = 0;
