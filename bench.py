@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--shard", default="none", choices=["none", "ipc", "a2a"],
                     help="row-shard the feature table over the ranks (a6): ipc = one-sided "
                          "gather of peer shards mapped by CUDA IPC, a2a = NCCL all-to-all")
+    ap.add_argument("--out-ld", type=int, default=0,
+                    help="row stride (floats) of the X_in / H outputs; 0 = the feature table's "
+                         "(layout experiments: a multiple of 8 starts every row on a 32-B sector)")
     ap.add_argument("--dst-order", default="on", choices=["on", "off"],
                     help="let the sampler write the last hop's dst visiting order for the fused "
                          "gather (cmb_blocks.dst_order; same bytes either way) -- A/B switch")
@@ -420,6 +423,8 @@ def run_cmb(args, bundle):
                                nb=G, law=args.law)
     for smp in pipe.samplers:
         smp.set_dst_order(args.dst_order == "on")
+        if args.out_ld:
+            smp.alloc_features_ld(args.out_ld)
     nb = pipe.n_batches
     stream = torch.cuda.current_stream()
     K, W = args.steps, args.warmup
