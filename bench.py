@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--out-ld", type=int, default=0,
                     help="row stride (floats) of the X_in / H outputs; 0 = the feature table's "
                          "(layout experiments: a multiple of 8 starts every row on a 32-B sector)")
+    ap.add_argument("--train-graph", default="on", choices=["on", "off"],
+                    help="replay each NEXT-4 training step as a captured CUDA graph "
+                         "(GraphSAGE.train_step(graph=True)) or enqueue it launch by launch")
     ap.add_argument("--dst-order", default="on", choices=["on", "off"],
                     help="let the sampler write the last hop's dst visiting order for the fused "
                          "gather (cmb_blocks.dst_order; same bytes either way) -- A/B switch")
@@ -1054,10 +1057,10 @@ def train_point(bundle, graph, cfg, args, n_batches=48):
             cmb.sample_multi(smps, [pipe.batch_roots(k0 + i) for i in range(nbl)],
                              [k0 + i for i in range(nbl)], 0.5, args.seed)
 
-        for w in range(0, 2 * nbl, nbl):
+        for w in range(0, 2 * nbl, nbl):  # the first step per sampler captures its CUDA graph
             group(w)
             for sm in smps:
-                model.train_step(sm, labels)
+                model.train_step(sm, labels, graph=args.train_graph == "on")
         torch.cuda.synchronize()
         ng = n // nbl
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 + nbl)] for _ in range(ng)]
@@ -1067,7 +1070,8 @@ def train_point(bundle, graph, cfg, args, n_batches=48):
             group(q * nbl)
             ev[q][1].record(s)
             for i, sm in enumerate(smps):
-                losses[q * nbl + i:q * nbl + i + 1].copy_(model.train_step(sm, labels))
+                losses[q * nbl + i:q * nbl + i + 1].copy_(
+                    model.train_step(sm, labels, graph=args.train_graph == "on"))
                 ev[q][2 + i].record(s)
         torch.cuda.synchronize()
         assert all(sm.status() == 0 for sm in smps) and int(model.status.item()) == 0
@@ -1086,7 +1090,8 @@ def train_point(bundle, graph, cfg, args, n_batches=48):
     return {"model": f"GraphSAGE {len(cfg.fanouts)} layers, hidden 256, {C} classes, Adam",
             "timed": f"{n_batches} consecutive batches of epoch 0 per point, 4 per sampler launch "
                      f"then a training step each (events around the sampler launch and the 4 "
-                     f"steps; host enqueue included)", "points": points}
+                     f"steps; host enqueue included)",
+            "cuda_graph": args.train_graph == "on", "points": points}
 
 
 def main():

@@ -665,6 +665,15 @@ CMB_API cmb_status cmb_adam_step_pack(float* w, const float* g, float* m, float*
                                       double weight_decay, int32_t step,
                                       const cmb_layer_pack* layers, int32_t n_layers,
                                       void* stream);
+/* The same with the step number on the DEVICE: `step` (device int32) is advanced by one on the
+ * stream, then read by the update, which forms the bias corrections from it in fp64 -- nothing
+ * step-dependent is baked into the launches, so a captured CUDA graph of a whole training step
+ * can be replayed (GraphSAGE.train_step(graph=True)).  Same arithmetic as cmb_adam_step_pack. */
+CMB_API cmb_status cmb_adam_step_pack_dev(float* w, const float* g, float* m, float* v,
+                                          int64_t n, double lr, double beta1, double beta2,
+                                          double eps, double weight_decay, int32_t* step,
+                                          const cmb_layer_pack* layers, int32_t n_layers,
+                                          void* stream);
 
 /* ------------------------------------------------------------------ status */
 /* Synchronises `stream`, returns (and clears) the sticky device status word of a

@@ -60,7 +60,7 @@ SYMBOLS = ["cmb_graph_workspace_bytes", "cmb_load_graph", "cmb_free_graph", "cmb
            "cmb_sage_hidden_weights_t_bytes", "cmb_sage_hidden_pack_weights_t",
            "cmb_sage_hidden_input_grad", "cmb_softmax_xent", "cmb_adam_step",
            "cmb_sage_saved_a_bytes", "cmb_sage_layer_forward_save", "cmb_sage_layer_backward_saved",
-           "cmb_adam_step_pack", "cmb_sage_dense_weights_bytes", "cmb_sage_dense_workspace_bytes",
+           "cmb_adam_step_pack", "cmb_adam_step_pack_dev", "cmb_sage_dense_weights_bytes", "cmb_sage_dense_workspace_bytes",
            "cmb_sage_dense_pack_weights", "cmb_sage_dense_forward", "cmb_sage_dense_backward",
            "cmb_get_device_status",
            "cmb_status_string", "cmb_last_error_message", "cmb_version"]
@@ -214,6 +214,9 @@ def lib():
             "cmb_adam_step_pack": (I32, [P, P, P, P, I64, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_double, ctypes.c_double, ctypes.c_double, I32,
                                          ctypes.POINTER(LayerPack), I32, P]),
+            "cmb_adam_step_pack_dev": (I32, [P, P, P, P, I64, ctypes.c_double, ctypes.c_double,
+                                             ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                             P, ctypes.POINTER(LayerPack), I32, P]),
             "cmb_sage_layer_forward_save": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, P, I32,
                                                   I32, I32, P, I64, P, SZ, P]),
             "cmb_sage_layer_backward_saved": (I32, [P, ctypes.POINTER(Blocks), I32, I64, P, SZ, P,
@@ -861,6 +864,9 @@ class GraphSAGE:
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self._bufs = {}
+        self._step_dev = torch.zeros(1, dtype=torch.int32, device=dev)  # graph-replayed steps
+        self._step_synced = 0  # step_count the device counter matched when last written
+        self._graphs = {}
         self.device = dev
         # layer 1's operand tiles are saved by the forward and reloaded by the backward instead
         # of re-gathering the feature rows; False re-gathers (same results)
@@ -897,9 +903,41 @@ class GraphSAGE:
                       sampler.sage_hidden(layer, h, ys[-1], out))
         return ys
 
-    def train_step(self, sampler: "Sampler", node_labels: torch.Tensor) -> torch.Tensor:
+    def train_step(self, sampler: "Sampler", node_labels: torch.Tensor,
+                   graph: bool = False) -> torch.Tensor:
         """One training step on the last sampled batch: forward, loss, backward, Adam, repack.
-        Returns the device fp64 loss tensor (no host synchronisation)."""
+        Returns the device fp64 loss tensor (no host synchronisation).
+
+        graph=True: the step's ~20 launches are captured once per (sampler, labels) pair into a
+        CUDA graph and replayed (no per-launch host cost or launch gaps).  Every launch reads its
+        sizes from the device and the Adam step number from a device counter
+        (cmb_adam_step_pack_dev), so a replay is exactly the eager step on the sampler's current
+        batch.  The first call with a new pair runs the step eagerly (it sizes every buffer) and
+        captures it for the next calls."""
+        if not graph:
+            return self._train_step(sampler, node_labels, dev_step=False)
+        key = (id(sampler), node_labels.data_ptr())
+        g = self._graphs.get(key)
+        if g is not None:
+            if int(self._step_synced) != self.step_count:  # eager host-step calls in between
+                self._step_dev.fill_(self.step_count)
+            g.replay()
+            self.step_count += 1
+            self._step_synced = self.step_count
+            return self.loss
+        self._train_step(sampler, node_labels, dev_step=True)       # eager: buffers sized
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self._train_step(sampler, node_labels, dev_step=True, count=False)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        self._graphs[key] = g
+        self._step_synced = self.step_count
+        return self.loss
+
+    def _train_step(self, sampler: "Sampler", node_labels: torch.Tensor, dev_step: bool,
+                    count: bool = True) -> torch.Tensor:
         L = self.L
         ys = self.forward(sampler)
         fo = self.dims[-1]
@@ -924,7 +962,8 @@ class GraphSAGE:
                 dy = sampler.sage_hidden_input_grad(
                     layer, h, dz, self._buf(("dx", l), sampler.n_cap[h + 1], layer.feat_dim,
                                             torch.float32)[:sampler.n_cap[h + 1]])
-        self.step_count += 1
+        if count:
+            self.step_count += 1
         # Adam and the repack of every weight image (forward and transposed) in one launch
         packs = (LayerPack * L)()
         for l, layer in enumerate(self.layers):
@@ -932,9 +971,18 @@ class GraphSAGE:
             packs[l] = LayerPack(self.offsets[l], layer.feat_dim, layer.out_dim,
                                  layer.w_img.data_ptr(), None if wt is None else wt.data_ptr(),
                                  int(isinstance(layer, DenseSageLayer)))
-        _check(lib().cmb_adam_step_pack(
-            _ptr(self.params), _ptr(self.grads), _ptr(self.m), _ptr(self.v), self.params.numel(),
-            self.lr, 0.9, 0.999, 1e-8, self.weight_decay, self.step_count, packs, L, _stream()))
+        if dev_step:  # the device counter holds the steps taken so far (eager or replayed)
+            if count:
+                self._step_dev.fill_(self.step_count - 1)
+            _check(lib().cmb_adam_step_pack_dev(
+                _ptr(self.params), _ptr(self.grads), _ptr(self.m), _ptr(self.v),
+                self.params.numel(), self.lr, 0.9, 0.999, 1e-8, self.weight_decay,
+                _ptr(self._step_dev), packs, L, _stream()))
+        else:
+            _check(lib().cmb_adam_step_pack(
+                _ptr(self.params), _ptr(self.grads), _ptr(self.m), _ptr(self.v),
+                self.params.numel(), self.lr, 0.9, 0.999, 1e-8, self.weight_decay,
+                self.step_count, packs, L, _stream()))
         return self.loss
 
 

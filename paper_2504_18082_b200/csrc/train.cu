@@ -137,11 +137,28 @@ struct PackTable {
   int dense[kMaxPackLayers];  // img in the dense.cu layout: row (h * Fp + c), column o
 };
 
+// step_dev != NULL: the step number is read on the device (after k_step_next advanced it) and
+// the bias corrections c1, c2 formed from it in fp64 there -- the form a captured CUDA graph
+// replays (no host value baked into the launch)
+__global__ void k_step_next(int32_t* step) { *step += 1; }
+
 __global__ void __launch_bounds__(256)
     k_adam_pack(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
                 float* __restrict__ v, int64_t n, float lr, float b1, float b2, float omb1,
                 float omb2, float eps, float wd, float c1, float c2,
-                const __grid_constant__ PackTable t) {
+                const __grid_constant__ PackTable t, const int32_t* __restrict__ step_dev,
+                double b1d, double b2d) {
+  if (step_dev) {
+    __shared__ float c12[2];
+    if (threadIdx.x == 0) {
+      const int s = *step_dev;
+      c12[0] = static_cast<float>(1.0 / (1.0 - pow(b1d, s)));
+      c12[1] = static_cast<float>(1.0 / (1.0 - pow(b2d, s)));
+    }
+    __syncthreads();
+    c1 = c12[0];
+    c2 = c12[1];
+  }
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const float gk = __fmaf_rn(wd, w[i], __ldg(g + i));
@@ -235,13 +252,14 @@ cmb_status cmb_adam_step(float* w, const float* g, float* m, float* v, int64_t n
   return CMB_OK;
 }
 
-cmb_status cmb_adam_step_pack(float* w, const float* g, float* m, float* v, int64_t n, double lr,
-                              double beta1, double beta2, double eps, double weight_decay,
-                              int32_t step, const cmb_layer_pack* layers, int32_t n_layers,
-                              void* stream) {
-  CMB_NVTX("cmb.next4.adam_step_pack");
+namespace {
+cmb_status adam_step_pack(float* w, const float* g, float* m, float* v, int64_t n, double lr,
+                          double beta1, double beta2, double eps, double weight_decay,
+                          int32_t step, int32_t* step_dev, const cmb_layer_pack* layers,
+                          int32_t n_layers, void* stream) {
   CMB_ARG(w && g && m && v && layers, "cmb_adam_step_pack: null argument");
-  CMB_ARG(n >= 0 && step >= 1 && beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0 &&
+  CMB_ARG(n >= 0 && (step >= 1 || step_dev) && beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 &&
+              beta2 < 1.0 &&
               n_layers >= 1 && n_layers <= tr::kMaxPackLayers,
           "cmb_adam_step_pack: need step >= 1, betas in [0, 1), 1 <= n_layers <= 8");
   tr::PackTable t{};
@@ -269,15 +287,41 @@ cmb_status cmb_adam_step_pack(float* w, const float* g, float* m, float* v, int6
   if (n == 0) return CMB_OK;
   cmb_status st = require_sm100();
   if (st != CMB_OK) return st;
-  const double c1 = 1.0 / (1.0 - std::pow(beta1, step));
-  const double c2 = 1.0 / (1.0 - std::pow(beta2, step));
+  const double c1 = step_dev ? 1.0 : 1.0 / (1.0 - std::pow(beta1, step));
+  const double c2 = step_dev ? 1.0 : 1.0 / (1.0 - std::pow(beta2, step));
   const int grid = static_cast<int>(n / 256 + 1 < 148 * 8 ? n / 256 + 1 : 148 * 8);
-  tr::k_adam_pack<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (step_dev) {
+    tr::k_step_next<<<1, 1, 0, s>>>(step_dev);
+    CMB_CUDA(cudaGetLastError());
+  }
+  tr::k_adam_pack<<<grid, 256, 0, s>>>(
       w, g, m, v, n, static_cast<float>(lr), static_cast<float>(beta1), static_cast<float>(beta2),
       static_cast<float>(1.0 - beta1), static_cast<float>(1.0 - beta2), static_cast<float>(eps),
-      static_cast<float>(weight_decay), static_cast<float>(c1), static_cast<float>(c2), t);
+      static_cast<float>(weight_decay), static_cast<float>(c1), static_cast<float>(c2), t,
+      step_dev, beta1, beta2);
   CMB_CUDA(cudaGetLastError());
   return CMB_OK;
+}
+}  // namespace
+
+cmb_status cmb_adam_step_pack(float* w, const float* g, float* m, float* v, int64_t n, double lr,
+                              double beta1, double beta2, double eps, double weight_decay,
+                              int32_t step, const cmb_layer_pack* layers, int32_t n_layers,
+                              void* stream) {
+  CMB_NVTX("cmb.next4.adam_step_pack");
+  return adam_step_pack(w, g, m, v, n, lr, beta1, beta2, eps, weight_decay, step, nullptr, layers,
+                        n_layers, stream);
+}
+
+cmb_status cmb_adam_step_pack_dev(float* w, const float* g, float* m, float* v, int64_t n,
+                                  double lr, double beta1, double beta2, double eps,
+                                  double weight_decay, int32_t* step,
+                                  const cmb_layer_pack* layers, int32_t n_layers, void* stream) {
+  CMB_NVTX("cmb.next4.adam_step_pack_dev");
+  CMB_ARG(step != nullptr, "cmb_adam_step_pack_dev: null step counter");
+  return adam_step_pack(w, g, m, v, n, lr, beta1, beta2, eps, weight_decay, 0, step, layers,
+                        n_layers, stream);
 }
 
 }  // extern "C"

@@ -292,3 +292,49 @@ def test_fused_adam_repack_equals_adam_then_pack():
             if layer.hidden:
                 assert torch.equal(layer.transposed_image(), ref.transposed_image())
     torch.cuda.synchronize()
+
+
+def test_graph_replayed_train_step_matches_eager():
+    """GraphSAGE.train_step(graph=True): the first call runs the step eagerly and captures it as
+    a CUDA graph, later calls replay it on whatever batch the sampler holds.  Per batch (5
+    different batches) the replayed model starts from the eager model's state (parameters,
+    moments, weight images): same loss and gradients as the eager step up to the fp32 rounding
+    order of the aggregation backward's atomics (R30), the device step counter in step, and the
+    replayed Adam + repack bit-exact against the unfused reference from its own gradients.
+    (Trajectories are not compared: Adam turns a last-bit gradient difference on a parameter
+    whose gradient is near zero into an lr-sized update difference.)"""
+    cfg = scaled(CONFIGS["products"], 0.01)
+    b = generate(cfg)
+    C = num_classes(cfg)
+    g = cmb.Graph.from_bundle(b)
+    L = len(cfg.fanouts)
+    labels = torch.from_numpy(make_labels(b, C)).cuda()
+    order = oracle.order_roots(b.train, b.comm, cfg.num_communities, oracle.MODE_RAND, 0.0, SEED, 0)
+    sampler = cmb.Sampler(g, cfg.batch_size, cfg.fanouts)
+    eager = cmb.GraphSAGE(cfg.feat_dim, C, num_layers=L, seed=4)
+    replay = cmb.GraphSAGE(cfg.feat_dim, C, num_layers=L, seed=4)
+    for k in range(5):
+        roots = oracle.batch_roots(order, cfg.batch_size // 2, k % 4)
+        sampler.sample(torch.from_numpy(roots).cuda(), cfg.p_intra, SEED, 10 + k)
+        for a, e in ((replay.params, eager.params), (replay.m, eager.m), (replay.v, eager.v)):
+            a.copy_(e)
+        for la, le_ in zip(replay.layers, eager.layers):
+            la.w_img.copy_(le_.w_img)
+            if la.hidden:
+                la.transposed_image().copy_(le_.transposed_image())
+        p_before, m_before, v_before = (t.clone() for t in (eager.params, eager.m, eager.v))
+        le = float(eager.train_step(sampler, labels).item())
+        lr_ = float(replay.train_step(sampler, labels, graph=True).item())
+        torch.cuda.synchronize()
+        assert replay.status.item() == 0 and eager.status.item() == 0
+        assert replay.step_count == eager.step_count == k + 1
+        assert int(replay._step_dev.item()) == k + 1
+        assert len(replay._graphs) == 1
+        assert abs(le - lr_) <= 1e-6 * abs(le) + 1e-9, (k, le, lr_)
+        scale = eager.grads.abs().max().item()
+        assert torch.allclose(replay.grads, eager.grads, rtol=1e-3, atol=1e-5 * scale), k
+        w, m, v = p_before.clone(), m_before.clone(), v_before.clone()
+        cmb.adam_step(w, replay.grads, m, v, replay.step_count, replay.lr,
+                      weight_decay=replay.weight_decay)
+        for got, want in ((replay.params, w), (replay.m, m), (replay.v, v)):
+            assert torch.equal(got.view(torch.int32), want.view(torch.int32)), k
