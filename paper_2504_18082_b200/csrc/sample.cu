@@ -26,6 +26,7 @@ struct SampleWs {
   unsigned* tag_ctr;         // [1] batches sampled with this workspace
   void* map;                 // [N] tagged dedup map: 32-bit words, or 64-bit (wide_map)
   uint32_t* scan;            // [max e_cap]
+  uint32_t* rank;            // [n_cap[L-1]] last-hop dst rows' ranks in their order buckets
 };
 
 // A batch needs 64-bit map words when one of its local ids or edge positions may reach 2^24
@@ -60,6 +61,7 @@ SampleWs carve_sample_ws(void* base, int64_t n_roots, const int32_t* fanouts, in
   else
     w.map = c.take<unsigned>(static_cast<size_t>(num_nodes));
   w.scan = c.take<uint32_t>(static_cast<size_t>(max_e) + 1);
+  w.rank = c.take<uint32_t>(static_cast<size_t>(n_cap[L - 1]) + 1);
   if (bytes) *bytes = c.bytes();
   return w;
 }
@@ -88,6 +90,7 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
   a.map = w.map;
   a.tag_ctr = w.tag_ctr;
   a.scan = w.scan;
+  a.rank = w.rank;
   a.pub = w.pub;
   a.bar = w.bar;
   a.prof = w.prof;

@@ -170,7 +170,8 @@ struct PArgs {
   unsigned* bar;            // [0] arrivals, [1] generation
   uint64_t* prof;           // [kMaxBlocks][64] per-block %globaltimer at sub-step boundaries
   uint32_t* hist;           // [kOrderBuckets] dst rows of hop L-1 per bucket v >> order_shift
-  uint32_t* cursor;         // [kOrderBuckets] rows of each bucket placed so far
+  uint32_t* cursor;         // [kOrderBuckets] (unused: the count step's ranks place the rows)
+  uint32_t* rank;           // [n_cap[L-1]] a last-hop dst row's rank within its order bucket
   int32_t* order;           // optional [n_{L-1}]: the visiting order of the last hop's dst rows
   int order_shift;
   int32_t* status;
@@ -552,14 +553,15 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
     int32_t c = 0;
     RowInfo r{};
     int32_t v = 0;
+    uint32_t rk = 0;
     if (i < hi) {
       v = __ldcg(dst + i);
       r = row_info_checked(a.g, v, a.wi, a.wo);
-      if (a.order && h == a.L - 1)  // an out-of-range root (flagged) counts in bucket 0
-        atomicAdd(a.hist + (static_cast<uint32_t>(v) < static_cast<uint64_t>(a.g.n)
-                                ? static_cast<uint32_t>(v) >> a.order_shift
-                                : 0u),
-                  1u);
+      if (a.order && h == a.L - 1)  // the row's rank in its bucket (an out-of-range root,
+        rk = atomicAdd(a.hist + (static_cast<uint32_t>(v) < static_cast<uint64_t>(a.g.n)  // flagged,
+                                     ? static_cast<uint32_t>(v) >> a.order_shift          // counts in
+                                     : 0u),                                               // bucket 0)
+                       1u);
       const int64_t m = r.ni_e + r.no_e;
       c = static_cast<int32_t>(m < f ? m : f);
       if (a.law == 1 && f < m) c = slot_count(v, h, f, a.wi, r.ni_e, r.no_e, a.k0, a.k1, a.batch);
@@ -570,6 +572,7 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
     if (i < hi) {
       const int64_t k = i - lo;
       a.indptr[h][i] = run + ex;
+      if (a.order && h == a.L - 1) a.rank[i] = rk;
       if (k < kRowCap) {
         rc.rs[k] = r.rs;
         rc.deg[k] = static_cast<uint32_t>(r.deg);
@@ -704,7 +707,8 @@ __device__ __forceinline__ void st8(int32_t* p, int64_t e0, int64_t n, const int
 
 // The visiting order of the last hop's dst rows (blocks.dst_order): after the grid barrier
 // that follows the count step every bucket count is final; each block scans the counts and
-// places its own dst rows (the count step's row range) at bucket offset + atomic cursor.
+// places its own dst rows (the count step's row range) at bucket offset + the rank the count
+// step's histogram atomic returned (no second atomic: 12.8 -> see DESIGN.md).
 template <int PB>
 __device__ void place_dst_rows(const PArgs& a, int h, int64_t n_h, Smem<PB>& sm) {
   static_assert(kOrderBuckets % PB == 0, "buckets per thread");
@@ -728,7 +732,7 @@ __device__ void place_dst_rows(const PArgs& a, int h, int64_t n_h, Smem<PB>& sm)
   const int32_t* dst = h == 0 ? a.roots : a.nodes;
   int64_t lo, hi;
   range_of(n_h, 1, lo, hi);
-  constexpr int U = 4;  // rows per thread per round: their atomics in flight together
+  constexpr int U = 4;  // rows per thread per round: their loads in flight together
   for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += static_cast<int64_t>(U) * PB) {
     uint32_t b[U], pos[U];
 #pragma unroll
@@ -736,10 +740,8 @@ __device__ void place_dst_rows(const PArgs& a, int h, int64_t n_h, Smem<PB>& sm)
       const int64_t i = i0 + static_cast<int64_t>(u) * PB;
       const uint32_t v = i < hi ? static_cast<uint32_t>(__ldcg(dst + i)) : 0u;
       b[u] = v < static_cast<uint64_t>(a.g.n) ? v >> a.order_shift : 0u;
+      pos[u] = i < hi ? __ldcg(a.rank + i) : 0u;
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      pos[u] = i0 + static_cast<int64_t>(u) * PB < hi ? atomicAdd(a.cursor + b[u], 1u) : 0u;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = i0 + static_cast<int64_t>(u) * PB;
@@ -768,7 +770,10 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   unsigned long long* bases = a.pub + 2 * kMaxBlocks;
   uint32_t* mask = (h == a.L - 1) ? a.mask : nullptr;
   const int32_t* nbr = a.indices[h];
-  if (a.order && h == a.L - 1) place_dst_rows<PB>(a, h, n_h, sm);
+  if (a.order && h == a.L - 1) {
+    place_dst_rows<PB>(a, h, n_h, sm);
+    CMB_PROF(a, pk);  // (timeline: the last hop's "place" sub-step)
+  }
   // a thread owns EPT consecutive edges per round (the block's range is 32-aligned, so 32 / EPT
   // threads fill one new-src mask word): their ids in vector loads, all EPT map lookups in
   // flight, one block scan per PB * EPT edges
@@ -832,6 +837,23 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
     int64_t per = (e_h + vgrid() - 1) / vgrid();  // range_of's block size
     per = (per + 31) / 32 * 32;
     int32_t* ind = a.indices[h];
+    // a node's first occurrence w precedes every other edge of it, so its block is this block
+    // or an earlier one: collect the bases of blocks 0 .. vblk() once (each published right
+    // after that block's prefix, which all aggregates this block already saw allow), then the
+    // edges' id lookups are independent loads -- no per-edge wait
+    uint32_t* sbase = reinterpret_cast<uint32_t*>(&sm.rows);  // the row cache is free here
+    const unsigned want = pub_tag(ctr, h);
+    for (int j = threadIdx.x; j <= vblk(); j += PB) {
+      if (j == vblk()) {
+        sbase[j] = static_cast<uint32_t>(base);
+      } else {
+        unsigned long long v;
+        while (((v = ld_acquire64(bases + j)) >> 32) != want) {
+        }
+        sbase[j] = static_cast<uint32_t>(v);
+      }
+    }
+    __syncthreads();  // (the acquires above order every thread's scan reads below)
     for (int64_t e0 = lo + static_cast<int64_t>(threadIdx.x) * 8; e0 < hi;
          e0 += static_cast<int64_t>(PB) * 8) {
       int32_t sc[8], u[8], id[8];
@@ -848,13 +870,8 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
         } else if (e0 + k >= hi) {
           id[k] = 0;
         } else {  // the id given to edge c, the node's first occurrence (maybe another block's)
-          const int b = static_cast<int>(c / per);
-          const unsigned want = pub_tag(ctr, h);
-          unsigned long long v;
-          while (((v = ld_acquire64(bases + b)) >> 32) != want) {
-          }
           const uint32_t cw = static_cast<uint32_t>(__ldcg(a.scan + c)) & 0x7fffffffu;
-          id[k] = static_cast<int32_t>(n_h + static_cast<int64_t>(v & 0xffffffffu) + cw - 1);
+          id[k] = static_cast<int32_t>(n_h + static_cast<int64_t>(sbase[c / per]) + cw - 1);
         }
       }
       st8(ind, e0, hi, id);

@@ -7,7 +7,7 @@ IFS=';' read -ra modes <<< "${3:-}"
 [ ${#modes[@]} -eq 0 ] && modes=("")
 mkdir -p $out
 timeout 900 python -m pytest tests/test_gpu_batched.py tests/test_gpu_headline.py tests/test_gpu_peer.py -x -q -p no:cacheprovider > $out/tests.log 2>&1
-for r in 1 2; do
+for r in ${ROUNDS:-1 2}; do
   for v in $libs; do
     name=$(basename $v .so)
     if [ "$v" = "intree" ]; then lib=""; else lib=$v; fi

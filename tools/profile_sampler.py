@@ -31,10 +31,17 @@ def main():
                                mode=os.environ.get("MODE", "rand"),
                                mix=float(os.environ.get("MIX", "0")), p=p, nb=nb)
     L = len(cfg.fanouts)
-    npts = 1 + 10 * L  # 32-bit map words: the last hop relabels inside its assign step
+    # 32-bit map words: the last hop relabels inside its assign step (no final barrier) and has
+    # one more stamp after the dst-order placement
+    npts = 2 + 10 * L
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     nblk = (sms - sms % nb) // nb  # virtual blocks of batch 0 of each launch
-    labels = [f"h{h}.{s}" for h in range(L) for s in SUB][:-1] + ["end"]
+    labels = [f"h{h}.{s}" for h in range(L - 1) for s in SUB]
+    for x in SUB[:-1]:
+        if x == "flag_scan":
+            labels.append(f"h{L - 1}.place_dst_rows")
+        labels.append(f"h{L - 1}.{x}")
+    labels.append("end")
     crit, mean, mx = [], [], []
     pipe.start_epoch(0)
     for t in range(25):
