@@ -546,41 +546,63 @@ __device__ void phase_count_sample(const PArgs& a, int h, Smem<PB>& sm, int& pk,
   range_of(n_h, 1, lo, hi);
   RowCache& rc = sm.rows;
   if (threadIdx.x == 0) sm.next = 0;  // read after publish_and_prefix's barrier
-  // (1) counts, block scan, cached row info
+  // (1) counts, block scan, cached row info.  A thread owns RPT consecutive rows per round: their
+  // ids, then their row records and the dst-order histogram atomics are issued before any is
+  // used (one block scan per PB * RPT rows); rows in (thread, row) order = row order
+#ifndef CMB_COUNT_RPT  // layout experiments only
+#define CMB_COUNT_RPT 1
+#endif
+  constexpr int RPT = CMB_COUNT_RPT;
+  const bool place = a.order && h == a.L - 1;
   int32_t run = 0;
-  for (int64_t t0 = lo; t0 < hi; t0 += PB) {
-    const int64_t i = t0 + threadIdx.x;
-    int32_t c = 0;
-    RowInfo r{};
-    int32_t v = 0;
-    uint32_t rk = 0;
-    if (i < hi) {
-      v = __ldcg(dst + i);
-      r = row_info_checked(a.g, v, a.wi, a.wo);
-      if (a.order && h == a.L - 1)  // the row's rank in its bucket (an out-of-range root,
-        rk = atomicAdd(a.hist + (static_cast<uint32_t>(v) < static_cast<uint64_t>(a.g.n)  // flagged,
-                                     ? static_cast<uint32_t>(v) >> a.order_shift          // counts in
-                                     : 0u),                                               // bucket 0)
-                       1u);
-      const int64_t m = r.ni_e + r.no_e;
-      c = static_cast<int32_t>(m < f ? m : f);
-      if (a.law == 1 && f < m) c = slot_count(v, h, f, a.wi, r.ni_e, r.no_e, a.k0, a.k1, a.batch);
+  for (int64_t t0 = lo; t0 < hi; t0 += static_cast<int64_t>(PB) * RPT) {
+    const int64_t i0 = t0 + static_cast<int64_t>(threadIdx.x) * RPT;
+    int32_t v[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) v[q] = i0 + q < hi ? __ldcg(dst + i0 + q) : 0;
+    RowInfo r[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q)
+      r[q] = i0 + q < hi ? row_info_checked(a.g, v[q], a.wi, a.wo) : RowInfo{0, 0, 0, 0, 0u, 0u};
+    uint32_t rk[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q)  // the row's rank in its bucket (an out-of-range root, flagged,
+      rk[q] = place && i0 + q < hi   // counts in bucket 0)
+                  ? atomicAdd(a.hist + (static_cast<uint32_t>(v[q]) < static_cast<uint64_t>(a.g.n)
+                                            ? static_cast<uint32_t>(v[q]) >> a.order_shift
+                                            : 0u),
+                              1u)
+                  : 0u;
+    int32_t c[RPT], sum = 0;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int64_t m = r[q].ni_e + r[q].no_e;
+      c[q] = static_cast<int32_t>(m < f ? m : f);
+      if (a.law == 1 && f < m)
+        c[q] = slot_count(v[q], h, f, a.wi, r[q].ni_e, r[q].no_e, a.k0, a.k1, a.batch);
+      sum += c[q];
     }
     int32_t ex, agg;
-    cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(c, ex, agg);
+    cub::BlockScan<int32_t, PB>(sm.cub.scan).ExclusiveSum(sum, ex, agg);
     __syncthreads();
-    if (i < hi) {
-      const int64_t k = i - lo;
-      a.indptr[h][i] = run + ex;
-      if (a.order && h == a.L - 1) a.rank[i] = rk;
-      if (k < kRowCap) {
-        rc.rs[k] = r.rs;
-        rc.deg[k] = static_cast<uint32_t>(r.deg);
-        rc.lo[k] = r.lo;
-        rc.hi[k] = r.hi;
-        rc.v[k] = v;
-        rc.off[k] = run + ex;
+    int32_t off = run + ex;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int64_t i = i0 + q;
+      if (i < hi) {
+        const int64_t k = i - lo;
+        a.indptr[h][i] = off;
+        if (place) a.rank[i] = rk[q];
+        if (k < kRowCap) {
+          rc.rs[k] = r[q].rs;
+          rc.deg[k] = static_cast<uint32_t>(r[q].deg);
+          rc.lo[k] = r[q].lo;
+          rc.hi[k] = r[q].hi;
+          rc.v[k] = v[q];
+          rc.off[k] = off;
+        }
       }
+      off += c[q];
     }
     run += agg;
   }
