@@ -20,10 +20,9 @@ struct SampleWs {
   WsHeader* hdr;
   unsigned* bar;             // grid barrier {arrivals, generation}
   unsigned long long* pub;   // [3][kMaxPersistBlocks] tagged block aggregates / bases
-  uint32_t* hist;            // [kOrderBuckets] dst rows of hop L-1 per node-id bucket, then
-  uint32_t* cursor;          // [kOrderBuckets] rows placed so far per bucket (contiguous)
+  uint32_t* hist;            // [kOrderBuckets] dst rows of hop L-1 per node-id bucket
   uint64_t* prof;            // [kMaxPersistBlocks][64] sub-step timeline
-  unsigned* tag_ctr;         // [1] batches sampled with this workspace
+  unsigned* tag_ctr;         // [2] batches sampled with this workspace, map width of the last
   void* map;                 // [N] tagged dedup map: 32-bit words, or 64-bit (wide_map)
   uint32_t* scan;            // [max e_cap]
   uint32_t* rank;            // [n_cap[L-1]] last-hop dst rows' ranks in their order buckets
@@ -52,8 +51,7 @@ SampleWs carve_sample_ws(void* base, int64_t n_roots, const int32_t* fanouts, in
   w.bar = c.take<unsigned>(64);
   // [3][kMaxPersistBlocks]: count and flag aggregates, then the last hop's block bases
   w.pub = c.take<unsigned long long>(3 * kMaxPersistBlocks);  // follows bar contiguously
-  w.hist = c.take<uint32_t>(2 * pst::kOrderBuckets);
-  w.cursor = w.hist + pst::kOrderBuckets;
+  w.hist = c.take<uint32_t>(pst::kOrderBuckets);
   w.prof = c.take<uint64_t>(static_cast<size_t>(kMaxPersistBlocks) * 64);
   w.tag_ctr = c.take<unsigned>(2);  // {batch counter, map width of the last batch}
   if (wide)
@@ -95,7 +93,6 @@ void fill_args(pst::PArgs& a, const cmb_graph* g, const int32_t* roots, int64_t 
   a.bar = w.bar;
   a.prof = w.prof;
   a.hist = w.hist;
-  a.cursor = w.cursor;
   a.order = out->dst_order;
   int bits = 0;
   while ((int64_t{1} << bits) < g->d.n) ++bits;

@@ -170,7 +170,6 @@ struct PArgs {
   unsigned* bar;            // [0] arrivals, [1] generation
   uint64_t* prof;           // [kMaxBlocks][64] per-block %globaltimer at sub-step boundaries
   uint32_t* hist;           // [kOrderBuckets] dst rows of hop L-1 per bucket v >> order_shift
-  uint32_t* cursor;         // [kOrderBuckets] (unused: the count step's ranks place the rows)
   uint32_t* rank;           // [n_cap[L-1]] a last-hop dst row's rank within its order bucket
   int32_t* order;           // optional [n_{L-1}]: the visiting order of the last hop's dst rows
   int order_shift;
@@ -956,7 +955,7 @@ __device__ __forceinline__ void run_batch(const PArgs& a) {
   // the dst-order buckets start empty: cleared here, before the grid barrier that precedes the
   // last hop's count step (one more barrier when that count step is hop 0's)
   if (a.order && vblk() == 0)
-    for (int i = threadIdx.x; i < 2 * kOrderBuckets; i += PB) a.hist[i] = 0u;  // (hist, cursor)
+    for (int i = threadIdx.x; i < kOrderBuckets; i += PB) a.hist[i] = 0u;
   if (a.order && a.L == 1) grid_barrier(a.bar, gen);
   CMB_PROF(a, pk);
   for (int64_t i = vblk() * (int64_t)PB + threadIdx.x; i < a.n_roots;

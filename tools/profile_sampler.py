@@ -15,8 +15,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2504_18082_b200 as cmb  # noqa: E402
 from gen import CONFIGS, generate  # noqa: E402
 
-PROF_OFFSET = 131584         # carve order: header 256, barrier 256, pub 3*4096*8, dst-order
-                             # hist + cursor 2*4096*4 (sample.cu)
+PROF_OFFSET = 115200         # carve order: header 256, barrier 256, pub 3*4096*8, dst-order
+                             # hist 4096*4 (sample.cu)
 SUB = ["relabel(h-1)", "count", "prefix", "positions", "picks+mark", "barrierA",
        "flag_scan", "prefix2", "assign", "barrierC"]
 
