@@ -39,7 +39,10 @@ constexpr int kMaxBlocks = 4096;
 #define CMB_ROW_CAP 3072
 #endif
 constexpr int kRowCap = CMB_ROW_CAP;  // dst rows per block cached in shared memory
-constexpr int kOrderBits = 12;                 // dst-order buckets: at most 2^12 node-id ranges
+#ifndef CMB_ORDER_BITS  // layout experiments only
+#define CMB_ORDER_BITS 12
+#endif
+constexpr int kOrderBits = CMB_ORDER_BITS;     // dst-order buckets: at most 2^12 node-id ranges
 constexpr int kOrderBuckets = 1 << kOrderBits;
 
 // the two map word layouts: tag in the top bits, then the final flag, then the value
