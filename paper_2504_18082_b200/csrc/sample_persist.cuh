@@ -888,7 +888,11 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
         const uint32_t c = static_cast<uint32_t>(sc[k]);
         if (c >> 31) {  // a first occurrence -> the next local id
           id[k] = static_cast<int32_t>(n_h + base + (c & 0x7fffffffu) - 1);
-          if (e0 + k < hi) a.nodes[id[k]] = u[k];
+          if (e0 + k < hi) {
+            a.nodes[id[k]] = u[k];
+            if (h < a.L - 1)  // the next hop's marks must see the node's final id
+              map_st(map + u[k], tag | M::kFinal | static_cast<uint32_t>(id[k]));
+          }
         } else if (c >> 30) {  // a node of an earlier hop
           id[k] = static_cast<int32_t>(c & 0x3fffffffu);
         } else if (e0 + k >= hi) {
@@ -899,7 +903,7 @@ __device__ void phase_flag_assign(const PArgs& a, int h, Smem<PB>& sm, int& pk,
         }
       }
       st8(ind, e0, hi, id);
-      st8(a.last_src, e0, hi, u);
+      if (h == a.L - 1) st8(a.last_src, e0, hi, u);
     }
     return;
   }
@@ -978,7 +982,8 @@ __device__ __forceinline__ void run_batch(const PArgs& a) {
   }
   if (vblk() == 0 && threadIdx.x == 0) a.sizes[0] = a.n_roots;
   for (int h = 0; h < a.L; ++h) {
-    if (h > 0) phase_relabel<PB, W>(a, h - 1);
+    // (32-bit words: every hop relabels inside its own assign step, so no pass here)
+    if (h > 0 && sizeof(T) != 4) phase_relabel<PB, W>(a, h - 1);
     CMB_PROF(a, pk);                                  // +0 relabel(h-1)
     const int f = a.fan[h];
 #if defined(CMB_SAMPLER_G8)
@@ -994,11 +999,12 @@ __device__ __forceinline__ void run_batch(const PArgs& a) {
       a.tag_ctr[0] = ctr;
       a.tag_ctr[1] = kWidth;
     }
-    // the last hop with 32-bit words relabels inside its assign step (no barrier, no pass)
-    const bool fuse = sizeof(T) == 4 && h == a.L - 1;
+    // with 32-bit words every hop relabels inside its assign step (no relabel pass; the last
+    // hop needs no barrier after it)
+    const bool fuse = sizeof(T) == 4;
     phase_flag_assign<PB, W>(a, h, sm, pk, tag, ctr, fuse);  // +6 flag scan, +7 prefix
     CMB_PROF(a, pk);                                  // +8 assign (+ relabel if fused)
-    if (fuse) break;
+    if (fuse && h == a.L - 1) break;
     grid_barrier(a.bar, gen);
     CMB_PROF(a, pk);                                  // +9 barrier
   }
