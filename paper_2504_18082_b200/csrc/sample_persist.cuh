@@ -25,8 +25,10 @@
 //     groups otherwise); each pick loads indices[pos] right away and marks its first occurrence
 //     with atomicMax(map[u], tag | kMarkerTop - e)
 //  C  flag + prefix + assign: first occurrences (map[u] == tag | kMarkerTop - e) get
-//     id = n_h + global flag scan - 1: map[u] := tag | kFinal | id, nodes[id] := u
-// then (after the barrier) relabel(h): indices[e] := id(map[u]), fused into hop h+1's A.
+//     id = n_h + global flag scan - 1: map[u] := tag | kFinal | id, nodes[id] := u.  With 32-bit
+//     words the assign step also writes every edge's local id (own id, an earlier hop's id, or
+//     the id of the node's first occurrence via the published block bases); with 64-bit words
+//     the relabel indices[e] := id(map[u]) runs after the barrier, fused into hop h+1's A.
 #pragma once
 
 namespace cmb {
